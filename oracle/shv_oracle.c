@@ -1,0 +1,419 @@
+/*
+ * shv_oracle.c — plain CPU oracle for the ShoveRand hot path. TEST
+ * INFRASTRUCTURE ONLY (see shv_oracle.h): only tests/, smoke() and bench.py's
+ * cpu_baseline / --impl reference legs may load it; the product never does.
+ *
+ * Everything here is the textbook definition written out, deliberately in a
+ * different formulation from the GPU path:
+ *   - MRG32k3a uses L'Ecuyer's signed form  p = a*x - b*y  reduced with C's
+ *     '%' (the GPU uses an unsigned rearrangement with 2^32-c folds);
+ *   - jumps are generic 3x3 matrix powers with 128-bit accumulation and '%'
+ *     (the GPU uses host-built per-bit tables and folded mat-vecs);
+ *   - stream positions are (A^(2^127))^g (A^(2^76))^u A^o built by repeated
+ *     squaring of A (no per-bit tables);
+ *   - Philox serves lanes through the SPEC's next_word buffer, one draw at a
+ *     time (the GPU computes whole counter blocks per store).
+ * Compiled with -O2 -ffp-contract=off. No SIMD, no lookup tables.
+ */
+#include "shv_oracle.h"
+
+#include <pthread.h>
+#include <stdlib.h>
+#include <string.h>
+
+typedef unsigned __int128 u128;
+
+/* MRG32k3a parameters, [LEcuyer1999] Table II (cited at P L84, L255):
+ *   x1,n = (1403580 x1,n-2 - 810728 x1,n-3) mod m1
+ *   x2,n = (527612 x2,n-1 - 1370589 x2,n-3) mod m2
+ *   z_n  = (x1,n - x2,n) mod m1, returned as m1 when it is 0 (R2). */
+static const int64_t m1 = 4294967087LL; /* 2^32 - 209   */
+static const int64_t m2 = 4294944443LL; /* 2^32 - 22853 */
+static const int64_t a12 = 1403580LL;
+static const int64_t a13n = 810728LL;
+static const int64_t a21 = 527612LL;
+static const int64_t a23n = 1370589LL;
+
+/* [LEcuyer1999]'s normalisation constant 1/(m1+1) as printed in his code
+ * ("#define norm 2.328306549295727688e-10"); R7. */
+static const double mrg_norm = 2.328306549295727688e-10;
+
+/* Philox4x32 constants, [Salmon.etal.2011] §3.3 / Random123 (P L327). */
+static const uint32_t PHILOX_M0 = 0xD2511F53u;
+static const uint32_t PHILOX_M1 = 0xCD9E8D57u;
+static const uint32_t PHILOX_W0 = 0x9E3779B9u; /* golden ratio */
+static const uint32_t PHILOX_W1 = 0xBB67AE85u; /* sqrt(3) - 1   */
+
+/* ------------------------------------------------------------------------ */
+/* MRG32k3a                                                                  */
+/* ------------------------------------------------------------------------ */
+
+uint32_t orc_mrg_step(uint32_t s[6])
+{
+    /* State (x1,n-3, x1,n-2, x1,n-1, x2,n-3, x2,n-2, x2,n-1) = s[0..5] (R1). */
+    int64_t p1 = a12 * (int64_t)s[1] - a13n * (int64_t)s[0];
+    p1 %= m1;
+    if (p1 < 0) p1 += m1;
+    int64_t p2 = a21 * (int64_t)s[5] - a23n * (int64_t)s[3];
+    p2 %= m2;
+    if (p2 < 0) p2 += m2;
+    s[0] = s[1]; s[1] = s[2]; s[2] = (uint32_t)p1;
+    s[3] = s[4]; s[4] = s[5]; s[5] = (uint32_t)p2;
+    /* Combination, [LEcuyer1999]: (p1 - p2) mod m1 with 0 mapped to m1. */
+    if (p1 > p2) return (uint32_t)(p1 - p2);
+    return (uint32_t)(p1 - p2 + m1);
+}
+
+void orc_mrg_matrices(uint64_t A1[9], uint64_t A2[9])
+{
+    /* Companion matrices acting on the column (x_{n-3}, x_{n-2}, x_{n-1}):
+     * the new last entry is the recurrence, the others shift up (R3). */
+    const uint64_t a[9] = {0, 1, 0,
+                           0, 0, 1,
+                           (uint64_t)(m1 - a13n), (uint64_t)a12, 0};
+    const uint64_t b[9] = {0, 1, 0,
+                           0, 0, 1,
+                           (uint64_t)(m2 - a23n), 0, (uint64_t)a21};
+    memcpy(A1, a, sizeof a);
+    memcpy(A2, b, sizeof b);
+}
+
+void orc_mat_mul(const uint64_t A[9], const uint64_t B[9], uint64_t m, uint64_t C[9])
+{
+    uint64_t T[9];
+    for (int r = 0; r < 3; ++r)
+        for (int c = 0; c < 3; ++c) {
+            u128 acc = 0;
+            for (int k = 0; k < 3; ++k) acc += (u128)A[3 * r + k] * B[3 * k + c];
+            T[3 * r + c] = (uint64_t)(acc % m);
+        }
+    memcpy(C, T, sizeof T);
+}
+
+void orc_mat_pow(const uint64_t A[9], uint64_t e_lo, uint64_t e_hi, uint64_t m, uint64_t out[9])
+{
+    u128 e = ((u128)e_hi << 64) | e_lo;
+    uint64_t R[9] = {1, 0, 0, 0, 1, 0, 0, 0, 1};
+    uint64_t P[9];
+    memcpy(P, A, sizeof P);
+    while (e) {
+        if (e & 1) orc_mat_mul(R, P, m, R);
+        orc_mat_mul(P, P, m, P);
+        e >>= 1;
+    }
+    memcpy(out, R, sizeof R);
+}
+
+static void mat_vec(const uint64_t M[9], const uint32_t v[3], uint64_t m, uint32_t out[3])
+{
+    uint32_t t[3];
+    for (int r = 0; r < 3; ++r) {
+        u128 acc = 0;
+        for (int k = 0; k < 3; ++k) acc += (u128)M[3 * r + k] * v[k];
+        t[r] = (uint32_t)(acc % m);
+    }
+    memcpy(out, t, sizeof t);
+}
+
+void orc_mrg_jump(uint32_t s[6], uint64_t e_lo, uint64_t e_hi)
+{
+    uint64_t A1[9], A2[9], P1[9], P2[9];
+    orc_mrg_matrices(A1, A2);
+    orc_mat_pow(A1, e_lo, e_hi, (uint64_t)m1, P1);
+    orc_mat_pow(A2, e_lo, e_hi, (uint64_t)m2, P2);
+    mat_vec(P1, s, (uint64_t)m1, s);
+    mat_vec(P2, s + 3, (uint64_t)m2, s + 3);
+}
+
+/* A^(2^k) by k squarings. */
+static void mat_pow2k(const uint64_t A[9], int k, uint64_t m, uint64_t out[9])
+{
+    uint64_t P[9];
+    memcpy(P, A, sizeof P);
+    for (int i = 0; i < k; ++i) orc_mat_mul(P, P, m, P);
+    memcpy(out, P, sizeof P);
+}
+
+void orc_mrg_position(const uint32_t seed[6], uint64_t g, uint64_t u,
+                      uint64_t o_lo, uint64_t o_hi, uint32_t out[6])
+{
+    /* Position g*2^127 + u*2^76 + o (P L264-268: 2^64 streams of 2^127,
+     * substreams of 2^76). The exponent can reach 2^191, so it is applied as
+     * three matrix powers rather than one (R4). */
+    uint64_t A[2][9], S127[9], S76[9], Pg[9], Pu[9], Po[9], M[9];
+    const uint64_t mod[2] = {(uint64_t)m1, (uint64_t)m2};
+    orc_mrg_matrices(A[0], A[1]);
+    for (int c = 0; c < 2; ++c) {
+        mat_pow2k(A[c], 127, mod[c], S127);
+        mat_pow2k(A[c], 76, mod[c], S76);
+        orc_mat_pow(S127, g, 0, mod[c], Pg);
+        orc_mat_pow(S76, u, 0, mod[c], Pu);
+        orc_mat_pow(A[c], o_lo, o_hi, mod[c], Po);
+        orc_mat_mul(Pg, Pu, mod[c], M);
+        orc_mat_mul(M, Po, mod[c], M);
+        mat_vec(M, seed + 3 * c, mod[c], out + 3 * c);
+    }
+}
+
+/* ------------------------------------------------------------------------ */
+/* Philox4x32                                                                */
+/* ------------------------------------------------------------------------ */
+
+static void mulhilo(uint32_t a, uint32_t b, uint32_t* hi, uint32_t* lo)
+{
+    uint64_t p = (uint64_t)a * (uint64_t)b;
+    *hi = (uint32_t)(p >> 32);
+    *lo = (uint32_t)p;
+}
+
+void orc_philox_block(const uint32_t ctr[4], const uint32_t key[2], int rounds, uint32_t out[4])
+{
+    /* [Salmon.etal.2011] Philox S-P network, N=4, W=32:
+     *   (hi0,lo0) = M0*c0, (hi1,lo1) = M1*c2
+     *   c' = (hi1 ^ c1 ^ k0, lo1, hi0 ^ c3 ^ k1, lo0)
+     * with the Weyl key bump k += (W0, W1) between rounds (R5). */
+    uint32_t c[4] = {ctr[0], ctr[1], ctr[2], ctr[3]};
+    uint32_t k0 = key[0], k1 = key[1];
+    for (int r = 0; r < rounds; ++r) {
+        if (r > 0) {
+            k0 += PHILOX_W0;
+            k1 += PHILOX_W1;
+        }
+        uint32_t hi0, lo0, hi1, lo1;
+        mulhilo(PHILOX_M0, c[0], &hi0, &lo0);
+        mulhilo(PHILOX_M1, c[2], &hi1, &lo1);
+        uint32_t n0 = hi1 ^ c[1] ^ k0;
+        uint32_t n1 = lo1;
+        uint32_t n2 = hi0 ^ c[3] ^ k1;
+        uint32_t n3 = lo0;
+        c[0] = n0; c[1] = n1; c[2] = n2; c[3] = n3;
+    }
+    memcpy(out, c, sizeof c);
+}
+
+/* ------------------------------------------------------------------------ */
+/* conversions (R7)                                                          */
+/* ------------------------------------------------------------------------ */
+
+float orc_to_f32(uint32_t w) { return (float)(w >> 8) * 0x1p-24f; }
+
+double orc_mrg_to_f64(uint32_t z) { return (double)z * mrg_norm; }
+
+double orc_philox_to_f64(uint32_t lo, uint32_t hi)
+{
+    uint64_t b = ((uint64_t)hi << 32) | lo;
+    return (double)(b >> 11) * 0x1p-53;
+}
+
+/* ------------------------------------------------------------------------ */
+/* streams (P L387-399: the per-PE object and next())                        */
+/* ------------------------------------------------------------------------ */
+
+static int seed_words_mrg(const uint32_t* seed, int nseed, uint32_t s[6])
+{
+    if (nseed == 1) {
+        for (int k = 0; k < 6; ++k) s[k] = seed[0];
+    } else if (nseed == 6) {
+        for (int k = 0; k < 6; ++k) s[k] = seed[k];
+    } else {
+        return -1;
+    }
+    /* S L114-119: residues in range, neither triple all zero. */
+    for (int k = 0; k < 3; ++k)
+        if ((int64_t)s[k] >= m1 || (int64_t)s[3 + k] >= m2) return -1;
+    if (!(s[0] | s[1] | s[2]) || !(s[3] | s[4] | s[5])) return -1;
+    return 0;
+}
+
+int orc_stream_open(orc_stream* st, int gen, const uint32_t* seed, int nseed,
+                    uint64_t first, uint64_t i, int spacing,
+                    uint64_t off_lo, uint64_t off_hi)
+{
+    memset(st, 0, sizeof *st);
+    st->gen = gen;
+    if (gen == ORC_MRG32K3A) {
+        uint32_t base[6];
+        if (seed_words_mrg(seed, nseed, base)) return -1;
+        /* Handle-stream i is stream first+i (STREAM) or substream first+i of
+         * stream 0 (SUBSTREAM) (R4). */
+        uint64_t g = 0, u = 0;
+        if (spacing == ORC_SPACING_STREAM) g = first + i;
+        else if (spacing == ORC_SPACING_SUBSTREAM) u = first + i;
+        else return -1;
+        orc_mrg_position(base, g, u, off_lo, off_hi, st->s);
+        return 0;
+    }
+    if (gen == ORC_PHILOX4X32_10) {
+        if (nseed != 1 && nseed != 2) return -1;
+        if (spacing != ORC_SPACING_STREAM) return -1;
+        if (off_hi >> 2) return -1; /* a stream holds 2^66 draws (R6) */
+        st->key[0] = seed[0];
+        st->key[1] = nseed == 2 ? seed[1] : 0;
+        st->g = first + i;
+        u128 d = ((u128)off_hi << 64) | off_lo;
+        st->blk = (uint64_t)(d >> 2);
+        st->buf_pos = 4;
+        int lane = (int)(d & 3);
+        if (lane) {
+            (void)orc_stream_next(st); /* fill the buffer at block d>>2 */
+            st->buf_pos = lane;
+        }
+        return 0;
+    }
+    return -1;
+}
+
+uint32_t orc_stream_next(orc_stream* st)
+{
+    if (st->gen == ORC_MRG32K3A) return orc_mrg_step(st->s);
+    /* SPEC next_word (S L258-266): serve x, y, z, w of the current block,
+     * then evaluate the next counter. Counter = (blk_lo, blk_hi, g_lo, g_hi),
+     * key = (seed0, seed1) (R6). */
+    if (st->buf_pos == 4) {
+        uint32_t ctr[4] = {(uint32_t)st->blk, (uint32_t)(st->blk >> 32),
+                           (uint32_t)st->g, (uint32_t)(st->g >> 32)};
+        orc_philox_block(ctr, st->key, 10, st->buf);
+        st->blk += 1;
+        st->buf_pos = 0;
+    }
+    return st->buf[st->buf_pos++];
+}
+
+/* ------------------------------------------------------------------------ */
+/* bulk rows and Monte Carlo, split over threads by contiguous stream ranges */
+/* ------------------------------------------------------------------------ */
+
+typedef struct {
+    int gen, nseed, spacing, kind, mc;
+    const uint32_t* seed;
+    uint64_t first, off_lo, off_hi, n; /* n = values per row, or samples */
+    const uint64_t* idx;               /* NULL: row r is stream r */
+    uint64_t r0, r1;                   /* rows [r0, r1) */
+    void* out;
+    uint64_t* counts;
+    uint64_t total;
+    int err;
+} job_t;
+
+static void* run_job(void* arg)
+{
+    job_t* jb = (job_t*)arg;
+    for (uint64_t r = jb->r0; r < jb->r1; ++r) {
+        uint64_t i = jb->idx ? jb->idx[r] : r;
+        orc_stream st;
+        if (orc_stream_open(&st, jb->gen, jb->seed, jb->nseed, jb->first, i, jb->spacing,
+                            jb->off_lo, jb->off_hi)) {
+            jb->err = 1;
+            return NULL;
+        }
+        if (jb->mc) {
+            /* Dartboard (S L529-537): x = w>>8, y = w'>>8 as 24-bit lattice
+             * points; x^2 + y^2 < 1 on the f32 values iff X^2+Y^2 < 2^48 (R9). */
+            uint64_t hits = 0;
+            for (uint64_t k = 0; k < jb->n; ++k) {
+                uint64_t X = orc_stream_next(&st) >> 8;
+                uint64_t Y = orc_stream_next(&st) >> 8;
+                if (X * X + Y * Y < ((uint64_t)1 << 48)) ++hits;
+            }
+            if (jb->counts) jb->counts[r] = hits;
+            jb->total += hits;
+            continue;
+        }
+        for (uint64_t j = 0; j < jb->n; ++j) {
+            uint64_t at = r * jb->n + j;
+            if (jb->kind == ORC_U32) {
+                ((uint32_t*)jb->out)[at] = orc_stream_next(&st);
+            } else if (jb->kind == ORC_F32) {
+                ((float*)jb->out)[at] = orc_to_f32(orc_stream_next(&st));
+            } else if (jb->gen == ORC_MRG32K3A) {
+                ((double*)jb->out)[at] = orc_mrg_to_f64(orc_stream_next(&st));
+            } else {
+                uint32_t lo = orc_stream_next(&st);
+                uint32_t hi = orc_stream_next(&st);
+                ((double*)jb->out)[at] = orc_philox_to_f64(lo, hi);
+            }
+        }
+    }
+    return NULL;
+}
+
+static int run_jobs(job_t proto, uint64_t rows, int nthreads, uint64_t* total)
+{
+    if (nthreads < 1) nthreads = 1;
+    if ((uint64_t)nthreads > rows) nthreads = rows ? (int)rows : 1;
+    job_t* jobs = (job_t*)calloc((size_t)nthreads, sizeof(job_t));
+    pthread_t* th = (pthread_t*)calloc((size_t)nthreads, sizeof(pthread_t));
+    if (!jobs || !th) {
+        free(jobs);
+        free(th);
+        return -1;
+    }
+    for (int t = 0; t < nthreads; ++t) {
+        jobs[t] = proto;
+        jobs[t].r0 = rows * (uint64_t)t / (uint64_t)nthreads;
+        jobs[t].r1 = rows * (uint64_t)(t + 1) / (uint64_t)nthreads;
+    }
+    for (int t = 1; t < nthreads; ++t) pthread_create(&th[t], NULL, run_job, &jobs[t]);
+    run_job(&jobs[0]);
+    for (int t = 1; t < nthreads; ++t) pthread_join(th[t], NULL);
+    int err = 0;
+    uint64_t sum = 0;
+    for (int t = 0; t < nthreads; ++t) {
+        err |= jobs[t].err;
+        sum += jobs[t].total;
+    }
+    free(jobs);
+    free(th);
+    if (total) *total = sum;
+    return err ? -1 : 0;
+}
+
+static job_t make_job(int gen, const uint32_t* seed, int nseed, uint64_t first, int spacing,
+                      uint64_t off_lo, uint64_t off_hi, uint64_t n, int kind,
+                      const uint64_t* idx, void* out, uint64_t* counts, int mc)
+{
+    job_t j;
+    memset(&j, 0, sizeof j);
+    j.gen = gen; j.seed = seed; j.nseed = nseed; j.first = first; j.spacing = spacing;
+    j.off_lo = off_lo; j.off_hi = off_hi; j.n = n; j.kind = kind; j.idx = idx;
+    j.out = out; j.counts = counts; j.mc = mc;
+    return j;
+}
+
+int orc_generate(int gen, const uint32_t* seed, int nseed, uint64_t first,
+                 uint64_t n_streams, int spacing, uint64_t off_lo, uint64_t off_hi,
+                 uint64_t n, int kind, void* out, int nthreads)
+{
+    job_t p = make_job(gen, seed, nseed, first, spacing, off_lo, off_hi, n, kind, NULL, out, NULL, 0);
+    return run_jobs(p, n_streams, nthreads, NULL);
+}
+
+int orc_generate_list(int gen, const uint32_t* seed, int nseed, uint64_t first,
+                      const uint64_t* idx, uint64_t n_idx, int spacing,
+                      uint64_t off_lo, uint64_t off_hi, uint64_t n, int kind,
+                      void* out, int nthreads)
+{
+    job_t p = make_job(gen, seed, nseed, first, spacing, off_lo, off_hi, n, kind, idx, out, NULL, 0);
+    return run_jobs(p, n_idx, nthreads, NULL);
+}
+
+uint64_t orc_mc_count(int gen, const uint32_t* seed, int nseed, uint64_t first,
+                      uint64_t n_streams, int spacing, uint64_t off_lo, uint64_t off_hi,
+                      uint64_t samples, uint64_t* counts, int nthreads)
+{
+    uint64_t total = 0;
+    job_t p = make_job(gen, seed, nseed, first, spacing, off_lo, off_hi, samples, 0, NULL, NULL, counts, 1);
+    if (run_jobs(p, n_streams, nthreads, &total)) return UINT64_MAX;
+    return total;
+}
+
+uint64_t orc_mc_count_list(int gen, const uint32_t* seed, int nseed, uint64_t first,
+                           const uint64_t* idx, uint64_t n_idx, int spacing,
+                           uint64_t off_lo, uint64_t off_hi, uint64_t samples,
+                           uint64_t* counts, int nthreads)
+{
+    uint64_t total = 0;
+    job_t p = make_job(gen, seed, nseed, first, spacing, off_lo, off_hi, samples, 0, idx, NULL, counts, 1);
+    if (run_jobs(p, n_idx, nthreads, &total)) return UINT64_MAX;
+    return total;
+}

@@ -1,0 +1,98 @@
+/*
+ * shv_oracle.h — plain, slow, obviously-correct CPU oracle for the ShoveRand
+ * hot path (arXiv 1412.8266). TEST INFRASTRUCTURE ONLY.
+ *
+ * Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline /
+ * --impl reference legs may load this library. The product path
+ * (paper_1412_8266_b200/, include/shv.h) shares no code, header, table or
+ * constant generator with this file, and never calls it.
+ *
+ * Citations: "P Lnn" = /root/reference/PAPER.md line nn, "S Lnn" = SPEC.md
+ * line nn. Readings of silent/ambiguous points are listed in DESIGN.md §3
+ * (R1..R12) and referenced here by their ID.
+ */
+#ifndef SHV_ORACLE_H
+#define SHV_ORACLE_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum { ORC_MRG32K3A = 1, ORC_PHILOX4X32_10 = 2 };
+enum { ORC_SPACING_STREAM = 0, ORC_SPACING_SUBSTREAM = 1 };
+enum { ORC_U32 = 0, ORC_F32 = 1, ORC_F64 = 2 };
+
+/* ---- MRG32k3a (P L250-282 §4.1; constants from [LEcuyer1999], P L255) ---- */
+/* One step of the combined recurrence. s = (s10,s11,s12,s20,s21,s22), oldest
+ * first (R1). Advances s in place and returns z in [1, m1] (R2). */
+uint32_t orc_mrg_step(uint32_t s[6]);
+/* The two 3x3 companion matrices A1 (mod m1) and A2 (mod m2), row-major. */
+void orc_mrg_matrices(uint64_t A1[9], uint64_t A2[9]);
+/* C = A*B mod m (3x3, row-major, entries < m). */
+void orc_mat_mul(const uint64_t A[9], const uint64_t B[9], uint64_t m, uint64_t C[9]);
+/* out = A^e mod m, e = e_hi*2^64 + e_lo, by square-and-multiply (P L112-117). */
+void orc_mat_pow(const uint64_t A[9], uint64_t e_lo, uint64_t e_hi, uint64_t m, uint64_t out[9]);
+/* s <- A^e s componentwise: the state after e steps (S L157-165). */
+void orc_mrg_jump(uint32_t s[6], uint64_t e_lo, uint64_t e_hi);
+/* State at position g*2^127 + u*2^76 + o of the sequence started at seed
+ * (P L264-268; S L166-174): (A^(2^127))^g (A^(2^76))^u A^o seed. */
+void orc_mrg_position(const uint32_t seed[6], uint64_t g, uint64_t u,
+                      uint64_t o_lo, uint64_t o_hi, uint32_t out[6]);
+
+/* ---- Philox4x32 (P L322-336 §4.3; constants from [Salmon.etal.2011]) ---- */
+void orc_philox_block(const uint32_t ctr[4], const uint32_t key[2], int rounds,
+                      uint32_t out[4]);
+
+/* ---- conversions (R7) ---- */
+float orc_to_f32(uint32_t w);
+double orc_mrg_to_f64(uint32_t z);
+double orc_philox_to_f64(uint32_t lo, uint32_t hi);
+
+/* ---- streams: the paper's per-PE object with next() (P L387-399 §5.2) ---- */
+typedef struct {
+    int gen;
+    uint32_t s[6];        /* MRG32k3a state */
+    uint32_t key[2];      /* Philox key (R6) */
+    uint64_t g;           /* Philox stream index -> ctr[2..3] (R6) */
+    uint64_t blk;         /* Philox next counter block -> ctr[0..1] (R6) */
+    uint32_t buf[4];      /* Philox lanes not yet served (S L258-266) */
+    int buf_pos;          /* next lane to serve; 4 = empty */
+} orc_stream;
+
+/* Open handle-stream i of a (gen, seed, first, spacing) family at draw offset
+ * (off_hi:off_lo). Returns 0 on success, -1 on invalid arguments. */
+int orc_stream_open(orc_stream* st, int gen, const uint32_t* seed, int nseed,
+                    uint64_t first, uint64_t i, int spacing,
+                    uint64_t off_lo, uint64_t off_hi);
+uint32_t orc_stream_next(orc_stream* st);
+
+/* Stream-major rows out[i*n + j] (R8) for streams i < n_streams; kind picks
+ * u32 / f32 / f64 (Philox f64 consumes two draws per value, R7).
+ * nthreads >= 1 splits streams into contiguous ranges (result independent
+ * of nthreads). Returns 0 or -1. */
+int orc_generate(int gen, const uint32_t* seed, int nseed, uint64_t first,
+                 uint64_t n_streams, int spacing, uint64_t off_lo, uint64_t off_hi,
+                 uint64_t n, int kind, void* out, int nthreads);
+
+/* Monte Carlo pi dartboard (S L529-537; R9): sample k of stream i uses draws
+ * 2k, 2k+1 from the offset; hit iff X^2+Y^2 < 2^48 with X = w>>8, Y = w'>>8.
+ * counts[i] (if non-NULL) receives per-stream hits; returns the total. */
+uint64_t orc_mc_count(int gen, const uint32_t* seed, int nseed, uint64_t first,
+                      uint64_t n_streams, int spacing, uint64_t off_lo, uint64_t off_hi,
+                      uint64_t samples, uint64_t* counts, int nthreads);
+/* Same, but only for an explicit list of handle-stream indices. */
+uint64_t orc_mc_count_list(int gen, const uint32_t* seed, int nseed, uint64_t first,
+                           const uint64_t* idx, uint64_t n_idx, int spacing,
+                           uint64_t off_lo, uint64_t off_hi, uint64_t samples,
+                           uint64_t* counts, int nthreads);
+/* Rows for an explicit list of handle-stream indices: out[r*n + j]. */
+int orc_generate_list(int gen, const uint32_t* seed, int nseed, uint64_t first,
+                      const uint64_t* idx, uint64_t n_idx, int spacing,
+                      uint64_t off_lo, uint64_t off_hi, uint64_t n, int kind,
+                      void* out, int nthreads);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

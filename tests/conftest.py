@@ -1,0 +1,54 @@
+import os
+import shutil
+import subprocess
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+
+def pytest_configure(config):
+    config.addinivalue_line("markers", "gpu: needs a B200 (sm_100a) and the CUDA library")
+    config.addinivalue_line("markers", "slow: long-running oracle work")
+
+
+@pytest.fixture(scope="session")
+def orc():
+    import oracle
+    oracle.build()
+    return oracle
+
+
+class CurandPin:
+    """cuRAND's header implementations compiled as host code (tests/pins)."""
+
+    def __init__(self, exe):
+        self.p = subprocess.Popen([exe], stdin=subprocess.PIPE, stdout=subprocess.PIPE,
+                                  text=True, bufsize=1)
+
+    def ask(self, *words):
+        self.p.stdin.write(" ".join(str(w) for w in words) + "\n")
+        self.p.stdin.flush()
+        line = self.p.stdout.readline().split()
+        assert line and line[0] != "error", words
+        return [int(v) for v in line]
+
+    def close(self):
+        self.p.stdin.close()
+        self.p.wait()
+
+
+@pytest.fixture(scope="session")
+def curand_pin(tmp_path_factory):
+    nvcc = shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
+    if not os.path.exists(nvcc):
+        pytest.skip("nvcc not available to build the cuRAND host pin")
+    exe = str(tmp_path_factory.mktemp("pin") / "curand_host_pin")
+    subprocess.check_call([nvcc, "-w", "-O1", "-o", exe,
+                           os.path.join(ROOT, "tests", "pins", "curand_host_pin.cu")])
+    pin = CurandPin(exe)
+    yield pin
+    pin.close()

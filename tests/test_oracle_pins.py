@@ -1,0 +1,330 @@
+"""Pins for the CPU oracle (oracle/), independent of the oracle itself.
+
+Every check compares the oracle with something it does not share code with:
+published constants and known-answer vectors (tests/golden/, each cited),
+NVIDIA cuRAND's header implementation compiled as host code (tests/pins/),
+closed forms, and invariants the generators' mathematics fixes (SPEC.md
+L600-608 acceptance criteria #1, #2, #3, #7). A plausible transcription error
+anywhere in the oracle (a constant, the state order, the matrix orientation,
+the tie rule, the Philox lane order or key schedule, a conversion) fails at
+least one of them.
+"""
+import math
+import os
+import random
+import re
+from fractions import Fraction
+
+import numpy as np
+import pytest
+
+import workloads as W
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+M1, M2 = 4294967087, 4294944443
+
+
+def _rows(name):
+    with open(os.path.join(GOLD, name)) as f:
+        return [ln.split() for ln in f if ln.strip() and not ln.startswith("#")]
+
+
+# --------------------------------------------------------------------------- Philox
+
+def test_philox_random123_kat(orc):
+    for fam, *words in _rows("philox4x32_kat.txt"):
+        rounds = int(fam.split("_")[1])
+        v = [int(w, 16) for w in words]
+        assert orc.philox_block(v[0:4], v[4:6], rounds) == v[6:10], fam
+
+
+def test_philox_cpp26_required_value(orc):
+    seed, nth, val = (int(x) for x in _rows("cpp26_philox4x32.txt")[0])
+    # through the block function: draw nth-1 = lane 3 of block 2499
+    d = nth - 1
+    assert orc.philox_block([d >> 2, 0, 0, 0], [seed, 0], 10)[d & 3] == val
+    # and through the stream layout (R6): stream 0, offset nth-1
+    row = orc.generate(W.PHILOX4X32_10, [seed], 1, 1, offset=d)
+    assert int(row[0, 0]) == val
+
+
+def test_philox_block_vs_curand(orc, curand_pin):
+    rng = random.Random(11)
+    for _ in range(300):
+        c = [rng.getrandbits(32) for _ in range(4)]
+        k = [rng.getrandbits(32) for _ in range(2)]
+        assert orc.philox_block(c, k, 10) == curand_pin.ask("philox", *c, *k)
+
+
+@pytest.mark.parametrize("offset", [0, 1, 2, 3, 4, 5, 1001, (1 << 33) + 3, (1 << 64) - 3])
+def test_philox_stream_layout_vs_curand(orc, curand_pin, offset):
+    # curand_init(seed, subsequence=g, offset) + curand() serves lanes x,y,z,w
+    # of ctr=(blk_lo, blk_hi, g_lo, g_hi), key=(seed_lo, seed_hi): R6.
+    rng = random.Random(offset)
+    for _ in range(4):
+        seed = rng.getrandbits(64)
+        g = rng.getrandbits(64)
+        got = orc.generate(W.PHILOX4X32_10, [seed & 0xFFFFFFFF, seed >> 32], 1, 37,
+                           first=g, offset=offset)[0]
+        assert [int(x) for x in got] == curand_pin.ask("pstream", seed, g, offset, 37)
+
+
+def test_philox_bijective_no_collisions(orc):
+    # S L230: distinct counters under one key -> no collisions over 10^6 blocks.
+    rows = orc.generate(W.PHILOX4X32_10, [7, 9], 1, 4 * 1_000_000)
+    blocks = rows.reshape(-1, 4).view(np.dtype((np.void, 16))).ravel()
+    assert len(np.unique(blocks)) == 1_000_000
+
+
+# --------------------------------------------------------------------------- MRG32k3a
+
+def test_mrg_first_outputs_seed12345(orc):
+    g = {r[0]: r[1:] for r in _rows("mrg32k3a_seed12345.txt")}
+    s = [12345] * 6
+    zs = []
+    for _ in range(10):
+        z, s = orc.mrg_step(s)
+        zs.append(z)
+    assert zs == [int(v) for v in g["z"]]
+    assert orc.mrg_to_f64(zs[0]) == float(g["u0"][0])
+    for name in ("stream1", "stream2", "stream3", "substream1", "substream2", "substream3"):
+        k = int(name[-1])
+        start = orc.mrg_position([12345] * 6, k if name.startswith("stream") else 0,
+                                 k if name.startswith("sub") else 0, 0)
+        assert start == [int(v) for v in g[name][:6]], name
+        assert orc.mrg_step(start)[0] == int(g[name][6]), name
+
+
+def _valid_seed(rng):
+    while True:
+        s = [rng.randrange(M1) for _ in range(3)] + [rng.randrange(M2) for _ in range(3)]
+        if any(s[:3]) and any(s[3:]):
+            return s
+
+
+def test_mrg_step_vs_curand(orc, curand_pin):
+    rng = random.Random(5)
+    seeds = [[12345] * 6, [M1 - 1] * 3 + [M2 - 1] * 3, [1, 0, 0, 1, 0, 0], [0, 0, 1, 0, 0, 1]]
+    seeds += [_valid_seed(rng) for _ in range(40)]
+    for s in seeds:
+        ref = curand_pin.ask("mrg", *s, 500)
+        got = []
+        st = list(s)
+        for _ in range(500):
+            z, st = orc.mrg_step(st)
+            got.append(z)
+        assert got == ref, s
+
+
+def test_mrg_tie_maps_to_m1(orc, curand_pin):
+    # R2: p1 == p2 gives z = m1 (L'Ecuyer, cuRAND), not 0.
+    tie = [0, 1, 0, 0, 0, 1226359468]
+    assert orc.mrg_step(tie)[0] == M1
+    assert curand_pin.ask("mrg", *tie, 1) == [M1]
+    # R11: SPEC L137's example state does NOT produce 0.
+    assert orc.mrg_step([0, 0, 1, 0, 0, 1])[0] == 4294439475
+    assert curand_pin.ask("mrg", 0, 0, 1, 0, 0, 1, 1) == [4294439475]
+
+
+def test_jump_matrices_vs_rngstreams(orc):
+    A1, A2 = orc.mrg_matrices()
+    g = {r[0]: [int(v) for v in r[1:]] for r in _rows("rngstream_matrices.txt")}
+    flat = lambda M: [v for row in M for v in row]
+    assert flat(orc.mat_pow(A1, 1 << 76, M1)) == g["A1p76"]
+    assert flat(orc.mat_pow(A2, 1 << 76, M2)) == g["A2p76"]
+    assert flat(orc.mat_pow(A1, 1 << 127, M1)) == g["A1p127"]
+    assert flat(orc.mat_pow(A2, 1 << 127, M2)) == g["A2p127"]
+
+
+def _curand_tables():
+    path = "/usr/local/cuda/include/curand_mrg32k3a.h"
+    if not os.path.exists(path):
+        pytest.skip("cuRAND headers not present")
+    txt = open(path).read()
+    out = {}
+    for name in ("mrg32k3aM1", "mrg32k3aM2", "mrg32k3aM1SubSeq", "mrg32k3aM2SubSeq",
+                 "mrg32k3aM1Seq", "mrg32k3aM2Seq"):
+        m = re.search(r"unsigned int %s\[(\d+)\]\[3\]\[3\] = \{(.*?)\};" % name, txt, re.S)
+        nums = [int(v) for v in re.findall(r"(\d+)u", m.group(2))]
+        out[name] = np.array(nums, dtype=np.uint64).reshape(-1, 3, 3)  # SubSeq: 51 of [56] filled
+    return out
+
+
+def test_jump_matrices_vs_curand_tables(orc):
+    # cuRAND precalc: M[i] = A^(2^i), SubSeq[i] = A^(2^(76+i)), Seq[i] = A^(2^(127+i)).
+    t = _curand_tables()
+    A1, A2 = orc.mrg_matrices()
+    for comp, A, m in (("1", A1, M1), ("2", A2, M2)):
+        for i in range(64):
+            assert orc.mat_pow(A, 1 << i, m) == t["mrg32k3aM%s" % comp][i].tolist()
+        for i in range(51):
+            assert orc.mat_pow(A, 1 << (76 + i), m) == t["mrg32k3aM%sSubSeq" % comp][i].tolist()
+        S127 = orc.mat_pow(A, 1 << 127, m)  # exponents beyond 2^128: chain the powers
+        for i in range(64):
+            assert orc.mat_pow(S127, 1 << i, m) == t["mrg32k3aM%sSeq" % comp][i].tolist()
+
+
+def test_position_vs_curand_skipahead(orc, curand_pin):
+    rng = random.Random(3)
+    for _ in range(40):
+        s = _valid_seed(rng)
+        g = rng.getrandbits(rng.choice([1, 8, 40, 64]))
+        u = rng.getrandbits(rng.choice([1, 10, 51]))
+        o = rng.getrandbits(rng.choice([1, 20, 64]))
+        assert orc.mrg_position(s, g, u, o) == curand_pin.ask("mrgskip", *s, g, u, o)
+
+
+def test_jump_equals_iterate(orc):
+    # SPEC L600 acceptance #1: 100 random n in [0, 10^6].
+    rng = random.Random(1)
+    seed = _valid_seed(rng)
+    base = orc.generate(W.MRG32K3A, seed, 1, 1_000_008)[0]
+    for n in [0, 1, 2, 3, 7, 100, 2000, 123456] + [rng.randrange(1_000_001) for _ in range(100)]:
+        got = orc.generate(W.MRG32K3A, seed, 1, 8, offset=n)[0]
+        assert np.array_equal(got, base[n:n + 8]), n
+    # and state-level: jump(n) == n steps (SPEC L165 example n = 123456)
+    s = list(seed)
+    for _ in range(123456):
+        _, s = orc.mrg_step(s)
+    assert orc.mrg_jump(seed, 123456) == s
+
+
+def test_jump_homomorphism_120bit(orc):
+    # SPEC L601 acceptance #2: J(a) J(b) = J(a+b) for random 120-bit a, b.
+    rng = random.Random(2)
+    A1, A2 = orc.mrg_matrices()
+    for _ in range(100):
+        a, b = rng.getrandbits(120), rng.getrandbits(120)
+        for A, m in ((A1, M1), (A2, M2)):
+            assert orc.mat_mul(orc.mat_pow(A, a, m), orc.mat_pow(A, b, m), m) == \
+                orc.mat_pow(A, a + b, m)
+
+
+def test_stream_geometry(orc):
+    # P L264-268: 2^64 streams x 2^127 = 2^191; 2^127 / 2^76 = 2^51 substreams.
+    A1, A2 = orc.mrg_matrices()
+    for A, m in ((A1, M1), (A2, M2)):
+        assert orc.mat_pow(orc.mat_pow(A, 1 << 76, m), 1 << 51, m) == orc.mat_pow(A, 1 << 127, m)
+        # full period 2^191 - 1 ... the component periods divide m^3 - 1: A^(m^3-1) = I
+        assert orc.mat_pow(A, m ** 3 - 1, m) == [[1, 0, 0], [0, 1, 0], [0, 0, 1]]
+    # substream adjacency (S L173)
+    s = [12345] * 6
+    assert orc.mrg_jump(orc.mrg_position(s, 0, 1, 0), 1 << 76) == orc.mrg_position(s, 0, 2, 0)
+    assert orc.mrg_position(s, 3, 0, 0) == orc.mrg_position(s, 2, 1 << 51, 0)
+
+
+def test_oracle_rejects_invalid_seeds(orc):
+    for bad in ([0] * 6, [1, 1, 1, 0, 0, 0], [M1, 1, 1, 1, 1, 1], [1, 1, 1, 1, 1, M2], [1, 2]):
+        with pytest.raises(ValueError):
+            orc.generate(W.MRG32K3A, bad, 1, 1)
+    with pytest.raises(ValueError):
+        orc.generate(W.PHILOX4X32_10, [1, 2, 3], 1, 1)
+    with pytest.raises(ValueError):
+        orc.generate(W.PHILOX4X32_10, [1], 1, 1, spacing=W.SPACING_SUBSTREAM)
+
+
+# --------------------------------------------------------------------------- conversions
+
+def test_norm_constant_and_f64_range(orc):
+    # R7: L'Ecuyer's norm as binary64; u = fl(z * norm) in (0, 1) for z in [1, m1].
+    assert float.hex(orc.mrg_to_f64(1)) == "0x1.000000d00000bp-32"
+    assert 0.0 < orc.mrg_to_f64(1) and orc.mrg_to_f64(M1) < 1.0
+    rng = random.Random(4)
+    norm = float.fromhex("0x1.000000d00000bp-32")
+    for z in [1, 2, M1 - 1, M1] + [rng.randrange(1, M1 + 1) for _ in range(2000)]:
+        # one correctly-rounded multiply: compare with exact rational rounding
+        exact = Fraction(z) * Fraction(norm)
+        got = orc.mrg_to_f64(z)
+        assert abs(Fraction(got) - exact) <= Fraction(math.ulp(got)) / 2
+
+
+def test_f32_and_philox_f64_exact(orc):
+    rng = random.Random(6)
+    for w in [0, 1, 255, 256, 0xFFFFFFFF] + [rng.getrandbits(32) for _ in range(2000)]:
+        assert Fraction(orc.to_f32(w)) == Fraction(w >> 8, 1 << 24)
+    for _ in range(2000):
+        lo, hi = rng.getrandbits(32), rng.getrandbits(32)
+        assert Fraction(orc.philox_to_f64(lo, hi)) == Fraction(((hi << 32) | lo) >> 11, 1 << 53)
+    assert orc.philox_to_f64(0xFFFFFFFF, 0xFFFFFFFF) < 1.0
+    assert orc.to_f32(0xFFFFFFFF) < 1.0
+
+
+def test_rows_ranges_and_conversions_agree(orc):
+    for gen, sp in ((W.MRG32K3A, 1), (W.PHILOX4X32_10, 0)):
+        u = orc.generate(gen, [12345], 16, 512, spacing=sp).astype(np.uint64)
+        f = orc.generate(gen, [12345], 16, 512, spacing=sp, kind=orc.F32)
+        assert np.array_equal(f, (u >> 8).astype(np.float32) * np.float32(2.0 ** -24))
+        d = orc.generate(gen, [12345], 16, 256, spacing=sp, kind=orc.F64)
+        if gen == W.MRG32K3A:
+            assert u.min() >= 1 and u.max() <= M1
+            norm = float.fromhex("0x1.000000d00000bp-32")
+            assert np.array_equal(d, u[:, :256].astype(np.float64) * norm)
+        else:
+            lo, hi = u[:, 0::2], u[:, 1::2]
+            ref = ((hi << np.uint64(32)) | lo) >> np.uint64(11)
+            assert np.array_equal(d, ref.astype(np.float64) * 2.0 ** -53)
+        assert d.min() > 0.0 if gen == W.MRG32K3A else d.min() >= 0.0
+        assert d.max() < 1.0
+
+
+# --------------------------------------------------------------------------- layout / replay
+
+@pytest.mark.parametrize("gen,sp", [(W.MRG32K3A, 0), (W.MRG32K3A, 1), (W.PHILOX4X32_10, 0)])
+def test_offset_replay_and_thread_invariance(orc, gen, sp):
+    full = orc.generate(gen, [12345], 9, 300, spacing=sp, first=5, nthreads=1)
+    for k in (1, 2, 3, 5, 7, 100):
+        part = orc.generate(gen, [12345], 9, 300 - k, spacing=sp, first=5, offset=k, nthreads=3)
+        assert np.array_equal(part, full[:, k:])
+    assert np.array_equal(full, orc.generate(gen, [12345], 9, 300, spacing=sp, first=5, nthreads=7))
+    lst = orc.generate(gen, [12345], 0, 300, spacing=sp, first=5, streams=[8, 0, 3])
+    assert np.array_equal(lst, full[[8, 0, 3]])
+    # first_stream shifts handle streams (R4)
+    assert np.array_equal(orc.generate(gen, [12345], 4, 300, spacing=sp, first=10), full[5:9])
+
+
+def test_philox_f64_straddles_blocks(orc):
+    u = orc.generate(W.PHILOX4X32_10, [3, 4], 2, 64, offset=1).astype(np.uint64)
+    d = orc.generate(W.PHILOX4X32_10, [3, 4], 2, 32, offset=1, kind=orc.F64)
+    ref = ((u[:, 1::2] << np.uint64(32)) | u[:, 0::2]) >> np.uint64(11)
+    assert np.array_equal(d, ref.astype(np.float64) * 2.0 ** -53)
+
+
+# --------------------------------------------------------------------------- Monte Carlo
+
+def test_lattice_hit_probability_closed_form():
+    # R9: #{(X,Y) in [0,2^24)^2 : X^2+Y^2 < 2^48} = sum_X (isqrt(2^48 - X^2 - 1) + 1).
+    X = np.arange(1 << 24, dtype=np.int64)
+    r = (1 << 48) - X * X - 1
+    y = np.sqrt(r.astype(np.float64)).astype(np.int64)
+    y -= (y * y > r)
+    y += ((y + 1) * (y + 1) <= r)
+    count = int((y + 1).sum())
+    assert count == 221069946527026  # SURVEY App. A D9 (independent scratch)
+    assert abs(4 * count / 2 ** 48 - math.pi) < 3e-7
+
+
+@pytest.mark.parametrize("gen,sp", [(W.MRG32K3A, 1), (W.PHILOX4X32_10, 0)])
+def test_mc_count_recount_from_rows(orc, gen, sp):
+    # sample k uses draws 2k, 2k+1 from the offset (R9); recount from the rows.
+    for off in (0, 1, 3):
+        tot, counts = orc.mc_count(gen, [12345], 16, 1000, spacing=sp, first=2, offset=off)
+        u = orc.generate(gen, [12345], 16, 2000, spacing=sp, first=2, offset=off).astype(np.uint64)
+        X, Y = u[:, 0::2] >> np.uint64(8), u[:, 1::2] >> np.uint64(8)
+        ref = ((X * X + Y * Y) < np.uint64(1 << 48)).sum(axis=1)
+        assert np.array_equal(counts, ref) and tot == int(ref.sum())
+
+
+def test_mc_pi_within_4_sigma(orc):
+    p = 221069946527026 / 2 ** 48
+    for gen, sp in ((W.MRG32K3A, 1), (W.PHILOX4X32_10, 0)):
+        N = 256 * (1 << 14)
+        tot, _ = orc.mc_count(gen, [12345], 256, 1 << 14, spacing=sp)
+        sigma = 4 * math.sqrt(p * (1 - p) / N)
+        assert abs(4 * tot / N - math.pi) <= 4 * sigma
+
+
+def test_mc_survey_cross_check_first_64(orc):
+    # SURVEY App. A.6 (independent scratch implementation): MRG32k3a substreams
+    # 0..63 of seed 12345, 2^18 samples each -> 13179528 hits.
+    tot, _ = orc.mc_count(W.MRG32K3A, [12345], 64, 1 << 18, spacing=W.SPACING_SUBSTREAM)
+    assert tot == 13179528

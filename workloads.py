@@ -1,0 +1,82 @@
+"""Seeded synthetic workloads shared by tests/ and bench.py (arXiv 1412.8266 hot path).
+
+This module holds NO arithmetic of the method: only the workload shapes of
+BASELINE.json ``configs`` (seeds, stream counts, draws per stream, spacing) and
+a SplitMix64 index sampler used to pick which streams a parity test checks.
+Both the oracle side and the CUDA side read their inputs from here; neither
+imports the other.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+MRG32K3A = 1
+PHILOX4X32_10 = 2
+SPACING_STREAM = 0
+SPACING_SUBSTREAM = 1
+
+
+@dataclass(frozen=True)
+class Workload:
+    name: str
+    gen: int
+    seed: tuple
+    n_streams: int
+    n: int            # values per stream (fills) or samples per stream (MC)
+    spacing: int = SPACING_STREAM
+    first: int = 0
+
+
+# BASELINE.json configs[0]: MRG32k3a, seed 12345, 4 streams x 1000 (STREAM spacing, R4).
+C1 = Workload("C1", MRG32K3A, (12345,), 4, 1000, SPACING_STREAM)
+# configs[1]: 2^16 counter-streams x 1024 u32, key (12345, 0) (R6).
+C2 = Workload("C2", PHILOX4X32_10, (12345,), 1 << 16, 1024, SPACING_STREAM)
+# configs[2]: 2^20 substreams x 4096 doubles (SUBSTREAM spacing, R4).
+C3 = Workload("C3", MRG32K3A, (12345,), 1 << 20, 4096, SPACING_SUBSTREAM)
+# configs[3]: MC pi, 2^38 samples over 2^20 streams (2^18 samples each).
+C4_MRG = Workload("C4-mrg", MRG32K3A, (12345,), 1 << 20, 1 << 18, SPACING_SUBSTREAM)
+C4_PHILOX = Workload("C4-philox", PHILOX4X32_10, (12345,), 1 << 20, 1 << 18, SPACING_STREAM)
+# configs[4]: 16 GiB u32 per GPU = 2^20 streams x 4096 per rank, both generators.
+C5_MRG = Workload("C5-mrg", MRG32K3A, (12345,), 1 << 20, 4096, SPACING_SUBSTREAM)
+C5_PHILOX = Workload("C5-philox", PHILOX4X32_10, (12345,), 1 << 20, 4096, SPACING_STREAM)
+
+
+def rank_slice(w: Workload, rank: int, world: int, weak: bool) -> Workload:
+    """The stream range rank ``rank`` of ``world`` owns.
+
+    weak=True: every rank gets w.n_streams streams starting at rank*n_streams
+    (C5). weak=False: the w.n_streams streams are split into contiguous ranges
+    (C4)."""
+    if weak:
+        return Workload(w.name, w.gen, w.seed, w.n_streams, w.n, w.spacing,
+                        w.first + rank * w.n_streams)
+    lo = w.n_streams * rank // world
+    hi = w.n_streams * (rank + 1) // world
+    return Workload(w.name, w.gen, w.seed, hi - lo, w.n, w.spacing, w.first + lo)
+
+
+def splitmix64(seed: int, count: int):
+    """SplitMix64 outputs (Steele et al. 2014) — index sampling only."""
+    out = []
+    x = seed & 0xFFFFFFFFFFFFFFFF
+    for _ in range(count):
+        x = (x + 0x9E3779B97F4A7C15) & 0xFFFFFFFFFFFFFFFF
+        z = x
+        z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & 0xFFFFFFFFFFFFFFFF
+        z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & 0xFFFFFFFFFFFFFFFF
+        out.append(z ^ (z >> 31))
+    return out
+
+
+def sample_streams(n_streams: int, k: int = 1024, seed: int = 2026):
+    """Sorted unique stream indices: edges (0..3, 2^b-1, 2^b, last) plus k
+    SplitMix64-drawn indices (SURVEY §8c parity selection)."""
+    s = {0, 1, 2, 3, n_streams - 1}
+    b = 4
+    while (1 << b) <= n_streams:
+        s.add((1 << b) - 1)
+        if (1 << b) < n_streams:
+            s.add(1 << b)
+        b += 1
+    s.update(v % n_streams for v in splitmix64(seed, k))
+    return sorted(i for i in s if 0 <= i < n_streams)
