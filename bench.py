@@ -1,0 +1,371 @@
+#!/usr/bin/env python
+"""Benchmark of the ShoveRand hot path on B200 (arXiv 1412.8266).
+
+Workload (BASELINE.json configs[4], "C5"; the metric is quoted on it): every
+rank fills 16 GiB = 2^20 streams x 4096 u32 from MRG32k3a (substreams of seed
+12345) and 16 GiB from Philox4x32-10 (counter-streams, key 12345); rank r owns
+streams [r*2^20, (r+1)*2^20) (weak scaling, no collective on the data path).
+One step = the whole bulk path for both generators: create (seed validation,
+jump-table products, per-stream start states) -> generate_u32 -> destroy.
+value = u32 numbers produced by all ranks / max-over-ranks device time.
+
+Also reported (same JSON line): per-kernel timings and the HBM-write roofline
+of the dominant kernel, the fused Monte Carlo pi (configs[3], strong scaling,
+one NCCL all_reduce of the hit count), the f64 fill (configs[2]), the oracle
+CPU baseline, e2e through shv_generate_u32_host (pinned host buffer), clocks.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl shv|reference]
+  torchrun --nproc-per-node N bench.py --gpus N ...
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import workloads as W  # noqa: E402
+
+METRIC = "Gnumbers/s (u32) per GPU and box at 1/2/4/8 B200; % of HBM-write roofline"
+UNIT = "Gnumbers/s"
+WORKLOAD = ("C5: bulk fill 16 GiB u32 per GPU from MRG32k3a (2^20 substreams x 4096, seed 12345) "
+            "and Philox4x32-10 (2^20 counter-streams x 4096, key 12345); rank r owns streams "
+            "[r*2^20,(r+1)*2^20)")
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def traffic_from_profiles(kernel_key):
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        v = d.get(kernel_key)
+        if v:
+            return float(v["dram_bytes_read"] + v["dram_bytes_write"])
+    return None
+
+
+class Clocks:
+    """nvidia-smi sampler running during the timed region (B200_PROFILING.md)."""
+
+    def __init__(self, gpus):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        q = ("index,clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                                       "-i", ",".join(str(g) for g in gpus), "-lms", "100"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except FileNotFoundError:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return None
+        self.p.terminate()
+        self.p.wait()
+        self.f.seek(0)
+        rows = [r.split(", ") for r in self.f.read().strip().splitlines() if r.count(",") >= 7]
+        os.unlink(self.f.name)
+        if not rows:
+            return None
+        sm = [float(r[1]) for r in rows if r[1].strip().isdigit()]
+        mx = max(float(r[2]) for r in rows if r[2].strip().isdigit())
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in rows for k in range(4) if r[4 + k].strip() == "Active"})
+        busy = [s for s in sm if s > 0.5 * mx] or sm
+        return {"sm_mhz": statistics.median(busy), "sm_max_mhz": mx, "reasons": reasons,
+                "samples": len(rows)}
+
+
+# ---------------------------------------------------------------------------- oracle arm
+
+def oracle_sample(target_s: float, threads: int):
+    """Time the oracle (as it stands) on a bounded prefix of the C5 workload:
+    the first k streams x 4096 u32 of each generator, k calibrated so the run
+    takes about target_s seconds. Returns (numbers, seconds, description)."""
+    import oracle
+    n = W.C5_MRG.n
+
+    def run(k):
+        t = time.perf_counter()
+        oracle.generate(W.MRG32K3A, list(W.C5_MRG.seed), k, n, spacing=W.C5_MRG.spacing,
+                        nthreads=threads)
+        oracle.generate(W.PHILOX4X32_10, list(W.C5_PHILOX.seed), k, n,
+                        spacing=W.C5_PHILOX.spacing, nthreads=threads)
+        return time.perf_counter() - t
+
+    k0 = max(threads, 16)
+    t0 = run(k0)
+    k = max(k0, min(W.C5_MRG.n_streams, int(k0 * target_s / max(t0, 1e-3))))
+    t = run(k)
+    return 2 * k * n, t, (f"first {k} of 2^20 streams x {n} u32 from each of MRG32k3a and "
+                          f"Philox4x32-10 (C5 prefix), {threads} threads")
+
+
+def cpu_baseline(threads):
+    nums, t, desc = oracle_sample(12.0, threads)
+    return {"value": nums / t / 1e9, "unit": UNIT, "cores": threads, "kind": "oracle",
+            "sample": desc, "seconds": round(t, 3)}
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    threads = len(os.sched_getaffinity(0))
+    import oracle
+    oracle.build()
+    per_step_target = max(2.0, min(20.0, 150.0 / max(1, args.steps + args.warmup)))
+    _, _, _ = oracle_sample(0.5, threads)  # warm the library
+    for _ in range(args.warmup):
+        oracle_sample(per_step_target, threads)
+    tot_n, tot_t, desc = 0, 0.0, ""
+    for _ in range(args.steps):
+        nums, t, desc = oracle_sample(per_step_target, threads)
+        tot_n += nums
+        tot_t += t
+    value = tot_n / tot_t / 1e9
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * tot_t / max(1, args.steps), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+            "config": {"workload": WORKLOAD, "sample": desc},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "oracle",
+                             "sample": desc},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------- GPU arm
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="shv", choices=["shv", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-parts", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3) if args.impl == "shv" else args.warmup
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_1412_8266_b200 as shv
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    stream = torch.cuda.current_stream()
+    sp = stream.cuda_stream
+    wm = W.rank_slice(W.C5_MRG, rank, world, weak=True)
+    wp = W.rank_slice(W.C5_PHILOX, rank, world, weak=True)
+    n = wm.n
+    total_per_rank = wm.n_streams * n  # per generator
+    out = torch.empty(total_per_rank, dtype=torch.int32, device=dev)  # 16 GiB
+    state = torch.empty(6 * wm.n_streams, dtype=torch.int32, device=dev)
+    ev = {k: [torch.cuda.Event(enable_timing=True) for _ in range(2)] for k in ("mrg", "philox")}
+    kt = {"mrg": [], "philox": []}
+
+    def step(timed_kernels=False):
+        h = shv.shv_streams_create_ex(wm.gen, list(wm.seed), wm.first, wm.n_streams, wm.spacing,
+                                      state, 0, local, sp)
+        if timed_kernels:
+            ev["mrg"][0].record(stream)
+        shv.shv_generate_u32(h, out, n, sp)
+        if timed_kernels:
+            ev["mrg"][1].record(stream)
+        shv.shv_streams_destroy(h)
+        h = shv.shv_streams_create_ex(wp.gen, list(wp.seed), wp.first, wp.n_streams, wp.spacing,
+                                      None, 0, local, sp)
+        if timed_kernels:
+            ev["philox"][0].record(stream)
+        shv.shv_generate_u32(h, out, n, sp)
+        if timed_kernels:
+            ev["philox"][1].record(stream)
+        shv.shv_streams_destroy(h)
+
+    for _ in range(args.warmup):
+        step()
+    # per-kernel durations (same launches as the step, events on the launching stream)
+    for _ in range(args.steps):
+        step(timed_kernels=True)
+        torch.cuda.synchronize()
+        for k in kt:
+            kt[k].append(ev[k][0].elapsed_time(ev[k][1]))
+
+    clocks = Clocks([local] if world == 1 else list(range(world))) if rank == 0 else None
+    barrier()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    for _ in range(args.steps):
+        step()
+    t1.record(stream)
+    barrier()
+    ms = max_over_ranks(t0.elapsed_time(t1))
+    clk = clocks.stop() if clocks else None
+    ms_step = ms / args.steps
+    numbers = 2 * total_per_rank * world * args.steps
+    value = numbers / (ms * 1e-3) / 1e9
+
+    peak, peak_src = peaks()
+    kms = {k: statistics.mean(v) for k, v in kt.items()}
+    dom = max(kms, key=kms.get)
+    alg_bytes = 4 * total_per_rank  # u32 written per launch (4 B/number, 0 read)
+    achieved = alg_bytes / (kms[dom] * 1e-3) / 1e9
+    roof = {"bound": "hbm", "kernel": "mrg_fill_kernel<u32>" if dom == "mrg" else "philox_fill_fast_kernel<u32>",
+            "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+            "frac": round(achieved / peak, 4), "peak_source": peak_src,
+            "traffic": traffic_from_profiles(dom),
+            "algorithmic_bytes_per_launch": alg_bytes}
+    parts = {k: {"ms": round(kms[k], 4), "Gnumbers_per_s": round(total_per_rank / (kms[k] * 1e-3) / 1e9, 1),
+                 "GB_per_s": round(alg_bytes / (kms[k] * 1e-3) / 1e9, 1),
+                 "frac_of_hbm_peak": round(alg_bytes / (kms[k] * 1e-3) / 1e9 / peak, 4)}
+             for k in kms}
+
+    # ---- fused Monte Carlo pi (configs[3]) and f64 fill (configs[2]) ----
+    if not args.no_parts:
+        for w in (W.C4_MRG, W.C4_PHILOX):
+            ws = W.rank_slice(w, rank, world, weak=False)
+            st = torch.empty(6 * ws.n_streams, dtype=torch.int32, device=dev)
+            hits = torch.zeros(1, dtype=torch.int64, device=dev)
+            times = []
+            for it in range(3):
+                h = shv.shv_streams_create_ex(ws.gen, list(ws.seed), ws.first, ws.n_streams, ws.spacing,
+                                              st if ws.gen == W.MRG32K3A else None, 0, local, sp)
+                hits.zero_()
+                barrier()
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+                shv.shv_mc_pi(h, ws.n, hits, sp)
+                if world > 1:
+                    dist.all_reduce(hits)
+                b.record(stream)
+                barrier()
+                shv.shv_streams_destroy(h)
+                times.append(max_over_ranks(a.elapsed_time(b)))
+            tot = int(hits.item())
+            N = w.n_streams * w.n
+            import math
+            p = 221069946527026 / 2 ** 48
+            pi_hat = 4 * tot / N
+            t_ms = min(times)
+            parts["mc_pi_" + ("mrg" if w.gen == W.MRG32K3A else "philox")] = {
+                "ms": round(t_ms, 3), "Gsamples_per_s": round(N / (t_ms * 1e-3) / 1e9, 1),
+                "Gnumbers_per_s": round(2 * N / (t_ms * 1e-3) / 1e9, 1), "hits": tot,
+                "pi_hat": pi_hat, "within_4sigma": abs(pi_hat - math.pi) <= 4 * 4 * math.sqrt(p * (1 - p) / N),
+                "scaling": "strong", "samples": N}
+            del st
+        ws = W.rank_slice(W.C3, rank, world, weak=True)
+        out64 = out.view(torch.float64)[: ws.n_streams * ws.n // 2]
+        # 2^20 x 4096 f64 needs 32 GiB: fill half the rows per launch into the 16 GiB buffer
+        half = ws.n_streams // 2
+        times = []
+        for it in range(4):
+            h = shv.shv_streams_create_ex(ws.gen, list(ws.seed), ws.first, half, ws.spacing, state,
+                                          0, local, sp)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            shv.shv_generate_f64(h, out64, ws.n, sp)
+            b.record(stream)
+            torch.cuda.synchronize()
+            shv.shv_streams_destroy(h)
+            if it:
+                times.append(a.elapsed_time(b))
+        t_ms = statistics.mean(times)
+        parts["mrg_fill_f64"] = {"ms": round(t_ms, 4), "numbers": half * ws.n,
+                                 "Gnumbers_per_s": round(half * ws.n / (t_ms * 1e-3) / 1e9, 1),
+                                 "GB_per_s": round(8 * half * ws.n / (t_ms * 1e-3) / 1e9, 1),
+                                 "frac_of_hbm_peak": round(8 * half * ws.n / (t_ms * 1e-3) / 1e9 / peak, 4)}
+
+    # ---- e2e: same workload through shv_generate_u32_host into pinned host memory ----
+    e2e = None
+    if not args.no_e2e:
+        host = torch.empty(total_per_rank, dtype=torch.int32, pin_memory=True)
+        e2e_steps = min(args.steps, 3)
+
+        def step_host():
+            for w, stt in ((wm, state), (wp, None)):
+                h = shv.shv_streams_create_ex(w.gen, list(w.seed), w.first, w.n_streams, w.spacing,
+                                              stt, 0, local, sp)
+                shv.shv_generate_u32_host(h, host, n, sp)
+                shv.shv_streams_destroy(h)
+        step_host()
+        barrier()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(e2e_steps):
+            step_host()
+        b.record(stream)
+        barrier()
+        e_ms = max_over_ranks(a.elapsed_time(b))
+        e2e = {"value": 2 * total_per_rank * world * e2e_steps / (e_ms * 1e-3) / 1e9, "unit": UNIT,
+               "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 2 * 4 * total_per_rank,
+               "steps": e2e_steps, "api": "shv_generate_u32_host (pinned host buffer)",
+               "note": "inputs are seed words passed as call arguments; no input tensor is copied"}
+        del host
+
+    if rank == 0:
+        cpu = None
+        if world == 1 and not args.no_cpu:
+            import oracle
+            oracle.build()
+            cpu = cpu_baseline(len(os.sched_getaffinity(0)))
+        line = {"metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 4),
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
+                "data": "synthetic",
+                "config": {"workload": WORKLOAD, "streams_per_gpu": wm.n_streams,
+                           "numbers_per_stream": n, "bytes_per_gpu_per_generator": alg_bytes,
+                           "parallelism": f"streams sharded over {world} GPU(s), no data-path collective",
+                           "l2": "no flush: each launch writes 16 GiB >> 126 MB L2"},
+                "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
+                "gpu_launches": 3 * args.steps, "clocks": clk, "parts": parts,
+                "per_gpu_Gnumbers_per_s": round(value / world, 2)}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,187 @@
+/*
+ * shv.h — C ABI of the B200-native ShoveRand hot path (arXiv 1412.8266):
+ * bulk generation of many independent, reproducible pseudorandom streams.
+ *
+ * Citations: "P Lnn" = PAPER.md line nn (section in brackets), "S Lnn" =
+ * SPEC.md line nn, "Rk" = reading k in DESIGN.md §3 (the paper is silent or
+ * ambiguous there). Library: paper_1412_8266_b200/libshv.so (sm_100a).
+ *
+ * Model of the problem (P L353-382 [§5.1], L480-499 [Listing 1]): the caller
+ * states only how much parallelism it needs (n_streams); the library owns the
+ * distribution of the random sequence over those streams (Sequence Splitting,
+ * P L109-112 [§2.3]) and keeps the user's buffers and kernels free of generator
+ * plumbing. Handle stream i < n_streams is
+ *   MRG32k3a, SHV_SPACING_STREAM    : stream first+i, 2^127 draws apart  (P L264-268 [§4.1])
+ *   MRG32k3a, SHV_SPACING_SUBSTREAM : substream first+i of stream 0, 2^76 apart (ibid.)
+ *   Philox4x32-10 (STREAM only)     : counter-stream g = first+i, counter
+ *                                     (blk_lo, blk_hi, g_lo, g_hi), key = seed (P L322-336 [§4.3]; R6)
+ * Every stream of a handle sits at the same draw offset o (u128), which each
+ * generate / mc_pi call advances by the draws it consumed (S L58; R8).
+ *
+ * Conventions for every call:
+ *  - extern "C", no exceptions escape, never aborts, does not change the
+ *    calling thread's current CUDA device (it is saved and restored).
+ *  - Device pointers are plain CUDA device addresses (e.g. torch
+ *    tensor.data_ptr()) on the handle's device; the caller owns them and keeps
+ *    them alive until the work queued on cuda_stream has completed.
+ *  - cuda_stream is a cudaStream_t (NULL = legacy default stream). Kernel work
+ *    is stream-ordered and asynchronous; host-side validation is synchronous.
+ *  - A call that returns an error has no side effects (no launch, no offset
+ *    change), except SHV_ERR_CUDA, which reports an error the CUDA runtime
+ *    raised while enqueueing. shv_last_error_message() gives detail
+ *    (thread-local).
+ *  - Handles are opaque non-zero ids in a mutex-protected registry; a handle
+ *    must not be used concurrently from two host threads (S L96).
+ */
+#ifndef SHV_H
+#define SHV_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    SHV_OK = 0,
+    SHV_ERR_INVALID_ARGUMENT = 1,     /* bad enum, NULL out-pointer, size overflow, stream exhausted */
+    SHV_ERR_INVALID_SEED = 2,         /* S L50, L117-118: residue >= m, or an all-zero MRG triple */
+    SHV_ERR_INSUFFICIENT_STREAMS = 3, /* S L50, L199-200: first+n beyond 2^64 streams / 2^51 substreams */
+    SHV_ERR_UNSUPPORTED = 4,          /* combination the generator does not define (Philox substreams) */
+    SHV_ERR_LIFECYCLE = 5,            /* S L67-72: unknown, destroyed or double-destroyed handle */
+    SHV_ERR_MISALIGNED = 6,           /* output pointer not aligned to its element size */
+    SHV_ERR_EMPTY_EXPERIMENT = 7,     /* S L535: Monte Carlo with zero samples */
+    SHV_ERR_MISSING_PARAMETERS = 8,   /* reserved for parameter-file generators (TinyMT, MTGP) */
+    SHV_ERR_CUDA = 9                  /* CUDA runtime error while enqueueing */
+} shv_status;
+
+typedef enum {
+    SHV_GEN_MRG32K3A = 1,       /* [LEcuyer1999], P L82-86, L250-282 [§4.1] */
+    SHV_GEN_PHILOX4X32_10 = 2   /* [Salmon.etal.2011], P L88-90, L322-336 [§4.3]; variant per S L275 */
+} shv_gen;
+
+typedef enum {
+    SHV_SPACING_STREAM = 0,     /* MRG: 2^127 draws apart; Philox: counter-stream index */
+    SHV_SPACING_SUBSTREAM = 1   /* MRG: 2^76 draws apart; Philox: SHV_ERR_UNSUPPORTED */
+} shv_spacing;
+
+typedef enum {
+    SHV_JUMP_DRAWS = 0,         /* o += n                            */
+    SHV_JUMP_SUBSTREAMS = 1,    /* o += n * 2^76  (MRG only)         */
+    SHV_JUMP_STREAMS = 2        /* o += n * 2^127 (MRG only)         */
+} shv_jump_kind;
+
+typedef uint64_t shv_streams; /* registry id; 0 is never valid */
+
+/* Checkpoint record (S L98-99, L193-194): a stream family is a pure function
+ * of these fields, so create_ex + shv_jump(offset) resumes bit-exactly. */
+typedef struct {
+    uint32_t gen, spacing;
+    uint32_t seed[6];     /* MRG: s10 s11 s12 s20 s21 s22; Philox: key0 key1 0 0 0 0 */
+    uint64_t first_stream, n_streams;
+    uint64_t offset_lo, offset_hi;
+} shv_position;
+
+/* Bytes of per-stream state a handle needs: MRG32k3a 24*n_streams (six u32
+ * per stream, SoA: word k of stream i at [k*n_streams + i]; P L257-258
+ * "only stores 6 integers"); Philox 0 (counter-based, no state). */
+size_t shv_state_bytes(int gen, uint64_t n_streams);
+
+/* Short form (north star): first_stream 0, SHV_SPACING_STREAM, current
+ * device, legacy default stream, library-allocated state (cudaMalloc, freed
+ * by shv_streams_destroy). Host-synchronous. */
+shv_status shv_streams_create(shv_streams* out, int gen, const uint32_t* seed,
+                              size_t seed_words, uint64_t n_streams);
+
+/* Full form (P L358-382 [§5.1] init(block_num)).
+ *  seed/seed_words: MRG32k3a 1 word v (all six residues = v) or 6 words
+ *    s10 s11 s12 s20 s21 s22 (S L114-119); Philox 1 or 2 words key0[, key1]
+ *    (key1 = 0 if omitted). Anything else: SHV_ERR_INVALID_ARGUMENT.
+ *  first_stream, n_streams: handle stream i is family stream first_stream+i.
+ *    n_streams >= 1.
+ *  spacing: see shv_spacing.
+ *  d_state: MRG only — device buffer of state_bytes >= shv_state_bytes(),
+ *    4-byte aligned, owned by the caller until destroy; NULL lets the library
+ *    allocate it. Ignored for Philox.
+ *  device: CUDA device ordinal the handle lives on (-1 = current device).
+ *  cuda_stream: the per-stream seeding kernel (start state = product of
+ *    host-built jump matrices applied to the seed, P L264-268) is enqueued
+ *    here; the first create on a device also uploads the jump tables
+ *    synchronously. */
+shv_status shv_streams_create_ex(shv_streams* out, int gen, const uint32_t* seed,
+                                 size_t seed_words, uint64_t first_stream, uint64_t n_streams,
+                                 int spacing, void* d_state, size_t state_bytes, int device,
+                                 void* cuda_stream);
+
+/* Advance every stream of the handle (host-side only; S L157-174):
+ * kind = SHV_JUMP_DRAWS / SUBSTREAMS / STREAMS, see shv_jump_kind.
+ * Errors: UNSUPPORTED for Philox sub/streams; INVALID_ARGUMENT if the offset
+ * would leave the stream (Philox 2^66 draws; MRG offset beyond 2^128). */
+shv_status shv_jump(shv_streams h, int kind, uint64_t n);
+
+/* Bulk fill (P L485-490 [Listing 1] with n_per_stream draws per stream):
+ * d_out[i*n + j] = value of draw o+j of stream i (f64 Philox: draws o+2j,
+ * o+2j+1), for i < n_streams, j < n; then o += n (Philox f64: 2n). Row-major,
+ * stream-major (R8). Values (R7):
+ *   u32: the generator word (MRG: z in [1, m1]; Philox: lane x,y,z,w order);
+ *   f32: (w >> 8) * 2^-24 in [0,1), exact;
+ *   f64: MRG fl64(z * 0x1.000000d00000bp-32) in (0,1); Philox
+ *        ((w_{2j+1} << 32 | w_{2j}) >> 11) * 2^-53 in [0,1), exact.
+ * d_out must be aligned to the element size (else SHV_ERR_MISALIGNED); a
+ * 32-byte aligned pointer with 32-byte rows takes the vectorised path, any
+ * other shape a scalar path with identical values. n = 0 is a no-op. */
+shv_status shv_generate_u32(shv_streams h, uint32_t* d_out, uint64_t n_per_stream, void* cuda_stream);
+shv_status shv_generate_f32(shv_streams h, float* d_out, uint64_t n_per_stream, void* cuda_stream);
+shv_status shv_generate_f64(shv_streams h, double* d_out, uint64_t n_per_stream, void* cuda_stream);
+
+/* Same values as shv_generate_u32, written to a HOST buffer h_out (pinned
+ * memory recommended). The library generates into device staging slices and
+ * copies them back on an internal copy stream overlapped with generation;
+ * completion is ordered on cuda_stream (synchronize it before reading). */
+shv_status shv_generate_u32_host(shv_streams h, uint32_t* h_out, uint64_t n_per_stream, void* cuda_stream);
+
+/* Fused Monte Carlo pi dartboard (P L18-21 [§1], S L529-537; R9): sample k of
+ * stream i uses draws o+2k, o+2k+1; X = w>>8, Y = w'>>8; hit iff
+ * X^2 + Y^2 < 2^48. Numbers never touch memory. *d_hits (device u64, zeroed
+ * by the caller) += total hits over the handle's streams; o += 2*samples.
+ * pi_hat = 4 * hits / (n_streams * samples). samples = 0:
+ * SHV_ERR_EMPTY_EXPERIMENT. d_stream_counts (optional, _ex only): device u64
+ * per stream, += that stream's hits (used by parity tests). */
+shv_status shv_mc_pi(shv_streams h, uint64_t samples_per_stream, uint64_t* d_hits, void* cuda_stream);
+shv_status shv_mc_pi_ex(shv_streams h, uint64_t samples_per_stream, uint64_t* d_hits,
+                        uint64_t* d_stream_counts, void* cuda_stream);
+
+shv_status shv_get_position(shv_streams h, shv_position* out);
+
+/* Release (P L498 [Listing 1] release()). Frees library-allocated state with
+ * cudaFree (which synchronizes the device); the id becomes invalid, a second
+ * destroy returns SHV_ERR_LIFECYCLE (S L67-72). */
+shv_status shv_streams_destroy(shv_streams h);
+
+const char* shv_status_string(shv_status s);
+const char* shv_last_error_message(void);
+
+/* ---- launch configuration (results never depend on it; R10) ---- */
+/* Override the persistent-grid shape and work split of one handle:
+ * blocks_per_sm (0 = occupancy maximum), threads_per_block (0 = 256,
+ * else a multiple of 32 in [32, 1024]), segment (0 = automatic; else the
+ * number of draws-per-value units one work item covers, a multiple of 8). */
+shv_status shv_set_launch_config(shv_streams h, uint32_t blocks_per_sm,
+                                 uint32_t threads_per_block, uint64_t segment);
+
+/* ---- host-only utilities (no GPU needed) ---- */
+/* Rank r of world w owns handle streams [*first, *first + *count) of a
+ * family of total_streams (contiguous split). */
+shv_status shv_partition(uint64_t total_streams, int rank, int world,
+                         uint64_t* first, uint64_t* count);
+/* The host-built jump matrices the kernels use: out[0..8] = A1^e mod m1,
+ * out[9..17] = A2^e mod m2 (row-major), e = e_hi*2^64 + e_lo (S L148-156). */
+shv_status shv_jump_matrix(uint64_t e_lo, uint64_t e_hi, uint32_t out[18]);
+/* Library version string and the sm_ architecture it was built for. */
+const char* shv_build_info(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SHV_H */

@@ -1,0 +1,687 @@
+// shv_api.cpp — the C ABI (include/shv.h): handle registry, validation,
+// host-side jump-matrix math (H1), partitioning and work split (H2), launches.
+//
+// Host math: 3x3 matrices mod m = 2^32 - c with entries < m; products folded
+// with 2^32 = c (mod m). A process-wide table P[b] = A^(2^b), b < 192, built
+// once by repeated squaring, turns any jump A^e (e < 2^192) into a product over
+// the set bits of e (P L112-117 [§2.3]: jump-ahead; P L264-268 [§4.1]: streams
+// 2^127 and substreams 2^76 apart).
+#include "../../include/shv.h"
+
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <unordered_map>
+
+#include "shv_internal.h"
+
+namespace shv {
+namespace {
+
+using u128 = unsigned __int128;
+
+constexpr uint32_t kM1 = 4294967087u, kM2 = 4294944443u;
+constexpr uint32_t kC[2] = {209u, 22853u};
+constexpr uint32_t kMod[2] = {kM1, kM2};
+
+thread_local std::string t_err;
+
+shv_status fail(shv_status s, const char* fmt, ...)
+{
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    t_err = buf;
+    return s;
+}
+
+// ---------------------------------------------------------------- H1: jump math
+
+struct Mat {
+    uint32_t v[9];
+};
+
+inline uint32_t fold(uint64_t x, int comp)
+{
+    const uint64_t c = kC[comp], m = kMod[comp];
+    x = (x >> 32) * c + (uint32_t)x;
+    x = (x >> 32) * c + (uint32_t)x;
+    return (uint32_t)(x >= m ? x - m : x);
+}
+
+Mat mul(const Mat& A, const Mat& B, int comp)
+{
+    Mat R;
+    for (int r = 0; r < 3; ++r)
+        for (int c = 0; c < 3; ++c) {
+            uint64_t s = 0;
+            for (int k = 0; k < 3; ++k) s += fold((uint64_t)A.v[3 * r + k] * B.v[3 * k + c], comp);
+            R.v[3 * r + c] = fold(s, comp);
+        }
+    return R;
+}
+
+const Mat kIdentity = {{1, 0, 0, 0, 1, 0, 0, 0, 1}};
+
+struct PowTable {
+    Mat p[2][192];  // p[comp][b] = A_comp^(2^b)
+    PowTable()
+    {
+        // Companion matrices of x1,n = a12 x1,n-2 - a13n x1,n-3 and
+        // x2,n = a21 x2,n-1 - a23n x2,n-3 on (x_{n-3}, x_{n-2}, x_{n-1}) (R3).
+        const Mat A1 = {{0, 1, 0, 0, 0, 1, kM1 - 810728u, 1403580u, 0}};
+        const Mat A2 = {{0, 1, 0, 0, 0, 1, kM2 - 1370589u, 0, 527612u}};
+        p[0][0] = A1;
+        p[1][0] = A2;
+        for (int c = 0; c < 2; ++c)
+            for (int b = 1; b < 192; ++b) p[c][b] = mul(p[c][b - 1], p[c][b - 1], c);
+    }
+};
+
+const PowTable& pow_table()
+{
+    static const PowTable t;
+    return t;
+}
+
+// A^(e * 2^shift), e < 2^128, shift + bitlen(e) <= 192.
+Mat mpow(u128 e, int shift, int comp)
+{
+    const PowTable& T = pow_table();
+    Mat R = kIdentity;
+    for (int b = 0; e; ++b, e >>= 1)
+        if (e & 1) R = mul(R, T.p[comp][b + shift], comp);
+    return R;
+}
+
+MatPair pair_pow(u128 e, int shift)
+{
+    MatPair P;
+    const Mat a = mpow(e, shift, 0), b = mpow(e, shift, 1);
+    memcpy(P.a, a.v, sizeof P.a);
+    memcpy(P.b, b.v, sizeof P.b);
+    return P;
+}
+
+MatPair pair_mul(const MatPair& X, const MatPair& Y)
+{
+    Mat xa, xb, ya, yb;
+    memcpy(xa.v, X.a, 36);
+    memcpy(xb.v, X.b, 36);
+    memcpy(ya.v, Y.a, 36);
+    memcpy(yb.v, Y.b, 36);
+    const Mat a = mul(xa, ya, 0), b = mul(xb, yb, 1);
+    MatPair R;
+    memcpy(R.a, a.v, 36);
+    memcpy(R.b, b.v, 36);
+    return R;
+}
+
+void pair_apply(const MatPair& P, uint32_t s[6])
+{
+    for (int c = 0; c < 2; ++c) {
+        const uint32_t* M = c ? P.b : P.a;
+        uint32_t* v = s + 3 * c;
+        uint32_t r[3];
+        for (int k = 0; k < 3; ++k) {
+            uint64_t acc = 0;
+            for (int q = 0; q < 3; ++q) acc += fold((uint64_t)M[3 * k + q] * v[q], c);
+            r[k] = fold(acc, c);
+        }
+        memcpy(v, r, sizeof r);
+    }
+}
+
+// ---------------------------------------------------------------- registry
+
+struct Handle {
+    int gen = 0, spacing = 0, device = 0;
+    uint32_t seed[6] = {};
+    uint64_t first = 0, n = 0;
+    u128 offset = 0;
+    uint32_t* state = nullptr;
+    bool own_state = false;
+    uint32_t bps = 0, tpb = 256;
+    uint64_t seg = 0;
+    int sms = 0;
+};
+
+std::mutex g_mu;
+std::unordered_map<uint64_t, std::shared_ptr<Handle>> g_handles;
+std::atomic<uint64_t> g_next_id{1};
+bool g_tables_on[64] = {};
+
+std::shared_ptr<Handle> lookup(shv_streams h)
+{
+    std::lock_guard<std::mutex> lk(g_mu);
+    auto it = g_handles.find(h);
+    return it == g_handles.end() ? nullptr : it->second;
+}
+
+// Saves/restores the caller's current device around a call.
+struct DeviceGuard {
+    int prev = -1;
+    cudaError_t err = cudaSuccess;
+    explicit DeviceGuard(int dev)
+    {
+        err = cudaGetDevice(&prev);
+        if (err == cudaSuccess && prev != dev) err = cudaSetDevice(dev);
+    }
+    ~DeviceGuard()
+    {
+        int cur = -1;
+        if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+shv_status cuda_fail(cudaError_t e, const char* what)
+{
+    return fail(SHV_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+shv_status ensure_tables(int dev)
+{
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (dev < 0 || dev >= 64) return fail(SHV_ERR_INVALID_ARGUMENT, "device %d out of range", dev);
+    if (g_tables_on[dev]) return SHV_OK;
+    MatPair sub[51], str[64];
+    for (int b = 0; b < 51; ++b) sub[b] = pair_pow(1, 76 + b);
+    for (int b = 0; b < 64; ++b) str[b] = pair_pow(1, 127 + b);
+    cudaError_t e = upload_jump_tables(sub, str);
+    if (e != cudaSuccess) return cuda_fail(e, "upload_jump_tables");
+    g_tables_on[dev] = true;
+    return SHV_OK;
+}
+
+// ---------------------------------------------------------------- H2: work split
+
+unsigned blocks_for(const Handle& h, int kernel, int kind, bool fast, uint64_t items)
+{
+    int bps = (int)h.bps;
+    if (bps == 0) {
+        if (max_blocks_per_sm(kernel, kind, fast, (int)h.tpb, &bps) != cudaSuccess || bps < 1) bps = 1;
+    }
+    const uint64_t full = (uint64_t)h.sms * (uint64_t)bps;
+    const uint64_t need = (items + h.tpb - 1) / h.tpb;
+    uint64_t b = need < full ? need : full;
+    return (unsigned)(b ? b : 1);
+}
+
+uint64_t resident_threads(const Handle& h, int kernel, int kind, bool fast)
+{
+    int bps = (int)h.bps;
+    if (bps == 0) {
+        if (max_blocks_per_sm(kernel, kind, fast, (int)h.tpb, &bps) != cudaSuccess || bps < 1) bps = 1;
+    }
+    return (uint64_t)h.sms * (uint64_t)bps * h.tpb;
+}
+
+// Split rows of `len` units into nseg segments of seg_len units (multiple of
+// `align`), aiming at `waves` x resident threads work items.
+void split(const Handle& h, uint64_t ns, uint64_t len, uint64_t align, uint64_t waves,
+           uint64_t resident, uint64_t cap, uint64_t* seg_len, uint32_t* nseg)
+{
+    uint64_t L;
+    if (h.seg) {
+        L = h.seg;
+    } else {
+        const uint64_t target = waves * resident;
+        uint64_t S = (target + ns - 1) / ns;
+        if (S < 1) S = 1;
+        if (S > (uint64_t)kMaxSeg) S = kMaxSeg;
+        L = (len + S - 1) / S;
+    }
+    L = (L + align - 1) / align * align;
+    if (L > cap) L = cap / align * align;
+    if (L == 0) L = align;
+    uint64_t S = (len + L - 1) / L;
+    while (S > (uint64_t)kMaxSeg) {  // user segment too short: grow it
+        L *= 2;
+        S = (len + L - 1) / L;
+    }
+    *seg_len = L;
+    *nseg = (uint32_t)(S ? S : 1);
+}
+
+shv_status check_advance(const Handle& h, u128 draws)
+{
+    if (h.gen == SHV_GEN_PHILOX4X32_10) {
+        if (draws > ((u128)1 << 66) || h.offset > ((u128)1 << 66) - draws)
+            return fail(SHV_ERR_INVALID_ARGUMENT, "Philox stream exhausted (2^66 draws per stream)");
+    } else if (h.offset + draws < h.offset) {
+        return fail(SHV_ERR_INVALID_ARGUMENT, "MRG32k3a offset would exceed 2^128");
+    }
+    return SHV_OK;
+}
+
+void fill_mrg_segments(const Handle& h, uint64_t units_per_seg, uint64_t draws_per_unit,
+                       uint32_t nseg, MatPair* seg)
+{
+    seg[0] = pair_pow(h.offset, 0);
+    const MatPair step = pair_pow((u128)units_per_seg * draws_per_unit, 0);
+    for (uint32_t j = 1; j < nseg; ++j) seg[j] = pair_mul(step, seg[j - 1]);
+}
+
+template <typename T>
+shv_status generate(shv_streams hid, T* out, uint64_t n, void* stream, int kind, bool host_out)
+{
+    auto hp = lookup(hid);
+    if (!hp) return fail(SHV_ERR_LIFECYCLE, "unknown or destroyed handle %llu", (unsigned long long)hid);
+    Handle& h = *hp;
+    if (!out && n) return fail(SHV_ERR_INVALID_ARGUMENT, "NULL output pointer");
+    if ((uintptr_t)out % sizeof(T)) return fail(SHV_ERR_MISALIGNED, "output not %zu-byte aligned", sizeof(T));
+    if (n == 0) return SHV_OK;
+    if (h.n > UINT64_MAX / n / sizeof(T)) return fail(SHV_ERR_INVALID_ARGUMENT, "size overflow");
+    const uint64_t dpv = (h.gen == SHV_GEN_PHILOX4X32_10 && kind == kF64) ? 2 : 1;
+    shv_status st = check_advance(h, (u128)n * dpv);
+    if (st) return st;
+    DeviceGuard dg(h.device);
+    if (dg.err != cudaSuccess) return cuda_fail(dg.err, "cudaSetDevice");
+    cudaStream_t s = (cudaStream_t)stream;
+
+    // Host output: generate stream slices into device staging buffers and
+    // copy them back on a second stream, two slices in flight.
+    uint64_t slice = h.n;
+    T* stage[2] = {nullptr, nullptr};
+    cudaStream_t cs = nullptr;
+    cudaEvent_t gen_done[2] = {}, copy_done[2] = {};
+    const uint64_t row_bytes = n * sizeof(T);
+    if (host_out) {
+        const uint64_t target = 256ull << 20;
+        slice = target / row_bytes;
+        if (slice < 1) slice = 1;
+        if (slice > h.n) slice = h.n;
+        cudaError_t e = cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking);
+        for (int b = 0; b < 2 && e == cudaSuccess; ++b) {
+            e = cudaMallocAsync((void**)&stage[b], slice * row_bytes, s);
+            if (e == cudaSuccess) e = cudaEventCreateWithFlags(&gen_done[b], cudaEventDisableTiming);
+            if (e == cudaSuccess) e = cudaEventCreateWithFlags(&copy_done[b], cudaEventDisableTiming);
+        }
+        if (e != cudaSuccess) return cuda_fail(e, "staging setup");
+    }
+
+    cudaError_t err = cudaSuccess;
+    const bool aligned32 = !host_out ? ((uintptr_t)out % 32 == 0) : true;
+    for (uint64_t s0 = 0, k = 0; s0 < h.n && err == cudaSuccess; s0 += slice, ++k) {
+        const uint64_t ns = (h.n - s0) < slice ? (h.n - s0) : slice;
+        T* dst = host_out ? stage[k & 1] : out;
+        if (host_out && k >= 2) err = cudaStreamWaitEvent(s, copy_done[k & 1], 0);
+        if (err != cudaSuccess) break;
+        if (h.gen == SHV_GEN_MRG32K3A) {
+            const bool vec = aligned32 && (n % 8 == 0);
+            auto P = std::make_unique<MrgLaunch>();
+            P->state = h.state;
+            P->stride = h.n;
+            P->stream_begin = s0;
+            P->ns = ns;
+            P->out = dst;
+            P->n = n;
+            split(h, ns, n, vec ? 8 : 1, 8, resident_threads(h, kKMrgFill, kind, vec), 1ull << 40,
+                  &P->seg_len, &P->nseg);
+            P->items = ns * P->nseg;
+            fill_mrg_segments(h, P->seg_len, 1, P->nseg, P->seg);
+            Grid g{blocks_for(h, kKMrgFill, kind, vec, P->items), h.tpb};
+            err = launch_mrg_fill(*P, kind, vec, g, s);
+        } else {
+            const uint64_t E = kind == kF64 ? 4 : 8;
+            const bool fast = aligned32 && (n % E == 0) && ((uint32_t)h.offset & 3) == 0;
+            PhiloxLaunch P{};
+            P.k0 = h.seed[0];
+            P.k1 = h.seed[1];
+            P.g0 = h.first + s0;
+            P.ns = ns;
+            P.o_blk = (uint64_t)(h.offset >> 2);
+            P.o_lane = (uint32_t)(h.offset & 3);
+            P.out = dst;
+            P.n = n;
+            P.items = fast ? ns * n / E : (ns * n + 7) / 8;
+            Grid g{blocks_for(h, kKPhiloxFill, kind, fast, P.items), h.tpb};
+            err = launch_philox_fill(P, kind, fast, g, s);
+        }
+        if (err != cudaSuccess) break;
+        if (host_out) {
+            err = cudaEventRecord(gen_done[k & 1], s);
+            if (err == cudaSuccess) err = cudaStreamWaitEvent(cs, gen_done[k & 1], 0);
+            if (err == cudaSuccess)
+                err = cudaMemcpyAsync(reinterpret_cast<char*>(out) + s0 * row_bytes, dst, ns * row_bytes,
+                                      cudaMemcpyDeviceToHost, cs);
+            if (err == cudaSuccess) err = cudaEventRecord(copy_done[k & 1], cs);
+        }
+    }
+    if (host_out) {
+        // Completion is ordered on the caller's stream.
+        for (int b = 0; b < 2; ++b) {
+            if (err == cudaSuccess && h.n > (uint64_t)b * slice) err = cudaStreamWaitEvent(s, copy_done[b], 0);
+            if (stage[b]) cudaFreeAsync(stage[b], s);
+        }
+        for (int b = 0; b < 2; ++b) {
+            if (gen_done[b]) cudaEventDestroy(gen_done[b]);
+            if (copy_done[b]) cudaEventDestroy(copy_done[b]);
+        }
+        if (cs) cudaStreamDestroy(cs);
+    }
+    if (err != cudaSuccess) return cuda_fail(err, "generate launch");
+    h.offset += (u128)n * dpv;
+    return SHV_OK;
+}
+
+shv_status validate_seed(int gen, const uint32_t* seed, size_t words, uint32_t out[6])
+{
+    memset(out, 0, 24);
+    if (!seed) return fail(SHV_ERR_INVALID_ARGUMENT, "NULL seed");
+    if (gen == SHV_GEN_MRG32K3A) {
+        if (words == 1) {
+            for (int k = 0; k < 6; ++k) out[k] = seed[0];
+        } else if (words == 6) {
+            memcpy(out, seed, 24);
+        } else {
+            return fail(SHV_ERR_INVALID_ARGUMENT, "MRG32k3a takes 1 or 6 seed words, got %zu", words);
+        }
+        for (int k = 0; k < 3; ++k)
+            if (out[k] >= kM1 || out[3 + k] >= kM2)
+                return fail(SHV_ERR_INVALID_SEED, "seed residue out of range (s1 < m1, s2 < m2)");
+        if (!(out[0] | out[1] | out[2]) || !(out[3] | out[4] | out[5]))
+            return fail(SHV_ERR_INVALID_SEED, "an all-zero MRG32k3a component never leaves zero");
+        return SHV_OK;
+    }
+    if (gen == SHV_GEN_PHILOX4X32_10) {
+        if (words != 1 && words != 2)
+            return fail(SHV_ERR_INVALID_ARGUMENT, "Philox4x32-10 takes 1 or 2 key words, got %zu", words);
+        out[0] = seed[0];
+        out[1] = words == 2 ? seed[1] : 0;
+        return SHV_OK;
+    }
+    return fail(SHV_ERR_INVALID_ARGUMENT, "unknown generator %d", gen);
+}
+
+}  // namespace
+}  // namespace shv
+
+using namespace shv;
+
+extern "C" {
+
+size_t shv_state_bytes(int gen, uint64_t n_streams)
+{
+    if (gen != SHV_GEN_MRG32K3A) return 0;
+    if (n_streams > SIZE_MAX / 24) return 0;
+    return (size_t)(24 * n_streams);
+}
+
+shv_status shv_streams_create_ex(shv_streams* out, int gen, const uint32_t* seed, size_t seed_words,
+                                 uint64_t first_stream, uint64_t n_streams, int spacing, void* d_state,
+                                 size_t state_bytes, int device, void* cuda_stream)
+{
+    if (!out) return fail(SHV_ERR_INVALID_ARGUMENT, "NULL out handle");
+    *out = 0;
+    uint32_t s6[6];
+    shv_status st = validate_seed(gen, seed, seed_words, s6);
+    if (st) return st;
+    if (n_streams == 0) return fail(SHV_ERR_INVALID_ARGUMENT, "n_streams must be >= 1");
+    if (spacing != SHV_SPACING_STREAM && spacing != SHV_SPACING_SUBSTREAM)
+        return fail(SHV_ERR_INVALID_ARGUMENT, "unknown spacing %d", spacing);
+    if (gen == SHV_GEN_PHILOX4X32_10 && spacing != SHV_SPACING_STREAM)
+        return fail(SHV_ERR_UNSUPPORTED, "Philox4x32-10 has no substreams");
+    const u128 end = (u128)first_stream + n_streams;
+    if (gen == SHV_GEN_MRG32K3A && spacing == SHV_SPACING_SUBSTREAM && end > ((u128)1 << 51))
+        return fail(SHV_ERR_INSUFFICIENT_STREAMS, "substreams end at 2^51 per stream");
+    if (end > ((u128)1 << 64)) return fail(SHV_ERR_INSUFFICIENT_STREAMS, "streams end at 2^64");
+    const size_t need = shv_state_bytes(gen, n_streams);
+    if (gen == SHV_GEN_MRG32K3A) {
+        if (need == 0) return fail(SHV_ERR_INVALID_ARGUMENT, "state size overflow");
+        if (d_state && state_bytes < need)
+            return fail(SHV_ERR_INVALID_ARGUMENT, "state buffer %zu B < %zu B", state_bytes, need);
+        if (d_state && ((uintptr_t)d_state & 3)) return fail(SHV_ERR_MISALIGNED, "state not 4-byte aligned");
+    }
+    int dev = device;
+    if (dev < 0) {
+        cudaError_t e = cudaGetDevice(&dev);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+    }
+    DeviceGuard dg(dev);
+    if (dg.err != cudaSuccess) return cuda_fail(dg.err, "cudaSetDevice");
+
+    auto h = std::make_shared<Handle>();
+    h->gen = gen;
+    h->spacing = spacing;
+    h->device = dev;
+    memcpy(h->seed, s6, sizeof s6);
+    h->first = first_stream;
+    h->n = n_streams;
+    cudaError_t e = cudaDeviceGetAttribute(&h->sms, cudaDevAttrMultiProcessorCount, dev);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaDeviceGetAttribute");
+
+    if (gen == SHV_GEN_MRG32K3A) {
+        st = ensure_tables(dev);
+        if (st) return st;
+        if (d_state) {
+            h->state = (uint32_t*)d_state;
+        } else {
+            e = cudaMalloc((void**)&h->state, need);
+            if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(state)");
+            h->own_state = true;
+        }
+        // Rank/handle base: seed jumped to stream (or substream) first_stream.
+        uint32_t base[6];
+        memcpy(base, s6, sizeof base);
+        const MatPair B = pair_pow(first_stream, spacing == SHV_SPACING_STREAM ? 127 : 76);
+        pair_apply(B, base);
+        const int table = spacing == SHV_SPACING_STREAM ? 1 : 0;
+        Grid g{(unsigned)((n_streams + 255) / 256), 256};
+        e = launch_mrg_seed(h->state, n_streams, base, table, g, (cudaStream_t)cuda_stream);
+        if (e != cudaSuccess) {
+            if (h->own_state) cudaFree(h->state);
+            return cuda_fail(e, "seed launch");
+        }
+    }
+    const uint64_t id = g_next_id.fetch_add(1);
+    {
+        std::lock_guard<std::mutex> lk(g_mu);
+        g_handles[id] = h;
+    }
+    *out = id;
+    return SHV_OK;
+}
+
+shv_status shv_streams_create(shv_streams* out, int gen, const uint32_t* seed, size_t seed_words,
+                              uint64_t n_streams)
+{
+    return shv_streams_create_ex(out, gen, seed, seed_words, 0, n_streams, SHV_SPACING_STREAM, nullptr, 0,
+                                 -1, nullptr);
+}
+
+shv_status shv_jump(shv_streams hid, int kind, uint64_t n)
+{
+    auto hp = lookup(hid);
+    if (!hp) return fail(SHV_ERR_LIFECYCLE, "unknown or destroyed handle");
+    Handle& h = *hp;
+    u128 d;
+    if (kind == SHV_JUMP_DRAWS) {
+        d = n;
+    } else if (kind == SHV_JUMP_SUBSTREAMS || kind == SHV_JUMP_STREAMS) {
+        if (h.gen != SHV_GEN_MRG32K3A) return fail(SHV_ERR_UNSUPPORTED, "Philox jumps by draws only");
+        const int sh = kind == SHV_JUMP_SUBSTREAMS ? 76 : 127;
+        if (n >> (128 - sh)) return fail(SHV_ERR_INVALID_ARGUMENT, "jump exceeds 2^128 draws");
+        d = (u128)n << sh;
+    } else {
+        return fail(SHV_ERR_INVALID_ARGUMENT, "unknown jump kind %d", kind);
+    }
+    shv_status st = check_advance(h, d);
+    if (st) return st;
+    h.offset += d;
+    return SHV_OK;
+}
+
+shv_status shv_generate_u32(shv_streams h, uint32_t* d_out, uint64_t n, void* s)
+{
+    return generate<uint32_t>(h, d_out, n, s, kU32, false);
+}
+shv_status shv_generate_f32(shv_streams h, float* d_out, uint64_t n, void* s)
+{
+    return generate<float>(h, d_out, n, s, kF32, false);
+}
+shv_status shv_generate_f64(shv_streams h, double* d_out, uint64_t n, void* s)
+{
+    return generate<double>(h, d_out, n, s, kF64, false);
+}
+shv_status shv_generate_u32_host(shv_streams h, uint32_t* h_out, uint64_t n, void* s)
+{
+    return generate<uint32_t>(h, h_out, n, s, kU32, true);
+}
+
+shv_status shv_mc_pi_ex(shv_streams hid, uint64_t samples, uint64_t* d_hits, uint64_t* d_counts,
+                        void* stream)
+{
+    auto hp = lookup(hid);
+    if (!hp) return fail(SHV_ERR_LIFECYCLE, "unknown or destroyed handle");
+    Handle& h = *hp;
+    if (samples == 0) return fail(SHV_ERR_EMPTY_EXPERIMENT, "zero samples per stream");
+    if (!d_hits) return fail(SHV_ERR_INVALID_ARGUMENT, "NULL d_hits");
+    if (((uintptr_t)d_hits & 7) || ((uintptr_t)d_counts & 7)) return fail(SHV_ERR_MISALIGNED, "counters not 8-byte aligned");
+    if (samples > (UINT64_MAX >> 2)) return fail(SHV_ERR_INVALID_ARGUMENT, "samples too large");
+    shv_status st = check_advance(h, (u128)samples * 2);
+    if (st) return st;
+    DeviceGuard dg(h.device);
+    if (dg.err != cudaSuccess) return cuda_fail(dg.err, "cudaSetDevice");
+    cudaStream_t s = (cudaStream_t)stream;
+    cudaError_t err;
+    const uint64_t cap = 1ull << 31;  // per-item count fits in u32
+    if (h.gen == SHV_GEN_MRG32K3A) {
+        auto P = std::make_unique<MrgLaunch>();
+        P->state = h.state;
+        P->stride = h.n;
+        P->stream_begin = 0;
+        P->ns = h.n;
+        P->out = nullptr;
+        P->n = samples;
+        P->hits = (unsigned long long*)d_hits;
+        P->counts = (unsigned long long*)d_counts;
+        split(h, h.n, samples, 2, 32, resident_threads(h, kKMrgMc, 0, true), cap, &P->seg_len, &P->nseg);
+        P->items = h.n * P->nseg;
+        fill_mrg_segments(h, P->seg_len, 2, P->nseg, P->seg);
+        Grid g{blocks_for(h, kKMrgMc, 0, true, P->items), h.tpb};
+        err = launch_mrg_mc(*P, g, s);
+    } else {
+        const bool fast = ((uint32_t)h.offset & 3) == 0;
+        PhiloxLaunch P{};
+        P.k0 = h.seed[0];
+        P.k1 = h.seed[1];
+        P.g0 = h.first;
+        P.ns = h.n;
+        P.o_blk = (uint64_t)(h.offset >> 2);
+        P.o_lane = (uint32_t)(h.offset & 3);
+        P.n = samples;
+        P.hits = (unsigned long long*)d_hits;
+        P.counts = (unsigned long long*)d_counts;
+        split(h, h.n, samples, 2, 32, resident_threads(h, kKPhiloxMc, 0, fast), cap, &P.seg_len, &P.nseg);
+        P.items = h.n * P.nseg;
+        Grid g{blocks_for(h, kKPhiloxMc, 0, fast, P.items), h.tpb};
+        err = launch_philox_mc(P, fast, g, s);
+    }
+    if (err != cudaSuccess) return cuda_fail(err, "mc_pi launch");
+    h.offset += (u128)samples * 2;
+    return SHV_OK;
+}
+
+shv_status shv_mc_pi(shv_streams h, uint64_t samples, uint64_t* d_hits, void* s)
+{
+    return shv_mc_pi_ex(h, samples, d_hits, nullptr, s);
+}
+
+shv_status shv_get_position(shv_streams hid, shv_position* out)
+{
+    auto hp = lookup(hid);
+    if (!hp) return fail(SHV_ERR_LIFECYCLE, "unknown or destroyed handle");
+    if (!out) return fail(SHV_ERR_INVALID_ARGUMENT, "NULL out");
+    const Handle& h = *hp;
+    out->gen = (uint32_t)h.gen;
+    out->spacing = (uint32_t)h.spacing;
+    memcpy(out->seed, h.seed, sizeof out->seed);
+    out->first_stream = h.first;
+    out->n_streams = h.n;
+    out->offset_lo = (uint64_t)h.offset;
+    out->offset_hi = (uint64_t)(h.offset >> 64);
+    return SHV_OK;
+}
+
+shv_status shv_streams_destroy(shv_streams hid)
+{
+    std::shared_ptr<Handle> h;
+    {
+        std::lock_guard<std::mutex> lk(g_mu);
+        auto it = g_handles.find(hid);
+        if (it == g_handles.end()) return fail(SHV_ERR_LIFECYCLE, "unknown or already destroyed handle");
+        h = it->second;
+        g_handles.erase(it);
+    }
+    if (h->own_state && h->state) {
+        DeviceGuard dg(h->device);
+        cudaFree(h->state);
+    }
+    return SHV_OK;
+}
+
+shv_status shv_set_launch_config(shv_streams hid, uint32_t bps, uint32_t tpb, uint64_t seg)
+{
+    auto hp = lookup(hid);
+    if (!hp) return fail(SHV_ERR_LIFECYCLE, "unknown or destroyed handle");
+    if (tpb == 0) tpb = 256;
+    if (tpb % 32 || tpb > 256) return fail(SHV_ERR_INVALID_ARGUMENT, "threads_per_block must be 32..256, multiple of 32");
+    if (seg % 8) return fail(SHV_ERR_INVALID_ARGUMENT, "segment must be a multiple of 8");
+    if (bps > 64) return fail(SHV_ERR_INVALID_ARGUMENT, "blocks_per_sm too large");
+    hp->bps = bps;
+    hp->tpb = tpb;
+    hp->seg = seg;
+    return SHV_OK;
+}
+
+const char* shv_status_string(shv_status s)
+{
+    switch (s) {
+    case SHV_OK: return "SHV_OK";
+    case SHV_ERR_INVALID_ARGUMENT: return "SHV_ERR_INVALID_ARGUMENT";
+    case SHV_ERR_INVALID_SEED: return "SHV_ERR_INVALID_SEED";
+    case SHV_ERR_INSUFFICIENT_STREAMS: return "SHV_ERR_INSUFFICIENT_STREAMS";
+    case SHV_ERR_UNSUPPORTED: return "SHV_ERR_UNSUPPORTED";
+    case SHV_ERR_LIFECYCLE: return "SHV_ERR_LIFECYCLE";
+    case SHV_ERR_MISALIGNED: return "SHV_ERR_MISALIGNED";
+    case SHV_ERR_EMPTY_EXPERIMENT: return "SHV_ERR_EMPTY_EXPERIMENT";
+    case SHV_ERR_MISSING_PARAMETERS: return "SHV_ERR_MISSING_PARAMETERS";
+    case SHV_ERR_CUDA: return "SHV_ERR_CUDA";
+    }
+    return "SHV_ERR_UNKNOWN";
+}
+
+const char* shv_last_error_message(void) { return t_err.c_str(); }
+
+shv_status shv_partition(uint64_t total, int rank, int world, uint64_t* first, uint64_t* count)
+{
+    if (!first || !count) return fail(SHV_ERR_INVALID_ARGUMENT, "NULL out");
+    if (world < 1 || rank < 0 || rank >= world) return fail(SHV_ERR_INVALID_ARGUMENT, "bad rank/world");
+    const uint64_t lo = (uint64_t)(((u128)total * (uint64_t)rank) / (uint64_t)world);
+    const uint64_t hi = (uint64_t)(((u128)total * (uint64_t)(rank + 1)) / (uint64_t)world);
+    *first = lo;
+    *count = hi - lo;
+    return SHV_OK;
+}
+
+shv_status shv_jump_matrix(uint64_t e_lo, uint64_t e_hi, uint32_t out[18])
+{
+    if (!out) return fail(SHV_ERR_INVALID_ARGUMENT, "NULL out");
+    const MatPair P = pair_pow(((u128)e_hi << 64) | e_lo, 0);
+    memcpy(out, P.a, 36);
+    memcpy(out + 9, P.b, 36);
+    return SHV_OK;
+}
+
+const char* shv_build_info(void) { return "shv 0.1 sm_100a"; }
+
+}  // extern "C"

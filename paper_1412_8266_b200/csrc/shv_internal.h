@@ -1,0 +1,85 @@
+// shv_internal.h — launch records shared by the ABI layer (shv_api.cpp) and the
+// sm_100a kernels (shv_kernels.cu). Not installed; the public ABI is include/shv.h.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace shv {
+
+// Most segments one launch splits a stream into (intra-stream Sequence
+// Splitting, P L109-112 [§2.3]); each needs its own jump matrix in the
+// kernel parameter block (72 B each).
+constexpr int kMaxSeg = 64;
+
+// Output kinds.
+enum Kind : int { kU32 = 0, kF32 = 1, kF64 = 2 };
+
+// A 3x3 jump matrix pair, row-major: a = A1^e mod m1, b = A2^e mod m2.
+struct MatPair {
+    uint32_t a[9];
+    uint32_t b[9];
+};
+
+// MRG32k3a bulk fill / Monte Carlo launch. Work item it in [0, items):
+// segment j = it / ns, stream i = it % ns (streams fastest so a warp shares
+// one segment matrix). Segment j covers values [j*seg_len, min(n,(j+1)*seg_len))
+// of the row and starts from seg[j] * state_i.
+struct MrgLaunch {
+    const uint32_t* state;   // SoA: word k of stream s at state[k*stride + s]
+    uint64_t stride;         // handle n_streams
+    uint64_t stream_begin;   // first handle stream of this launch (host slices)
+    uint64_t ns;             // streams in this launch
+    void* out;               // fill: row i at out + i*n (elements); MC: unused
+    uint64_t n;              // fill: values per row; MC: samples per stream
+    uint64_t seg_len;        // values (fill) or samples (MC) per segment
+    uint64_t items;          // ns * nseg
+    unsigned long long* hits;    // MC only
+    unsigned long long* counts;  // MC only, optional (indexed by launch stream)
+    uint32_t nseg;
+    MatPair seg[kMaxSeg];
+};
+
+// Philox4x32-10 bulk fill / Monte Carlo launch. Draw d of handle stream i
+// (d counted from the handle offset o = 4*o_blk + o_lane) is lane
+// (o_lane + d) & 3 of counter block o_blk + ((o_lane + d) >> 2) with
+// ctr = (blk_lo, blk_hi, g_lo, g_hi), g = g0 + i, key = (k0, k1) (R6).
+struct PhiloxLaunch {
+    uint32_t k0, k1;
+    uint64_t g0;             // family stream of launch stream 0
+    uint64_t ns;             // streams in this launch
+    uint64_t o_blk;          // offset / 4
+    uint32_t o_lane;         // offset % 4
+    void* out;
+    uint64_t n;              // fill: values per row; MC: samples per stream
+    uint64_t seg_len;        // MC: samples per work item
+    uint64_t items;          // fill: chunks; MC: ns * nseg
+    uint32_t nseg;
+    unsigned long long* hits;
+    unsigned long long* counts;
+};
+
+struct Grid {
+    unsigned blocks;
+    unsigned threads;
+};
+
+// ---- launchers (shv_kernels.cu) ----
+cudaError_t upload_jump_tables(const MatPair* sub51, const MatPair* str64);
+cudaError_t launch_mrg_seed(uint32_t* state, uint64_t n, const uint32_t base[6], int table,
+                            Grid g, cudaStream_t s);
+cudaError_t launch_mrg_fill(const MrgLaunch& p, int kind, bool vec, Grid g, cudaStream_t s);
+cudaError_t launch_mrg_mc(const MrgLaunch& p, Grid g, cudaStream_t s);
+cudaError_t launch_philox_fill(const PhiloxLaunch& p, int kind, bool fast, Grid g, cudaStream_t s);
+cudaError_t launch_philox_mc(const PhiloxLaunch& p, bool fast, Grid g, cudaStream_t s);
+
+// Which kernel an occupancy query refers to.
+enum KernelId : int {
+    kKSeed = 0,
+    kKMrgFill = 1,
+    kKMrgMc = 2,
+    kKPhiloxFill = 3,
+    kKPhiloxMc = 4,
+};
+cudaError_t max_blocks_per_sm(int kernel, int kind, bool fast, int threads, int* out);
+
+}  // namespace shv

@@ -1,0 +1,384 @@
+"""GPU parity: the sm_100a path (through the C ABI) against the CPU oracle.
+
+Bar (R1-R12): every u32 value, and every f32/f64 value as a bit
+pattern, equal to the oracle's on the same seeded workload — integer work is
+bit-exact, and the conversions are exact or one correctly-rounded multiply.
+Small configs are compared in full (several segments, ragged tails); the full
+BASELINE.json sizes are compared on sampled streams (workloads.sample_streams)
+and on whole-output checksums written by tests/golden/make_golden.py (oracle
+only), in the launch configuration bench.py uses.
+"""
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+
+import workloads as W
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+M1 = 4294967087
+
+
+@pytest.fixture(scope="module")
+def shv():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_1412_8266_b200 as shv
+    return shv
+
+
+DT = {"u32": (torch.int32, np.uint32), "f32": (torch.float32, np.float32),
+      "f64": (torch.float64, np.float64)}
+
+
+class Fam:
+    """A handle plus the arguments the oracle needs to replay it."""
+
+    def __init__(self, shv, gen, seed, n_streams, spacing=0, first=0):
+        self.shv, self.gen, self.seed = shv, gen, list(seed) if not isinstance(seed, int) else [seed]
+        self.n_streams, self.spacing, self.first = n_streams, spacing, first
+        self.state = None
+        if gen == W.MRG32K3A:
+            self.state = torch.empty(6 * n_streams, dtype=torch.int32, device="cuda")
+        self.h = shv.shv_streams_create_ex(gen, self.seed, first, n_streams, spacing, self.state,
+                                           0, torch.cuda.current_device(), None)
+        self.offset = 0
+
+    def gen_(self, n, kind="u32", out=None):
+        tdt, ndt = DT[kind]
+        if out is None:
+            out = torch.empty(self.n_streams * n, dtype=tdt, device="cuda")
+        getattr(self.shv, "shv_generate_" + kind)(self.h, out, n, None)
+        torch.cuda.synchronize()
+        self.offset += n * (2 if (kind == "f64" and self.gen == W.PHILOX4X32_10) else 1)
+        return out.cpu().numpy().view(ndt).reshape(self.n_streams, n) if n else out
+
+    def ref(self, orc, n, kind="u32", offset=None, streams=None):
+        return orc.generate(self.gen, self.seed, self.n_streams, n, first=self.first,
+                            spacing=self.spacing, offset=self.offset if offset is None else offset,
+                            kind={"u32": 0, "f32": 1, "f64": 2}[kind], streams=streams)
+
+    def close(self):
+        self.shv.shv_streams_destroy(self.h)
+
+
+def same(a, b):
+    assert a.shape == b.shape
+    if a.dtype.kind == "f":
+        a = a.view(np.uint32 if a.itemsize == 4 else np.uint64)
+        b = b.view(a.dtype)
+    bad = np.nonzero(a != b)
+    assert len(bad[0]) == 0, f"{len(bad[0])} mismatches, first at {[x[:5] for x in bad]}"
+
+
+# ---------------------------------------------------------------- C1
+
+@pytest.mark.parametrize("kind", ["u32", "f32", "f64"])
+def test_c1_mrg_4x1000_full(shv, orc, kind):
+    f = Fam(shv, W.MRG32K3A, W.C1.seed, W.C1.n_streams, W.C1.spacing)
+    ref = f.ref(orc, W.C1.n, kind)
+    got = f.gen_(W.C1.n, kind)
+    same(got, ref)
+    if kind == "u32":  # SURVEY App. A.2 first/last values
+        assert got[:, 0].tolist() == [545508589, 3262379099, 3128925555, 411039607]
+        assert got[:, 999].tolist() == [4235174647, 1962922018, 1313695736, 2457220498]
+    f.close()
+
+
+# ---------------------------------------------------------------- C2 + KATs
+
+def test_c2_philox_full(shv, orc):
+    w = W.C2
+    f = Fam(shv, w.gen, w.seed, w.n_streams)
+    got = f.gen_(w.n)
+    same(got, f.ref(orc, w.n, offset=0))
+    f.close()
+
+
+def test_philox_kats_through_abi(shv):
+    rows = [ln.split() for ln in open(os.path.join(GOLD, "philox4x32_kat.txt"))
+            if ln.strip() and not ln.startswith("#")]
+    for fam, *words in rows:
+        if fam != "philox4x32_10":
+            continue
+        v = [int(x, 16) for x in words]
+        ctr, key, exp = v[0:4], v[4:6], v[6:10]
+        g = ctr[2] | (ctr[3] << 32)
+        blk = ctr[0] | (ctr[1] << 32)
+        h = shv.shv_streams_create_ex(W.PHILOX4X32_10, key, g, 1, 0, None, 0, -1, None)
+        for _ in range(4):  # offset 4*blk may exceed 2^64: jump in four parts
+            shv.shv_jump(h, shv.SHV_JUMP_DRAWS, blk)
+        out = torch.empty(4, dtype=torch.int32, device="cuda")
+        shv.shv_generate_u32(h, out, 4, None)
+        assert out.cpu().numpy().view(np.uint32).tolist() == exp, fam
+        shv.shv_streams_destroy(h)
+
+
+# ---------------------------------------------------------------- C3 (reduced, full compare)
+
+@pytest.mark.parametrize("kind", ["u32", "f64", "f32"])
+def test_c3_shape_reduced_full_compare(shv, orc, kind):
+    f = Fam(shv, W.MRG32K3A, W.C3.seed, 1 << 12, W.SPACING_SUBSTREAM)
+    ref = f.ref(orc, 4096, kind)
+    same(f.gen_(4096, kind), ref)
+    f.close()
+
+
+# ---------------------------------------------------------------- edge cases
+
+@pytest.mark.parametrize("gen,sp", [(W.MRG32K3A, 0), (W.MRG32K3A, 1), (W.PHILOX4X32_10, 0)])
+@pytest.mark.parametrize("kind", ["u32", "f32", "f64"])
+def test_ragged_offsets_and_replay(shv, orc, gen, sp, kind):
+    """Rows that are not 32-byte multiples, offsets not multiples of 4 or 8,
+    consecutive calls (offset advance), first_stream != 0, a single stream."""
+    for ns, first in ((37, 5), (1, 0), (300, 1 << 40)):
+        f = Fam(shv, gen, [12345] if gen == W.MRG32K3A else [12345, 777], ns, sp, first)
+        for n in (1, 3, 8, 13, 64, 1000, 0, 7):
+            before = f.offset
+            got = f.gen_(n, kind)
+            if n:
+                same(got, f.ref(orc, n, kind, offset=before))
+        f.close()
+
+
+@pytest.mark.parametrize("gen,sp", [(W.MRG32K3A, 1), (W.PHILOX4X32_10, 0)])
+def test_generate_twice_equals_generate_2n(shv, gen, sp):
+    a = Fam(shv, gen, [99], 1000, sp)
+    b = Fam(shv, gen, [99], 1000, sp)
+    x1, x2 = a.gen_(512), a.gen_(512)
+    y = b.gen_(1024)
+    assert np.array_equal(np.concatenate([x1, x2], axis=1), y)
+    # jump(k) then generate == generate and discard k
+    c = Fam(shv, gen, [99], 1000, sp)
+    shv.shv_jump(c.h, shv.SHV_JUMP_DRAWS, 300)
+    assert np.array_equal(c.gen_(724), y[:, 300:])
+    for f in (a, b, c):
+        f.close()
+
+
+def test_mrg_substream_and_stream_jumps(shv, orc):
+    f = Fam(shv, W.MRG32K3A, [12345], 8, W.SPACING_SUBSTREAM)
+    shv.shv_jump(f.h, shv.SHV_JUMP_SUBSTREAMS, 3)  # stream i -> substream i+3
+    g = Fam(shv, W.MRG32K3A, [12345], 8, W.SPACING_SUBSTREAM, first=3)
+    assert np.array_equal(f.gen_(64), g.gen_(64))
+    shv.shv_jump(f.h, shv.SHV_JUMP_STREAMS, 1)
+    pos = shv.shv_get_position(f.h)
+    assert pos["offset"] == (1 << 127) + 3 * (1 << 76) + 64
+    ref = orc.generate(W.MRG32K3A, [12345], 8, 16, spacing=1, offset=pos["offset"])
+    same(f.gen_(16), ref)
+    f.close()
+    g.close()
+
+
+def test_misaligned_output_and_errors(shv, orc):
+    f = Fam(shv, W.PHILOX4X32_10, [5], 16)
+    buf = torch.zeros(16 * 64 + 8, dtype=torch.int32, device="cuda")
+    shv.shv_generate_u32(f.h, buf.data_ptr() + 4, 64, None)  # 4-byte aligned only
+    torch.cuda.synchronize()
+    got = buf.cpu().numpy().view(np.uint32)[1:1 + 16 * 64].reshape(16, 64)
+    same(got, f.ref(orc, 64))
+    f.offset += 64
+    with pytest.raises(shv.ShvError) as ei:
+        shv.shv_generate_u32(f.h, buf.data_ptr() + 2, 64, None)
+    assert ei.value.status == shv.SHV_ERR_MISALIGNED
+    with pytest.raises(shv.ShvError) as ei:
+        shv.shv_generate_u32(f.h, 0, 64, None)
+    assert ei.value.status == shv.SHV_ERR_INVALID_ARGUMENT
+    shv.shv_generate_u32(f.h, 0, 0, None)  # n = 0: no-op
+    assert shv.shv_get_position(f.h)["offset"] == 64
+    hits = torch.zeros(1, dtype=torch.int64, device="cuda")
+    with pytest.raises(shv.ShvError) as ei:
+        shv.shv_mc_pi(f.h, 0, hits, None)
+    assert ei.value.status == shv.SHV_ERR_EMPTY_EXPERIMENT
+    with pytest.raises(shv.ShvError) as ei:
+        shv.shv_jump(f.h, shv.SHV_JUMP_SUBSTREAMS, 1)
+    assert ei.value.status == shv.SHV_ERR_UNSUPPORTED
+    f.close()
+    with pytest.raises(shv.ShvError) as ei:
+        f.close()
+    assert ei.value.status == shv.SHV_ERR_LIFECYCLE
+
+
+def test_short_form_create(shv, orc):
+    h = shv.shv_streams_create(W.MRG32K3A, 12345, 4)
+    out = torch.empty(4 * 1000, dtype=torch.int32, device="cuda")
+    shv.shv_generate_u32(h, out, 1000, 0)
+    torch.cuda.synchronize()
+    same(out.cpu().numpy().view(np.uint32).reshape(4, 1000), orc.generate(W.MRG32K3A, [12345], 4, 1000))
+    shv.shv_streams_destroy(h)
+
+
+@pytest.mark.parametrize("gen,sp", [(W.MRG32K3A, 1), (W.PHILOX4X32_10, 0)])
+def test_launch_config_invariance(shv, gen, sp):
+    """R10: grid shape and segment length never change the values."""
+    ref = None
+    for bps, tpb, seg in ((0, 0, 0), (1, 32, 8), (3, 128, 64), (2, 256, 1024), (0, 64, 4096)):
+        f = Fam(shv, gen, [31337], 777, sp)
+        shv.shv_set_launch_config(f.h, bps, tpb, seg)
+        x = np.concatenate([f.gen_(1000), f.gen_(24, "f64").view(np.uint32)], axis=1)
+        hits = torch.zeros(1, dtype=torch.int64, device="cuda")
+        cnt = torch.zeros(777, dtype=torch.int64, device="cuda")
+        shv.shv_mc_pi_ex(f.h, 333, hits, cnt, None)
+        torch.cuda.synchronize()
+        res = (x, int(hits.item()), cnt.cpu().numpy())
+        if ref is None:
+            ref = res
+        else:
+            assert np.array_equal(res[0], ref[0]) and res[1] == ref[1]
+            assert np.array_equal(res[2], ref[2])
+        f.close()
+
+
+def test_host_output_matches_device(shv, orc):
+    # 40000 x 4000 u32 = 640 MB: three 256 MB staging slices, two in flight.
+    for gen, sp, ns, n in ((W.MRG32K3A, 1, 40000, 4000), (W.PHILOX4X32_10, 0, 3000, 2000)):
+        a = Fam(shv, gen, [4242], ns, sp)
+        b = Fam(shv, gen, [4242], ns, sp)
+        host = torch.empty(ns * n, dtype=torch.int32, pin_memory=True)
+        shv.shv_generate_u32_host(a.h, host, n, None)
+        torch.cuda.synchronize()
+        dev = b.gen_(n)
+        assert np.array_equal(host.numpy().view(np.uint32).reshape(ns, n), dev)
+        assert shv.shv_get_position(a.h)["offset"] == n
+        a.close()
+        b.close()
+
+
+# ---------------------------------------------------------------- Monte Carlo
+
+@pytest.mark.parametrize("gen,sp", [(W.MRG32K3A, 1), (W.PHILOX4X32_10, 0)])
+def test_mc_counts_small_full(shv, orc, gen, sp):
+    f = Fam(shv, gen, [12345], 300, sp, first=17)
+    for samples, pre in ((1000, 0), (777, 1), (5, 3), (4096, 2)):
+        if pre:
+            shv.shv_jump(f.h, shv.SHV_JUMP_DRAWS, pre)
+            f.offset += pre
+        hits = torch.zeros(1, dtype=torch.int64, device="cuda")
+        cnt = torch.zeros(300, dtype=torch.int64, device="cuda")
+        shv.shv_mc_pi_ex(f.h, samples, hits, cnt, None)
+        torch.cuda.synchronize()
+        tot, ref = orc.mc_count(gen, [12345], 300, samples, first=17, spacing=sp, offset=f.offset)
+        f.offset += 2 * samples
+        assert np.array_equal(cnt.cpu().numpy().astype(np.uint64), ref)
+        assert int(hits.item()) == tot
+    f.close()
+
+
+# ---------------------------------------------------------------- full BASELINE sizes
+
+def _golden_full():
+    p = os.path.join(GOLD, "oracle_full.json")
+    if not os.path.exists(p):
+        pytest.skip("tests/golden/oracle_full.json not generated")
+    return json.load(open(p))
+
+
+def _checksums_gpu(t_u32: torch.Tensor, n: int, t_f64=None):
+    """Test-side reductions of a GPU output (the same aggregates make_golden.py
+    computes with the oracle): sum, weighted XOR over J = i*n + j, ties."""
+    v = t_u32.view(-1)
+    N = v.numel()
+    sum_z, wx, ties, sum_f = 0, 0, 0, 0
+    CH = 1 << 27
+    for s in range(0, N, CH):
+        x = v[s:s + CH].to(torch.int64) & 0xFFFFFFFF
+        J = torch.arange(s, s + x.numel(), device=x.device, dtype=torch.int64)
+        sum_z += int(x.sum().item()) & ((1 << 64) - 1)
+        ties += int((x == M1).sum().item())
+        p = x * (2 * J + 1)  # wraps mod 2^64 in two's complement
+        while p.numel() > 1:
+            if p.numel() & 1:
+                p = torch.cat([p, torch.zeros(1, dtype=p.dtype, device=p.device)])
+            p = torch.bitwise_xor(p[0::2], p[1::2])
+        wx ^= int(p.item()) & ((1 << 64) - 1)
+        if t_f64 is not None:
+            sum_f += int(t_f64.view(-1)[s:s + CH].view(torch.int64).sum().item())
+        del x, J, p
+    return sum_z % (1 << 64), "%016x" % wx, ties, "%016x" % (sum_f % (1 << 64))
+
+
+def test_c2_checksums(shv):
+    g = _golden_full()
+    if "C2_u32" not in g:
+        pytest.skip("C2 checksums not generated")
+    w = W.C2
+    f = Fam(shv, w.gen, w.seed, w.n_streams)
+    out = torch.empty(w.n_streams * w.n, dtype=torch.int32, device="cuda")
+    shv.shv_generate_u32(f.h, out, w.n, None)
+    sz, wx, _, _ = _checksums_gpu(out, w.n)
+    assert (sz, wx) == (g["C2_u32"]["sum_z"], g["C2_u32"]["wxor"])
+    f.close()
+
+
+def test_c3_full_size_sampled_and_checksums(shv, orc):
+    """2^20 substreams x 4096 (u32 and f64): sampled rows vs oracle, plus
+    whole-output checksums vs tests/golden/oracle_full.json."""
+    w = W.C3
+    streams = W.sample_streams(w.n_streams, 512)
+    a = Fam(shv, w.gen, w.seed, w.n_streams, w.spacing)
+    out = torch.empty(w.n_streams * w.n, dtype=torch.int32, device="cuda")
+    shv.shv_generate_u32(a.h, out, w.n, None)
+    torch.cuda.synchronize()
+    idx = torch.tensor(streams, device="cuda")
+    rows = out.view(w.n_streams, w.n)[idx].cpu().numpy().view(np.uint32)
+    same(rows, orc.generate(w.gen, list(w.seed), 0, w.n, spacing=w.spacing, streams=streams))
+    b = Fam(shv, w.gen, w.seed, w.n_streams, w.spacing)
+    out64 = torch.empty(w.n_streams * w.n, dtype=torch.float64, device="cuda")
+    shv.shv_generate_f64(b.h, out64, w.n, None)
+    torch.cuda.synchronize()
+    rows64 = out64.view(w.n_streams, w.n)[idx].cpu().numpy()
+    same(rows64, orc.generate(w.gen, list(w.seed), 0, w.n, spacing=w.spacing, streams=streams,
+                              kind=2))
+    g = _golden_full().get("C3")
+    if g:
+        sz, wx, ties, sf = _checksums_gpu(out, w.n, out64)
+        assert (sz, wx, ties, sf) == (g["sum_z"], g["wxor"], g["ties"], g["sum_f64_bits"])
+    a.close()
+    b.close()
+
+
+@pytest.mark.parametrize("w", [W.C4_MRG, W.C4_PHILOX], ids=["mrg", "philox"])
+def test_c4_mc_pi_full_size(shv, orc, w):
+    """2^38 samples over 2^20 streams: sampled per-stream counts vs oracle,
+    total vs oracle total (golden), pi within the 4-sigma binomial bound."""
+    f = Fam(shv, w.gen, w.seed, w.n_streams, w.spacing)
+    hits = torch.zeros(1, dtype=torch.int64, device="cuda")
+    cnt = torch.zeros(w.n_streams, dtype=torch.int64, device="cuda")
+    shv.shv_mc_pi_ex(f.h, w.n, hits, cnt, None)
+    torch.cuda.synchronize()
+    total = int(hits.item())
+    counts = cnt.cpu().numpy().astype(np.uint64)
+    assert int(counts.sum()) == total
+    streams = W.sample_streams(w.n_streams, 256)
+    _, ref = orc.mc_count(w.gen, list(w.seed), 0, w.n, spacing=w.spacing, streams=streams)
+    assert np.array_equal(counts[streams], ref)
+    N = w.n_streams * w.n
+    p = 221069946527026 / 2 ** 48
+    assert abs(4 * total / N - math.pi) <= 4 * 4 * math.sqrt(p * (1 - p) / N)
+    key = "C4_mrg_total" if w.gen == W.MRG32K3A else "C4_philox_total"
+    g = _golden_full()
+    if key in g:
+        assert total == g[key]
+    f.close()
+
+
+@pytest.mark.parametrize("w", [W.C5_MRG, W.C5_PHILOX], ids=["mrg", "philox"])
+def test_c5_rank_slices_match(shv, orc, w):
+    """Weak-scaling shards (rank r fills streams [r*2^20, (r+1)*2^20)): sampled
+    rows of rank 3 of 8 at full size vs the oracle, in bench.py's launch
+    configuration."""
+    ws = W.rank_slice(w, 3, 8, weak=True)
+    f = Fam(shv, ws.gen, ws.seed, ws.n_streams, ws.spacing, ws.first)
+    out = torch.empty(ws.n_streams * ws.n, dtype=torch.int32, device="cuda")
+    shv.shv_generate_u32(f.h, out, ws.n, None)
+    torch.cuda.synchronize()
+    streams = W.sample_streams(ws.n_streams, 256)
+    rows = out.view(ws.n_streams, ws.n)[torch.tensor(streams, device="cuda")].cpu().numpy()
+    same(rows.view(np.uint32), orc.generate(ws.gen, list(ws.seed), 0, ws.n, first=ws.first,
+                                            spacing=ws.spacing, streams=streams))
+    f.close()
