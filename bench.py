@@ -98,51 +98,60 @@ class Clocks:
 
 # ---------------------------------------------------------------------------- oracle arm
 
-def oracle_sample(target_s: float, threads: int):
-    """Time the oracle (as it stands) on a bounded prefix of the C5 workload:
-    the first k streams x 4096 u32 of each generator, k calibrated so the run
-    takes about target_s seconds. Returns (numbers, seconds, description)."""
+def _oracle_run(k: int, threads: int) -> float:
+    """Oracle (as it stands) on the first k streams x 4096 u32 of each C5
+    generator; returns seconds."""
     import oracle
     n = W.C5_MRG.n
-
-    def run(k):
-        t = time.perf_counter()
-        oracle.generate(W.MRG32K3A, list(W.C5_MRG.seed), k, n, spacing=W.C5_MRG.spacing,
+    t = time.perf_counter()
+    for s0 in range(0, k, 1 << 14):  # 256 MiB chunks: bounded host memory
+        ns = min(1 << 14, k - s0)
+        oracle.generate(W.MRG32K3A, list(W.C5_MRG.seed), ns, n, first=s0, spacing=W.C5_MRG.spacing,
                         nthreads=threads)
-        oracle.generate(W.PHILOX4X32_10, list(W.C5_PHILOX.seed), k, n,
+        oracle.generate(W.PHILOX4X32_10, list(W.C5_PHILOX.seed), ns, n, first=s0,
                         spacing=W.C5_PHILOX.spacing, nthreads=threads)
-        return time.perf_counter() - t
+    return time.perf_counter() - t
 
-    k0 = max(threads, 16)
-    t0 = run(k0)
-    k = max(k0, min(W.C5_MRG.n_streams, int(k0 * target_s / max(t0, 1e-3))))
-    t = run(k)
-    return 2 * k * n, t, (f"first {k} of 2^20 streams x {n} u32 from each of MRG32k3a and "
-                          f"Philox4x32-10 (C5 prefix), {threads} threads")
+
+def _oracle_calibrate(target_s: float, threads: int) -> int:
+    """Stream-prefix length k whose oracle run takes about target_s seconds."""
+    k = max(threads, 16)
+    while True:
+        t = _oracle_run(k, threads)
+        if t >= 1.0 or k >= W.C5_MRG.n_streams:
+            break
+        k = min(W.C5_MRG.n_streams, k * 4)
+    return max(1, min(W.C5_MRG.n_streams, int(k * target_s / max(t, 1e-3))))
+
+
+def _sample_desc(k: int, threads: int) -> str:
+    return (f"first {k} of 2^20 streams x {W.C5_MRG.n} u32 from each of MRG32k3a and "
+            f"Philox4x32-10 (C5 prefix), {threads} threads")
 
 
 def cpu_baseline(threads):
-    nums, t, desc = oracle_sample(12.0, threads)
-    return {"value": nums / t / 1e9, "unit": UNIT, "cores": threads, "kind": "oracle",
-            "sample": desc, "seconds": round(t, 3)}
+    k = _oracle_calibrate(12.0, threads)
+    t = _oracle_run(k, threads)
+    return {"value": 2 * k * W.C5_MRG.n / t / 1e9, "unit": UNIT, "cores": threads, "kind": "oracle",
+            "sample": _sample_desc(k, threads), "seconds": round(t, 3)}
 
 
 def run_reference(args, rank, world):
+    """--impl reference: the oracle, as it stands, on the host cores; rank 0 only."""
     if rank != 0:
         return
     threads = len(os.sched_getaffinity(0))
     import oracle
     oracle.build()
-    per_step_target = max(2.0, min(20.0, 150.0 / max(1, args.steps + args.warmup)))
-    _, _, _ = oracle_sample(0.5, threads)  # warm the library
+    per_step = max(1.0, min(20.0, 150.0 / max(1, args.steps + args.warmup)))
+    k = _oracle_calibrate(per_step, threads)
     for _ in range(args.warmup):
-        oracle_sample(per_step_target, threads)
-    tot_n, tot_t, desc = 0, 0.0, ""
+        _oracle_run(k, threads)
+    tot_t = 0.0
     for _ in range(args.steps):
-        nums, t, desc = oracle_sample(per_step_target, threads)
-        tot_n += nums
-        tot_t += t
-    value = tot_n / tot_t / 1e9
+        tot_t += _oracle_run(k, threads)
+    value = 2 * k * W.C5_MRG.n * args.steps / tot_t / 1e9
+    desc = _sample_desc(k, threads)
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1e3 * tot_t / max(1, args.steps), "higher_is_better": True,
@@ -159,7 +168,7 @@ def run_reference(args, rank, world):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="shv", choices=["shv", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
@@ -227,6 +236,8 @@ def main():
 
     for _ in range(args.warmup):
         step()
+    clocks = Clocks([local] if world == 1 else list(range(world))) if rank == 0 else None
+    time.sleep(0.3)  # let the sampler start before the measured loops
     # per-kernel durations (same launches as the step, events on the launching stream)
     for _ in range(args.steps):
         step(timed_kernels=True)
@@ -234,7 +245,6 @@ def main():
         for k in kt:
             kt[k].append(ev[k][0].elapsed_time(ev[k][1]))
 
-    clocks = Clocks([local] if world == 1 else list(range(world))) if rank == 0 else None
     barrier()
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     t0.record(stream)

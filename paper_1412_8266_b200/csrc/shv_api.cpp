@@ -316,7 +316,7 @@ shv_status generate(shv_streams hid, T* out, uint64_t n, void* stream, int kind,
         if (host_out && k >= 2) err = cudaStreamWaitEvent(s, copy_done[k & 1], 0);
         if (err != cudaSuccess) break;
         if (h.gen == SHV_GEN_MRG32K3A) {
-            const bool vec = aligned32 && (n % 8 == 0);
+            bool vec = aligned32 && (n % 8 == 0);
             auto P = std::make_unique<MrgLaunch>();
             P->state = h.state;
             P->stride = h.n;
@@ -324,8 +324,10 @@ shv_status generate(shv_streams hid, T* out, uint64_t n, void* stream, int kind,
             P->ns = ns;
             P->out = dst;
             P->n = n;
-            split(h, ns, n, vec ? 8 : 1, 8, resident_threads(h, kKMrgFill, kind, vec), 1ull << 40,
+            // vector path: segments in whole 256-byte staging rounds (64 values)
+            split(h, ns, n, vec ? 64 : 1, 8, resident_threads(h, kKMrgFill, kind, vec), 1ull << 40,
                   &P->seg_len, &P->nseg);
+            if (vec && P->seg_len % 8) vec = false;
             P->items = ns * P->nseg;
             fill_mrg_segments(h, P->seg_len, 1, P->nseg, P->seg);
             Grid g{blocks_for(h, kKMrgFill, kind, vec, P->items), h.tpb};
@@ -342,8 +344,24 @@ shv_status generate(shv_streams hid, T* out, uint64_t n, void* stream, int kind,
             P.o_lane = (uint32_t)(h.offset & 3);
             P.out = dst;
             P.n = n;
-            P.items = fast ? ns * n / E : (ns * n + 7) / 8;
-            Grid g{blocks_for(h, kKPhiloxFill, kind, fast, P.items), h.tpb};
+            Grid g{};
+            if (fast) {
+                // warp tasks of (row, 32*R chunks); R shrinks until there are
+                // >= 4 tasks per resident warp.
+                const uint64_t cpr = n / E;
+                const uint64_t rwarps = resident_threads(h, kKPhiloxFill, kind, true) / 32;
+                uint64_t R = (cpr + 31) / 32;
+                if (R > 16) R = 16;
+                if (h.seg) R = h.seg / 8 < 1 ? 1 : (h.seg / 8 > 64 ? 64 : h.seg / 8);
+                auto tasks = [&](uint64_t r) { return ns * ((cpr + 32 * r - 1) / (32 * r)); };
+                while (!h.seg && R > 1 && tasks(R) < 4 * rwarps) R /= 2;
+                P.nseg = (uint32_t)R;
+                P.items = tasks(R);
+                g = Grid{blocks_for(h, kKPhiloxFill, kind, true, P.items * 32), h.tpb};
+            } else {
+                P.items = (ns * n + 7) / 8;
+                g = Grid{blocks_for(h, kKPhiloxFill, kind, false, P.items), h.tpb};
+            }
             err = launch_philox_fill(P, kind, fast, g, s);
         }
         if (err != cudaSuccess) break;

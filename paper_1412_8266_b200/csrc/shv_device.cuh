@@ -1,0 +1,432 @@
+// shv_device.cuh — device-side generator primitives of the ShoveRand hot path
+// (arXiv 1412.8266) for sm_100a. Included by shv_kernels.cu (and by the
+// kernel lab under tools/lab/, which times variants of the same functions).
+//
+// Pipe budget on B200 (measured, profiles/r01_microbench.json): IMAD.WIDE.U32
+// occupies the FMA-heavy pipe for 4 cycles per warp (IMAD/IADD3/LOP3: 2), and
+// the FP64 pipe (DFMA/DADD/DMUL: 2 cycles per warp) is otherwise idle. The
+// MRG32k3a step below therefore splits its two components across pipes:
+// component 1 in 32-bit integer arithmetic (FMA-heavy + ALU), component 2 in
+// exact binary64 arithmetic (FP64 pipe), as in L'Ecuyer's original
+// floating-point formulation [LEcuyer1999] (products < 2^53, exact).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace shv {
+namespace dev {
+
+// [LEcuyer1999] MRG32k3a parameters (PAPER.md L255 cites them; not restated there).
+constexpr uint32_t kM1 = 4294967087u;  // 2^32 - 209
+constexpr uint32_t kM2 = 4294944443u;  // 2^32 - 22853
+constexpr uint32_t kC1 = 209u;
+constexpr uint32_t kC2 = 22853u;
+constexpr uint32_t kA12 = 1403580u;
+constexpr uint32_t kA13n = 810728u;
+constexpr uint32_t kA21 = 527612u;
+constexpr uint32_t kA23n = 1370589u;
+// [Salmon.etal.2011] Philox4x32 multipliers and Weyl key increments.
+constexpr uint32_t kPM0 = 0xD2511F53u;
+constexpr uint32_t kPM1 = 0xCD9E8D57u;
+constexpr uint32_t kPW0 = 0x9E3779B9u;
+constexpr uint32_t kPW1 = 0xBB67AE85u;
+
+// ------------------------------------------------------------------ integer helpers
+
+// 64-bit + 32-bit on the ALU pipe (add.cc/addc -> IADD3 with carry), keeping
+// index arithmetic off the FMA-heavy pipe that the generators saturate.
+__device__ __forceinline__ uint64_t add64(uint64_t a, uint32_t b)
+{
+    uint32_t lo, hi;
+    asm("add.cc.u32 %0, %2, %3;\n\taddc.u32 %1, %4, 0;"
+        : "=r"(lo), "=r"(hi)
+        : "r"((uint32_t)a), "r"(b), "r"((uint32_t)(a >> 32)));
+    return ((uint64_t)hi << 32) | lo;
+}
+
+// x mod (2^32 - c) for any 64-bit x (c < 2^15): two folds + one subtraction.
+template <uint32_t C>
+__device__ __forceinline__ uint32_t red64(uint64_t x)
+{
+    x = (x >> 32) * C + (uint32_t)x;  // < 2^47.1
+    x = (x >> 32) * C + (uint32_t)x;  // < 2^32 + 2^30
+    const uint64_t m = (1ull << 32) - C;
+    return (uint32_t)(x >= m ? x - m : x);
+}
+
+// r = M v (mod 2^32 - C), M row-major 3x3 with entries < m, v canonical.
+template <uint32_t C>
+__device__ __forceinline__ void matvec(const uint32_t* M, uint32_t& v0, uint32_t& v1, uint32_t& v2)
+{
+    uint32_t r[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        const uint64_t s = (uint64_t)red64<C>((uint64_t)M[3 * k] * v0) +
+                           red64<C>((uint64_t)M[3 * k + 1] * v1) +
+                           red64<C>((uint64_t)M[3 * k + 2] * v2);
+        r[k] = red64<C>(s);
+    }
+    v0 = r[0];
+    v1 = r[1];
+    v2 = r[2];
+}
+
+// ------------------------------------------------------------------ MRG32k3a
+
+// Integer state (used for jumps, seeding and the reference step).
+struct Mrg {
+    uint32_t x0, x1, x2;  // component 1, oldest -> newest (R1)
+    uint32_t y0, y1, y2;  // component 2
+};
+
+__device__ __forceinline__ void apply(const uint32_t* a, const uint32_t* b, Mrg& s)
+{
+    matvec<kC1>(a, s.x0, s.x1, s.x2);
+    matvec<kC2>(b, s.y0, s.y1, s.y2);
+}
+
+// Component 1, integer: P = a12*x1 + a13n*(m1-x0) < 2^53.06, split at bit
+// 32 as (H, L). U = (H+1)*209 + L < 2^33 is congruent to P + 209 and U >= 209,
+// so P mod m1 = U - 2^32 if U >= 2^32, else U - 209. The +1 on H comes for
+// free by adding 2^32 to P; U's carry bit is read off a single IMAD.WIDE
+// v = H'*209 + (H':L) = U + H'*2^32 as v.hi != H'. (DESIGN.md §4.2.)
+__device__ __forceinline__ uint32_t mrg_c1(uint32_t x0, uint32_t x1)
+{
+    uint32_t r;
+    asm("{\n\t"
+        ".reg .u64 q, v;\n\t"
+        ".reg .u32 t, l, h, vh;\n\t"
+        ".reg .pred c;\n\t"
+        "mad.wide.u32 q, %2, 1403580, 4294967296;\n\t"  // a12*x1 + 2^32
+        "sub.u32 t, 4294967087, %1;\n\t"                // m1 - x0
+        "mad.wide.u32 q, t, 810728, q;\n\t"             // P + 2^32 = (H+1, L)
+        "mov.b64 {l, h}, q;\n\t"
+        "mad.wide.u32 v, h, 209, q;\n\t"                // U + (H+1)*2^32
+        "mov.b64 {%0, vh}, v;\n\t"
+        "setp.ne.u32 c, vh, h;\n\t"                     // U >= 2^32
+        "@!c sub.u32 %0, %0, 209;\n\t"
+        "}"
+        : "=r"(r)
+        : "r"(x0), "r"(x1));
+    return r;
+}
+
+// Component 2, integer (reference / seeding path): Q = a21*y2 + a23n*(m2-y0)
+// < 2^52.9 folded twice with 2^32 = 22853 (mod m2).
+__device__ __forceinline__ uint32_t mrg_c2_int(uint32_t y0, uint32_t y2)
+{
+    const uint64_t q = (uint64_t)kA21 * y2 + (uint64_t)kA23n * (kM2 - y0);
+    const uint64_t t = (uint64_t)(uint32_t)(q >> 32) * kC2 + (uint32_t)q;
+    const uint32_t tlo = (uint32_t)t;
+    const uint32_t r2 = tlo + (uint32_t)(t >> 32) * kC2;
+    return r2 + ((r2 < tlo) | (r2 >= kM2) ? kC2 : 0u);
+}
+
+// Combination (R2): (p1 - p2) mod m1 with 0 -> m1, exact in wrap-around.
+__device__ __forceinline__ uint32_t mrg_combine(uint32_t p1, uint32_t p2)
+{
+    uint32_t z;
+    asm("{\n\t.reg .pred le;\n\t"
+        "sub.u32 %0, %1, %2;\n\t"
+        "setp.le.u32 le, %1, %2;\n\t"
+        "@le add.u32 %0, %0, 4294967087;\n\t}"
+        : "=r"(z)
+        : "r"(p1), "r"(p2));
+    return z;
+}
+
+__device__ __forceinline__ uint32_t mrg_next(Mrg& s)
+{
+    const uint32_t p1 = mrg_c1(s.x0, s.x1);
+    s.x0 = s.x1;
+    s.x1 = s.x2;
+    s.x2 = p1;
+    const uint32_t p2 = mrg_c2_int(s.y0, s.y2);
+    s.y0 = s.y1;
+    s.y1 = s.y2;
+    s.y2 = p2;
+    return mrg_combine(p1, p2);
+}
+
+// Hybrid state: component 2 held as exact binary64 integers.
+struct MrgH {
+    uint32_t x0, x1, x2;
+    double y0, y1, y2;
+};
+
+__device__ __forceinline__ MrgH to_hybrid(const Mrg& s)
+{
+    return MrgH{s.x0, s.x1, s.x2, __uint2double_rn(s.y0), __uint2double_rn(s.y1), __uint2double_rn(s.y2)};
+}
+
+// One component on the FP64 pipe. The state holds *signed* residues
+// y in (-m/2 - 2, m/2 + 2) (or canonical ones, < 2^32, right after a jump):
+// p = a*yb - b*yc is exact (|p| < 2^52.4). k' = fma(p, RN(1/m), 1.5*2^52)
+// rounds p/m to the nearest integer k = k' - 1.5*2^52 with
+// |p/m - k| <= 1/2 + 2^-31, so r = fma(-k, m, p) is exact, congruent to the
+// next value, and |r| <= m/2 + 2. The canonical output in [0, m) is the low
+// word of r + 1.5*2^52 (= r mod 2^32: the sum lies in [2^52, 2^53), where the
+// ulp is 1), plus m when r < 0 (sign bit of that word). 6 FP64 operations.
+template <uint32_t M, uint32_t A, uint32_t B>
+__device__ __forceinline__ uint32_t mrg_fp64(double yb, double yc, double& r_out)
+{
+    const double kMagic = 6755399441055744.0;  // 1.5 * 2^52
+    const double t = __dmul_rn((double)B, yc);
+    const double p = __fma_rn((double)A, yb, -t);
+    const double k = __dadd_rn(__fma_rn(p, 1.0 / (double)M, kMagic), -kMagic);
+    const double r = __fma_rn(-k, (double)M, p);
+    r_out = r;
+    uint32_t w = (uint32_t)__double2loint(__dadd_rn(r, kMagic));  // r mod 2^32
+    asm("{\n\t.reg .pred n;\n\tsetp.lt.s32 n, %0, 0;\n\t@n add.u32 %0, %0, %1;\n\t}" : "+r"(w) : "n"(M));
+    return w;
+}
+
+// Same result with a shorter dependency chain on the recurrence input yb:
+// q = fma(RN(a/m), yb, RN(-b*yc/m)) approximates p/m to within 2^-31, so
+// k = rint(q) (one FRND) keeps |p/m - k| <= 1/2 + 2^-31; the chain from yb to
+// r is fma -> rint -> fma instead of fma -> fma -> add -> fma.
+template <uint32_t M, uint32_t A, uint32_t B>
+__device__ __forceinline__ uint32_t mrg_fp64_short(double yb, double yc, double& r_out)
+{
+    const double kMagic = 6755399441055744.0;  // 1.5 * 2^52
+    const double t = __dmul_rn((double)B, yc);
+    const double c0 = __dmul_rn(t, -1.0 / (double)M);
+    const double p = __fma_rn((double)A, yb, -t);
+    const double q = __fma_rn((double)A / (double)M, yb, c0);
+    double k;
+    asm("cvt.rni.f64.f64 %0, %1;" : "=d"(k) : "d"(q));
+    const double r = __fma_rn(-k, (double)M, p);
+    r_out = r;
+    uint32_t w = (uint32_t)__double2loint(__dadd_rn(r, kMagic));  // r mod 2^32
+    asm("{\n\t.reg .pred n;\n\tsetp.lt.s32 n, %0, 0;\n\t@n add.u32 %0, %0, %1;\n\t}" : "+r"(w) : "n"(M));
+    return w;
+}
+
+// Component 2: y_n = a21 y_{n-1} - a23n y_{n-3} (mod m2).
+__device__ __forceinline__ uint32_t mrg_c2_fp64(double y0, double y2, double& r_out)
+{
+    return mrg_fp64<kM2, kA21, kA23n>(y2, y0, r_out);
+}
+
+__device__ __forceinline__ uint32_t mrg_next(MrgH& s)
+{
+    const uint32_t p1 = mrg_c1(s.x0, s.x1);
+    s.x0 = s.x1;
+    s.x1 = s.x2;
+    s.x2 = p1;
+    double r;
+    const uint32_t p2 = mrg_c2_fp64(s.y0, s.y2, r);
+    s.y0 = s.y1;
+    s.y1 = s.y2;
+    s.y2 = r;
+    return mrg_combine(p1, p2);
+}
+
+// Both components on the FP64 pipe (lab variant).
+struct MrgD {
+    double x0, x1, x2;
+    double y0, y1, y2;
+};
+
+__device__ __forceinline__ MrgD to_fp64(const Mrg& s)
+{
+    return MrgD{__uint2double_rn(s.x0), __uint2double_rn(s.x1), __uint2double_rn(s.x2),
+                __uint2double_rn(s.y0), __uint2double_rn(s.y1), __uint2double_rn(s.y2)};
+}
+
+__device__ __forceinline__ uint32_t mrg_next(MrgD& s)
+{
+    double r1, r2;
+    const uint32_t p1 = mrg_fp64<kM1, kA12, kA13n>(s.x1, s.x0, r1);  // x1,n = a12 x1,n-2 - a13n x1,n-3
+    s.x0 = s.x1;
+    s.x1 = s.x2;
+    s.x2 = r1;
+    const uint32_t p2 = mrg_c2_fp64(s.y0, s.y2, r2);
+    s.y0 = s.y1;
+    s.y1 = s.y2;
+    s.y2 = r2;
+    return mrg_combine(p1, p2);
+}
+
+// Both components on the FP64 pipe, short-chain form (lab variant).
+struct MrgS {
+    double x0, x1, x2;
+    double y0, y1, y2;
+    int pad;
+};
+
+__device__ __forceinline__ MrgS to_fp64s(const Mrg& s)
+{
+    return MrgS{__uint2double_rn(s.x0), __uint2double_rn(s.x1), __uint2double_rn(s.x2),
+                __uint2double_rn(s.y0), __uint2double_rn(s.y1), __uint2double_rn(s.y2), 0};
+}
+
+__device__ __forceinline__ uint32_t mrg_next(MrgS& s)
+{
+    double r1, r2;
+    const uint32_t p1 = mrg_fp64_short<kM1, kA12, kA13n>(s.x1, s.x0, r1);
+    s.x0 = s.x1;
+    s.x1 = s.x2;
+    s.x2 = r1;
+    const uint32_t p2 = mrg_fp64_short<kM2, kA21, kA23n>(s.y2, s.y0, r2);
+    s.y0 = s.y1;
+    s.y1 = s.y2;
+    s.y2 = r2;
+    return mrg_combine(p1, p2);
+}
+
+// ------------------------------------------------------------------ Philox4x32-10
+
+struct W4 {
+    uint32_t x, y, z, w;
+};
+
+__device__ __forceinline__ W4 philox10(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3,
+                                       uint32_t k0, uint32_t k1)
+{
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+        const uint64_t p0 = (uint64_t)kPM0 * c0;
+        const uint64_t p1 = (uint64_t)kPM1 * c2;
+        const uint32_t n0 = (uint32_t)(p1 >> 32) ^ c1 ^ k0;
+        const uint32_t n2 = (uint32_t)(p0 >> 32) ^ c3 ^ k1;
+        c1 = (uint32_t)p1;
+        c3 = (uint32_t)p0;
+        c0 = n0;
+        c2 = n2;
+        k0 += kPW0;
+        k1 += kPW1;
+    }
+    return W4{c0, c1, c2, c3};
+}
+
+// Rounds 2..10 of a block whose round-1 products are given (lets callers
+// hoist the multiplications that only depend on the stream index).
+__device__ __forceinline__ W4 philox10_from_r1(uint32_t hi0, uint32_t lo0, uint32_t hi1, uint32_t lo1,
+                                               uint32_t c1, uint32_t c3, uint32_t k0, uint32_t k1)
+{
+    uint32_t c0 = hi1 ^ c1 ^ k0, c2 = hi0 ^ c3 ^ k1;
+    c1 = lo1;
+    c3 = lo0;
+    k0 += kPW0;
+    k1 += kPW1;
+#pragma unroll
+    for (int r = 1; r < 10; ++r) {
+        const uint64_t p0 = (uint64_t)kPM0 * c0;
+        const uint64_t p1 = (uint64_t)kPM1 * c2;
+        const uint32_t n0 = (uint32_t)(p1 >> 32) ^ c1 ^ k0;
+        const uint32_t n2 = (uint32_t)(p0 >> 32) ^ c3 ^ k1;
+        c1 = (uint32_t)p1;
+        c3 = (uint32_t)p0;
+        c0 = n0;
+        c2 = n2;
+        k0 += kPW0;
+        k1 += kPW1;
+    }
+    return W4{c0, c1, c2, c3};
+}
+
+__device__ __forceinline__ W4 philox_blk(uint64_t blk, uint64_t g, uint32_t k0, uint32_t k1)
+{
+    return philox10((uint32_t)blk, (uint32_t)(blk >> 32), (uint32_t)g, (uint32_t)(g >> 32), k0, k1);
+}
+
+__device__ __forceinline__ uint32_t lane_of(const W4& v, uint32_t l)
+{
+    return l == 0 ? v.x : l == 1 ? v.y : l == 2 ? v.z : v.w;
+}
+
+// Generic per-draw access with a one-block cache (arbitrary offsets).
+struct PhiloxCursor {
+    uint64_t g;
+    uint32_t k0, k1;
+    uint64_t blk;
+    bool valid;
+    W4 v;
+    __device__ __forceinline__ uint32_t word(uint64_t b, uint32_t lane)
+    {
+        if (!valid || b != blk) {
+            v = philox_blk(b, g, k0, k1);
+            blk = b;
+            valid = true;
+        }
+        return lane_of(v, lane);
+    }
+};
+
+// ------------------------------------------------------------------ conversions (R7)
+
+__device__ __forceinline__ float to_f32(uint32_t w)
+{
+    return __fmul_rn(__uint2float_rn(w >> 8), 0x1p-24f);
+}
+
+__device__ __forceinline__ double mrg_f64(uint32_t z)
+{
+    return __dmul_rn(__uint2double_rn(z), 0x1.000000d00000bp-32);
+}
+
+__device__ __forceinline__ double philox_f64(uint32_t lo, uint32_t hi)
+{
+    const uint64_t b = (((uint64_t)hi << 32) | lo) >> 11;
+    return __dmul_rn(__ull2double_rn(b), 0x1p-53);
+}
+
+// ------------------------------------------------------------------ stores
+
+// One full 32-byte sector per thread: STG.E.ENL2.256 on sm_100a.
+__device__ __forceinline__ void st_v8(void* p, uint32_t a, uint32_t b, uint32_t c, uint32_t d,
+                                      uint32_t e, uint32_t f, uint32_t g, uint32_t h)
+{
+    asm volatile("st.global.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(p), "r"(a),
+                 "r"(b), "r"(c), "r"(d), "r"(e), "r"(f), "r"(g), "r"(h)
+                 : "memory");
+}
+
+__device__ __forceinline__ void st_v8(void* p, uint4 a, uint4 b)
+{
+    st_v8(p, a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w);
+}
+
+__device__ __forceinline__ void st_v8f(void* p, float a, float b, float c, float d, float e,
+                                       float f, float g, float h)
+{
+    st_v8(p, __float_as_uint(a), __float_as_uint(b), __float_as_uint(c), __float_as_uint(d),
+          __float_as_uint(e), __float_as_uint(f), __float_as_uint(g), __float_as_uint(h));
+}
+
+__device__ __forceinline__ void st_v4d(void* p, double a, double b, double c, double d)
+{
+    st_v8(p, __double2loint(a), __double2hiint(a), __double2loint(b), __double2hiint(b),
+          __double2loint(c), __double2hiint(c), __double2loint(d), __double2hiint(d));
+}
+
+// ------------------------------------------------------------------ reduction
+
+__device__ __forceinline__ void block_reduce_add(uint64_t v, unsigned long long* dst)
+{
+    __shared__ unsigned long long part[32];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    const unsigned warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (lane == 0) part[warp] = v;
+    __syncthreads();
+    if (warp == 0) {
+        const unsigned nw = (blockDim.x + 31) >> 5;
+        v = lane < nw ? part[lane] : 0ull;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (lane == 0 && v) atomicAdd(dst, (unsigned long long)v);
+    }
+}
+
+// Dartboard hit (R9): X = w0>>8, Y = w1>>8, X^2 + Y^2 < 2^48.
+__device__ __forceinline__ uint32_t hit(uint32_t w0, uint32_t w1)
+{
+    const uint32_t X = w0 >> 8, Y = w1 >> 8;
+    const uint64_t r2 = (uint64_t)X * X + (uint64_t)Y * Y;  // < 2^49
+    return (uint32_t)(r2 >> 48) == 0u;
+}
+
+}  // namespace dev
+}  // namespace shv

@@ -1,6 +1,7 @@
 // shv_internal.h — launch records shared by the ABI layer (shv_api.cpp) and the
 // sm_100a kernels (shv_kernels.cu). Not installed; the public ABI is include/shv.h.
 #pragma once
+#include <cstddef>
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -81,5 +82,7 @@ enum KernelId : int {
     kKPhiloxMc = 4,
 };
 cudaError_t max_blocks_per_sm(int kernel, int kind, bool fast, int threads, int* out);
+// Dynamic shared memory of the MRG vector-fill kernel at a block size.
+size_t mrg_fill_smem(int threads);
 
 }  // namespace shv

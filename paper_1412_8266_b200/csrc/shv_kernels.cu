@@ -1,109 +1,56 @@
 // shv_kernels.cu — sm_100a kernels of the ShoveRand hot path (arXiv 1412.8266).
 //
-// Design: one persistent grid sized to the SM count; generator
-// state lives in registers (P L257-258: MRG32k3a "only stores 6 integers";
-// Philox is stateless, P L329-331); numbers leave the SM as full 32-byte
-// sectors (st.global.v8.b32 -> STG.E.ENL2.256, sm_100+), or never leave it
-// (fused Monte Carlo: warp shuffle + shared-memory block reduction + one
-// 64-bit atomic per block). No tensor cores: nothing here is a contraction.
+// Design: persistent grids sized to the SM count; generator
+// state in registers (P L257-258: MRG32k3a "only stores 6 integers"; Philox is
+// stateless, P L329-331); numbers leave the SM as 256-byte contiguous runs of
+// 32-byte vector stores (st.global.v8.b32 -> STG.E.ENL2.256, sm_100+), or
+// never leave it (fused Monte Carlo: warp shuffle + shared-memory block
+// reduction + one 64-bit atomic per block). No tensor cores: nothing here is
+// a contraction. Generator arithmetic lives in shv_device.cuh.
 //
-// Arithmetic (exact, integer only; bounds in DESIGN.md §4.2):
-//   MRG32k3a step  p1 = a12*x1 + a13n*(m1-x0) folded with 2^32 = 209 (mod m1)
-//                  p2 = a21*y2 + a23n*(m2-y0) folded twice with 2^32 = 22853 (mod m2)
-//                  z  = p1 - p2 (+ m1 if p1 <= p2), z in [1, m1]         (R1, R2)
-//   Philox4x32-10  10 rounds of two 32x32->64 multiplies and two 3-way XORs;
-//                  the key schedule is warp-uniform (uniform datapath).    (R5, R6)
+// Compile-time variants (the kernel lab, tools/lab/, builds each):
+//   SHV_MRG_STEP  0 = all-integer step, 1 = hybrid (component 2 on the FP64 pipe),
+//                 2 = both components on the FP64 pipe (default; fastest measured)
+//   SHV_MRG_STAGE 0 = each lane stores its own row directly, 1 = lanes stage 64
+//                 values in shared memory and the warp writes 256-byte runs
 #include <cstdint>
+#include <type_traits>
 #include <cuda_runtime.h>
 
+#include "shv_device.cuh"
 #include "shv_internal.h"
 
-namespace shv {
-namespace {
+#ifndef SHV_MRG_STEP
+#define SHV_MRG_STEP 2
+#endif
+#ifndef SHV_MRG_STAGE
+#define SHV_MRG_STAGE 1
+#endif
 
-// [LEcuyer1999] MRG32k3a parameters (PAPER.md L255 cites them; not restated there).
-constexpr uint32_t kM1 = 4294967087u;  // 2^32 - 209
-constexpr uint32_t kM2 = 4294944443u;  // 2^32 - 22853
-constexpr uint32_t kC1 = 209u;
-constexpr uint32_t kC2 = 22853u;
-constexpr uint32_t kA12 = 1403580u;
-constexpr uint32_t kA13n = 810728u;
-constexpr uint32_t kA21 = 527612u;
-constexpr uint32_t kA23n = 1370589u;
-// [Salmon.etal.2011] Philox4x32 multipliers and Weyl key increments.
-constexpr uint32_t kPM0 = 0xD2511F53u;
-constexpr uint32_t kPM1 = 0xCD9E8D57u;
-constexpr uint32_t kPW0 = 0x9E3779B9u;
-constexpr uint32_t kPW1 = 0xBB67AE85u;
+namespace shv {
 
 // Jump tables: [0][b] = A^(2^(76+b)) (substreams, b < 51),
 //              [1][b] = A^(2^(127+b)) (streams, b < 64).
 __device__ MatPair g_jump_tab[2][64];
 
-// ------------------------------------------------------------------ MRG32k3a
+namespace {
 
-struct Mrg {
-    uint32_t x0, x1, x2;  // component 1, oldest -> newest (R1)
-    uint32_t y0, y1, y2;  // component 2
-};
+using namespace dev;
 
-__device__ __forceinline__ uint32_t mrg_next(Mrg& s)
-{
-    // Component 1. P < 2^53.06, hi < 2^21.1, hi*209 < 2^29: one 32-bit fold
-    // whose carry-out or a result >= m1 both mean "subtract m1" = "+209".
-    const uint64_t p = (uint64_t)kA12 * s.x1 + (uint64_t)kA13n * (kM1 - s.x0);
-    const uint32_t lo = (uint32_t)p;
-    const uint32_t r = lo + (uint32_t)(p >> 32) * kC1;
-    const uint32_t p1 = r + ((r < lo) | (r >= kM1) ? kC1 : 0u);
-    s.x0 = s.x1;
-    s.x1 = s.x2;
-    s.x2 = p1;
-    // Component 2. Q < 2^52.9, hi*22853 < 2^35.4: fold to T < 2^35.6, then a
-    // second 32-bit fold as above with c = 22853.
-    const uint64_t q = (uint64_t)kA21 * s.y2 + (uint64_t)kA23n * (kM2 - s.y0);
-    const uint64_t t = (uint64_t)(uint32_t)(q >> 32) * kC2 + (uint32_t)q;
-    const uint32_t tlo = (uint32_t)t;
-    const uint32_t r2 = tlo + (uint32_t)(t >> 32) * kC2;
-    const uint32_t p2 = r2 + ((r2 < tlo) | (r2 >= kM2) ? kC2 : 0u);
-    s.y0 = s.y1;
-    s.y1 = s.y2;
-    s.y2 = p2;
-    // Combination: (p1 - p2) mod m1 with 0 -> m1 (R2); exact in wrap-around.
-    const uint32_t z = p1 - p2;
-    return p1 > p2 ? z : z + kM1;
-}
+template <int KIND>
+using OutT = typename std::conditional<KIND == kF64, double,
+                                       typename std::conditional<KIND == kF32, float, uint32_t>::type>::type;
 
-// x mod (2^32 - c) for any 64-bit x (c < 2^15): two folds + one subtraction.
-template <uint32_t C>
-__device__ __forceinline__ uint32_t red64(uint64_t x)
-{
-    x = (x >> 32) * C + (uint32_t)x;  // < 2^47.1
-    x = (x >> 32) * C + (uint32_t)x;  // < 2^32 + 2^30
-    const uint64_t m = (1ull << 32) - C;
-    return (uint32_t)(x >= m ? x - m : x);
-}
-
-template <uint32_t C>
-__device__ __forceinline__ void matvec(const uint32_t* M, uint32_t& v0, uint32_t& v1, uint32_t& v2)
-{
-    uint32_t r[3];
-#pragma unroll
-    for (int k = 0; k < 3; ++k) {
-        const uint64_t s = (uint64_t)red64<C>((uint64_t)M[3 * k] * v0) +
-                           red64<C>((uint64_t)M[3 * k + 1] * v1) +
-                           red64<C>((uint64_t)M[3 * k + 2] * v2);
-        r[k] = red64<C>(s);
-    }
-    v0 = r[0];
-    v1 = r[1];
-    v2 = r[2];
-}
-
-__device__ __forceinline__ void apply(const MatPair& P, Mrg& s)
-{
-    matvec<kC1>(P.a, s.x0, s.x1, s.x2);
-    matvec<kC2>(P.b, s.y0, s.y1, s.y2);
-}
+#if SHV_MRG_STEP == 2
+using Gen = MrgD;
+__device__ __forceinline__ Gen make_gen(const Mrg& s) { return to_fp64(s); }
+#elif SHV_MRG_STEP == 1
+using Gen = MrgH;
+__device__ __forceinline__ Gen make_gen(const Mrg& s) { return to_hybrid(s); }
+#else
+using Gen = Mrg;
+__device__ __forceinline__ Gen make_gen(const Mrg& s) { return s; }
+#endif
 
 __device__ __forceinline__ Mrg load_state(const uint32_t* __restrict__ st, uint64_t stride, uint64_t i)
 {
@@ -117,125 +64,49 @@ __device__ __forceinline__ Mrg load_state(const uint32_t* __restrict__ st, uint6
     return s;
 }
 
-// ------------------------------------------------------------------ Philox
-
-struct W4 {
-    uint32_t x, y, z, w;
-};
-
-__device__ __forceinline__ W4 philox10(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3,
-                                       uint32_t k0, uint32_t k1)
+// Start state of work item (stream i of the launch, segment j).
+__device__ __forceinline__ Gen item_state(const MrgLaunch& P, uint64_t i, uint64_t j)
 {
+    Mrg s = load_state(P.state, P.stride, P.stream_begin + i);
+    apply(P.seg[j].a, P.seg[j].b, s);
+    return make_gen(s);
+}
+
+template <int KIND>
+__device__ __forceinline__ uint4 pack4(uint32_t a, uint32_t b, uint32_t c, uint32_t d)
+{
+    if (KIND == kF32)
+        return make_uint4(__float_as_uint(to_f32(a)), __float_as_uint(to_f32(b)),
+                          __float_as_uint(to_f32(c)), __float_as_uint(to_f32(d)));
+    return make_uint4(a, b, c, d);
+}
+
+// Staging slot of 16-byte piece q of lane L: conflict-free for the per-lane
+// 128-bit writes (8 lanes, same q) and for the write-out reads (8 lanes, same
+// L, pieces 2p resp. 2p+1).
+__device__ __forceinline__ unsigned slot(unsigned L, unsigned q)
+{
+    return 16 * L + 8 * (q & 1) + (((q >> 1) + L) & 7);
+}
+
+// 8 values -> staging pieces (u32/f32: 2 pieces; f64: 4 pieces).
+template <int KIND>
+__device__ __forceinline__ void stage8(uint4* wb, unsigned lane, unsigned q0, Gen& s)
+{
+    uint32_t v[8];
 #pragma unroll
-    for (int r = 0; r < 10; ++r) {
-        const uint64_t p0 = (uint64_t)kPM0 * c0;
-        const uint64_t p1 = (uint64_t)kPM1 * c2;
-        const uint32_t n0 = (uint32_t)(p1 >> 32) ^ c1 ^ k0;
-        const uint32_t n2 = (uint32_t)(p0 >> 32) ^ c3 ^ k1;
-        c1 = (uint32_t)p1;
-        c3 = (uint32_t)p0;
-        c0 = n0;
-        c2 = n2;
-        k0 += kPW0;
-        k1 += kPW1;
-    }
-    return W4{c0, c1, c2, c3};
-}
-
-__device__ __forceinline__ W4 philox_blk(uint64_t blk, uint64_t g, uint32_t k0, uint32_t k1)
-{
-    return philox10((uint32_t)blk, (uint32_t)(blk >> 32), (uint32_t)g, (uint32_t)(g >> 32), k0, k1);
-}
-
-__device__ __forceinline__ uint32_t lane_of(const W4& v, uint32_t l)
-{
-    return l == 0 ? v.x : l == 1 ? v.y : l == 2 ? v.z : v.w;
-}
-
-// Generic per-draw access with a one-block cache (arbitrary offsets).
-struct PhiloxCursor {
-    uint64_t g;
-    uint32_t k0, k1;
-    uint64_t blk;
-    bool valid;
-    W4 v;
-    __device__ __forceinline__ uint32_t word(uint64_t b, uint32_t lane)
-    {
-        if (!valid || b != blk) {
-            v = philox_blk(b, g, k0, k1);
-            blk = b;
-            valid = true;
+    for (int u = 0; u < 8; ++u) v[u] = mrg_next(s);
+    if (KIND == kF64) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const double a = mrg_f64(v[2 * u]), b = mrg_f64(v[2 * u + 1]);
+            wb[slot(lane, q0 + u)] = make_uint4(__double2loint(a), __double2hiint(a),
+                                                __double2loint(b), __double2hiint(b));
         }
-        return lane_of(v, lane);
+    } else {
+        wb[slot(lane, q0)] = pack4<KIND>(v[0], v[1], v[2], v[3]);
+        wb[slot(lane, q0 + 1)] = pack4<KIND>(v[4], v[5], v[6], v[7]);
     }
-};
-
-// ------------------------------------------------------------------ conversions (R7)
-
-__device__ __forceinline__ float to_f32(uint32_t w)
-{
-    return __fmul_rn(__uint2float_rn(w >> 8), 0x1p-24f);
-}
-
-__device__ __forceinline__ double mrg_f64(uint32_t z)
-{
-    return __dmul_rn(__uint2double_rn(z), 0x1.000000d00000bp-32);
-}
-
-__device__ __forceinline__ double philox_f64(uint32_t lo, uint32_t hi)
-{
-    const uint64_t b = (((uint64_t)hi << 32) | lo) >> 11;
-    return __dmul_rn(__ull2double_rn(b), 0x1p-53);
-}
-
-// ------------------------------------------------------------------ stores
-
-// One full 32-byte sector per thread: STG.E.ENL2.256 on sm_100a.
-__device__ __forceinline__ void st_v8(void* p, uint32_t a, uint32_t b, uint32_t c, uint32_t d,
-                                      uint32_t e, uint32_t f, uint32_t g, uint32_t h)
-{
-    asm volatile("st.global.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(p), "r"(a),
-                 "r"(b), "r"(c), "r"(d), "r"(e), "r"(f), "r"(g), "r"(h)
-                 : "memory");
-}
-
-__device__ __forceinline__ void st_v8f(void* p, float a, float b, float c, float d, float e,
-                                       float f, float g, float h)
-{
-    st_v8(p, __float_as_uint(a), __float_as_uint(b), __float_as_uint(c), __float_as_uint(d),
-          __float_as_uint(e), __float_as_uint(f), __float_as_uint(g), __float_as_uint(h));
-}
-
-__device__ __forceinline__ void st_v4d(void* p, double a, double b, double c, double d)
-{
-    st_v8(p, __double2loint(a), __double2hiint(a), __double2loint(b), __double2hiint(b),
-          __double2loint(c), __double2hiint(c), __double2loint(d), __double2hiint(d));
-}
-
-// ------------------------------------------------------------------ reduction
-
-__device__ __forceinline__ void block_reduce_add(uint64_t v, unsigned long long* dst)
-{
-    __shared__ unsigned long long part[32];
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    const unsigned warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    if (lane == 0) part[warp] = v;
-    __syncthreads();
-    if (warp == 0) {
-        const unsigned nw = (blockDim.x + 31) >> 5;
-        v = lane < nw ? part[lane] : 0ull;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-        if (lane == 0 && v) atomicAdd(dst, (unsigned long long)v);
-    }
-}
-
-__device__ __forceinline__ uint32_t hit(uint32_t w0, uint32_t w1)
-{
-    const uint32_t X = w0 >> 8, Y = w1 >> 8;
-    const uint64_t r2 = (uint64_t)X * X + (uint64_t)Y * Y;  // < 2^49
-    return (uint32_t)(r2 >> 48) == 0u;
 }
 
 // ================================================================== kernels
@@ -250,7 +121,7 @@ __global__ void __launch_bounds__(256) mrg_seed_kernel(uint32_t* __restrict__ st
     Mrg s{b0, b1, b2, b3, b4, b5};
     uint64_t bits = i;
     for (int b = 0; bits; ++b, bits >>= 1)
-        if (bits & 1) apply(g_jump_tab[table][b], s);
+        if (bits & 1) apply(g_jump_tab[table][b].a, g_jump_tab[table][b].b, s);
     state[i] = s.x0;
     state[n + i] = s.x1;
     state[2 * n + i] = s.x2;
@@ -259,42 +130,103 @@ __global__ void __launch_bounds__(256) mrg_seed_kernel(uint32_t* __restrict__ st
     state[5 * n + i] = s.y2;
 }
 
-template <int KIND, bool VEC>
-__global__ void __launch_bounds__(256) mrg_fill_kernel(const __grid_constant__ MrgLaunch P)
+// MRG32k3a fill, vector path (32-byte aligned rows, seg_len % 8 == 0).
+// Staged: each lane generates 256 B of its row into shared memory per round,
+// then the warp writes them as eight 1-KB store instructions, each covering
+// four rows x 256 contiguous bytes.
+template <int KIND>
+__global__ void __launch_bounds__(256) mrg_fill_vec_kernel(const __grid_constant__ MrgLaunch P)
 {
-    using T = typename std::conditional<KIND == kF64, double,
-                                        typename std::conditional<KIND == kF32, float, uint32_t>::type>::type;
+    using T = OutT<KIND>;
+    const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#if SHV_MRG_STAGE
+    extern __shared__ uint4 smem[];
+    uint4* wb = smem + warp * 512;
+    constexpr uint32_t G = 256 / sizeof(T);  // values per lane per round
+    const uint64_t wstride = (uint64_t)gridDim.x * (blockDim.x >> 5) * 32;
+    for (uint64_t base = ((uint64_t)blockIdx.x * (blockDim.x >> 5) + warp) * 32; base < P.items;
+         base += wstride) {
+        const uint64_t it = base + lane;
+        uint32_t len = 0;
+        uint64_t row = 0;
+        Gen s{};
+        if (it < P.items) {
+            const uint64_t j = it / P.ns;
+            const uint64_t i = it - j * P.ns;
+            s = item_state(P, i, j);
+            const uint64_t c0 = j * P.seg_len;
+            len = (uint32_t)min(P.seg_len, P.n - c0);
+            row = (uint64_t)P.out + (i * P.n + c0) * sizeof(T);
+        }
+        const uint32_t maxlen = __reduce_max_sync(0xffffffffu, len);
+        for (uint32_t r = 0; r < maxlen; r += G) {
+            const uint32_t cnt = len > r ? min(G, len - r) : 0u;
+            if (cnt == G) {
+#pragma unroll
+                for (unsigned g = 0; g < G / 8; ++g) stage8<KIND>(wb, lane, g * (KIND == kF64 ? 4 : 2), s);
+            } else {
+                for (unsigned g = 0; g < cnt / 8; ++g) stage8<KIND>(wb, lane, g * (KIND == kF64 ? 4 : 2), s);
+            }
+            __syncwarp();
+#pragma unroll
+            for (unsigned k = 0; k < 8; ++k) {
+                const unsigned src = 4 * k + (lane >> 3), p = lane & 7;
+                const uint32_t scnt = __shfl_sync(0xffffffffu, cnt, src);
+                const uint64_t srow = __shfl_sync(0xffffffffu, row, src);
+                if (32 * p < scnt * sizeof(T))
+                    st_v8(reinterpret_cast<char*>(srow) + (uint64_t)r * sizeof(T) + 32 * p,
+                          wb[slot(src, 2 * p)], wb[slot(src, 2 * p + 1)]);
+            }
+            __syncwarp();
+        }
+    }
+#else
+    (void)lane;
+    (void)warp;
     const uint64_t nthr = (uint64_t)gridDim.x * blockDim.x;
     for (uint64_t it = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; it < P.items; it += nthr) {
         const uint64_t j = it / P.ns;
         const uint64_t i = it - j * P.ns;
-        Mrg s = load_state(P.state, P.stride, P.stream_begin + i);
-        apply(P.seg[j], s);
+        Gen s = item_state(P, i, j);
         const uint64_t c0 = j * P.seg_len;
         const uint64_t len = min(P.seg_len, P.n - c0);
         T* o = reinterpret_cast<T*>(P.out) + i * P.n + c0;
-        if (VEC) {
-            for (uint64_t t = 0; t < len; t += 8) {
-                uint32_t v[8];
+        for (uint64_t t = 0; t < len; t += 8) {
+            uint32_t v[8];
 #pragma unroll
-                for (int u = 0; u < 8; ++u) v[u] = mrg_next(s);
-                if (KIND == kU32) {
-                    st_v8(o + t, v[0], v[1], v[2], v[3], v[4], v[5], v[6], v[7]);
-                } else if (KIND == kF32) {
-                    st_v8f(o + t, to_f32(v[0]), to_f32(v[1]), to_f32(v[2]), to_f32(v[3]),
-                           to_f32(v[4]), to_f32(v[5]), to_f32(v[6]), to_f32(v[7]));
-                } else {
-                    st_v4d(o + t, mrg_f64(v[0]), mrg_f64(v[1]), mrg_f64(v[2]), mrg_f64(v[3]));
-                    st_v4d(o + t + 4, mrg_f64(v[4]), mrg_f64(v[5]), mrg_f64(v[6]), mrg_f64(v[7]));
-                }
+            for (int u = 0; u < 8; ++u) v[u] = mrg_next(s);
+            if (KIND == kU32) {
+                st_v8(o + t, v[0], v[1], v[2], v[3], v[4], v[5], v[6], v[7]);
+            } else if (KIND == kF32) {
+                st_v8f(o + t, to_f32(v[0]), to_f32(v[1]), to_f32(v[2]), to_f32(v[3]), to_f32(v[4]),
+                       to_f32(v[5]), to_f32(v[6]), to_f32(v[7]));
+            } else {
+                st_v4d(o + t, mrg_f64(v[0]), mrg_f64(v[1]), mrg_f64(v[2]), mrg_f64(v[3]));
+                st_v4d(o + t + 4, mrg_f64(v[4]), mrg_f64(v[5]), mrg_f64(v[6]), mrg_f64(v[7]));
             }
-        } else {
-            for (uint64_t t = 0; t < len; ++t) {
-                const uint32_t z = mrg_next(s);
-                if (KIND == kU32) o[t] = (T)z;
-                else if (KIND == kF32) o[t] = (T)to_f32(z);
-                else o[t] = (T)mrg_f64(z);
-            }
+        }
+    }
+#endif
+}
+
+// MRG32k3a fill, scalar path (any row length / element-aligned pointer).
+template <int KIND>
+__global__ void __launch_bounds__(256) mrg_fill_scalar_kernel(const __grid_constant__ MrgLaunch P)
+{
+    using T = OutT<KIND>;
+    const uint64_t nthr = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t it = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; it < P.items; it += nthr) {
+        const uint64_t j = it / P.ns;
+        const uint64_t i = it - j * P.ns;
+        Gen s = item_state(P, i, j);
+        const uint64_t c0 = j * P.seg_len;
+        const uint64_t len = min(P.seg_len, P.n - c0);
+        T* o = reinterpret_cast<T*>(P.out) + i * P.n + c0;
+        for (uint64_t t = 0; t < len; ++t) {
+            const uint32_t z = mrg_next(s);
+            if (KIND == kU32) o[t] = (T)z;
+            else if (KIND == kF32) o[t] = (T)to_f32(z);
+            else o[t] = (T)mrg_f64(z);
         }
     }
 }
@@ -306,15 +238,14 @@ __global__ void __launch_bounds__(256) mrg_mc_kernel(const __grid_constant__ Mrg
     for (uint64_t it = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; it < P.items; it += nthr) {
         const uint64_t j = it / P.ns;
         const uint64_t i = it - j * P.ns;
-        Mrg s = load_state(P.state, P.stride, P.stream_begin + i);
-        apply(P.seg[j], s);
+        Gen s = item_state(P, i, j);
         const uint64_t c0 = j * P.seg_len;
         const uint32_t len = (uint32_t)min(P.seg_len, P.n - c0);
         uint32_t h = 0;
         uint32_t k = 0;
-        for (; k + 4 <= len; k += 4) {
+        for (; k + 12 <= len; k += 12) {
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
+            for (int u = 0; u < 12; ++u) {
                 const uint32_t w0 = mrg_next(s);
                 const uint32_t w1 = mrg_next(s);
                 h += hit(w0, w1);
@@ -332,39 +263,55 @@ __global__ void __launch_bounds__(256) mrg_mc_kernel(const __grid_constant__ Mrg
 }
 
 // Fast Philox fill: offset lane 0, rows a multiple of E elements, 32-byte
-// aligned output. Work item = one 32-byte chunk = two counter blocks.
+// aligned output. A warp task is (row i, run of 32*R chunks of 32 bytes); lane
+// l handles chunks l, l+32, ... so each store instruction writes 1 KB
+// contiguous. The round-1 product of the stream word is hoisted per task.
 template <int KIND>
 __global__ void __launch_bounds__(256) philox_fill_fast_kernel(const __grid_constant__ PhiloxLaunch P)
 {
     constexpr uint64_t E = KIND == kF64 ? 4 : 8;  // elements per 32-byte chunk
-    const uint64_t nthr = (uint64_t)gridDim.x * blockDim.x;
-    uint64_t c = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (c >= P.items) return;
-    // (i, j) of the chunk's first element, advanced incrementally by the stride.
-    uint64_t i = (c * E) / P.n;
-    uint64_t j = c * E - i * P.n;
-    const uint64_t stride_e = nthr * E;
-    const uint64_t qs = stride_e / P.n, rs = stride_e - qs * P.n;
-    for (; c < P.items; c += nthr) {
+    const unsigned lane = threadIdx.x & 31;
+    const uint64_t cpr = P.n / E;                  // chunks per row
+    const uint64_t span = 32ull * P.nseg;          // chunks per task (nseg = R)
+    const uint64_t tpr = (cpr + span - 1) / span;  // tasks per row
+    const uint64_t nw = (uint64_t)gridDim.x * (blockDim.x >> 5);
+    uint64_t task = (uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (task >= P.items) return;
+    uint64_t i = task / tpr, kb = task - i * tpr;
+    const uint64_t qs = nw / tpr, rs = nw - qs * tpr;
+    for (; task < P.items; task += nw) {
         const uint64_t g = P.g0 + i;
-        // u32/f32: draws j..j+7 = blocks b, b+1. f64: draws 2j..2j+7, same.
-        const uint64_t b = P.o_blk + (KIND == kF64 ? j / 2 : j / 4);
-        const W4 a = philox_blk(b, g, P.k0, P.k1);
-        const W4 d = philox_blk(b + 1, g, P.k0, P.k1);
-        void* o = reinterpret_cast<char*>(P.out) + (c * 32);
-        if (KIND == kU32) {
-            st_v8(o, a.x, a.y, a.z, a.w, d.x, d.y, d.z, d.w);
-        } else if (KIND == kF32) {
-            st_v8f(o, to_f32(a.x), to_f32(a.y), to_f32(a.z), to_f32(a.w), to_f32(d.x),
-                   to_f32(d.y), to_f32(d.z), to_f32(d.w));
-        } else {
-            st_v4d(o, philox_f64(a.x, a.y), philox_f64(a.z, a.w), philox_f64(d.x, d.y),
-                   philox_f64(d.z, d.w));
+        const uint64_t p1 = (uint64_t)kPM1 * (uint32_t)g;  // round-1 product, task-invariant
+        const uint64_t c0 = kb * span;
+        const uint64_t left = cpr - c0;
+        const uint32_t nch = (uint32_t)(left < span ? left : span);
+        const uint32_t mine = nch > lane ? (nch - lane + 31) / 32 : 0u;
+        uint64_t blk = P.o_blk + 2 * (c0 + lane);
+        char* o = reinterpret_cast<char*>(P.out) + ((i * cpr + c0 + lane) << 5);
+        for (uint32_t r = 0; r < mine; ++r) {
+            const uint64_t b1 = add64(blk, 1u);
+            const uint64_t pa = (uint64_t)kPM0 * (uint32_t)blk;
+            const uint64_t pb = (uint64_t)kPM0 * (uint32_t)b1;
+            const W4 a = philox10_from_r1((uint32_t)(pa >> 32), (uint32_t)pa, (uint32_t)(p1 >> 32), (uint32_t)p1,
+                                          (uint32_t)(blk >> 32), (uint32_t)(g >> 32), P.k0, P.k1);
+            const W4 d = philox10_from_r1((uint32_t)(pb >> 32), (uint32_t)pb, (uint32_t)(p1 >> 32), (uint32_t)p1,
+                                          (uint32_t)(b1 >> 32), (uint32_t)(g >> 32), P.k0, P.k1);
+            if (KIND == kU32) {
+                st_v8(o, a.x, a.y, a.z, a.w, d.x, d.y, d.z, d.w);
+            } else if (KIND == kF32) {
+                st_v8f(o, to_f32(a.x), to_f32(a.y), to_f32(a.z), to_f32(a.w), to_f32(d.x), to_f32(d.y),
+                       to_f32(d.z), to_f32(d.w));
+            } else {
+                st_v4d(o, philox_f64(a.x, a.y), philox_f64(a.z, a.w), philox_f64(d.x, d.y),
+                       philox_f64(d.z, d.w));
+            }
+            blk = add64(blk, 64u);
+            o += 1024;
         }
-        j += rs;
+        kb += rs;
         i += qs;
-        if (j >= P.n) {
-            j -= P.n;
+        if (kb >= tpr) {
+            kb -= tpr;
             ++i;
         }
     }
@@ -375,8 +322,7 @@ __global__ void __launch_bounds__(256) philox_fill_fast_kernel(const __grid_cons
 template <int KIND>
 __global__ void __launch_bounds__(256) philox_fill_generic_kernel(const __grid_constant__ PhiloxLaunch P)
 {
-    using T = typename std::conditional<KIND == kF64, double,
-                                        typename std::conditional<KIND == kF32, float, uint32_t>::type>::type;
+    using T = OutT<KIND>;
     const uint64_t nthr = (uint64_t)gridDim.x * blockDim.x;
     const uint64_t total = P.ns * P.n;
     const uint32_t dpv = KIND == kF64 ? 2 : 1;
@@ -425,20 +371,18 @@ __global__ void __launch_bounds__(256) philox_mc_kernel(const __grid_constant__ 
         const uint32_t len = (uint32_t)min(P.seg_len, P.n - k0);
         uint32_t h = 0;
         if (FAST) {
-            const uint64_t b0 = P.o_blk + k0 / 2;
+            const uint64_t p1 = (uint64_t)kPM1 * (uint32_t)g;
+            uint64_t b = P.o_blk + k0 / 2;
             const uint32_t nb = len / 2;
-            uint32_t q = 0;
-            for (; q + 2 <= nb; q += 2) {
-                const W4 a = philox_blk(b0 + q, g, P.k0, P.k1);
-                const W4 b = philox_blk(b0 + q + 1, g, P.k0, P.k1);
-                h += hit(a.x, a.y) + hit(a.z, a.w) + hit(b.x, b.y) + hit(b.z, b.w);
-            }
-            for (; q < nb; ++q) {
-                const W4 a = philox_blk(b0 + q, g, P.k0, P.k1);
+            for (uint32_t q = 0; q < nb; ++q) {
+                const uint64_t pa = (uint64_t)kPM0 * (uint32_t)b;
+                const W4 a = philox10_from_r1((uint32_t)(pa >> 32), (uint32_t)pa, (uint32_t)(p1 >> 32),
+                                              (uint32_t)p1, (uint32_t)(b >> 32), (uint32_t)(g >> 32), P.k0, P.k1);
                 h += hit(a.x, a.y) + hit(a.z, a.w);
+                b = add64(b, 1u);
             }
             if (len & 1) {
-                const W4 a = philox_blk(b0 + nb, g, P.k0, P.k1);
+                const W4 a = philox_blk(b, g, P.k0, P.k1);
                 h += hit(a.x, a.y);
             }
         } else {
@@ -457,12 +401,27 @@ __global__ void __launch_bounds__(256) philox_mc_kernel(const __grid_constant__ 
 }
 
 template <typename K>
-cudaError_t occ(K kernel, int threads, int* out)
+cudaError_t occ(K kernel, int threads, size_t smem, int* out)
 {
-    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(out, kernel, threads, 0);
+    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(out, kernel, threads, smem);
+}
+
+template <int KIND>
+cudaError_t launch_vec(const MrgLaunch& p, Grid g, cudaStream_t s)
+{
+    const size_t smem = SHV_MRG_STAGE ? (size_t)(g.threads / 32) * 8192 : 0;
+    if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(mrg_fill_vec_kernel<KIND>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+    }
+    mrg_fill_vec_kernel<KIND><<<g.blocks, g.threads, smem, s>>>(p);
+    return cudaGetLastError();
 }
 
 }  // namespace
+
+size_t mrg_fill_smem(int threads) { return SHV_MRG_STAGE ? (size_t)(threads / 32) * 8192 : 0; }
 
 cudaError_t upload_jump_tables(const MatPair* sub51, const MatPair* str64)
 {
@@ -482,11 +441,14 @@ cudaError_t launch_mrg_seed(uint32_t* state, uint64_t n, const uint32_t base[6],
 
 cudaError_t launch_mrg_fill(const MrgLaunch& p, int kind, bool vec, Grid g, cudaStream_t s)
 {
-#define SHV_MRG_FILL(K, V) mrg_fill_kernel<K, V><<<g.blocks, g.threads, 0, s>>>(p)
-    if (kind == kU32) vec ? SHV_MRG_FILL(kU32, true) : SHV_MRG_FILL(kU32, false);
-    else if (kind == kF32) vec ? SHV_MRG_FILL(kF32, true) : SHV_MRG_FILL(kF32, false);
-    else vec ? SHV_MRG_FILL(kF64, true) : SHV_MRG_FILL(kF64, false);
-#undef SHV_MRG_FILL
+    if (vec) {
+        if (kind == kU32) return launch_vec<kU32>(p, g, s);
+        if (kind == kF32) return launch_vec<kF32>(p, g, s);
+        return launch_vec<kF64>(p, g, s);
+    }
+    if (kind == kU32) mrg_fill_scalar_kernel<kU32><<<g.blocks, g.threads, 0, s>>>(p);
+    else if (kind == kF32) mrg_fill_scalar_kernel<kF32><<<g.blocks, g.threads, 0, s>>>(p);
+    else mrg_fill_scalar_kernel<kF64><<<g.blocks, g.threads, 0, s>>>(p);
     return cudaGetLastError();
 }
 
@@ -521,26 +483,35 @@ cudaError_t max_blocks_per_sm(int kernel, int kind, bool fast, int threads, int*
 {
     switch (kernel) {
     case kKSeed:
-        return occ(mrg_seed_kernel, threads, out);
-    case kKMrgFill:
-        if (kind == kU32) return fast ? occ(mrg_fill_kernel<kU32, true>, threads, out)
-                                      : occ(mrg_fill_kernel<kU32, false>, threads, out);
-        if (kind == kF32) return fast ? occ(mrg_fill_kernel<kF32, true>, threads, out)
-                                      : occ(mrg_fill_kernel<kF32, false>, threads, out);
-        return fast ? occ(mrg_fill_kernel<kF64, true>, threads, out)
-                    : occ(mrg_fill_kernel<kF64, false>, threads, out);
+        return occ(mrg_seed_kernel, threads, 0, out);
+    case kKMrgFill: {
+        const size_t sm = mrg_fill_smem(threads);
+        if (fast && sm > 48 * 1024) {
+            cudaError_t e = cudaSuccess;
+            if (kind == kU32) e = cudaFuncSetAttribute(mrg_fill_vec_kernel<kU32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+            else if (kind == kF32) e = cudaFuncSetAttribute(mrg_fill_vec_kernel<kF32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+            else e = cudaFuncSetAttribute(mrg_fill_vec_kernel<kF64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+            if (e != cudaSuccess) return e;
+        }
+        if (kind == kU32) return fast ? occ(mrg_fill_vec_kernel<kU32>, threads, sm, out)
+                                      : occ(mrg_fill_scalar_kernel<kU32>, threads, 0, out);
+        if (kind == kF32) return fast ? occ(mrg_fill_vec_kernel<kF32>, threads, sm, out)
+                                      : occ(mrg_fill_scalar_kernel<kF32>, threads, 0, out);
+        return fast ? occ(mrg_fill_vec_kernel<kF64>, threads, sm, out)
+                    : occ(mrg_fill_scalar_kernel<kF64>, threads, 0, out);
+    }
     case kKMrgMc:
-        return occ(mrg_mc_kernel, threads, out);
+        return occ(mrg_mc_kernel, threads, 0, out);
     case kKPhiloxFill:
-        if (kind == kU32) return fast ? occ(philox_fill_fast_kernel<kU32>, threads, out)
-                                      : occ(philox_fill_generic_kernel<kU32>, threads, out);
-        if (kind == kF32) return fast ? occ(philox_fill_fast_kernel<kF32>, threads, out)
-                                      : occ(philox_fill_generic_kernel<kF32>, threads, out);
-        return fast ? occ(philox_fill_fast_kernel<kF64>, threads, out)
-                    : occ(philox_fill_generic_kernel<kF64>, threads, out);
+        if (kind == kU32) return fast ? occ(philox_fill_fast_kernel<kU32>, threads, 0, out)
+                                      : occ(philox_fill_generic_kernel<kU32>, threads, 0, out);
+        if (kind == kF32) return fast ? occ(philox_fill_fast_kernel<kF32>, threads, 0, out)
+                                      : occ(philox_fill_generic_kernel<kF32>, threads, 0, out);
+        return fast ? occ(philox_fill_fast_kernel<kF64>, threads, 0, out)
+                    : occ(philox_fill_generic_kernel<kF64>, threads, 0, out);
     case kKPhiloxMc:
-        return fast ? occ(philox_mc_kernel<true>, threads, out)
-                    : occ(philox_mc_kernel<false>, threads, out);
+        return fast ? occ(philox_mc_kernel<true>, threads, 0, out)
+                    : occ(philox_mc_kernel<false>, threads, 0, out);
     }
     return cudaErrorInvalidValue;
 }
