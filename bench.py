@@ -263,7 +263,7 @@ def main():
     dom = max(kms, key=kms.get)
     alg_bytes = 4 * total_per_rank  # u32 written per launch (4 B/number, 0 read)
     achieved = alg_bytes / (kms[dom] * 1e-3) / 1e9
-    roof = {"bound": "hbm", "kernel": "mrg_fill_kernel<u32>" if dom == "mrg" else "philox_fill_fast_kernel<u32>",
+    roof = {"bound": "hbm", "kernel": "mrg_fill_vec_kernel<u32>" if dom == "mrg" else "philox_fill_fast_kernel<u32>",
             "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
             "frac": round(achieved / peak, 4), "peak_source": peak_src,
             "traffic": traffic_from_profiles(dom),
