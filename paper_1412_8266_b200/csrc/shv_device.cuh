@@ -275,6 +275,105 @@ __device__ __forceinline__ uint32_t mrg_next(MrgS& s)
     return mrg_combine(p1, p2);
 }
 
+// Both components on the FP64 pipe with the output word computed on the
+// integer pipe (lab variant "W"): r mod 2^32 = a*wb - b*wc - k*m (mod 2^32),
+// where wb, wc are the previous outputs' residues mod 2^32 and k's low word is
+// read off the magic-rounded k' (k' = 1.5*2^52 + k, ulp 1). 5 FP64 ops and
+// 3 IMAD per component instead of 6 FP64 ops.
+template <uint32_t M, uint32_t A, uint32_t B>
+__device__ __forceinline__ uint32_t mrg_fp64w(double yb, double yc, uint32_t wb, uint32_t wc, double& r_out,
+                                              uint32_t& w_out)
+{
+    const double kMagic = 6755399441055744.0;  // 1.5 * 2^52
+    const double t = __dmul_rn((double)B, yc);
+    const double p = __fma_rn((double)A, yb, -t);
+    const double kk = __fma_rn(p, 1.0 / (double)M, kMagic);
+    const double r = __fma_rn(-__dadd_rn(kk, -kMagic), (double)M, p);
+    r_out = r;
+    const uint32_t klo = (uint32_t)__double2loint(kk);
+    uint32_t w = wb * A - wc * B - klo * M;
+    w_out = w;
+    asm("{\n\t.reg .pred n;\n\tsetp.lt.s32 n, %0, 0;\n\t@n add.u32 %0, %0, %1;\n\t}" : "+r"(w) : "n"(M));
+    return w;
+}
+
+struct MrgW {
+    double x0, x1, x2;
+    double y0, y1, y2;
+    uint32_t u0, u1, u2, v0, v1, v2;  // the same residues mod 2^32
+};
+
+__device__ __forceinline__ MrgW to_fp64w(const Mrg& s)
+{
+    return MrgW{__uint2double_rn(s.x0), __uint2double_rn(s.x1), __uint2double_rn(s.x2),
+                __uint2double_rn(s.y0), __uint2double_rn(s.y1), __uint2double_rn(s.y2),
+                s.x0, s.x1, s.x2, s.y0, s.y1, s.y2};
+}
+
+__device__ __forceinline__ uint32_t mrg_next(MrgW& s)
+{
+    double r1, r2;
+    uint32_t w1, w2;
+    const uint32_t p1 = mrg_fp64w<kM1, kA12, kA13n>(s.x1, s.x0, s.u1, s.u0, r1, w1);
+    s.x0 = s.x1; s.x1 = s.x2; s.x2 = r1;
+    s.u0 = s.u1; s.u1 = s.u2; s.u2 = w1;
+    const uint32_t p2 = mrg_fp64w<kM2, kA21, kA23n>(s.y2, s.y0, s.v2, s.v0, r2, w2);
+    s.y0 = s.y1; s.y1 = s.y2; s.y2 = r2;
+    s.v0 = s.v1; s.v1 = s.v2; s.v2 = w2;
+    return mrg_combine(p1, p2);
+}
+
+// Lab variants of the all-FP64 step: V=2 mask-add decode, V=3 mask-add decode
+// with cvt.rni.s32.f64 instead of the magic-add conversion, V=4 decode via
+// IMAD ((w >> 31) * -m + w).
+template <uint32_t M, uint32_t A, uint32_t B, int V>
+__device__ __forceinline__ uint32_t mrg_fp64v(double yb, double yc, double& r_out)
+{
+    const double kMagic = 6755399441055744.0;  // 1.5 * 2^52
+    const double t = __dmul_rn((double)B, yc);
+    const double p = __fma_rn((double)A, yb, -t);
+    const double k = __dadd_rn(__fma_rn(p, 1.0 / (double)M, kMagic), -kMagic);
+    const double r = __fma_rn(-k, (double)M, p);
+    r_out = r;
+    uint32_t w;
+    if (V == 3) {
+        int32_t i;
+        asm("cvt.rni.s32.f64 %0, %1;" : "=r"(i) : "d"(r));
+        w = (uint32_t)i;
+    } else {
+        w = (uint32_t)__double2loint(__dadd_rn(r, kMagic));
+    }
+    if (V == 4) return (uint32_t)((int32_t)w >> 31) * (0u - M) + w;
+    return w + ((uint32_t)((int32_t)w >> 31) & M);
+}
+
+template <int V>
+struct MrgDV {
+    double x0, x1, x2;
+    double y0, y1, y2;
+    char pad[8 * V];
+};
+
+template <int V>
+__device__ __forceinline__ MrgDV<V> to_fp64v(const Mrg& s)
+{
+    MrgDV<V> d;
+    d.x0 = __uint2double_rn(s.x0); d.x1 = __uint2double_rn(s.x1); d.x2 = __uint2double_rn(s.x2);
+    d.y0 = __uint2double_rn(s.y0); d.y1 = __uint2double_rn(s.y1); d.y2 = __uint2double_rn(s.y2);
+    return d;
+}
+
+template <int V>
+__device__ __forceinline__ uint32_t mrg_next(MrgDV<V>& s)
+{
+    double r1, r2;
+    const uint32_t p1 = mrg_fp64v<kM1, kA12, kA13n, V>(s.x1, s.x0, r1);
+    s.x0 = s.x1; s.x1 = s.x2; s.x2 = r1;
+    const uint32_t p2 = mrg_fp64v<kM2, kA21, kA23n, V>(s.y2, s.y0, r2);
+    s.y0 = s.y1; s.y1 = s.y2; s.y2 = r2;
+    return mrg_combine(p1, p2);
+}
+
 // ------------------------------------------------------------------ Philox4x32-10
 
 struct W4 {
@@ -324,6 +423,52 @@ __device__ __forceinline__ W4 philox10_from_r1(uint32_t hi0, uint32_t lo0, uint3
         k1 += kPW1;
     }
     return W4{c0, c1, c2, c3};
+}
+
+// Block from its round-1 outputs' varying half: for a fixed stream g and a
+// fixed high counter word, round 1 gives c0' = hi(M1*g_lo) ^ blk_hi ^ k0 and
+// c1' = lo(M1*g_lo) (both fixed), so round 2's M0*c0' (q) is fixed too; only
+// pa = M0*blk_lo varies. Rounds 3..10 as usual. 17 IMAD.WIDE per block.
+__device__ __forceinline__ W4 philox10_from_r2(uint64_t pa, uint64_t q, uint32_t c1r1, uint32_t g_hi,
+                                               uint32_t k0, uint32_t k1)
+{
+    // round 1 (key k0, k1): c2' = hi(pa) ^ g_hi ^ k1, c3' = lo(pa)
+    const uint32_t c2 = (uint32_t)(pa >> 32) ^ g_hi ^ k1;
+    const uint32_t c3 = (uint32_t)pa;
+    k0 += kPW0;
+    k1 += kPW1;
+    // round 2: p0 = q (= M0*c0'), p1 = M1*c2'
+    const uint64_t p1 = (uint64_t)kPM1 * c2;
+    uint32_t d0 = (uint32_t)(p1 >> 32) ^ c1r1 ^ k0;
+    uint32_t d1 = (uint32_t)p1;
+    uint32_t d2 = (uint32_t)(q >> 32) ^ c3 ^ k1;
+    uint32_t d3 = (uint32_t)q;
+    k0 += kPW0;
+    k1 += kPW1;
+#pragma unroll
+    for (int r = 2; r < 10; ++r) {
+        const uint64_t e0 = (uint64_t)kPM0 * d0;
+        const uint64_t e1 = (uint64_t)kPM1 * d2;
+        const uint32_t n0 = (uint32_t)(e1 >> 32) ^ d1 ^ k0;
+        const uint32_t n2 = (uint32_t)(e0 >> 32) ^ d3 ^ k1;
+        d1 = (uint32_t)e1;
+        d3 = (uint32_t)e0;
+        d0 = n0;
+        d2 = n2;
+        k0 += kPW0;
+        k1 += kPW1;
+    }
+    return W4{d0, d1, d2, d3};
+}
+
+// 64-bit + 64-bit on the ALU pipe.
+__device__ __forceinline__ uint64_t add64w(uint64_t a, uint64_t b)
+{
+    uint32_t lo, hi;
+    asm("add.cc.u32 %0, %2, %3;\n\taddc.u32 %1, %4, %5;"
+        : "=r"(lo), "=r"(hi)
+        : "r"((uint32_t)a), "r"((uint32_t)b), "r"((uint32_t)(a >> 32)), "r"((uint32_t)(b >> 32)));
+    return ((uint64_t)hi << 32) | lo;
 }
 
 __device__ __forceinline__ W4 philox_blk(uint64_t blk, uint64_t g, uint32_t k0, uint32_t k1)
@@ -426,6 +571,17 @@ __device__ __forceinline__ uint32_t hit(uint32_t w0, uint32_t w1)
     const uint32_t X = w0 >> 8, Y = w1 >> 8;
     const uint64_t r2 = (uint64_t)X * X + (uint64_t)Y * Y;  // < 2^49
     return (uint32_t)(r2 >> 48) == 0u;
+}
+
+// The same test on the FP64 pipe (for kernels whose FMA-heavy pipe is the
+// bottleneck): X, Y < 2^24 become exact doubles via the 2^52 bit pattern,
+// X^2 + Y^2 < 2^49 is exact in binary64, and the comparison is exact.
+__device__ __forceinline__ uint32_t hit_fp64(uint32_t w0, uint32_t w1)
+{
+    const double two52 = 4503599627370496.0;
+    const double x = __dadd_rn(__hiloint2double(0x43300000, (int)(w0 >> 8)), -two52);
+    const double y = __dadd_rn(__hiloint2double(0x43300000, (int)(w1 >> 8)), -two52);
+    return __fma_rn(x, x, __dmul_rn(y, y)) < 281474976710656.0 ? 1u : 0u;  // 2^48
 }
 
 }  // namespace dev

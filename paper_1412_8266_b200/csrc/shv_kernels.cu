@@ -81,12 +81,25 @@ __device__ __forceinline__ uint4 pack4(uint32_t a, uint32_t b, uint32_t c, uint3
     return make_uint4(a, b, c, d);
 }
 
-// Staging slot of 16-byte piece q of lane L: conflict-free for the per-lane
-// 128-bit writes (8 lanes, same q) and for the write-out reads (8 lanes, same
-// L, pieces 2p resp. 2p+1).
+// Bytes each lane stages per round (256: eight 1-KB store instructions per
+// round, each covering four rows x 256 B; 128: four instructions, eight rows
+// x 128 B each), and the min-blocks hint of the vector kernel.
+#ifndef SHV_MRG_RB
+#define SHV_MRG_RB 256
+#endif
+#ifndef SHV_MRG_MINB
+#define SHV_MRG_MINB 4  // <= 64 registers (fewer spill or slow the FP64 step; lab)
+#endif
+constexpr unsigned kRB = SHV_MRG_RB;
+constexpr unsigned kPieces = kRB / 16;  // 16-byte pieces per lane per round
+
+// Staging slot of 16-byte piece q of lane L, conflict-free for the per-lane
+// 128-bit writes (8 lanes, same q) and for the write-out reads (8 lanes that
+// read pieces 2p resp. 2p+1 of one source lane (kRB=256) or two (kRB=128)).
 __device__ __forceinline__ unsigned slot(unsigned L, unsigned q)
 {
-    return 16 * L + 8 * (q & 1) + (((q >> 1) + L) & 7);
+    if (kRB == 256) return 16 * L + 8 * (q & 1) + (((q >> 1) + L) & 7);
+    return 8 * L + ((q + L) & 7);
 }
 
 // 8 values -> staging pieces (u32/f32: 2 pieces; f64: 4 pieces).
@@ -135,14 +148,14 @@ __global__ void __launch_bounds__(256) mrg_seed_kernel(uint32_t* __restrict__ st
 // then the warp writes them as eight 1-KB store instructions, each covering
 // four rows x 256 contiguous bytes.
 template <int KIND>
-__global__ void __launch_bounds__(256) mrg_fill_vec_kernel(const __grid_constant__ MrgLaunch P)
+__global__ void __launch_bounds__(256, SHV_MRG_MINB) mrg_fill_vec_kernel(const __grid_constant__ MrgLaunch P)
 {
     using T = OutT<KIND>;
     const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #if SHV_MRG_STAGE
     extern __shared__ uint4 smem[];
-    uint4* wb = smem + warp * 512;
-    constexpr uint32_t G = 256 / sizeof(T);  // values per lane per round
+    uint4* wb = smem + warp * (32 * kPieces);
+    constexpr uint32_t G = kRB / sizeof(T);  // values per lane per round
     const uint64_t wstride = (uint64_t)gridDim.x * (blockDim.x >> 5) * 32;
     for (uint64_t base = ((uint64_t)blockIdx.x * (blockDim.x >> 5) + warp) * 32; base < P.items;
          base += wstride) {
@@ -169,8 +182,9 @@ __global__ void __launch_bounds__(256) mrg_fill_vec_kernel(const __grid_constant
             }
             __syncwarp();
 #pragma unroll
-            for (unsigned k = 0; k < 8; ++k) {
-                const unsigned src = 4 * k + (lane >> 3), p = lane & 7;
+            for (unsigned k = 0; k < kRB / 32; ++k) {
+                // each instruction: 1024/kRB source lanes x kRB contiguous bytes
+                const unsigned src = (1024 / kRB) * k + lane / (kRB / 32), p = lane % (kRB / 32);
                 const uint32_t scnt = __shfl_sync(0xffffffffu, cnt, src);
                 const uint64_t srow = __shfl_sync(0xffffffffu, row, src);
                 if (32 * p < scnt * sizeof(T))
@@ -262,6 +276,20 @@ __global__ void __launch_bounds__(256) mrg_mc_kernel(const __grid_constant__ Mrg
     block_reduce_add(total, P.hits);
 }
 
+// 8 draws (two blocks) -> one 32-byte chunk of u32 / f32 / f64 values.
+template <int KIND>
+__device__ __forceinline__ void store_chunk(void* o, const W4& a, const W4& d)
+{
+    if (KIND == kU32) {
+        st_v8(o, a.x, a.y, a.z, a.w, d.x, d.y, d.z, d.w);
+    } else if (KIND == kF32) {
+        st_v8f(o, to_f32(a.x), to_f32(a.y), to_f32(a.z), to_f32(a.w), to_f32(d.x), to_f32(d.y), to_f32(d.z),
+               to_f32(d.w));
+    } else {
+        st_v4d(o, philox_f64(a.x, a.y), philox_f64(a.z, a.w), philox_f64(d.x, d.y), philox_f64(d.z, d.w));
+    }
+}
+
 // Fast Philox fill: offset lane 0, rows a multiple of E elements, 32-byte
 // aligned output. A warp task is (row i, run of 32*R chunks of 32 bytes); lane
 // l handles chunks l, l+32, ... so each store instruction writes 1 KB
@@ -288,25 +316,34 @@ __global__ void __launch_bounds__(256) philox_fill_fast_kernel(const __grid_cons
         const uint32_t mine = nch > lane ? (nch - lane + 31) / 32 : 0u;
         uint64_t blk = P.o_blk + 2 * (c0 + lane);
         char* o = reinterpret_cast<char*>(P.out) + ((i * cpr + c0 + lane) << 5);
-        for (uint32_t r = 0; r < mine; ++r) {
-            const uint64_t b1 = add64(blk, 1u);
-            const uint64_t pa = (uint64_t)kPM0 * (uint32_t)blk;
-            const uint64_t pb = (uint64_t)kPM0 * (uint32_t)b1;
-            const W4 a = philox10_from_r1((uint32_t)(pa >> 32), (uint32_t)pa, (uint32_t)(p1 >> 32), (uint32_t)p1,
-                                          (uint32_t)(blk >> 32), (uint32_t)(g >> 32), P.k0, P.k1);
-            const W4 d = philox10_from_r1((uint32_t)(pb >> 32), (uint32_t)pb, (uint32_t)(p1 >> 32), (uint32_t)p1,
-                                          (uint32_t)(b1 >> 32), (uint32_t)(g >> 32), P.k0, P.k1);
-            if (KIND == kU32) {
-                st_v8(o, a.x, a.y, a.z, a.w, d.x, d.y, d.z, d.w);
-            } else if (KIND == kF32) {
-                st_v8f(o, to_f32(a.x), to_f32(a.y), to_f32(a.z), to_f32(a.w), to_f32(d.x), to_f32(d.y),
-                       to_f32(d.z), to_f32(d.w));
-            } else {
-                st_v4d(o, philox_f64(a.x, a.y), philox_f64(a.z, a.w), philox_f64(d.x, d.y),
-                       philox_f64(d.z, d.w));
+        // Fast sub-path: the low counter word does not wrap inside this task,
+        // so blk_hi is fixed, round 2's M0 product is hoisted, and the round-1
+        // products M0*blk_lo advance by additions (M0*(b+1) = M0*b + M0).
+        if ((uint32_t)blk <= 0xFFFFFFFFu - 64u * mine - 1u) {
+            const uint32_t c0r1 = (uint32_t)(p1 >> 32) ^ (uint32_t)(blk >> 32) ^ P.k0;
+            const uint64_t q = (uint64_t)kPM0 * c0r1;
+            uint64_t pa = (uint64_t)kPM0 * (uint32_t)blk;
+            for (uint32_t r = 0; r < mine; ++r) {
+                const uint64_t pb = add64w(pa, kPM0);
+                const W4 a = philox10_from_r2(pa, q, (uint32_t)p1, (uint32_t)(g >> 32), P.k0, P.k1);
+                const W4 d = philox10_from_r2(pb, q, (uint32_t)p1, (uint32_t)(g >> 32), P.k0, P.k1);
+                store_chunk<KIND>(o, a, d);
+                pa = add64w(pa, 64ull * kPM0);
+                o += 1024;
             }
-            blk = add64(blk, 64u);
-            o += 1024;
+        } else {
+            for (uint32_t r = 0; r < mine; ++r) {
+                const uint64_t b1 = add64(blk, 1u);
+                const uint64_t pa = (uint64_t)kPM0 * (uint32_t)blk;
+                const uint64_t pb = (uint64_t)kPM0 * (uint32_t)b1;
+                const W4 a = philox10_from_r1((uint32_t)(pa >> 32), (uint32_t)pa, (uint32_t)(p1 >> 32), (uint32_t)p1,
+                                              (uint32_t)(blk >> 32), (uint32_t)(g >> 32), P.k0, P.k1);
+                const W4 d = philox10_from_r1((uint32_t)(pb >> 32), (uint32_t)pb, (uint32_t)(p1 >> 32), (uint32_t)p1,
+                                              (uint32_t)(b1 >> 32), (uint32_t)(g >> 32), P.k0, P.k1);
+                store_chunk<KIND>(o, a, d);
+                blk = add64(blk, 64u);
+                o += 1024;
+            }
         }
         kb += rs;
         i += qs;
@@ -374,12 +411,26 @@ __global__ void __launch_bounds__(256) philox_mc_kernel(const __grid_constant__ 
             const uint64_t p1 = (uint64_t)kPM1 * (uint32_t)g;
             uint64_t b = P.o_blk + k0 / 2;
             const uint32_t nb = len / 2;
-            for (uint32_t q = 0; q < nb; ++q) {
-                const uint64_t pa = (uint64_t)kPM0 * (uint32_t)b;
-                const W4 a = philox10_from_r1((uint32_t)(pa >> 32), (uint32_t)pa, (uint32_t)(p1 >> 32),
-                                              (uint32_t)p1, (uint32_t)(b >> 32), (uint32_t)(g >> 32), P.k0, P.k1);
-                h += hit(a.x, a.y) + hit(a.z, a.w);
-                b = add64(b, 1u);
+            if ((uint32_t)b <= 0xFFFFFFFFu - nb - 1u) {
+                // no wrap of the low counter word: hoisted round-2 product,
+                // round-1 products by addition (see philox_fill_fast_kernel)
+                const uint32_t c0r1 = (uint32_t)(p1 >> 32) ^ (uint32_t)(b >> 32) ^ P.k0;
+                const uint64_t q = (uint64_t)kPM0 * c0r1;
+                uint64_t pa = (uint64_t)kPM0 * (uint32_t)b;
+                for (uint32_t r = 0; r < nb; ++r) {
+                    const W4 a = philox10_from_r2(pa, q, (uint32_t)p1, (uint32_t)(g >> 32), P.k0, P.k1);
+                    h += hit_fp64(a.x, a.y) + hit_fp64(a.z, a.w);
+                    pa = add64w(pa, kPM0);
+                }
+                b = add64(b, nb);
+            } else {
+                for (uint32_t r = 0; r < nb; ++r) {
+                    const uint64_t pa = (uint64_t)kPM0 * (uint32_t)b;
+                    const W4 a = philox10_from_r1((uint32_t)(pa >> 32), (uint32_t)pa, (uint32_t)(p1 >> 32),
+                                                  (uint32_t)p1, (uint32_t)(b >> 32), (uint32_t)(g >> 32), P.k0, P.k1);
+                    h += hit_fp64(a.x, a.y) + hit_fp64(a.z, a.w);
+                    b = add64(b, 1u);
+                }
             }
             if (len & 1) {
                 const W4 a = philox_blk(b, g, P.k0, P.k1);
@@ -409,7 +460,7 @@ cudaError_t occ(K kernel, int threads, size_t smem, int* out)
 template <int KIND>
 cudaError_t launch_vec(const MrgLaunch& p, Grid g, cudaStream_t s)
 {
-    const size_t smem = SHV_MRG_STAGE ? (size_t)(g.threads / 32) * 8192 : 0;
+    const size_t smem = mrg_fill_smem((int)g.threads);
     if (smem > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(mrg_fill_vec_kernel<KIND>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -421,7 +472,7 @@ cudaError_t launch_vec(const MrgLaunch& p, Grid g, cudaStream_t s)
 
 }  // namespace
 
-size_t mrg_fill_smem(int threads) { return SHV_MRG_STAGE ? (size_t)(threads / 32) * 8192 : 0; }
+size_t mrg_fill_smem(int threads) { return SHV_MRG_STAGE ? (size_t)(threads / 32) * 32 * kRB : 0; }
 
 cudaError_t upload_jump_tables(const MatPair* sub51, const MatPair* str64)
 {

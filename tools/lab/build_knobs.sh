@@ -1,0 +1,12 @@
+#!/bin/bash
+# Build libshv variants over the MRG fill knobs: name:flags pairs.
+set -e
+cd "$(dirname "$0")/../.."
+OUT=tools/lab/build; mkdir -p $OUT
+ARCH="-gencode arch=compute_100a,code=sm_100a"
+for spec in "$@"; do
+  name=${spec%%:*}; flags=${spec#*:}
+  nvcc $ARCH -O3 -std=c++17 -lineinfo -Xcompiler -fPIC -shared -cudart static -I include $flags \
+    -o $OUT/libshv_$name.so paper_1412_8266_b200/csrc/shv_kernels.cu paper_1412_8266_b200/csrc/shv_api.cpp &
+done
+wait
