@@ -203,12 +203,30 @@ shv_status ensure_tables(int dev)
 
 // ---------------------------------------------------------------- H2: work split
 
+// Occupancy (blocks per SM) of a kernel variant at a block size, cached per
+// device: the query is host work on every launch otherwise.
+int occupancy(int device, int kernel, int kind, bool fast, int tpb)
+{
+    static std::mutex mu;
+    static std::unordered_map<uint64_t, int> cache;
+    const uint64_t key = ((uint64_t)(device & 0xff) << 32) | ((uint64_t)kernel << 24) |
+                         ((uint64_t)kind << 16) | ((uint64_t)fast << 12) | (uint64_t)tpb;
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        auto it = cache.find(key);
+        if (it != cache.end()) return it->second;
+    }
+    int bps = 0;
+    if (max_blocks_per_sm(kernel, kind, fast, tpb, &bps) != cudaSuccess || bps < 1) bps = 1;
+    std::lock_guard<std::mutex> lk(mu);
+    cache[key] = bps;
+    return bps;
+}
+
 unsigned blocks_for(const Handle& h, int kernel, int kind, bool fast, uint64_t items)
 {
     int bps = (int)h.bps;
-    if (bps == 0) {
-        if (max_blocks_per_sm(kernel, kind, fast, (int)h.tpb, &bps) != cudaSuccess || bps < 1) bps = 1;
-    }
+    if (bps == 0) bps = occupancy(h.device, kernel, kind, fast, (int)h.tpb);
     const uint64_t full = (uint64_t)h.sms * (uint64_t)bps;
     const uint64_t need = (items + h.tpb - 1) / h.tpb;
     uint64_t b = need < full ? need : full;
@@ -218,9 +236,7 @@ unsigned blocks_for(const Handle& h, int kernel, int kind, bool fast, uint64_t i
 uint64_t resident_threads(const Handle& h, int kernel, int kind, bool fast)
 {
     int bps = (int)h.bps;
-    if (bps == 0) {
-        if (max_blocks_per_sm(kernel, kind, fast, (int)h.tpb, &bps) != cudaSuccess || bps < 1) bps = 1;
-    }
+    if (bps == 0) bps = occupancy(h.device, kernel, kind, fast, (int)h.tpb);
     return (uint64_t)h.sms * (uint64_t)bps * h.tpb;
 }
 
@@ -493,8 +509,12 @@ shv_status shv_streams_create_ex(shv_streams* out, int gen, const uint32_t* seed
         const MatPair B = pair_pow(first_stream, spacing == SHV_SPACING_STREAM ? 127 : 76);
         pair_apply(B, base);
         const int table = spacing == SHV_SPACING_STREAM ? 1 : 0;
-        Grid g{(unsigned)((n_streams + 255) / 256), 256};
-        e = launch_mrg_seed(h->state, n_streams, base, table, g, (cudaStream_t)cuda_stream);
+        // 2^16 seeding threads (fewer for small n), each walking its streams
+        // by the jump A^(T * spacing).
+        const uint64_t T = n_streams < (1u << 16) ? (n_streams + 255) / 256 * 256 : (1u << 16);
+        Grid g{(unsigned)(T / 256), 256};
+        const MatPair step = pair_pow(T, spacing == SHV_SPACING_STREAM ? 127 : 76);
+        e = launch_mrg_seed(h->state, n_streams, base, table, step, g, (cudaStream_t)cuda_stream);
         if (e != cudaSuccess) {
             if (h->own_state) cudaFree(h->state);
             return cuda_fail(e, "seed launch");

@@ -66,8 +66,9 @@ struct Grid {
 
 // ---- launchers (shv_kernels.cu) ----
 cudaError_t upload_jump_tables(const MatPair* sub51, const MatPair* str64);
+// T = g.blocks * g.threads seeding threads; step = A^(T * spacing).
 cudaError_t launch_mrg_seed(uint32_t* state, uint64_t n, const uint32_t base[6], int table,
-                            Grid g, cudaStream_t s);
+                            const MatPair& step, Grid g, cudaStream_t s);
 cudaError_t launch_mrg_fill(const MrgLaunch& p, int kind, bool vec, Grid g, cudaStream_t s);
 cudaError_t launch_mrg_mc(const MrgLaunch& p, Grid g, cudaStream_t s);
 cudaError_t launch_philox_fill(const PhiloxLaunch& p, int kind, bool fast, Grid g, cudaStream_t s);

@@ -13,6 +13,7 @@
 //                 2 = both components on the FP64 pipe (default; fastest measured)
 //   SHV_MRG_STAGE 0 = each lane stores its own row directly, 1 = lanes stage 64
 //                 values in shared memory and the warp writes 256-byte runs
+#include <atomic>
 #include <cstdint>
 #include <type_traits>
 #include <cuda_runtime.h>
@@ -124,23 +125,32 @@ __device__ __forceinline__ void stage8(uint4* wb, unsigned lane, unsigned q0, Ge
 
 // ================================================================== kernels
 
+// Per-stream start states (row a3). Thread t of T handles streams t, t+T,
+// t+2T, ...: its first state is the product of the per-bit jump tables for t
+// (<= log2 T mat-vecs), each next one is one mat-vec with step = A^(T*spacing)
+// (host-built). ~2 mat-vecs per stream instead of popcount(i) <= 20; the SoA
+// stores of a warp are coalesced.
 __global__ void __launch_bounds__(256) mrg_seed_kernel(uint32_t* __restrict__ state, uint64_t n,
                                                        uint32_t b0, uint32_t b1, uint32_t b2,
                                                        uint32_t b3, uint32_t b4, uint32_t b5,
-                                                       int table)
+                                                       int table, MatPair step)
 {
-    const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
+    const uint64_t T = (uint64_t)gridDim.x * blockDim.x;
+    const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n) return;
     Mrg s{b0, b1, b2, b3, b4, b5};
-    uint64_t bits = i;
+    uint64_t bits = t;
     for (int b = 0; bits; ++b, bits >>= 1)
         if (bits & 1) apply(g_jump_tab[table][b].a, g_jump_tab[table][b].b, s);
-    state[i] = s.x0;
-    state[n + i] = s.x1;
-    state[2 * n + i] = s.x2;
-    state[3 * n + i] = s.y0;
-    state[4 * n + i] = s.y1;
-    state[5 * n + i] = s.y2;
+    for (uint64_t i = t; i < n; i += T) {
+        state[i] = s.x0;
+        state[n + i] = s.x1;
+        state[2 * n + i] = s.x2;
+        state[3 * n + i] = s.y0;
+        state[4 * n + i] = s.y1;
+        state[5 * n + i] = s.y2;
+        if (i + T < n) apply(step.a, step.b, s);
+    }
 }
 
 // MRG32k3a fill, vector path (32-byte aligned rows, seg_len % 8 == 0).
@@ -457,13 +467,29 @@ cudaError_t occ(K kernel, int threads, size_t smem, int* out)
     return cudaOccupancyMaxActiveBlocksPerMultiprocessor(out, kernel, threads, smem);
 }
 
+// Opt the vector fill kernels into > 48 KB of dynamic shared memory, once per
+// device (the attribute is per function and context).
+template <int KIND>
+cudaError_t ensure_smem_attr()
+{
+    static std::atomic<uint64_t> done{0};
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    const uint64_t bit = 1ull << (dev & 63);
+    if (done.load(std::memory_order_acquire) & bit) return cudaSuccess;
+    e = cudaFuncSetAttribute(mrg_fill_vec_kernel<KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)mrg_fill_smem(256));
+    if (e == cudaSuccess) done.fetch_or(bit, std::memory_order_release);
+    return e;
+}
+
 template <int KIND>
 cudaError_t launch_vec(const MrgLaunch& p, Grid g, cudaStream_t s)
 {
     const size_t smem = mrg_fill_smem((int)g.threads);
     if (smem > 48 * 1024) {
-        cudaError_t e = cudaFuncSetAttribute(mrg_fill_vec_kernel<KIND>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaError_t e = ensure_smem_attr<KIND>();
         if (e != cudaSuccess) return e;
     }
     mrg_fill_vec_kernel<KIND><<<g.blocks, g.threads, smem, s>>>(p);
@@ -482,11 +508,11 @@ cudaError_t upload_jump_tables(const MatPair* sub51, const MatPair* str64)
     return cudaMemcpyToSymbol(g_jump_tab, h, sizeof h);
 }
 
-cudaError_t launch_mrg_seed(uint32_t* state, uint64_t n, const uint32_t base[6], int table, Grid g,
-                            cudaStream_t s)
+cudaError_t launch_mrg_seed(uint32_t* state, uint64_t n, const uint32_t base[6], int table,
+                            const MatPair& step, Grid g, cudaStream_t s)
 {
     mrg_seed_kernel<<<g.blocks, g.threads, 0, s>>>(state, n, base[0], base[1], base[2], base[3],
-                                                   base[4], base[5], table);
+                                                   base[4], base[5], table, step);
     return cudaGetLastError();
 }
 
@@ -538,10 +564,8 @@ cudaError_t max_blocks_per_sm(int kernel, int kind, bool fast, int threads, int*
     case kKMrgFill: {
         const size_t sm = mrg_fill_smem(threads);
         if (fast && sm > 48 * 1024) {
-            cudaError_t e = cudaSuccess;
-            if (kind == kU32) e = cudaFuncSetAttribute(mrg_fill_vec_kernel<kU32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-            else if (kind == kF32) e = cudaFuncSetAttribute(mrg_fill_vec_kernel<kF32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-            else e = cudaFuncSetAttribute(mrg_fill_vec_kernel<kF64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+            cudaError_t e = kind == kU32 ? ensure_smem_attr<kU32>()
+                          : kind == kF32 ? ensure_smem_attr<kF32>() : ensure_smem_attr<kF64>();
             if (e != cudaSuccess) return e;
         }
         if (kind == kU32) return fast ? occ(mrg_fill_vec_kernel<kU32>, threads, sm, out)
