@@ -174,6 +174,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-parts", action="store_true")
+    ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
+                    help="process-group backend (gloo: validate the N>1 logic with ranks sharing a GPU)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "shv" else args.warmup
 
@@ -188,10 +190,14 @@ def main():
 
     import paper_1412_8266_b200 as shv
 
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if args.backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group("gloo")
 
     def barrier():
         if world > 1:
@@ -236,7 +242,7 @@ def main():
 
     for _ in range(args.warmup):
         step()
-    clocks = Clocks([local] if world == 1 else list(range(world))) if rank == 0 else None
+    clocks = Clocks([local] if world == 1 else list(range(min(world, torch.cuda.device_count())))) if rank == 0 else None
     time.sleep(0.3)  # let the sampler start before the measured loops
     # per-kernel durations (same launches as the step, events on the launching stream)
     for _ in range(args.steps):

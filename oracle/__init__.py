@@ -25,6 +25,7 @@ MRG32K3A = 1
 PHILOX4X32_10 = 2
 SPACING_STREAM = 0
 SPACING_SUBSTREAM = 1
+SPACING_KEYED = 2
 U32, F32, F64 = 0, 1, 2
 
 _lib = None

@@ -244,12 +244,26 @@ int orc_stream_open(orc_stream* st, int gen, const uint32_t* seed, int nseed,
         return 0;
     }
     if (gen == ORC_PHILOX4X32_10) {
-        if (nseed != 1 && nseed != 2) return -1;
-        if (spacing != ORC_SPACING_STREAM) return -1;
         if (off_hi >> 2) return -1; /* a stream holds 2^66 draws (R6) */
-        st->key[0] = seed[0];
-        st->key[1] = nseed == 2 ? seed[1] : 0;
-        st->g = first + i;
+        if (spacing == ORC_SPACING_STREAM) {
+            if (nseed != 1 && nseed != 2) return -1;
+            st->key[0] = seed[0];
+            st->key[1] = nseed == 2 ? seed[1] : 0;
+            st->g = first + i;
+        } else if (spacing == ORC_SPACING_KEYED) {
+            /* Parameterization by key (P L331-334: "a single key that can be
+             * set at runtime according to each thread's unique identifier";
+             * S L249-257): key0 = stream id, key1 = experiment tag = seed[0];
+             * counter = (blk_lo, blk_hi, 0, 0). Ids beyond 2^32 exhaust the
+             * key word (S L253). */
+            if (nseed != 1) return -1;
+            if (first + i > 0xFFFFFFFFull || first + i < first) return -1;
+            st->key[0] = (uint32_t)(first + i);
+            st->key[1] = seed[0];
+            st->g = 0;
+        } else {
+            return -1;
+        }
         u128 d = ((u128)off_hi << 64) | off_lo;
         st->blk = (uint64_t)(d >> 2);
         st->buf_pos = 4;

@@ -20,7 +20,7 @@ extern "C" {
 #endif
 
 enum { ORC_MRG32K3A = 1, ORC_PHILOX4X32_10 = 2 };
-enum { ORC_SPACING_STREAM = 0, ORC_SPACING_SUBSTREAM = 1 };
+enum { ORC_SPACING_STREAM = 0, ORC_SPACING_SUBSTREAM = 1, ORC_SPACING_KEYED = 2 };
 enum { ORC_U32 = 0, ORC_F32 = 1, ORC_F64 = 2 };
 
 /* ---- MRG32k3a (P L250-282 §4.1; constants from [LEcuyer1999], P L255) ---- */

@@ -69,6 +69,20 @@ def test_philox_stream_layout_vs_curand(orc, curand_pin, offset):
         assert [int(x) for x in got] == curand_pin.ask("pstream", seed, g, offset, 37)
 
 
+@pytest.mark.parametrize("offset", [0, 1, 6, 1 << 40])
+def test_philox_keyed_mode_vs_curand(orc, curand_pin, offset):
+    # Key-per-stream Parameterization (P L331-334, S L249-257): stream id -> key0,
+    # tag -> key1, counter (blk, 0): cuRAND curand_init(tag<<32 | id, 0, offset).
+    tag = 0xC0FFEE
+    got = orc.generate(W.PHILOX4X32_10, [tag], 5, 29, first=77, spacing=W.SPACING_KEYED,
+                       offset=offset)
+    for r in range(5):
+        assert [int(x) for x in got[r]] == curand_pin.ask("pstream", (tag << 32) | (77 + r), 0,
+                                                           offset, 29)
+    with pytest.raises(ValueError):  # key space exhausted (S L253)
+        orc.generate(W.PHILOX4X32_10, [tag], 2, 4, first=(1 << 32) - 1, spacing=W.SPACING_KEYED)
+
+
 def test_philox_bijective_no_collisions(orc):
     # S L230: distinct counters under one key -> no collisions over 10^6 blocks.
     rows = orc.generate(W.PHILOX4X32_10, [7, 9], 1, 4 * 1_000_000)

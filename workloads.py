@@ -14,6 +14,7 @@ MRG32K3A = 1
 PHILOX4X32_10 = 2
 SPACING_STREAM = 0
 SPACING_SUBSTREAM = 1
+SPACING_KEYED = 2
 
 
 @dataclass(frozen=True)
