@@ -13,8 +13,9 @@
  * plumbing. Handle stream i < n_streams is
  *   MRG32k3a, SHV_SPACING_STREAM    : stream first+i, 2^127 draws apart  (P L264-268 [§4.1])
  *   MRG32k3a, SHV_SPACING_SUBSTREAM : substream first+i of stream 0, 2^76 apart (ibid.)
- *   Philox4x32-10 (STREAM only)     : counter-stream g = first+i, counter
+ *   Philox4x32-10, SHV_SPACING_STREAM: counter-stream g = first+i, counter
  *                                     (blk_lo, blk_hi, g_lo, g_hi), key = seed (P L322-336 [§4.3]; R6)
+ *   Philox4x32-10, SHV_SPACING_KEYED : key = (first+i, tag), counter (blk_lo, blk_hi, 0, 0)
  * Every stream of a handle sits at the same draw offset o (u128), which each
  * generate / mc_pi call advances by the draws it consumed (S L58; R8).
  *
@@ -63,7 +64,14 @@ typedef enum {
 
 typedef enum {
     SHV_SPACING_STREAM = 0,     /* MRG: 2^127 draws apart; Philox: counter-stream index */
-    SHV_SPACING_SUBSTREAM = 1   /* MRG: 2^76 draws apart; Philox: SHV_ERR_UNSUPPORTED */
+    SHV_SPACING_SUBSTREAM = 1,  /* MRG: 2^76 draws apart; Philox: SHV_ERR_UNSUPPORTED */
+    SHV_SPACING_KEYED = 2       /* Philox only: Parameterization, one key per stream
+                                   (P L331-334 "a single key that can be set at runtime
+                                   according to each thread's unique identifier"; S L249-257):
+                                   key = (first+i, tag), counter = (blk_lo, blk_hi, 0, 0);
+                                   seed = 1 word, the experiment tag; first+n <= 2^32
+                                   (else SHV_ERR_INSUFFICIENT_STREAMS, S L253 KeySpaceExhausted).
+                                   MRG: SHV_ERR_UNSUPPORTED */
 } shv_spacing;
 
 typedef enum {
@@ -153,6 +161,25 @@ shv_status shv_mc_pi_ex(shv_streams h, uint64_t samples_per_stream, uint64_t* d_
                         uint64_t* d_stream_counts, void* cuda_stream);
 
 shv_status shv_get_position(shv_streams h, shv_position* out);
+
+/* Device-side view of a handle for user kernels (the paper's device API,
+ * P L387-399 [§5.2], Listing 1 P L485-490): pass it by value to a kernel and
+ * construct shv::Rng<GEN>(view, i) from include/shv_rng.cuh in each thread;
+ * rng.next_u32()/next_f32()/next_f64() then produce exactly the values
+ * shv_generate_* would write for stream i at the handle's current offset
+ * (R7, R8). The view is a snapshot: after a kernel consumed up to K draws per
+ * stream, advance the handle with shv_jump(h, SHV_JUMP_DRAWS, K). The state
+ * pointer stays valid until shv_streams_destroy. */
+typedef struct {
+    uint32_t gen, spacing;
+    uint32_t key0, key1;          /* Philox key words (keyed: key1 = tag) */
+    uint64_t first_stream, n_streams;
+    uint64_t offset_lo, offset_hi;
+    const uint32_t* state;        /* MRG: SoA start states (offset 0); NULL for Philox */
+    uint32_t jump[18];            /* MRG: A1^o (mod m1), A2^o (mod m2), row-major */
+} shv_device_view;
+
+shv_status shv_get_device_view(shv_streams h, shv_device_view* out);
 
 /* Release (P L498 [Listing 1] release()). Frees library-allocated state with
  * cudaFree (which synchronizes the device); the id becomes invalid, a second

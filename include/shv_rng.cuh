@@ -1,0 +1,91 @@
+/*
+ * shv_rng.cuh — device-side generator objects for user kernels: the paper's
+ * device API (P L387-399 [§5.2]: "create an instance of the PRNG you want to
+ * use and let its class' constructor do the rest ... pick random numbers by
+ * calling the next() method"; Listing 1, P L485-490).
+ *
+ *   __global__ void fooKernel(float* ddata, shv_device_view v) {   // Listing 1
+ *       const uint64_t i = blockDim.x * blockIdx.x + threadIdx.x;
+ *       shv::Rng<SHV_GEN_MRG32K3A> rng(v, i);
+ *       ddata[i] = rng.next_f32();
+ *   }
+ *   // host: h = shv_streams_create(...block_num * thread_num streams...);
+ *   //       shv_get_device_view(h, &v); fooKernel<<<block_num, thread_num>>>(d, v);
+ *   //       shv_jump(h, SHV_JUMP_DRAWS, draws_per_thread); ...; shv_streams_destroy(h);
+ *
+ * Thread i's sequence is stream i of the handle at the view's offset, value
+ * for value the one shv_generate_u32/f32/f64 writes (R7, R8); the state lives
+ * in registers. The arithmetic is shv_device.cuh's (MRG32k3a on the FP64 pipe,
+ * Philox4x32-10 with the warp-uniform key schedule when keys are shared).
+ */
+#pragma once
+#include "shv.h"
+#include "shv_device.cuh"
+
+namespace shv {
+
+template <int GEN>
+class Rng;
+
+template <>
+class Rng<SHV_GEN_MRG32K3A> {
+public:
+    // Stream i: its start state (offset 0) jumped by the view's A^o.
+    __device__ Rng(const shv_device_view& v, uint64_t i)
+    {
+        const uint32_t* st = v.state;
+        const uint64_t n = v.n_streams;
+        dev::Mrg m{st[i], st[n + i], st[2 * n + i], st[3 * n + i], st[4 * n + i], st[5 * n + i]};
+        dev::apply(v.jump, v.jump + 9, m);
+        s_ = dev::to_fp64(m);
+    }
+    __device__ uint32_t next_u32() { return dev::mrg_next(s_); }  // z in [1, m1]
+    __device__ float next_f32() { return dev::to_f32(next_u32()); }
+    __device__ double next_f64() { return dev::mrg_f64(next_u32()); }
+
+private:
+    dev::MrgD s_;
+};
+
+template <>
+class Rng<SHV_GEN_PHILOX4X32_10> {
+public:
+    __device__ Rng(const shv_device_view& v, uint64_t i)
+    {
+        if (v.spacing == SHV_SPACING_KEYED) {
+            k0_ = (uint32_t)(v.first_stream + i);
+            k1_ = v.key1;
+            g_ = 0;
+        } else {
+            k0_ = v.key0;
+            k1_ = v.key1;
+            g_ = v.first_stream + i;
+        }
+        blk_ = (v.offset_lo >> 2) | (v.offset_hi << 62);  // draw o -> block o/4, lane o%4
+        lane_ = (uint32_t)(v.offset_lo & 3);
+        buf_ = dev::philox_blk(blk_, g_, k0_, k1_);
+    }
+    __device__ uint32_t next_u32()
+    {
+        if (lane_ == 4) {
+            ++blk_;
+            buf_ = dev::philox_blk(blk_, g_, k0_, k1_);
+            lane_ = 0;
+        }
+        return dev::lane_of(buf_, lane_++);
+    }
+    __device__ float next_f32() { return dev::to_f32(next_u32()); }
+    __device__ double next_f64()  // two draws per value (R7)
+    {
+        const uint32_t lo = next_u32();
+        return dev::philox_f64(lo, next_u32());
+    }
+
+private:
+    uint32_t k0_, k1_;
+    uint64_t g_, blk_;
+    uint32_t lane_;
+    dev::W4 buf_;
+};
+
+}  // namespace shv

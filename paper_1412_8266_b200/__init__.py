@@ -30,6 +30,7 @@ SHV_GEN_MRG32K3A = 1
 SHV_GEN_PHILOX4X32_10 = 2
 SHV_SPACING_STREAM = 0
 SHV_SPACING_SUBSTREAM = 1
+SHV_SPACING_KEYED = 2
 SHV_JUMP_DRAWS = 0
 SHV_JUMP_SUBSTREAMS = 1
 SHV_JUMP_STREAMS = 2
@@ -40,7 +41,7 @@ EXPORTS = (
     "shv_generate_u32", "shv_generate_f32", "shv_generate_f64", "shv_generate_u32_host",
     "shv_mc_pi", "shv_mc_pi_ex", "shv_get_position", "shv_streams_destroy",
     "shv_status_string", "shv_last_error_message", "shv_set_launch_config",
-    "shv_partition", "shv_jump_matrix", "shv_build_info",
+    "shv_partition", "shv_jump_matrix", "shv_build_info", "shv_get_device_view",
 )
 
 
@@ -54,6 +55,13 @@ class shv_position(C.Structure):
     _fields_ = [("gen", C.c_uint32), ("spacing", C.c_uint32), ("seed", C.c_uint32 * 6),
                 ("first_stream", C.c_uint64), ("n_streams", C.c_uint64),
                 ("offset_lo", C.c_uint64), ("offset_hi", C.c_uint64)]
+
+
+class shv_device_view(C.Structure):
+    _fields_ = [("gen", C.c_uint32), ("spacing", C.c_uint32), ("key0", C.c_uint32),
+                ("key1", C.c_uint32), ("first_stream", C.c_uint64), ("n_streams", C.c_uint64),
+                ("offset_lo", C.c_uint64), ("offset_hi", C.c_uint64), ("state", C.c_void_p),
+                ("jump", C.c_uint32 * 18)]
 
 
 LIB_PATH = _build.LIB
@@ -85,6 +93,7 @@ def _load():
         "shv_partition": (st, [u64, C.c_int, C.c_int, C.POINTER(u64), C.POINTER(u64)]),
         "shv_jump_matrix": (st, [u64, u64, u32p]),
         "shv_build_info": (C.c_char_p, []),
+        "shv_get_device_view": (st, [u64, C.POINTER(shv_device_view)]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -181,6 +190,13 @@ def shv_get_position(h: int) -> dict:
     return {"gen": p.gen, "spacing": p.spacing, "seed": list(p.seed),
             "first_stream": p.first_stream, "n_streams": p.n_streams,
             "offset": p.offset_lo | (p.offset_hi << 64)}
+
+
+def shv_get_device_view(h: int) -> shv_device_view:
+    """The POD view a user kernel takes by value (include/shv_rng.cuh)."""
+    v = shv_device_view()
+    _check(lib.shv_get_device_view(h, C.byref(v)))
+    return v
 
 
 def shv_streams_destroy(h: int):

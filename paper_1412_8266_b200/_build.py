@@ -10,7 +10,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libshv.so")
 SOURCES = [os.path.join(CSRC, "shv_kernels.cu"), os.path.join(CSRC, "shv_api.cpp")]
-DEPS = SOURCES + [os.path.join(CSRC, "shv_internal.h"), os.path.join(CSRC, "shv_device.cuh"), os.path.join(ROOT, "include", "shv.h")]
+DEPS = SOURCES + [os.path.join(CSRC, "shv_internal.h"), os.path.join(ROOT, "include", "shv_device.cuh"), os.path.join(ROOT, "include", "shv.h")]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

@@ -352,8 +352,9 @@ shv_status generate(shv_streams hid, T* out, uint64_t n, void* stream, int kind,
             const uint64_t E = kind == kF64 ? 4 : 8;
             const bool fast = aligned32 && (n % E == 0) && ((uint32_t)h.offset & 3) == 0;
             PhiloxLaunch P{};
+            P.keyed = h.spacing == SHV_SPACING_KEYED;
             P.k0 = h.seed[0];
-            P.k1 = h.seed[1];
+            P.k1 = P.keyed ? h.seed[0] : h.seed[1];
             P.g0 = h.first + s0;
             P.ns = ns;
             P.o_blk = (uint64_t)(h.offset >> 2);
@@ -365,7 +366,8 @@ shv_status generate(shv_streams hid, T* out, uint64_t n, void* stream, int kind,
                 // warp tasks of (row, 32*R chunks); R shrinks until there are
                 // >= 4 tasks per resident warp.
                 const uint64_t cpr = n / E;
-                const uint64_t rwarps = resident_threads(h, kKPhiloxFill, kind, true) / 32;
+                const int kid = P.keyed ? kKPhiloxFillKeyed : kKPhiloxFill;
+                const uint64_t rwarps = resident_threads(h, kid, kind, true) / 32;
                 uint64_t R = (cpr + 31) / 32;
                 if (R > 16) R = 16;
                 if (h.seg) R = h.seg / 8 < 1 ? 1 : (h.seg / 8 > 64 ? 64 : h.seg / 8);
@@ -373,10 +375,10 @@ shv_status generate(shv_streams hid, T* out, uint64_t n, void* stream, int kind,
                 while (!h.seg && R > 1 && tasks(R) < 4 * rwarps) R /= 2;
                 P.nseg = (uint32_t)R;
                 P.items = tasks(R);
-                g = Grid{blocks_for(h, kKPhiloxFill, kind, true, P.items * 32), h.tpb};
+                g = Grid{blocks_for(h, kid, kind, true, P.items * 32), h.tpb};
             } else {
                 P.items = (ns * n + 7) / 8;
-                g = Grid{blocks_for(h, kKPhiloxFill, kind, false, P.items), h.tpb};
+                g = Grid{blocks_for(h, P.keyed ? kKPhiloxFillKeyed : kKPhiloxFill, kind, false, P.items), h.tpb};
             }
             err = launch_philox_fill(P, kind, fast, g, s);
         }
@@ -460,11 +462,17 @@ shv_status shv_streams_create_ex(shv_streams* out, int gen, const uint32_t* seed
     shv_status st = validate_seed(gen, seed, seed_words, s6);
     if (st) return st;
     if (n_streams == 0) return fail(SHV_ERR_INVALID_ARGUMENT, "n_streams must be >= 1");
-    if (spacing != SHV_SPACING_STREAM && spacing != SHV_SPACING_SUBSTREAM)
+    if (spacing != SHV_SPACING_STREAM && spacing != SHV_SPACING_SUBSTREAM && spacing != SHV_SPACING_KEYED)
         return fail(SHV_ERR_INVALID_ARGUMENT, "unknown spacing %d", spacing);
-    if (gen == SHV_GEN_PHILOX4X32_10 && spacing != SHV_SPACING_STREAM)
+    if (gen == SHV_GEN_PHILOX4X32_10 && spacing == SHV_SPACING_SUBSTREAM)
         return fail(SHV_ERR_UNSUPPORTED, "Philox4x32-10 has no substreams");
+    if (gen == SHV_GEN_MRG32K3A && spacing == SHV_SPACING_KEYED)
+        return fail(SHV_ERR_UNSUPPORTED, "MRG32k3a has no keys (use STREAM or SUBSTREAM spacing)");
+    if (spacing == SHV_SPACING_KEYED && seed_words != 1)
+        return fail(SHV_ERR_INVALID_ARGUMENT, "keyed Philox takes one seed word (the experiment tag)");
     const u128 end = (u128)first_stream + n_streams;
+    if (spacing == SHV_SPACING_KEYED && end > ((u128)1 << 32))
+        return fail(SHV_ERR_INSUFFICIENT_STREAMS, "key space exhausted: stream ids end at 2^32");
     if (gen == SHV_GEN_MRG32K3A && spacing == SHV_SPACING_SUBSTREAM && end > ((u128)1 << 51))
         return fail(SHV_ERR_INSUFFICIENT_STREAMS, "substreams end at 2^51 per stream");
     if (end > ((u128)1 << 64)) return fail(SHV_ERR_INSUFFICIENT_STREAMS, "streams end at 2^64");
@@ -610,8 +618,9 @@ shv_status shv_mc_pi_ex(shv_streams hid, uint64_t samples, uint64_t* d_hits, uin
     } else {
         const bool fast = ((uint32_t)h.offset & 3) == 0;
         PhiloxLaunch P{};
+        P.keyed = h.spacing == SHV_SPACING_KEYED;
         P.k0 = h.seed[0];
-        P.k1 = h.seed[1];
+        P.k1 = P.keyed ? h.seed[0] : h.seed[1];
         P.g0 = h.first;
         P.ns = h.n;
         P.o_blk = (uint64_t)(h.offset >> 2);
@@ -619,9 +628,10 @@ shv_status shv_mc_pi_ex(shv_streams hid, uint64_t samples, uint64_t* d_hits, uin
         P.n = samples;
         P.hits = (unsigned long long*)d_hits;
         P.counts = (unsigned long long*)d_counts;
-        split(h, h.n, samples, 2, 32, resident_threads(h, kKPhiloxMc, 0, fast), cap, &P.seg_len, &P.nseg);
+        const int kid = P.keyed ? kKPhiloxMcKeyed : kKPhiloxMc;
+        split(h, h.n, samples, 2, 32, resident_threads(h, kid, 0, fast), cap, &P.seg_len, &P.nseg);
         P.items = h.n * P.nseg;
-        Grid g{blocks_for(h, kKPhiloxMc, 0, fast, P.items), h.tpb};
+        Grid g{blocks_for(h, kid, 0, fast, P.items), h.tpb};
         err = launch_philox_mc(P, fast, g, s);
     }
     if (err != cudaSuccess) return cuda_fail(err, "mc_pi launch");
@@ -647,6 +657,30 @@ shv_status shv_get_position(shv_streams hid, shv_position* out)
     out->n_streams = h.n;
     out->offset_lo = (uint64_t)h.offset;
     out->offset_hi = (uint64_t)(h.offset >> 64);
+    return SHV_OK;
+}
+
+shv_status shv_get_device_view(shv_streams hid, shv_device_view* out)
+{
+    auto hp = lookup(hid);
+    if (!hp) return fail(SHV_ERR_LIFECYCLE, "unknown or destroyed handle");
+    if (!out) return fail(SHV_ERR_INVALID_ARGUMENT, "NULL out");
+    const Handle& h = *hp;
+    memset(out, 0, sizeof *out);
+    out->gen = (uint32_t)h.gen;
+    out->spacing = (uint32_t)h.spacing;
+    out->key0 = h.seed[0];
+    out->key1 = h.spacing == SHV_SPACING_KEYED ? h.seed[0] : h.seed[1];
+    out->first_stream = h.first;
+    out->n_streams = h.n;
+    out->offset_lo = (uint64_t)h.offset;
+    out->offset_hi = (uint64_t)(h.offset >> 64);
+    if (h.gen == SHV_GEN_MRG32K3A) {
+        out->state = h.state;
+        const MatPair J = pair_pow(h.offset, 0);
+        memcpy(out->jump, J.a, 36);
+        memcpy(out->jump + 9, J.b, 36);
+    }
     return SHV_OK;
 }
 

@@ -43,7 +43,8 @@ struct MrgLaunch {
 // Philox4x32-10 bulk fill / Monte Carlo launch. Draw d of handle stream i
 // (d counted from the handle offset o = 4*o_blk + o_lane) is lane
 // (o_lane + d) & 3 of counter block o_blk + ((o_lane + d) >> 2) with
-// ctr = (blk_lo, blk_hi, g_lo, g_hi), g = g0 + i, key = (k0, k1) (R6).
+// ctr = (blk_lo, blk_hi, g_lo, g_hi), g = g0 + i, key = (k0, k1) (R6); with
+// keyed = 1 instead key = (g0 + i, k1) and ctr = (blk_lo, blk_hi, 0, 0).
 struct PhiloxLaunch {
     uint32_t k0, k1;
     uint64_t g0;             // family stream of launch stream 0
@@ -57,6 +58,7 @@ struct PhiloxLaunch {
     uint32_t nseg;
     unsigned long long* hits;
     unsigned long long* counts;
+    uint32_t keyed;          // 1: key = (g0 + i, k1), ctr[2..3] = 0 (SHV_SPACING_KEYED)
 };
 
 struct Grid {
@@ -81,6 +83,8 @@ enum KernelId : int {
     kKMrgMc = 2,
     kKPhiloxFill = 3,
     kKPhiloxMc = 4,
+    kKPhiloxFillKeyed = 5,
+    kKPhiloxMcKeyed = 6,
 };
 cudaError_t max_blocks_per_sm(int kernel, int kind, bool fast, int threads, int* out);
 // Dynamic shared memory of the MRG vector-fill kernel at a block size.

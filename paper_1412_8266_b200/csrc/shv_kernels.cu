@@ -18,7 +18,7 @@
 #include <type_traits>
 #include <cuda_runtime.h>
 
-#include "shv_device.cuh"
+#include "../../include/shv_device.cuh"
 #include "shv_internal.h"
 
 #ifndef SHV_MRG_STEP
@@ -286,6 +286,24 @@ __global__ void __launch_bounds__(256) mrg_mc_kernel(const __grid_constant__ Mrg
     block_reduce_add(total, P.hits);
 }
 
+// Key and counter-stream word of launch stream i. Counter-split layout (R6):
+// key = seed, stream g -> ctr[2..3]. KEYED (Parameterization, P L331-334):
+// key = (stream id, tag), ctr[2..3] = 0.
+template <bool KEYED>
+__device__ __forceinline__ void stream_key(const PhiloxLaunch& P, uint64_t i, uint32_t& k0, uint32_t& k1,
+                                           uint64_t& g)
+{
+    if (KEYED) {
+        k0 = (uint32_t)(P.g0 + i);
+        k1 = P.k1;
+        g = 0;
+    } else {
+        k0 = P.k0;
+        k1 = P.k1;
+        g = P.g0 + i;
+    }
+}
+
 // 8 draws (two blocks) -> one 32-byte chunk of u32 / f32 / f64 values.
 template <int KIND>
 __device__ __forceinline__ void store_chunk(void* o, const W4& a, const W4& d)
@@ -304,7 +322,7 @@ __device__ __forceinline__ void store_chunk(void* o, const W4& a, const W4& d)
 // aligned output. A warp task is (row i, run of 32*R chunks of 32 bytes); lane
 // l handles chunks l, l+32, ... so each store instruction writes 1 KB
 // contiguous. The round-1 product of the stream word is hoisted per task.
-template <int KIND>
+template <int KIND, bool KEYED>
 __global__ void __launch_bounds__(256) philox_fill_fast_kernel(const __grid_constant__ PhiloxLaunch P)
 {
     constexpr uint64_t E = KIND == kF64 ? 4 : 8;  // elements per 32-byte chunk
@@ -318,7 +336,9 @@ __global__ void __launch_bounds__(256) philox_fill_fast_kernel(const __grid_cons
     uint64_t i = task / tpr, kb = task - i * tpr;
     const uint64_t qs = nw / tpr, rs = nw - qs * tpr;
     for (; task < P.items; task += nw) {
-        const uint64_t g = P.g0 + i;
+        uint32_t k0, k1;
+        uint64_t g;
+        stream_key<KEYED>(P, i, k0, k1, g);
         const uint64_t p1 = (uint64_t)kPM1 * (uint32_t)g;  // round-1 product, task-invariant
         const uint64_t c0 = kb * span;
         const uint64_t left = cpr - c0;
@@ -330,13 +350,13 @@ __global__ void __launch_bounds__(256) philox_fill_fast_kernel(const __grid_cons
         // so blk_hi is fixed, round 2's M0 product is hoisted, and the round-1
         // products M0*blk_lo advance by additions (M0*(b+1) = M0*b + M0).
         if ((uint32_t)blk <= 0xFFFFFFFFu - 64u * mine - 1u) {
-            const uint32_t c0r1 = (uint32_t)(p1 >> 32) ^ (uint32_t)(blk >> 32) ^ P.k0;
+            const uint32_t c0r1 = (uint32_t)(p1 >> 32) ^ (uint32_t)(blk >> 32) ^ k0;
             const uint64_t q = (uint64_t)kPM0 * c0r1;
             uint64_t pa = (uint64_t)kPM0 * (uint32_t)blk;
             for (uint32_t r = 0; r < mine; ++r) {
                 const uint64_t pb = add64w(pa, kPM0);
-                const W4 a = philox10_from_r2(pa, q, (uint32_t)p1, (uint32_t)(g >> 32), P.k0, P.k1);
-                const W4 d = philox10_from_r2(pb, q, (uint32_t)p1, (uint32_t)(g >> 32), P.k0, P.k1);
+                const W4 a = philox10_from_r2(pa, q, (uint32_t)p1, (uint32_t)(g >> 32), k0, k1);
+                const W4 d = philox10_from_r2(pb, q, (uint32_t)p1, (uint32_t)(g >> 32), k0, k1);
                 store_chunk<KIND>(o, a, d);
                 pa = add64w(pa, 64ull * kPM0);
                 o += 1024;
@@ -347,9 +367,9 @@ __global__ void __launch_bounds__(256) philox_fill_fast_kernel(const __grid_cons
                 const uint64_t pa = (uint64_t)kPM0 * (uint32_t)blk;
                 const uint64_t pb = (uint64_t)kPM0 * (uint32_t)b1;
                 const W4 a = philox10_from_r1((uint32_t)(pa >> 32), (uint32_t)pa, (uint32_t)(p1 >> 32), (uint32_t)p1,
-                                              (uint32_t)(blk >> 32), (uint32_t)(g >> 32), P.k0, P.k1);
+                                              (uint32_t)(blk >> 32), (uint32_t)(g >> 32), k0, k1);
                 const W4 d = philox10_from_r1((uint32_t)(pb >> 32), (uint32_t)pb, (uint32_t)(p1 >> 32), (uint32_t)p1,
-                                              (uint32_t)(b1 >> 32), (uint32_t)(g >> 32), P.k0, P.k1);
+                                              (uint32_t)(b1 >> 32), (uint32_t)(g >> 32), k0, k1);
                 store_chunk<KIND>(o, a, d);
                 blk = add64(blk, 64u);
                 o += 1024;
@@ -366,7 +386,7 @@ __global__ void __launch_bounds__(256) philox_fill_fast_kernel(const __grid_cons
 
 // Generic Philox fill: any offset, any row length, element-aligned output.
 // Work item = up to 8 consecutive elements of the flat stream-major array.
-template <int KIND>
+template <int KIND, bool KEYED>
 __global__ void __launch_bounds__(256) philox_fill_generic_kernel(const __grid_constant__ PhiloxLaunch P)
 {
     using T = OutT<KIND>;
@@ -377,10 +397,13 @@ __global__ void __launch_bounds__(256) philox_fill_generic_kernel(const __grid_c
         uint64_t e = c * 8;
         uint64_t i = e / P.n;
         uint64_t j = e - i * P.n;
-        PhiloxCursor cur{P.g0 + i, P.k0, P.k1, 0, false, {}};
+        PhiloxCursor cur{0, 0, 0, 0, false, {}};
+        stream_key<KEYED>(P, i, cur.k0, cur.k1, cur.g);
+        uint64_t ci = i;
         for (int u = 0; u < 8 && e < total; ++u, ++e) {
-            if (cur.g != P.g0 + i) {
-                cur.g = P.g0 + i;
+            if (ci != i) {
+                ci = i;
+                stream_key<KEYED>(P, i, cur.k0, cur.k1, cur.g);
                 cur.valid = false;
             }
             const uint64_t d = P.o_lane + j * dpv;  // draw index relative to 4*o_blk
@@ -405,7 +428,7 @@ __global__ void __launch_bounds__(256) philox_fill_generic_kernel(const __grid_c
 
 // Fused Philox Monte Carlo. FAST: offset lane 0 and even segment length, so
 // sample pairs never straddle a counter block (two samples per block).
-template <bool FAST>
+template <bool FAST, bool KEYED>
 __global__ void __launch_bounds__(256) philox_mc_kernel(const __grid_constant__ PhiloxLaunch P)
 {
     const uint64_t nthr = (uint64_t)gridDim.x * blockDim.x;
@@ -413,7 +436,9 @@ __global__ void __launch_bounds__(256) philox_mc_kernel(const __grid_constant__ 
     for (uint64_t it = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; it < P.items; it += nthr) {
         const uint64_t j = it / P.ns;
         const uint64_t i = it - j * P.ns;
-        const uint64_t g = P.g0 + i;
+        uint32_t key0, key1;
+        uint64_t g;
+        stream_key<KEYED>(P, i, key0, key1, g);
         const uint64_t k0 = j * P.seg_len;
         const uint32_t len = (uint32_t)min(P.seg_len, P.n - k0);
         uint32_t h = 0;
@@ -424,11 +449,11 @@ __global__ void __launch_bounds__(256) philox_mc_kernel(const __grid_constant__ 
             if ((uint32_t)b <= 0xFFFFFFFFu - nb - 1u) {
                 // no wrap of the low counter word: hoisted round-2 product,
                 // round-1 products by addition (see philox_fill_fast_kernel)
-                const uint32_t c0r1 = (uint32_t)(p1 >> 32) ^ (uint32_t)(b >> 32) ^ P.k0;
+                const uint32_t c0r1 = (uint32_t)(p1 >> 32) ^ (uint32_t)(b >> 32) ^ key0;
                 const uint64_t q = (uint64_t)kPM0 * c0r1;
                 uint64_t pa = (uint64_t)kPM0 * (uint32_t)b;
                 for (uint32_t r = 0; r < nb; ++r) {
-                    const W4 a = philox10_from_r2(pa, q, (uint32_t)p1, (uint32_t)(g >> 32), P.k0, P.k1);
+                    const W4 a = philox10_from_r2(pa, q, (uint32_t)p1, (uint32_t)(g >> 32), key0, key1);
                     h += hit_fp64(a.x, a.y) + hit_fp64(a.z, a.w);
                     pa = add64w(pa, kPM0);
                 }
@@ -437,17 +462,17 @@ __global__ void __launch_bounds__(256) philox_mc_kernel(const __grid_constant__ 
                 for (uint32_t r = 0; r < nb; ++r) {
                     const uint64_t pa = (uint64_t)kPM0 * (uint32_t)b;
                     const W4 a = philox10_from_r1((uint32_t)(pa >> 32), (uint32_t)pa, (uint32_t)(p1 >> 32),
-                                                  (uint32_t)p1, (uint32_t)(b >> 32), (uint32_t)(g >> 32), P.k0, P.k1);
+                                                  (uint32_t)p1, (uint32_t)(b >> 32), (uint32_t)(g >> 32), key0, key1);
                     h += hit_fp64(a.x, a.y) + hit_fp64(a.z, a.w);
                     b = add64(b, 1u);
                 }
             }
             if (len & 1) {
-                const W4 a = philox_blk(b, g, P.k0, P.k1);
+                const W4 a = philox_blk(b, g, key0, key1);
                 h += hit(a.x, a.y);
             }
         } else {
-            PhiloxCursor cur{g, P.k0, P.k1, 0, false, {}};
+            PhiloxCursor cur{g, key0, key1, 0, false, {}};
             for (uint32_t k = 0; k < len; ++k) {
                 const uint64_t d = P.o_lane + 2 * (k0 + k);
                 const uint32_t w0 = cur.word(P.o_blk + (d >> 2), (uint32_t)(d & 3));
@@ -535,24 +560,35 @@ cudaError_t launch_mrg_mc(const MrgLaunch& p, Grid g, cudaStream_t s)
     return cudaGetLastError();
 }
 
-cudaError_t launch_philox_fill(const PhiloxLaunch& p, int kind, bool fast, Grid g, cudaStream_t s)
+template <bool KEYED>
+cudaError_t launch_philox_fill_t(const PhiloxLaunch& p, int kind, bool fast, Grid g, cudaStream_t s)
 {
     if (fast) {
-        if (kind == kU32) philox_fill_fast_kernel<kU32><<<g.blocks, g.threads, 0, s>>>(p);
-        else if (kind == kF32) philox_fill_fast_kernel<kF32><<<g.blocks, g.threads, 0, s>>>(p);
-        else philox_fill_fast_kernel<kF64><<<g.blocks, g.threads, 0, s>>>(p);
+        if (kind == kU32) philox_fill_fast_kernel<kU32, KEYED><<<g.blocks, g.threads, 0, s>>>(p);
+        else if (kind == kF32) philox_fill_fast_kernel<kF32, KEYED><<<g.blocks, g.threads, 0, s>>>(p);
+        else philox_fill_fast_kernel<kF64, KEYED><<<g.blocks, g.threads, 0, s>>>(p);
     } else {
-        if (kind == kU32) philox_fill_generic_kernel<kU32><<<g.blocks, g.threads, 0, s>>>(p);
-        else if (kind == kF32) philox_fill_generic_kernel<kF32><<<g.blocks, g.threads, 0, s>>>(p);
-        else philox_fill_generic_kernel<kF64><<<g.blocks, g.threads, 0, s>>>(p);
+        if (kind == kU32) philox_fill_generic_kernel<kU32, KEYED><<<g.blocks, g.threads, 0, s>>>(p);
+        else if (kind == kF32) philox_fill_generic_kernel<kF32, KEYED><<<g.blocks, g.threads, 0, s>>>(p);
+        else philox_fill_generic_kernel<kF64, KEYED><<<g.blocks, g.threads, 0, s>>>(p);
     }
     return cudaGetLastError();
 }
 
+cudaError_t launch_philox_fill(const PhiloxLaunch& p, int kind, bool fast, Grid g, cudaStream_t s)
+{
+    return p.keyed ? launch_philox_fill_t<true>(p, kind, fast, g, s) : launch_philox_fill_t<false>(p, kind, fast, g, s);
+}
+
 cudaError_t launch_philox_mc(const PhiloxLaunch& p, bool fast, Grid g, cudaStream_t s)
 {
-    if (fast) philox_mc_kernel<true><<<g.blocks, g.threads, 0, s>>>(p);
-    else philox_mc_kernel<false><<<g.blocks, g.threads, 0, s>>>(p);
+    if (p.keyed) {
+        if (fast) philox_mc_kernel<true, true><<<g.blocks, g.threads, 0, s>>>(p);
+        else philox_mc_kernel<false, true><<<g.blocks, g.threads, 0, s>>>(p);
+    } else {
+        if (fast) philox_mc_kernel<true, false><<<g.blocks, g.threads, 0, s>>>(p);
+        else philox_mc_kernel<false, false><<<g.blocks, g.threads, 0, s>>>(p);
+    }
     return cudaGetLastError();
 }
 
@@ -578,15 +614,25 @@ cudaError_t max_blocks_per_sm(int kernel, int kind, bool fast, int threads, int*
     case kKMrgMc:
         return occ(mrg_mc_kernel, threads, 0, out);
     case kKPhiloxFill:
-        if (kind == kU32) return fast ? occ(philox_fill_fast_kernel<kU32>, threads, 0, out)
-                                      : occ(philox_fill_generic_kernel<kU32>, threads, 0, out);
-        if (kind == kF32) return fast ? occ(philox_fill_fast_kernel<kF32>, threads, 0, out)
-                                      : occ(philox_fill_generic_kernel<kF32>, threads, 0, out);
-        return fast ? occ(philox_fill_fast_kernel<kF64>, threads, 0, out)
-                    : occ(philox_fill_generic_kernel<kF64>, threads, 0, out);
+        if (kind == kU32) return fast ? occ(philox_fill_fast_kernel<kU32, false>, threads, 0, out)
+                                      : occ(philox_fill_generic_kernel<kU32, false>, threads, 0, out);
+        if (kind == kF32) return fast ? occ(philox_fill_fast_kernel<kF32, false>, threads, 0, out)
+                                      : occ(philox_fill_generic_kernel<kF32, false>, threads, 0, out);
+        return fast ? occ(philox_fill_fast_kernel<kF64, false>, threads, 0, out)
+                    : occ(philox_fill_generic_kernel<kF64, false>, threads, 0, out);
+    case kKPhiloxFillKeyed:
+        if (kind == kU32) return fast ? occ(philox_fill_fast_kernel<kU32, true>, threads, 0, out)
+                                      : occ(philox_fill_generic_kernel<kU32, true>, threads, 0, out);
+        if (kind == kF32) return fast ? occ(philox_fill_fast_kernel<kF32, true>, threads, 0, out)
+                                      : occ(philox_fill_generic_kernel<kF32, true>, threads, 0, out);
+        return fast ? occ(philox_fill_fast_kernel<kF64, true>, threads, 0, out)
+                    : occ(philox_fill_generic_kernel<kF64, true>, threads, 0, out);
     case kKPhiloxMc:
-        return fast ? occ(philox_mc_kernel<true>, threads, 0, out)
-                    : occ(philox_mc_kernel<false>, threads, 0, out);
+        return fast ? occ(philox_mc_kernel<true, false>, threads, 0, out)
+                    : occ(philox_mc_kernel<false, false>, threads, 0, out);
+    case kKPhiloxMcKeyed:
+        return fast ? occ(philox_mc_kernel<true, true>, threads, 0, out)
+                    : occ(philox_mc_kernel<false, true>, threads, 0, out);
     }
     return cudaErrorInvalidValue;
 }

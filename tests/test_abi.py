@@ -65,6 +65,11 @@ def test_validation_errors_without_gpu(shv):
         (dict(gen=shv.SHV_GEN_PHILOX4X32_10, seed=[5], first=(1 << 64) - 3, n_streams=4),
          shv.SHV_ERR_INSUFFICIENT_STREAMS),
         (dict(gen=shv.SHV_GEN_MRG32K3A, seed=[5], spacing=9), shv.SHV_ERR_INVALID_ARGUMENT),
+        # keyed Philox (Parameterization): MRG has no keys; one tag word; ids < 2^32
+        (dict(gen=shv.SHV_GEN_MRG32K3A, seed=[5], spacing=2), shv.SHV_ERR_UNSUPPORTED),
+        (dict(gen=shv.SHV_GEN_PHILOX4X32_10, seed=[5, 6], spacing=2), shv.SHV_ERR_INVALID_ARGUMENT),
+        (dict(gen=shv.SHV_GEN_PHILOX4X32_10, seed=[5], spacing=2, first=(1 << 32) - 3, n_streams=4),
+         shv.SHV_ERR_INSUFFICIENT_STREAMS),
     ]
     for kw, code in cases:
         with pytest.raises(E) as ei:

@@ -146,6 +146,27 @@ def test_ragged_offsets_and_replay(shv, orc, gen, sp, kind):
         f.close()
 
 
+@pytest.mark.parametrize("kind", ["u32", "f32", "f64"])
+def test_philox_keyed_mode(shv, orc, kind):
+    """Parameterization (P L331-334): key = (first+i, tag), counter (blk, 0)."""
+    for ns, first, n in ((300, 7, 1024), (33, (1 << 32) - 40, 13), (1, 0, 1000)):
+        f = Fam(shv, W.PHILOX4X32_10, [0xABCD], ns, W.SPACING_KEYED, first)
+        for pre in (0, 3):
+            if pre:
+                shv.shv_jump(f.h, shv.SHV_JUMP_DRAWS, pre)
+                f.offset += pre
+            before = f.offset
+            same(f.gen_(n, kind), f.ref(orc, n, kind, offset=before))
+        hits = torch.zeros(1, dtype=torch.int64, device="cuda")
+        cnt = torch.zeros(ns, dtype=torch.int64, device="cuda")
+        shv.shv_mc_pi_ex(f.h, 501, hits, cnt, None)
+        torch.cuda.synchronize()
+        tot, ref = orc.mc_count(W.PHILOX4X32_10, [0xABCD], ns, 501, first=first,
+                                spacing=W.SPACING_KEYED, offset=f.offset)
+        assert np.array_equal(cnt.cpu().numpy().astype(np.uint64), ref) and int(hits.item()) == tot
+        f.close()
+
+
 @pytest.mark.parametrize("gen,sp", [(W.MRG32K3A, 1), (W.PHILOX4X32_10, 0)])
 def test_generate_twice_equals_generate_2n(shv, gen, sp):
     a = Fam(shv, gen, [99], 1000, sp)

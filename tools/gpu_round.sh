@@ -10,6 +10,6 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --lo
   python bench.py --steps 3 --warmup 3 --no-e2e --no-cpu --no-parts > /dev/null 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"mrg_fill|philox_fill_fast" -s 2 -c 2 \
   -o gpurun_out/prof_fill_$TAG python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu --no-parts > gpurun_out/ncu_full_$TAG.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"mrg_mc|philox_mc" -s 2 -c 4 \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"mrg_mc|philox_mc" -s 2 -c 2 \
   -o gpurun_out/prof_mc_$TAG python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu > gpurun_out/ncu_mc_$TAG.log 2>&1
 ls gpurun_out

@@ -5,7 +5,7 @@
 #include <cstdio>
 #include <cstdint>
 #include <cuda_runtime.h>
-#include "../../paper_1412_8266_b200/csrc/shv_device.cuh"
+#include "../../include/shv_device.cuh"
 using namespace shv::dev;
 
 constexpr int ITER = 2048;  // x 8 steps
