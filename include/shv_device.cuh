@@ -13,6 +13,10 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#ifndef SHV_DECODE_PRED
+#define SHV_DECODE_PRED 0
+#endif
+
 namespace shv {
 namespace dev {
 
@@ -176,9 +180,14 @@ __device__ __forceinline__ uint32_t mrg_fp64(double yb, double yc, double& r_out
     const double k = __dadd_rn(__fma_rn(p, 1.0 / (double)M, kMagic), -kMagic);
     const double r = __fma_rn(-k, (double)M, p);
     r_out = r;
-    uint32_t w = (uint32_t)__double2loint(__dadd_rn(r, kMagic));  // r mod 2^32
-    asm("{\n\t.reg .pred n;\n\tsetp.lt.s32 n, %0, 0;\n\t@n add.u32 %0, %0, %1;\n\t}" : "+r"(w) : "n"(M));
-    return w;
+    const uint32_t w = (uint32_t)__double2loint(__dadd_rn(r, kMagic));  // r mod 2^32
+#if SHV_DECODE_PRED
+    uint32_t c = w;
+    asm("{\n\t.reg .pred n;\n\tsetp.lt.s32 n, %0, 0;\n\t@n add.u32 %0, %0, %1;\n\t}" : "+r"(c) : "n"(M));
+    return c;
+#else
+    return w + ((uint32_t)((int32_t)w >> 31) & M);  // + m if r < 0 (sign mask, no predicate)
+#endif
 }
 
 // Same result with a shorter dependency chain on the recurrence input yb:

@@ -27,7 +27,8 @@ int main(int argc, char** argv)
     void* h = dlopen(argv[1], RTLD_NOW | RTLD_LOCAL);
     if (!h) { printf("dlopen: %s\n", dlerror()); return 1; }
     const int reps = argc > 2 ? atoi(argv[2]) : 10;
-    F(shv_streams_create_ex) F(shv_generate_u32) F(shv_streams_destroy) F(shv_last_error_message) F(shv_generate_f64) F(shv_mc_pi)
+    F(shv_streams_create_ex) F(shv_generate_u32) F(shv_streams_destroy) F(shv_last_error_message) F(shv_generate_f64) F(shv_mc_pi) F(shv_set_launch_config)
+    const unsigned tpb = argc > 3 ? (unsigned)atoi(argv[3]) : 0;
     const uint64_t ns = 1 << 20, n = 4096;
     uint32_t* out; uint32_t* st; unsigned long long* ck;
     cudaMalloc(&out, ns * n * 8); cudaMalloc(&st, 24 * ns); cudaMalloc(&ck, 16);
@@ -40,6 +41,7 @@ int main(int argc, char** argv)
             uint64_t nsk = kind ? ns / 2 : ns;  // f64: 16 GiB
             if (shv_streams_create_ex(&hd, gen, &seed, 1, 0, nsk, gen == 1 ? 1 : 0, gen == 1 ? st : nullptr, 24 * ns, 0, 0)) {
                 printf("create: %s\n", shv_last_error_message()); return 1; }
+            if (tpb) shv_set_launch_config(hd, 0, tpb, 0);
             float best = 1e30f, sum = 0;
             for (int r = 0; r < reps + 2; ++r) {
                 cudaEventRecord(a);
