@@ -174,6 +174,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-parts", action="store_true")
+    ap.add_argument("--small", action="store_true",
+                    help="test mode: 2^14 streams per rank, 2^12 MC samples per stream (not a bench number)")
     ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
                     help="process-group backend (gloo: validate the N>1 logic with ranks sharing a GPU)")
     args = ap.parse_args()
@@ -213,8 +215,14 @@ def main():
 
     stream = torch.cuda.current_stream()
     sp = stream.cuda_stream
-    wm = W.rank_slice(W.C5_MRG, rank, world, weak=True)
-    wp = W.rank_slice(W.C5_PHILOX, rank, world, weak=True)
+    def shrink(w, mc=False):
+        if not args.small:
+            return w
+        return W.Workload(w.name + "-small", w.gen, w.seed, min(w.n_streams, 1 << 14),
+                          min(w.n, 1 << 12) if mc else w.n, w.spacing, w.first)
+
+    wm = W.rank_slice(shrink(W.C5_MRG), rank, world, weak=True)
+    wp = W.rank_slice(shrink(W.C5_PHILOX), rank, world, weak=True)
     n = wm.n
     total_per_rank = wm.n_streams * n  # per generator
     out = torch.empty(total_per_rank, dtype=torch.int32, device=dev)  # 16 GiB
@@ -281,7 +289,8 @@ def main():
 
     # ---- fused Monte Carlo pi (configs[3]) and f64 fill (configs[2]) ----
     if not args.no_parts:
-        for w in (W.C4_MRG, W.C4_PHILOX):
+        for w0 in (W.C4_MRG, W.C4_PHILOX):
+            w = shrink(w0, mc=True)
             ws = W.rank_slice(w, rank, world, weak=False)
             st = torch.empty(6 * ws.n_streams, dtype=torch.int32, device=dev)
             hits = torch.zeros(1, dtype=torch.int64, device=dev)
@@ -312,7 +321,7 @@ def main():
                 "pi_hat": pi_hat, "within_4sigma": abs(pi_hat - math.pi) <= 4 * 4 * math.sqrt(p * (1 - p) / N),
                 "scaling": "strong", "samples": N}
             del st
-        ws = W.rank_slice(W.C3, rank, world, weak=True)
+        ws = W.rank_slice(shrink(W.C3), rank, world, weak=True)
         out64 = out.view(torch.float64)[: ws.n_streams * ws.n // 2]
         # 2^20 x 4096 f64 needs 32 GiB: fill half the rows per launch into the 16 GiB buffer
         half = ws.n_streams // 2

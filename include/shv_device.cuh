@@ -14,7 +14,7 @@
 #include <cuda_runtime.h>
 
 #ifndef SHV_DECODE_PRED
-#define SHV_DECODE_PRED 0
+#define SHV_DECODE_PRED 1
 #endif
 
 namespace shv {
