@@ -59,7 +59,8 @@ typedef enum {
 
 typedef enum {
     SHV_GEN_MRG32K3A = 1,       /* [LEcuyer1999], P L82-86, L250-282 [§4.1] */
-    SHV_GEN_PHILOX4X32_10 = 2   /* [Salmon.etal.2011], P L88-90, L322-336 [§4.3]; variant per S L275 */
+    SHV_GEN_PHILOX4X32_10 = 2,  /* [Salmon.etal.2011], P L88-90, L322-336 [§4.3]; variant per S L275 */
+    SHV_GEN_TINYMT32 = 3        /* [Saito2011], P L287-317 [§4.2]; shv_streams_create_tinymt32 */
 } shv_gen;
 
 typedef enum {
@@ -128,6 +129,27 @@ shv_status shv_streams_create_ex(shv_streams* out, int gen, const uint32_t* seed
  * would leave the stream (Philox 2^66 draws; MRG offset beyond 2^128). */
 shv_status shv_jump(shv_streams h, int kind, uint64_t n);
 
+/* TinyMT32 handles (NEXT-3; P L287-317 [§4.2]; R15) — the paper's hybrid:
+ * one Dynamic Creator parameter set per group of group_size streams ("the
+ * same independent parameterized status is shared among all the threads of a
+ * CUDA block", P L309-313), and inside a group, stream s is slice s of the
+ * group's sequence: 2^64 draws per slice after the authors' init(params, seed)
+ * ("the original stream is sliced in equal chunks", P L313-317).
+ *  params: n_params records (mat1, mat2, tmat), host memory, DC output supplied
+ *    by the caller (P L304-306); family stream g = first+i uses record g/group_size.
+ *  group_size: power of two <= 2^16 (slice starts via GF(2) jump matrices
+ *    built on the device at create).
+ *  d_state: 16*n_streams bytes (SoA, four words per stream) or NULL.
+ * The handle is stateful: generate/mc_pi advance the state buffer in place;
+ * shv_jump(DRAWS, n <= 2^32) advances sequentially on cuda_stream (S L355).
+ * TinyMT f64 values use two draws, like Philox (R7). Errors: params NULL or
+ * n_params 0 -> SHV_ERR_MISSING_PARAMETERS; groups beyond n_params ->
+ * SHV_ERR_INSUFFICIENT_STREAMS. Host-synchronous (waits for seeding). */
+shv_status shv_streams_create_tinymt32(shv_streams* out, const uint32_t* params, size_t n_params,
+                                       uint32_t seed, uint32_t group_size, uint64_t first_stream,
+                                       uint64_t n_streams, void* d_state, size_t state_bytes,
+                                       int device, void* cuda_stream);
+
 /* Bulk fill (P L485-490 [Listing 1] with n_per_stream draws per stream):
  * d_out[i*n + j] = value of draw o+j of stream i (f64 Philox: draws o+2j,
  * o+2j+1), for i < n_streams, j < n; then o += n (Philox f64: 2n). Row-major,
@@ -175,8 +197,11 @@ typedef struct {
     uint32_t key0, key1;          /* Philox key words (keyed: key1 = tag) */
     uint64_t first_stream, n_streams;
     uint64_t offset_lo, offset_hi;
-    const uint32_t* state;        /* MRG: SoA start states (offset 0); NULL for Philox */
+    const uint32_t* state;        /* MRG: SoA start states (offset 0); TinyMT: current states; NULL for Philox */
     uint32_t jump[18];            /* MRG: A1^o (mod m1), A2^o (mod m2), row-major */
+    const uint32_t* params;       /* TinyMT: (mat1, mat2, tmat) per group from group0 */
+    uint64_t group0;              /* TinyMT: first group of the handle */
+    uint32_t group_size, pad_;    /* TinyMT */
 } shv_device_view;
 
 shv_status shv_get_device_view(shv_streams h, shv_device_view* out);

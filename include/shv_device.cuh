@@ -152,17 +152,6 @@ __device__ __forceinline__ uint32_t mrg_next(Mrg& s)
     return mrg_combine(p1, p2);
 }
 
-// Hybrid state: component 2 held as exact binary64 integers.
-struct MrgH {
-    uint32_t x0, x1, x2;
-    double y0, y1, y2;
-};
-
-__device__ __forceinline__ MrgH to_hybrid(const Mrg& s)
-{
-    return MrgH{s.x0, s.x1, s.x2, __uint2double_rn(s.y0), __uint2double_rn(s.y1), __uint2double_rn(s.y2)};
-}
-
 // One component on the FP64 pipe. The state holds *signed* residues
 // y in (-m/2 - 2, m/2 + 2) (or canonical ones, < 2^32, right after a jump):
 // p = a*yb - b*yc is exact (|p| < 2^52.4). k' = fma(p, RN(1/m), 1.5*2^52)
@@ -190,48 +179,14 @@ __device__ __forceinline__ uint32_t mrg_fp64(double yb, double yc, double& r_out
 #endif
 }
 
-// Same result with a shorter dependency chain on the recurrence input yb:
-// q = fma(RN(a/m), yb, RN(-b*yc/m)) approximates p/m to within 2^-31, so
-// k = rint(q) (one FRND) keeps |p/m - k| <= 1/2 + 2^-31; the chain from yb to
-// r is fma -> rint -> fma instead of fma -> fma -> add -> fma.
-template <uint32_t M, uint32_t A, uint32_t B>
-__device__ __forceinline__ uint32_t mrg_fp64_short(double yb, double yc, double& r_out)
-{
-    const double kMagic = 6755399441055744.0;  // 1.5 * 2^52
-    const double t = __dmul_rn((double)B, yc);
-    const double c0 = __dmul_rn(t, -1.0 / (double)M);
-    const double p = __fma_rn((double)A, yb, -t);
-    const double q = __fma_rn((double)A / (double)M, yb, c0);
-    double k;
-    asm("cvt.rni.f64.f64 %0, %1;" : "=d"(k) : "d"(q));
-    const double r = __fma_rn(-k, (double)M, p);
-    r_out = r;
-    uint32_t w = (uint32_t)__double2loint(__dadd_rn(r, kMagic));  // r mod 2^32
-    asm("{\n\t.reg .pred n;\n\tsetp.lt.s32 n, %0, 0;\n\t@n add.u32 %0, %0, %1;\n\t}" : "+r"(w) : "n"(M));
-    return w;
-}
-
 // Component 2: y_n = a21 y_{n-1} - a23n y_{n-3} (mod m2).
 __device__ __forceinline__ uint32_t mrg_c2_fp64(double y0, double y2, double& r_out)
 {
     return mrg_fp64<kM2, kA21, kA23n>(y2, y0, r_out);
 }
 
-__device__ __forceinline__ uint32_t mrg_next(MrgH& s)
-{
-    const uint32_t p1 = mrg_c1(s.x0, s.x1);
-    s.x0 = s.x1;
-    s.x1 = s.x2;
-    s.x2 = p1;
-    double r;
-    const uint32_t p2 = mrg_c2_fp64(s.y0, s.y2, r);
-    s.y0 = s.y1;
-    s.y1 = s.y2;
-    s.y2 = r;
-    return mrg_combine(p1, p2);
-}
-
-// Both components on the FP64 pipe (lab variant).
+// Both components on the FP64 pipe: the product's MRG32k3a step (24 issue
+// slots, 12 of them FP64, per number).
 struct MrgD {
     double x0, x1, x2;
     double y0, y1, y2;
@@ -254,132 +209,6 @@ __device__ __forceinline__ uint32_t mrg_next(MrgD& s)
     s.y0 = s.y1;
     s.y1 = s.y2;
     s.y2 = r2;
-    return mrg_combine(p1, p2);
-}
-
-// Both components on the FP64 pipe, short-chain form (lab variant).
-struct MrgS {
-    double x0, x1, x2;
-    double y0, y1, y2;
-    int pad;
-};
-
-__device__ __forceinline__ MrgS to_fp64s(const Mrg& s)
-{
-    return MrgS{__uint2double_rn(s.x0), __uint2double_rn(s.x1), __uint2double_rn(s.x2),
-                __uint2double_rn(s.y0), __uint2double_rn(s.y1), __uint2double_rn(s.y2), 0};
-}
-
-__device__ __forceinline__ uint32_t mrg_next(MrgS& s)
-{
-    double r1, r2;
-    const uint32_t p1 = mrg_fp64_short<kM1, kA12, kA13n>(s.x1, s.x0, r1);
-    s.x0 = s.x1;
-    s.x1 = s.x2;
-    s.x2 = r1;
-    const uint32_t p2 = mrg_fp64_short<kM2, kA21, kA23n>(s.y2, s.y0, r2);
-    s.y0 = s.y1;
-    s.y1 = s.y2;
-    s.y2 = r2;
-    return mrg_combine(p1, p2);
-}
-
-// Both components on the FP64 pipe with the output word computed on the
-// integer pipe (lab variant "W"): r mod 2^32 = a*wb - b*wc - k*m (mod 2^32),
-// where wb, wc are the previous outputs' residues mod 2^32 and k's low word is
-// read off the magic-rounded k' (k' = 1.5*2^52 + k, ulp 1). 5 FP64 ops and
-// 3 IMAD per component instead of 6 FP64 ops.
-template <uint32_t M, uint32_t A, uint32_t B>
-__device__ __forceinline__ uint32_t mrg_fp64w(double yb, double yc, uint32_t wb, uint32_t wc, double& r_out,
-                                              uint32_t& w_out)
-{
-    const double kMagic = 6755399441055744.0;  // 1.5 * 2^52
-    const double t = __dmul_rn((double)B, yc);
-    const double p = __fma_rn((double)A, yb, -t);
-    const double kk = __fma_rn(p, 1.0 / (double)M, kMagic);
-    const double r = __fma_rn(-__dadd_rn(kk, -kMagic), (double)M, p);
-    r_out = r;
-    const uint32_t klo = (uint32_t)__double2loint(kk);
-    uint32_t w = wb * A - wc * B - klo * M;
-    w_out = w;
-    asm("{\n\t.reg .pred n;\n\tsetp.lt.s32 n, %0, 0;\n\t@n add.u32 %0, %0, %1;\n\t}" : "+r"(w) : "n"(M));
-    return w;
-}
-
-struct MrgW {
-    double x0, x1, x2;
-    double y0, y1, y2;
-    uint32_t u0, u1, u2, v0, v1, v2;  // the same residues mod 2^32
-};
-
-__device__ __forceinline__ MrgW to_fp64w(const Mrg& s)
-{
-    return MrgW{__uint2double_rn(s.x0), __uint2double_rn(s.x1), __uint2double_rn(s.x2),
-                __uint2double_rn(s.y0), __uint2double_rn(s.y1), __uint2double_rn(s.y2),
-                s.x0, s.x1, s.x2, s.y0, s.y1, s.y2};
-}
-
-__device__ __forceinline__ uint32_t mrg_next(MrgW& s)
-{
-    double r1, r2;
-    uint32_t w1, w2;
-    const uint32_t p1 = mrg_fp64w<kM1, kA12, kA13n>(s.x1, s.x0, s.u1, s.u0, r1, w1);
-    s.x0 = s.x1; s.x1 = s.x2; s.x2 = r1;
-    s.u0 = s.u1; s.u1 = s.u2; s.u2 = w1;
-    const uint32_t p2 = mrg_fp64w<kM2, kA21, kA23n>(s.y2, s.y0, s.v2, s.v0, r2, w2);
-    s.y0 = s.y1; s.y1 = s.y2; s.y2 = r2;
-    s.v0 = s.v1; s.v1 = s.v2; s.v2 = w2;
-    return mrg_combine(p1, p2);
-}
-
-// Lab variants of the all-FP64 step: V=2 mask-add decode, V=3 mask-add decode
-// with cvt.rni.s32.f64 instead of the magic-add conversion, V=4 decode via
-// IMAD ((w >> 31) * -m + w).
-template <uint32_t M, uint32_t A, uint32_t B, int V>
-__device__ __forceinline__ uint32_t mrg_fp64v(double yb, double yc, double& r_out)
-{
-    const double kMagic = 6755399441055744.0;  // 1.5 * 2^52
-    const double t = __dmul_rn((double)B, yc);
-    const double p = __fma_rn((double)A, yb, -t);
-    const double k = __dadd_rn(__fma_rn(p, 1.0 / (double)M, kMagic), -kMagic);
-    const double r = __fma_rn(-k, (double)M, p);
-    r_out = r;
-    uint32_t w;
-    if (V == 3) {
-        int32_t i;
-        asm("cvt.rni.s32.f64 %0, %1;" : "=r"(i) : "d"(r));
-        w = (uint32_t)i;
-    } else {
-        w = (uint32_t)__double2loint(__dadd_rn(r, kMagic));
-    }
-    if (V == 4) return (uint32_t)((int32_t)w >> 31) * (0u - M) + w;
-    return w + ((uint32_t)((int32_t)w >> 31) & M);
-}
-
-template <int V>
-struct MrgDV {
-    double x0, x1, x2;
-    double y0, y1, y2;
-    char pad[8 * V];
-};
-
-template <int V>
-__device__ __forceinline__ MrgDV<V> to_fp64v(const Mrg& s)
-{
-    MrgDV<V> d;
-    d.x0 = __uint2double_rn(s.x0); d.x1 = __uint2double_rn(s.x1); d.x2 = __uint2double_rn(s.x2);
-    d.y0 = __uint2double_rn(s.y0); d.y1 = __uint2double_rn(s.y1); d.y2 = __uint2double_rn(s.y2);
-    return d;
-}
-
-template <int V>
-__device__ __forceinline__ uint32_t mrg_next(MrgDV<V>& s)
-{
-    double r1, r2;
-    const uint32_t p1 = mrg_fp64v<kM1, kA12, kA13n, V>(s.x1, s.x0, r1);
-    s.x0 = s.x1; s.x1 = s.x2; s.x2 = r1;
-    const uint32_t p2 = mrg_fp64v<kM2, kA21, kA23n, V>(s.y2, s.y0, r2);
-    s.y0 = s.y1; s.y1 = s.y2; s.y2 = r2;
     return mrg_combine(p1, p2);
 }
 
@@ -507,6 +336,81 @@ struct PhiloxCursor {
         return lane_of(v, lane);
     }
 };
+
+// ------------------------------------------------------------------ TinyMT32
+
+// TinyMT32 [Saito2011] (P L287-317 §4.2): 127-bit F2-linear state in four
+// words plus the parameter set (mat1, mat2, tmat) from Dynamic Creator.
+struct TinyMT {
+    uint32_t s0, s1, s2, s3;
+    uint32_t mat1, mat2, tmat;
+};
+
+__device__ __forceinline__ void tinymt_next_state(TinyMT& t)
+{
+    uint32_t y = t.s3;
+    uint32_t x = (t.s0 & 0x7fffffffu) ^ t.s1 ^ t.s2;
+    x ^= x << 1;
+    y ^= (y >> 1) ^ x;
+    const uint32_t m = 0u - (y & 1u);
+    t.s0 = t.s1;
+    t.s1 = t.s2 ^ (m & t.mat1);
+    t.s2 = x ^ (y << 10) ^ (m & t.mat2);
+    t.s3 = y;
+}
+
+__device__ __forceinline__ uint32_t tinymt_temper(const TinyMT& t)
+{
+    const uint32_t t1 = t.s0 + (t.s2 >> 8);
+    return t.s3 ^ t1 ^ ((0u - (t1 & 1u)) & t.tmat);
+}
+
+__device__ __forceinline__ uint32_t tinymt_next(TinyMT& t)
+{
+    tinymt_next_state(t);
+    return tinymt_temper(t);
+}
+
+// The authors' seeding: 7 rounds of the 1812433253 scramble, period
+// certification ("TINY" if the 127 significant bits are zero), 8 pre-steps.
+__device__ __forceinline__ void tinymt_init(TinyMT& t, uint32_t mat1, uint32_t mat2, uint32_t tmat, uint32_t seed)
+{
+    uint32_t st[4] = {seed, mat1, mat2, tmat};
+#pragma unroll
+    for (int i = 1; i < 8; ++i)
+        st[i & 3] ^= (uint32_t)i + 1812433253u * (st[(i - 1) & 3] ^ (st[(i - 1) & 3] >> 30));
+    if ((st[0] & 0x7fffffffu) == 0 && st[1] == 0 && st[2] == 0 && st[3] == 0) {
+        st[0] = 'T';
+        st[1] = 'I';
+        st[2] = 'N';
+        st[3] = 'Y';
+    }
+    t = TinyMT{st[0], st[1], st[2], st[3], mat1, mat2, tmat};
+#pragma unroll 1
+    for (int i = 0; i < 8; ++i) tinymt_next_state(t);
+}
+
+// y = M x over GF(2) for a 128x128 matrix stored as 128 columns of 4 words
+// (column c = image of unit vector e_c): XOR of the columns x selects.
+__device__ __forceinline__ void gf2_apply(const uint32_t* __restrict__ M, TinyMT& t)
+{
+    const uint32_t x[4] = {t.s0, t.s1, t.s2, t.s3};
+    uint32_t y0 = 0, y1 = 0, y2 = 0, y3 = 0;
+#pragma unroll 4
+    for (int c = 0; c < 128; ++c) {
+        if ((x[c >> 5] >> (c & 31)) & 1u) {
+            const uint4 col = *reinterpret_cast<const uint4*>(M + 4 * c);
+            y0 ^= col.x;
+            y1 ^= col.y;
+            y2 ^= col.z;
+            y3 ^= col.w;
+        }
+    }
+    t.s0 = y0;
+    t.s1 = y1;
+    t.s2 = y2;
+    t.s3 = y3;
+}
 
 // ------------------------------------------------------------------ conversions (R7)
 

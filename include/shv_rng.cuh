@@ -88,4 +88,28 @@ private:
     dev::W4 buf_;
 };
 
+template <>
+class Rng<SHV_GEN_TINYMT32> {
+public:
+    // Stream i: its current state (TinyMT handles are stateful) and the
+    // parameter set of its group.
+    __device__ Rng(const shv_device_view& v, uint64_t i)
+    {
+        const uint32_t* st = v.state;
+        const uint64_t n = v.n_streams;
+        const uint32_t* pr = v.params + 3 * ((v.first_stream + i) / v.group_size - v.group0);
+        t_ = dev::TinyMT{st[i], st[n + i], st[2 * n + i], st[3 * n + i], pr[0], pr[1], pr[2]};
+    }
+    __device__ uint32_t next_u32() { return dev::tinymt_next(t_); }
+    __device__ float next_f32() { return dev::to_f32(next_u32()); }
+    __device__ double next_f64()
+    {
+        const uint32_t lo = next_u32();
+        return dev::philox_f64(lo, next_u32());
+    }
+
+private:
+    dev::TinyMT t_;
+};
+
 }  // namespace shv

@@ -192,6 +192,109 @@ void orc_philox_block(const uint32_t ctr[4], const uint32_t key[2], int rounds, 
 }
 
 /* ------------------------------------------------------------------------ */
+/* TinyMT32 ([Saito2011]: tinymt32.h/.c of the authors' distribution)       */
+/* ------------------------------------------------------------------------ */
+
+#define TINYMT32_MASK 0x7fffffffu
+#define TINYMT32_SH0 1
+#define TINYMT32_SH1 10
+#define TINYMT32_SH8 8
+
+void orc_tinymt32_next_state(orc_tinymt32* t)
+{
+    uint32_t x, y;
+    y = t->st[3];
+    x = (t->st[0] & TINYMT32_MASK) ^ t->st[1] ^ t->st[2];
+    x ^= (x << TINYMT32_SH0);
+    y ^= (y >> TINYMT32_SH0) ^ x;
+    t->st[0] = t->st[1];
+    t->st[1] = t->st[2];
+    t->st[2] = x ^ (y << TINYMT32_SH1);
+    t->st[3] = y;
+    t->st[1] ^= (uint32_t)(-(int32_t)(y & 1)) & t->mat1;
+    t->st[2] ^= (uint32_t)(-(int32_t)(y & 1)) & t->mat2;
+}
+
+uint32_t orc_tinymt32_temper(const orc_tinymt32* t)
+{
+    uint32_t t0, t1;
+    t0 = t->st[3];
+    t1 = t->st[0] + (t->st[2] >> TINYMT32_SH8);
+    t0 ^= t1;
+    t0 ^= (uint32_t)(-(int32_t)(t1 & 1)) & t->tmat;
+    return t0;
+}
+
+uint32_t orc_tinymt32_generate(orc_tinymt32* t)
+{
+    orc_tinymt32_next_state(t);
+    return orc_tinymt32_temper(t);
+}
+
+void orc_tinymt32_init(orc_tinymt32* t, uint32_t mat1, uint32_t mat2, uint32_t tmat, uint32_t seed)
+{
+    t->mat1 = mat1;
+    t->mat2 = mat2;
+    t->tmat = tmat;
+    t->st[0] = seed;
+    t->st[1] = mat1;
+    t->st[2] = mat2;
+    t->st[3] = tmat;
+    for (int i = 1; i < 8; i++)
+        t->st[i & 3] ^= (uint32_t)i + 1812433253u * (t->st[(i - 1) & 3] ^ (t->st[(i - 1) & 3] >> 30));
+    /* period certification: the 127 significant bits must not all be zero */
+    if ((t->st[0] & TINYMT32_MASK) == 0 && t->st[1] == 0 && t->st[2] == 0 && t->st[3] == 0) {
+        t->st[0] = 'T';
+        t->st[1] = 'I';
+        t->st[2] = 'N';
+        t->st[3] = 'Y';
+    }
+    for (int i = 0; i < 8; i++) orc_tinymt32_next_state(t);
+}
+
+/* 128x128 matrices over GF(2): row r is bits r of the image; M[r][w] holds
+ * 32 columns. Column c of T = next_state(e_c), so y = T x is the XOR of the
+ * columns selected by the bits of x. Stored column-major: col[c][4]. */
+typedef struct { uint32_t col[128][4]; } gf2mat;
+
+static void gf2_apply(const gf2mat* M, const uint32_t x[4], uint32_t y[4])
+{
+    uint32_t r[4] = {0, 0, 0, 0};
+    for (int c = 0; c < 128; ++c)
+        if ((x[c >> 5] >> (c & 31)) & 1)
+            for (int w = 0; w < 4; ++w) r[w] ^= M->col[c][w];
+    memcpy(y, r, sizeof r);
+}
+
+static void gf2_mul(const gf2mat* A, const gf2mat* B, gf2mat* C) /* C = A B */
+{
+    gf2mat T;
+    for (int c = 0; c < 128; ++c) gf2_apply(A, B->col[c], T.col[c]);
+    *C = T;
+}
+
+void orc_tinymt32_jump(orc_tinymt32* t, uint64_t e_lo, uint64_t e_hi)
+{
+    gf2mat P, R;
+    memset(&R, 0, sizeof R);
+    for (int c = 0; c < 128; ++c) R.col[c][c >> 5] = 1u << (c & 31); /* identity */
+    for (int c = 0; c < 128; ++c) { /* P = T */
+        orc_tinymt32 u = *t;
+        memset(u.st, 0, sizeof u.st);
+        u.st[c >> 5] = 1u << (c & 31);
+        orc_tinymt32_next_state(&u);
+        memcpy(P.col[c], u.st, sizeof u.st);
+    }
+    u128 e = ((u128)e_hi << 64) | e_lo;
+    while (e) {
+        if (e & 1) gf2_mul(&P, &R, &R);
+        gf2_mul(&P, &P, &P);
+        e >>= 1;
+    }
+    gf2_apply(&R, t->st, t->st);
+}
+
+/* ------------------------------------------------------------------------ */
 /* conversions (R7)                                                          */
 /* ------------------------------------------------------------------------ */
 
@@ -243,6 +346,20 @@ int orc_stream_open(orc_stream* st, int gen, const uint32_t* seed, int nseed,
         orc_mrg_position(base, g, u, off_lo, off_hi, st->s);
         return 0;
     }
+    if (gen == ORC_TINYMT32) {
+        /* seed = {seed, group_size, n_params, params...} (R15) */
+        if (nseed < 6 || spacing != ORC_SPACING_STREAM) return -1;
+        const uint32_t gs = seed[1], np = seed[2];
+        if (gs == 0 || (uint64_t)nseed != 3 + 3ull * np) return -1;
+        const uint64_t g = first + i, group = g / gs, slice = g % gs;
+        if (group >= np) return -1; /* one parameter set per group */
+        const uint32_t* p = seed + 3 + 3 * group;
+        orc_tinymt32_init(&st->tm, p[0], p[1], p[2], seed[0]);
+        /* slice start: 2^64 * slice draws (u128 exponent: slice < 2^64) */
+        orc_tinymt32_jump(&st->tm, 0, slice);
+        orc_tinymt32_jump(&st->tm, off_lo, off_hi);
+        return 0;
+    }
     if (gen == ORC_PHILOX4X32_10) {
         if (off_hi >> 2) return -1; /* a stream holds 2^66 draws (R6) */
         if (spacing == ORC_SPACING_STREAM) {
@@ -280,6 +397,7 @@ int orc_stream_open(orc_stream* st, int gen, const uint32_t* seed, int nseed,
 uint32_t orc_stream_next(orc_stream* st)
 {
     if (st->gen == ORC_MRG32K3A) return orc_mrg_step(st->s);
+    if (st->gen == ORC_TINYMT32) return orc_tinymt32_generate(&st->tm);
     /* SPEC next_word (S L258-266): serve x, y, z, w of the current block,
      * then evaluate the next counter. Counter = (blk_lo, blk_hi, g_lo, g_hi),
      * key = (seed0, seed1) (R6). */
@@ -341,7 +459,7 @@ static void* run_job(void* arg)
                 ((float*)jb->out)[at] = orc_to_f32(orc_stream_next(&st));
             } else if (jb->gen == ORC_MRG32K3A) {
                 ((double*)jb->out)[at] = orc_mrg_to_f64(orc_stream_next(&st));
-            } else {
+            } else { /* Philox and TinyMT32: 53 bits from two consecutive words (R7) */
                 uint32_t lo = orc_stream_next(&st);
                 uint32_t hi = orc_stream_next(&st);
                 ((double*)jb->out)[at] = orc_philox_to_f64(lo, hi);

@@ -19,7 +19,7 @@
 extern "C" {
 #endif
 
-enum { ORC_MRG32K3A = 1, ORC_PHILOX4X32_10 = 2 };
+enum { ORC_MRG32K3A = 1, ORC_PHILOX4X32_10 = 2, ORC_TINYMT32 = 3 };
 enum { ORC_SPACING_STREAM = 0, ORC_SPACING_SUBSTREAM = 1, ORC_SPACING_KEYED = 2 };
 enum { ORC_U32 = 0, ORC_F32 = 1, ORC_F64 = 2 };
 
@@ -44,6 +44,21 @@ void orc_mrg_position(const uint32_t seed[6], uint64_t g, uint64_t u,
 void orc_philox_block(const uint32_t ctr[4], const uint32_t key[2], int rounds,
                       uint32_t out[4]);
 
+/* ---- TinyMT32 (P L287-317 §4.2; algorithm from [Saito2011], P L292) ---- */
+/* State: status[4] plus the parameter set (mat1, mat2, tmat). */
+typedef struct {
+    uint32_t st[4];
+    uint32_t mat1, mat2, tmat;
+} orc_tinymt32;
+void orc_tinymt32_init(orc_tinymt32* t, uint32_t mat1, uint32_t mat2, uint32_t tmat, uint32_t seed);
+void orc_tinymt32_next_state(orc_tinymt32* t);
+uint32_t orc_tinymt32_temper(const orc_tinymt32* t);
+uint32_t orc_tinymt32_generate(orc_tinymt32* t); /* next_state then temper */
+/* The transition is linear over GF(2) on the 128 status bits: jump e steps
+ * by applying T^e, T built column by column from next_state of unit vectors
+ * (e = e_hi*2^64 + e_lo, square-and-multiply; R15). */
+void orc_tinymt32_jump(orc_tinymt32* t, uint64_t e_lo, uint64_t e_hi);
+
 /* ---- conversions (R7) ---- */
 float orc_to_f32(uint32_t w);
 double orc_mrg_to_f64(uint32_t z);
@@ -54,6 +69,7 @@ typedef struct {
     int gen;
     uint32_t s[6];        /* MRG32k3a state */
     uint32_t key[2];      /* Philox key (R6) */
+    orc_tinymt32 tm;      /* TinyMT32 state and parameters */
     uint64_t g;           /* Philox stream index -> ctr[2..3] (R6) */
     uint64_t blk;         /* Philox next counter block -> ctr[0..1] (R6) */
     uint32_t buf[4];      /* Philox lanes not yet served (S L258-266) */
@@ -61,7 +77,12 @@ typedef struct {
 } orc_stream;
 
 /* Open handle-stream i of a (gen, seed, first, spacing) family at draw offset
- * (off_hi:off_lo). Returns 0 on success, -1 on invalid arguments. */
+ * (off_hi:off_lo). Returns 0 on success, -1 on invalid arguments.
+ * TinyMT32 (R15): seed = {seed, group_size, n_params, mat1_0, mat2_0, tmat_0,
+ * mat1_1, ...} (nseed = 3 + 3*n_params); family stream g = first + i lies in
+ * group g / group_size, which uses parameter set g / group_size (one set per
+ * group, P L309-313), and is slice g % group_size of that group's sequence,
+ * i.e. starts 2^64 * (g % group_size) draws after init(params, seed). */
 int orc_stream_open(orc_stream* st, int gen, const uint32_t* seed, int nseed,
                     uint64_t first, uint64_t i, int spacing,
                     uint64_t off_lo, uint64_t off_hi);

@@ -28,6 +28,7 @@ SHV_ERR_CUDA = 9
 
 SHV_GEN_MRG32K3A = 1
 SHV_GEN_PHILOX4X32_10 = 2
+SHV_GEN_TINYMT32 = 3
 SHV_SPACING_STREAM = 0
 SHV_SPACING_SUBSTREAM = 1
 SHV_SPACING_KEYED = 2
@@ -42,6 +43,7 @@ EXPORTS = (
     "shv_mc_pi", "shv_mc_pi_ex", "shv_get_position", "shv_streams_destroy",
     "shv_status_string", "shv_last_error_message", "shv_set_launch_config",
     "shv_partition", "shv_jump_matrix", "shv_build_info", "shv_get_device_view",
+    "shv_streams_create_tinymt32",
 )
 
 
@@ -61,7 +63,8 @@ class shv_device_view(C.Structure):
     _fields_ = [("gen", C.c_uint32), ("spacing", C.c_uint32), ("key0", C.c_uint32),
                 ("key1", C.c_uint32), ("first_stream", C.c_uint64), ("n_streams", C.c_uint64),
                 ("offset_lo", C.c_uint64), ("offset_hi", C.c_uint64), ("state", C.c_void_p),
-                ("jump", C.c_uint32 * 18)]
+                ("jump", C.c_uint32 * 18), ("params", C.c_void_p), ("group0", C.c_uint64),
+                ("group_size", C.c_uint32), ("pad_", C.c_uint32)]
 
 
 LIB_PATH = _build.LIB
@@ -94,6 +97,8 @@ def _load():
         "shv_jump_matrix": (st, [u64, u64, u32p]),
         "shv_build_info": (C.c_char_p, []),
         "shv_get_device_view": (st, [u64, C.POINTER(shv_device_view)]),
+        "shv_streams_create_tinymt32": (st, [C.POINTER(u64), u32p, C.c_size_t, C.c_uint32, C.c_uint32,
+                                             u64, u64, vp, C.c_size_t, C.c_int, vp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -152,6 +157,21 @@ def shv_streams_create_ex(gen: int, seed, first_stream: int, n_streams: int, spa
         state_bytes = d_state.numel() * d_state.element_size()
     _check(lib.shv_streams_create_ex(C.byref(h), gen, arr, nw, first_stream, n_streams, spacing,
                                      _ptr(d_state), state_bytes, device, _stream(stream)))
+    return h.value
+
+
+def shv_streams_create_tinymt32(params, seed: int, group_size: int, first_stream: int,
+                                n_streams: int, d_state=None, state_bytes: int = 0, device: int = -1,
+                                stream=None) -> int:
+    """params: sequence of (mat1, mat2, tmat) records, one per group."""
+    flat = [int(w) for rec in params for w in rec]
+    arr = (C.c_uint32 * max(1, len(flat)))(*flat)
+    h = C.c_uint64(0)
+    if d_state is not None and not isinstance(d_state, int) and not state_bytes:
+        state_bytes = d_state.numel() * d_state.element_size()
+    _check(lib.shv_streams_create_tinymt32(C.byref(h), arr if flat else None, len(flat) // 3, seed,
+                                           group_size, first_stream, n_streams, _ptr(d_state),
+                                           state_bytes, device, _stream(stream)))
     return h.value
 
 

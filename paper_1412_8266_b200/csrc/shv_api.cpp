@@ -152,7 +152,25 @@ struct Handle {
     uint32_t bps = 0, tpb = 256;
     uint64_t seg = 0;
     int sms = 0;
+    // TinyMT32 (stateful; R15)
+    uint32_t* params = nullptr;  // owned, (mat1, mat2, tmat) per group from group0
+    uint64_t group0 = 0;
+    uint32_t group_size = 0;
+    cudaStream_t home = nullptr;  // stream of create: TinyMT jumps are enqueued there
 };
+
+TinyMtLaunch tm_launch(const Handle& h, uint64_t s0, uint64_t ns)
+{
+    TinyMtLaunch P{};
+    P.state = h.state + s0;
+    P.stride = h.n;
+    P.ns = ns;
+    P.params = h.params;
+    P.first = h.first + s0;
+    P.group0 = h.group0;
+    P.group_size = h.group_size;
+    return P;
+}
 
 std::mutex g_mu;
 std::unordered_map<uint64_t, std::shared_ptr<Handle>> g_handles;
@@ -296,7 +314,7 @@ shv_status generate(shv_streams hid, T* out, uint64_t n, void* stream, int kind,
     if ((uintptr_t)out % sizeof(T)) return fail(SHV_ERR_MISALIGNED, "output not %zu-byte aligned", sizeof(T));
     if (n == 0) return SHV_OK;
     if (h.n > UINT64_MAX / n / sizeof(T)) return fail(SHV_ERR_INVALID_ARGUMENT, "size overflow");
-    const uint64_t dpv = (h.gen == SHV_GEN_PHILOX4X32_10 && kind == kF64) ? 2 : 1;
+    const uint64_t dpv = (h.gen != SHV_GEN_MRG32K3A && kind == kF64) ? 2 : 1;
     shv_status st = check_advance(h, (u128)n * dpv);
     if (st) return st;
     DeviceGuard dg(h.device);
@@ -331,7 +349,15 @@ shv_status generate(shv_streams hid, T* out, uint64_t n, void* stream, int kind,
         T* dst = host_out ? stage[k & 1] : out;
         if (host_out && k >= 2) err = cudaStreamWaitEvent(s, copy_done[k & 1], 0);
         if (err != cudaSuccess) break;
-        if (h.gen == SHV_GEN_MRG32K3A) {
+        if (h.gen == SHV_GEN_TINYMT32) {
+            const bool vec = aligned32 && (n % 8 == 0) && n <= 0xFFFFFFFFull;
+            TinyMtLaunch P = tm_launch(h, s0, ns);
+            P.out = dst;
+            P.n = n;
+            const unsigned full = (unsigned)((ns + h.tpb - 1) / h.tpb);
+            Grid g{vec ? blocks_for(h, kKTinyFill, kind, true, ns) : full, h.tpb};
+            err = launch_tinymt_fill(P, kind, vec, g, s);
+        } else if (h.gen == SHV_GEN_MRG32K3A) {
             bool vec = aligned32 && (n % 8 == 0);
             auto P = std::make_unique<MrgLaunch>();
             P->state = h.state;
@@ -435,6 +461,8 @@ shv_status validate_seed(int gen, const uint32_t* seed, size_t words, uint32_t o
         out[1] = words == 2 ? seed[1] : 0;
         return SHV_OK;
     }
+    if (gen == SHV_GEN_TINYMT32)
+        return fail(SHV_ERR_MISSING_PARAMETERS, "TinyMT32 handles come from shv_streams_create_tinymt32");
     return fail(SHV_ERR_INVALID_ARGUMENT, "unknown generator %d", gen);
 }
 
@@ -447,9 +475,86 @@ extern "C" {
 
 size_t shv_state_bytes(int gen, uint64_t n_streams)
 {
-    if (gen != SHV_GEN_MRG32K3A) return 0;
-    if (n_streams > SIZE_MAX / 24) return 0;
-    return (size_t)(24 * n_streams);
+    const uint64_t per = gen == SHV_GEN_MRG32K3A ? 24 : gen == SHV_GEN_TINYMT32 ? 16 : 0;
+    if (!per || n_streams > SIZE_MAX / per) return 0;
+    return (size_t)(per * n_streams);
+}
+
+shv_status shv_streams_create_tinymt32(shv_streams* out, const uint32_t* params, size_t n_params, uint32_t seed,
+                                       uint32_t group_size, uint64_t first_stream, uint64_t n_streams, void* d_state,
+                                       size_t state_bytes, int device, void* cuda_stream)
+{
+    if (!out) return fail(SHV_ERR_INVALID_ARGUMENT, "NULL out handle");
+    *out = 0;
+    if (!params || n_params == 0)
+        return fail(SHV_ERR_MISSING_PARAMETERS, "TinyMT32 needs Dynamic Creator parameter sets (P L304-306)");
+    if (n_streams == 0) return fail(SHV_ERR_INVALID_ARGUMENT, "n_streams must be >= 1");
+    if (group_size == 0 || (group_size & (group_size - 1)) || group_size > (1u << 16))
+        return fail(SHV_ERR_INVALID_ARGUMENT, "group_size must be a power of two <= 2^16");
+    const u128 end = (u128)first_stream + n_streams;
+    if (end > ((u128)1 << 64)) return fail(SHV_ERR_INSUFFICIENT_STREAMS, "streams end at 2^64");
+    const uint64_t g0 = first_stream / group_size, g1 = (uint64_t)((end - 1) / group_size);
+    if (g1 >= n_params)
+        return fail(SHV_ERR_INSUFFICIENT_STREAMS, "streams need %llu parameter sets, %zu given (one per group)",
+                    (unsigned long long)(g1 + 1), n_params);
+    const size_t need = shv_state_bytes(SHV_GEN_TINYMT32, n_streams);
+    if (need == 0) return fail(SHV_ERR_INVALID_ARGUMENT, "state size overflow");
+    if (d_state && state_bytes < need) return fail(SHV_ERR_INVALID_ARGUMENT, "state buffer %zu B < %zu B", state_bytes, need);
+    if (d_state && ((uintptr_t)d_state & 3)) return fail(SHV_ERR_MISALIGNED, "state not 4-byte aligned");
+    int dev = device;
+    if (dev < 0) {
+        cudaError_t e = cudaGetDevice(&dev);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+    }
+    DeviceGuard dg(dev);
+    if (dg.err != cudaSuccess) return cuda_fail(dg.err, "cudaSetDevice");
+    auto h = std::make_shared<Handle>();
+    h->gen = SHV_GEN_TINYMT32;
+    h->spacing = SHV_SPACING_STREAM;
+    h->device = dev;
+    h->seed[0] = seed;
+    h->seed[1] = group_size;
+    h->first = first_stream;
+    h->n = n_streams;
+    h->group0 = g0;
+    h->group_size = group_size;
+    h->home = (cudaStream_t)cuda_stream;
+    cudaStream_t s = (cudaStream_t)cuda_stream;
+    cudaError_t e = cudaDeviceGetAttribute(&h->sms, cudaDevAttrMultiProcessorCount, dev);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaDeviceGetAttribute");
+    const uint64_t ng = g1 - g0 + 1;
+    e = cudaMalloc((void**)&h->params, 12 * ng);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(params)");
+    e = cudaMemcpyAsync(h->params, params + 3 * g0, 12 * ng, cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess && d_state) {
+        h->state = (uint32_t*)d_state;
+    } else if (e == cudaSuccess) {
+        e = cudaMalloc((void**)&h->state, need);
+        h->own_state = e == cudaSuccess;
+    }
+    int log2_gs = 0;
+    while ((1u << log2_gs) < group_size) ++log2_gs;
+    uint32_t* tables = nullptr;
+    if (e == cudaSuccess && log2_gs > 0) e = cudaMallocAsync((void**)&tables, (size_t)ng * log2_gs * 2048, s);
+    if (e == cudaSuccess) e = launch_tinymt_prep(h->params, ng, log2_gs, tables, s);
+    if (e == cudaSuccess) {
+        TinyMtLaunch P = tm_launch(*h, 0, n_streams);
+        e = launch_tinymt_seed(P, seed, tables, log2_gs, Grid{(unsigned)((n_streams + 255) / 256), 256}, s);
+    }
+    if (tables) cudaFreeAsync(tables, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);  // the host params copy must complete
+    if (e != cudaSuccess) {
+        if (h->own_state) cudaFree(h->state);
+        cudaFree(h->params);
+        return cuda_fail(e, "tinymt32 create");
+    }
+    const uint64_t id = g_next_id.fetch_add(1);
+    {
+        std::lock_guard<std::mutex> lk(g_mu);
+        g_handles[id] = h;
+    }
+    *out = id;
+    return SHV_OK;
 }
 
 shv_status shv_streams_create_ex(shv_streams* out, int gen, const uint32_t* seed, size_t seed_words,
@@ -550,6 +655,21 @@ shv_status shv_jump(shv_streams hid, int kind, uint64_t n)
     if (!hp) return fail(SHV_ERR_LIFECYCLE, "unknown or destroyed handle");
     Handle& h = *hp;
     u128 d;
+    if (h.gen == SHV_GEN_TINYMT32) {
+        // sequential advance on the device (S L355), on the create stream
+        if (kind != SHV_JUMP_DRAWS) return fail(SHV_ERR_UNSUPPORTED, "TinyMT32 jumps by draws only");
+        if (n > 0xFFFFFFFFull) return fail(SHV_ERR_INVALID_ARGUMENT, "TinyMT32 advances at most 2^32 draws per jump");
+        if (n == 0) return SHV_OK;
+        DeviceGuard dg(h.device);
+        if (dg.err != cudaSuccess) return cuda_fail(dg.err, "cudaSetDevice");
+        TinyMtLaunch P = tm_launch(h, 0, h.n);
+        P.steps = n;
+        Grid g{(unsigned)((h.n + 255) / 256), 256};
+        cudaError_t e = launch_tinymt_advance(P, g, h.home);
+        if (e != cudaSuccess) return cuda_fail(e, "tinymt advance");
+        h.offset += n;
+        return SHV_OK;
+    }
     if (kind == SHV_JUMP_DRAWS) {
         d = n;
     } else if (kind == SHV_JUMP_SUBSTREAMS || kind == SHV_JUMP_STREAMS) {
@@ -600,7 +720,14 @@ shv_status shv_mc_pi_ex(shv_streams hid, uint64_t samples, uint64_t* d_hits, uin
     cudaStream_t s = (cudaStream_t)stream;
     cudaError_t err;
     const uint64_t cap = 1ull << 31;  // per-item count fits in u32
-    if (h.gen == SHV_GEN_MRG32K3A) {
+    if (h.gen == SHV_GEN_TINYMT32) {
+        TinyMtLaunch P = tm_launch(h, 0, h.n);
+        P.n = samples;
+        P.hits = (unsigned long long*)d_hits;
+        P.counts = (unsigned long long*)d_counts;
+        Grid g{(unsigned)((h.n + h.tpb - 1) / h.tpb), h.tpb};
+        err = launch_tinymt_mc(P, g, s);
+    } else if (h.gen == SHV_GEN_MRG32K3A) {
         auto P = std::make_unique<MrgLaunch>();
         P->state = h.state;
         P->stride = h.n;
@@ -675,7 +802,12 @@ shv_status shv_get_device_view(shv_streams hid, shv_device_view* out)
     out->n_streams = h.n;
     out->offset_lo = (uint64_t)h.offset;
     out->offset_hi = (uint64_t)(h.offset >> 64);
-    if (h.gen == SHV_GEN_MRG32K3A) {
+    if (h.gen == SHV_GEN_TINYMT32) {
+        out->state = h.state;  // current states (stateful handle)
+        out->params = h.params;
+        out->group0 = h.group0;
+        out->group_size = h.group_size;
+    } else if (h.gen == SHV_GEN_MRG32K3A) {
         out->state = h.state;
         const MatPair J = pair_pow(h.offset, 0);
         memcpy(out->jump, J.a, 36);
@@ -694,9 +826,10 @@ shv_status shv_streams_destroy(shv_streams hid)
         h = it->second;
         g_handles.erase(it);
     }
-    if (h->own_state && h->state) {
+    if ((h->own_state && h->state) || h->params) {
         DeviceGuard dg(h->device);
-        cudaFree(h->state);
+        if (h->own_state && h->state) cudaFree(h->state);
+        if (h->params) cudaFree(h->params);
     }
     return SHV_OK;
 }

@@ -61,12 +61,39 @@ struct PhiloxLaunch {
     uint32_t keyed;          // 1: key = (g0 + i, k1), ctr[2..3] = 0 (SHV_SPACING_KEYED)
 };
 
+// TinyMT32 launch (NEXT-3; R15). Stateful: the SoA state buffer holds every
+// stream's current state and each launch writes it back. Family stream
+// g = first + i belongs to group g / group_size, whose parameter set is
+// params[3 * (g / group_size - group0) ..].
+struct TinyMtLaunch {
+    uint32_t* state;          // SoA: word k of stream i at state[k*stride + i]
+    uint64_t stride;          // handle n_streams
+    uint64_t ns;              // streams in this launch (from stream 0)
+    const uint32_t* params;   // (mat1, mat2, tmat) per group from group0
+    uint64_t first;
+    uint64_t group0;
+    uint32_t group_size;
+    void* out;                // fill: row i at out + i*n elements
+    uint64_t n;               // values per row (fill) or samples (MC)
+    uint64_t steps;           // advance kernel: draws to skip
+    unsigned long long* hits;
+    unsigned long long* counts;
+};
+
 struct Grid {
     unsigned blocks;
     unsigned threads;
 };
 
 // ---- launchers (shv_kernels.cu) ----
+// TinyMT32: tables[g][b] = (T_g^(2^64))^(2^b), 128 columns x 4 words each.
+cudaError_t launch_tinymt_prep(const uint32_t* params, uint64_t n_groups, int log2_gs, uint32_t* tables,
+                               cudaStream_t s);
+cudaError_t launch_tinymt_seed(const TinyMtLaunch& p, uint32_t seed, const uint32_t* tables, int log2_gs,
+                               Grid g, cudaStream_t s);
+cudaError_t launch_tinymt_fill(const TinyMtLaunch& p, int kind, bool vec, Grid g, cudaStream_t s);
+cudaError_t launch_tinymt_advance(const TinyMtLaunch& p, Grid g, cudaStream_t s);
+cudaError_t launch_tinymt_mc(const TinyMtLaunch& p, Grid g, cudaStream_t s);
 cudaError_t upload_jump_tables(const MatPair* sub51, const MatPair* str64);
 // T = g.blocks * g.threads seeding threads; step = A^(T * spacing).
 cudaError_t launch_mrg_seed(uint32_t* state, uint64_t n, const uint32_t base[6], int table,
@@ -85,6 +112,8 @@ enum KernelId : int {
     kKPhiloxMc = 4,
     kKPhiloxFillKeyed = 5,
     kKPhiloxMcKeyed = 6,
+    kKTinyFill = 7,
+    kKTinyMc = 8,
 };
 cudaError_t max_blocks_per_sm(int kernel, int kind, bool fast, int threads, int* out);
 // Dynamic shared memory of the MRG vector-fill kernel at a block size.

@@ -9,8 +9,8 @@
 // a contraction. Generator arithmetic lives in shv_device.cuh.
 //
 // Compile-time variants (the kernel lab, tools/lab/, builds each):
-//   SHV_MRG_STEP  0 = all-integer step, 1 = hybrid (component 2 on the FP64 pipe),
-//                 2 = both components on the FP64 pipe (default; fastest measured)
+//   SHV_MRG_STEP  0 = all-integer step, 2 = both components on the FP64 pipe
+//                 (default; fastest measured; other forms live in tools/lab/)
 //   SHV_MRG_STAGE 0 = each lane stores its own row directly, 1 = lanes stage 64
 //                 values in shared memory and the warp writes 256-byte runs
 #include <atomic>
@@ -45,9 +45,6 @@ using OutT = typename std::conditional<KIND == kF64, double,
 #if SHV_MRG_STEP == 2
 using Gen = MrgD;
 __device__ __forceinline__ Gen make_gen(const Mrg& s) { return to_fp64(s); }
-#elif SHV_MRG_STEP == 1
-using Gen = MrgH;
-__device__ __forceinline__ Gen make_gen(const Mrg& s) { return to_hybrid(s); }
 #else
 using Gen = Mrg;
 __device__ __forceinline__ Gen make_gen(const Mrg& s) { return s; }
@@ -123,6 +120,64 @@ __device__ __forceinline__ void stage8(uint4* wb, unsigned lane, unsigned q0, Ge
     }
 }
 
+// Write one staged round of the warp: lane L's cnt values (kRB bytes at most)
+// go to row_L + r values; each store instruction covers 1024/kRB source lanes
+// x kRB contiguous bytes.
+template <typename T>
+__device__ __forceinline__ void write_round(const uint4* wb, unsigned lane, uint32_t r, uint32_t cnt, uint64_t row)
+{
+    __syncwarp();
+#pragma unroll
+    for (unsigned k = 0; k < kRB / 32; ++k) {
+        const unsigned src = (1024 / kRB) * k + lane / (kRB / 32), p = lane % (kRB / 32);
+        const uint32_t scnt = __shfl_sync(0xffffffffu, cnt, src);
+        const uint64_t srow = __shfl_sync(0xffffffffu, row, src);
+        if (32 * p < scnt * sizeof(T))
+            st_v8(reinterpret_cast<char*>(srow) + (uint64_t)r * sizeof(T) + 32 * p, wb[slot(src, 2 * p)],
+                  wb[slot(src, 2 * p + 1)]);
+    }
+    __syncwarp();
+}
+
+// TinyMT32: 8 values -> staging pieces (u32/f32: 8 words; f64: 16 words, two
+// per value like Philox, R7/R15).
+template <int KIND>
+__device__ __forceinline__ void stage8_tm(uint4* wb, unsigned lane, unsigned q0, TinyMT& t)
+{
+    if (KIND == kF64) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const uint32_t a0 = tinymt_next(t), a1 = tinymt_next(t), b0 = tinymt_next(t), b1 = tinymt_next(t);
+            const double a = philox_f64(a0, a1), b = philox_f64(b0, b1);
+            wb[slot(lane, q0 + u)] = make_uint4(__double2loint(a), __double2hiint(a), __double2loint(b),
+                                                __double2hiint(b));
+        }
+    } else {
+        uint32_t v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = tinymt_next(t);
+        wb[slot(lane, q0)] = pack4<KIND>(v[0], v[1], v[2], v[3]);
+        wb[slot(lane, q0 + 1)] = pack4<KIND>(v[4], v[5], v[6], v[7]);
+    }
+}
+
+__device__ __forceinline__ TinyMT tm_load(const TinyMtLaunch& P, uint64_t i)
+{
+    const uint64_t n = P.stride;
+    const uint32_t* pr = P.params + 3 * ((P.first + i) / P.group_size - P.group0);
+    return TinyMT{__ldg(P.state + i), __ldg(P.state + n + i), __ldg(P.state + 2 * n + i),
+                  __ldg(P.state + 3 * n + i), __ldg(pr), __ldg(pr + 1), __ldg(pr + 2)};
+}
+
+__device__ __forceinline__ void tm_store(const TinyMtLaunch& P, uint64_t i, const TinyMT& t)
+{
+    const uint64_t n = P.stride;
+    P.state[i] = t.s0;
+    P.state[n + i] = t.s1;
+    P.state[2 * n + i] = t.s2;
+    P.state[3 * n + i] = t.s3;
+}
+
 // ================================================================== kernels
 
 // Per-stream start states (row a3). Thread t of T handles streams t, t+T,
@@ -190,18 +245,7 @@ __global__ void __launch_bounds__(256, SHV_MRG_MINB) mrg_fill_vec_kernel(const _
             } else {
                 for (unsigned g = 0; g < cnt / 8; ++g) stage8<KIND>(wb, lane, g * (KIND == kF64 ? 4 : 2), s);
             }
-            __syncwarp();
-#pragma unroll
-            for (unsigned k = 0; k < kRB / 32; ++k) {
-                // each instruction: 1024/kRB source lanes x kRB contiguous bytes
-                const unsigned src = (1024 / kRB) * k + lane / (kRB / 32), p = lane % (kRB / 32);
-                const uint32_t scnt = __shfl_sync(0xffffffffu, cnt, src);
-                const uint64_t srow = __shfl_sync(0xffffffffu, row, src);
-                if (32 * p < scnt * sizeof(T))
-                    st_v8(reinterpret_cast<char*>(srow) + (uint64_t)r * sizeof(T) + 32 * p,
-                          wb[slot(src, 2 * p)], wb[slot(src, 2 * p + 1)]);
-            }
-            __syncwarp();
+            write_round<T>(wb, lane, r, cnt, row);
         }
     }
 #else
@@ -486,6 +530,135 @@ __global__ void __launch_bounds__(256) philox_mc_kernel(const __grid_constant__ 
     block_reduce_add(total, P.hits);
 }
 
+
+// ------------------------------------------------------------------ TinyMT32 (NEXT-3)
+
+// One block of 128 threads per parameter set: thread c builds column c of the
+// transition T (next_state of unit vector e_c), then the block squares the
+// matrix 64 times (T^(2^64), the slice length) and log2_gs - 1 more times,
+// storing (T^(2^64))^(2^b) for b < log2_gs.
+__global__ void __launch_bounds__(128) tinymt_prep_kernel(const uint32_t* __restrict__ params, int log2_gs,
+                                                          uint32_t* __restrict__ tables)
+{
+    __shared__ uint4 M[128], N[128];
+    const unsigned c = threadIdx.x;
+    const uint32_t* pr = params + 3 * blockIdx.x;
+    TinyMT t{0, 0, 0, 0, pr[0], pr[1], pr[2]};
+    (c < 32 ? t.s0 : c < 64 ? t.s1 : c < 96 ? t.s2 : t.s3) = 1u << (c & 31);
+    tinymt_next_state(t);
+    M[c] = make_uint4(t.s0, t.s1, t.s2, t.s3);
+    __syncthreads();
+    for (int k = 0; k < 64 + log2_gs; ++k) {
+        if (k >= 64) {  // M = (T^(2^64))^(2^(k-64)): emit table entry k-64
+            reinterpret_cast<uint4*>(tables)[((size_t)blockIdx.x * log2_gs + (k - 64)) * 128 + c] = M[c];
+            if (k == 64 + log2_gs - 1) break;
+        }
+        const uint4 x = M[c];  // column c of M*M = M applied to column c of M
+        const uint32_t xs[4] = {x.x, x.y, x.z, x.w};
+        uint4 y = make_uint4(0, 0, 0, 0);
+        for (int b = 0; b < 128; ++b)
+            if ((xs[b >> 5] >> (b & 31)) & 1u) {
+                const uint4 col = M[b];
+                y.x ^= col.x;
+                y.y ^= col.y;
+                y.z ^= col.z;
+                y.w ^= col.w;
+            }
+        N[c] = y;
+        __syncthreads();
+        M[c] = N[c];
+        __syncthreads();
+    }
+}
+
+// Stream i: init(params of its group, seed), then slice s = g % group_size
+// via the per-bit tables (popcount(s) GF(2) mat-vecs).
+__global__ void __launch_bounds__(256) tinymt_seed_kernel(const TinyMtLaunch P, uint32_t seed,
+                                                          const uint32_t* __restrict__ tables, int log2_gs)
+{
+    const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= P.ns) return;
+    const uint64_t g = P.first + i;
+    const uint64_t grp = g / P.group_size - P.group0;
+    const uint32_t* pr = P.params + 3 * grp;
+    TinyMT t;
+    tinymt_init(t, pr[0], pr[1], pr[2], seed);
+    const uint32_t slice = (uint32_t)(g % P.group_size);
+    for (int b = 0; b < log2_gs; ++b)
+        if ((slice >> b) & 1u) gf2_apply(tables + ((size_t)grp * log2_gs + b) * 512, t);
+    tm_store(P, i, t);
+}
+
+// Vector fill: one stream per lane, staged 256-byte runs (as the MRG kernel).
+template <int KIND>
+__global__ void __launch_bounds__(256, 4) tinymt_fill_vec_kernel(const __grid_constant__ TinyMtLaunch P)
+{
+    using T = OutT<KIND>;
+    const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    extern __shared__ uint4 smem[];
+    uint4* wb = smem + warp * (32 * kPieces);
+    constexpr uint32_t G = kRB / sizeof(T);
+    const uint64_t wstride = (uint64_t)gridDim.x * (blockDim.x >> 5) * 32;
+    for (uint64_t base = ((uint64_t)blockIdx.x * (blockDim.x >> 5) + warp) * 32; base < P.ns; base += wstride) {
+        const uint64_t i = base + lane;
+        const bool on = i < P.ns;
+        TinyMT t = on ? tm_load(P, i) : TinyMT{};
+        const uint32_t len = on ? (uint32_t)P.n : 0u;
+        const uint64_t row = on ? (uint64_t)P.out + i * P.n * sizeof(T) : 0;
+        for (uint32_t r = 0; r < (uint32_t)P.n; r += G) {
+            const uint32_t cnt = len > r ? min(G, len - r) : 0u;
+            for (unsigned g = 0; g < cnt / 8; ++g) stage8_tm<KIND>(wb, lane, g * (KIND == kF64 ? 4 : 2), t);
+            write_round<T>(wb, lane, r, cnt, row);
+        }
+        if (on) tm_store(P, i, t);
+    }
+}
+
+template <int KIND>
+__global__ void __launch_bounds__(256) tinymt_fill_scalar_kernel(const __grid_constant__ TinyMtLaunch P)
+{
+    using T = OutT<KIND>;
+    const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= P.ns) return;
+    TinyMT t = tm_load(P, i);
+    T* o = reinterpret_cast<T*>(P.out) + i * P.n;
+    for (uint64_t j = 0; j < P.n; ++j) {
+        if (KIND == kU32) o[j] = (T)tinymt_next(t);
+        else if (KIND == kF32) o[j] = (T)to_f32(tinymt_next(t));
+        else {
+            const uint32_t lo = tinymt_next(t);
+            o[j] = (T)philox_f64(lo, tinymt_next(t));
+        }
+    }
+    tm_store(P, i, t);
+}
+
+// Sequential advance by P.steps draws (TinyMT32 jumps, S L355).
+__global__ void __launch_bounds__(256) tinymt_advance_kernel(const TinyMtLaunch P)
+{
+    const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= P.ns) return;
+    TinyMT t = tm_load(P, i);
+    for (uint64_t k = 0; k < P.steps; ++k) tinymt_next_state(t);
+    tm_store(P, i, t);
+}
+
+__global__ void __launch_bounds__(256) tinymt_mc_kernel(const __grid_constant__ TinyMtLaunch P)
+{
+    const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    uint64_t h = 0;
+    if (i < P.ns) {
+        TinyMT t = tm_load(P, i);
+        for (uint64_t k = 0; k < P.n; ++k) {
+            const uint32_t w0 = tinymt_next(t);
+            h += hit(w0, tinymt_next(t));
+        }
+        tm_store(P, i, t);
+        if (P.counts) atomicAdd(P.counts + i, (unsigned long long)h);
+    }
+    block_reduce_add(h, P.hits);
+}
+
 template <typename K>
 cudaError_t occ(K kernel, int threads, size_t smem, int* out)
 {
@@ -592,6 +765,64 @@ cudaError_t launch_philox_mc(const PhiloxLaunch& p, bool fast, Grid g, cudaStrea
     return cudaGetLastError();
 }
 
+cudaError_t launch_tinymt_prep(const uint32_t* params, uint64_t n_groups, int log2_gs, uint32_t* tables,
+                               cudaStream_t s)
+{
+    if (log2_gs == 0 || n_groups == 0) return cudaSuccess;
+    tinymt_prep_kernel<<<(unsigned)n_groups, 128, 0, s>>>(params, log2_gs, tables);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_tinymt_seed(const TinyMtLaunch& p, uint32_t seed, const uint32_t* tables, int log2_gs, Grid g,
+                               cudaStream_t s)
+{
+    tinymt_seed_kernel<<<g.blocks, g.threads, 0, s>>>(p, seed, tables, log2_gs);
+    return cudaGetLastError();
+}
+
+template <int KIND>
+cudaError_t launch_tm_vec(const TinyMtLaunch& p, Grid g, cudaStream_t s)
+{
+    const size_t smem = (size_t)(g.threads / 32) * 32 * kRB;
+    static std::atomic<uint64_t> done{0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const uint64_t bit = 1ull << (dev & 63);
+    if (!(done.load() & bit)) {
+        cudaError_t e = cudaFuncSetAttribute(tinymt_fill_vec_kernel<KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)((256 / 32) * 32 * kRB));
+        if (e != cudaSuccess) return e;
+        done.fetch_or(bit);
+    }
+    tinymt_fill_vec_kernel<KIND><<<g.blocks, g.threads, smem, s>>>(p);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_tinymt_fill(const TinyMtLaunch& p, int kind, bool vec, Grid g, cudaStream_t s)
+{
+    if (vec) {
+        if (kind == kU32) return launch_tm_vec<kU32>(p, g, s);
+        if (kind == kF32) return launch_tm_vec<kF32>(p, g, s);
+        return launch_tm_vec<kF64>(p, g, s);
+    }
+    if (kind == kU32) tinymt_fill_scalar_kernel<kU32><<<g.blocks, g.threads, 0, s>>>(p);
+    else if (kind == kF32) tinymt_fill_scalar_kernel<kF32><<<g.blocks, g.threads, 0, s>>>(p);
+    else tinymt_fill_scalar_kernel<kF64><<<g.blocks, g.threads, 0, s>>>(p);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_tinymt_advance(const TinyMtLaunch& p, Grid g, cudaStream_t s)
+{
+    tinymt_advance_kernel<<<g.blocks, g.threads, 0, s>>>(p);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_tinymt_mc(const TinyMtLaunch& p, Grid g, cudaStream_t s)
+{
+    tinymt_mc_kernel<<<g.blocks, g.threads, 0, s>>>(p);
+    return cudaGetLastError();
+}
+
 cudaError_t max_blocks_per_sm(int kernel, int kind, bool fast, int threads, int* out)
 {
     switch (kernel) {
@@ -630,6 +861,21 @@ cudaError_t max_blocks_per_sm(int kernel, int kind, bool fast, int threads, int*
     case kKPhiloxMc:
         return fast ? occ(philox_mc_kernel<true, false>, threads, 0, out)
                     : occ(philox_mc_kernel<false, false>, threads, 0, out);
+    case kKTinyFill: {
+        const size_t sm = (size_t)(threads / 32) * 32 * kRB;
+        if (kind == kU32) {
+            cudaFuncSetAttribute(tinymt_fill_vec_kernel<kU32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(8 * 32 * kRB));
+            return occ(tinymt_fill_vec_kernel<kU32>, threads, sm, out);
+        }
+        if (kind == kF32) {
+            cudaFuncSetAttribute(tinymt_fill_vec_kernel<kF32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(8 * 32 * kRB));
+            return occ(tinymt_fill_vec_kernel<kF32>, threads, sm, out);
+        }
+        cudaFuncSetAttribute(tinymt_fill_vec_kernel<kF64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(8 * 32 * kRB));
+        return occ(tinymt_fill_vec_kernel<kF64>, threads, sm, out);
+    }
+    case kKTinyMc:
+        return occ(tinymt_mc_kernel, threads, 0, out);
     case kKPhiloxMcKeyed:
         return fast ? occ(philox_mc_kernel<true, true>, threads, 0, out)
                     : occ(philox_mc_kernel<false, true>, threads, 0, out);

@@ -78,6 +78,24 @@ def test_validation_errors_without_gpu(shv):
         assert ei.value.status == code, kw
 
 
+def test_tinymt32_validation_without_gpu(shv):
+    E = shv.ShvError
+    P = [(0x8F7011EE, 0xFC78FF1F, 0x3793FDFF)] * 2
+    for args, code in (((None, 1, 4, 0, 8), shv.SHV_ERR_MISSING_PARAMETERS),
+                       (([], 1, 4, 0, 8), shv.SHV_ERR_MISSING_PARAMETERS),
+                       ((P, 1, 4, 0, 9), shv.SHV_ERR_INSUFFICIENT_STREAMS),   # 3 groups, 2 sets
+                       ((P, 1, 3, 0, 4), shv.SHV_ERR_INVALID_ARGUMENT),      # not a power of two
+                       ((P, 1, 4, 0, 0), shv.SHV_ERR_INVALID_ARGUMENT)):
+        params, seed, gs, first, n = args
+        with pytest.raises(E) as ei:
+            shv.shv_streams_create_tinymt32(params or [], seed, gs, first, n, None, 0, 0, 0)
+        assert ei.value.status == code, args
+    with pytest.raises(E) as ei:  # the generic create does not make TinyMT handles
+        shv.shv_streams_create_ex(shv.SHV_GEN_TINYMT32, [1], 0, 4, 0, None, 0, 0, 0)
+    assert ei.value.status == shv.SHV_ERR_MISSING_PARAMETERS
+    assert shv.shv_state_bytes(shv.SHV_GEN_TINYMT32, 10) == 160
+
+
 def test_lifecycle_errors_without_gpu(shv):
     for fn in (lambda: shv.shv_streams_destroy(123456789),
                lambda: shv.shv_jump(123456789, 0, 1),

@@ -342,3 +342,44 @@ def test_mc_survey_cross_check_first_64(orc):
     # 0..63 of seed 12345, 2^18 samples each -> 13179528 hits.
     tot, _ = orc.mc_count(W.MRG32K3A, [12345], 64, 1 << 18, spacing=W.SPACING_SUBSTREAM)
     assert tot == 13179528
+
+
+# --------------------------------------------------------------------------- TinyMT32 (NEXT-3)
+
+def _tm_seed(seed, gs, params):
+    return W.tinymt32_seed_words(seed, gs, params)
+
+
+def test_tinymt32_check_output(orc):
+    rows = _rows("tinymt32_check.txt")
+    m1, m2, tm, seed, *outs = rows[0]
+    params = [(int(m1, 16), int(m2, 16), int(tm, 16))]
+    got = orc.generate(W.TINYMT32, _tm_seed(int(seed), 1, params), 1, 10)[0]
+    assert [int(x) for x in got] == [int(v) for v in outs]
+
+
+def test_tinymt32_jump_equals_iterate_and_slices(orc):
+    params = W.tinymt32_test_params(3)
+    sd = _tm_seed(99, 4, params)
+    base = orc.generate(W.TINYMT32, sd, 1, 5000, first=5)[0]
+    for k in (1, 2, 3, 127, 128, 129, 1000, 4321):  # GF(2) matrix jump == k steps
+        assert np.array_equal(orc.generate(W.TINYMT32, sd, 1, 16, first=5, offset=k)[0], base[k:k + 16]), k
+    # slice contiguity (S L345-353): slice s advanced 2^64 draws is slice s+1
+    for s in (0, 1, 2):
+        a = orc.generate(W.TINYMT32, sd, 1, 32, first=4 + s, offset=1 << 64)[0]
+        b = orc.generate(W.TINYMT32, sd, 1, 32, first=4 + s + 1)[0]
+        assert np.array_equal(a, b), s
+    # group 1 and group 2 differ (one parameter set per group, P L309-313)
+    assert not np.array_equal(orc.generate(W.TINYMT32, sd, 1, 32, first=4)[0],
+                              orc.generate(W.TINYMT32, sd, 1, 32, first=8)[0])
+    # large jumps compose: offset X+5 equals offset X then 5 steps
+    X = (1 << 70) + 12340
+    a = orc.generate(W.TINYMT32, sd, 1, 8, first=6, offset=X + 5)[0]
+    b = orc.generate(W.TINYMT32, sd, 1, 13, first=6, offset=X)[0]
+    assert np.array_equal(a, b[5:13])
+
+
+def test_tinymt32_rejects(orc):
+    params = W.tinymt32_test_params(2)
+    with pytest.raises(ValueError):  # group 2 has no parameter set
+        orc.generate(W.TINYMT32, _tm_seed(1, 4, params), 1, 4, first=8)

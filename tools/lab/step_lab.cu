@@ -5,7 +5,7 @@
 #include <cstdio>
 #include <cstdint>
 #include <cuda_runtime.h>
-#include "../../include/shv_device.cuh"
+#include "lab_variants.cuh"
 using namespace shv::dev;
 
 constexpr int ITER = 2048;  // x 8 steps

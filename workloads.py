@@ -12,6 +12,7 @@ from dataclasses import dataclass
 
 MRG32K3A = 1
 PHILOX4X32_10 = 2
+TINYMT32 = 3
 SPACING_STREAM = 0
 SPACING_SUBSTREAM = 1
 SPACING_KEYED = 2
@@ -54,6 +55,27 @@ def rank_slice(w: Workload, rank: int, world: int, weak: bool) -> Workload:
     lo = w.n_streams * rank // world
     hi = w.n_streams * (rank + 1) // world
     return Workload(w.name, w.gen, w.seed, hi - lo, w.n, w.spacing, w.first + lo)
+
+
+# TinyMT32 parameter set of the authors' check output (tinymt32dc check
+# parameters): (mat1, mat2, tmat).
+TINYMT32_CHECK_PARAMS = (0x8F7011EE, 0xFC78FF1F, 0x3793FDFF)
+
+
+def tinymt32_test_params(k: int):
+    """k parameter records for parity tests: the check set, then SplitMix64
+    words. TEST-ONLY: the extra records are not Dynamic Creator output, so
+    their periods are not certified; oracle and GPU must agree regardless."""
+    out = [TINYMT32_CHECK_PARAMS]
+    words = splitmix64(1412, 3 * k)
+    for r in range(1, k):
+        out.append(tuple(w & 0xFFFFFFFF for w in words[3 * r:3 * r + 3]))
+    return out[:k]
+
+
+def tinymt32_seed_words(seed: int, group_size: int, params):
+    """The oracle's TinyMT32 seed vector: {seed, group_size, n_params, params...} (R15)."""
+    return [seed, group_size, len(params)] + [w for rec in params for w in rec]
 
 
 def splitmix64(seed: int, count: int):
