@@ -343,6 +343,29 @@ def main():
                                  "GB_per_s": round(8 * half * ws.n / (t_ms * 1e-3) / 1e9, 1),
                                  "frac_of_hbm_peak": round(8 * half * ws.n / (t_ms * 1e-3) / 1e9 / peak, 4)}
 
+        # TinyMT32 (NEXT-3) on the C5 shape: 2^20 streams x 4096 u32, groups of 256
+        # streams sharing a parameter set (test parameter sets, R15)
+        ns_t = wm.n_streams
+        params = W.tinymt32_test_params((wm.first + ns_t) // 256 + 1)
+        st_t = torch.empty(4 * ns_t, dtype=torch.int32, device=dev)
+        h = shv.shv_streams_create_tinymt32(params, 12345, 256, wm.first, ns_t, st_t, 0, local, sp)
+        times = []
+        for it in range(4):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            shv.shv_generate_u32(h, out, n, sp)
+            b.record(stream)
+            torch.cuda.synchronize()
+            if it:
+                times.append(a.elapsed_time(b))
+        shv.shv_streams_destroy(h)
+        del st_t
+        t_ms = statistics.mean(times)
+        parts["tinymt_fill_u32"] = {"ms": round(t_ms, 4),
+                                    "Gnumbers_per_s": round(total_per_rank / (t_ms * 1e-3) / 1e9, 1),
+                                    "GB_per_s": round(alg_bytes / (t_ms * 1e-3) / 1e9, 1),
+                                    "frac_of_hbm_peak": round(alg_bytes / (t_ms * 1e-3) / 1e9 / peak, 4)}
+
     # ---- e2e: same workload through shv_generate_u32_host into pinned host memory ----
     e2e = None
     if not args.no_e2e:
