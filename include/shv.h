@@ -16,6 +16,8 @@
  *   Philox4x32-10, SHV_SPACING_STREAM: counter-stream g = first+i, counter
  *                                     (blk_lo, blk_hi, g_lo, g_hi), key = seed (P L322-336 [§4.3]; R6)
  *   Philox4x32-10, SHV_SPACING_KEYED : key = (first+i, tag), counter (blk_lo, blk_hi, 0, 0)
+ *   Threefry4x64-20 (STREAM)        : ctr = (blk, first+i, 0, 0), key from the seed words (R16)
+ *   TinyMT32 (shv_streams_create_tinymt32): parameter set per group, 2^64-draw slices (R15)
  * Every stream of a handle sits at the same draw offset o (u128), which each
  * generate / mc_pi call advances by the draws it consumed (S L58; R8).
  *
@@ -60,7 +62,11 @@ typedef enum {
 typedef enum {
     SHV_GEN_MRG32K3A = 1,       /* [LEcuyer1999], P L82-86, L250-282 [§4.1] */
     SHV_GEN_PHILOX4X32_10 = 2,  /* [Salmon.etal.2011], P L88-90, L322-336 [§4.3]; variant per S L275 */
-    SHV_GEN_TINYMT32 = 3        /* [Saito2011], P L287-317 [§4.2]; shv_streams_create_tinymt32 */
+    SHV_GEN_TINYMT32 = 3,       /* [Saito2011], P L287-317 [§4.2]; shv_streams_create_tinymt32 */
+    SHV_GEN_THREEFRY4X64_20 = 4 /* [Salmon.etal.2011], P L322-336 [§4.3]; variant per S L275;
+                                   key = (s0|s1<<32, s2|s3<<32, 0, 0) from 1..4 seed words,
+                                   counter-stream g: ctr = (blk, g, 0, 0); draws are the (lo, hi)
+                                   32-bit words of the four 64-bit lanes (R16); STREAM spacing only */
 } shv_gen;
 
 typedef enum {
@@ -201,7 +207,8 @@ typedef struct {
     uint32_t jump[18];            /* MRG: A1^o (mod m1), A2^o (mod m2), row-major */
     const uint32_t* params;       /* TinyMT: (mat1, mat2, tmat) per group from group0 */
     uint64_t group0;              /* TinyMT: first group of the handle */
-    uint32_t group_size, pad_;    /* TinyMT */
+    uint32_t group_size;          /* TinyMT */
+    uint32_t key2, key3;          /* Threefry key words 2, 3 */
 } shv_device_view;
 
 shv_status shv_get_device_view(shv_streams h, shv_device_view* out);

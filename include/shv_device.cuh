@@ -337,6 +337,64 @@ struct PhiloxCursor {
     }
 };
 
+// ------------------------------------------------------------------ Threefry4x64-20
+
+// Threefry4x64-20 [Salmon.etal.2011] (P L322-336): Threefish-256 ARX rounds
+// (64-bit add, rotate, xor: ALU pipe only, no multiplies), key injection every
+// 4 rounds from ks = (k0..k3, parity), here with k2 = k3 = 0 (R16).
+struct Q4 {
+    uint64_t x, y, z, w;
+};
+
+template <int R>
+__device__ __forceinline__ uint64_t rotl64(uint64_t v)
+{
+    return (v << R) | (v >> (64 - R));
+}
+
+template <int A, int B, bool ODD>
+__device__ __forceinline__ void tf_mix(Q4& v)
+{
+    if (!ODD) {
+        v.x += v.y; v.y = rotl64<A>(v.y) ^ v.x;
+        v.z += v.w; v.w = rotl64<B>(v.w) ^ v.z;
+    } else {
+        v.x += v.w; v.w = rotl64<A>(v.w) ^ v.x;
+        v.z += v.y; v.y = rotl64<B>(v.y) ^ v.z;
+    }
+}
+
+__device__ __forceinline__ void tf_inject(Q4& v, const uint64_t* ks, int s)
+{
+    v.x += ks[s % 5];
+    v.y += ks[(s + 1) % 5];
+    v.z += ks[(s + 2) % 5];
+    v.w += ks[(s + 3) % 5] + (uint64_t)s;
+}
+
+// Block (blk, g, 0, 0) under key (k0, k1, 0, 0).
+__device__ __forceinline__ Q4 threefry20(uint64_t blk, uint64_t g, uint64_t k0, uint64_t k1)
+{
+    const uint64_t ks[5] = {k0, k1, 0, 0, 0x1BD11BDAA9FC1A22ull ^ k0 ^ k1};
+    Q4 v{blk + k0, g + k1, 0, 0};
+#pragma unroll
+    for (int q = 0; q < 5; ++q) {  // rounds 4q..4q+3 use R[(4q..4q+3) % 8]
+        if ((q & 1) == 0) {
+            tf_mix<14, 16, false>(v);
+            tf_mix<52, 57, true>(v);
+            tf_mix<23, 40, false>(v);
+            tf_mix<5, 37, true>(v);
+        } else {
+            tf_mix<25, 33, false>(v);
+            tf_mix<46, 12, true>(v);
+            tf_mix<58, 22, false>(v);
+            tf_mix<32, 32, true>(v);
+        }
+        tf_inject(v, ks, q + 1);
+    }
+    return v;
+}
+
 // ------------------------------------------------------------------ TinyMT32
 
 // TinyMT32 [Saito2011] (P L287-317 §4.2): 127-bit F2-linear state in four

@@ -89,6 +89,39 @@ private:
 };
 
 template <>
+class Rng<SHV_GEN_THREEFRY4X64_20> {
+public:
+    __device__ Rng(const shv_device_view& v, uint64_t i)
+        : k0_((uint64_t)v.key0 | ((uint64_t)v.key1 << 32)), k1_((uint64_t)v.key2 | ((uint64_t)v.key3 << 32)),
+          g_(v.first_stream + i), blk_((v.offset_lo >> 3) | (v.offset_hi << 61)), word_((uint32_t)(v.offset_lo & 7))
+    {
+        buf_ = dev::threefry20(blk_, g_, k0_, k1_);
+    }
+    __device__ uint32_t next_u32()
+    {
+        if (word_ == 8) {
+            ++blk_;
+            buf_ = dev::threefry20(blk_, g_, k0_, k1_);
+            word_ = 0;
+        }
+        const uint32_t w = word_++;
+        const uint64_t lane = (w >> 1) == 0 ? buf_.x : (w >> 1) == 1 ? buf_.y : (w >> 1) == 2 ? buf_.z : buf_.w;
+        return (w & 1) ? (uint32_t)(lane >> 32) : (uint32_t)lane;
+    }
+    __device__ float next_f32() { return dev::to_f32(next_u32()); }
+    __device__ double next_f64()
+    {
+        const uint32_t lo = next_u32();
+        return dev::philox_f64(lo, next_u32());
+    }
+
+private:
+    uint64_t k0_, k1_, g_, blk_;
+    uint32_t word_;
+    dev::Q4 buf_;
+};
+
+template <>
 class Rng<SHV_GEN_TINYMT32> {
 public:
     // Stream i: its current state (TinyMT handles are stateful) and the

@@ -23,6 +23,8 @@ LIB = os.path.join(HERE, "liboracle.so")
 
 MRG32K3A = 1
 PHILOX4X32_10 = 2
+TINYMT32 = 3
+THREEFRY4X64_20 = 4
 SPACING_STREAM = 0
 SPACING_SUBSTREAM = 1
 SPACING_KEYED = 2
@@ -58,6 +60,7 @@ def lib():
         L.orc_mrg_jump.argtypes = [u32p, C.c_uint64, C.c_uint64]
         L.orc_mrg_position.argtypes = [u32p, C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64, u32p]
         L.orc_philox_block.argtypes = [u32p, u32p, C.c_int, u32p]
+        L.orc_threefry4x64_block.argtypes = [u64p, u64p, C.c_int, u64p]
         L.orc_to_f32.restype = C.c_float
         L.orc_to_f32.argtypes = [C.c_uint32]
         L.orc_mrg_to_f64.restype = C.c_double
@@ -150,6 +153,14 @@ def philox_block(ctr, key, rounds: int = 10):
     k, pk = _u32(key)
     out, po = _u32(np.zeros(4))
     lib().orc_philox_block(pc, pk, rounds, po)
+    return [int(v) for v in out]
+
+
+def threefry4x64_block(ctr, key, rounds: int = 20):
+    c, pc = _u64(ctr)
+    k, pk = _u64(key)
+    out, po = _u64(np.zeros(4))
+    lib().orc_threefry4x64_block(pc, pk, rounds, po)
     return [int(v) for v in out]
 
 

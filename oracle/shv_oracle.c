@@ -192,6 +192,43 @@ void orc_philox_block(const uint32_t ctr[4], const uint32_t key[2], int rounds, 
 }
 
 /* ------------------------------------------------------------------------ */
+/* Threefry4x64 ([Salmon.etal.2011] §3.2: Threefish-256 with a 20-round ARX  */
+/* schedule, key injection every 4 rounds, no tweak)                        */
+/* ------------------------------------------------------------------------ */
+
+static uint64_t rotl64(uint64_t x, int r) { return (x << r) | (x >> (64 - r)); }
+
+void orc_threefry4x64_block(const uint64_t ctr[4], const uint64_t key[4], int rounds, uint64_t out[4])
+{
+    /* Threefish-256 rotation constants and the key-schedule parity word. */
+    static const int R[8][2] = {{14, 16}, {52, 57}, {23, 40}, {5, 37},
+                                {25, 33}, {46, 12}, {58, 22}, {32, 32}};
+    uint64_t ks[5];
+    ks[4] = 0x1BD11BDAA9FC1A22ull;
+    for (int i = 0; i < 4; ++i) {
+        ks[i] = key[i];
+        ks[4] ^= key[i];
+    }
+    uint64_t x[4];
+    for (int i = 0; i < 4; ++i) x[i] = ctr[i] + ks[i];
+    for (int r = 0; r < rounds; ++r) {
+        if (r % 2 == 0) { /* mix (0,1), (2,3) */
+            x[0] += x[1]; x[1] = rotl64(x[1], R[r % 8][0]) ^ x[0];
+            x[2] += x[3]; x[3] = rotl64(x[3], R[r % 8][1]) ^ x[2];
+        } else { /* permuted: mix (0,3), (2,1) */
+            x[0] += x[3]; x[3] = rotl64(x[3], R[r % 8][0]) ^ x[0];
+            x[2] += x[1]; x[1] = rotl64(x[1], R[r % 8][1]) ^ x[2];
+        }
+        if (r % 4 == 3) { /* key injection s = (r+1)/4 */
+            const uint64_t inj = (uint64_t)(r + 1) / 4;
+            for (int i = 0; i < 4; ++i) x[i] += ks[(inj + i) % 5];
+            x[3] += inj;
+        }
+    }
+    memcpy(out, x, sizeof x);
+}
+
+/* ------------------------------------------------------------------------ */
 /* TinyMT32 ([Saito2011]: tinymt32.h/.c of the authors' distribution)       */
 /* ------------------------------------------------------------------------ */
 
@@ -360,6 +397,28 @@ int orc_stream_open(orc_stream* st, int gen, const uint32_t* seed, int nseed,
         orc_tinymt32_jump(&st->tm, off_lo, off_hi);
         return 0;
     }
+    if (gen == ORC_THREEFRY4X64_20) {
+        /* R16: key = (s0 | s1<<32, s2 | s3<<32, 0, 0) from 1..4 seed words;
+         * stream g -> ctr = (blk, g, 0, 0); draw d -> word d & 7 of block
+         * d >> 3, words = (lo, hi) of lanes 0..3. */
+        if (nseed < 1 || nseed > 4 || spacing != ORC_SPACING_STREAM) return -1;
+        if (off_hi >> 3) return -1; /* a stream holds 2^67 draws */
+        uint32_t w[4] = {0, 0, 0, 0};
+        for (int k = 0; k < nseed; ++k) w[k] = seed[k];
+        st->tkey[0] = (uint64_t)w[0] | ((uint64_t)w[1] << 32);
+        st->tkey[1] = (uint64_t)w[2] | ((uint64_t)w[3] << 32);
+        st->tkey[2] = st->tkey[3] = 0;
+        st->g = first + i;
+        u128 d = ((u128)off_hi << 64) | off_lo;
+        st->blk = (uint64_t)(d >> 3);
+        st->tpos = 8;
+        int word = (int)(d & 7);
+        if (word) {
+            (void)orc_stream_next(st); /* fill the buffer at block d>>3 */
+            st->tpos = word;
+        }
+        return 0;
+    }
     if (gen == ORC_PHILOX4X32_10) {
         if (off_hi >> 2) return -1; /* a stream holds 2^66 draws (R6) */
         if (spacing == ORC_SPACING_STREAM) {
@@ -398,6 +457,20 @@ uint32_t orc_stream_next(orc_stream* st)
 {
     if (st->gen == ORC_MRG32K3A) return orc_mrg_step(st->s);
     if (st->gen == ORC_TINYMT32) return orc_tinymt32_generate(&st->tm);
+    if (st->gen == ORC_THREEFRY4X64_20) {
+        if (st->tpos == 8) {
+            const uint64_t ctr[4] = {st->blk, st->g, 0, 0};
+            uint64_t out[4];
+            orc_threefry4x64_block(ctr, st->tkey, 20, out);
+            for (int l = 0; l < 4; ++l) {
+                st->tbuf[2 * l] = (uint32_t)out[l];
+                st->tbuf[2 * l + 1] = (uint32_t)(out[l] >> 32);
+            }
+            st->blk += 1;
+            st->tpos = 0;
+        }
+        return st->tbuf[st->tpos++];
+    }
     /* SPEC next_word (S L258-266): serve x, y, z, w of the current block,
      * then evaluate the next counter. Counter = (blk_lo, blk_hi, g_lo, g_hi),
      * key = (seed0, seed1) (R6). */

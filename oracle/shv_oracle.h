@@ -19,7 +19,7 @@
 extern "C" {
 #endif
 
-enum { ORC_MRG32K3A = 1, ORC_PHILOX4X32_10 = 2, ORC_TINYMT32 = 3 };
+enum { ORC_MRG32K3A = 1, ORC_PHILOX4X32_10 = 2, ORC_TINYMT32 = 3, ORC_THREEFRY4X64_20 = 4 };
 enum { ORC_SPACING_STREAM = 0, ORC_SPACING_SUBSTREAM = 1, ORC_SPACING_KEYED = 2 };
 enum { ORC_U32 = 0, ORC_F32 = 1, ORC_F64 = 2 };
 
@@ -43,6 +43,9 @@ void orc_mrg_position(const uint32_t seed[6], uint64_t g, uint64_t u,
 /* ---- Philox4x32 (P L322-336 §4.3; constants from [Salmon.etal.2011]) ---- */
 void orc_philox_block(const uint32_t ctr[4], const uint32_t key[2], int rounds,
                       uint32_t out[4]);
+
+/* ---- Threefry4x64 (P L322-336 §4.3; [Salmon.etal.2011]) ---- */
+void orc_threefry4x64_block(const uint64_t ctr[4], const uint64_t key[4], int rounds, uint64_t out[4]);
 
 /* ---- TinyMT32 (P L287-317 §4.2; algorithm from [Saito2011], P L292) ---- */
 /* State: status[4] plus the parameter set (mat1, mat2, tmat). */
@@ -74,6 +77,9 @@ typedef struct {
     uint64_t blk;         /* Philox next counter block -> ctr[0..1] (R6) */
     uint32_t buf[4];      /* Philox lanes not yet served (S L258-266) */
     int buf_pos;          /* next lane to serve; 4 = empty */
+    uint64_t tkey[4];     /* Threefry key (R16) */
+    uint32_t tbuf[8];     /* Threefry words not yet served; tpos = 8: empty */
+    int tpos;
 } orc_stream;
 
 /* Open handle-stream i of a (gen, seed, first, spacing) family at draw offset

@@ -29,6 +29,7 @@ SHV_ERR_CUDA = 9
 SHV_GEN_MRG32K3A = 1
 SHV_GEN_PHILOX4X32_10 = 2
 SHV_GEN_TINYMT32 = 3
+SHV_GEN_THREEFRY4X64_20 = 4
 SHV_SPACING_STREAM = 0
 SHV_SPACING_SUBSTREAM = 1
 SHV_SPACING_KEYED = 2
@@ -64,7 +65,7 @@ class shv_device_view(C.Structure):
                 ("key1", C.c_uint32), ("first_stream", C.c_uint64), ("n_streams", C.c_uint64),
                 ("offset_lo", C.c_uint64), ("offset_hi", C.c_uint64), ("state", C.c_void_p),
                 ("jump", C.c_uint32 * 18), ("params", C.c_void_p), ("group0", C.c_uint64),
-                ("group_size", C.c_uint32), ("pad_", C.c_uint32)]
+                ("group_size", C.c_uint32), ("key2", C.c_uint32), ("key3", C.c_uint32)]
 
 
 LIB_PATH = _build.LIB

@@ -287,6 +287,11 @@ void split(const Handle& h, uint64_t ns, uint64_t len, uint64_t align, uint64_t 
 
 shv_status check_advance(const Handle& h, u128 draws)
 {
+    if (h.gen == SHV_GEN_THREEFRY4X64_20) {
+        if (draws > ((u128)1 << 67) || h.offset > ((u128)1 << 67) - draws)
+            return fail(SHV_ERR_INVALID_ARGUMENT, "Threefry stream exhausted (2^67 draws per stream)");
+        return SHV_OK;
+    }
     if (h.gen == SHV_GEN_PHILOX4X32_10) {
         if (draws > ((u128)1 << 66) || h.offset > ((u128)1 << 66) - draws)
             return fail(SHV_ERR_INVALID_ARGUMENT, "Philox stream exhausted (2^66 draws per stream)");
@@ -349,7 +354,36 @@ shv_status generate(shv_streams hid, T* out, uint64_t n, void* stream, int kind,
         T* dst = host_out ? stage[k & 1] : out;
         if (host_out && k >= 2) err = cudaStreamWaitEvent(s, copy_done[k & 1], 0);
         if (err != cudaSuccess) break;
-        if (h.gen == SHV_GEN_TINYMT32) {
+        if (h.gen == SHV_GEN_THREEFRY4X64_20) {
+            const uint64_t E = kind == kF64 ? 4 : 8;
+            const bool fast = aligned32 && (n % E == 0) && ((uint32_t)h.offset & 7) == 0;
+            ThreefryLaunch P{};
+            P.k0 = (uint64_t)h.seed[0] | ((uint64_t)h.seed[1] << 32);
+            P.k1 = (uint64_t)h.seed[2] | ((uint64_t)h.seed[3] << 32);
+            P.g0 = h.first + s0;
+            P.ns = ns;
+            P.o_blk = (uint64_t)(h.offset >> 3);
+            P.o_word = (uint32_t)(h.offset & 7);
+            P.out = dst;
+            P.n = n;
+            Grid g{};
+            if (fast) {
+                const uint64_t cpr = n / E;
+                const uint64_t rwarps = resident_threads(h, kKThreefryFill, kind, true) / 32;
+                uint64_t R = (cpr + 31) / 32;
+                if (R > 16) R = 16;
+                if (h.seg) R = h.seg / 8 < 1 ? 1 : (h.seg / 8 > 64 ? 64 : h.seg / 8);
+                auto tasks = [&](uint64_t r) { return ns * ((cpr + 32 * r - 1) / (32 * r)); };
+                while (!h.seg && R > 1 && tasks(R) < 4 * rwarps) R /= 2;
+                P.nseg = (uint32_t)R;
+                P.items = tasks(R);
+                g = Grid{blocks_for(h, kKThreefryFill, kind, true, P.items * 32), h.tpb};
+            } else {
+                P.items = (ns * n + 7) / 8;
+                g = Grid{blocks_for(h, kKThreefryFill, kind, false, P.items), h.tpb};
+            }
+            err = launch_threefry_fill(P, kind, fast, g, s);
+        } else if (h.gen == SHV_GEN_TINYMT32) {
             const bool vec = aligned32 && (n % 8 == 0) && n <= 0xFFFFFFFFull;
             TinyMtLaunch P = tm_launch(h, s0, ns);
             P.out = dst;
@@ -459,6 +493,12 @@ shv_status validate_seed(int gen, const uint32_t* seed, size_t words, uint32_t o
             return fail(SHV_ERR_INVALID_ARGUMENT, "Philox4x32-10 takes 1 or 2 key words, got %zu", words);
         out[0] = seed[0];
         out[1] = words == 2 ? seed[1] : 0;
+        return SHV_OK;
+    }
+    if (gen == SHV_GEN_THREEFRY4X64_20) {
+        if (words < 1 || words > 4)
+            return fail(SHV_ERR_INVALID_ARGUMENT, "Threefry4x64-20 takes 1 to 4 key words, got %zu", words);
+        for (size_t k = 0; k < words; ++k) out[k] = seed[k];
         return SHV_OK;
     }
     if (gen == SHV_GEN_TINYMT32)
@@ -571,6 +611,8 @@ shv_status shv_streams_create_ex(shv_streams* out, int gen, const uint32_t* seed
         return fail(SHV_ERR_INVALID_ARGUMENT, "unknown spacing %d", spacing);
     if (gen == SHV_GEN_PHILOX4X32_10 && spacing == SHV_SPACING_SUBSTREAM)
         return fail(SHV_ERR_UNSUPPORTED, "Philox4x32-10 has no substreams");
+    if (gen == SHV_GEN_THREEFRY4X64_20 && spacing != SHV_SPACING_STREAM)
+        return fail(SHV_ERR_UNSUPPORTED, "Threefry4x64-20 supports counter-stream spacing only");
     if (gen == SHV_GEN_MRG32K3A && spacing == SHV_SPACING_KEYED)
         return fail(SHV_ERR_UNSUPPORTED, "MRG32k3a has no keys (use STREAM or SUBSTREAM spacing)");
     if (spacing == SHV_SPACING_KEYED && seed_words != 1)
@@ -673,7 +715,7 @@ shv_status shv_jump(shv_streams hid, int kind, uint64_t n)
     if (kind == SHV_JUMP_DRAWS) {
         d = n;
     } else if (kind == SHV_JUMP_SUBSTREAMS || kind == SHV_JUMP_STREAMS) {
-        if (h.gen != SHV_GEN_MRG32K3A) return fail(SHV_ERR_UNSUPPORTED, "Philox jumps by draws only");
+        if (h.gen != SHV_GEN_MRG32K3A) return fail(SHV_ERR_UNSUPPORTED, "counter-based generators jump by draws only");
         const int sh = kind == SHV_JUMP_SUBSTREAMS ? 76 : 127;
         if (n >> (128 - sh)) return fail(SHV_ERR_INVALID_ARGUMENT, "jump exceeds 2^128 draws");
         d = (u128)n << sh;
@@ -720,7 +762,23 @@ shv_status shv_mc_pi_ex(shv_streams hid, uint64_t samples, uint64_t* d_hits, uin
     cudaStream_t s = (cudaStream_t)stream;
     cudaError_t err;
     const uint64_t cap = 1ull << 31;  // per-item count fits in u32
-    if (h.gen == SHV_GEN_TINYMT32) {
+    if (h.gen == SHV_GEN_THREEFRY4X64_20) {
+        const bool fast = ((uint32_t)h.offset & 7) == 0;
+        ThreefryLaunch P{};
+        P.k0 = (uint64_t)h.seed[0] | ((uint64_t)h.seed[1] << 32);
+        P.k1 = (uint64_t)h.seed[2] | ((uint64_t)h.seed[3] << 32);
+        P.g0 = h.first;
+        P.ns = h.n;
+        P.o_blk = (uint64_t)(h.offset >> 3);
+        P.o_word = (uint32_t)(h.offset & 7);
+        P.n = samples;
+        P.hits = (unsigned long long*)d_hits;
+        P.counts = (unsigned long long*)d_counts;
+        split(h, h.n, samples, 4, 32, resident_threads(h, kKThreefryMc, 0, fast), cap, &P.seg_len, &P.nseg);
+        P.items = h.n * P.nseg;
+        Grid g{blocks_for(h, kKThreefryMc, 0, fast, P.items), h.tpb};
+        err = launch_threefry_mc(P, fast, g, s);
+    } else if (h.gen == SHV_GEN_TINYMT32) {
         TinyMtLaunch P = tm_launch(h, 0, h.n);
         P.n = samples;
         P.hits = (unsigned long long*)d_hits;
@@ -798,6 +856,8 @@ shv_status shv_get_device_view(shv_streams hid, shv_device_view* out)
     out->spacing = (uint32_t)h.spacing;
     out->key0 = h.seed[0];
     out->key1 = h.spacing == SHV_SPACING_KEYED ? h.seed[0] : h.seed[1];
+    out->key2 = h.seed[2];
+    out->key3 = h.seed[3];
     out->first_stream = h.first;
     out->n_streams = h.n;
     out->offset_lo = (uint64_t)h.offset;

@@ -61,6 +61,24 @@ struct PhiloxLaunch {
     uint32_t keyed;          // 1: key = (g0 + i, k1), ctr[2..3] = 0 (SHV_SPACING_KEYED)
 };
 
+// Threefry4x64-20 launch (NEXT-2; R16). Draw d of launch stream i is word
+// (o_word + d) & 7 of block o_blk + ((o_word + d) >> 3), ctr = (blk, g0 + i, 0, 0),
+// key = (k0, k1, 0, 0); words are (lo, hi) of the four 64-bit lanes.
+struct ThreefryLaunch {
+    uint64_t k0, k1;
+    uint64_t g0;
+    uint64_t ns;
+    uint64_t o_blk;
+    uint32_t o_word;
+    uint32_t nseg;            // fill fast path: chunks per lane per task (R); MC: segments
+    void* out;
+    uint64_t n;
+    uint64_t seg_len;         // MC: samples per work item
+    uint64_t items;
+    unsigned long long* hits;
+    unsigned long long* counts;
+};
+
 // TinyMT32 launch (NEXT-3; R15). Stateful: the SoA state buffer holds every
 // stream's current state and each launch writes it back. Family stream
 // g = first + i belongs to group g / group_size, whose parameter set is
@@ -87,6 +105,8 @@ struct Grid {
 
 // ---- launchers (shv_kernels.cu) ----
 // TinyMT32: tables[g][b] = (T_g^(2^64))^(2^b), 128 columns x 4 words each.
+cudaError_t launch_threefry_fill(const ThreefryLaunch& p, int kind, bool fast, Grid g, cudaStream_t s);
+cudaError_t launch_threefry_mc(const ThreefryLaunch& p, bool fast, Grid g, cudaStream_t s);
 cudaError_t launch_tinymt_prep(const uint32_t* params, uint64_t n_groups, int log2_gs, uint32_t* tables,
                                cudaStream_t s);
 cudaError_t launch_tinymt_seed(const TinyMtLaunch& p, uint32_t seed, const uint32_t* tables, int log2_gs,
@@ -114,6 +134,8 @@ enum KernelId : int {
     kKPhiloxMcKeyed = 6,
     kKTinyFill = 7,
     kKTinyMc = 8,
+    kKThreefryFill = 9,
+    kKThreefryMc = 10,
 };
 cudaError_t max_blocks_per_sm(int kernel, int kind, bool fast, int threads, int* out);
 // Dynamic shared memory of the MRG vector-fill kernel at a block size.

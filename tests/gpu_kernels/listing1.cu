@@ -32,6 +32,7 @@ extern "C" int launch_listing1(int gen, int kind, void* out, const shv_device_vi
 {
     if (gen == SHV_GEN_MRG32K3A) launch<SHV_GEN_MRG32K3A>(kind, out, *v, per_thread, blocks, threads);
     else if (gen == SHV_GEN_TINYMT32) launch<SHV_GEN_TINYMT32>(kind, out, *v, per_thread, blocks, threads);
+    else if (gen == SHV_GEN_THREEFRY4X64_20) launch<SHV_GEN_THREEFRY4X64_20>(kind, out, *v, per_thread, blocks, threads);
     else launch<SHV_GEN_PHILOX4X32_10>(kind, out, *v, per_thread, blocks, threads);
     return (int)cudaDeviceSynchronize();
 }

@@ -42,12 +42,12 @@ DT = {0: (torch.int32, np.uint32), 1: (torch.float32, np.float32), 2: (torch.flo
 
 @pytest.mark.parametrize("gen,sp", [(W.MRG32K3A, W.SPACING_STREAM), (W.MRG32K3A, W.SPACING_SUBSTREAM),
                                     (W.PHILOX4X32_10, W.SPACING_STREAM),
-                                    (W.PHILOX4X32_10, W.SPACING_KEYED)])
+                                    (W.PHILOX4X32_10, W.SPACING_KEYED), (W.THREEFRY4X64_20, W.SPACING_STREAM)])
 @pytest.mark.parametrize("kind", [0, 1, 2])
 def test_listing1_kernel_matches_oracle(shv, orc, listing1, gen, sp, kind):
     block_num, thread_num = 37, 128          # Listing 1: init(block_num); <<<block_num, thread_num>>>
     n = block_num * thread_num
-    seed = [12345] if gen == W.MRG32K3A else [777]
+    seed = [12345] if gen == W.MRG32K3A else ([777, 5, 6, 7] if gen == W.THREEFRY4X64_20 else [777])
     first = 5
     state = torch.empty(6 * n, dtype=torch.int32, device="cuda") if gen == W.MRG32K3A else None
     h = shv.shv_streams_create_ex(gen, seed, first, n, sp, state, 0, torch.cuda.current_device(), None)
@@ -67,7 +67,7 @@ def test_listing1_kernel_matches_oracle(shv, orc, listing1, gen, sp, kind):
         bits = np.uint32 if got.itemsize == 4 else np.uint64  # compare bit patterns
         assert np.array_equal(got.view(bits), ref.view(bits))
         # the kernel consumed per_thread values per stream: advance the handle
-        draws = per_thread * (2 if (kind == 2 and gen == W.PHILOX4X32_10) else 1)
+        draws = per_thread * (2 if (kind == 2 and gen != W.MRG32K3A) else 1)
         shv.shv_jump(h, shv.SHV_JUMP_DRAWS, draws)
         offset += draws
     # the bulk path continues exactly where the device API left off

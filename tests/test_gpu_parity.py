@@ -55,7 +55,7 @@ class Fam:
             out = torch.empty(self.n_streams * n, dtype=tdt, device="cuda")
         getattr(self.shv, "shv_generate_" + kind)(self.h, out, n, None)
         torch.cuda.synchronize()
-        self.offset += n * (2 if (kind == "f64" and self.gen == W.PHILOX4X32_10) else 1)
+        self.offset += n * (2 if (kind == "f64" and self.gen != W.MRG32K3A) else 1)
         return out.cpu().numpy().view(ndt).reshape(self.n_streams, n) if n else out
 
     def ref(self, orc, n, kind="u32", offset=None, streams=None):
@@ -100,6 +100,31 @@ def test_c2_philox_full(shv, orc):
     f.close()
 
 
+def test_threefry_c2_shape_full_and_kats(shv, orc):
+    """Threefry4x64-20 (NEXT-2): 2^16 counter-streams x 1024 u32 vs the oracle,
+    and the Random123 KATs through the ABI (key = 4 words, ctr = (blk, g, 0, 0))."""
+    f = Fam(shv, W.THREEFRY4X64_20, [12345, 6789, 42, 7], 1 << 16)
+    ref = f.ref(orc, 1024, offset=0)
+    same(f.gen_(1024), ref)
+    f.close()
+    rows = [ln.split() for ln in open(os.path.join(GOLD, "threefry4x64_kat.txt"))
+            if ln.strip() and not ln.startswith("#")]
+    for fam, *words in rows:
+        v = [int(x, 16) for x in words]
+        ctr, key, exp = v[0:4], v[4:8], v[8:12]
+        if ctr[2] or ctr[3] or key[2] or key[3]:
+            continue  # the ABI layout fixes ctr[2..3] = key[2..3] = 0
+        seed = [key[0] & 0xFFFFFFFF, key[0] >> 32, key[1] & 0xFFFFFFFF, key[1] >> 32]
+        h = shv.shv_streams_create_ex(W.THREEFRY4X64_20, seed, ctr[1], 1, 0, None, 0, -1, None)
+        for _ in range(8):
+            shv.shv_jump(h, shv.SHV_JUMP_DRAWS, ctr[0])
+        out = torch.empty(8, dtype=torch.int32, device="cuda")
+        shv.shv_generate_u32(h, out, 8, None)
+        w = out.cpu().numpy().view(np.uint32).tolist()
+        assert [w[2 * l] | (w[2 * l + 1] << 32) for l in range(4)] == exp, fam
+        shv.shv_streams_destroy(h)
+
+
 def test_philox_kats_through_abi(shv):
     rows = [ln.split() for ln in open(os.path.join(GOLD, "philox4x32_kat.txt"))
             if ln.strip() and not ln.startswith("#")]
@@ -131,7 +156,8 @@ def test_c3_shape_reduced_full_compare(shv, orc, kind):
 
 # ---------------------------------------------------------------- edge cases
 
-@pytest.mark.parametrize("gen,sp", [(W.MRG32K3A, 0), (W.MRG32K3A, 1), (W.PHILOX4X32_10, 0)])
+@pytest.mark.parametrize("gen,sp", [(W.MRG32K3A, 0), (W.MRG32K3A, 1), (W.PHILOX4X32_10, 0),
+                                    (W.THREEFRY4X64_20, 0)])
 @pytest.mark.parametrize("kind", ["u32", "f32", "f64"])
 def test_ragged_offsets_and_replay(shv, orc, gen, sp, kind):
     """Rows that are not 32-byte multiples, offsets not multiples of 4 or 8,
@@ -167,7 +193,7 @@ def test_philox_keyed_mode(shv, orc, kind):
         f.close()
 
 
-@pytest.mark.parametrize("gen,sp", [(W.MRG32K3A, 1), (W.PHILOX4X32_10, 0)])
+@pytest.mark.parametrize("gen,sp", [(W.MRG32K3A, 1), (W.PHILOX4X32_10, 0), (W.THREEFRY4X64_20, 0)])
 def test_generate_twice_equals_generate_2n(shv, gen, sp):
     a = Fam(shv, gen, [99], 1000, sp)
     b = Fam(shv, gen, [99], 1000, sp)
@@ -234,7 +260,7 @@ def test_short_form_create(shv, orc):
     shv.shv_streams_destroy(h)
 
 
-@pytest.mark.parametrize("gen,sp", [(W.MRG32K3A, 1), (W.PHILOX4X32_10, 0)])
+@pytest.mark.parametrize("gen,sp", [(W.MRG32K3A, 1), (W.PHILOX4X32_10, 0), (W.THREEFRY4X64_20, 0)])
 def test_launch_config_invariance(shv, gen, sp):
     """R10: grid shape and segment length never change the values."""
     ref = None
@@ -272,7 +298,7 @@ def test_host_output_matches_device(shv, orc):
 
 # ---------------------------------------------------------------- Monte Carlo
 
-@pytest.mark.parametrize("gen,sp", [(W.MRG32K3A, 1), (W.PHILOX4X32_10, 0)])
+@pytest.mark.parametrize("gen,sp", [(W.MRG32K3A, 1), (W.PHILOX4X32_10, 0), (W.THREEFRY4X64_20, 0)])
 def test_mc_counts_small_full(shv, orc, gen, sp):
     f = Fam(shv, gen, [12345], 300, sp, first=17)
     for samples, pre in ((1000, 0), (777, 1), (5, 3), (4096, 2)):

@@ -383,3 +383,62 @@ def test_tinymt32_rejects(orc):
     params = W.tinymt32_test_params(2)
     with pytest.raises(ValueError):  # group 2 has no parameter set
         orc.generate(W.TINYMT32, _tm_seed(1, 4, params), 1, 4, first=8)
+
+
+# --------------------------------------------------------------------------- Threefry4x64-20 (NEXT-2)
+
+_TF_R = [(14, 16), (52, 57), (23, 40), (5, 37), (25, 33), (46, 12), (58, 22), (32, 32)]
+_M64 = (1 << 64) - 1
+
+
+def _tf_decrypt(y, key, rounds=20):
+    """Inverse of Threefry4x64 written from the round definition (SPEC S L233,
+    acceptance #3: inverse-round recovery); shares nothing with the oracle."""
+    ks = list(key) + [0x1BD11BDAA9FC1A22 ^ key[0] ^ key[1] ^ key[2] ^ key[3]]
+    x = list(y)
+    ror = lambda v, r: ((v >> r) | (v << (64 - r))) & _M64
+    for r in reversed(range(rounds)):
+        if r % 4 == 3:
+            s = (r + 1) // 4
+            x[3] = (x[3] - s) & _M64
+            for i in range(4):
+                x[i] = (x[i] - ks[(s + i) % 5]) & _M64
+        a, b = _TF_R[r % 8]
+        if r % 2 == 0:
+            x[3] = ror(x[3] ^ x[2], b); x[2] = (x[2] - x[3]) & _M64
+            x[1] = ror(x[1] ^ x[0], a); x[0] = (x[0] - x[1]) & _M64
+        else:
+            x[1] = ror(x[1] ^ x[2], b); x[2] = (x[2] - x[1]) & _M64
+            x[3] = ror(x[3] ^ x[0], a); x[0] = (x[0] - x[3]) & _M64
+    return [(x[i] - ks[i]) & _M64 for i in range(4)]
+
+
+def test_threefry_random123_kat(orc):
+    for fam, *words in _rows("threefry4x64_kat.txt"):
+        rounds = int(fam.split("_")[1])
+        v = [int(w, 16) for w in words]
+        assert orc.threefry4x64_block(v[0:4], v[4:8], rounds) == v[8:12], fam
+
+
+def test_threefry_inverse_recovers_counter(orc):
+    rng = random.Random(77)
+    for _ in range(1000):
+        c = [rng.getrandbits(64) for _ in range(4)]
+        k = [rng.getrandbits(64) for _ in range(4)]
+        assert _tf_decrypt(orc.threefry4x64_block(c, k, 20), k) == c
+
+
+@pytest.mark.parametrize("offset", [0, 1, 5, 8, 13, (1 << 40) + 3])
+def test_threefry_stream_layout(orc, offset):
+    # R16: key (s0|s1<<32, s2|s3<<32, 0, 0); ctr (blk, g, 0, 0); words lo, hi of lanes 0..3
+    seed = [0x01234567, 0x89ABCDEF, 0xDEADBEEF]
+    key = [seed[0] | (seed[1] << 32), seed[2], 0, 0]
+    g = 1234567
+    row = orc.generate(W.THREEFRY4X64_20, seed, 1, 40, first=g, offset=offset)[0]
+    for j in range(40):
+        d = offset + j
+        out = orc.threefry4x64_block([d >> 3, g, 0, 0], key, 20)
+        lane = out[(d & 7) >> 1]
+        assert int(row[j]) == ((lane >> 32) if d & 1 else lane & 0xFFFFFFFF)
+    full = orc.generate(W.THREEFRY4X64_20, seed, 3, 64, first=g)
+    assert np.array_equal(orc.generate(W.THREEFRY4X64_20, seed, 3, 59, first=g, offset=5), full[:, 5:])

@@ -13,6 +13,7 @@ from dataclasses import dataclass
 MRG32K3A = 1
 PHILOX4X32_10 = 2
 TINYMT32 = 3
+THREEFRY4X64_20 = 4
 SPACING_STREAM = 0
 SPACING_SUBSTREAM = 1
 SPACING_KEYED = 2
