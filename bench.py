@@ -343,6 +343,24 @@ def main():
                                  "GB_per_s": round(8 * half * ws.n / (t_ms * 1e-3) / 1e9, 1),
                                  "frac_of_hbm_peak": round(8 * half * ws.n / (t_ms * 1e-3) / 1e9 / peak, 4)}
 
+        # Threefry4x64-20 (NEXT-2) on the C5 shape: 2^20 counter-streams x 4096 u32
+        h = shv.shv_streams_create_ex(W.THREEFRY4X64_20, [12345], wp.first, wp.n_streams, 0, None, 0,
+                                      local, sp)
+        times = []
+        for it in range(4):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            shv.shv_generate_u32(h, out, n, sp)
+            b.record(stream)
+            torch.cuda.synchronize()
+            if it:
+                times.append(a.elapsed_time(b))
+        shv.shv_streams_destroy(h)
+        t_ms = statistics.mean(times)
+        parts["threefry_fill_u32"] = {"ms": round(t_ms, 4),
+                                      "Gnumbers_per_s": round(total_per_rank / (t_ms * 1e-3) / 1e9, 1),
+                                      "GB_per_s": round(alg_bytes / (t_ms * 1e-3) / 1e9, 1),
+                                      "frac_of_hbm_peak": round(alg_bytes / (t_ms * 1e-3) / 1e9 / peak, 4)}
         # TinyMT32 (NEXT-3) on the C5 shape: 2^20 streams x 4096 u32, groups of 256
         # streams sharing a parameter set (test parameter sets, R15)
         ns_t = wm.n_streams
