@@ -21,6 +21,8 @@
 
 #include "shv_internal.h"
 
+#include <nvtx3/nvToolsExt.h>
+
 namespace shv {
 namespace {
 
@@ -31,6 +33,13 @@ constexpr uint32_t kC[2] = {209u, 22853u};
 constexpr uint32_t kMod[2] = {kM1, kM2};
 
 thread_local std::string t_err;
+
+// NVTX range around each ABI call (visible in nsys / ncu --nvtx; a no-op
+// unless a tool is attached).
+struct Range {
+    explicit Range(const char* name) { nvtxRangePushA(name); }
+    ~Range() { nvtxRangePop(); }
+};
 
 shv_status fail(shv_status s, const char* fmt, ...)
 {
@@ -312,6 +321,7 @@ void fill_mrg_segments(const Handle& h, uint64_t units_per_seg, uint64_t draws_p
 template <typename T>
 shv_status generate(shv_streams hid, T* out, uint64_t n, void* stream, int kind, bool host_out)
 {
+    Range nvtx_range(host_out ? "shv_generate_u32_host" : kind == kU32 ? "shv_generate_u32" : kind == kF32 ? "shv_generate_f32" : "shv_generate_f64");
     auto hp = lookup(hid);
     if (!hp) return fail(SHV_ERR_LIFECYCLE, "unknown or destroyed handle %llu", (unsigned long long)hid);
     Handle& h = *hp;
@@ -524,6 +534,7 @@ shv_status shv_streams_create_tinymt32(shv_streams* out, const uint32_t* params,
                                        uint32_t group_size, uint64_t first_stream, uint64_t n_streams, void* d_state,
                                        size_t state_bytes, int device, void* cuda_stream)
 {
+    Range nvtx_range("shv_streams_create_tinymt32");
     if (!out) return fail(SHV_ERR_INVALID_ARGUMENT, "NULL out handle");
     *out = 0;
     if (!params || n_params == 0)
@@ -601,6 +612,7 @@ shv_status shv_streams_create_ex(shv_streams* out, int gen, const uint32_t* seed
                                  uint64_t first_stream, uint64_t n_streams, int spacing, void* d_state,
                                  size_t state_bytes, int device, void* cuda_stream)
 {
+    Range nvtx_range("shv_streams_create_ex");
     if (!out) return fail(SHV_ERR_INVALID_ARGUMENT, "NULL out handle");
     *out = 0;
     uint32_t s6[6];
@@ -693,6 +705,7 @@ shv_status shv_streams_create(shv_streams* out, int gen, const uint32_t* seed, s
 
 shv_status shv_jump(shv_streams hid, int kind, uint64_t n)
 {
+    Range nvtx_range("shv_jump");
     auto hp = lookup(hid);
     if (!hp) return fail(SHV_ERR_LIFECYCLE, "unknown or destroyed handle");
     Handle& h = *hp;
@@ -748,6 +761,7 @@ shv_status shv_generate_u32_host(shv_streams h, uint32_t* h_out, uint64_t n, voi
 shv_status shv_mc_pi_ex(shv_streams hid, uint64_t samples, uint64_t* d_hits, uint64_t* d_counts,
                         void* stream)
 {
+    Range nvtx_range("shv_mc_pi_ex");
     auto hp = lookup(hid);
     if (!hp) return fail(SHV_ERR_LIFECYCLE, "unknown or destroyed handle");
     Handle& h = *hp;
@@ -847,6 +861,7 @@ shv_status shv_get_position(shv_streams hid, shv_position* out)
 
 shv_status shv_get_device_view(shv_streams hid, shv_device_view* out)
 {
+    Range nvtx_range("shv_get_device_view");
     auto hp = lookup(hid);
     if (!hp) return fail(SHV_ERR_LIFECYCLE, "unknown or destroyed handle");
     if (!out) return fail(SHV_ERR_INVALID_ARGUMENT, "NULL out");
@@ -878,6 +893,7 @@ shv_status shv_get_device_view(shv_streams hid, shv_device_view* out)
 
 shv_status shv_streams_destroy(shv_streams hid)
 {
+    Range nvtx_range("shv_streams_destroy");
     std::shared_ptr<Handle> h;
     {
         std::lock_guard<std::mutex> lk(g_mu);

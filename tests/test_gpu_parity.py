@@ -429,3 +429,36 @@ def test_c5_rank_slices_match(shv, orc, w):
     same(rows.view(np.uint32), orc.generate(ws.gen, list(ws.seed), 0, ws.n, first=ws.first,
                                             spacing=ws.spacing, streams=streams))
     f.close()
+
+
+def test_concurrent_handles_from_threads(shv, orc):
+    """The registry is mutex-protected (include/shv.h): host threads creating,
+    filling (each on its own CUDA stream) and destroying handles concurrently
+    get exactly their own streams' values."""
+    import threading
+    results, errors = {}, []
+
+    def worker(k):
+        try:
+            s = torch.cuda.Stream()
+            with torch.cuda.stream(s):
+                gen = (W.MRG32K3A, W.PHILOX4X32_10, W.THREEFRY4X64_20)[k % 3]
+                st = torch.empty(6 * 64, dtype=torch.int32, device="cuda") if gen == W.MRG32K3A else None
+                for rep in range(5):
+                    h = shv.shv_streams_create_ex(gen, [1000 + k], 64 * k, 64, 0, st, 0, -1, s)
+                    out = torch.empty(64 * 96, dtype=torch.int32, device="cuda")
+                    shv.shv_generate_u32(h, out, 96, s)
+                    s.synchronize()
+                    shv.shv_streams_destroy(h)
+                results[k] = (gen, out.cpu().numpy().view(np.uint32).reshape(64, 96))
+        except Exception as e:  # surfaced below
+            errors.append(e)
+
+    threads = [threading.Thread(target=worker, args=(k,)) for k in range(9)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    assert not errors, errors
+    for k, (gen, got) in results.items():
+        same(got, orc.generate(gen, [1000 + k], 64, 96, first=64 * k))

@@ -1,0 +1,52 @@
+"""Small-shape driver for compute-sanitizer: exercises every
+kernel of libshv once (vector and scalar fill paths, all output kinds, fused
+MC, seeding, TinyMT32 preparation) so memcheck / racecheck / synccheck /
+initcheck see each of them.   compute-sanitizer --tool memcheck python tools/sanitize_driver.py"""
+import os
+import sys
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_1412_8266_b200 as shv  # noqa: E402
+import workloads as W  # noqa: E402
+
+
+def run():
+    dev = torch.cuda.current_device()
+    ns = 300
+    for gen, sp, seed in ((W.MRG32K3A, 1, [12345]), (W.MRG32K3A, 0, [7]), (W.PHILOX4X32_10, 0, [5, 6]),
+                          (W.PHILOX4X32_10, 2, [9]), (W.THREEFRY4X64_20, 0, [1, 2, 3])):
+        st = torch.empty(6 * ns, dtype=torch.int32, device="cuda") if gen == W.MRG32K3A else None
+        h = shv.shv_streams_create_ex(gen, seed, 11, ns, sp, st, 0, dev, None)
+        for n in (64, 13):                      # vector path, scalar/generic path
+            for dt, fn in ((torch.int32, shv.shv_generate_u32), (torch.float32, shv.shv_generate_f32),
+                           (torch.float64, shv.shv_generate_f64)):
+                out = torch.empty(ns * n, dtype=dt, device="cuda")
+                fn(h, out, n, None)
+        shv.shv_jump(h, shv.SHV_JUMP_DRAWS, 3)  # unaligned offsets: generic kernels
+        out = torch.empty(ns * 64, dtype=torch.int32, device="cuda")
+        shv.shv_generate_u32(h, out, 64, None)
+        hits = torch.zeros(1, dtype=torch.int64, device="cuda")
+        cnt = torch.zeros(ns, dtype=torch.int64, device="cuda")
+        shv.shv_mc_pi_ex(h, 501, hits, cnt, None)
+        host = torch.empty(ns * 64, dtype=torch.int32, pin_memory=True)
+        shv.shv_generate_u32_host(h, host, 64, None)
+        torch.cuda.synchronize()
+        shv.shv_streams_destroy(h)
+    params = W.tinymt32_test_params(20)
+    h = shv.shv_streams_create_tinymt32(params, 3, 16, 5, ns, None, 0, dev, None)
+    for n in (64, 13):
+        for dt, fn in ((torch.int32, shv.shv_generate_u32), (torch.float64, shv.shv_generate_f64)):
+            out = torch.empty(ns * n, dtype=dt, device="cuda")
+            fn(h, out, n, None)
+    shv.shv_jump(h, shv.SHV_JUMP_DRAWS, 5)
+    hits = torch.zeros(1, dtype=torch.int64, device="cuda")
+    shv.shv_mc_pi(h, 100, hits, None)
+    torch.cuda.synchronize()
+    shv.shv_streams_destroy(h)
+    print("sanitize driver done")
+
+
+if __name__ == "__main__":
+    run()
