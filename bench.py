@@ -62,6 +62,20 @@ def traffic_from_profiles(kernel_key):
     return None
 
 
+def limiter_from_profiles(kernel_key):
+    """What ncu says binds the kernel (profiles/ncu_traffic.json), for the reader."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if not os.path.exists(p):
+        return None
+    v = json.load(open(p)).get(kernel_key)
+    if not v:
+        return None
+    pipes = {"fp64": v.get("fp64_pipe_pct"), "fma_heavy": v.get("fmaheavy_pipe_pct"),
+             "alu": v.get("alu_pipe_pct"), "issue": v.get("issue_active_pct")}
+    top = max((k for k in pipes if pipes[k] is not None), key=lambda k: pipes[k])
+    return f"ncu: {top} {pipes[top]:.0f}% busy ({', '.join(f'{k} {x:.0f}%' for k, x in pipes.items() if x is not None)})"
+
+
 class Clocks:
     """nvidia-smi sampler running during the timed region (B200_PROFILING.md)."""
 
@@ -281,6 +295,7 @@ def main():
             "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
             "frac": round(achieved / peak, 4), "peak_source": peak_src,
             "traffic": traffic_from_profiles(dom),
+            "limiter": limiter_from_profiles(dom),
             "algorithmic_bytes_per_launch": alg_bytes}
     parts = {k: {"ms": round(kms[k], 4), "Gnumbers_per_s": round(total_per_rank / (kms[k] * 1e-3) / 1e9, 1),
                  "GB_per_s": round(alg_bytes / (kms[k] * 1e-3) / 1e9, 1),

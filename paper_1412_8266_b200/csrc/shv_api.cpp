@@ -318,6 +318,22 @@ void fill_mrg_segments(const Handle& h, uint64_t units_per_seg, uint64_t draws_p
     for (uint32_t j = 1; j < nseg; ++j) seg[j] = pair_mul(step, seg[j - 1]);
 }
 
+// Warp tasks of the counter-based fast fills: (row, 32*R chunks of 32 B). R
+// starts at ceil(chunks_per_row / 32) <= 16 and halves until there are >= 4
+// tasks per resident warp (load balance); a launch-config segment overrides it.
+void counter_tasks(const Handle& h, uint64_t ns, uint64_t cpr, uint64_t resident, uint32_t* R_out,
+                   uint64_t* tasks_out)
+{
+    const uint64_t rwarps = resident / 32;
+    uint64_t R = (cpr + 31) / 32;
+    if (R > 16) R = 16;
+    if (h.seg) R = h.seg / 8 < 1 ? 1 : (h.seg / 8 > 64 ? 64 : h.seg / 8);
+    auto tasks = [&](uint64_t r) { return ns * ((cpr + 32 * r - 1) / (32 * r)); };
+    while (!h.seg && R > 1 && tasks(R) < 4 * rwarps) R /= 2;
+    *R_out = (uint32_t)R;
+    *tasks_out = tasks(R);
+}
+
 template <typename T>
 shv_status generate(shv_streams hid, T* out, uint64_t n, void* stream, int kind, bool host_out)
 {
@@ -354,7 +370,15 @@ shv_status generate(shv_streams hid, T* out, uint64_t n, void* stream, int kind,
             if (e == cudaSuccess) e = cudaEventCreateWithFlags(&gen_done[b], cudaEventDisableTiming);
             if (e == cudaSuccess) e = cudaEventCreateWithFlags(&copy_done[b], cudaEventDisableTiming);
         }
-        if (e != cudaSuccess) return cuda_fail(e, "staging setup");
+        if (e != cudaSuccess) {
+            for (int b = 0; b < 2; ++b) {
+                if (stage[b]) cudaFreeAsync(stage[b], s);
+                if (gen_done[b]) cudaEventDestroy(gen_done[b]);
+                if (copy_done[b]) cudaEventDestroy(copy_done[b]);
+            }
+            if (cs) cudaStreamDestroy(cs);
+            return cuda_fail(e, "staging setup");
+        }
     }
 
     cudaError_t err = cudaSuccess;
@@ -378,15 +402,7 @@ shv_status generate(shv_streams hid, T* out, uint64_t n, void* stream, int kind,
             P.n = n;
             Grid g{};
             if (fast) {
-                const uint64_t cpr = n / E;
-                const uint64_t rwarps = resident_threads(h, kKThreefryFill, kind, true) / 32;
-                uint64_t R = (cpr + 31) / 32;
-                if (R > 16) R = 16;
-                if (h.seg) R = h.seg / 8 < 1 ? 1 : (h.seg / 8 > 64 ? 64 : h.seg / 8);
-                auto tasks = [&](uint64_t r) { return ns * ((cpr + 32 * r - 1) / (32 * r)); };
-                while (!h.seg && R > 1 && tasks(R) < 4 * rwarps) R /= 2;
-                P.nseg = (uint32_t)R;
-                P.items = tasks(R);
+                counter_tasks(h, ns, n / E, resident_threads(h, kKThreefryFill, kind, true), &P.nseg, &P.items);
                 g = Grid{blocks_for(h, kKThreefryFill, kind, true, P.items * 32), h.tpb};
             } else {
                 P.items = (ns * n + 7) / 8;
@@ -433,18 +449,8 @@ shv_status generate(shv_streams hid, T* out, uint64_t n, void* stream, int kind,
             P.n = n;
             Grid g{};
             if (fast) {
-                // warp tasks of (row, 32*R chunks); R shrinks until there are
-                // >= 4 tasks per resident warp.
-                const uint64_t cpr = n / E;
                 const int kid = P.keyed ? kKPhiloxFillKeyed : kKPhiloxFill;
-                const uint64_t rwarps = resident_threads(h, kid, kind, true) / 32;
-                uint64_t R = (cpr + 31) / 32;
-                if (R > 16) R = 16;
-                if (h.seg) R = h.seg / 8 < 1 ? 1 : (h.seg / 8 > 64 ? 64 : h.seg / 8);
-                auto tasks = [&](uint64_t r) { return ns * ((cpr + 32 * r - 1) / (32 * r)); };
-                while (!h.seg && R > 1 && tasks(R) < 4 * rwarps) R /= 2;
-                P.nseg = (uint32_t)R;
-                P.items = tasks(R);
+                counter_tasks(h, ns, n / E, resident_threads(h, kid, kind, true), &P.nseg, &P.items);
                 g = Grid{blocks_for(h, kid, kind, true, P.items * 32), h.tpb};
             } else {
                 P.items = (ns * n + 7) / 8;
