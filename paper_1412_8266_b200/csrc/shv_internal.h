@@ -139,6 +139,6 @@ enum KernelId : int {
 };
 cudaError_t max_blocks_per_sm(int kernel, int kind, bool fast, int threads, int* out);
 // Dynamic shared memory of the MRG vector-fill kernel at a block size.
-size_t mrg_fill_smem(int threads);
+size_t mrg_fill_smem(int threads, int kind);
 
 }  // namespace shv

@@ -11,8 +11,11 @@
 // Compile-time variants (the kernel lab, tools/lab/, builds each):
 //   SHV_MRG_STEP  0 = all-integer step, 2 = both components on the FP64 pipe
 //                 (default; fastest measured; other forms live in tools/lab/)
-//   SHV_MRG_STAGE 0 = each lane stores its own row directly, 1 = lanes stage 64
-//                 values in shared memory and the warp writes 256-byte runs
+//   SHV_MRG_STAGE 0 = each lane stores its own row directly (32-byte vector
+//                 stores); 2 = lanes stage 256 B in shared memory and the warp
+//                 writes 256-byte runs; 1 (default) = stage the 8-byte (f64)
+//                 outputs only: the compute-bound u32/f32 fills run faster
+//                 without staging (more warps), the HBM-bound f64 fill needs it
 #include <atomic>
 #include <cstdint>
 #include <type_traits>
@@ -213,11 +216,17 @@ __global__ void __launch_bounds__(256) mrg_seed_kernel(uint32_t* __restrict__ st
 // then the warp writes them as eight 1-KB store instructions, each covering
 // four rows x 256 contiguous bytes.
 template <int KIND>
+__host__ __device__ constexpr bool mrg_staged()
+{
+    return SHV_MRG_STAGE == 2 || (SHV_MRG_STAGE == 1 && KIND == kF64);
+}
+
+template <int KIND>
 __global__ void __launch_bounds__(256, SHV_MRG_MINB) mrg_fill_vec_kernel(const __grid_constant__ MrgLaunch P)
 {
     using T = OutT<KIND>;
     const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-#if SHV_MRG_STAGE
+    if constexpr (mrg_staged<KIND>()) {
     extern __shared__ uint4 smem[];
     uint4* wb = smem + warp * (32 * kPieces);
     constexpr uint32_t G = kRB / sizeof(T);  // values per lane per round
@@ -248,7 +257,7 @@ __global__ void __launch_bounds__(256, SHV_MRG_MINB) mrg_fill_vec_kernel(const _
             write_round<T>(wb, lane, r, cnt, row);
         }
     }
-#else
+    } else {
     (void)lane;
     (void)warp;
     const uint64_t nthr = (uint64_t)gridDim.x * blockDim.x;
@@ -274,7 +283,7 @@ __global__ void __launch_bounds__(256, SHV_MRG_MINB) mrg_fill_vec_kernel(const _
             }
         }
     }
-#endif
+    }
 }
 
 // MRG32k3a fill, scalar path (any row length / element-aligned pointer).
@@ -824,7 +833,7 @@ cudaError_t ensure_smem_attr()
     const uint64_t bit = 1ull << (dev & 63);
     if (done.load(std::memory_order_acquire) & bit) return cudaSuccess;
     e = cudaFuncSetAttribute(mrg_fill_vec_kernel<KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)mrg_fill_smem(256));
+                             (int)mrg_fill_smem(256, KIND));
     if (e == cudaSuccess) done.fetch_or(bit, std::memory_order_release);
     return e;
 }
@@ -832,7 +841,7 @@ cudaError_t ensure_smem_attr()
 template <int KIND>
 cudaError_t launch_vec(const MrgLaunch& p, Grid g, cudaStream_t s)
 {
-    const size_t smem = mrg_fill_smem((int)g.threads);
+    const size_t smem = mrg_fill_smem((int)g.threads, KIND);
     if (smem > 48 * 1024) {
         cudaError_t e = ensure_smem_attr<KIND>();
         if (e != cudaSuccess) return e;
@@ -843,7 +852,11 @@ cudaError_t launch_vec(const MrgLaunch& p, Grid g, cudaStream_t s)
 
 }  // namespace
 
-size_t mrg_fill_smem(int threads) { return SHV_MRG_STAGE ? (size_t)(threads / 32) * 32 * kRB : 0; }
+size_t mrg_fill_smem(int threads, int kind)
+{
+    const bool staged = kind == kU32 ? mrg_staged<kU32>() : kind == kF32 ? mrg_staged<kF32>() : mrg_staged<kF64>();
+    return staged ? (size_t)(threads / 32) * 32 * kRB : 0;
+}
 
 cudaError_t upload_jump_tables(const MatPair* sub51, const MatPair* str64)
 {
@@ -997,7 +1010,7 @@ cudaError_t max_blocks_per_sm(int kernel, int kind, bool fast, int threads, int*
     case kKSeed:
         return occ(mrg_seed_kernel, threads, 0, out);
     case kKMrgFill: {
-        const size_t sm = mrg_fill_smem(threads);
+        const size_t sm = fast ? mrg_fill_smem(threads, kind) : 0;
         if (fast && sm > 48 * 1024) {
             cudaError_t e = kind == kU32 ? ensure_smem_attr<kU32>()
                           : kind == kF32 ? ensure_smem_attr<kF32>() : ensure_smem_attr<kF64>();
