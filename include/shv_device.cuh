@@ -1,5 +1,5 @@
 // shv_device.cuh — device-side generator primitives of the ShoveRand hot path
-// (arXiv 1412.8266) for sm_100a. Included by shv_kernels.cu (and by the
+// (arXiv 1412.8266) for sm_100a. Included by the kernels_*.cu files (and by the
 // kernel lab under tools/lab/, which times variants of the same functions).
 //
 // Pipe budget on B200 (measured, profiles/r01_microbench.json): IMAD.WIDE.U32

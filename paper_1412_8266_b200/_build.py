@@ -9,8 +9,9 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libshv.so")
-SOURCES = [os.path.join(CSRC, "shv_kernels.cu"), os.path.join(CSRC, "shv_api.cpp")]
-DEPS = SOURCES + [os.path.join(CSRC, "shv_internal.h"), os.path.join(ROOT, "include", "shv_device.cuh"), os.path.join(ROOT, "include", "shv.h")]
+SOURCES = [os.path.join(CSRC, f) for f in ("kernels_mrg.cu", "kernels_philox.cu", "kernels_threefry.cu",
+                                            "kernels_tinymt32.cu", "shv_api.cpp")]
+DEPS = SOURCES + [os.path.join(CSRC, "shv_internal.h"), os.path.join(CSRC, "kernels_common.cuh"), os.path.join(ROOT, "include", "shv_device.cuh"), os.path.join(ROOT, "include", "shv.h")]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

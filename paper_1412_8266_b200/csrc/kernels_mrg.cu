@@ -1,0 +1,323 @@
+// kernels_mrg.cu — MRG32k3a kernels (arXiv 1412.8266 P L257-263 [§4.1]):
+// per-stream seeding by jump matrices, bulk fills (u32 / f32 / f64) and the
+// fused Monte Carlo pi kernel. Common pieces: kernels_common.cuh.
+//
+// Compile-time variants (the kernel lab, tools/lab/, builds each):
+//   SHV_MRG_STEP  0 = all-integer step, 2 = both components on the FP64 pipe
+//                 (default; fastest measured; other forms live in tools/lab/)
+//   SHV_MRG_STAGE 0 = each lane stores its own row directly (32-byte vector
+//                 stores); 2 = lanes stage 256 B in shared memory and the warp
+//                 writes 256-byte runs; 1 (default) = stage the 8-byte (f64)
+//                 outputs only: the compute-bound u32/f32 fills run faster
+//                 without staging (more warps), the HBM-bound f64 fill needs it
+//   SHV_MRG_MINB  min-blocks hint of the vector fill (4: <= 64 registers;
+//                 fewer spill or slow the FP64 step, lab)
+#include "kernels_common.cuh"
+
+#ifndef SHV_MRG_STEP
+#define SHV_MRG_STEP 2
+#endif
+#ifndef SHV_MRG_STAGE
+#define SHV_MRG_STAGE 1
+#endif
+#ifndef SHV_MRG_MINB
+#define SHV_MRG_MINB 4
+#endif
+
+namespace shv {
+
+// Jump tables: [0][b] = A^(2^(76+b)) (substreams, b < 51),
+//              [1][b] = A^(2^(127+b)) (streams, b < 64).
+__device__ MatPair g_jump_tab[2][64];
+
+namespace {
+
+#if SHV_MRG_STEP == 2
+using Gen = MrgD;
+__device__ __forceinline__ Gen make_gen(const Mrg& s) { return to_fp64(s); }
+#else
+using Gen = Mrg;
+__device__ __forceinline__ Gen make_gen(const Mrg& s) { return s; }
+#endif
+
+__device__ __forceinline__ Mrg load_state(const uint32_t* __restrict__ st, uint64_t stride, uint64_t i)
+{
+    Mrg s;
+    s.x0 = __ldg(st + i);
+    s.x1 = __ldg(st + stride + i);
+    s.x2 = __ldg(st + 2 * stride + i);
+    s.y0 = __ldg(st + 3 * stride + i);
+    s.y1 = __ldg(st + 4 * stride + i);
+    s.y2 = __ldg(st + 5 * stride + i);
+    return s;
+}
+
+// Start state of work item (stream i of the launch, segment j).
+__device__ __forceinline__ Gen item_state(const MrgLaunch& P, uint64_t i, uint64_t j)
+{
+    Mrg s = load_state(P.state, P.stride, P.stream_begin + i);
+    apply(P.seg[j].a, P.seg[j].b, s);
+    return make_gen(s);
+}
+
+// 8 values -> staging pieces (u32/f32: 2 pieces; f64: 4 pieces).
+template <int KIND>
+__device__ __forceinline__ void stage8(uint4* wb, unsigned lane, unsigned q0, Gen& s)
+{
+    uint32_t v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = mrg_next(s);
+    if (KIND == kF64) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const double a = mrg_f64(v[2 * u]), b = mrg_f64(v[2 * u + 1]);
+            wb[slot(lane, q0 + u)] = make_uint4(__double2loint(a), __double2hiint(a),
+                                                __double2loint(b), __double2hiint(b));
+        }
+    } else {
+        wb[slot(lane, q0)] = pack4<KIND>(v[0], v[1], v[2], v[3]);
+        wb[slot(lane, q0 + 1)] = pack4<KIND>(v[4], v[5], v[6], v[7]);
+    }
+}
+
+// Per-stream start states (row a3). Thread t of T handles streams t, t+T,
+// t+2T, ...: its first state is the product of the per-bit jump tables for t
+// (<= log2 T mat-vecs), each next one is one mat-vec with step = A^(T*spacing)
+// (host-built). ~2 mat-vecs per stream instead of popcount(i) <= 20; the SoA
+// stores of a warp are coalesced.
+__global__ void __launch_bounds__(256) mrg_seed_kernel(uint32_t* __restrict__ state, uint64_t n,
+                                                       uint32_t b0, uint32_t b1, uint32_t b2,
+                                                       uint32_t b3, uint32_t b4, uint32_t b5,
+                                                       int table, MatPair step)
+{
+    const uint64_t T = (uint64_t)gridDim.x * blockDim.x;
+    const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n) return;
+    Mrg s{b0, b1, b2, b3, b4, b5};
+    uint64_t bits = t;
+    for (int b = 0; bits; ++b, bits >>= 1)
+        if (bits & 1) apply(g_jump_tab[table][b].a, g_jump_tab[table][b].b, s);
+    for (uint64_t i = t; i < n; i += T) {
+        state[i] = s.x0;
+        state[n + i] = s.x1;
+        state[2 * n + i] = s.x2;
+        state[3 * n + i] = s.y0;
+        state[4 * n + i] = s.y1;
+        state[5 * n + i] = s.y2;
+        if (i + T < n) apply(step.a, step.b, s);
+    }
+}
+
+// MRG32k3a fill, vector path (32-byte aligned rows, seg_len % 8 == 0).
+// Staged: each lane generates 256 B of its row into shared memory per round,
+// then the warp writes them as eight 1-KB store instructions, each covering
+// four rows x 256 contiguous bytes.
+template <int KIND>
+__host__ __device__ constexpr bool mrg_staged()
+{
+    return SHV_MRG_STAGE == 2 || (SHV_MRG_STAGE == 1 && KIND == kF64);
+}
+
+template <int KIND>
+__global__ void __launch_bounds__(256, SHV_MRG_MINB) mrg_fill_vec_kernel(const __grid_constant__ MrgLaunch P)
+{
+    using T = OutT<KIND>;
+    const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if constexpr (mrg_staged<KIND>()) {
+    extern __shared__ uint4 smem[];
+    uint4* wb = smem + warp * (32 * kPieces);
+    constexpr uint32_t G = kRB / sizeof(T);  // values per lane per round
+    const uint64_t wstride = (uint64_t)gridDim.x * (blockDim.x >> 5) * 32;
+    for (uint64_t base = ((uint64_t)blockIdx.x * (blockDim.x >> 5) + warp) * 32; base < P.items;
+         base += wstride) {
+        const uint64_t it = base + lane;
+        uint32_t len = 0;
+        uint64_t row = 0;
+        Gen s{};
+        if (it < P.items) {
+            const uint64_t j = it / P.ns;
+            const uint64_t i = it - j * P.ns;
+            s = item_state(P, i, j);
+            const uint64_t c0 = j * P.seg_len;
+            len = (uint32_t)min(P.seg_len, P.n - c0);
+            row = (uint64_t)P.out + (i * P.n + c0) * sizeof(T);
+        }
+        const uint32_t maxlen = __reduce_max_sync(0xffffffffu, len);
+        for (uint32_t r = 0; r < maxlen; r += G) {
+            const uint32_t cnt = len > r ? min(G, len - r) : 0u;
+            if (cnt == G) {
+#pragma unroll
+                for (unsigned g = 0; g < G / 8; ++g) stage8<KIND>(wb, lane, g * (KIND == kF64 ? 4 : 2), s);
+            } else {
+                for (unsigned g = 0; g < cnt / 8; ++g) stage8<KIND>(wb, lane, g * (KIND == kF64 ? 4 : 2), s);
+            }
+            write_round<T>(wb, lane, r, cnt, row);
+        }
+    }
+    } else {
+    (void)lane;
+    (void)warp;
+    const uint64_t nthr = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t it = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; it < P.items; it += nthr) {
+        const uint64_t j = it / P.ns;
+        const uint64_t i = it - j * P.ns;
+        Gen s = item_state(P, i, j);
+        const uint64_t c0 = j * P.seg_len;
+        const uint64_t len = min(P.seg_len, P.n - c0);
+        T* o = reinterpret_cast<T*>(P.out) + i * P.n + c0;
+        for (uint64_t t = 0; t < len; t += 8) {
+            uint32_t v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) v[u] = mrg_next(s);
+            if (KIND == kU32) {
+                st_v8(o + t, v[0], v[1], v[2], v[3], v[4], v[5], v[6], v[7]);
+            } else if (KIND == kF32) {
+                st_v8f(o + t, to_f32(v[0]), to_f32(v[1]), to_f32(v[2]), to_f32(v[3]), to_f32(v[4]),
+                       to_f32(v[5]), to_f32(v[6]), to_f32(v[7]));
+            } else {
+                st_v4d(o + t, mrg_f64(v[0]), mrg_f64(v[1]), mrg_f64(v[2]), mrg_f64(v[3]));
+                st_v4d(o + t + 4, mrg_f64(v[4]), mrg_f64(v[5]), mrg_f64(v[6]), mrg_f64(v[7]));
+            }
+        }
+    }
+    }
+}
+
+// MRG32k3a fill, scalar path (any row length / element-aligned pointer).
+template <int KIND>
+__global__ void __launch_bounds__(256) mrg_fill_scalar_kernel(const __grid_constant__ MrgLaunch P)
+{
+    using T = OutT<KIND>;
+    const uint64_t nthr = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t it = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; it < P.items; it += nthr) {
+        const uint64_t j = it / P.ns;
+        const uint64_t i = it - j * P.ns;
+        Gen s = item_state(P, i, j);
+        const uint64_t c0 = j * P.seg_len;
+        const uint64_t len = min(P.seg_len, P.n - c0);
+        T* o = reinterpret_cast<T*>(P.out) + i * P.n + c0;
+        for (uint64_t t = 0; t < len; ++t) {
+            const uint32_t z = mrg_next(s);
+            if (KIND == kU32) o[t] = (T)z;
+            else if (KIND == kF32) o[t] = (T)to_f32(z);
+            else o[t] = (T)mrg_f64(z);
+        }
+    }
+}
+
+__global__ void __launch_bounds__(256) mrg_mc_kernel(const __grid_constant__ MrgLaunch P)
+{
+    const uint64_t nthr = (uint64_t)gridDim.x * blockDim.x;
+    uint64_t total = 0;
+    for (uint64_t it = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; it < P.items; it += nthr) {
+        const uint64_t j = it / P.ns;
+        const uint64_t i = it - j * P.ns;
+        Gen s = item_state(P, i, j);
+        const uint64_t c0 = j * P.seg_len;
+        const uint32_t len = (uint32_t)min(P.seg_len, P.n - c0);
+        uint32_t h = 0;
+        uint32_t k = 0;
+        for (; k + 12 <= len; k += 12) {
+#pragma unroll
+            for (int u = 0; u < 12; ++u) {
+                const uint32_t w0 = mrg_next(s);
+                const uint32_t w1 = mrg_next(s);
+                h += hit(w0, w1);
+            }
+        }
+        for (; k < len; ++k) {
+            const uint32_t w0 = mrg_next(s);
+            const uint32_t w1 = mrg_next(s);
+            h += hit(w0, w1);
+        }
+        total += h;
+        if (P.counts) atomicAdd(P.counts + i, (unsigned long long)h);
+    }
+    block_reduce_add(total, P.hits);
+}
+
+template <int KIND>
+cudaError_t ensure_smem_attr()
+{
+    static std::atomic<uint64_t> done{0};
+    return ensure_dyn_smem(mrg_fill_vec_kernel<KIND>, mrg_fill_smem(256, KIND), done);
+}
+
+template <int KIND>
+cudaError_t launch_vec(const MrgLaunch& p, Grid g, cudaStream_t s)
+{
+    const cudaError_t e = ensure_smem_attr<KIND>();
+    if (e != cudaSuccess) return e;
+    mrg_fill_vec_kernel<KIND><<<g.blocks, g.threads, mrg_fill_smem((int)g.threads, KIND), s>>>(p);
+    return cudaGetLastError();
+}
+
+}  // namespace
+
+size_t mrg_fill_smem(int threads, int kind)
+{
+    const bool staged = kind == kU32 ? mrg_staged<kU32>() : kind == kF32 ? mrg_staged<kF32>() : mrg_staged<kF64>();
+    return staged ? staged_smem(threads) : 0;
+}
+
+cudaError_t upload_jump_tables(const MatPair* sub51, const MatPair* str64)
+{
+    MatPair h[2][64] = {};
+    for (int b = 0; b < 51; ++b) h[0][b] = sub51[b];
+    for (int b = 0; b < 64; ++b) h[1][b] = str64[b];
+    return cudaMemcpyToSymbol(g_jump_tab, h, sizeof h);
+}
+
+cudaError_t launch_mrg_seed(uint32_t* state, uint64_t n, const uint32_t base[6], int table,
+                            const MatPair& step, Grid g, cudaStream_t s)
+{
+    mrg_seed_kernel<<<g.blocks, g.threads, 0, s>>>(state, n, base[0], base[1], base[2], base[3],
+                                                   base[4], base[5], table, step);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_mrg_fill(const MrgLaunch& p, int kind, bool vec, Grid g, cudaStream_t s)
+{
+    if (vec) {
+        if (kind == kU32) return launch_vec<kU32>(p, g, s);
+        if (kind == kF32) return launch_vec<kF32>(p, g, s);
+        return launch_vec<kF64>(p, g, s);
+    }
+    if (kind == kU32) mrg_fill_scalar_kernel<kU32><<<g.blocks, g.threads, 0, s>>>(p);
+    else if (kind == kF32) mrg_fill_scalar_kernel<kF32><<<g.blocks, g.threads, 0, s>>>(p);
+    else mrg_fill_scalar_kernel<kF64><<<g.blocks, g.threads, 0, s>>>(p);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_mrg_mc(const MrgLaunch& p, Grid g, cudaStream_t s)
+{
+    mrg_mc_kernel<<<g.blocks, g.threads, 0, s>>>(p);
+    return cudaGetLastError();
+}
+
+cudaError_t mrg_occupancy(int kernel, int kind, bool fast, int threads, int* out)
+{
+    switch (kernel) {
+    case kKSeed:
+        return occ(mrg_seed_kernel, threads, 0, out);
+    case kKMrgFill: {
+        const size_t sm = fast ? mrg_fill_smem(threads, kind) : 0;
+        if (fast) {
+            const cudaError_t e = kind == kU32 ? ensure_smem_attr<kU32>()
+                                : kind == kF32 ? ensure_smem_attr<kF32>() : ensure_smem_attr<kF64>();
+            if (e != cudaSuccess) return e;
+        }
+        if (kind == kU32) return fast ? occ(mrg_fill_vec_kernel<kU32>, threads, sm, out)
+                                      : occ(mrg_fill_scalar_kernel<kU32>, threads, 0, out);
+        if (kind == kF32) return fast ? occ(mrg_fill_vec_kernel<kF32>, threads, sm, out)
+                                      : occ(mrg_fill_scalar_kernel<kF32>, threads, 0, out);
+        return fast ? occ(mrg_fill_vec_kernel<kF64>, threads, sm, out)
+                    : occ(mrg_fill_scalar_kernel<kF64>, threads, 0, out);
+    }
+    case kKMrgMc:
+        return occ(mrg_mc_kernel, threads, 0, out);
+    }
+    return cudaErrorInvalidValue;
+}
+
+}  // namespace shv

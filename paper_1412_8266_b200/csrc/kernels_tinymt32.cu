@@ -1,0 +1,254 @@
+// kernels_tinymt32.cu — TinyMT32 kernels (NEXT-3; R15; S L355): GF(2)
+// jump tables, per-stream seeding, staged bulk fills, sequential advance and
+// the fused Monte Carlo pi kernel. Stateful: every launch writes the SoA state
+// back.
+#include "kernels_common.cuh"
+
+namespace shv {
+namespace {
+
+// TinyMT32: 8 values -> staging pieces (u32/f32: 8 words; f64: 16 words, two
+// per value like Philox, R7/R15).
+template <int KIND>
+__device__ __forceinline__ void stage8_tm(uint4* wb, unsigned lane, unsigned q0, TinyMT& t)
+{
+    if (KIND == kF64) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const uint32_t a0 = tinymt_next(t), a1 = tinymt_next(t), b0 = tinymt_next(t), b1 = tinymt_next(t);
+            const double a = philox_f64(a0, a1), b = philox_f64(b0, b1);
+            wb[slot(lane, q0 + u)] = make_uint4(__double2loint(a), __double2hiint(a), __double2loint(b),
+                                                __double2hiint(b));
+        }
+    } else {
+        uint32_t v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = tinymt_next(t);
+        wb[slot(lane, q0)] = pack4<KIND>(v[0], v[1], v[2], v[3]);
+        wb[slot(lane, q0 + 1)] = pack4<KIND>(v[4], v[5], v[6], v[7]);
+    }
+}
+
+__device__ __forceinline__ TinyMT tm_load(const TinyMtLaunch& P, uint64_t i)
+{
+    const uint64_t n = P.stride;
+    const uint32_t* pr = P.params + 3 * ((P.first + i) / P.group_size - P.group0);
+    return TinyMT{__ldg(P.state + i), __ldg(P.state + n + i), __ldg(P.state + 2 * n + i),
+                  __ldg(P.state + 3 * n + i), __ldg(pr), __ldg(pr + 1), __ldg(pr + 2)};
+}
+
+__device__ __forceinline__ void tm_store(const TinyMtLaunch& P, uint64_t i, const TinyMT& t)
+{
+    const uint64_t n = P.stride;
+    P.state[i] = t.s0;
+    P.state[n + i] = t.s1;
+    P.state[2 * n + i] = t.s2;
+    P.state[3 * n + i] = t.s3;
+}
+
+// ------------------------------------------------------------------ TinyMT32 (NEXT-3)
+
+// One block of 128 threads per parameter set: thread c builds column c of the
+// transition T (next_state of unit vector e_c), then the block squares the
+// matrix 64 times (T^(2^64), the slice length) and log2_gs - 1 more times,
+// storing (T^(2^64))^(2^b) for b < log2_gs.
+__global__ void __launch_bounds__(128) tinymt_prep_kernel(const uint32_t* __restrict__ params, int log2_gs,
+                                                          uint32_t* __restrict__ tables)
+{
+    __shared__ uint4 M[128], N[128];
+    const unsigned c = threadIdx.x;
+    const uint32_t* pr = params + 3 * blockIdx.x;
+    TinyMT t{0, 0, 0, 0, pr[0], pr[1], pr[2]};
+    (c < 32 ? t.s0 : c < 64 ? t.s1 : c < 96 ? t.s2 : t.s3) = 1u << (c & 31);
+    tinymt_next_state(t);
+    M[c] = make_uint4(t.s0, t.s1, t.s2, t.s3);
+    __syncthreads();
+    for (int k = 0; k < 64 + log2_gs; ++k) {
+        if (k >= 64) {  // M = (T^(2^64))^(2^(k-64)): emit table entry k-64
+            reinterpret_cast<uint4*>(tables)[((size_t)blockIdx.x * log2_gs + (k - 64)) * 128 + c] = M[c];
+            if (k == 64 + log2_gs - 1) break;
+        }
+        const uint4 x = M[c];  // column c of M*M = M applied to column c of M
+        const uint32_t xs[4] = {x.x, x.y, x.z, x.w};
+        uint4 y = make_uint4(0, 0, 0, 0);
+        for (int b = 0; b < 128; ++b)
+            if ((xs[b >> 5] >> (b & 31)) & 1u) {
+                const uint4 col = M[b];
+                y.x ^= col.x;
+                y.y ^= col.y;
+                y.z ^= col.z;
+                y.w ^= col.w;
+            }
+        N[c] = y;
+        __syncthreads();
+        M[c] = N[c];
+        __syncthreads();
+    }
+}
+
+// Stream i: init(params of its group, seed), then slice s = g % group_size
+// via the per-bit tables (popcount(s) GF(2) mat-vecs).
+__global__ void __launch_bounds__(256) tinymt_seed_kernel(const TinyMtLaunch P, uint32_t seed,
+                                                          const uint32_t* __restrict__ tables, int log2_gs)
+{
+    const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= P.ns) return;
+    const uint64_t g = P.first + i;
+    const uint64_t grp = g / P.group_size - P.group0;
+    const uint32_t* pr = P.params + 3 * grp;
+    TinyMT t;
+    tinymt_init(t, pr[0], pr[1], pr[2], seed);
+    const uint32_t slice = (uint32_t)(g % P.group_size);
+    for (int b = 0; b < log2_gs; ++b)
+        if ((slice >> b) & 1u) gf2_apply(tables + ((size_t)grp * log2_gs + b) * 512, t);
+    tm_store(P, i, t);
+}
+
+// Vector fill: one stream per lane, staged 256-byte runs (as the MRG kernel).
+template <int KIND>
+__global__ void __launch_bounds__(256, 4) tinymt_fill_vec_kernel(const __grid_constant__ TinyMtLaunch P)
+{
+    using T = OutT<KIND>;
+    const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    extern __shared__ uint4 smem[];
+    uint4* wb = smem + warp * (32 * kPieces);
+    constexpr uint32_t G = kRB / sizeof(T);
+    const uint64_t wstride = (uint64_t)gridDim.x * (blockDim.x >> 5) * 32;
+    for (uint64_t base = ((uint64_t)blockIdx.x * (blockDim.x >> 5) + warp) * 32; base < P.ns; base += wstride) {
+        const uint64_t i = base + lane;
+        const bool on = i < P.ns;
+        TinyMT t = on ? tm_load(P, i) : TinyMT{};
+        const uint32_t len = on ? (uint32_t)P.n : 0u;
+        const uint64_t row = on ? (uint64_t)P.out + i * P.n * sizeof(T) : 0;
+        for (uint32_t r = 0; r < (uint32_t)P.n; r += G) {
+            const uint32_t cnt = len > r ? min(G, len - r) : 0u;
+            for (unsigned g = 0; g < cnt / 8; ++g) stage8_tm<KIND>(wb, lane, g * (KIND == kF64 ? 4 : 2), t);
+            write_round<T>(wb, lane, r, cnt, row);
+        }
+        if (on) tm_store(P, i, t);
+    }
+}
+
+template <int KIND>
+__global__ void __launch_bounds__(256) tinymt_fill_scalar_kernel(const __grid_constant__ TinyMtLaunch P)
+{
+    using T = OutT<KIND>;
+    const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= P.ns) return;
+    TinyMT t = tm_load(P, i);
+    T* o = reinterpret_cast<T*>(P.out) + i * P.n;
+    for (uint64_t j = 0; j < P.n; ++j) {
+        if (KIND == kU32) o[j] = (T)tinymt_next(t);
+        else if (KIND == kF32) o[j] = (T)to_f32(tinymt_next(t));
+        else {
+            const uint32_t lo = tinymt_next(t);
+            o[j] = (T)philox_f64(lo, tinymt_next(t));
+        }
+    }
+    tm_store(P, i, t);
+}
+
+// Sequential advance by P.steps draws (TinyMT32 jumps, S L355).
+__global__ void __launch_bounds__(256) tinymt_advance_kernel(const TinyMtLaunch P)
+{
+    const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= P.ns) return;
+    TinyMT t = tm_load(P, i);
+    for (uint64_t k = 0; k < P.steps; ++k) tinymt_next_state(t);
+    tm_store(P, i, t);
+}
+
+__global__ void __launch_bounds__(256) tinymt_mc_kernel(const __grid_constant__ TinyMtLaunch P)
+{
+    const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    uint64_t h = 0;
+    if (i < P.ns) {
+        TinyMT t = tm_load(P, i);
+        for (uint64_t k = 0; k < P.n; ++k) {
+            const uint32_t w0 = tinymt_next(t);
+            h += hit(w0, tinymt_next(t));
+        }
+        tm_store(P, i, t);
+        if (P.counts) atomicAdd(P.counts + i, (unsigned long long)h);
+    }
+    block_reduce_add(h, P.hits);
+}
+
+template <int KIND>
+cudaError_t ensure_tm_smem()
+{
+    static std::atomic<uint64_t> done{0};
+    return ensure_dyn_smem(tinymt_fill_vec_kernel<KIND>, staged_smem(256), done);
+}
+
+template <int KIND>
+cudaError_t launch_tm_vec(const TinyMtLaunch& p, Grid g, cudaStream_t s)
+{
+    const cudaError_t e = ensure_tm_smem<KIND>();
+    if (e != cudaSuccess) return e;
+    tinymt_fill_vec_kernel<KIND><<<g.blocks, g.threads, staged_smem((int)g.threads), s>>>(p);
+    return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t launch_tinymt_prep(const uint32_t* params, uint64_t n_groups, int log2_gs, uint32_t* tables,
+                               cudaStream_t s)
+{
+    if (log2_gs == 0 || n_groups == 0) return cudaSuccess;
+    tinymt_prep_kernel<<<(unsigned)n_groups, 128, 0, s>>>(params, log2_gs, tables);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_tinymt_seed(const TinyMtLaunch& p, uint32_t seed, const uint32_t* tables, int log2_gs, Grid g,
+                               cudaStream_t s)
+{
+    tinymt_seed_kernel<<<g.blocks, g.threads, 0, s>>>(p, seed, tables, log2_gs);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_tinymt_fill(const TinyMtLaunch& p, int kind, bool vec, Grid g, cudaStream_t s)
+{
+    if (vec) {
+        if (kind == kU32) return launch_tm_vec<kU32>(p, g, s);
+        if (kind == kF32) return launch_tm_vec<kF32>(p, g, s);
+        return launch_tm_vec<kF64>(p, g, s);
+    }
+    if (kind == kU32) tinymt_fill_scalar_kernel<kU32><<<g.blocks, g.threads, 0, s>>>(p);
+    else if (kind == kF32) tinymt_fill_scalar_kernel<kF32><<<g.blocks, g.threads, 0, s>>>(p);
+    else tinymt_fill_scalar_kernel<kF64><<<g.blocks, g.threads, 0, s>>>(p);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_tinymt_advance(const TinyMtLaunch& p, Grid g, cudaStream_t s)
+{
+    tinymt_advance_kernel<<<g.blocks, g.threads, 0, s>>>(p);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_tinymt_mc(const TinyMtLaunch& p, Grid g, cudaStream_t s)
+{
+    tinymt_mc_kernel<<<g.blocks, g.threads, 0, s>>>(p);
+    return cudaGetLastError();
+}
+
+cudaError_t tinymt_occupancy(int kernel, int kind, bool fast, int threads, int* out)
+{
+    (void)fast;
+    switch (kernel) {
+    case kKTinyFill: {
+        const cudaError_t e = kind == kU32 ? ensure_tm_smem<kU32>()
+                            : kind == kF32 ? ensure_tm_smem<kF32>() : ensure_tm_smem<kF64>();
+        if (e != cudaSuccess) return e;
+        const size_t sm = staged_smem(threads);
+        if (kind == kU32) return occ(tinymt_fill_vec_kernel<kU32>, threads, sm, out);
+        if (kind == kF32) return occ(tinymt_fill_vec_kernel<kF32>, threads, sm, out);
+        return occ(tinymt_fill_vec_kernel<kF64>, threads, sm, out);
+    }
+    case kKTinyMc:
+        return occ(tinymt_mc_kernel, threads, 0, out);
+    }
+    return cudaErrorInvalidValue;
+}
+
+}  // namespace shv

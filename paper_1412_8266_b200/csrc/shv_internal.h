@@ -1,5 +1,5 @@
 // shv_internal.h — launch records shared by the ABI layer (shv_api.cpp) and the
-// sm_100a kernels (shv_kernels.cu). Not installed; the public ABI is include/shv.h.
+// sm_100a kernels (kernels_*.cu). Not installed; the public ABI is include/shv.h.
 #pragma once
 #include <cstddef>
 #include <cstdint>
@@ -103,7 +103,7 @@ struct Grid {
     unsigned threads;
 };
 
-// ---- launchers (shv_kernels.cu) ----
+// ---- launchers (kernels_mrg.cu, kernels_philox.cu, kernels_threefry.cu, kernels_tinymt32.cu) ----
 // TinyMT32: tables[g][b] = (T_g^(2^64))^(2^b), 128 columns x 4 words each.
 cudaError_t launch_threefry_fill(const ThreefryLaunch& p, int kind, bool fast, Grid g, cudaStream_t s);
 cudaError_t launch_threefry_mc(const ThreefryLaunch& p, bool fast, Grid g, cudaStream_t s);
@@ -137,7 +137,26 @@ enum KernelId : int {
     kKThreefryFill = 9,
     kKThreefryMc = 10,
 };
-cudaError_t max_blocks_per_sm(int kernel, int kind, bool fast, int threads, int* out);
+// Occupancy of one kernel variant; each per-generator file answers for its own
+// ids (cudaErrorInvalidValue otherwise).
+cudaError_t mrg_occupancy(int kernel, int kind, bool fast, int threads, int* out);
+cudaError_t philox_occupancy(int kernel, int kind, bool fast, int threads, int* out);
+cudaError_t threefry_occupancy(int kernel, int kind, bool fast, int threads, int* out);
+cudaError_t tinymt_occupancy(int kernel, int kind, bool fast, int threads, int* out);
+inline cudaError_t max_blocks_per_sm(int kernel, int kind, bool fast, int threads, int* out)
+{
+    switch (kernel) {
+    case kKSeed: case kKMrgFill: case kKMrgMc:
+        return mrg_occupancy(kernel, kind, fast, threads, out);
+    case kKPhiloxFill: case kKPhiloxMc: case kKPhiloxFillKeyed: case kKPhiloxMcKeyed:
+        return philox_occupancy(kernel, kind, fast, threads, out);
+    case kKThreefryFill: case kKThreefryMc:
+        return threefry_occupancy(kernel, kind, fast, threads, out);
+    case kKTinyFill: case kKTinyMc:
+        return tinymt_occupancy(kernel, kind, fast, threads, out);
+    }
+    return cudaErrorInvalidValue;
+}
 // Dynamic shared memory of the MRG vector-fill kernel at a block size.
 size_t mrg_fill_smem(int threads, int kind);
 
