@@ -369,46 +369,61 @@ def main():
                                  "GB_per_s": round(8 * half * ws.n / (t_ms * 1e-3) / 1e9, 1),
                                  "frac_of_hbm_peak": round(8 * half * ws.n / (t_ms * 1e-3) / 1e9 / peak, 4)}
 
+        def fill_ms(h, buf, nn, reps=3, kind="u32"):
+            """Mean of `reps` launches after one untimed launch (events on the launching stream)."""
+            gen = {"u32": shv.shv_generate_u32, "f64": shv.shv_generate_f64}[kind]
+            times = []
+            for it in range(reps + 1):
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+                gen(h, buf, nn, sp)
+                b.record(stream)
+                torch.cuda.synchronize()
+                if it:
+                    times.append(a.elapsed_time(b))
+            return statistics.mean(times)
+
+        def fill_part(t_ms, numbers, bpn=4):
+            return {"ms": round(t_ms, 4), "Gnumbers_per_s": round(numbers / (t_ms * 1e-3) / 1e9, 1),
+                    "GB_per_s": round(bpn * numbers / (t_ms * 1e-3) / 1e9, 1),
+                    "frac_of_hbm_peak": round(bpn * numbers / (t_ms * 1e-3) / 1e9 / peak, 4)}
+
         # Threefry4x64-20 (NEXT-2) on the C5 shape: 2^20 counter-streams x 4096 u32
         h = shv.shv_streams_create_ex(W.THREEFRY4X64_20, [12345], wp.first, wp.n_streams, 0, None, 0,
                                       local, sp)
-        times = []
-        for it in range(4):
-            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a.record(stream)
-            shv.shv_generate_u32(h, out, n, sp)
-            b.record(stream)
-            torch.cuda.synchronize()
-            if it:
-                times.append(a.elapsed_time(b))
+        parts["threefry_fill_u32"] = fill_part(fill_ms(h, out, n), total_per_rank)
         shv.shv_streams_destroy(h)
-        t_ms = statistics.mean(times)
-        parts["threefry_fill_u32"] = {"ms": round(t_ms, 4),
-                                      "Gnumbers_per_s": round(total_per_rank / (t_ms * 1e-3) / 1e9, 1),
-                                      "GB_per_s": round(alg_bytes / (t_ms * 1e-3) / 1e9, 1),
-                                      "frac_of_hbm_peak": round(alg_bytes / (t_ms * 1e-3) / 1e9 / peak, 4)}
         # TinyMT32 (NEXT-3) on the C5 shape: 2^20 streams x 4096 u32, groups of 256
         # streams sharing a parameter set (test parameter sets, R15)
         ns_t = wm.n_streams
         params = W.tinymt32_test_params((wm.first + ns_t) // 256 + 1)
         st_t = torch.empty(4 * ns_t, dtype=torch.int32, device=dev)
         h = shv.shv_streams_create_tinymt32(params, 12345, 256, wm.first, ns_t, st_t, 0, local, sp)
-        times = []
-        for it in range(4):
-            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a.record(stream)
-            shv.shv_generate_u32(h, out, n, sp)
-            b.record(stream)
-            torch.cuda.synchronize()
-            if it:
-                times.append(a.elapsed_time(b))
+        parts["tinymt_fill_u32"] = fill_part(fill_ms(h, out, n), total_per_rank)
         shv.shv_streams_destroy(h)
         del st_t
-        t_ms = statistics.mean(times)
-        parts["tinymt_fill_u32"] = {"ms": round(t_ms, 4),
-                                    "Gnumbers_per_s": round(total_per_rank / (t_ms * 1e-3) / 1e9, 1),
-                                    "GB_per_s": round(alg_bytes / (t_ms * 1e-3) / 1e9, 1),
-                                    "frac_of_hbm_peak": round(alg_bytes / (t_ms * 1e-3) / 1e9 / peak, 4)}
+
+        # C6 (SURVEY 8(d)): stream-count sweep at a fixed 2^32 u32 per GPU (16 GiB),
+        # n_streams = 2^13 .. 2^22, n_per_stream = total / n_streams, both generators.
+        # Acceptance: every point within 10% of the C5 (2^20 x 4096) figure.
+        sweep = {"mrg": {}, "philox": {}}
+        st_s = torch.empty(6 << 22, dtype=torch.int32, device=dev)
+        for lg in range(13, 23):
+            ns = 1 << lg
+            nn = total_per_rank // ns
+            if nn < 8:
+                continue
+            for key, w in (("mrg", wm), ("philox", wp)):
+                h = shv.shv_streams_create_ex(w.gen, list(w.seed), rank * ns, ns, w.spacing,
+                                              st_s if key == "mrg" else None, 0, local, sp)
+                sweep[key][f"2^{lg}"] = round(ns * nn / (fill_ms(h, out, nn) * 1e-3) / 1e9, 1)
+                shv.shv_streams_destroy(h)
+        del st_s
+        c5 = {k: parts[k]["Gnumbers_per_s"] for k in ("mrg", "philox")}
+        parts["c6_stream_sweep"] = {
+            "unit": "Gnumbers/s", "numbers_per_gpu": total_per_rank, **sweep, "c5": c5,
+            "min_over_c5": {k: round(min(v.values()) / c5[k], 3) for k, v in sweep.items() if v},
+            "flat_within_10pct": all(min(v.values()) >= 0.9 * c5[k] for k, v in sweep.items() if v)}
 
     # ---- e2e: same workload through shv_generate_u32_host into pinned host memory ----
     e2e = None

@@ -28,6 +28,7 @@ THREEFRY4X64_20 = 4
 SPACING_STREAM = 0
 SPACING_SUBSTREAM = 1
 SPACING_KEYED = 2
+SPACING_LEAPFROG = 3
 U32, F32, F64 = 0, 1, 2
 
 _lib = None
@@ -80,6 +81,14 @@ def lib():
         L.orc_mc_count_list.restype = C.c_uint64
         L.orc_mc_count_list.argtypes = [C.c_int, u32p, C.c_int, C.c_uint64, u64p, C.c_uint64,
                                         C.c_int, C.c_uint64, C.c_uint64, C.c_uint64, u64p, C.c_int]
+        L.orc_generate_leapfrog.restype = C.c_int
+        L.orc_generate_leapfrog.argtypes = [C.c_int, u32p, C.c_int, C.c_uint64, C.c_uint64, u64p,
+                                            C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64, C.c_int,
+                                            C.c_void_p, C.c_int]
+        L.orc_mc_count_leapfrog.restype = C.c_uint64
+        L.orc_mc_count_leapfrog.argtypes = [C.c_int, u32p, C.c_int, C.c_uint64, C.c_uint64, u64p,
+                                            C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64, u64p,
+                                            C.c_int]
         _lib = L
     return _lib
 
@@ -180,12 +189,21 @@ _DT = {U32: np.uint32, F32: np.float32, F64: np.float64}
 
 
 def generate(gen, seed, n_streams, n, *, first=0, spacing=SPACING_STREAM, offset=0,
-             kind=U32, nthreads=None, streams=None):
-    """Rows out[i, j] (R8). ``streams`` optionally lists handle-stream indices."""
+             kind=U32, nthreads=None, streams=None, players=None):
+    """Rows out[i, j] (R8). ``streams`` optionally lists handle-stream indices.
+    spacing=SPACING_LEAPFROG deals one base sequence to ``players`` players;
+    row i is player first + i (orc_stream_open_leapfrog)."""
     nthreads = nthreads or os.cpu_count() or 1
     sd, ps = _u32(seed)
     lo, hi = _split(offset)
-    if streams is None:
+    if spacing == SPACING_LEAPFROG:
+        idx, pi = _u64(streams if streams is not None else [])
+        rows = len(idx) if streams is not None else n_streams
+        out = np.empty((rows, n), dtype=_DT[kind])
+        rc = lib().orc_generate_leapfrog(gen, ps, len(sd), players, first,
+                                         pi if streams is not None else None, rows, lo, hi, n,
+                                         kind, out.ctypes.data, nthreads)
+    elif streams is None:
         out = np.empty((n_streams, n), dtype=_DT[kind])
         rc = lib().orc_generate(gen, ps, len(sd), first, n_streams, spacing, lo, hi, n, kind,
                                 out.ctypes.data, nthreads)
@@ -200,12 +218,19 @@ def generate(gen, seed, n_streams, n, *, first=0, spacing=SPACING_STREAM, offset
 
 
 def mc_count(gen, seed, n_streams, samples, *, first=0, spacing=SPACING_STREAM, offset=0,
-             nthreads=None, streams=None):
+             nthreads=None, streams=None, players=None):
     """(total hits, per-stream counts) of the dartboard (R9)."""
     nthreads = nthreads or os.cpu_count() or 1
     sd, ps = _u32(seed)
     lo, hi = _split(offset)
-    if streams is None:
+    if spacing == SPACING_LEAPFROG:
+        idx, pi = _u64(streams if streams is not None else [])
+        rows = len(idx) if streams is not None else n_streams
+        counts, pc = _u64(np.zeros(rows))
+        tot = lib().orc_mc_count_leapfrog(gen, ps, len(sd), players, first,
+                                          pi if streams is not None else None, rows, lo, hi,
+                                          samples, pc, nthreads)
+    elif streams is None:
         counts, pc = _u64(np.zeros(n_streams))
         tot = lib().orc_mc_count(gen, ps, len(sd), first, n_streams, spacing, lo, hi, samples,
                                  pc, nthreads)

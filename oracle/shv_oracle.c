@@ -453,8 +453,71 @@ int orc_stream_open(orc_stream* st, int gen, const uint32_t* seed, int nseed,
     return -1;
 }
 
+int orc_stream_open_leapfrog(orc_stream* st, int gen, const uint32_t* seed, int nseed,
+                             uint64_t players, uint64_t player, uint64_t off_lo, uint64_t off_hi)
+{
+    if (players == 0 || player >= players) return -1;
+    const u128 off = ((u128)off_hi << 64) | off_lo;
+    /* d0 = player + K*off, the first base draw this player receives */
+    if (off > (~(u128)0 - player) / players) return -1;
+    const u128 d0 = (u128)player + (u128)players * off;
+    if (gen == ORC_MRG32K3A) {
+        if (orc_stream_open(st, gen, seed, nseed, 0, 0, ORC_SPACING_STREAM, (uint64_t)d0,
+                            (uint64_t)(d0 >> 64)))
+            return -1;
+        uint64_t A1[9], A2[9];
+        orc_mrg_matrices(A1, A2);
+        orc_mat_pow(A1, players - 1, 0, (uint64_t)m1, st->leapA1);
+        orc_mat_pow(A2, players - 1, 0, (uint64_t)m2, st->leapA2);
+    } else if (gen == ORC_PHILOX4X32_10 || gen == ORC_THREEFRY4X64_20) {
+        if (orc_stream_open(st, gen, seed, nseed, 0, 0, ORC_SPACING_STREAM, 0, 0)) return -1;
+        if (d0 >= ((u128)1 << (gen == ORC_PHILOX4X32_10 ? 66 : 67))) return -1;
+        st->pos_lo = (uint64_t)d0;
+        st->pos_hi = (uint64_t)(d0 >> 64);
+    } else {
+        return -1;
+    }
+    st->leap = players;
+    return 0;
+}
+
+/* Draw at base index d of counter stream 0 (Leap Frog, R17). */
+static uint32_t counter_word(const orc_stream* st, u128 d)
+{
+    if (st->gen == ORC_THREEFRY4X64_20) {
+        const uint64_t ctr[4] = {(uint64_t)(d >> 3), 0, 0, 0};
+        uint64_t out[4];
+        orc_threefry4x64_block(ctr, st->tkey, 20, out);
+        const uint64_t lane = out[(d & 7) >> 1];
+        return (d & 1) ? (uint32_t)(lane >> 32) : (uint32_t)lane;
+    }
+    const uint64_t b = (uint64_t)(d >> 2);
+    const uint32_t ctr[4] = {(uint32_t)b, (uint32_t)(b >> 32), 0, 0};
+    uint32_t out[4];
+    orc_philox_block(ctr, st->key, 10, out);
+    return out[d & 3];
+}
+
 uint32_t orc_stream_next(orc_stream* st)
 {
+    if (st->leap) {
+        /* Leap Frog: serve the next base draw, then skip K-1 base draws. */
+        if (st->gen == ORC_MRG32K3A) {
+            const uint32_t z = orc_mrg_step(st->s);
+            uint32_t a[3], b[3];
+            mat_vec(st->leapA1, st->s, (uint64_t)m1, a);
+            mat_vec(st->leapA2, st->s + 3, (uint64_t)m2, b);
+            memcpy(st->s, a, sizeof a);
+            memcpy(st->s + 3, b, sizeof b);
+            return z;
+        }
+        const u128 d = ((u128)st->pos_hi << 64) | st->pos_lo;
+        const uint32_t w = counter_word(st, d);
+        const u128 nd = d + st->leap;
+        st->pos_lo = (uint64_t)nd;
+        st->pos_hi = (uint64_t)(nd >> 64);
+        return w;
+    }
     if (st->gen == ORC_MRG32K3A) return orc_mrg_step(st->s);
     if (st->gen == ORC_TINYMT32) return orc_tinymt32_generate(&st->tm);
     if (st->gen == ORC_THREEFRY4X64_20) {
@@ -490,6 +553,7 @@ uint32_t orc_stream_next(orc_stream* st)
 
 typedef struct {
     int gen, nseed, spacing, kind, mc;
+    uint64_t players;                  /* Leap Frog: K (spacing LEAPFROG) */
     const uint32_t* seed;
     uint64_t first, off_lo, off_hi, n; /* n = values per row, or samples */
     const uint64_t* idx;               /* NULL: row r is stream r */
@@ -506,8 +570,12 @@ static void* run_job(void* arg)
     for (uint64_t r = jb->r0; r < jb->r1; ++r) {
         uint64_t i = jb->idx ? jb->idx[r] : r;
         orc_stream st;
-        if (orc_stream_open(&st, jb->gen, jb->seed, jb->nseed, jb->first, i, jb->spacing,
-                            jb->off_lo, jb->off_hi)) {
+        const int bad = jb->spacing == ORC_SPACING_LEAPFROG
+                            ? orc_stream_open_leapfrog(&st, jb->gen, jb->seed, jb->nseed, jb->players,
+                                                       jb->first + i, jb->off_lo, jb->off_hi)
+                            : orc_stream_open(&st, jb->gen, jb->seed, jb->nseed, jb->first, i,
+                                              jb->spacing, jb->off_lo, jb->off_hi);
+        if (bad) {
             jb->err = 1;
             return NULL;
         }
@@ -620,5 +688,27 @@ uint64_t orc_mc_count_list(int gen, const uint32_t* seed, int nseed, uint64_t fi
     uint64_t total = 0;
     job_t p = make_job(gen, seed, nseed, first, spacing, off_lo, off_hi, samples, 0, idx, NULL, counts, 1);
     if (run_jobs(p, n_idx, nthreads, &total)) return UINT64_MAX;
+    return total;
+}
+
+int orc_generate_leapfrog(int gen, const uint32_t* seed, int nseed, uint64_t players, uint64_t first,
+                          const uint64_t* idx, uint64_t n_rows, uint64_t off_lo, uint64_t off_hi,
+                          uint64_t n, int kind, void* out, int nthreads)
+{
+    job_t p = make_job(gen, seed, nseed, first, ORC_SPACING_LEAPFROG, off_lo, off_hi, n, kind, idx,
+                       out, NULL, 0);
+    p.players = players;
+    return run_jobs(p, n_rows, nthreads, NULL);
+}
+
+uint64_t orc_mc_count_leapfrog(int gen, const uint32_t* seed, int nseed, uint64_t players,
+                               uint64_t first, const uint64_t* idx, uint64_t n_rows, uint64_t off_lo,
+                               uint64_t off_hi, uint64_t samples, uint64_t* counts, int nthreads)
+{
+    uint64_t total = 0;
+    job_t p = make_job(gen, seed, nseed, first, ORC_SPACING_LEAPFROG, off_lo, off_hi, samples, 0, idx,
+                       NULL, counts, 1);
+    p.players = players;
+    if (run_jobs(p, n_rows, nthreads, &total)) return UINT64_MAX;
     return total;
 }

@@ -20,7 +20,7 @@ extern "C" {
 #endif
 
 enum { ORC_MRG32K3A = 1, ORC_PHILOX4X32_10 = 2, ORC_TINYMT32 = 3, ORC_THREEFRY4X64_20 = 4 };
-enum { ORC_SPACING_STREAM = 0, ORC_SPACING_SUBSTREAM = 1, ORC_SPACING_KEYED = 2 };
+enum { ORC_SPACING_STREAM = 0, ORC_SPACING_SUBSTREAM = 1, ORC_SPACING_KEYED = 2, ORC_SPACING_LEAPFROG = 3 };
 enum { ORC_U32 = 0, ORC_F32 = 1, ORC_F64 = 2 };
 
 /* ---- MRG32k3a (P L250-282 §4.1; constants from [LEcuyer1999], P L255) ---- */
@@ -80,6 +80,9 @@ typedef struct {
     uint64_t tkey[4];     /* Threefry key (R16) */
     uint32_t tbuf[8];     /* Threefry words not yet served; tpos = 8: empty */
     int tpos;
+    uint64_t leap;        /* Leap Frog: players K (0: not a leap-frog stream) */
+    uint64_t leapA1[9], leapA2[9]; /* MRG32k3a: A^(K-1), the K-1 skipped draws */
+    uint64_t pos_lo, pos_hi;       /* counter-based: next base draw index */
 } orc_stream;
 
 /* Open handle-stream i of a (gen, seed, first, spacing) family at draw offset
@@ -93,6 +96,18 @@ int orc_stream_open(orc_stream* st, int gen, const uint32_t* seed, int nseed,
                     uint64_t first, uint64_t i, int spacing,
                     uint64_t off_lo, uint64_t off_hi);
 uint32_t orc_stream_next(orc_stream* st);
+
+/* Leap Frog (P L118-122 [§2.3]: "like a deck of cards dealt to card
+ * players"; S L397, L424): one base sequence dealt round-robin to K players;
+ * player p receives base draws p, p+K, p+2K, ... Its draw offset o counts its
+ * own draws (base draw p + K*o is its next). Base sequence (R17): MRG32k3a
+ * stream 0 of seed; Philox4x32-10 / Threefry4x64-20 counter stream 0 of key
+ * seed. Each draw takes the next base draw, then skips K-1 base draws (MRG:
+ * the jump A^(K-1), S L157-165; counter-based: the index advances by K).
+ * TinyMT32: -1. Returns -1 if p >= K or the base sequence is exhausted at the
+ * start position (Philox 2^66, Threefry 2^67, MRG 2^128 draws). */
+int orc_stream_open_leapfrog(orc_stream* st, int gen, const uint32_t* seed, int nseed,
+                             uint64_t players, uint64_t player, uint64_t off_lo, uint64_t off_hi);
 
 /* Stream-major rows out[i*n + j] (R8) for streams i < n_streams; kind picks
  * u32 / f32 / f64 (Philox f64 consumes two draws per value, R7).
@@ -118,6 +133,15 @@ int orc_generate_list(int gen, const uint32_t* seed, int nseed, uint64_t first,
                       const uint64_t* idx, uint64_t n_idx, int spacing,
                       uint64_t off_lo, uint64_t off_hi, uint64_t n, int kind,
                       void* out, int nthreads);
+
+/* Leap Frog rows / dartboard for players first + idx[r] (idx NULL: first + r,
+ * r < n_rows) of K = players (see orc_stream_open_leapfrog). */
+int orc_generate_leapfrog(int gen, const uint32_t* seed, int nseed, uint64_t players, uint64_t first,
+                          const uint64_t* idx, uint64_t n_rows, uint64_t off_lo, uint64_t off_hi,
+                          uint64_t n, int kind, void* out, int nthreads);
+uint64_t orc_mc_count_leapfrog(int gen, const uint32_t* seed, int nseed, uint64_t players,
+                               uint64_t first, const uint64_t* idx, uint64_t n_rows, uint64_t off_lo,
+                               uint64_t off_hi, uint64_t samples, uint64_t* counts, int nthreads);
 
 #ifdef __cplusplus
 }

@@ -442,3 +442,87 @@ def test_threefry_stream_layout(orc, offset):
         assert int(row[j]) == ((lane >> 32) if d & 1 else lane & 0xFFFFFFFF)
     full = orc.generate(W.THREEFRY4X64_20, seed, 3, 64, first=g)
     assert np.array_equal(orc.generate(W.THREEFRY4X64_20, seed, 3, 59, first=g, offset=5), full[:, 5:])
+
+
+# --------------------------------------------------------------------------- Leap Frog (NEXT-4, R17)
+# P L118-122 [§2.3]: the base sequence is "dealt" to K players like cards;
+# player p receives base draws p, p+K, p+2K, ... (S L397, L404, L418).
+
+LEAP_GENS = ((W.MRG32K3A, [12345]), (W.PHILOX4X32_10, [12345, 678]), (W.THREEFRY4X64_20, [1, 2, 3, 4]))
+
+
+@pytest.mark.parametrize("gen,seed", LEAP_GENS)
+def test_leapfrog_one_player_is_the_base_sequence(orc, gen, seed):
+    base = orc.generate(gen, seed, 1, 300)
+    lf = orc.generate(gen, seed, 1, 300, spacing=W.SPACING_LEAPFROG, players=1)
+    assert np.array_equal(lf, base)  # S L404: LeapFrog{1}, PE 0 = the base sequence
+
+
+@pytest.mark.parametrize("gen,seed", LEAP_GENS)
+@pytest.mark.parametrize("K,offset", [(2, 0), (3, 5), (8, 1), (13, 0)])
+def test_leapfrog_coverage_reinterleaves_base(orc, gen, seed, K, offset):
+    # S L418: the K player sequences, re-interleaved round-robin, equal the base
+    # sequence over K*horizon draws; a player offset o starts at base draw K*o.
+    h = 40
+    base = orc.generate(gen, seed, 1, K * (offset + h))[0]
+    lf = orc.generate(gen, seed, K, h, spacing=W.SPACING_LEAPFROG, players=K, offset=offset)
+    assert np.array_equal(lf.T.reshape(-1), base[K * offset:])
+    # a sub-range of players (a rank's share) is the same rows
+    sub = orc.generate(gen, seed, 2, h, spacing=W.SPACING_LEAPFROG, players=K, offset=offset,
+                       first=K - 2)
+    assert np.array_equal(sub, lf[K - 2:])
+
+
+def test_leapfrog_mrg_far_players_vs_curand(orc, curand_pin):
+    # Large K and offsets: player p draw t is base draw d = p + K*(o+t),
+    # checked against cuRAND's skipahead (a different jump implementation).
+    s = [12345] * 6
+    for K, p, o in ((1 << 40, 12345, 7), (1000003, 999999, 1 << 30), (3, 2, 1 << 61)):
+        row = orc.generate(W.MRG32K3A, s, 1, 3, spacing=W.SPACING_LEAPFROG, players=K, first=p,
+                           offset=o)[0]
+        for t in range(3):
+            d = p + K * (o + t)
+            st = curand_pin.ask("mrgskip", *s, 0, 0, d)
+            assert int(row[t]) == curand_pin.ask("mrg", *st, 1)[0], (K, p, o, t)
+
+
+def test_leapfrog_philox_far_players_vs_curand(orc, curand_pin):
+    seed = 12345 | (678 << 32)
+    for K, p, o in ((1 << 40, 12345, 7), (1000003, 999999, 1 << 30), (5, 4, 1 << 61)):
+        row = orc.generate(W.PHILOX4X32_10, [12345, 678], 1, 3, spacing=W.SPACING_LEAPFROG,
+                           players=K, first=p, offset=o)[0]
+        for t in range(3):
+            d = p + K * (o + t)
+            assert int(row[t]) == curand_pin.ask("pstream", seed, 0, d, 1)[0], (K, p, o, t)
+
+
+@pytest.mark.parametrize("gen,seed", LEAP_GENS)
+def test_leapfrog_conversions_and_dartboard_use_player_draws(orc, gen, seed):
+    # f64 / MC consume the player's own draws (R7, R9): Philox/Threefry f64 from
+    # two consecutive player draws; MRG one; MC sample k from player draws 2k, 2k+1.
+    K, h = 5, 64
+    u = orc.generate(gen, seed, K, 2 * h, spacing=W.SPACING_LEAPFROG, players=K).astype(np.uint64)
+    f = orc.generate(gen, seed, K, h, spacing=W.SPACING_LEAPFROG, players=K, kind=orc.F64)
+    for r in range(K):
+        for k in range(h):
+            if gen == W.MRG32K3A:
+                want = Fraction(int(u[r, k])) * Fraction(2.328306549295727688e-10)
+                assert f[r, k] == float(want)
+            else:
+                m = ((int(u[r, 2 * k + 1]) << 32 | int(u[r, 2 * k])) >> 11)
+                assert f[r, k] == m * 2.0 ** -53
+    tot, counts = orc.mc_count(gen, seed, K, h, spacing=W.SPACING_LEAPFROG, players=K)
+    X, Y = u[:, 0::2] >> 8, u[:, 1::2] >> 8
+    want = ((X * X + Y * Y) < (1 << 48)).sum(axis=1)
+    assert np.array_equal(counts, want) and tot == int(want.sum())
+
+
+def test_leapfrog_rejects_bad_plans(orc):
+    L = W.SPACING_LEAPFROG
+    with pytest.raises(ValueError):  # player id >= K
+        orc.generate(W.MRG32K3A, [1] * 6, 2, 4, spacing=L, players=3, first=2)
+    with pytest.raises(ValueError):  # TinyMT32 has no leap-frog layout here
+        orc.generate(W.TINYMT32, [1, 1, 1, 0x8F7011EE, 0xFC78FF1F, 0x3793FDFF], 1, 4, spacing=L,
+                     players=2)
+    with pytest.raises(ValueError):  # Philox base stream exhausted (2^66 draws)
+        orc.generate(W.PHILOX4X32_10, [1], 1, 4, spacing=L, players=1 << 40, offset=1 << 26)

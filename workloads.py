@@ -17,6 +17,7 @@ THREEFRY4X64_20 = 4
 SPACING_STREAM = 0
 SPACING_SUBSTREAM = 1
 SPACING_KEYED = 2
+SPACING_LEAPFROG = 3  # Leap Frog partition (P L118-122): players dealt one base sequence
 
 
 @dataclass(frozen=True)
