@@ -403,6 +403,17 @@ def main():
         shv.shv_streams_destroy(h)
         del st_t
 
+        # Leap Frog (NEXT-4, R17) on the C5 shape: 2^20 players of one base
+        # sequence x 4096 u32 per rank (rank r deals players [r*2^20, (r+1)*2^20)
+        # of K = world*2^20)
+        K = wm.n_streams * world
+        for key, gen, seed in (("leapfrog_mrg_fill_u32", W.MRG32K3A, wm.seed),
+                               ("leapfrog_philox_fill_u32", W.PHILOX4X32_10, wp.seed)):
+            h = shv.shv_streams_create_leapfrog(gen, list(seed), K, rank * wm.n_streams, wm.n_streams,
+                                                state if gen == W.MRG32K3A else None, 0, local, sp)
+            parts[key] = fill_part(fill_ms(h, out, n), total_per_rank)
+            shv.shv_streams_destroy(h)
+
         # C6: stream-count sweep at a fixed 2^32 u32 per GPU (16 GiB),
         # n_streams = 2^13 .. 2^22, n_per_stream = total / n_streams, both generators.
         # Acceptance: every point within 10% of the C5 (2^20 x 4096) figure.

@@ -18,6 +18,8 @@
  *   Philox4x32-10, SHV_SPACING_KEYED : key = (first+i, tag), counter (blk_lo, blk_hi, 0, 0)
  *   Threefry4x64-20 (STREAM)        : ctr = (blk, first+i, 0, 0), key from the seed words (R16)
  *   TinyMT32 (shv_streams_create_tinymt32): parameter set per group, 2^64-draw slices (R15)
+ *   SHV_SPACING_LEAPFROG (shv_streams_create_leapfrog): player first+i of K
+ *                                     receives base draws p, p+K, ... (P L118-122 [§2.3]; R17)
  * Every stream of a handle sits at the same draw offset o (u128), which each
  * generate / mc_pi call advances by the draws it consumed (S L58; R8).
  *
@@ -72,13 +74,14 @@ typedef enum {
 typedef enum {
     SHV_SPACING_STREAM = 0,     /* MRG: 2^127 draws apart; Philox: counter-stream index */
     SHV_SPACING_SUBSTREAM = 1,  /* MRG: 2^76 draws apart; Philox: SHV_ERR_UNSUPPORTED */
-    SHV_SPACING_KEYED = 2       /* Philox only: Parameterization, one key per stream
+    SHV_SPACING_KEYED = 2,      /* Philox only: Parameterization, one key per stream
                                    (P L331-334 "a single key that can be set at runtime
                                    according to each thread's unique identifier"; S L249-257):
                                    key = (first+i, tag), counter = (blk_lo, blk_hi, 0, 0);
                                    seed = 1 word, the experiment tag; first+n <= 2^32
                                    (else SHV_ERR_INSUFFICIENT_STREAMS, S L253 KeySpaceExhausted).
                                    MRG: SHV_ERR_UNSUPPORTED */
+    SHV_SPACING_LEAPFROG = 3    /* Leap Frog partition; handles from shv_streams_create_leapfrog */
 } shv_spacing;
 
 typedef enum {
@@ -96,6 +99,7 @@ typedef struct {
     uint32_t seed[6];     /* MRG: s10 s11 s12 s20 s21 s22; Philox: key0 key1 0 0 0 0 */
     uint64_t first_stream, n_streams;
     uint64_t offset_lo, offset_hi;
+    uint64_t players;     /* SHV_SPACING_LEAPFROG: K; otherwise 0 */
 } shv_position;
 
 /* Bytes of per-stream state a handle needs: MRG32k3a 24*n_streams (six u32
@@ -154,6 +158,30 @@ shv_status shv_jump(shv_streams h, int kind, uint64_t n);
 shv_status shv_streams_create_tinymt32(shv_streams* out, const uint32_t* params, size_t n_params,
                                        uint32_t seed, uint32_t group_size, uint64_t first_stream,
                                        uint64_t n_streams, void* d_state, size_t state_bytes,
+                                       int device, void* cuda_stream);
+
+/* Leap Frog handles (NEXT-4; P L118-122 [§2.3]: "Assigning random sequences
+ * ... like a deck of cards dealt to card players"; S L397-424; R17). One base
+ * sequence is dealt round-robin to `players` (K >= 1) players: handle stream i
+ * is player p = first_player + i and its draw t is base draw p + K*t (t counted
+ * from the handle offset o, which counts the player's own draws). Base
+ * sequence: MRG32k3a stream 0 of the seed (seed words as create_ex);
+ * Philox4x32-10 / Threefry4x64-20 counter stream 0 of the key (ctr[2..3] = 0
+ * resp. ctr[1] = 0). TinyMT32: SHV_ERR_UNSUPPORTED. first_player + n_players
+ * must be <= players (else SHV_ERR_INSUFFICIENT_STREAMS). generate_* and
+ * mc_pi* work as for any handle (f64 / MC consume the player's own draws,
+ * R7, R9); shv_jump takes SHV_JUMP_DRAWS only (player draws); a call whose
+ * last base draw would leave the base stream (Philox 2^66, Threefry 2^67,
+ * MRG 2^128 draws) fails with SHV_ERR_INVALID_ARGUMENT. The device view
+ * (shv_get_device_view) is SHV_ERR_UNSUPPORTED for these handles.
+ *  d_state: MRG32k3a only, shv_state_bytes(MRG, n_players) bytes or NULL: the
+ *    base state A^p * seed of each player (SoA, P L257-258), seeded on
+ *    cuda_stream as in create_ex. Kernels step a player with the order-3
+ *    recurrence that A^K's characteristic polynomial gives each component
+ *    (DESIGN.md §4.6): 6 modular products per draw for any K. */
+shv_status shv_streams_create_leapfrog(shv_streams* out, int gen, const uint32_t* seed,
+                                       size_t seed_words, uint64_t players, uint64_t first_player,
+                                       uint64_t n_players, void* d_state, size_t state_bytes,
                                        int device, void* cuda_stream);
 
 /* Bulk fill (P L485-490 [Listing 1] with n_per_stream draws per stream):
@@ -224,7 +252,7 @@ const char* shv_last_error_message(void);
 /* ---- launch configuration (results never depend on it; R10) ---- */
 /* Override the persistent-grid shape and work split of one handle:
  * blocks_per_sm (0 = occupancy maximum), threads_per_block (0 = 256,
- * else a multiple of 32 in [32, 1024]), segment (0 = automatic; else the
+ * else a multiple of 32 in [32, 256]), segment (0 = automatic; else the
  * number of draws-per-value units one work item covers, a multiple of 8). */
 shv_status shv_set_launch_config(shv_streams h, uint32_t blocks_per_sm,
                                  uint32_t threads_per_block, uint64_t segment);

@@ -33,6 +33,7 @@ SHV_GEN_THREEFRY4X64_20 = 4
 SHV_SPACING_STREAM = 0
 SHV_SPACING_SUBSTREAM = 1
 SHV_SPACING_KEYED = 2
+SHV_SPACING_LEAPFROG = 3
 SHV_JUMP_DRAWS = 0
 SHV_JUMP_SUBSTREAMS = 1
 SHV_JUMP_STREAMS = 2
@@ -44,7 +45,7 @@ EXPORTS = (
     "shv_mc_pi", "shv_mc_pi_ex", "shv_get_position", "shv_streams_destroy",
     "shv_status_string", "shv_last_error_message", "shv_set_launch_config",
     "shv_partition", "shv_jump_matrix", "shv_build_info", "shv_get_device_view",
-    "shv_streams_create_tinymt32",
+    "shv_streams_create_tinymt32", "shv_streams_create_leapfrog",
 )
 
 
@@ -57,7 +58,7 @@ class ShvError(RuntimeError):
 class shv_position(C.Structure):
     _fields_ = [("gen", C.c_uint32), ("spacing", C.c_uint32), ("seed", C.c_uint32 * 6),
                 ("first_stream", C.c_uint64), ("n_streams", C.c_uint64),
-                ("offset_lo", C.c_uint64), ("offset_hi", C.c_uint64)]
+                ("offset_lo", C.c_uint64), ("offset_hi", C.c_uint64), ("players", C.c_uint64)]
 
 
 class shv_device_view(C.Structure):
@@ -100,6 +101,8 @@ def _load():
         "shv_get_device_view": (st, [u64, C.POINTER(shv_device_view)]),
         "shv_streams_create_tinymt32": (st, [C.POINTER(u64), u32p, C.c_size_t, C.c_uint32, C.c_uint32,
                                              u64, u64, vp, C.c_size_t, C.c_int, vp]),
+        "shv_streams_create_leapfrog": (st, [C.POINTER(u64), C.c_int, u32p, C.c_size_t, u64, u64, u64,
+                                             vp, C.c_size_t, C.c_int, vp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -176,6 +179,19 @@ def shv_streams_create_tinymt32(params, seed: int, group_size: int, first_stream
     return h.value
 
 
+def shv_streams_create_leapfrog(gen: int, seed, players: int, first_player: int, n_players: int,
+                                d_state=None, state_bytes: int = 0, device: int = -1,
+                                stream=None) -> int:
+    """Leap Frog handle: row i is player first_player + i of ``players`` (R17)."""
+    h = C.c_uint64(0)
+    arr, nw = _seed(seed)
+    if d_state is not None and not isinstance(d_state, int) and not state_bytes:
+        state_bytes = d_state.numel() * d_state.element_size()
+    _check(lib.shv_streams_create_leapfrog(C.byref(h), gen, arr, nw, players, first_player, n_players,
+                                           _ptr(d_state), state_bytes, device, _stream(stream)))
+    return h.value
+
+
 def shv_jump(h: int, kind: int, n: int):
     _check(lib.shv_jump(h, kind, n))
 
@@ -210,7 +226,7 @@ def shv_get_position(h: int) -> dict:
     _check(lib.shv_get_position(h, C.byref(p)))
     return {"gen": p.gen, "spacing": p.spacing, "seed": list(p.seed),
             "first_stream": p.first_stream, "n_streams": p.n_streams,
-            "offset": p.offset_lo | (p.offset_hi << 64)}
+            "offset": p.offset_lo | (p.offset_hi << 64), "players": p.players}
 
 
 def shv_get_device_view(h: int) -> shv_device_view:

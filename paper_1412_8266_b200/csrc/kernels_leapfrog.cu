@@ -1,0 +1,272 @@
+// kernels_leapfrog.cu — Leap Frog partition kernels (NEXT-4; P L118-122
+// [§2.3]: one base sequence "dealt" round-robin to K players; R17): bulk fills
+// (u32 / f32 / f64) and the fused Monte Carlo pi kernel for MRG32k3a,
+// Philox4x32-10 and Threefry4x64-20 handles.
+//
+// Player p's draw t is base draw p + K*t. Counter-based generators compute it
+// directly (one block per draw; a cached block serves K < words-per-block).
+// MRG32k3a cannot skip K-1 draws for free, so each component of the player's
+// subsequence is stepped by the order-3 linear recurrence that the
+// characteristic polynomial of B = A^K gives (Cayley-Hamilton: B^3 = tr(B) B^2
+// - M2(B) B + det(B) I, so u_{t+3} = tr u_{t+2} - M2 u_{t+1} + det u_t for any
+// linear functional u_t of B^t w): 3 modular products per component and draw,
+// independent of K. The host builds the coefficients, B, and
+// the segment start jumps.
+#include "kernels_common.cuh"
+
+namespace shv {
+namespace {
+
+// (c0 u0 + c1 u1 + c2 u2) mod (2^32 - C), all operands < 2^32 - C. The three
+// 64-bit products are summed with carries (s = cy*2^64 + s2), then folded with
+// 2^32 = C and 2^64 = C^2: x < 2^46.6, one more fold gives < 2m.
+template <uint32_t C>
+__device__ __forceinline__ uint32_t dot3(uint32_t c0, uint32_t u0, uint32_t c1, uint32_t u1, uint32_t c2,
+                                         uint32_t u2)
+{
+    const uint64_t p0 = (uint64_t)c0 * u0, p1 = (uint64_t)c1 * u1, p2 = (uint64_t)c2 * u2;
+    const uint64_t s = p0 + p1;
+    const uint64_t s2 = s + p2;
+    const uint32_t cy = (uint32_t)(s < p0) + (uint32_t)(s2 < s);
+    uint64_t x = (s2 >> 32) * C + (uint32_t)s2 + (uint64_t)cy * ((uint64_t)C * C);
+    x = (x >> 32) * C + (uint32_t)x;
+    const uint64_t m = (1ull << 32) - C;
+    return (uint32_t)(x >= m ? x - m : x);
+}
+
+using u128 = unsigned __int128;
+
+template <int G>
+struct LeapCursor;
+
+// MRG32k3a player: (x0, x1, x2) = newest component-1 words of the states at
+// player draws t, t+1, t+2 (likewise y for component 2); draw t is their
+// combination (R2).
+template <>
+struct LeapCursor<kLeapMrg> {
+    uint32_t x0, x1, x2, y0, y1, y2;
+
+    __device__ __forceinline__ void init(const LeapLaunch& P, uint64_t i, uint64_t j)
+    {
+        const uint32_t* st = P.state;
+        const uint64_t n = P.stride, q = P.stream_begin + i;
+        Mrg s{__ldg(st + q), __ldg(st + n + q), __ldg(st + 2 * n + q),
+              __ldg(st + 3 * n + q), __ldg(st + 4 * n + q), __ldg(st + 5 * n + q)};
+        apply(P.start.a, P.start.b, s);  // A^(1 + K*o) A^p seed: state of player draw o
+        for (int b = 0; j; ++b, j >>= 1)  // segment j starts j*seg_draws player draws later
+            if (j & 1) apply(P.segpow[b].a, P.segpow[b].b, s);
+        x0 = s.x2;
+        y0 = s.y2;
+        apply(P.B.a, P.B.b, s);
+        x1 = s.x2;
+        y1 = s.y2;
+        apply(P.B.a, P.B.b, s);
+        x2 = s.x2;
+        y2 = s.y2;
+    }
+
+    __device__ __forceinline__ uint32_t next(const LeapLaunch& P)
+    {
+        const uint32_t z = mrg_combine(x0, y0);
+        const uint32_t nx = dot3<kC1>(P.cp1[0], x0, P.cp1[1], x1, P.cp1[2], x2);
+        const uint32_t ny = dot3<kC2>(P.cp2[0], y0, P.cp2[1], y1, P.cp2[2], y2);
+        x0 = x1;
+        x1 = x2;
+        x2 = nx;
+        y0 = y1;
+        y1 = y2;
+        y2 = ny;
+        return z;
+    }
+};
+
+// Counter-based player: next base draw index d (u128), advanced by K.
+template <>
+struct LeapCursor<kLeapPhilox> {
+    u128 d;
+    uint64_t cb;
+    bool valid;
+    W4 v;
+
+    __device__ __forceinline__ void init(const LeapLaunch& P, uint64_t i, uint64_t j)
+    {
+        const u128 o = ((u128)P.o_hi << 64) | P.o_lo;
+        d = (u128)(P.first + i) + (u128)P.players * (o + (u128)j * P.seg_draws);
+        valid = false;
+    }
+
+    __device__ __forceinline__ uint32_t next(const LeapLaunch& P)
+    {
+        const uint64_t b = (uint64_t)(d >> 2);
+        if (!valid || b != cb) {
+            v = philox_blk(b, 0, (uint32_t)P.k0, (uint32_t)P.k1);
+            cb = b;
+            valid = true;
+        }
+        const uint32_t w = (uint32_t)d & 3;
+        d += P.players;
+        return w == 0 ? v.x : w == 1 ? v.y : w == 2 ? v.z : v.w;
+    }
+};
+
+template <>
+struct LeapCursor<kLeapThreefry> {
+    u128 d;
+    uint64_t cb;
+    bool valid;
+    Q4 v;
+
+    __device__ __forceinline__ void init(const LeapLaunch& P, uint64_t i, uint64_t j)
+    {
+        const u128 o = ((u128)P.o_hi << 64) | P.o_lo;
+        d = (u128)(P.first + i) + (u128)P.players * (o + (u128)j * P.seg_draws);
+        valid = false;
+    }
+
+    __device__ __forceinline__ uint32_t next(const LeapLaunch& P)
+    {
+        const uint64_t b = (uint64_t)(d >> 3);
+        if (!valid || b != cb) {
+            v = threefry20(b, 0, P.k0, P.k1);
+            cb = b;
+            valid = true;
+        }
+        const uint32_t w = (uint32_t)d & 7;
+        d += P.players;
+        const uint64_t lane = (w >> 1) == 0 ? v.x : (w >> 1) == 1 ? v.y : (w >> 1) == 2 ? v.z : v.w;
+        return (w & 1) ? (uint32_t)(lane >> 32) : (uint32_t)lane;
+    }
+};
+
+template <int G, int KIND>
+__device__ __forceinline__ OutT<KIND> leap_value(LeapCursor<G>& c, const LeapLaunch& P)
+{
+    const uint32_t w = c.next(P);
+    if constexpr (KIND == kU32) return w;
+    else if constexpr (KIND == kF32) return to_f32(w);
+    else if constexpr (G == kLeapMrg) return mrg_f64(w);
+    else return philox_f64(w, c.next(P));  // two player draws per double (R7)
+}
+
+// Fill: each thread writes one segment of one row. VEC: 32-byte aligned
+// rows and seg_len % 8 == 0, so every 8 values (u32/f32) or 4 (f64) leave as
+// one 32-byte store.
+template <int G, int KIND, bool VEC>
+__global__ void __launch_bounds__(256) leap_fill_kernel(const __grid_constant__ LeapLaunch P)
+{
+    using T = OutT<KIND>;
+    const uint64_t nthr = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t it = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; it < P.items; it += nthr) {
+        const uint64_t j = it / P.ns;
+        const uint64_t i = it - j * P.ns;
+        const uint64_t c0 = j * P.seg_len;
+        const uint64_t len = min(P.seg_len, P.n - c0);
+        LeapCursor<G> cur;
+        cur.init(P, i, j);
+        T* o = reinterpret_cast<T*>(P.out) + i * P.n + c0;
+        if (VEC) {
+            for (uint64_t t = 0; t < len; t += 8) {
+                if (KIND == kF64) {
+                    const double a = leap_value<G, KIND>(cur, P), b = leap_value<G, KIND>(cur, P),
+                                 c = leap_value<G, KIND>(cur, P), d = leap_value<G, KIND>(cur, P);
+                    st_v4d(o + t, a, b, c, d);
+                    const double e = leap_value<G, KIND>(cur, P), f = leap_value<G, KIND>(cur, P),
+                                 g = leap_value<G, KIND>(cur, P), h = leap_value<G, KIND>(cur, P);
+                    st_v4d(o + t + 4, e, f, g, h);
+                } else {
+                    uint32_t v[8];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) {
+                        const T x = leap_value<G, KIND>(cur, P);
+                        v[u] = KIND == kF32 ? __float_as_uint((float)x) : (uint32_t)x;
+                    }
+                    st_v8(o + t, v[0], v[1], v[2], v[3], v[4], v[5], v[6], v[7]);
+                }
+            }
+        } else {
+            for (uint64_t t = 0; t < len; ++t) o[t] = leap_value<G, KIND>(cur, P);
+        }
+    }
+}
+
+// Fused Monte Carlo: sample k of a player uses its draws 2k, 2k+1 (R9).
+template <int G>
+__global__ void __launch_bounds__(256) leap_mc_kernel(const __grid_constant__ LeapLaunch P)
+{
+    const uint64_t nthr = (uint64_t)gridDim.x * blockDim.x;
+    uint64_t total = 0;
+    for (uint64_t it = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; it < P.items; it += nthr) {
+        const uint64_t j = it / P.ns;
+        const uint64_t i = it - j * P.ns;
+        const uint64_t k0 = j * P.seg_len;
+        const uint32_t len = (uint32_t)min(P.seg_len, P.n - k0);
+        LeapCursor<G> cur;
+        cur.init(P, i, j);
+        uint32_t h = 0;
+        for (uint32_t k = 0; k < len; ++k) {
+            const uint32_t w0 = cur.next(P);
+            h += hit(w0, cur.next(P));
+        }
+        total += h;
+        if (P.counts) atomicAdd(P.counts + i, (unsigned long long)h);
+    }
+    block_reduce_add(total, P.hits);
+}
+
+template <int G>
+cudaError_t fill_g(const LeapLaunch& p, int kind, bool vec, Grid g, cudaStream_t s)
+{
+    if (vec) {
+        if (kind == kU32) leap_fill_kernel<G, kU32, true><<<g.blocks, g.threads, 0, s>>>(p);
+        else if (kind == kF32) leap_fill_kernel<G, kF32, true><<<g.blocks, g.threads, 0, s>>>(p);
+        else leap_fill_kernel<G, kF64, true><<<g.blocks, g.threads, 0, s>>>(p);
+    } else {
+        if (kind == kU32) leap_fill_kernel<G, kU32, false><<<g.blocks, g.threads, 0, s>>>(p);
+        else if (kind == kF32) leap_fill_kernel<G, kF32, false><<<g.blocks, g.threads, 0, s>>>(p);
+        else leap_fill_kernel<G, kF64, false><<<g.blocks, g.threads, 0, s>>>(p);
+    }
+    return cudaGetLastError();
+}
+
+template <int G>
+cudaError_t occ_fill_g(int kind, bool vec, int threads, int* out)
+{
+    if (kind == kU32) return vec ? occ(leap_fill_kernel<G, kU32, true>, threads, 0, out)
+                                 : occ(leap_fill_kernel<G, kU32, false>, threads, 0, out);
+    if (kind == kF32) return vec ? occ(leap_fill_kernel<G, kF32, true>, threads, 0, out)
+                                 : occ(leap_fill_kernel<G, kF32, false>, threads, 0, out);
+    return vec ? occ(leap_fill_kernel<G, kF64, true>, threads, 0, out)
+               : occ(leap_fill_kernel<G, kF64, false>, threads, 0, out);
+}
+
+}  // namespace
+
+cudaError_t launch_leap_fill(const LeapLaunch& p, int lgen, int kind, bool vec, Grid g, cudaStream_t s)
+{
+    if (lgen == kLeapMrg) return fill_g<kLeapMrg>(p, kind, vec, g, s);
+    if (lgen == kLeapPhilox) return fill_g<kLeapPhilox>(p, kind, vec, g, s);
+    return fill_g<kLeapThreefry>(p, kind, vec, g, s);
+}
+
+cudaError_t launch_leap_mc(const LeapLaunch& p, int lgen, Grid g, cudaStream_t s)
+{
+    if (lgen == kLeapMrg) leap_mc_kernel<kLeapMrg><<<g.blocks, g.threads, 0, s>>>(p);
+    else if (lgen == kLeapPhilox) leap_mc_kernel<kLeapPhilox><<<g.blocks, g.threads, 0, s>>>(p);
+    else leap_mc_kernel<kLeapThreefry><<<g.blocks, g.threads, 0, s>>>(p);
+    return cudaGetLastError();
+}
+
+cudaError_t leap_occupancy(int kernel, int kind, bool fast, int threads, int* out)
+{
+    switch (kernel) {
+    case leap_kernel_id(kKLeapFill, kLeapMrg): return occ_fill_g<kLeapMrg>(kind, fast, threads, out);
+    case leap_kernel_id(kKLeapFill, kLeapPhilox): return occ_fill_g<kLeapPhilox>(kind, fast, threads, out);
+    case leap_kernel_id(kKLeapFill, kLeapThreefry): return occ_fill_g<kLeapThreefry>(kind, fast, threads, out);
+    case leap_kernel_id(kKLeapMc, kLeapMrg): return occ(leap_mc_kernel<kLeapMrg>, threads, 0, out);
+    case leap_kernel_id(kKLeapMc, kLeapPhilox): return occ(leap_mc_kernel<kLeapPhilox>, threads, 0, out);
+    case leap_kernel_id(kKLeapMc, kLeapThreefry): return occ(leap_mc_kernel<kLeapThreefry>, threads, 0, out);
+    }
+    return cudaErrorInvalidValue;
+}
+
+}  // namespace shv

@@ -27,8 +27,9 @@
 namespace shv {
 
 // Jump tables: [0][b] = A^(2^(76+b)) (substreams, b < 51),
-//              [1][b] = A^(2^(127+b)) (streams, b < 64).
-__device__ MatPair g_jump_tab[2][64];
+//              [1][b] = A^(2^(127+b)) (streams, b < 64),
+//              [2][b] = A^(2^b) (draws: Leap Frog players, b < 64).
+__device__ MatPair g_jump_tab[3][64];
 
 namespace {
 
@@ -260,11 +261,12 @@ size_t mrg_fill_smem(int threads, int kind)
     return staged ? staged_smem(threads) : 0;
 }
 
-cudaError_t upload_jump_tables(const MatPair* sub51, const MatPair* str64)
+cudaError_t upload_jump_tables(const MatPair* sub51, const MatPair* str64, const MatPair* draw64)
 {
-    MatPair h[2][64] = {};
+    MatPair h[3][64] = {};
     for (int b = 0; b < 51; ++b) h[0][b] = sub51[b];
     for (int b = 0; b < 64; ++b) h[1][b] = str64[b];
+    for (int b = 0; b < 64; ++b) h[2][b] = draw64[b];
     return cudaMemcpyToSymbol(g_jump_tab, h, sizeof h);
 }
 

@@ -166,6 +166,7 @@ struct Handle {
     uint64_t group0 = 0;
     uint32_t group_size = 0;
     cudaStream_t home = nullptr;  // stream of create: TinyMT jumps are enqueued there
+    uint64_t players = 0;         // Leap Frog: K (spacing SHV_SPACING_LEAPFROG)
 };
 
 TinyMtLaunch tm_launch(const Handle& h, uint64_t s0, uint64_t ns)
@@ -219,10 +220,11 @@ shv_status ensure_tables(int dev)
     std::lock_guard<std::mutex> lk(g_mu);
     if (dev < 0 || dev >= 64) return fail(SHV_ERR_INVALID_ARGUMENT, "device %d out of range", dev);
     if (g_tables_on[dev]) return SHV_OK;
-    MatPair sub[51], str[64];
+    MatPair sub[51], str[64], drw[64];
     for (int b = 0; b < 51; ++b) sub[b] = pair_pow(1, 76 + b);
     for (int b = 0; b < 64; ++b) str[b] = pair_pow(1, 127 + b);
-    cudaError_t e = upload_jump_tables(sub, str);
+    for (int b = 0; b < 64; ++b) drw[b] = pair_pow(1, b);
+    cudaError_t e = upload_jump_tables(sub, str, drw);
     if (e != cudaSuccess) return cuda_fail(e, "upload_jump_tables");
     g_tables_on[dev] = true;
     return SHV_OK;
@@ -294,8 +296,25 @@ void split(const Handle& h, uint64_t ns, uint64_t len, uint64_t align, uint64_t 
     *nseg = (uint32_t)(S ? S : 1);
 }
 
+// Leap Frog: the last base draw a call touches is (first+n-1) + K*(o+draws-1);
+// it must exist in the base stream (R17).
+shv_status check_leap_advance(const Handle& h, u128 draws)
+{
+    const u128 top = ~(u128)0;
+    const u128 K = h.players;
+    if (draws == 0) return SHV_OK;
+    if (h.offset > top - draws || h.offset + draws > top / K)
+        return fail(SHV_ERR_INVALID_ARGUMENT, "Leap Frog position would exceed 2^128 base draws");
+    const u128 last = (u128)(h.first + h.n - 1) + K * (h.offset + draws - 1);
+    const int lim = h.gen == SHV_GEN_PHILOX4X32_10 ? 66 : h.gen == SHV_GEN_THREEFRY4X64_20 ? 67 : 128;
+    if (lim < 128 && last >= ((u128)1 << lim))
+        return fail(SHV_ERR_INVALID_ARGUMENT, "Leap Frog base stream exhausted (2^%d draws)", lim);
+    return SHV_OK;
+}
+
 shv_status check_advance(const Handle& h, u128 draws)
 {
+    if (h.spacing == SHV_SPACING_LEAPFROG) return check_leap_advance(h, draws);
     if (h.gen == SHV_GEN_THREEFRY4X64_20) {
         if (draws > ((u128)1 << 67) || h.offset > ((u128)1 << 67) - draws)
             return fail(SHV_ERR_INVALID_ARGUMENT, "Threefry stream exhausted (2^67 draws per stream)");
@@ -332,6 +351,81 @@ void counter_tasks(const Handle& h, uint64_t ns, uint64_t cpr, uint64_t resident
     while (!h.seg && R > 1 && tasks(R) < 4 * rwarps) R /= 2;
     *R_out = (uint32_t)R;
     *tasks_out = tasks(R);
+}
+
+// ---------------------------------------------------------------- Leap Frog (R17)
+
+uint32_t mulmod(uint64_t a, uint64_t b, uint64_t m) { return (uint32_t)((u128)a * b % m); }
+
+// Coefficients of u_{t+3} = cp[2] u_{t+2} + cp[1] u_{t+1} + cp[0] u_t for the
+// order-3 recurrence B's characteristic polynomial gives (Cayley-Hamilton:
+// B^3 = tr B^2 - M2 B + det I; M2 = sum of the principal 2x2 minors).
+void charpoly(const uint32_t* B, int comp, uint32_t cp[3])
+{
+    const uint64_t m = kMod[comp];
+    auto e = [&](int r, int c) -> uint64_t { return B[3 * r + c]; };
+    auto minor = [&](int a, int b) -> uint64_t {  // B[a][a] B[b][b] - B[a][b] B[b][a] (mod m)
+        return (mulmod(e(a, a), e(b, b), m) + m - mulmod(e(a, b), e(b, a), m)) % m;
+    };
+    const uint64_t tr = (e(0, 0) + e(1, 1) + e(2, 2)) % m;
+    const uint64_t m2 = (minor(0, 1) + minor(0, 2) + minor(1, 2)) % m;
+    const uint64_t c0 = (mulmod(e(1, 1), e(2, 2), m) + m - mulmod(e(1, 2), e(2, 1), m)) % m;
+    const uint64_t c1 = (mulmod(e(1, 0), e(2, 2), m) + m - mulmod(e(1, 2), e(2, 0), m)) % m;
+    const uint64_t c2 = (mulmod(e(1, 0), e(2, 1), m) + m - mulmod(e(1, 1), e(2, 0), m)) % m;
+    const uint64_t det = (mulmod(e(0, 0), c0, m) + m - mulmod(e(0, 1), c1, m) + mulmod(e(0, 2), c2, m)) % m;
+    cp[2] = (uint32_t)tr;
+    cp[1] = (uint32_t)((m - m2) % m);
+    cp[0] = (uint32_t)det;
+}
+
+int leap_gen(int gen) { return gen == SHV_GEN_MRG32K3A ? kLeapMrg : gen == SHV_GEN_PHILOX4X32_10 ? kLeapPhilox : kLeapThreefry; }
+
+// A Leap Frog launch over handle rows [s0, s0+ns): len units per row (values
+// or samples), dpv player draws per unit. Segments of >= 64 units (a MRG
+// segment start costs up to 35 mat-vecs), enough work items for 8 waves.
+std::unique_ptr<LeapLaunch> leap_launch(const Handle& h, uint64_t s0, uint64_t ns, uint64_t len, uint64_t dpv,
+                                        uint64_t align, uint64_t resident)
+{
+    auto P = std::make_unique<LeapLaunch>();
+    uint64_t L;
+    if (h.seg) {
+        L = h.seg;
+    } else {
+        const uint64_t target = 8 * resident;
+        const uint64_t S = (target + ns - 1) / ns;
+        L = (len + S - 1) / S;
+        if (L < 64) L = 64;
+    }
+    L = (L + align - 1) / align * align;
+    if (L > (1ull << 31)) L = (1ull << 31) / align * align;  // MC: per-item counts fit in u32
+    const uint64_t nseg = (len + L - 1) / L;
+    P->players = h.players;
+    P->first = h.first + s0;
+    P->ns = ns;
+    P->o_lo = (uint64_t)h.offset;
+    P->o_hi = (uint64_t)(h.offset >> 64);
+    P->seg_len = L;
+    P->seg_draws = L * dpv;
+    P->n = len;
+    P->items = ns * nseg;
+    if (h.gen == SHV_GEN_PHILOX4X32_10) {
+        P->k0 = h.seed[0];
+        P->k1 = h.seed[1];
+    } else if (h.gen == SHV_GEN_THREEFRY4X64_20) {
+        P->k0 = (uint64_t)h.seed[0] | ((uint64_t)h.seed[1] << 32);
+        P->k1 = (uint64_t)h.seed[2] | ((uint64_t)h.seed[3] << 32);
+    } else {
+        P->state = h.state;
+        P->stride = h.n;
+        P->stream_begin = s0;
+        P->B = pair_pow(h.players, 0);
+        charpoly(P->B.a, 0, P->cp1);
+        charpoly(P->B.b, 1, P->cp2);
+        P->start = pair_pow(1 + (u128)h.players * h.offset, 0);
+        P->segpow[0] = pair_pow((u128)h.players * P->seg_draws, 0);
+        for (int b = 1; b < kLeapSegBits && (nseg - 1) >> b; ++b) P->segpow[b] = pair_mul(P->segpow[b - 1], P->segpow[b - 1]);
+    }
+    return P;
 }
 
 template <typename T>
@@ -388,7 +482,16 @@ shv_status generate(shv_streams hid, T* out, uint64_t n, void* stream, int kind,
         T* dst = host_out ? stage[k & 1] : out;
         if (host_out && k >= 2) err = cudaStreamWaitEvent(s, copy_done[k & 1], 0);
         if (err != cudaSuccess) break;
-        if (h.gen == SHV_GEN_THREEFRY4X64_20) {
+        if (h.spacing == SHV_SPACING_LEAPFROG) {
+            const int lg = leap_gen(h.gen);
+            bool vec = aligned32 && (n % 8 == 0);
+            const int kid = leap_kernel_id(kKLeapFill, lg);
+            auto P = leap_launch(h, s0, ns, n, dpv, vec ? 8 : 1, resident_threads(h, kid, kind, vec));
+            if (vec && P->seg_len % 8) vec = false;
+            P->out = dst;
+            Grid g{blocks_for(h, kid, kind, vec, P->items), h.tpb};
+            err = launch_leap_fill(*P, lg, kind, vec, g, s);
+        } else if (h.gen == SHV_GEN_THREEFRY4X64_20) {
             const uint64_t E = kind == kF64 ? 4 : 8;
             const bool fast = aligned32 && (n % E == 0) && ((uint32_t)h.offset & 7) == 0;
             ThreefryLaunch P{};
@@ -709,6 +812,79 @@ shv_status shv_streams_create(shv_streams* out, int gen, const uint32_t* seed, s
                                  -1, nullptr);
 }
 
+shv_status shv_streams_create_leapfrog(shv_streams* out, int gen, const uint32_t* seed, size_t seed_words,
+                                       uint64_t players, uint64_t first_player, uint64_t n_players, void* d_state,
+                                       size_t state_bytes, int device, void* cuda_stream)
+{
+    Range nvtx_range("shv_streams_create_leapfrog");
+    if (!out) return fail(SHV_ERR_INVALID_ARGUMENT, "NULL out handle");
+    *out = 0;
+    if (gen == SHV_GEN_TINYMT32) return fail(SHV_ERR_UNSUPPORTED, "TinyMT32 has no Leap Frog layout (R17)");
+    uint32_t s6[6];
+    shv_status st = validate_seed(gen, seed, seed_words, s6);
+    if (st) return st;
+    if (players == 0) return fail(SHV_ERR_INVALID_ARGUMENT, "players must be >= 1");
+    if (n_players == 0) return fail(SHV_ERR_INVALID_ARGUMENT, "n_players must be >= 1");
+    if ((u128)first_player + n_players > players)
+        return fail(SHV_ERR_INSUFFICIENT_STREAMS, "players [%llu, %llu) beyond K = %llu",
+                    (unsigned long long)first_player, (unsigned long long)(first_player + n_players),
+                    (unsigned long long)players);
+    const size_t need = shv_state_bytes(SHV_GEN_MRG32K3A, n_players);
+    if (gen == SHV_GEN_MRG32K3A) {
+        if (need == 0) return fail(SHV_ERR_INVALID_ARGUMENT, "state size overflow");
+        if (d_state && state_bytes < need)
+            return fail(SHV_ERR_INVALID_ARGUMENT, "state buffer %zu B < %zu B", state_bytes, need);
+        if (d_state && ((uintptr_t)d_state & 3)) return fail(SHV_ERR_MISALIGNED, "state not 4-byte aligned");
+    }
+    int dev = device;
+    if (dev < 0) {
+        cudaError_t e = cudaGetDevice(&dev);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+    }
+    DeviceGuard dg(dev);
+    if (dg.err != cudaSuccess) return cuda_fail(dg.err, "cudaSetDevice");
+    auto h = std::make_shared<Handle>();
+    h->gen = gen;
+    h->spacing = SHV_SPACING_LEAPFROG;
+    h->device = dev;
+    memcpy(h->seed, s6, sizeof s6);
+    h->first = first_player;
+    h->n = n_players;
+    h->players = players;
+    cudaError_t e = cudaDeviceGetAttribute(&h->sms, cudaDevAttrMultiProcessorCount, dev);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaDeviceGetAttribute");
+    if (gen == SHV_GEN_MRG32K3A) {
+        st = ensure_tables(dev);
+        if (st) return st;
+        if (d_state) {
+            h->state = (uint32_t*)d_state;
+        } else {
+            e = cudaMalloc((void**)&h->state, need);
+            if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(state)");
+            h->own_state = true;
+        }
+        // Player p's base state A^p * seed: base A^first * seed, then per-bit
+        // single-draw tables (table 2) and the stride jump A^T.
+        uint32_t base[6];
+        memcpy(base, s6, sizeof base);
+        pair_apply(pair_pow(first_player, 0), base);
+        const uint64_t T = n_players < (1u << 16) ? (n_players + 255) / 256 * 256 : (1u << 16);
+        e = launch_mrg_seed(h->state, n_players, base, 2, pair_pow(T, 0), Grid{(unsigned)(T / 256), 256},
+                            (cudaStream_t)cuda_stream);
+        if (e != cudaSuccess) {
+            if (h->own_state) cudaFree(h->state);
+            return cuda_fail(e, "seed launch");
+        }
+    }
+    const uint64_t id = g_next_id.fetch_add(1);
+    {
+        std::lock_guard<std::mutex> lk(g_mu);
+        g_handles[id] = h;
+    }
+    *out = id;
+    return SHV_OK;
+}
+
 shv_status shv_jump(shv_streams hid, int kind, uint64_t n)
 {
     Range nvtx_range("shv_jump");
@@ -734,6 +910,7 @@ shv_status shv_jump(shv_streams hid, int kind, uint64_t n)
     if (kind == SHV_JUMP_DRAWS) {
         d = n;
     } else if (kind == SHV_JUMP_SUBSTREAMS || kind == SHV_JUMP_STREAMS) {
+        if (h.spacing == SHV_SPACING_LEAPFROG) return fail(SHV_ERR_UNSUPPORTED, "Leap Frog players jump by draws only");
         if (h.gen != SHV_GEN_MRG32K3A) return fail(SHV_ERR_UNSUPPORTED, "counter-based generators jump by draws only");
         const int sh = kind == SHV_JUMP_SUBSTREAMS ? 76 : 127;
         if (n >> (128 - sh)) return fail(SHV_ERR_INVALID_ARGUMENT, "jump exceeds 2^128 draws");
@@ -782,7 +959,15 @@ shv_status shv_mc_pi_ex(shv_streams hid, uint64_t samples, uint64_t* d_hits, uin
     cudaStream_t s = (cudaStream_t)stream;
     cudaError_t err;
     const uint64_t cap = 1ull << 31;  // per-item count fits in u32
-    if (h.gen == SHV_GEN_THREEFRY4X64_20) {
+    if (h.spacing == SHV_SPACING_LEAPFROG) {
+        const int lg = leap_gen(h.gen);
+        const int kid = leap_kernel_id(kKLeapMc, lg);
+        auto P = leap_launch(h, 0, h.n, samples, 2, 1, resident_threads(h, kid, 0, true));
+        P->hits = (unsigned long long*)d_hits;
+        P->counts = (unsigned long long*)d_counts;
+        Grid g{blocks_for(h, kid, 0, true, P->items), h.tpb};
+        err = launch_leap_mc(*P, lg, g, s);
+    } else if (h.gen == SHV_GEN_THREEFRY4X64_20) {
         const bool fast = ((uint32_t)h.offset & 7) == 0;
         ThreefryLaunch P{};
         P.k0 = (uint64_t)h.seed[0] | ((uint64_t)h.seed[1] << 32);
@@ -862,6 +1047,7 @@ shv_status shv_get_position(shv_streams hid, shv_position* out)
     out->n_streams = h.n;
     out->offset_lo = (uint64_t)h.offset;
     out->offset_hi = (uint64_t)(h.offset >> 64);
+    out->players = h.players;
     return SHV_OK;
 }
 
@@ -872,6 +1058,7 @@ shv_status shv_get_device_view(shv_streams hid, shv_device_view* out)
     if (!hp) return fail(SHV_ERR_LIFECYCLE, "unknown or destroyed handle");
     if (!out) return fail(SHV_ERR_INVALID_ARGUMENT, "NULL out");
     const Handle& h = *hp;
+    if (h.spacing == SHV_SPACING_LEAPFROG) return fail(SHV_ERR_UNSUPPORTED, "no device view for Leap Frog handles");
     memset(out, 0, sizeof *out);
     out->gen = (uint32_t)h.gen;
     out->spacing = (uint32_t)h.spacing;

@@ -98,12 +98,42 @@ struct TinyMtLaunch {
     unsigned long long* counts;
 };
 
+// Leap Frog launch (NEXT-4; R17). Work item it in [0, items): segment
+// j = it / ns, row i = it % ns (player p = first + i). Segment j covers values
+// [j*seg_len, min(n, (j+1)*seg_len)) of the row, i.e. player draws from
+// o + j*seg_len*dpv (dpv = draws per value, 2 for counter-based f64 and MC).
+enum LeapGen : int { kLeapMrg = 0, kLeapPhilox = 1, kLeapThreefry = 2 };
+constexpr int kLeapSegBits = 32;
+struct LeapLaunch {
+    uint64_t players;            // K
+    uint64_t first;              // player id of launch row 0
+    uint64_t ns;                 // rows in this launch
+    uint64_t o_lo, o_hi;         // counter-based: player draw offset o (u128)
+    uint64_t seg_draws;          // counter-based: player draws per segment
+    void* out;
+    uint64_t n;                  // fill: values per row; MC: samples per row
+    uint64_t seg_len;            // values (fill) or samples (MC) per segment
+    uint64_t items;              // ns * nseg
+    unsigned long long* hits;    // MC only
+    unsigned long long* counts;  // MC only, optional (indexed by launch row)
+    uint64_t k0, k1;             // Philox: key (k0, k1) (32-bit); Threefry: key lanes 0, 1
+    // MRG32k3a: state[k*stride + stream_begin + i] = word k of A^p * seed.
+    const uint32_t* state;
+    uint64_t stride;
+    uint64_t stream_begin;
+    uint32_t cp1[3], cp2[3];     // u_{t+3} = cp[2] u_{t+2} + cp[1] u_{t+1} + cp[0] u_t (mod m1 / m2)
+    MatPair B;                   // A^K
+    MatPair start;               // A^(1 + K*o)
+    MatPair segpow[kLeapSegBits];  // (A^(K*seg_draws))^(2^b)
+};
+
 struct Grid {
     unsigned blocks;
     unsigned threads;
 };
 
-// ---- launchers (kernels_mrg.cu, kernels_philox.cu, kernels_threefry.cu, kernels_tinymt32.cu) ----
+// ---- launchers (kernels_mrg.cu, kernels_philox.cu, kernels_threefry.cu, kernels_tinymt32.cu,
+//      kernels_leapfrog.cu) ----
 // TinyMT32: tables[g][b] = (T_g^(2^64))^(2^b), 128 columns x 4 words each.
 cudaError_t launch_threefry_fill(const ThreefryLaunch& p, int kind, bool fast, Grid g, cudaStream_t s);
 cudaError_t launch_threefry_mc(const ThreefryLaunch& p, bool fast, Grid g, cudaStream_t s);
@@ -114,14 +144,18 @@ cudaError_t launch_tinymt_seed(const TinyMtLaunch& p, uint32_t seed, const uint3
 cudaError_t launch_tinymt_fill(const TinyMtLaunch& p, int kind, bool vec, Grid g, cudaStream_t s);
 cudaError_t launch_tinymt_advance(const TinyMtLaunch& p, Grid g, cudaStream_t s);
 cudaError_t launch_tinymt_mc(const TinyMtLaunch& p, Grid g, cudaStream_t s);
-cudaError_t upload_jump_tables(const MatPair* sub51, const MatPair* str64);
-// T = g.blocks * g.threads seeding threads; step = A^(T * spacing).
+cudaError_t upload_jump_tables(const MatPair* sub51, const MatPair* str64, const MatPair* draw64);
+// T = g.blocks * g.threads seeding threads; step = A^(T * spacing); table 0
+// substreams, 1 streams, 2 single draws (Leap Frog players).
 cudaError_t launch_mrg_seed(uint32_t* state, uint64_t n, const uint32_t base[6], int table,
                             const MatPair& step, Grid g, cudaStream_t s);
 cudaError_t launch_mrg_fill(const MrgLaunch& p, int kind, bool vec, Grid g, cudaStream_t s);
 cudaError_t launch_mrg_mc(const MrgLaunch& p, Grid g, cudaStream_t s);
 cudaError_t launch_philox_fill(const PhiloxLaunch& p, int kind, bool fast, Grid g, cudaStream_t s);
 cudaError_t launch_philox_mc(const PhiloxLaunch& p, bool fast, Grid g, cudaStream_t s);
+// Leap Frog (kernels_leapfrog.cu): vec = 32-byte aligned rows, seg_len % 8 == 0.
+cudaError_t launch_leap_fill(const LeapLaunch& p, int lgen, int kind, bool vec, Grid g, cudaStream_t s);
+cudaError_t launch_leap_mc(const LeapLaunch& p, int lgen, Grid g, cudaStream_t s);
 
 // Which kernel an occupancy query refers to.
 enum KernelId : int {
@@ -136,13 +170,18 @@ enum KernelId : int {
     kKTinyMc = 8,
     kKThreefryFill = 9,
     kKThreefryMc = 10,
+    kKLeapFill = 11,  // kind = output kind; `fast` = vector path; generator via leap_kernel_id
+    kKLeapMc = 14,
 };
+// Leap kernels are keyed by (base id + generator): 11..13 fills, 14..16 MC.
+constexpr int leap_kernel_id(int base, int lgen) { return base + lgen; }
 // Occupancy of one kernel variant; each per-generator file answers for its own
 // ids (cudaErrorInvalidValue otherwise).
 cudaError_t mrg_occupancy(int kernel, int kind, bool fast, int threads, int* out);
 cudaError_t philox_occupancy(int kernel, int kind, bool fast, int threads, int* out);
 cudaError_t threefry_occupancy(int kernel, int kind, bool fast, int threads, int* out);
 cudaError_t tinymt_occupancy(int kernel, int kind, bool fast, int threads, int* out);
+cudaError_t leap_occupancy(int kernel, int kind, bool fast, int threads, int* out);
 inline cudaError_t max_blocks_per_sm(int kernel, int kind, bool fast, int threads, int* out)
 {
     switch (kernel) {
@@ -154,6 +193,8 @@ inline cudaError_t max_blocks_per_sm(int kernel, int kind, bool fast, int thread
         return threefry_occupancy(kernel, kind, fast, threads, out);
     case kKTinyFill: case kKTinyMc:
         return tinymt_occupancy(kernel, kind, fast, threads, out);
+    default:
+        if (kernel >= kKLeapFill && kernel < kKLeapMc + 3) return leap_occupancy(kernel, kind, fast, threads, out);
     }
     return cudaErrorInvalidValue;
 }

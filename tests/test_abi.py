@@ -141,3 +141,19 @@ def test_product_does_not_touch_oracle():
             if f.endswith((".py", ".cu", ".cpp", ".h", ".cuh")):
                 txt = open(os.path.join(dirpath, f)).read()
                 assert "oracle" not in txt.lower().replace("no cpu fallback", ""), f
+
+
+def test_leapfrog_validation_without_gpu(shv):
+    # Leap Frog handles (R17): rejected before any CUDA call
+    E = shv.ShvError
+    for args, code in (((shv.SHV_GEN_TINYMT32, [1], 4, 0, 4), shv.SHV_ERR_UNSUPPORTED),
+                       ((shv.SHV_GEN_PHILOX4X32_10, [1], 0, 0, 4), shv.SHV_ERR_INVALID_ARGUMENT),
+                       ((shv.SHV_GEN_PHILOX4X32_10, [1], 4, 0, 0), shv.SHV_ERR_INVALID_ARGUMENT),
+                       ((shv.SHV_GEN_PHILOX4X32_10, [1], 4, 2, 3), shv.SHV_ERR_INSUFFICIENT_STREAMS),
+                       ((shv.SHV_GEN_MRG32K3A, [1], (1 << 64) - 1, (1 << 64) - 2, 2),
+                        shv.SHV_ERR_INSUFFICIENT_STREAMS),
+                       ((shv.SHV_GEN_MRG32K3A, [0] * 6, 4, 0, 4), shv.SHV_ERR_INVALID_SEED),
+                       ((shv.SHV_GEN_THREEFRY4X64_20, [1] * 5, 4, 0, 4), shv.SHV_ERR_INVALID_ARGUMENT)):
+        with pytest.raises(E) as ei:
+            shv.shv_streams_create_leapfrog(*args, None, 0, 0, 0)
+        assert ei.value.status == code, args
