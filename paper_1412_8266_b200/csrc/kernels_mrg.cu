@@ -53,11 +53,29 @@ __device__ __forceinline__ Mrg load_state(const uint32_t* __restrict__ st, uint6
     return s;
 }
 
+// Work item -> (launch stream i, segment j): streams fastest (a warp = 32
+// rows, one segment), or segments fastest when rows are long (P.seg_fastest,
+// set by the host for rows > 512 KB: a stream-fastest warp would scatter its
+// 32 stores over 16+ different 2-MB pages).
+template <bool SEG_FASTEST>
+__device__ __forceinline__ void item_ij(const MrgLaunch& P, uint64_t it, uint64_t& i, uint64_t& j)
+{
+    if (SEG_FASTEST) {
+        i = it / P.nseg;
+        j = it - i * P.nseg;
+    } else {
+        j = it / P.ns;
+        i = it - j * P.ns;
+    }
+}
+
 // Start state of work item (stream i of the launch, segment j).
 __device__ __forceinline__ Gen item_state(const MrgLaunch& P, uint64_t i, uint64_t j)
 {
     Mrg s = load_state(P.state, P.stride, P.stream_begin + i);
-    apply(P.seg[j].a, P.seg[j].b, s);
+    apply(P.seg0.a, P.seg0.b, s);
+    for (int b = 0; j; ++b, j >>= 1)
+        if (j & 1) apply(P.segpow[b].a, P.segpow[b].b, s);
     return make_gen(s);
 }
 
@@ -119,7 +137,7 @@ __host__ __device__ constexpr bool mrg_staged()
     return SHV_MRG_STAGE == 2 || (SHV_MRG_STAGE == 1 && KIND == kF64);
 }
 
-template <int KIND>
+template <int KIND, bool SEG_FASTEST>
 __global__ void __launch_bounds__(256, SHV_MRG_MINB) mrg_fill_vec_kernel(const __grid_constant__ MrgLaunch P)
 {
     using T = OutT<KIND>;
@@ -136,8 +154,8 @@ __global__ void __launch_bounds__(256, SHV_MRG_MINB) mrg_fill_vec_kernel(const _
         uint64_t row = 0;
         Gen s{};
         if (it < P.items) {
-            const uint64_t j = it / P.ns;
-            const uint64_t i = it - j * P.ns;
+            uint64_t i, j;
+            item_ij<SEG_FASTEST>(P, it, i, j);
             s = item_state(P, i, j);
             const uint64_t c0 = j * P.seg_len;
             len = (uint32_t)min(P.seg_len, P.n - c0);
@@ -160,8 +178,8 @@ __global__ void __launch_bounds__(256, SHV_MRG_MINB) mrg_fill_vec_kernel(const _
     (void)warp;
     const uint64_t nthr = (uint64_t)gridDim.x * blockDim.x;
     for (uint64_t it = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; it < P.items; it += nthr) {
-        const uint64_t j = it / P.ns;
-        const uint64_t i = it - j * P.ns;
+        uint64_t i, j;
+        item_ij<SEG_FASTEST>(P, it, i, j);
         Gen s = item_state(P, i, j);
         const uint64_t c0 = j * P.seg_len;
         const uint64_t len = min(P.seg_len, P.n - c0);
@@ -191,8 +209,8 @@ __global__ void __launch_bounds__(256) mrg_fill_scalar_kernel(const __grid_const
     using T = OutT<KIND>;
     const uint64_t nthr = (uint64_t)gridDim.x * blockDim.x;
     for (uint64_t it = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; it < P.items; it += nthr) {
-        const uint64_t j = it / P.ns;
-        const uint64_t i = it - j * P.ns;
+        uint64_t i, j;
+        item_ij<false>(P, it, i, j);
         Gen s = item_state(P, i, j);
         const uint64_t c0 = j * P.seg_len;
         const uint64_t len = min(P.seg_len, P.n - c0);
@@ -211,8 +229,8 @@ __global__ void __launch_bounds__(256) mrg_mc_kernel(const __grid_constant__ Mrg
     const uint64_t nthr = (uint64_t)gridDim.x * blockDim.x;
     uint64_t total = 0;
     for (uint64_t it = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; it < P.items; it += nthr) {
-        const uint64_t j = it / P.ns;
-        const uint64_t i = it - j * P.ns;
+        uint64_t i, j;
+        item_ij<false>(P, it, i, j);
         Gen s = item_state(P, i, j);
         const uint64_t c0 = j * P.seg_len;
         const uint32_t len = (uint32_t)min(P.seg_len, P.n - c0);
@@ -241,7 +259,10 @@ template <int KIND>
 cudaError_t ensure_smem_attr()
 {
     static std::atomic<uint64_t> done{0};
-    return ensure_dyn_smem(mrg_fill_vec_kernel<KIND>, mrg_fill_smem(256, KIND), done);
+    cudaError_t e = ensure_dyn_smem(mrg_fill_vec_kernel<KIND, false>, mrg_fill_smem(256, KIND), done);
+    static std::atomic<uint64_t> done_sf{0};
+    if (e == cudaSuccess) e = ensure_dyn_smem(mrg_fill_vec_kernel<KIND, true>, mrg_fill_smem(256, KIND), done_sf);
+    return e;
 }
 
 template <int KIND>
@@ -249,7 +270,8 @@ cudaError_t launch_vec(const MrgLaunch& p, Grid g, cudaStream_t s)
 {
     const cudaError_t e = ensure_smem_attr<KIND>();
     if (e != cudaSuccess) return e;
-    mrg_fill_vec_kernel<KIND><<<g.blocks, g.threads, mrg_fill_smem((int)g.threads, KIND), s>>>(p);
+    if (p.seg_fastest) mrg_fill_vec_kernel<KIND, true><<<g.blocks, g.threads, mrg_fill_smem((int)g.threads, KIND), s>>>(p);
+    else mrg_fill_vec_kernel<KIND, false><<<g.blocks, g.threads, mrg_fill_smem((int)g.threads, KIND), s>>>(p);
     return cudaGetLastError();
 }
 
@@ -309,11 +331,11 @@ cudaError_t mrg_occupancy(int kernel, int kind, bool fast, int threads, int* out
                                 : kind == kF32 ? ensure_smem_attr<kF32>() : ensure_smem_attr<kF64>();
             if (e != cudaSuccess) return e;
         }
-        if (kind == kU32) return fast ? occ(mrg_fill_vec_kernel<kU32>, threads, sm, out)
+        if (kind == kU32) return fast ? occ(mrg_fill_vec_kernel<kU32, false>, threads, sm, out)
                                       : occ(mrg_fill_scalar_kernel<kU32>, threads, 0, out);
-        if (kind == kF32) return fast ? occ(mrg_fill_vec_kernel<kF32>, threads, sm, out)
+        if (kind == kF32) return fast ? occ(mrg_fill_vec_kernel<kF32, false>, threads, sm, out)
                                       : occ(mrg_fill_scalar_kernel<kF32>, threads, 0, out);
-        return fast ? occ(mrg_fill_vec_kernel<kF64>, threads, sm, out)
+        return fast ? occ(mrg_fill_vec_kernel<kF64, false>, threads, sm, out)
                     : occ(mrg_fill_scalar_kernel<kF64>, threads, 0, out);
     }
     case kKMrgMc:

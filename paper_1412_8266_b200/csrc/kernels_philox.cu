@@ -54,6 +54,52 @@ __global__ void __launch_bounds__(256) philox_fill_fast_kernel(const __grid_cons
     const uint64_t nw = (uint64_t)gridDim.x * (blockDim.x >> 5);
     uint64_t task = (uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     if (task >= P.items) return;
+    if (P.rpt > 1) {
+        // Short rows: a task is rpt whole rows (one run each). The counter
+        // block of a lane's chunk depends only on its column, so the round-1
+        // product M0*blk_lo is row-invariant; per row only the stream word's
+        // products (p1, and q through round 1's output) are recomputed.
+        const uint32_t mine = cpr > lane ? (uint32_t)((cpr - lane + 31) / 32) : 0u;
+        const uint64_t blk = P.o_blk + 2 * lane;
+        const bool nowrap = (uint32_t)blk <= 0xFFFFFFFFu - 64u * mine - 1u;
+        const uint64_t pa0 = (uint64_t)kPM0 * (uint32_t)blk;
+        for (; task < P.items; task += nw) {
+            const uint64_t i0 = task * P.rpt;
+            const uint64_t i1 = min(i0 + P.rpt, P.ns);
+            char* orow = reinterpret_cast<char*>(P.out) + ((i0 * cpr + lane) << 5);
+            for (uint64_t i = i0; i < i1; ++i, orow += cpr << 5) {
+                uint32_t k0, k1;
+                uint64_t g;
+                stream_key<KEYED>(P, i, k0, k1, g);
+                const uint64_t p1 = (uint64_t)kPM1 * (uint32_t)g;
+                char* o = orow;
+                if (nowrap) {
+                    const uint32_t c0r1 = (uint32_t)(p1 >> 32) ^ (uint32_t)(blk >> 32) ^ k0;
+                    const uint64_t q = (uint64_t)kPM0 * c0r1;
+                    uint64_t pa = pa0;
+                    for (uint32_t r = 0; r < mine; ++r) {
+                        const uint64_t pb = add64w(pa, kPM0);
+                        const W4 a = philox10_from_r2(pa, q, (uint32_t)p1, (uint32_t)(g >> 32), k0, k1);
+                        const W4 d = philox10_from_r2(pb, q, (uint32_t)p1, (uint32_t)(g >> 32), k0, k1);
+                        store_chunk<KIND>(o, a, d);
+                        pa = add64w(pa, 64ull * kPM0);
+                        o += 1024;
+                    }
+                } else {
+                    uint64_t b = blk;
+                    for (uint32_t r = 0; r < mine; ++r) {
+                        const uint64_t b1 = add64(b, 1u);
+                        const W4 a = philox_blk(b, g, k0, k1);
+                        const W4 d = philox_blk(b1, g, k0, k1);
+                        store_chunk<KIND>(o, a, d);
+                        b = add64(b, 64u);
+                        o += 1024;
+                    }
+                }
+            }
+        }
+        return;
+    }
     uint64_t i = task / tpr, kb = task - i * tpr;
     const uint64_t qs = nw / tpr, rs = nw - qs * tpr;
     for (; task < P.items; task += nw) {

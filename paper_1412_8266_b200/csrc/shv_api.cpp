@@ -270,25 +270,25 @@ uint64_t resident_threads(const Handle& h, int kernel, int kind, bool fast)
 }
 
 // Split rows of `len` units into nseg segments of seg_len units (multiple of
-// `align`), aiming at `waves` x resident threads work items.
+// `align`, at least min_len unless the row is shorter), aiming at `waves` x
+// resident threads work items; nseg < 2^kSegBits.
 void split(const Handle& h, uint64_t ns, uint64_t len, uint64_t align, uint64_t waves,
-           uint64_t resident, uint64_t cap, uint64_t* seg_len, uint32_t* nseg)
+           uint64_t resident, uint64_t cap, uint64_t* seg_len, uint32_t* nseg, uint64_t min_len = 256)
 {
     uint64_t L;
     if (h.seg) {
         L = h.seg;
     } else {
         const uint64_t target = waves * resident;
-        uint64_t S = (target + ns - 1) / ns;
-        if (S < 1) S = 1;
-        if (S > (uint64_t)kMaxSeg) S = kMaxSeg;
+        const uint64_t S = (target + ns - 1) / ns;
         L = (len + S - 1) / S;
+        if (L < min_len) L = min_len;
     }
     L = (L + align - 1) / align * align;
     if (L > cap) L = cap / align * align;
     if (L == 0) L = align;
     uint64_t S = (len + L - 1) / L;
-    while (S > (uint64_t)kMaxSeg) {  // user segment too short: grow it
+    while (S >= (1ull << kSegBits)) {  // user segment too short for 2^32 segments: grow it
         L *= 2;
         S = (len + L - 1) / L;
     }
@@ -329,19 +329,24 @@ shv_status check_advance(const Handle& h, u128 draws)
     return SHV_OK;
 }
 
-void fill_mrg_segments(const Handle& h, uint64_t units_per_seg, uint64_t draws_per_unit,
-                       uint32_t nseg, MatPair* seg)
+// Segment jumps of a MRG launch: seg0 = A^o, segpow[b] = (A^(L*dpu))^(2^b)
+// for the bits b that segment indices < nseg use.
+void fill_mrg_segments(const Handle& h, uint64_t units_per_seg, uint64_t draws_per_unit, uint32_t nseg,
+                       MrgLaunch* P)
 {
-    seg[0] = pair_pow(h.offset, 0);
-    const MatPair step = pair_pow((u128)units_per_seg * draws_per_unit, 0);
-    for (uint32_t j = 1; j < nseg; ++j) seg[j] = pair_mul(step, seg[j - 1]);
+    P->seg0 = pair_pow(h.offset, 0);
+    P->segpow[0] = pair_pow((u128)units_per_seg * draws_per_unit, 0);
+    for (int b = 1; b < kSegBits && ((uint64_t)nseg - 1) >> b; ++b)
+        P->segpow[b] = pair_mul(P->segpow[b - 1], P->segpow[b - 1]);
 }
 
 // Warp tasks of the counter-based fast fills: (row, 32*R chunks of 32 B). R
 // starts at ceil(chunks_per_row / 32) <= 16 and halves until there are >= 4
 // tasks per resident warp (load balance); a launch-config segment overrides it.
+// Rows of at most 16 runs per lane are grouped: *rpt_out whole rows per task,
+// about 16 runs per lane, still >= 4 tasks per resident warp.
 void counter_tasks(const Handle& h, uint64_t ns, uint64_t cpr, uint64_t resident, uint32_t* R_out,
-                   uint64_t* tasks_out)
+                   uint64_t* tasks_out, uint32_t* rpt_out = nullptr)
 {
     const uint64_t rwarps = resident / 32;
     uint64_t R = (cpr + 31) / 32;
@@ -351,6 +356,15 @@ void counter_tasks(const Handle& h, uint64_t ns, uint64_t cpr, uint64_t resident
     while (!h.seg && R > 1 && tasks(R) < 4 * rwarps) R /= 2;
     *R_out = (uint32_t)R;
     *tasks_out = tasks(R);
+    if (!rpt_out) return;
+    *rpt_out = 1;
+    if (h.seg || 32 * R < cpr) return;  // rows span several tasks
+    uint64_t rpt = 16 / R;
+    while (rpt > 1 && (ns + rpt - 1) / rpt < 4 * rwarps) rpt /= 2;
+    if (rpt > 1) {
+        *rpt_out = (uint32_t)rpt;
+        *tasks_out = (ns + rpt - 1) / rpt;
+    }
 }
 
 // ---------------------------------------------------------------- Leap Frog (R17)
@@ -423,7 +437,7 @@ std::unique_ptr<LeapLaunch> leap_launch(const Handle& h, uint64_t s0, uint64_t n
         charpoly(P->B.b, 1, P->cp2);
         P->start = pair_pow(1 + (u128)h.players * h.offset, 0);
         P->segpow[0] = pair_pow((u128)h.players * P->seg_draws, 0);
-        for (int b = 1; b < kLeapSegBits && (nseg - 1) >> b; ++b) P->segpow[b] = pair_mul(P->segpow[b - 1], P->segpow[b - 1]);
+        for (int b = 1; b < kSegBits && (nseg - 1) >> b; ++b) P->segpow[b] = pair_mul(P->segpow[b - 1], P->segpow[b - 1]);
     }
     return P;
 }
@@ -534,13 +548,15 @@ shv_status generate(shv_streams hid, T* out, uint64_t n, void* stream, int kind,
                   &P->seg_len, &P->nseg);
             if (vec && P->seg_len % 8) vec = false;
             P->items = ns * P->nseg;
-            fill_mrg_segments(h, P->seg_len, 1, P->nseg, P->seg);
+            P->seg_fastest = row_bytes > (512u << 10);
+            fill_mrg_segments(h, P->seg_len, 1, P->nseg, P.get());
             Grid g{blocks_for(h, kKMrgFill, kind, vec, P->items), h.tpb};
             err = launch_mrg_fill(*P, kind, vec, g, s);
         } else {
             const uint64_t E = kind == kF64 ? 4 : 8;
             const bool fast = aligned32 && (n % E == 0) && ((uint32_t)h.offset & 3) == 0;
             PhiloxLaunch P{};
+            P.rpt = 1;
             P.keyed = h.spacing == SHV_SPACING_KEYED;
             P.k0 = h.seed[0];
             P.k1 = P.keyed ? h.seed[0] : h.seed[1];
@@ -553,7 +569,7 @@ shv_status generate(shv_streams hid, T* out, uint64_t n, void* stream, int kind,
             Grid g{};
             if (fast) {
                 const int kid = P.keyed ? kKPhiloxFillKeyed : kKPhiloxFill;
-                counter_tasks(h, ns, n / E, resident_threads(h, kid, kind, true), &P.nseg, &P.items);
+                counter_tasks(h, ns, n / E, resident_threads(h, kid, kind, true), &P.nseg, &P.items, &P.rpt);
                 g = Grid{blocks_for(h, kid, kind, true, P.items * 32), h.tpb};
             } else {
                 P.items = (ns * n + 7) / 8;
@@ -1002,7 +1018,7 @@ shv_status shv_mc_pi_ex(shv_streams hid, uint64_t samples, uint64_t* d_hits, uin
         P->counts = (unsigned long long*)d_counts;
         split(h, h.n, samples, 2, 32, resident_threads(h, kKMrgMc, 0, true), cap, &P->seg_len, &P->nseg);
         P->items = h.n * P->nseg;
-        fill_mrg_segments(h, P->seg_len, 2, P->nseg, P->seg);
+        fill_mrg_segments(h, P->seg_len, 2, P->nseg, P.get());
         Grid g{blocks_for(h, kKMrgMc, 0, true, P->items), h.tpb};
         err = launch_mrg_mc(*P, g, s);
     } else {

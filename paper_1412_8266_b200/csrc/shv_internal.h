@@ -7,10 +7,11 @@
 
 namespace shv {
 
-// Most segments one launch splits a stream into (intra-stream Sequence
-// Splitting, P L109-112 [§2.3]); each needs its own jump matrix in the
-// kernel parameter block (72 B each).
-constexpr int kMaxSeg = 64;
+// Intra-stream Sequence Splitting (P L109-112 [§2.3]): a launch splits each
+// row into up to 2^kSegBits segments; segment j starts j segment lengths
+// later, reached through per-bit jump tables in the kernel parameter block
+// (72 B per entry).
+constexpr int kSegBits = 32;
 
 // Output kinds.
 enum Kind : int { kU32 = 0, kF32 = 1, kF64 = 2 };
@@ -23,8 +24,8 @@ struct MatPair {
 
 // MRG32k3a bulk fill / Monte Carlo launch. Work item it in [0, items):
 // segment j = it / ns, stream i = it % ns (streams fastest so a warp shares
-// one segment matrix). Segment j covers values [j*seg_len, min(n,(j+1)*seg_len))
-// of the row and starts from seg[j] * state_i.
+// one segment matrix), or i = it / nseg, j = it % nseg with seg_fastest. Segment j covers values [j*seg_len, min(n,(j+1)*seg_len))
+// of the row and starts from (prod over set bits b of j of segpow[b]) * seg0 * state_i.
 struct MrgLaunch {
     const uint32_t* state;   // SoA: word k of stream s at state[k*stride + s]
     uint64_t stride;         // handle n_streams
@@ -37,7 +38,9 @@ struct MrgLaunch {
     unsigned long long* hits;    // MC only
     unsigned long long* counts;  // MC only, optional (indexed by launch stream)
     uint32_t nseg;
-    MatPair seg[kMaxSeg];
+    uint32_t seg_fastest;    // 1: work item it -> (i = it / nseg, j = it % nseg)
+    MatPair seg0;                 // A^o (o = handle offset)
+    MatPair segpow[kSegBits];     // (A^(seg_len * draws per unit))^(2^b)
 };
 
 // Philox4x32-10 bulk fill / Monte Carlo launch. Draw d of handle stream i
@@ -54,8 +57,9 @@ struct PhiloxLaunch {
     void* out;
     uint64_t n;              // fill: values per row; MC: samples per stream
     uint64_t seg_len;        // MC: samples per work item
-    uint64_t items;          // fill: chunks; MC: ns * nseg
-    uint32_t nseg;
+    uint64_t items;          // fill: warp tasks; MC: ns * nseg
+    uint32_t nseg;           // fill fast path: chunks per lane per row (R); MC: segments
+    uint32_t rpt;            // fill fast path: whole rows per warp task (>= 1)
     unsigned long long* hits;
     unsigned long long* counts;
     uint32_t keyed;          // 1: key = (g0 + i, k1), ctr[2..3] = 0 (SHV_SPACING_KEYED)
@@ -103,7 +107,6 @@ struct TinyMtLaunch {
 // [j*seg_len, min(n, (j+1)*seg_len)) of the row, i.e. player draws from
 // o + j*seg_len*dpv (dpv = draws per value, 2 for counter-based f64 and MC).
 enum LeapGen : int { kLeapMrg = 0, kLeapPhilox = 1, kLeapThreefry = 2 };
-constexpr int kLeapSegBits = 32;
 struct LeapLaunch {
     uint64_t players;            // K
     uint64_t first;              // player id of launch row 0
@@ -124,7 +127,7 @@ struct LeapLaunch {
     uint32_t cp1[3], cp2[3];     // u_{t+3} = cp[2] u_{t+2} + cp[1] u_{t+1} + cp[0] u_t (mod m1 / m2)
     MatPair B;                   // A^K
     MatPair start;               // A^(1 + K*o)
-    MatPair segpow[kLeapSegBits];  // (A^(K*seg_draws))^(2^b)
+    MatPair segpow[kSegBits];  // (A^(K*seg_draws))^(2^b)
 };
 
 struct Grid {

@@ -193,6 +193,26 @@ def test_philox_keyed_mode(shv, orc, kind):
         f.close()
 
 
+@pytest.mark.parametrize("sp,seed", [(W.SPACING_STREAM, [12345, 9]), (W.SPACING_KEYED, [0xABCD])])
+@pytest.mark.parametrize("kind,n", [("u32", 256), ("f32", 136), ("f64", 128), ("u32", 1024)])
+def test_philox_short_rows_grouped_tasks(shv, orc, sp, seed, kind, n):
+    """Many short rows (2^18 x <= 1 KB): the fast fill groups whole rows per
+    warp task (PhiloxLaunch.rpt > 1); sampled rows and the jump-offset path."""
+    ns = 1 << 18
+    f = Fam(shv, W.PHILOX4X32_10, seed, ns, sp)
+    rows = W.sample_streams(ns, 256, seed=11)
+    try:
+        for pre in (0, 4, 2):  # offset lane 0 (fast path), then lane 2 (generic path)
+            if pre:
+                shv.shv_jump(f.h, shv.SHV_JUMP_DRAWS, pre)
+                f.offset += pre
+            before = f.offset
+            got = f.gen_(n, kind)
+            same(got[rows], f.ref(orc, n, kind, offset=before, streams=rows))
+    finally:
+        f.close()
+
+
 @pytest.mark.parametrize("gen,sp", [(W.MRG32K3A, 1), (W.PHILOX4X32_10, 0), (W.THREEFRY4X64_20, 0)])
 def test_generate_twice_equals_generate_2n(shv, gen, sp):
     a = Fam(shv, gen, [99], 1000, sp)
