@@ -242,3 +242,36 @@ def mc_count(gen, seed, n_streams, samples, *, first=0, spacing=SPACING_STREAM, 
     if tot == (1 << 64) - 1:
         raise ValueError("oracle rejected the arguments")
     return int(tot), counts
+
+
+def verify_disjoint(rows):
+    """Disjointness audit by definition (S L407-415 verify_disjoint; S L425):
+    ``rows`` = one array of u32 draws per PE, in PE order. Every window of 4
+    consecutive draws is recorded with its (pe, pos); a collision is a window
+    held by two different PEs. Returns {"disjoint", "windows"} and, if not
+    disjoint, the lexicographically smallest (pe_a, pos_a, pe_b, pos_b) with
+    pe_a < pe_b over all colliding pairs. Plain dict of windows; no hashing
+    shortcut, no sorting."""
+    seen = {}
+    windows = 0
+    for pe, r in enumerate(rows):
+        r = [int(x) for x in r]
+        for pos in range(len(r) - 3):
+            seen.setdefault(tuple(r[pos:pos + 4]), []).append((pe, pos))
+            windows += 1
+    best = None
+    for occ in seen.values():
+        if len(occ) < 2:
+            continue
+        for x in range(len(occ)):
+            for y in range(x + 1, len(occ)):
+                (pa, qa), (pb, qb) = occ[x], occ[y]
+                if pa == pb:
+                    continue
+                cand = (pa, qa, pb, qb) if pa < pb else (pb, qb, pa, qa)
+                if best is None or cand < best:
+                    best = cand
+    out = {"disjoint": best is None, "windows": windows}
+    if best is not None:
+        out.update(pe_a=best[0], pos_a=best[1], pe_b=best[2], pos_b=best[3])
+    return out

@@ -526,3 +526,47 @@ def test_leapfrog_rejects_bad_plans(orc):
                      players=2)
     with pytest.raises(ValueError):  # Philox base stream exhausted (2^66 draws)
         orc.generate(W.PHILOX4X32_10, [1], 1, 4, spacing=L, players=1 << 40, offset=1 << 26)
+
+
+# --------------------------------------------------------------------------- verify_disjoint (NEXT-4)
+# S L407-415: windows of 4 consecutive draws; a collision is a window shared by
+# two different PEs; the constructed overlapping plan collides at position 0.
+
+def _brute_first_collision(rows):
+    best = None
+    for a in range(len(rows)):
+        for b in range(a + 1, len(rows)):
+            for i in range(len(rows[a]) - 3):
+                for j in range(len(rows[b]) - 3):
+                    if all(int(rows[a][i + k]) == int(rows[b][j + k]) for k in range(4)):
+                        cand = (a, i, b, j)
+                        best = cand if best is None or cand < best else best
+    return best
+
+
+def test_verify_disjoint_matches_brute_force(orc):
+    rng = np.random.default_rng(5)
+    for trial in range(40):
+        rows = [rng.integers(0, 3, size=int(rng.integers(4, 14))).astype(np.uint32) for _ in range(4)]
+        got = orc.verify_disjoint(rows)
+        want = _brute_first_collision(rows)
+        assert got["disjoint"] == (want is None), trial
+        if want is not None:
+            assert (got["pe_a"], got["pos_a"], got["pe_b"], got["pos_b"]) == want, trial
+        assert got["windows"] == sum(len(r) - 3 for r in rows)
+
+
+def test_verify_disjoint_spec_examples(orc):
+    # deliberately overlapping plan: Philox streams [0,4) and [2,6) (S L414)
+    a = orc.generate(W.PHILOX4X32_10, [7], 4, 200)
+    b = orc.generate(W.PHILOX4X32_10, [7], 4, 200, first=2)
+    r = orc.verify_disjoint(list(a) + list(b))
+    assert not r["disjoint"] and (r["pe_a"], r["pos_a"], r["pe_b"], r["pos_b"]) == (2, 0, 4, 0)
+    # shifted overlap: stream 1 at offset 17 is also in the plan
+    c = orc.generate(W.PHILOX4X32_10, [7], 1, 100, first=1, offset=17)
+    r = orc.verify_disjoint(list(a) + list(c))
+    assert (r["pe_a"], r["pos_a"], r["pe_b"], r["pos_b"]) == (1, 17, 4, 0)
+    # MRG32k3a Sequence Splitting, 8 PEs, horizon 10^5 (S L412); LeapFrog{2}, 10^4 (S L415)
+    assert orc.verify_disjoint(list(orc.generate(W.MRG32K3A, [12345], 8, 100000)))["disjoint"]
+    lf = orc.generate(W.MRG32K3A, [12345], 2, 10000, spacing=W.SPACING_LEAPFROG, players=2)
+    assert orc.verify_disjoint(list(lf))["disjoint"]
