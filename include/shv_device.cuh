@@ -212,6 +212,117 @@ __device__ __forceinline__ uint32_t mrg_next(MrgD& s)
     return mrg_combine(p1, p2);
 }
 
+// FP64 constants of the floor reductions. The kernels pass a copy read from
+// their launch parameters, so ptxas keeps them in registers instead of
+// re-materialising the non-immediate doubles inside the loop (8-14 extra
+// issue slots per 8 numbers); the device API uses mrg_fpk() (immediates).
+struct MrgFpK {
+    double magic;   // 1.5 * 2^52: ulp 1 on [2^52, 2^53)
+    double inv1;    // RN(1/m1) = 1/m1 + delta1, 0 < delta1 < 0.34 ulp
+    double inv2;    // RU(1/m2) = 1/m2 + delta2, 0 < delta2 < 0.54 ulp
+    double m1, m2;
+    double a23n_m2; // a23n * m2 = 5886603609186927, exact
+};
+__host__ __device__ __forceinline__ constexpr MrgFpK mrg_fpk()
+{
+    return MrgFpK{6755399441055744.0, 1.0 / (double)kM1, 0x1.000059451f212p-32,
+                  (double)kM1, (double)kM2, (double)kA23n * (double)kM2};
+}
+
+// Component 2 on the FP64 pipe with a floor reduction, no decode. For a
+// canonical state (y < m2) the positive form p = a21*y2 + a23n*(m2 - y0) lies
+// in [0, 2^52.86), exact in binary64 (t = fma(-a23n, y0, a23n*m2) and
+// p = fma(a21, y2, t) are exact integers). With inv2 = RU(1/m2) =
+// 1/m2 + delta, 0 < delta < 0.54 ulp, p*delta*m2 < 0.97 for every such p, so
+// floor(p*inv2) = floor(p/m2) exactly; fma.rm(p, inv2, 1.5*2^52) returns
+// 1.5*2^52 + floor(p/m2) (ulp 1 there). r = p - k*m2 is then the canonical
+// residue in [0, m2): it is both the next state word (canonical again, so the
+// bound holds at every step) and, as the low word of r + 1.5*2^52, the
+// component's output, with no sign fix-up. 6 FP64 operations, 0 integer.
+__device__ __forceinline__ uint32_t mrg_c2_floor(double y0, double y2, double& r_out, const MrgFpK& K)
+{
+    const double t = __fma_rn(-(double)kA23n, y0, K.a23n_m2);  // a23n*(m2 - y0)
+    const double p = __fma_rn((double)kA21, y2, t);
+    const double k = __dadd_rn(__fma_rd(p, K.inv2, K.magic), -K.magic);
+    const double r = __fma_rn(-k, K.m2, p);
+    r_out = r;
+    return (uint32_t)__double2loint(__dadd_rn(r, K.magic));
+}
+
+// Component 1 on the FP64 pipe with a floor reduction. The signed form
+// p = a12*x1 - a13n*x0 satisfies |p| < 2^52.42 for states in [0, m1]. With
+// kInv = RN(1/m1) = 1/m1 + delta, 0 < delta < 0.34 ulp, |p|*delta*m1 < 0.45,
+// so floor(p*kInv) = floor(p/m1) except when p = k*m1 exactly with p < 0,
+// where it is k - 1 and r = m1 (= 0 mod m1). r is therefore in [0, m1], a
+// valid state word, and the output r (low word of r + 1.5*2^52) equals p1 or,
+// only when p1 = 0, m1 — which mrg_combine maps to the same z (p1 - p2 + m1 if
+// p1 <= p2 gives m1 - p2 for p1 = 0; m1 - p2 > 0 for p1 = m1). 6 FP64 ops.
+__device__ __forceinline__ uint32_t mrg_c1_floor(double x0, double x1, double& r_out, const MrgFpK& K)
+{
+    const double t = __dmul_rn((double)kA13n, x0);
+    const double p = __fma_rn((double)kA12, x1, -t);
+    const double k = __dadd_rn(__fma_rd(p, K.inv1, K.magic), -K.magic);
+    const double r = __fma_rn(-k, K.m1, p);
+    r_out = r;
+    return (uint32_t)__double2loint(__dadd_rn(r, K.magic));
+}
+
+// Both components on the FP64 pipe with floor reductions: 12 FP64 ops and the
+// 3-instruction combine per number (no decode fix-ups).
+struct MrgFF {
+    double x0, x1, x2;
+    double y0, y1, y2;
+};
+
+__device__ __forceinline__ MrgFF to_mrg_ff(const Mrg& s)
+{
+    return MrgFF{__uint2double_rn(s.x0), __uint2double_rn(s.x1), __uint2double_rn(s.x2),
+                 __uint2double_rn(s.y0), __uint2double_rn(s.y1), __uint2double_rn(s.y2)};
+}
+
+__device__ __forceinline__ uint32_t mrg_next(MrgFF& s, const MrgFpK& K = mrg_fpk())
+{
+    double r1, r2;
+    const uint32_t p1 = mrg_c1_floor(s.x0, s.x1, r1, K);
+    s.x0 = s.x1;
+    s.x1 = s.x2;
+    s.x2 = r1;
+    const uint32_t p2 = mrg_c2_floor(s.y0, s.y2, r2, K);
+    s.y0 = s.y1;
+    s.y1 = s.y2;
+    s.y2 = r2;
+    return mrg_combine(p1, p2);
+}
+
+// The product's MRG32k3a step: component 1 in integer arithmetic (FMA-heavy
+// + ALU: 3 IMAD.WIDE, 3 ALU), component 2 on the FP64 pipe (6 ops), combine on
+// the ALU (3) — 15 issue slots per number with the three pipes each ~12
+// cycles per warp, instead of 23.5 slots and 24 FP64 cycles for both
+// components on the FP64 pipe.
+struct MrgIF {
+    uint32_t x0, x1, x2;
+    double y0, y1, y2;
+};
+
+__device__ __forceinline__ MrgIF to_mrg_if(const Mrg& s)
+{
+    return MrgIF{s.x0, s.x1, s.x2, __uint2double_rn(s.y0), __uint2double_rn(s.y1), __uint2double_rn(s.y2)};
+}
+
+__device__ __forceinline__ uint32_t mrg_next(MrgIF& s, const MrgFpK& K = mrg_fpk())
+{
+    const uint32_t p1 = mrg_c1(s.x0, s.x1);
+    s.x0 = s.x1;
+    s.x1 = s.x2;
+    s.x2 = p1;
+    double r;
+    const uint32_t p2 = mrg_c2_floor(s.y0, s.y2, r, K);
+    s.y0 = s.y1;
+    s.y1 = s.y2;
+    s.y2 = r;
+    return mrg_combine(p1, p2);
+}
+
 // ------------------------------------------------------------------ Philox4x32-10
 
 struct W4 {

@@ -37,14 +37,15 @@ public:
         const uint64_t n = v.n_streams;
         dev::Mrg m{st[i], st[n + i], st[2 * n + i], st[3 * n + i], st[4 * n + i], st[5 * n + i]};
         dev::apply(v.jump, v.jump + 9, m);
-        s_ = dev::to_fp64(m);
+        s_ = dev::to_mrg_ff(m);
     }
-    __device__ uint32_t next_u32() { return dev::mrg_next(s_); }  // z in [1, m1]
+    // z in [1, m1]; the library fills' step (both components on the FP64 pipe, floor reductions)
+    __device__ uint32_t next_u32() { return dev::mrg_next(s_); }
     __device__ float next_f32() { return dev::to_f32(next_u32()); }
     __device__ double next_f64() { return dev::mrg_f64(next_u32()); }
 
 private:
-    dev::MrgD s_;
+    dev::MrgFF s_;
 };
 
 template <>

@@ -3,8 +3,11 @@
 // fused Monte Carlo pi kernel. Common pieces: kernels_common.cuh.
 //
 // Compile-time variants (the kernel lab, tools/lab/, builds each):
-//   SHV_MRG_STEP  0 = all-integer step, 2 = both components on the FP64 pipe
-//                 (default; fastest measured; other forms live in tools/lab/)
+//   SHV_MRG_STEP  0 = all-integer step, 2 = both components on the FP64 pipe,
+//                 3 = component 1 integer, component 2 FP64 with the floor
+//                 reduction (MrgIF in shv_device.cuh), 4 = both components on
+//                 the FP64 pipe with floor reductions (MrgFF; default, fastest
+//                 measured: tools/lab/step2_lab.cu), 9 = lab null generator
 //   SHV_MRG_STAGE 0 = each lane stores its own row directly (32-byte vector
 //                 stores); 2 = lanes stage 256 B in shared memory and the warp
 //                 writes 256-byte runs; 1 (default) = stage the 8-byte (f64)
@@ -15,7 +18,7 @@
 #include "kernels_common.cuh"
 
 #ifndef SHV_MRG_STEP
-#define SHV_MRG_STEP 2
+#define SHV_MRG_STEP 4
 #endif
 #ifndef SHV_MRG_STAGE
 #define SHV_MRG_STAGE 1
@@ -33,11 +36,33 @@ __device__ MatPair g_jump_tab[3][64];
 
 namespace {
 
-#if SHV_MRG_STEP == 2
+__device__ __forceinline__ MrgFpK load_fpk(const MrgLaunch& P)
+{
+    return MrgFpK{P.fpk[0], P.fpk[1], P.fpk[2], P.fpk[3], P.fpk[4], P.fpk[5]};
+}
+
+#if SHV_MRG_STEP == 9
+// Lab only: a trivial "generator" (one IADD per value) that keeps the fill
+// kernels' work split and stores, to measure the store path's ceiling.
+struct MrgNull {
+    uint32_t x;
+};
+using Gen = MrgNull;
+__device__ __forceinline__ Gen make_gen(const Mrg& s) { return MrgNull{s.x0 ^ s.y2}; }
+__device__ __forceinline__ uint32_t mrg_next(MrgNull& s, const MrgFpK&) { return s.x++; }
+#elif SHV_MRG_STEP == 4
+using Gen = MrgFF;
+__device__ __forceinline__ Gen make_gen(const Mrg& s) { return to_mrg_ff(s); }
+#elif SHV_MRG_STEP == 3
+using Gen = MrgIF;
+__device__ __forceinline__ Gen make_gen(const Mrg& s) { return to_mrg_if(s); }
+#elif SHV_MRG_STEP == 2
 using Gen = MrgD;
+__device__ __forceinline__ uint32_t mrg_next(MrgD& s, const MrgFpK&) { return mrg_next(s); }
 __device__ __forceinline__ Gen make_gen(const Mrg& s) { return to_fp64(s); }
 #else
 using Gen = Mrg;
+__device__ __forceinline__ uint32_t mrg_next(Mrg& s, const MrgFpK&) { return mrg_next(s); }
 __device__ __forceinline__ Gen make_gen(const Mrg& s) { return s; }
 #endif
 
@@ -81,11 +106,11 @@ __device__ __forceinline__ Gen item_state(const MrgLaunch& P, uint64_t i, uint64
 
 // 8 values -> staging pieces (u32/f32: 2 pieces; f64: 4 pieces).
 template <int KIND>
-__device__ __forceinline__ void stage8(uint4* wb, unsigned lane, unsigned q0, Gen& s)
+__device__ __forceinline__ void stage8(uint4* wb, unsigned lane, unsigned q0, Gen& s, const MrgFpK& K)
 {
     uint32_t v[8];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) v[u] = mrg_next(s);
+    for (int u = 0; u < 8; ++u) v[u] = mrg_next(s, K);
     if (KIND == kF64) {
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
@@ -141,6 +166,7 @@ template <int KIND, bool SEG_FASTEST>
 __global__ void __launch_bounds__(256, SHV_MRG_MINB) mrg_fill_vec_kernel(const __grid_constant__ MrgLaunch P)
 {
     using T = OutT<KIND>;
+    const MrgFpK K = load_fpk(P);
     const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     if constexpr (mrg_staged<KIND>()) {
     extern __shared__ uint4 smem[];
@@ -166,9 +192,9 @@ __global__ void __launch_bounds__(256, SHV_MRG_MINB) mrg_fill_vec_kernel(const _
             const uint32_t cnt = len > r ? min(G, len - r) : 0u;
             if (cnt == G) {
 #pragma unroll
-                for (unsigned g = 0; g < G / 8; ++g) stage8<KIND>(wb, lane, g * (KIND == kF64 ? 4 : 2), s);
+                for (unsigned g = 0; g < G / 8; ++g) stage8<KIND>(wb, lane, g * (KIND == kF64 ? 4 : 2), s, K);
             } else {
-                for (unsigned g = 0; g < cnt / 8; ++g) stage8<KIND>(wb, lane, g * (KIND == kF64 ? 4 : 2), s);
+                for (unsigned g = 0; g < cnt / 8; ++g) stage8<KIND>(wb, lane, g * (KIND == kF64 ? 4 : 2), s, K);
             }
             write_round<T>(wb, lane, r, cnt, row);
         }
@@ -187,7 +213,7 @@ __global__ void __launch_bounds__(256, SHV_MRG_MINB) mrg_fill_vec_kernel(const _
         for (uint64_t t = 0; t < len; t += 8) {
             uint32_t v[8];
 #pragma unroll
-            for (int u = 0; u < 8; ++u) v[u] = mrg_next(s);
+            for (int u = 0; u < 8; ++u) v[u] = mrg_next(s, K);
             if (KIND == kU32) {
                 st_v8(o + t, v[0], v[1], v[2], v[3], v[4], v[5], v[6], v[7]);
             } else if (KIND == kF32) {
@@ -202,11 +228,93 @@ __global__ void __launch_bounds__(256, SHV_MRG_MINB) mrg_fill_vec_kernel(const _
     }
 }
 
+// MRG32k3a fill, TMA store path. A warp owns a tile of 32
+// consecutive rows (streams 32g..32g+31 of the launch) x one segment; lane l
+// generates row 32g+l. Each round the lanes write 128 B of their rows into the
+// warp's 4-KB shared-memory box (128-B swizzle: 16-byte chunk q of row l sits
+// at chunk q ^ (l & 7), so the eight lanes of a quarter-warp hit distinct
+// banks), and one lane hands the 32 x 128-B box to the TMA engine
+// (cp.async.bulk.tensor.2d shared -> global). The SM's load/store unit never
+// sees the scattered 32-byte row pieces that cap per-lane STG.256 stores at
+// ~4.5 TB/s (tools/lab, null generator); boxes that run past the row end or
+// past the launch's last row are clipped by the tensor map bounds.
+template <int KIND, bool SEG_FASTEST>
+__global__ void __launch_bounds__(256, SHV_MRG_MINB)
+    mrg_fill_tma_kernel(const __grid_constant__ MrgLaunch P, const __grid_constant__ CUtensorMap tmap)
+{
+    using T = OutT<KIND>;
+    constexpr uint32_t W = 128 / sizeof(T);  // values per row per box
+    extern __shared__ uint8_t tma_smem[];
+    const MrgFpK K = load_fpk(P);
+    const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    // 1024-byte aligned boxes (128-B swizzle); the launch adds 1 KB of slack
+    const uint32_t base = ((uint32_t)__cvta_generic_to_shared(tma_smem) + 1023u) & ~1023u;
+    const uint32_t box = base + warp * 4096u;
+    const uint32_t rowsw = box + lane * 128u + ((lane & 7u) << 4);  // ^ (q << 4) = chunk q
+    const uint64_t G = (P.ns + 31) / 32, ntiles = G * P.nseg;
+    const uint64_t wstride = (uint64_t)gridDim.x * (blockDim.x >> 5);
+    for (uint64_t t = (uint64_t)blockIdx.x * (blockDim.x >> 5) + warp; t < ntiles; t += wstride) {
+        uint64_t g, j;
+        if (SEG_FASTEST) {
+            g = t / P.nseg;
+            j = t - g * P.nseg;
+        } else {
+            j = t / G;
+            g = t - j * G;
+        }
+        const uint64_t i = 32 * g + lane;
+        // rows past the launch's last stream compute a clipped, discarded row
+        Gen s = item_state(P, i < P.ns ? i : P.ns - 1, j);
+        const uint64_t c0 = j * P.seg_len;
+        const uint32_t len = (uint32_t)min(P.seg_len, P.n - c0);  // warp-uniform
+        for (uint32_t r = 0; r < len; r += W) {
+#pragma unroll
+            for (unsigned q8 = 0; q8 < W / 8; ++q8) {
+                uint32_t v[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) v[u] = mrg_next(s, K);
+                if (q8 == 0) {  // the previous box must have left shared memory
+                    if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+                    __syncwarp();
+                }
+                if (KIND == kF64) {
+#pragma unroll
+                    for (unsigned k = 0; k < 4; ++k) {
+                        const double a = mrg_f64(v[2 * k]), b = mrg_f64(v[2 * k + 1]);
+                        asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(rowsw ^ ((4 * q8 + k) << 4)),
+                                     "r"(__double2loint(a)), "r"(__double2hiint(a)), "r"(__double2loint(b)),
+                                     "r"(__double2hiint(b))
+                                     : "memory");
+                    }
+                } else {
+                    const uint4 a = pack4<KIND>(v[0], v[1], v[2], v[3]), b = pack4<KIND>(v[4], v[5], v[6], v[7]);
+                    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(rowsw ^ ((2 * q8) << 4)), "r"(a.x),
+                                 "r"(a.y), "r"(a.z), "r"(a.w)
+                                 : "memory");
+                    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(rowsw ^ ((2 * q8 + 1) << 4)),
+                                 "r"(b.x), "r"(b.y), "r"(b.z), "r"(b.w)
+                                 : "memory");
+                }
+            }
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // st.shared -> async proxy
+            __syncwarp();
+            if (lane == 0) {
+                asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(&tmap),
+                             "r"(box), "r"((int)(c0 + r)), "r"((int)(32 * g))
+                             : "memory");
+                asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            }
+        }
+    }
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
 // MRG32k3a fill, scalar path (any row length / element-aligned pointer).
 template <int KIND>
 __global__ void __launch_bounds__(256) mrg_fill_scalar_kernel(const __grid_constant__ MrgLaunch P)
 {
     using T = OutT<KIND>;
+    const MrgFpK K = load_fpk(P);
     const uint64_t nthr = (uint64_t)gridDim.x * blockDim.x;
     for (uint64_t it = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; it < P.items; it += nthr) {
         uint64_t i, j;
@@ -216,7 +324,7 @@ __global__ void __launch_bounds__(256) mrg_fill_scalar_kernel(const __grid_const
         const uint64_t len = min(P.seg_len, P.n - c0);
         T* o = reinterpret_cast<T*>(P.out) + i * P.n + c0;
         for (uint64_t t = 0; t < len; ++t) {
-            const uint32_t z = mrg_next(s);
+            const uint32_t z = mrg_next(s, K);
             if (KIND == kU32) o[t] = (T)z;
             else if (KIND == kF32) o[t] = (T)to_f32(z);
             else o[t] = (T)mrg_f64(z);
@@ -226,6 +334,7 @@ __global__ void __launch_bounds__(256) mrg_fill_scalar_kernel(const __grid_const
 
 __global__ void __launch_bounds__(256) mrg_mc_kernel(const __grid_constant__ MrgLaunch P)
 {
+    const MrgFpK K = load_fpk(P);
     const uint64_t nthr = (uint64_t)gridDim.x * blockDim.x;
     uint64_t total = 0;
     for (uint64_t it = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; it < P.items; it += nthr) {
@@ -239,14 +348,14 @@ __global__ void __launch_bounds__(256) mrg_mc_kernel(const __grid_constant__ Mrg
         for (; k + 12 <= len; k += 12) {
 #pragma unroll
             for (int u = 0; u < 12; ++u) {
-                const uint32_t w0 = mrg_next(s);
-                const uint32_t w1 = mrg_next(s);
+                const uint32_t w0 = mrg_next(s, K);
+                const uint32_t w1 = mrg_next(s, K);
                 h += hit(w0, w1);
             }
         }
         for (; k < len; ++k) {
-            const uint32_t w0 = mrg_next(s);
-            const uint32_t w1 = mrg_next(s);
+            const uint32_t w0 = mrg_next(s, K);
+            const uint32_t w1 = mrg_next(s, K);
             h += hit(w0, w1);
         }
         total += h;
@@ -276,6 +385,24 @@ cudaError_t launch_vec(const MrgLaunch& p, Grid g, cudaStream_t s)
 }
 
 }  // namespace
+
+size_t mrg_fill_tma_smem(int threads) { return (size_t)(threads / 32) * 4096 + 1024; }
+
+cudaError_t launch_mrg_fill_tma(const MrgLaunch& p, const CUtensorMap& tmap, int kind, Grid g, cudaStream_t s)
+{
+    const size_t sm = mrg_fill_tma_smem((int)g.threads);
+    if (kind == kF64) {
+        if (p.seg_fastest) mrg_fill_tma_kernel<kF64, true><<<g.blocks, g.threads, sm, s>>>(p, tmap);
+        else mrg_fill_tma_kernel<kF64, false><<<g.blocks, g.threads, sm, s>>>(p, tmap);
+    } else if (kind == kF32) {
+        if (p.seg_fastest) mrg_fill_tma_kernel<kF32, true><<<g.blocks, g.threads, sm, s>>>(p, tmap);
+        else mrg_fill_tma_kernel<kF32, false><<<g.blocks, g.threads, sm, s>>>(p, tmap);
+    } else {
+        if (p.seg_fastest) mrg_fill_tma_kernel<kU32, true><<<g.blocks, g.threads, sm, s>>>(p, tmap);
+        else mrg_fill_tma_kernel<kU32, false><<<g.blocks, g.threads, sm, s>>>(p, tmap);
+    }
+    return cudaGetLastError();
+}
 
 size_t mrg_fill_smem(int threads, int kind)
 {
@@ -340,6 +467,12 @@ cudaError_t mrg_occupancy(int kernel, int kind, bool fast, int threads, int* out
     }
     case kKMrgMc:
         return occ(mrg_mc_kernel, threads, 0, out);
+    case kKMrgFillTma: {
+        const size_t sm = mrg_fill_tma_smem(threads);
+        if (kind == kU32) return occ(mrg_fill_tma_kernel<kU32, false>, threads, sm, out);
+        if (kind == kF32) return occ(mrg_fill_tma_kernel<kF32, false>, threads, sm, out);
+        return occ(mrg_fill_tma_kernel<kF64, false>, threads, sm, out);
+    }
     }
     return cudaErrorInvalidValue;
 }

@@ -21,6 +21,15 @@
 
 #include "shv_internal.h"
 
+#include <cudaTypedefs.h>  // PFN_cuTensorMapEncodeTiled
+
+#ifndef SHV_MRG_ORDER
+#define SHV_MRG_ORDER 0  // lab: 0 = by row length, 1 = streams fastest, 2 = segments fastest
+#endif
+#ifndef SHV_MRG_TMA
+#define SHV_MRG_TMA 1  // MRG32k3a fills store through TMA (0: per-lane vector stores; lab A/B)
+#endif
+
 #include <nvtx3/nvToolsExt.h>
 
 namespace shv {
@@ -329,11 +338,44 @@ shv_status check_advance(const Handle& h, u128 draws)
     return SHV_OK;
 }
 
+// cuTensorMapEncodeTiled from the driver (no libcuda link); nullptr if absent.
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder()
+{
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            p = nullptr;
+        return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }();
+    return fn;
+}
+
+// 2D map of `ns` rows x `n` values of `elem` bytes at `out` (row-major), box
+// 128 B x 32 rows with the 128-byte swizzle (mrg_fill_tma_kernel).
+bool encode_rows_map(CUtensorMap* m, void* out, uint64_t n, uint64_t ns, int elem)
+{
+    const auto enc = tensor_map_encoder();
+    if (!enc) return false;
+    const cuuint64_t dims[2] = {n, ns};
+    const cuuint64_t strides[1] = {n * (uint64_t)elem};
+    const cuuint32_t box[2] = {128u / (cuuint32_t)elem, 32u};
+    const cuuint32_t estr[2] = {1, 1};
+    return enc(m, elem == 8 ? CU_TENSOR_MAP_DATA_TYPE_UINT64 : CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, out, dims, strides,
+               box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 // Segment jumps of a MRG launch: seg0 = A^o, segpow[b] = (A^(L*dpu))^(2^b)
 // for the bits b that segment indices < nseg use.
 void fill_mrg_segments(const Handle& h, uint64_t units_per_seg, uint64_t draws_per_unit, uint32_t nseg,
                        MrgLaunch* P)
 {
+    // shv::dev::MrgFpK: 1.5*2^52, RN(1/m1), RU(1/m2), m1, m2, a23n*m2 (include/shv_device.cuh)
+    const double fpk[6] = {6755399441055744.0, 1.0 / 4294967087.0, 0x1.000059451f212p-32,
+                           4294967087.0, 4294944443.0, 5886603609186927.0};
+    memcpy(P->fpk, fpk, sizeof fpk);
     P->seg0 = pair_pow(h.offset, 0);
     P->segpow[0] = pair_pow((u128)units_per_seg * draws_per_unit, 0);
     for (int b = 1; b < kSegBits && ((uint64_t)nseg - 1) >> b; ++b)
@@ -543,15 +585,26 @@ shv_status generate(shv_streams hid, T* out, uint64_t n, void* stream, int kind,
             P->ns = ns;
             P->out = dst;
             P->n = n;
-            // vector path: segments in whole 256-byte staging rounds (64 values)
-            split(h, ns, n, vec ? 64 : 1, 8, resident_threads(h, kKMrgFill, kind, vec), 1ull << 40,
+            // TMA path for 4-byte values: 128-B boxes of 32 rows (16-B aligned rows, int32 box
+            // coordinates). f64 keeps the staged 256-B warp stores, faster there.
+            bool tma = SHV_MRG_TMA && vec && kind != kF64 && n < (1ull << 31) && ns < (1ull << 31);
+            const int kid = tma ? kKMrgFillTma : kKMrgFill;
+            // vector paths: segments in whole 256-byte rounds (64 values; 2 or 4 TMA boxes)
+            split(h, ns, n, vec ? 64 : 1, 8, resident_threads(h, kid, kind, vec), 1ull << 40,
                   &P->seg_len, &P->nseg);
-            if (vec && P->seg_len % 8) vec = false;
+            if (vec && P->seg_len % 64) vec = tma = false;  // user segment length: per-lane paths
             P->items = ns * P->nseg;
-            P->seg_fastest = row_bytes > (512u << 10);
+            P->seg_fastest = SHV_MRG_ORDER ? SHV_MRG_ORDER == 2 : row_bytes > (512u << 10);
             fill_mrg_segments(h, P->seg_len, 1, P->nseg, P.get());
-            Grid g{blocks_for(h, kKMrgFill, kind, vec, P->items), h.tpb};
-            err = launch_mrg_fill(*P, kind, vec, g, s);
+            CUtensorMap tmap;
+            if (tma && !encode_rows_map(&tmap, dst, n, ns, (int)sizeof(T))) tma = false;
+            if (tma) {
+                Grid g{blocks_for(h, kKMrgFillTma, kind, true, P->items), h.tpb};
+                err = launch_mrg_fill_tma(*P, tmap, kind, g, s);
+            } else {
+                Grid g{blocks_for(h, kKMrgFill, kind, vec, P->items), h.tpb};
+                err = launch_mrg_fill(*P, kind, vec, g, s);
+            }
         } else {
             const uint64_t E = kind == kF64 ? 4 : 8;
             const bool fast = aligned32 && (n % E == 0) && ((uint32_t)h.offset & 3) == 0;

@@ -3,6 +3,7 @@
 #pragma once
 #include <cstddef>
 #include <cstdint>
+#include <cuda.h>  // CUtensorMap (types only; the encoder comes from cudaGetDriverEntryPoint)
 #include <cuda_runtime.h>
 
 namespace shv {
@@ -41,6 +42,9 @@ struct MrgLaunch {
     uint32_t seg_fastest;    // 1: work item it -> (i = it / nseg, j = it % nseg)
     MatPair seg0;                 // A^o (o = handle offset)
     MatPair segpow[kSegBits];     // (A^(seg_len * draws per unit))^(2^b)
+    double fpk[6];                // FP64 step constants (shv::dev::MrgFpK order), set by
+                                  // fill_mrg_segments: read from the parameter block so
+                                  // ptxas keeps them in registers
 };
 
 // Philox4x32-10 bulk fill / Monte Carlo launch. Draw d of handle stream i
@@ -153,6 +157,11 @@ cudaError_t upload_jump_tables(const MatPair* sub51, const MatPair* str64, const
 cudaError_t launch_mrg_seed(uint32_t* state, uint64_t n, const uint32_t base[6], int table,
                             const MatPair& step, Grid g, cudaStream_t s);
 cudaError_t launch_mrg_fill(const MrgLaunch& p, int kind, bool vec, Grid g, cudaStream_t s);
+// MRG32k3a fill with TMA stores: `tmap` is a 2D map of the launch's rows
+// (dim0 = n values, dim1 = ns rows, box 128 B x 32 rows, 128-B swizzle);
+// needs seg_len % (128 / value bytes) == 0, n and ns < 2^31.
+cudaError_t launch_mrg_fill_tma(const MrgLaunch& p, const CUtensorMap& tmap, int kind, Grid g, cudaStream_t s);
+size_t mrg_fill_tma_smem(int threads);
 cudaError_t launch_mrg_mc(const MrgLaunch& p, Grid g, cudaStream_t s);
 cudaError_t launch_philox_fill(const PhiloxLaunch& p, int kind, bool fast, Grid g, cudaStream_t s);
 cudaError_t launch_philox_mc(const PhiloxLaunch& p, bool fast, Grid g, cudaStream_t s);
@@ -175,6 +184,7 @@ enum KernelId : int {
     kKThreefryMc = 10,
     kKLeapFill = 11,  // kind = output kind; `fast` = vector path; generator via leap_kernel_id
     kKLeapMc = 14,
+    kKMrgFillTma = 17,  // after the leap ids 11..16
 };
 // Leap kernels are keyed by (base id + generator): 11..13 fills, 14..16 MC.
 constexpr int leap_kernel_id(int base, int lgen) { return base + lgen; }
@@ -188,7 +198,7 @@ cudaError_t leap_occupancy(int kernel, int kind, bool fast, int threads, int* ou
 inline cudaError_t max_blocks_per_sm(int kernel, int kind, bool fast, int threads, int* out)
 {
     switch (kernel) {
-    case kKSeed: case kKMrgFill: case kKMrgMc:
+    case kKSeed: case kKMrgFill: case kKMrgMc: case kKMrgFillTma:
         return mrg_occupancy(kernel, kind, fast, threads, out);
     case kKPhiloxFill: case kKPhiloxMc: case kKPhiloxFillKeyed: case kKPhiloxMcKeyed:
         return philox_occupancy(kernel, kind, fast, threads, out);

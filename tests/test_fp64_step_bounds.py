@@ -1,0 +1,73 @@
+"""Exactness argument of the FP64 MRG32k3a step (include/shv_device.cuh:
+mrg_c1_floor, mrg_c2_floor), checked with exact rationals.
+
+The GPU step computes k = floor(p * inv) with one fma rounded toward -inf and
+r = p - k*m. It is exact iff inv's rounding error delta keeps p*inv on the
+same side of every integer as p/m. These tests pin the constants the header
+uses and the bounds the argument needs; they do not run the kernels (the
+GPU parity tests do)."""
+import math
+import os
+import random
+from fractions import Fraction as Fr
+
+M1, M2 = 4294967087, 4294944443
+A12, A13N, A21, A23N = 1403580, 810728, 527612, 1370589
+INV1 = 1.0 / M1                       # RN(1/m1)
+INV2 = float.fromhex("0x1.000059451f212p-32")  # RU(1/m2)
+HDR = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "include", "shv_device.cuh")
+
+
+def floor_red(p: int, inv: float, m: int) -> int:
+    """r = p - floor(p*inv)*m with p*inv exact (the fma's exact product, then RD)."""
+    return p - math.floor(Fr(p) * Fr(inv)) * m
+
+
+def test_header_constants():
+    src = open(HDR).read()
+    assert "0x1.000059451f212p-32" in src and "1.0 / (double)kM1" in src
+    assert INV2 == math.nextafter(1.0 / M2, 1.0)  # RU(1/m2): RN(1/m2) rounds down
+    assert A23N * M2 == 5886603609186927 and float(A23N * M2) == A23N * M2 < 2**53
+
+
+def test_inverse_errors_and_bounds():
+    d1 = Fr(INV1) - Fr(1, M1)
+    d2 = Fr(INV2) - Fr(1, M2)
+    assert d1 > 0 and d2 > 0
+    # component 1: signed form, states in [0, m1] -> |p| <= max(a12, a13n) * m1 < 2^53
+    p1max = max(A12, A13N) * M1
+    assert p1max < 2**53 and p1max * M1 * d1 < 1
+    # component 2: positive form a21*y2 + a23n*(m2 - y0), y in [0, m2)
+    p2max = A21 * (M2 - 1) + A23N * M2
+    assert p2max < 2**53 and p2max * M2 * d2 < 1
+
+
+def test_floor_reduction_edges_and_random():
+    rng = random.Random(1412)
+    # component 2: always the canonical residue
+    cases = [0, 1, M2 - 1, M2, M2 + 1, A23N * M2, A21 * (M2 - 1) + A23N * M2]
+    cases += [k * M2 + r for k in (1, 7, 1 << 20) for r in (0, 1, M2 - 1)]
+    for _ in range(20000):
+        y0, y2 = rng.randrange(M2), rng.randrange(M2)
+        cases.append(A21 * y2 + A23N * (M2 - y0))
+    for p in cases:
+        assert floor_red(p, INV2, M2) == p % M2, p
+    # component 1: canonical, or m1 when p is a negative multiple of m1
+    cases = [0, 1, -1, M1 - 1, -(M1 - 1), M1, -M1, A12 * M1, -A13N * M1]
+    cases += [s * (k * M1 + r) for s in (1, -1) for k in (1, 5, 1 << 19) for r in (0, 1, M1 - 1)]
+    for _ in range(20000):
+        x0, x1 = rng.randrange(M1 + 1), rng.randrange(M1 + 1)
+        cases.append(A12 * x1 - A13N * x0)
+    for p in cases:
+        r = floor_red(p, INV1, M1)
+        assert r == p % M1 or (r == M1 and p % M1 == 0 and p < 0), p
+        assert 0 <= r <= M1
+
+
+def test_combine_maps_m1_like_zero():
+    # mrg_combine(p1, p2) = p1 - p2 (+ m1 if p1 <= p2), wrap-around u32
+    def comb(p1, p2):
+        z = (p1 - p2) % 2**32
+        return (z + M1) % 2**32 if p1 <= p2 else z
+    for p2 in (0, 1, 12345, M2 - 1):
+        assert comb(M1, p2) == comb(0, p2)

@@ -336,6 +336,36 @@ def test_mc_counts_small_full(shv, orc, gen, sp):
     f.close()
 
 
+# Seeds whose first step hits the edges of the FP64 floor reductions
+# (tests/test_fp64_step_bounds.py): component 1 at residue 0 with p < 0 (the
+# step carries r = m1) together with component 2 at residue 0 (a tie, z = m1);
+# both components at residue m - 1; SURVEY App. A.1's tie state.
+EDGE_SEEDS = [
+    [4294809486, 2474611487, 12345, 0, 1, 0],
+    [4294967086, 3588371285, 7, 0, 5, 4239484263],
+    [0, 1, 0, 0, 0, 1226359468],
+]
+
+
+@pytest.mark.parametrize("seed", EDGE_SEEDS)
+def test_mrg_fp64_step_edge_states(shv, orc, seed):
+    for n, kind in ((64, "u32"), (37, "u32"), (64, "f32"), (32, "f64")):
+        f = Fam(shv, W.MRG32K3A, seed, 3, 0)
+        got = f.gen_(n, kind)
+        same(got, f.ref(orc, n, kind, offset=0))
+        f.close()
+    z0 = orc.generate(W.MRG32K3A, seed, 1, 1)[0, 0]
+    assert seed != EDGE_SEEDS[0] or z0 == M1  # the tie
+    f = Fam(shv, W.MRG32K3A, seed, 3, 0)
+    hits = torch.zeros(1, dtype=torch.int64, device="cuda")
+    cnt = torch.zeros(3, dtype=torch.int64, device="cuda")
+    shv.shv_mc_pi_ex(f.h, 100, hits, cnt, None)
+    torch.cuda.synchronize()
+    tot, ref = orc.mc_count(W.MRG32K3A, seed, 3, 100)
+    assert np.array_equal(cnt.cpu().numpy().astype(np.uint64), ref) and int(hits.item()) == tot
+    f.close()
+
+
 # ---------------------------------------------------------------- full BASELINE sizes
 
 def _golden_full():

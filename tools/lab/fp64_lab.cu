@@ -19,6 +19,8 @@ __global__ void k(double* out, double s, double u)
             if (K == 4) a[c] = __fma_rn(a[c], a[(c + 2) % CH], a[(c + 1) % CH]);  // DFMA 3 pairs
             if (K == 5) a[c] = __dadd_rn(a[c], a[(c + 1) % CH]);              // DADD 2 pairs
             if (K == 6) a[c] = __dmul_rn(a[c], a[(c + 1) % CH]);              // DMUL 2 pairs
+            if (K == 7) a[c] = __fma_rd(a[c], u, a[(c + 1) % CH]);            // DFMA.RM uniform, 2 pairs
+            if (K == 8) a[c] = __fma_rn(a[c], 1e-300, 0.5);                   // DFMA imm + const, 1 pair
         }
     }
     double r = 0;
@@ -33,8 +35,8 @@ int main()
     int sms; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
     double* o; cudaMalloc(&o, 8);
     const int blocks = sms * 8, thr = 256;
-    const char* names[] = {"dadd_imm", "dmul_imm", "dfma_imm_2pairs", "dfma_ur_2pairs", "dfma_3pairs", "dadd_2pairs", "dmul_2pairs"};
-    float t[7];
+    const char* names[] = {"dadd_imm", "dmul_imm", "dfma_imm_2pairs", "dfma_ur_2pairs", "dfma_3pairs", "dadd_2pairs", "dmul_2pairs", "dfma_rm_ur_2pairs", "dfma_1pair"};
+    float t[9];
     t[0] = tms([&] { k<0><<<blocks, thr>>>(o, 1.0, 0.5); });
     t[1] = tms([&] { k<1><<<blocks, thr>>>(o, 1.0, 0.5); });
     t[2] = tms([&] { k<2><<<blocks, thr>>>(o, 1.0, 0.5); });
@@ -42,8 +44,10 @@ int main()
     t[4] = tms([&] { k<4><<<blocks, thr>>>(o, 1.0, 0.5); });
     t[5] = tms([&] { k<5><<<blocks, thr>>>(o, 1.0, 0.5); });
     t[6] = tms([&] { k<6><<<blocks, thr>>>(o, 1.0, 0.5); });
+    t[7] = tms([&] { k<7><<<blocks, thr>>>(o, 1.0, 0.5); });
+    t[8] = tms([&] { k<8><<<blocks, thr>>>(o, 1.0, 0.5); });
     printf("{");
-    for (int i = 0; i < 7; ++i)  // ops per SM per ns (divide by GHz for per clock)
+    for (int i = 0; i < 9; ++i)  // ops per SM per ns (divide by GHz for per clock)
         printf("%s\"%s_per_sm_per_ns\": %.2f", i ? ", " : "", names[i], (double)blocks * thr * IT * CH / (t[i] * 1e6) / sms);
     printf("}\n");
 }
