@@ -416,6 +416,32 @@ def main():
             parts[key] = fill_part(fill_ms(h, out, n), total_per_rank)
             shv.shv_streams_destroy(h)
 
+        # Disjointness audit (NEXT-4; S L407-415) of the first 2^18 MRG32k3a C5
+        # rows (2^18 x 4093 ~ 1.07e9 four-word windows, 34 GB hash table)
+        na = min(wm.n_streams, 1 << 18)
+        h = shv.shv_streams_create_ex(wm.gen, list(wm.seed), wm.first, na, wm.spacing, state, 0, local, sp)
+        shv.shv_generate_u32(h, out, n, sp)
+        shv.shv_streams_destroy(h)
+        wsb = shv.shv_verify_disjoint_workspace_bytes(na, n)
+        ws_a = torch.empty(wsb // 8, dtype=torch.int64, device=dev)
+        rep = torch.zeros(7, dtype=torch.int64, device=dev)
+        times = []
+        for it in range(3):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            shv.shv_verify_disjoint(out, na, n, ws_a, wsb, rep, sp)
+            b.record(stream)
+            torch.cuda.synchronize()
+            if it:
+                times.append(a.elapsed_time(b))
+        r = dict(zip(shv.DISJOINT_REPORT_FIELDS, rep.cpu().tolist()))
+        t_ms = statistics.mean(times)
+        parts["audit_mrg_c5_prefix"] = {"ms": round(t_ms, 3), "pe": na, "horizon": n, "windows": r["windows"],
+                                        "Gwindows_per_s": round(r["windows"] / (t_ms * 1e-3) / 1e9, 2),
+                                        "disjoint": bool(r["disjoint"]), "colliding": r["colliding"],
+                                        "workspace_bytes": wsb}
+        del ws_a
+
         # C6: stream-count sweep at a fixed 2^32 u32 per GPU (16 GiB),
         # n_streams = 2^13 .. 2^22, n_per_stream = total / n_streams, both generators.
         # Acceptance: every point within 10% of the C5 (2^20 x 4096) figure.

@@ -249,6 +249,40 @@ shv_status shv_streams_destroy(shv_streams h);
 const char* shv_status_string(shv_status s);
 const char* shv_last_error_message(void);
 
+/* ---- disjointness audit (S L407-415 [partition: verify_disjoint], L425-426) ----
+ * Audits rows that were generated for n_pe processing elements (e.g. the
+ * d_out of shv_generate_u32: row i = the draws of stream i; P L109-122 [§2.3]
+ * "non-overlapping contiguous blocks"): every window of 4 consecutive u32
+ * draws of every row is hashed into a table in d_workspace, and a window value
+ * held by two DIFFERENT rows is a collision (single-word coincidences are
+ * expected by birthday statistics and prove nothing, S L426).
+ *   d_rows      device u32[n_pe * horizon], row-major (row i at i*horizon);
+ *   horizon     draws per PE; rows shorter than 4 have no windows;
+ *   d_workspace device scratch of workspace_bytes, 8-byte aligned, at least
+ *               16 * (windows + 1) bytes; shv_verify_disjoint_workspace_bytes
+ *               gives the recommended size (table load 1/2; a fuller table is
+ *               correct but probes longer);
+ *   d_report    device shv_disjoint_report, written stream-ordered.
+ * The report is a function of the rows alone (deterministic merge, S L429):
+ * if not disjoint, (pe_a, pos_a, pe_b, pos_b) is the lexicographically
+ * smallest over all pairs of equal windows with pe_a < pe_b; otherwise those
+ * four fields are ~0. Runs on the CURRENT CUDA device (all three pointers must
+ * be on it). Errors: NULL pointers or n_pe * horizon >= 2^40 ->
+ * SHV_ERR_INVALID_ARGUMENT; workspace too small -> SHV_ERR_INVALID_ARGUMENT;
+ * misaligned workspace or report -> SHV_ERR_MISALIGNED. */
+typedef struct {
+    uint64_t disjoint;    /* 1: no window value is held by two different PEs */
+    uint64_t windows;     /* n_pe * (horizon - 3), 0 if horizon < 4 */
+    uint64_t colliding;   /* distinct window values held by >= 2 different PEs */
+    uint64_t pe_a, pos_a; /* first collision (see above) */
+    uint64_t pe_b, pos_b;
+} shv_disjoint_report;
+
+size_t shv_verify_disjoint_workspace_bytes(uint64_t n_pe, uint64_t horizon);
+shv_status shv_verify_disjoint(const uint32_t* d_rows, uint64_t n_pe, uint64_t horizon,
+                               void* d_workspace, size_t workspace_bytes,
+                               shv_disjoint_report* d_report, void* cuda_stream);
+
 /* ---- launch configuration (results never depend on it; R10) ---- */
 /* Override the persistent-grid shape and work split of one handle:
  * blocks_per_sm (0 = occupancy maximum), threads_per_block (0 = 256,

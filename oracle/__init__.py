@@ -248,7 +248,8 @@ def verify_disjoint(rows):
     """Disjointness audit by definition (S L407-415 verify_disjoint; S L425):
     ``rows`` = one array of u32 draws per PE, in PE order. Every window of 4
     consecutive draws is recorded with its (pe, pos); a collision is a window
-    held by two different PEs. Returns {"disjoint", "windows"} and, if not
+    held by two different PEs. Returns {"disjoint", "windows", "colliding" (distinct
+    window values held by >= 2 different PEs)} and, if not
     disjoint, the lexicographically smallest (pe_a, pos_a, pe_b, pos_b) with
     pe_a < pe_b over all colliding pairs. Plain dict of windows; no hashing
     shortcut, no sorting."""
@@ -260,9 +261,12 @@ def verify_disjoint(rows):
             seen.setdefault(tuple(r[pos:pos + 4]), []).append((pe, pos))
             windows += 1
     best = None
+    colliding = 0
     for occ in seen.values():
         if len(occ) < 2:
             continue
+        if len({pe for pe, _ in occ}) > 1:
+            colliding += 1
         for x in range(len(occ)):
             for y in range(x + 1, len(occ)):
                 (pa, qa), (pb, qb) = occ[x], occ[y]
@@ -271,7 +275,7 @@ def verify_disjoint(rows):
                 cand = (pa, qa, pb, qb) if pa < pb else (pb, qb, pa, qa)
                 if best is None or cand < best:
                     best = cand
-    out = {"disjoint": best is None, "windows": windows}
+    out = {"disjoint": best is None, "windows": windows, "colliding": colliding}
     if best is not None:
         out.update(pe_a=best[0], pos_a=best[1], pe_b=best[2], pos_b=best[3])
     return out

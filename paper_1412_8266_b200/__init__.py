@@ -46,7 +46,11 @@ EXPORTS = (
     "shv_status_string", "shv_last_error_message", "shv_set_launch_config",
     "shv_partition", "shv_jump_matrix", "shv_build_info", "shv_get_device_view",
     "shv_streams_create_tinymt32", "shv_streams_create_leapfrog",
+    "shv_verify_disjoint_workspace_bytes", "shv_verify_disjoint",
 )
+
+#: Field order of shv_disjoint_report (seven u64 words, include/shv.h).
+DISJOINT_REPORT_FIELDS = ("disjoint", "windows", "colliding", "pe_a", "pos_a", "pe_b", "pos_b")
 
 
 class ShvError(RuntimeError):
@@ -103,6 +107,8 @@ def _load():
                                              u64, u64, vp, C.c_size_t, C.c_int, vp]),
         "shv_streams_create_leapfrog": (st, [C.POINTER(u64), C.c_int, u32p, C.c_size_t, u64, u64, u64,
                                              vp, C.c_size_t, C.c_int, vp]),
+        "shv_verify_disjoint_workspace_bytes": (C.c_size_t, [u64, u64]),
+        "shv_verify_disjoint": (st, [vp, u64, u64, vp, C.c_size_t, vp, vp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -256,6 +262,18 @@ def shv_jump_matrix(e: int):
     _check(lib.shv_jump_matrix(e & ((1 << 64) - 1), e >> 64, out))
     v = list(out)
     return [v[0:3], v[3:6], v[6:9]], [v[9:12], v[12:15], v[15:18]]
+
+
+def shv_verify_disjoint_workspace_bytes(n_pe: int, horizon: int) -> int:
+    return int(lib.shv_verify_disjoint_workspace_bytes(n_pe, horizon))
+
+
+def shv_verify_disjoint(d_rows, n_pe: int, horizon: int, d_workspace, workspace_bytes: int,
+                        d_report, stream=None):
+    """Stream-ordered; d_report (7 u64 on the device, DISJOINT_REPORT_FIELDS
+    order) is valid after the stream completes."""
+    _check(lib.shv_verify_disjoint(_ptr(d_rows), n_pe, horizon, _ptr(d_workspace), workspace_bytes,
+                                   _ptr(d_report), _stream(stream)))
 
 
 def shv_status_string(s: int) -> str:

@@ -1186,6 +1186,52 @@ shv_status shv_set_launch_config(shv_streams hid, uint32_t bps, uint32_t tpb, ui
     return SHV_OK;
 }
 
+static uint64_t audit_windows(uint64_t n_pe, uint64_t horizon)
+{
+    return horizon < 4 ? 0 : n_pe * (horizon - 3);
+}
+
+size_t shv_verify_disjoint_workspace_bytes(uint64_t n_pe, uint64_t horizon)
+{
+    if (n_pe && horizon > (((uint64_t)1 << 40) - 1) / n_pe) return 0;
+    return (size_t)16 * (2 * audit_windows(n_pe, horizon) + 1);
+}
+
+shv_status shv_verify_disjoint(const uint32_t* d_rows, uint64_t n_pe, uint64_t horizon, void* d_ws,
+                               size_t ws_bytes, shv_disjoint_report* d_report, void* stream)
+{
+    Range nvtx_range("shv_verify_disjoint");
+    if (!d_report) return fail(SHV_ERR_INVALID_ARGUMENT, "NULL d_report");
+    if ((uintptr_t)d_report & 7) return fail(SHV_ERR_MISALIGNED, "d_report not 8-byte aligned");
+    if (n_pe && horizon > (((uint64_t)1 << 40) - 2) / n_pe)
+        return fail(SHV_ERR_INVALID_ARGUMENT, "n_pe * horizon must be below 2^40 - 1");
+    AuditLaunch P{};
+    P.rows = d_rows;
+    P.horizon = horizon;
+    P.wpr = horizon < 4 ? 0 : horizon - 3;
+    P.windows = audit_windows(n_pe, horizon);
+    P.report = d_report;
+    if (P.windows) {
+        if (!d_rows || !d_ws) return fail(SHV_ERR_INVALID_ARGUMENT, "NULL d_rows or d_workspace");
+        if ((uintptr_t)d_ws & 7) return fail(SHV_ERR_MISALIGNED, "d_workspace not 8-byte aligned");
+        P.cap = ws_bytes / 16;
+        if (P.cap <= P.windows)
+            return fail(SHV_ERR_INVALID_ARGUMENT, "workspace of %zu bytes holds %llu slots; %llu windows need more",
+                        ws_bytes, (unsigned long long)P.cap, (unsigned long long)P.windows);
+        P.slots = (unsigned long long*)d_ws;
+        P.second = P.slots + P.cap;
+    }
+    int dev = 0, sms = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (e != cudaSuccess) return cuda_fail(e, "device query");
+    const uint64_t want = (P.windows + 255) / 256;
+    const unsigned blocks = (unsigned)(want < (uint64_t)sms * 8 ? (want ? want : 1) : (uint64_t)sms * 8);
+    e = launch_audit(P, blocks, (cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_fail(e, "verify_disjoint launch");
+    return SHV_OK;
+}
+
 const char* shv_status_string(shv_status s)
 {
     switch (s) {

@@ -6,6 +6,8 @@
 #include <cuda.h>  // CUtensorMap (types only; the encoder comes from cudaGetDriverEntryPoint)
 #include <cuda_runtime.h>
 
+#include "../../include/shv.h"  // shv_disjoint_report
+
 namespace shv {
 
 // Intra-stream Sequence Splitting (P L109-112 [§2.3]): a launch splits each
@@ -165,6 +167,17 @@ size_t mrg_fill_tma_smem(int threads);
 cudaError_t launch_mrg_mc(const MrgLaunch& p, Grid g, cudaStream_t s);
 cudaError_t launch_philox_fill(const PhiloxLaunch& p, int kind, bool fast, Grid g, cudaStream_t s);
 cudaError_t launch_philox_mc(const PhiloxLaunch& p, bool fast, Grid g, cudaStream_t s);
+// Disjointness audit (kernels_audit.cu; S L407-415): rows = n_pe rows of
+// `horizon` u32, windows = n_pe * wpr (wpr = horizon - 3), table of cap slots
+// (slots, second: cap u64 each), report on the device.
+struct AuditLaunch {
+    const uint32_t* rows;
+    uint64_t horizon, wpr, windows, cap;
+    unsigned long long* slots;
+    unsigned long long* second;
+    shv_disjoint_report* report;
+};
+cudaError_t launch_audit(const AuditLaunch& p, unsigned blocks, cudaStream_t s);
 // Leap Frog (kernels_leapfrog.cu): vec = 32-byte aligned rows, seg_len % 8 == 0.
 cudaError_t launch_leap_fill(const LeapLaunch& p, int lgen, int kind, bool vec, Grid g, cudaStream_t s);
 cudaError_t launch_leap_mc(const LeapLaunch& p, int lgen, Grid g, cudaStream_t s);

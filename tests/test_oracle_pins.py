@@ -544,6 +544,14 @@ def _brute_first_collision(rows):
     return best
 
 
+def _brute_colliding(rows):
+    # distinct window values that occur in at least two different rows
+    values = {tuple(int(x) for x in r[i:i + 4]) for r in rows for i in range(len(r) - 3)}
+    def holds(r, v):
+        return any(tuple(int(x) for x in r[i:i + 4]) == v for i in range(len(r) - 3))
+    return sum(1 for v in values if sum(holds(r, v) for r in rows) >= 2)
+
+
 def test_verify_disjoint_matches_brute_force(orc):
     rng = np.random.default_rng(5)
     for trial in range(40):
@@ -554,6 +562,7 @@ def test_verify_disjoint_matches_brute_force(orc):
         if want is not None:
             assert (got["pe_a"], got["pos_a"], got["pe_b"], got["pos_b"]) == want, trial
         assert got["windows"] == sum(len(r) - 3 for r in rows)
+        assert got["colliding"] == _brute_colliding(rows), trial
 
 
 def test_verify_disjoint_spec_examples(orc):
@@ -562,6 +571,7 @@ def test_verify_disjoint_spec_examples(orc):
     b = orc.generate(W.PHILOX4X32_10, [7], 4, 200, first=2)
     r = orc.verify_disjoint(list(a) + list(b))
     assert not r["disjoint"] and (r["pe_a"], r["pos_a"], r["pe_b"], r["pos_b"]) == (2, 0, 4, 0)
+    assert r["colliding"] == 2 * 197  # streams 2 and 3 appear twice: every window of both rows
     # shifted overlap: stream 1 at offset 17 is also in the plan
     c = orc.generate(W.PHILOX4X32_10, [7], 1, 100, first=1, offset=17)
     r = orc.verify_disjoint(list(a) + list(c))
