@@ -292,24 +292,29 @@ def main():
     dom = max(kms, key=kms.get)
     alg_bytes = 4 * total_per_rank  # u32 written per launch (4 B/number, 0 read)
     achieved = alg_bytes / (kms[dom] * 1e-3) / 1e9
-    roof = {"bound": "hbm", "kernel": "mrg_fill_tma_kernel<u32>" if dom == "mrg" else "philox_fill_fast_kernel<u32>",
-            "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-            "frac": round(achieved / peak, 4), "peak_source": peak_src,
-            "traffic": traffic_from_profiles(dom),
-            "limiter": limiter_from_profiles(dom),
-            "algorithmic_bytes_per_launch": alg_bytes}
-    # The MRG32k3a fill also has a compute roofline on the FP64 pipe (DESIGN.md
-    # §4.2/§11): 12 FP64 instructions per number (SASS count of the step),
-    # against the measured FP64 rate (tools/lab/fp64_lab.cu: 122.4
-    # DFMA/DMUL/DADD per SM per ns at 1965 MHz, i.e. 62.3 per SM per clock) x
-    # 148 SMs.
+    hbm = {"bound": "hbm", "kernel": "mrg_fill_tma_kernel<u32>" if dom == "mrg" else "philox_fill_fast_kernel<u32>",
+           "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+           "frac": round(achieved / peak, 4), "peak_source": peak_src,
+           "traffic": traffic_from_profiles(dom),
+           "limiter": limiter_from_profiles(dom),
+           "algorithmic_bytes_per_launch": alg_bytes}
+    roof = hbm
+    # The MRG32k3a fill binds on the FP64 pipe before it reaches the HBM-write
+    # roofline (DESIGN.md §4.2/§4.5; ncu: fp64 pipe ~76 %, DRAM ~56 %): 12 FP64
+    # instructions per number (SASS count of the step) cap it at 18.61/12 =
+    # 1.55 T numbers/s = 6.2 TB/s, below the 6.55 TB/s copy peak. Peak from unit
+    # counts and clock (B200_PROFILING: 148 SMs, 1965 MHz max; 64 FP64
+    # instructions per SM per clock, measured 62.3 by tools/lab/fp64_lab.cu).
+    # The top-level roofline is the binding one ("whichever binds", north star);
+    # the HBM figure stays beside it.
     if dom == "mrg":
-        fp64_peak = 122.4 * 148 / 1e3  # T FP64 instructions / s
+        fp64_peak = 148 * 64 * 1.965e9 / 1e12  # T FP64 instructions / s
         fp64_ach = 12 * total_per_rank / (kms["mrg"] * 1e-3) / 1e12
-        roof["compute"] = {"bound": "alu", "pipe": "fp64", "achieved": round(fp64_ach, 2),
-                           "peak": round(fp64_peak, 2), "unit": "T instr/s",
-                           "frac": round(fp64_ach / fp64_peak, 4),
-                           "per_number": "12 FP64 instructions (SASS of mrg_fill_tma_kernel<u32>)"}
+        roof = {"bound": "alu", "pipe": "fp64", "kernel": hbm["kernel"], "achieved": round(fp64_ach, 2),
+                "peak": round(fp64_peak, 2), "unit": "T instr/s", "frac": round(fp64_ach / fp64_peak, 4),
+                "peak_source": "unit counts x clock: 148 SMs x 64 FP64/clk x 1.965 GHz (measured 18.12, fp64_lab)",
+                "per_number": "12 FP64 instructions (SASS of mrg_fill_tma_kernel<u32>)",
+                "traffic": hbm["traffic"], "limiter": hbm["limiter"], "hbm": hbm}
     parts = {k: {"ms": round(kms[k], 4), "Gnumbers_per_s": round(total_per_rank / (kms[k] * 1e-3) / 1e9, 1),
                  "GB_per_s": round(alg_bytes / (kms[k] * 1e-3) / 1e9, 1),
                  "frac_of_hbm_peak": round(alg_bytes / (kms[k] * 1e-3) / 1e9 / peak, 4)}
