@@ -25,6 +25,7 @@ MRG32K3A = 1
 PHILOX4X32_10 = 2
 TINYMT32 = 3
 THREEFRY4X64_20 = 4
+MTGP32 = 5
 SPACING_STREAM = 0
 SPACING_SUBSTREAM = 1
 SPACING_KEYED = 2

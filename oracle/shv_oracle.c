@@ -332,6 +332,49 @@ void orc_tinymt32_jump(orc_tinymt32* t, uint64_t e_lo, uint64_t e_hi)
 }
 
 /* ------------------------------------------------------------------------ */
+/* MTGP32 ([Saito.Matsumoto2012]; P L74-76, L133-136), MEXP 11213            */
+/* ------------------------------------------------------------------------ */
+
+void orc_mtgp32_init(orc_mtgp32* m, const orc_mtgp32_params* p, uint32_t seed)
+{
+    const int n = ORC_MTGP32_N; /* mexp / 32 + 1 */
+    m->p = *p;
+    m->idx = 0;
+    const uint32_t hidden = p->tbl[4] ^ (p->tbl[8] << 16);
+    uint32_t fill = hidden;
+    fill += fill >> 16;
+    fill += fill >> 8;
+    fill &= 0xffu;
+    for (int i = 0; i < n; ++i) m->x[i] = fill * 0x01010101u; /* every byte = fill */
+    m->x[0] = seed;
+    m->x[1] = hidden;
+    for (int i = 1; i < n; ++i)
+        m->x[i] ^= 1812433253u * (m->x[i - 1] ^ (m->x[i - 1] >> 30)) + (uint32_t)i;
+}
+
+uint32_t orc_mtgp32_generate(orc_mtgp32* m)
+{
+    const int n = ORC_MTGP32_N;
+    const orc_mtgp32_params* p = &m->p;
+    const uint32_t x1 = m->x[m->idx];                           /* x_k */
+    const uint32_t x2 = m->x[(m->idx + 1) % n];                 /* x_{k+1} */
+    uint32_t y = m->x[(m->idx + (int)p->pos) % n];              /* x_{k+pos} */
+    const uint32_t t = m->x[(m->idx + (int)p->pos - 1) % n];    /* x_{k+pos-1} */
+    /* recursion (para_rec) */
+    uint32_t x = (x1 & p->mask) ^ x2;
+    x ^= x << p->sh1;
+    y = x ^ (y >> p->sh2);
+    const uint32_t r = y ^ p->tbl[y & 0x0f];
+    m->x[m->idx] = r; /* x_{k+N} takes x_k's slot */
+    m->idx = (m->idx + 1) % n;
+    /* tempering */
+    uint32_t u = t;
+    u ^= u >> 16;
+    u ^= u >> 8;
+    return r ^ p->tmp_tbl[u & 0x0f];
+}
+
+/* ------------------------------------------------------------------------ */
 /* conversions (R7)                                                          */
 /* ------------------------------------------------------------------------ */
 
@@ -395,6 +438,29 @@ int orc_stream_open(orc_stream* st, int gen, const uint32_t* seed, int nseed,
         /* slice start: 2^64 * slice draws (u128 exponent: slice < 2^64) */
         orc_tinymt32_jump(&st->tm, 0, slice);
         orc_tinymt32_jump(&st->tm, off_lo, off_hi);
+        return 0;
+    }
+    if (gen == ORC_MTGP32) {
+        /* seed = {seed_lo, seed_hi, n_params, 36 words per set} (R18) */
+        if (nseed < 3 || spacing != ORC_SPACING_STREAM || off_hi) return -1;
+        const uint32_t np = seed[2];
+        if ((uint64_t)nseed != 3 + 36ull * np) return -1;
+        const uint64_t g = first + i;
+        if (g >= np) return -1; /* one parameter set per state */
+        const uint32_t* w = seed + 3 + 36 * g;
+        orc_mtgp32_params p;
+        p.pos = w[0];
+        p.sh1 = w[1];
+        p.sh2 = w[2];
+        p.mask = w[3];
+        for (int k = 0; k < 16; ++k) {
+            p.tbl[k] = w[4 + k];
+            p.tmp_tbl[k] = w[20 + k];
+        }
+        if (p.pos < 2 || p.pos >= ORC_MTGP32_N || p.sh1 > 31 || p.sh2 > 31) return -1;
+        const uint64_t s64 = (uint64_t)seed[0] | ((uint64_t)seed[1] << 32);
+        orc_mtgp32_init(&st->mt, &p, (uint32_t)(s64 ^ (s64 >> 32)) + (uint32_t)g + 1u);
+        for (uint64_t k = 0; k < off_lo; ++k) (void)orc_mtgp32_generate(&st->mt);
         return 0;
     }
     if (gen == ORC_THREEFRY4X64_20) {
@@ -520,6 +586,7 @@ uint32_t orc_stream_next(orc_stream* st)
     }
     if (st->gen == ORC_MRG32K3A) return orc_mrg_step(st->s);
     if (st->gen == ORC_TINYMT32) return orc_tinymt32_generate(&st->tm);
+    if (st->gen == ORC_MTGP32) return orc_mtgp32_generate(&st->mt);
     if (st->gen == ORC_THREEFRY4X64_20) {
         if (st->tpos == 8) {
             const uint64_t ctr[4] = {st->blk, st->g, 0, 0};
@@ -600,7 +667,7 @@ static void* run_job(void* arg)
                 ((float*)jb->out)[at] = orc_to_f32(orc_stream_next(&st));
             } else if (jb->gen == ORC_MRG32K3A) {
                 ((double*)jb->out)[at] = orc_mrg_to_f64(orc_stream_next(&st));
-            } else { /* Philox and TinyMT32: 53 bits from two consecutive words (R7) */
+            } else { /* Philox, TinyMT32, MTGP32: 53 bits from two consecutive words (R7) */
                 uint32_t lo = orc_stream_next(&st);
                 uint32_t hi = orc_stream_next(&st);
                 ((double*)jb->out)[at] = orc_philox_to_f64(lo, hi);

@@ -19,7 +19,7 @@
 extern "C" {
 #endif
 
-enum { ORC_MRG32K3A = 1, ORC_PHILOX4X32_10 = 2, ORC_TINYMT32 = 3, ORC_THREEFRY4X64_20 = 4 };
+enum { ORC_MRG32K3A = 1, ORC_PHILOX4X32_10 = 2, ORC_TINYMT32 = 3, ORC_THREEFRY4X64_20 = 4, ORC_MTGP32 = 5 };
 enum { ORC_SPACING_STREAM = 0, ORC_SPACING_SUBSTREAM = 1, ORC_SPACING_KEYED = 2, ORC_SPACING_LEAPFROG = 3 };
 enum { ORC_U32 = 0, ORC_F32 = 1, ORC_F64 = 2 };
 
@@ -62,6 +62,26 @@ uint32_t orc_tinymt32_generate(orc_tinymt32* t); /* next_state then temper */
  * (e = e_hi*2^64 + e_lo, square-and-multiply; R15). */
 void orc_tinymt32_jump(orc_tinymt32* t, uint64_t e_lo, uint64_t e_hi);
 
+/* ---- MTGP32 (P L74-76 [§2.2], L133-136 [§2.3]; algorithm from
+ * [Saito.Matsumoto2012], Mersenne exponent 11213: N = 11213/32 + 1 = 351
+ * state words). Parameter set (one per state, the DC output; R18):
+ * pos, sh1, sh2, mask, tbl[16], tmp_tbl[16]. ---- */
+#define ORC_MTGP32_N 351
+typedef struct {
+    uint32_t pos, sh1, sh2, mask;
+    uint32_t tbl[16], tmp_tbl[16];
+} orc_mtgp32_params;
+typedef struct {
+    uint32_t x[ORC_MTGP32_N]; /* ring: x[(idx + k) % N] is the k-th oldest word */
+    int idx;
+    orc_mtgp32_params p;
+} orc_mtgp32;
+/* State from a 32-bit seed ([Saito.Matsumoto2012] init_state: hidden seed
+ * from tbl[4], tbl[8]; byte fill; Knuth's 1812433253 recursion). */
+void orc_mtgp32_init(orc_mtgp32* m, const orc_mtgp32_params* p, uint32_t seed);
+/* x_{k+N} = rec(x_k, x_{k+1}, x_{k+pos}); output = temper(x_{k+N}, x_{k+pos-1}). */
+uint32_t orc_mtgp32_generate(orc_mtgp32* m);
+
 /* ---- conversions (R7) ---- */
 float orc_to_f32(uint32_t w);
 double orc_mrg_to_f64(uint32_t z);
@@ -73,6 +93,7 @@ typedef struct {
     uint32_t s[6];        /* MRG32k3a state */
     uint32_t key[2];      /* Philox key (R6) */
     orc_tinymt32 tm;      /* TinyMT32 state and parameters */
+    orc_mtgp32 mt;        /* MTGP32 state and parameters */
     uint64_t g;           /* Philox stream index -> ctr[2..3] (R6) */
     uint64_t blk;         /* Philox next counter block -> ctr[0..1] (R6) */
     uint32_t buf[4];      /* Philox lanes not yet served (S L258-266) */
@@ -91,7 +112,12 @@ typedef struct {
  * mat1_1, ...} (nseed = 3 + 3*n_params); family stream g = first + i lies in
  * group g / group_size, which uses parameter set g / group_size (one set per
  * group, P L309-313), and is slice g % group_size of that group's sequence,
- * i.e. starts 2^64 * (g % group_size) draws after init(params, seed). */
+ * i.e. starts 2^64 * (g % group_size) draws after init(params, seed).
+ * MTGP32 (R18): seed = {seed_lo, seed_hi, n_params, then 36 words per
+ * parameter set (pos, sh1, sh2, mask, tbl[16], tmp_tbl[16])}; family stream
+ * g = first + i uses parameter set g (g < n_params; Parameterization, one
+ * set per state, P L74-76) seeded with (uint32)(s ^ s >> 32) + g + 1,
+ * s = seed_hi:seed_lo; the offset is reached by stepping (off < 2^64). */
 int orc_stream_open(orc_stream* st, int gen, const uint32_t* seed, int nseed,
                     uint64_t first, uint64_t i, int spacing,
                     uint64_t off_lo, uint64_t off_hi);

@@ -52,3 +52,18 @@ def curand_pin(tmp_path_factory):
     pin = CurandPin(exe)
     yield pin
     pin.close()
+
+
+@pytest.fixture(scope="session")
+def mtgp_pin(tmp_path_factory):
+    """cuRAND's MTGP32 (host-callable header code + the 11213 parameter sets)."""
+    gxx = shutil.which("g++")
+    inc = "/usr/local/cuda/include"
+    if not gxx or not os.path.exists(os.path.join(inc, "curand_mtgp32dc_p_11213.h")):
+        pytest.skip("g++ or the CUDA toolkit headers are not available for the MTGP32 pin")
+    exe = str(tmp_path_factory.mktemp("mtgp") / "mtgp_host_pin")
+    subprocess.check_call([gxx, "-w", "-O1", "-I", inc, "-o", exe,
+                           os.path.join(ROOT, "tests", "pins", "mtgp_host_pin.cpp")])
+    pin = CurandPin(exe)
+    yield pin
+    pin.close()

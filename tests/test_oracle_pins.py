@@ -580,3 +580,77 @@ def test_verify_disjoint_spec_examples(orc):
     assert orc.verify_disjoint(list(orc.generate(W.MRG32K3A, [12345], 8, 100000)))["disjoint"]
     lf = orc.generate(W.MRG32K3A, [12345], 2, 10000, spacing=W.SPACING_LEAPFROG, players=2)
     assert orc.verify_disjoint(list(lf))["disjoint"]
+
+
+# --------------------------------------------------------------------------- MTGP32 (NEXT-4c)
+# [Saito.Matsumoto2012] via P L74-76, L133-136; R18. Pinned to cuRAND's own
+# MTGP32 code compiled for the host (tests/pins/mtgp_host_pin.cpp) and, apart
+# from any implementation, to the generator's GF(2) linear complexity.
+
+def test_mtgp32_params_parse_matches_curand(mtgp_pin):
+    P = W.mtgp32_params()
+    assert len(P) == 200
+    for p in (0, 1, 57, 123, 199):
+        assert list(P[p]) == mtgp_pin.ask("params", p), p
+
+
+@pytest.mark.parametrize("seed", [0, 12345, (1 << 40) + 7])
+def test_mtgp32_matches_curand_host(orc, mtgp_pin, seed):
+    P = W.mtgp32_params()
+    n = 1500  # > 4 rings of N = 351 words
+    streams = [0, 1, 57, 199]
+    rows = orc.generate(W.MTGP32, W.mtgp32_seed_words(seed, P), 200, n, streams=streams)
+    for r, p in enumerate(streams):
+        assert rows[r].tolist() == mtgp_pin.ask("gen", p, seed, n), (seed, p)
+
+
+def test_mtgp32_offset_first_and_kinds(orc):
+    P = W.mtgp32_params(12)
+    sw = W.mtgp32_seed_words(99, P)
+    full = orc.generate(W.MTGP32, sw, 12, 900)
+    # first / streams select the parameter set of family stream g
+    assert (orc.generate(W.MTGP32, sw, 4, 900, first=8) == full[8:12]).all()
+    # an offset is the same row, later (stepping)
+    assert (orc.generate(W.MTGP32, sw, 12, 300, offset=600) == full[:, 600:]).all()
+    # f32 = (w>>8)*2^-24; f64 = 53 bits of (w1<<32 | w0) (R7)
+    f32 = orc.generate(W.MTGP32, sw, 12, 900, kind=orc.F32)
+    assert (f32 == (full >> 8).astype(np.float64) * 2.0 ** -24).all()
+    f64 = orc.generate(W.MTGP32, sw, 12, 450, kind=orc.F64)
+    w = full.astype(np.uint64)
+    assert (f64 == ((w[:, 1::2] << np.uint64(32) | w[:, 0::2]) >> np.uint64(11)).astype(np.float64) * 2.0 ** -53).all()
+    # a parameter set must exist for every family stream
+    with pytest.raises(ValueError):
+        orc.generate(W.MTGP32, sw, 13, 10)
+
+
+def _linear_complexity(bits):
+    """Berlekamp-Massey over GF(2) (bit lists as Python ints)."""
+    c, b = 1, 1
+    L, m = 0, 1
+    rev = 0  # bit j = s_{n-j}
+    for n, s in enumerate(bits):
+        rev = (rev << 1) | s
+        d = ((c & rev).bit_count()) & 1
+        if d == 0:
+            m += 1
+        elif 2 * L <= n:
+            t = c
+            c ^= b << m
+            L, b, m = n + 1 - L, t, 1
+        else:
+            c ^= b << m
+            m += 1
+    return L
+
+
+@pytest.mark.parametrize("bit", [0, 31])
+def test_mtgp32_linear_complexity_is_the_mersenne_exponent(orc, bit):
+    """MTGP32-11213 is F2-linear with a primitive characteristic polynomial of
+    degree 11213 (the Mersenne exponent): any output bit sequence has linear
+    complexity exactly 11213. A wrong shift, mask, index or table breaks it."""
+    P = W.mtgp32_params(3)
+    n = 2 * 11213 + 400
+    for p in (0, 2):
+        row = orc.generate(W.MTGP32, W.mtgp32_seed_words(7, P), 3, n, streams=[p])[0]
+        bits = [int(v >> bit) & 1 for v in row]
+        assert _linear_complexity(bits) == 11213, p

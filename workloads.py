@@ -14,6 +14,7 @@ MRG32K3A = 1
 PHILOX4X32_10 = 2
 TINYMT32 = 3
 THREEFRY4X64_20 = 4
+MTGP32 = 5
 SPACING_STREAM = 0
 SPACING_SUBSTREAM = 1
 SPACING_KEYED = 2
@@ -78,6 +79,41 @@ def tinymt32_test_params(k: int):
 def tinymt32_seed_words(seed: int, group_size: int, params):
     """The oracle's TinyMT32 seed vector: {seed, group_size, n_params, params...} (R15)."""
     return [seed, group_size, len(params)] + [w for rec in params for w in rec]
+
+
+MTGP32_PARAM_HEADER = "curand_mtgp32dc_p_11213.h"
+
+
+def mtgp32_params(k: int = 200):
+    """The first k MTGP32-11213 parameter sets (the MTGP authors' Dynamic
+    Creator output, 200 sets, as shipped in the CUDA toolkit's
+    curand_mtgp32dc_p_11213.h), each as 36 words: pos, sh1, sh2, mask,
+    tbl[16], tmp_tbl[16] (R18). Parsed from the header text; input data only."""
+    import os
+    import re
+    roots = [os.environ.get("CUDA_HOME", ""), "/usr/local/cuda"]
+    path = next((os.path.join(r, "include", MTGP32_PARAM_HEADER) for r in roots
+                 if r and os.path.exists(os.path.join(r, "include", MTGP32_PARAM_HEADER))), None)
+    if path is None:
+        raise FileNotFoundError(MTGP32_PARAM_HEADER + " not found under CUDA_HOME or /usr/local/cuda")
+    text = open(path).read()
+    body = text[text.index("mtgp32dc_params_fast_11213[]"):]
+    sets = []
+    for rec in re.finditer(r"/\* No\.(\d+)[^*]*\*/(.*?)(?=/\* No\.|\};\s*$|\}\s*;)", body, re.S):
+        nums = [int(v, 0) for v in re.findall(r"0x[0-9a-fA-F]+|\b\d+\b", rec.group(2))]
+        # mexp, pos, sh1, sh2, tbl[16], tmp_tbl[16], flt_tmp_tbl[16], mask, poly_sha1[21]
+        mexp, pos, sh1, sh2 = nums[:4]
+        tbl, tmp_tbl, mask = nums[4:20], nums[20:36], nums[52]
+        assert mexp == 11213, mexp
+        sets.append(tuple([pos, sh1, sh2, mask] + tbl + tmp_tbl))
+        if len(sets) == k:
+            break
+    return sets
+
+
+def mtgp32_seed_words(seed: int, params):
+    """The oracle's MTGP32 seed vector: {seed_lo, seed_hi, n_params, 36 words per set} (R18)."""
+    return [seed & 0xFFFFFFFF, seed >> 32, len(params)] + [w for rec in params for w in rec]
 
 
 def splitmix64(seed: int, count: int):
