@@ -410,6 +410,19 @@ def main():
         shv.shv_streams_destroy(h)
         del st_t
 
+        # MTGP32-11213 (NEXT-4c, R18): the 200 parameter sets of the toolkit's DC
+        # table, one CTA-cooperative state each, 2^32 / 200 u32 per stream
+        try:
+            mt_params = W.mtgp32_params()
+        except FileNotFoundError:
+            mt_params = None
+        if mt_params:
+            nmt = total_per_rank // len(mt_params)
+            h = shv.shv_streams_create_mtgp32(mt_params, 12345, 0, len(mt_params), None, 0, local, sp)
+            parts["mtgp32_fill_u32"] = {**fill_part(fill_ms(h, out, nmt), nmt * len(mt_params)),
+                                        "streams": len(mt_params), "numbers_per_stream": nmt}
+            shv.shv_streams_destroy(h)
+
         # Leap Frog (NEXT-4, R17) on the C5 shape: 2^20 players of one base
         # sequence x 4096 u32 per rank (rank r deals players [r*2^20, (r+1)*2^20)
         # of K = world*2^20)

@@ -65,6 +65,9 @@ typedef enum {
     SHV_GEN_MRG32K3A = 1,       /* [LEcuyer1999], P L82-86, L250-282 [§4.1] */
     SHV_GEN_PHILOX4X32_10 = 2,  /* [Salmon.etal.2011], P L88-90, L322-336 [§4.3]; variant per S L275 */
     SHV_GEN_TINYMT32 = 3,       /* [Saito2011], P L287-317 [§4.2]; shv_streams_create_tinymt32 */
+    SHV_GEN_MTGP32 = 5,         /* [Saito.Matsumoto2012], P L74-76 [§2.2], L133-136 [§2.3]:
+                                   MTGP32-11213, one Dynamic Creator parameter set per stream;
+                                   shv_streams_create_mtgp32 (R18) */
     SHV_GEN_THREEFRY4X64_20 = 4 /* [Salmon.etal.2011], P L322-336 [§4.3]; variant per S L275;
                                    key = (s0|s1<<32, s2|s3<<32, 0, 0) from 1..4 seed words,
                                    counter-stream g: ctr = (blk, g, 0, 0); draws are the (lo, hi)
@@ -104,7 +107,8 @@ typedef struct {
 
 /* Bytes of per-stream state a handle needs: MRG32k3a 24*n_streams (six u32
  * per stream, SoA: word k of stream i at [k*n_streams + i]; P L257-258
- * "only stores 6 integers"); Philox 0 (counter-based, no state). */
+ * "only stores 6 integers"); Philox 0 (counter-based, no state); TinyMT32 16;
+ * MTGP32 1408 (352 words per stream). */
 size_t shv_state_bytes(int gen, uint64_t n_streams);
 
 /* Short form (north star): first_stream 0, SHV_SPACING_STREAM, current
@@ -198,6 +202,29 @@ shv_status shv_streams_create_leapfrog(shv_streams* out, int gen, const uint32_t
 shv_status shv_generate_u32(shv_streams h, uint32_t* d_out, uint64_t n_per_stream, void* cuda_stream);
 shv_status shv_generate_f32(shv_streams h, float* d_out, uint64_t n_per_stream, void* cuda_stream);
 shv_status shv_generate_f64(shv_streams h, double* d_out, uint64_t n_per_stream, void* cuda_stream);
+
+/* MTGP32-11213 handle (NEXT-4c; Parameterization, P L74-76 [§2.2]: "MTGP
+ * ... comes with companion software for parallelization (MTGPDC)";
+ * P L133-136; R18). params: n_params records of 36 u32 words, the Dynamic
+ * Creator output for Mersenne exponent 11213 — pos, sh1, sh2, mask,
+ * tbl[16], tmp_tbl[16] (e.g. the 200 sets of the CUDA toolkit's
+ * curand_mtgp32dc_p_11213.h); host memory, copied. Family stream g =
+ * first_stream + i (i < n_streams) uses parameter set g, so
+ * first_stream + n_streams <= n_params (else SHV_ERR_INSUFFICIENT_STREAMS),
+ * and starts from the authors' init_state(params[g], (uint32)(s ^ s >> 32)
+ * + g + 1), s = seed (the convention of cuRAND's
+ * curandMakeMTGP32KernelState). The handle is stateful: 1408 bytes per stream
+ * (shv_state_bytes; d_state as in shv_streams_create_ex), rewritten by every
+ * generate / mc_pi call and by shv_jump (SHV_JUMP_DRAWS only; sequential
+ * advance enqueued on the create stream). f32/f64/Monte Carlo conversions
+ * as for Philox (R7, R9: f64 and each sample take two draws). No device view
+ * and no Leap Frog layout (SHV_ERR_UNSUPPORTED): MTGP32 is generated by the
+ * threads of a block together. Errors: NULL params ->
+ * SHV_ERR_MISSING_PARAMETERS; a record with pos outside [3, 349] or a shift
+ * above 31 -> SHV_ERR_INVALID_ARGUMENT. */
+shv_status shv_streams_create_mtgp32(shv_streams* out, const uint32_t* params, size_t n_params,
+                                     uint64_t seed, uint64_t first_stream, uint64_t n_streams,
+                                     void* d_state, size_t state_bytes, int device, void* cuda_stream);
 
 /* Same values as shv_generate_u32, written to a HOST buffer h_out (pinned
  * memory recommended). The library generates into device staging slices and

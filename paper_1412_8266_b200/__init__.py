@@ -30,6 +30,7 @@ SHV_GEN_MRG32K3A = 1
 SHV_GEN_PHILOX4X32_10 = 2
 SHV_GEN_TINYMT32 = 3
 SHV_GEN_THREEFRY4X64_20 = 4
+SHV_GEN_MTGP32 = 5
 SHV_SPACING_STREAM = 0
 SHV_SPACING_SUBSTREAM = 1
 SHV_SPACING_KEYED = 2
@@ -46,7 +47,7 @@ EXPORTS = (
     "shv_status_string", "shv_last_error_message", "shv_set_launch_config",
     "shv_partition", "shv_jump_matrix", "shv_build_info", "shv_get_device_view",
     "shv_streams_create_tinymt32", "shv_streams_create_leapfrog",
-    "shv_verify_disjoint_workspace_bytes", "shv_verify_disjoint",
+    "shv_verify_disjoint_workspace_bytes", "shv_verify_disjoint", "shv_streams_create_mtgp32",
 )
 
 #: Field order of shv_disjoint_report (seven u64 words, include/shv.h).
@@ -108,6 +109,8 @@ def _load():
         "shv_streams_create_leapfrog": (st, [C.POINTER(u64), C.c_int, u32p, C.c_size_t, u64, u64, u64,
                                              vp, C.c_size_t, C.c_int, vp]),
         "shv_verify_disjoint_workspace_bytes": (C.c_size_t, [u64, u64]),
+        "shv_streams_create_mtgp32": (st, [C.POINTER(u64), u32p, C.c_size_t, u64, u64, u64, vp, C.c_size_t,
+                                           C.c_int, vp]),
         "shv_verify_disjoint": (st, [vp, u64, u64, vp, C.c_size_t, vp, vp]),
     }
     for name, (res, args) in sig.items():
@@ -182,6 +185,21 @@ def shv_streams_create_tinymt32(params, seed: int, group_size: int, first_stream
     _check(lib.shv_streams_create_tinymt32(C.byref(h), arr if flat else None, len(flat) // 3, seed,
                                            group_size, first_stream, n_streams, _ptr(d_state),
                                            state_bytes, device, _stream(stream)))
+    return h.value
+
+
+def shv_streams_create_mtgp32(params, seed: int, first_stream: int, n_streams: int, d_state=None,
+                              state_bytes: int = 0, device: int = -1, stream=None) -> int:
+    """MTGP32-11213 handle (R18): ``params`` = parameter records of 36 words
+    (pos, sh1, sh2, mask, tbl[16], tmp_tbl[16]); family stream g uses record g."""
+    h = C.c_uint64(0)
+    words = [int(w) for rec in params for w in rec]
+    arr = (C.c_uint32 * max(len(words), 1))(*words)
+    if d_state is not None and not isinstance(d_state, int) and not state_bytes:
+        state_bytes = d_state.numel() * d_state.element_size()
+    _check(lib.shv_streams_create_mtgp32(C.byref(h), arr if words else None, len(words) // 36, seed,
+                                         first_stream, n_streams, _ptr(d_state), state_bytes, device,
+                                         _stream(stream)))
     return h.value
 
 

@@ -10,7 +10,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libshv.so")
 SOURCES = [os.path.join(CSRC, f) for f in ("kernels_mrg.cu", "kernels_philox.cu", "kernels_threefry.cu",
-                                            "kernels_tinymt32.cu", "kernels_leapfrog.cu", "kernels_audit.cu",
+                                            "kernels_tinymt32.cu", "kernels_leapfrog.cu", "kernels_audit.cu", "kernels_mtgp32.cu",
                                             "shv_api.cpp")]
 DEPS = SOURCES + [os.path.join(CSRC, "shv_internal.h"), os.path.join(CSRC, "kernels_common.cuh"), os.path.join(ROOT, "include", "shv_device.cuh"), os.path.join(ROOT, "include", "shv.h")]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

@@ -191,6 +191,24 @@ TinyMtLaunch tm_launch(const Handle& h, uint64_t s0, uint64_t ns)
     return P;
 }
 
+MtgpLaunch mtgp_launch(const Handle& h, uint64_t s0, uint64_t ns)
+{
+    MtgpLaunch P{};
+    P.state = h.state + kMtgpStateWords * s0;
+    P.params = h.params + kMtgpParamWords * s0;
+    P.ns = ns;
+    P.first = h.first + s0;
+    return P;
+}
+
+// One CTA per MTGP32 state (the generator's block-cooperative design); CTAs
+// loop over states when there are more than fit at once.
+unsigned mtgp_blocks(const Handle& h, uint64_t ns)
+{
+    const uint64_t cap = (uint64_t)(h.sms > 0 ? h.sms : 148) * 8;
+    return (unsigned)(ns < cap ? (ns ? ns : 1) : cap);
+}
+
 std::mutex g_mu;
 std::unordered_map<uint64_t, std::shared_ptr<Handle>> g_handles;
 std::atomic<uint64_t> g_next_id{1};
@@ -333,7 +351,7 @@ shv_status check_advance(const Handle& h, u128 draws)
         if (draws > ((u128)1 << 66) || h.offset > ((u128)1 << 66) - draws)
             return fail(SHV_ERR_INVALID_ARGUMENT, "Philox stream exhausted (2^66 draws per stream)");
     } else if (h.offset + draws < h.offset) {
-        return fail(SHV_ERR_INVALID_ARGUMENT, "MRG32k3a offset would exceed 2^128");
+        return fail(SHV_ERR_INVALID_ARGUMENT, "offset would exceed 2^128 draws");
     }
     return SHV_OK;
 }
@@ -568,6 +586,11 @@ shv_status generate(shv_streams hid, T* out, uint64_t n, void* stream, int kind,
                 g = Grid{blocks_for(h, kKThreefryFill, kind, false, P.items), h.tpb};
             }
             err = launch_threefry_fill(P, kind, fast, g, s);
+        } else if (h.gen == SHV_GEN_MTGP32) {
+            MtgpLaunch P = mtgp_launch(h, s0, ns);
+            P.out = dst;
+            P.n = n;
+            err = launch_mtgp(P, kind, mtgp_blocks(h, ns), s);
         } else if (h.gen == SHV_GEN_TINYMT32) {
             const bool vec = aligned32 && (n % 8 == 0) && n <= 0xFFFFFFFFull;
             TinyMtLaunch P = tm_launch(h, s0, ns);
@@ -691,6 +714,8 @@ shv_status validate_seed(int gen, const uint32_t* seed, size_t words, uint32_t o
     }
     if (gen == SHV_GEN_TINYMT32)
         return fail(SHV_ERR_MISSING_PARAMETERS, "TinyMT32 handles come from shv_streams_create_tinymt32");
+    if (gen == SHV_GEN_MTGP32)
+        return fail(SHV_ERR_MISSING_PARAMETERS, "MTGP32 handles come from shv_streams_create_mtgp32");
     return fail(SHV_ERR_INVALID_ARGUMENT, "unknown generator %d", gen);
 }
 
@@ -703,7 +728,8 @@ extern "C" {
 
 size_t shv_state_bytes(int gen, uint64_t n_streams)
 {
-    const uint64_t per = gen == SHV_GEN_MRG32K3A ? 24 : gen == SHV_GEN_TINYMT32 ? 16 : 0;
+    const uint64_t per = gen == SHV_GEN_MRG32K3A ? 24 : gen == SHV_GEN_TINYMT32 ? 16
+                       : gen == SHV_GEN_MTGP32 ? 4 * kMtgpStateWords : 0;
     if (!per || n_streams > SIZE_MAX / per) return 0;
     return (size_t)(per * n_streams);
 }
@@ -776,6 +802,74 @@ shv_status shv_streams_create_tinymt32(shv_streams* out, const uint32_t* params,
         if (h->own_state) cudaFree(h->state);
         cudaFree(h->params);
         return cuda_fail(e, "tinymt32 create");
+    }
+    const uint64_t id = g_next_id.fetch_add(1);
+    {
+        std::lock_guard<std::mutex> lk(g_mu);
+        g_handles[id] = h;
+    }
+    *out = id;
+    return SHV_OK;
+}
+
+shv_status shv_streams_create_mtgp32(shv_streams* out, const uint32_t* params, size_t n_params, uint64_t seed,
+                                     uint64_t first_stream, uint64_t n_streams, void* d_state, size_t state_bytes,
+                                     int device, void* cuda_stream)
+{
+    Range nvtx_range("shv_streams_create_mtgp32");
+    if (!out) return fail(SHV_ERR_INVALID_ARGUMENT, "NULL out handle");
+    *out = 0;
+    if (!params || n_params == 0)
+        return fail(SHV_ERR_MISSING_PARAMETERS, "MTGP32 needs Dynamic Creator parameter sets (P L74-76)");
+    if (n_streams == 0) return fail(SHV_ERR_INVALID_ARGUMENT, "n_streams must be >= 1");
+    if (first_stream >= n_params || n_streams > n_params - first_stream)
+        return fail(SHV_ERR_INSUFFICIENT_STREAMS, "streams [%llu, %llu) need as many parameter sets, %zu given",
+                    (unsigned long long)first_stream, (unsigned long long)(first_stream + n_streams), n_params);
+    for (uint64_t g = first_stream; g < first_stream + n_streams; ++g) {
+        const uint32_t* r = params + kMtgpParamWords * g;
+        if (r[0] < 3 || r[0] > kMtgpN - 2 || r[1] > 31 || r[2] > 31)
+            return fail(SHV_ERR_INVALID_ARGUMENT, "parameter set %llu: pos %u sh1 %u sh2 %u out of range",
+                        (unsigned long long)g, r[0], r[1], r[2]);
+    }
+    const size_t need = shv_state_bytes(SHV_GEN_MTGP32, n_streams);
+    if (need == 0) return fail(SHV_ERR_INVALID_ARGUMENT, "state size overflow");
+    if (d_state && state_bytes < need) return fail(SHV_ERR_INVALID_ARGUMENT, "state buffer %zu B < %zu B", state_bytes, need);
+    if (d_state && ((uintptr_t)d_state & 15)) return fail(SHV_ERR_MISALIGNED, "state not 16-byte aligned");
+    int dev = device;
+    if (dev < 0) {
+        cudaError_t e = cudaGetDevice(&dev);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+    }
+    DeviceGuard dg(dev);
+    if (dg.err != cudaSuccess) return cuda_fail(dg.err, "cudaSetDevice");
+    auto h = std::make_shared<Handle>();
+    h->gen = SHV_GEN_MTGP32;
+    h->spacing = SHV_SPACING_STREAM;
+    h->device = dev;
+    h->seed[0] = (uint32_t)seed;
+    h->seed[1] = (uint32_t)(seed >> 32);
+    h->first = first_stream;
+    h->n = n_streams;
+    h->home = (cudaStream_t)cuda_stream;
+    cudaStream_t s = (cudaStream_t)cuda_stream;
+    cudaError_t e = cudaDeviceGetAttribute(&h->sms, cudaDevAttrMultiProcessorCount, dev);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaDeviceGetAttribute");
+    const size_t pbytes = 4 * kMtgpParamWords * n_streams;
+    e = cudaMalloc((void**)&h->params, pbytes);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(params)");
+    e = cudaMemcpyAsync(h->params, params + kMtgpParamWords * first_stream, pbytes, cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess && d_state) {
+        h->state = (uint32_t*)d_state;
+    } else if (e == cudaSuccess) {
+        e = cudaMalloc((void**)&h->state, need);
+        h->own_state = e == cudaSuccess;
+    }
+    if (e == cudaSuccess) e = launch_mtgp_seed(mtgp_launch(*h, 0, n_streams), (uint32_t)(seed ^ (seed >> 32)), s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);  // the host params copy must complete
+    if (e != cudaSuccess) {
+        if (h->own_state) cudaFree(h->state);
+        cudaFree(h->params);
+        return cuda_fail(e, "mtgp32 create");
     }
     const uint64_t id = g_next_id.fetch_add(1);
     {
@@ -889,6 +983,7 @@ shv_status shv_streams_create_leapfrog(shv_streams* out, int gen, const uint32_t
     if (!out) return fail(SHV_ERR_INVALID_ARGUMENT, "NULL out handle");
     *out = 0;
     if (gen == SHV_GEN_TINYMT32) return fail(SHV_ERR_UNSUPPORTED, "TinyMT32 has no Leap Frog layout (R17)");
+    if (gen == SHV_GEN_MTGP32) return fail(SHV_ERR_UNSUPPORTED, "MTGP32 has no Leap Frog layout (R18)");
     uint32_t s6[6];
     shv_status st = validate_seed(gen, seed, seed_words, s6);
     if (st) return st;
@@ -961,6 +1056,21 @@ shv_status shv_jump(shv_streams hid, int kind, uint64_t n)
     if (!hp) return fail(SHV_ERR_LIFECYCLE, "unknown or destroyed handle");
     Handle& h = *hp;
     u128 d;
+    if (h.gen == SHV_GEN_MTGP32) {
+        // sequential advance on the device (no jump polynomial), on the create stream
+        if (kind != SHV_JUMP_DRAWS) return fail(SHV_ERR_UNSUPPORTED, "MTGP32 jumps by draws only");
+        if (n == 0) return SHV_OK;
+        shv_status st = check_advance(h, n);
+        if (st) return st;
+        DeviceGuard dg(h.device);
+        if (dg.err != cudaSuccess) return cuda_fail(dg.err, "cudaSetDevice");
+        MtgpLaunch P = mtgp_launch(h, 0, h.n);
+        P.n = n;
+        cudaError_t e = launch_mtgp(P, 4, mtgp_blocks(h, h.n), h.home);
+        if (e != cudaSuccess) return cuda_fail(e, "mtgp32 advance");
+        h.offset += n;
+        return SHV_OK;
+    }
     if (h.gen == SHV_GEN_TINYMT32) {
         // sequential advance on the device (S L355), on the create stream
         if (kind != SHV_JUMP_DRAWS) return fail(SHV_ERR_UNSUPPORTED, "TinyMT32 jumps by draws only");
@@ -1052,6 +1162,12 @@ shv_status shv_mc_pi_ex(shv_streams hid, uint64_t samples, uint64_t* d_hits, uin
         P.items = h.n * P.nseg;
         Grid g{blocks_for(h, kKThreefryMc, 0, fast, P.items), h.tpb};
         err = launch_threefry_mc(P, fast, g, s);
+    } else if (h.gen == SHV_GEN_MTGP32) {
+        MtgpLaunch P = mtgp_launch(h, 0, h.n);
+        P.n = samples;
+        P.hits = (unsigned long long*)d_hits;
+        P.counts = (unsigned long long*)d_counts;
+        err = launch_mtgp(P, 3, mtgp_blocks(h, h.n), s);
     } else if (h.gen == SHV_GEN_TINYMT32) {
         TinyMtLaunch P = tm_launch(h, 0, h.n);
         P.n = samples;
@@ -1128,6 +1244,8 @@ shv_status shv_get_device_view(shv_streams hid, shv_device_view* out)
     if (!out) return fail(SHV_ERR_INVALID_ARGUMENT, "NULL out");
     const Handle& h = *hp;
     if (h.spacing == SHV_SPACING_LEAPFROG) return fail(SHV_ERR_UNSUPPORTED, "no device view for Leap Frog handles");
+    if (h.gen == SHV_GEN_MTGP32)
+        return fail(SHV_ERR_UNSUPPORTED, "no per-thread device view for MTGP32 (block-cooperative generator)");
     memset(out, 0, sizeof *out);
     out->gen = (uint32_t)h.gen;
     out->spacing = (uint32_t)h.spacing;

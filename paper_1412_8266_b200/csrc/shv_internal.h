@@ -167,6 +167,25 @@ size_t mrg_fill_tma_smem(int threads);
 cudaError_t launch_mrg_mc(const MrgLaunch& p, Grid g, cudaStream_t s);
 cudaError_t launch_philox_fill(const PhiloxLaunch& p, int kind, bool fast, Grid g, cudaStream_t s);
 cudaError_t launch_philox_mc(const PhiloxLaunch& p, bool fast, Grid g, cudaStream_t s);
+// MTGP32-11213 launch (kernels_mtgp32.cu; R18): stream i of the launch has
+// its parameter set at params + 36*i (pos, sh1, sh2, mask, tbl[16],
+// tmp_tbl[16]) and its state at state + 352*i (the N = 351 current words,
+// oldest first, one pad word).
+constexpr uint32_t kMtgpN = 351, kMtgpStateWords = 352, kMtgpParamWords = 36;
+struct MtgpLaunch {
+    uint32_t* state;
+    const uint32_t* params;
+    uint64_t ns;
+    uint64_t first;            // family index of launch stream 0 (seeding)
+    void* out;                 // fill: row i at out + i*n elements
+    uint64_t n;                // values per row (fill), samples (MC), draws (skip)
+    unsigned long long* hits;
+    unsigned long long* counts;
+};
+cudaError_t launch_mtgp_seed(const MtgpLaunch& p, uint32_t seed_base, cudaStream_t s);
+// mode: 0 u32, 1 f32, 2 f64 fill; 3 Monte Carlo; 4 skip n draws
+cudaError_t launch_mtgp(const MtgpLaunch& p, int mode, unsigned blocks, cudaStream_t s);
+
 // Disjointness audit (kernels_audit.cu; S L407-415): rows = n_pe rows of
 // `horizon` u32, windows = n_pe * wpr (wpr = horizon - 3), table of cap slots
 // (slots, second: cap u64 each), report on the device.
