@@ -5,13 +5,14 @@
 //
 // Recursion over N = 351 words: x_{k+N} = rec(x_k, x_{k+1}, x_{k+pos}),
 // output_k = temper(x_{k+N}, x_{k+pos-1}). Elements k .. k+R-1 are independent
-// when R <= N - pos (every operand is older than the round), so a CTA of 256
-// threads computes R = min(256, N - pos) draws per round from a 1024-word
-// shared-memory ring, with ONE barrier per round: a round reads ring slots
-// [o, o+R+pos) and writes [o+N, o+N+R); the next round's writes
-// [o+R+N, o+2R+N) never alias this round's reads (the distance R+N+t-u lies in
-// (N-pos, 2R+N) and never reaches 1024). Draw o+t leaves as word t of the
-// round: 1 KB contiguous per round (u32/f32); f64 pairs draws (2j, 2j+1) of
+// when R <= N - pos (every operand is older than the round), so the threads of
+// a CTA compute R = (N - pos) & ~1 draws per round (128 threads, three
+// elements each) from a 1024-word shared-memory ring, with ONE barrier per
+// round: a round reads ring slots [o, o+R+pos) and writes [o+N, o+N+R), which
+// stay apart (R+pos <= N) and do not wrap onto the live words (N+R <= 699 <
+// 1024); the barrier orders one round's writes before the next round's reads.
+// Draw o+e leaves as word e of the round: R contiguous words per round
+// (u32/f32); f64 pairs draws (2j, 2j+1) of
 // adjacent lanes with a shuffle, as does the Monte Carlo hit test (R7, R9).
 // State in HBM: 352 words per stream (the N current words, oldest first, and
 // one pad word), read at the start of a call and written back at its end.
@@ -48,8 +49,20 @@ __global__ void __launch_bounds__(256) mtgp_seed_kernel(const __grid_constant__ 
     x[kN] = 0u;
 }
 
+// One round of up to R = (N - pos) & ~1 (<= 348) draws: thread t computes
+// elements t, t + 128, t + 256 (kEpt independent chains for latency hiding;
+// 4 warps, so the per-round barrier is cheap). Element e is draw d0 + e.
+#ifndef SHV_MT_THREADS
+#define SHV_MT_THREADS 128
+#endif
+#ifndef SHV_MT_EPT
+#define SHV_MT_EPT 3
+#endif
+constexpr unsigned kMtThreads = SHV_MT_THREADS, kEpt = SHV_MT_EPT;
+static_assert(kMtThreads % 32 == 0, "whole warps");
+
 template <int MODE>
-__global__ void __launch_bounds__(256) mtgp_kernel(const __grid_constant__ MtgpLaunch P)
+__global__ void __launch_bounds__(kMtThreads) mtgp_kernel(const __grid_constant__ MtgpLaunch P)
 {
     __shared__ uint32_t ring[kRing];
     __shared__ uint32_t tbl[16], ttbl[16], prm[4];
@@ -63,45 +76,63 @@ __global__ void __launch_bounds__(256) mtgp_kernel(const __grid_constant__ MtgpL
         else if (t < 20) tbl[t - 4] = pp[t];
         else if (t < 36) ttbl[t - 20] = pp[t];
         uint32_t* st = P.state + kMtgpStateWords * i;
-        for (uint32_t k = t; k < kN; k += blockDim.x) ring[k] = st[k];
+        for (uint32_t k = t; k < kN; k += kMtThreads) ring[k] = st[k];
         __syncthreads();
         const uint32_t pos = prm[0], sh1 = prm[1], sh2 = prm[2], mask = prm[3];
-        const uint32_t R = min((uint32_t)blockDim.x, (kN - pos) & ~1u);
+        const uint32_t R = min(kMtThreads * kEpt, (kN - pos) & ~1u);
         uint32_t o = 0;  // ring index of the oldest word
         uint32_t h = 0;
         for (uint64_t d0 = 0; d0 < D; d0 += R) {
             const uint32_t cnt = (uint32_t)min((uint64_t)R, D - d0);
-            uint32_t v = 0;
-            if (t < cnt) {
-                const uint32_t k = o + t;
-                const uint32_t x1 = ring[k & (kRing - 1)], x2 = ring[(k + 1) & (kRing - 1)];
-                uint32_t y = ring[(k + pos) & (kRing - 1)];
-                uint32_t tt = ring[(k + pos - 1) & (kRing - 1)];
-                uint32_t x = (x1 & mask) ^ x2;
-                x ^= x << sh1;
-                y = x ^ (y >> sh2);
-                const uint32_t r = y ^ tbl[y & 0x0f];
-                ring[(k + kN) & (kRing - 1)] = r;
-                tt ^= tt >> 16;
-                tt ^= tt >> 8;
-                v = r ^ ttbl[tt & 0x0f];
+            // all loads of the round first: the ring stores below cannot then
+            // order (alias) the next element's loads behind them
+            uint32_t x1[kEpt], x2[kEpt], y[kEpt], tt[kEpt], v[kEpt];
+#pragma unroll
+            for (unsigned q = 0; q < kEpt; ++q) {
+                const uint32_t k = o + t + q * kMtThreads;
+                x1[q] = ring[k & (kRing - 1)];
+                x2[q] = ring[(k + 1) & (kRing - 1)];
+                y[q] = ring[(k + pos) & (kRing - 1)];
+                tt[q] = ring[(k + pos - 1) & (kRing - 1)];
             }
-            if (MODE == kMtU32 || MODE == kMtF32) {
-                if (t < cnt) {
-                    if (MODE == kMtU32) reinterpret_cast<uint32_t*>(P.out)[i * P.n + d0 + t] = v;
-                    else reinterpret_cast<float*>(P.out)[i * P.n + d0 + t] = to_f32(v);
-                }
-            } else if (MODE == kMtF64 || MODE == kMtMc) {
-                const uint32_t hi = __shfl_down_sync(0xffffffffu, v, 1);
-                if (!(lane & 1) && t < cnt) {  // d0 and t even: draws (d0+t, d0+t+1) = value (d0+t)/2
-                    if (MODE == kMtF64) reinterpret_cast<double*>(P.out)[i * P.n + (d0 + t) / 2] = philox_f64(v, hi);
-                    else h += hit(v, hi);
+            uint32_t r[kEpt];
+#pragma unroll
+            for (unsigned q = 0; q < kEpt; ++q) {
+                uint32_t x = (x1[q] & mask) ^ x2[q];
+                x ^= x << sh1;
+                const uint32_t yy = x ^ (y[q] >> sh2);
+                r[q] = yy ^ tbl[yy & 0x0f];
+                uint32_t u = tt[q];
+                u ^= u >> 16;
+                u ^= u >> 8;
+                v[q] = r[q] ^ ttbl[u & 0x0f];
+            }
+#pragma unroll
+            for (unsigned q = 0; q < kEpt; ++q)
+                if (t + q * kMtThreads < cnt) ring[(o + t + q * kMtThreads + kN) & (kRing - 1)] = r[q];
+#pragma unroll
+            for (unsigned q = 0; q < kEpt; ++q) {
+                const uint32_t e = t + q * kMtThreads;
+                if (MODE == kMtU32 || MODE == kMtF32) {
+                    if (e < cnt) {
+                        if (MODE == kMtU32) reinterpret_cast<uint32_t*>(P.out)[i * P.n + d0 + e] = v[q];
+                        else reinterpret_cast<float*>(P.out)[i * P.n + d0 + e] = to_f32(v[q]);
+                    }
+                } else if (MODE == kMtF64 || MODE == kMtMc) {
+                    // d0, R and kMtThreads even: draws (d0+e, d0+e+1) of lanes e, e+1 = value (d0+e)/2
+                    const uint32_t hi = __shfl_down_sync(0xffffffffu, v[q], 1);
+                    if (!(lane & 1) && e < cnt) {
+                        if (MODE == kMtF64)
+                            reinterpret_cast<double*>(P.out)[i * P.n + (d0 + e) / 2] = philox_f64(v[q], hi);
+                        else
+                            h += hit(v[q], hi);
+                    }
                 }
             }
             o += cnt;
             __syncthreads();
         }
-        for (uint32_t k = t; k < kN; k += blockDim.x) st[k] = ring[(o + k) & (kRing - 1)];
+        for (uint32_t k = t; k < kN; k += kMtThreads) st[k] = ring[(o + k) & (kRing - 1)];
         if (MODE == kMtMc) {
             total += h;
             if (P.counts) {
@@ -130,11 +161,11 @@ cudaError_t launch_mtgp(const MtgpLaunch& p, int mode, unsigned blocks, cudaStre
 {
     if (p.ns == 0) return cudaSuccess;
     switch (mode) {
-    case kMtU32: mtgp_kernel<kMtU32><<<blocks, 256, 0, s>>>(p); break;
-    case kMtF32: mtgp_kernel<kMtF32><<<blocks, 256, 0, s>>>(p); break;
-    case kMtF64: mtgp_kernel<kMtF64><<<blocks, 256, 0, s>>>(p); break;
-    case kMtMc: mtgp_kernel<kMtMc><<<blocks, 256, 0, s>>>(p); break;
-    default: mtgp_kernel<kMtSkip><<<blocks, 256, 0, s>>>(p); break;
+    case kMtU32: mtgp_kernel<kMtU32><<<blocks, kMtThreads, 0, s>>>(p); break;
+    case kMtF32: mtgp_kernel<kMtF32><<<blocks, kMtThreads, 0, s>>>(p); break;
+    case kMtF64: mtgp_kernel<kMtF64><<<blocks, kMtThreads, 0, s>>>(p); break;
+    case kMtMc: mtgp_kernel<kMtMc><<<blocks, kMtThreads, 0, s>>>(p); break;
+    default: mtgp_kernel<kMtSkip><<<blocks, kMtThreads, 0, s>>>(p); break;
     }
     return cudaGetLastError();
 }

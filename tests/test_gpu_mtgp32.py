@@ -81,7 +81,8 @@ def test_jump_and_offsets(shv, orc, params):
     shv.shv_jump(mt.h, shv.SHV_JUMP_DRAWS, 5001)
     mt.offset += 5001
     torch.cuda.synchronize()
-    assert (mt.gen(2048) == mt.ref(orc, 2048)).all()
+    want = mt.ref(orc, 2048)
+    assert (mt.gen(2048) == want).all()
     assert shv.shv_get_position(mt.h)["offset"] == 77 + 5001 + 2048
     with pytest.raises(shv.ShvError) as e:
         shv.shv_jump(mt.h, shv.SHV_JUMP_SUBSTREAMS, 1)
@@ -94,9 +95,9 @@ def test_more_states_than_resident_ctas(shv, orc, params):
     streams) > 148 x 8 resident CTAs: CTAs loop over states."""
     P = [params[g % 200] for g in range(2000)]
     mt = Mt(shv, P, 99, 0, 2000)
-    got = mt.gen(600)
     idx = W.sample_streams(2000, 64)
     want = mt.ref(orc, 600, streams=idx)
+    got = mt.gen(600)
     assert (got[idx] == want).all()
     mt.close()
 
@@ -116,7 +117,8 @@ def test_long_rows_sampled(shv, orc, params):
     rows = [0, 99, 199]
     assert (got[rows] == mt.ref(orc, m, streams=rows, offset=0)).all()
     # the state after the call continues exactly
-    assert (mt.gen(1000)[rows] == mt.ref(orc, 1000, streams=rows)).all()
+    want = mt.ref(orc, 1000, streams=rows)
+    assert (mt.gen(1000)[rows] == want).all()
     mt.close()
 
 
@@ -132,7 +134,8 @@ def test_mc_counts(shv, orc, params):
     assert int(hits.item()) == tot
     assert (counts.cpu().numpy() == np.asarray(want)).all()
     mt.offset = 11 + 2 * samples
-    assert (mt.gen(100) == mt.ref(orc, 100)).all()
+    want = mt.ref(orc, 100)
+    assert (mt.gen(100) == want).all()
     mt.close()
 
 
