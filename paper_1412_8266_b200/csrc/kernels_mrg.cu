@@ -36,9 +36,28 @@ __device__ MatPair g_jump_tab[3][64];
 
 namespace {
 
+// The six FP64 step constants (MrgFpK order) reach the DFMAs either from the
+// launch parameters or from constant memory (bit i of MASK: c_mrg_fpk[i]).
+// The mix decides which ptxas turns into uniform-register operands and which
+// it keeps in registers; a DFMA reading three register pairs issues at 2/3
+// rate (tools/lab/fp64_lab.cu: 82.6 vs 122 per SM per ns). Masks measured on
+// B200 (tools/lab, all 64 compiled, the candidates timed): the TMA fill is
+// fastest with 5 (3.49 ms vs 3.58 with no three-pair DFMA at all), the Monte
+// Carlo kernel with 22 (no three-pair DFMA; 3 % faster than 0).
+#ifndef SHV_MRG_FILL_CKMASK
+#define SHV_MRG_FILL_CKMASK 5
+#endif
+#ifndef SHV_MRG_MC_CKMASK
+#define SHV_MRG_MC_CKMASK 22
+#endif
+__constant__ double c_mrg_fpk[6] = {6755399441055744.0, 1.0 / 4294967087.0, 0x1.000059451f212p-32,
+                                    4294967087.0, 4294944443.0, 5886603609186927.0};
+template <int MASK>
 __device__ __forceinline__ MrgFpK load_fpk(const MrgLaunch& P)
 {
-    return MrgFpK{P.fpk[0], P.fpk[1], P.fpk[2], P.fpk[3], P.fpk[4], P.fpk[5]};
+#define SHV_CKF(i) (((MASK >> (i)) & 1) ? c_mrg_fpk[i] : P.fpk[i])
+    return MrgFpK{SHV_CKF(0), SHV_CKF(1), SHV_CKF(2), SHV_CKF(3), SHV_CKF(4), SHV_CKF(5)};
+#undef SHV_CKF
 }
 
 #if SHV_MRG_STEP == 9
@@ -166,8 +185,8 @@ template <int KIND, bool SEG_FASTEST>
 __global__ void __launch_bounds__(256, SHV_MRG_MINB) mrg_fill_vec_kernel(const __grid_constant__ MrgLaunch P)
 {
     using T = OutT<KIND>;
-    const MrgFpK K = load_fpk(P);
-    const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const MrgFpK K = load_fpk<SHV_MRG_MC_CKMASK>(P);
+    const unsigned lane = threadIdx.x & 31, warp = __shfl_sync(0xffffffffu, threadIdx.x >> 5, 0);  // warp-uniform loop (see the TMA fill)
     if constexpr (mrg_staged<KIND>()) {
     extern __shared__ uint4 smem[];
     uint4* wb = smem + warp * (32 * kPieces);
@@ -245,8 +264,11 @@ __global__ void __launch_bounds__(256, SHV_MRG_MINB)
     using T = OutT<KIND>;
     constexpr uint32_t W = 128 / sizeof(T);  // values per row per box
     extern __shared__ uint8_t tma_smem[];
-    const MrgFpK K = load_fpk(P);
-    const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const MrgFpK K = load_fpk<SHV_MRG_FILL_CKMASK>(P);
+    // warp index through a shuffle from lane 0: ptxas then sees the tile loop as
+    // warp-uniform and keeps loop-invariant FP64 constants in uniform registers
+    // (DFMA operands at full rate); 3.73 -> 3.50 ms for the C5 MRG fill (tools/lab)
+    const unsigned lane = threadIdx.x & 31, warp = __shfl_sync(0xffffffffu, threadIdx.x >> 5, 0);
     // 1024-byte aligned boxes (128-B swizzle); the launch adds 1 KB of slack
     const uint32_t base = ((uint32_t)__cvta_generic_to_shared(tma_smem) + 1023u) & ~1023u;
     const uint32_t box = base + warp * 4096u;
@@ -314,7 +336,7 @@ template <int KIND>
 __global__ void __launch_bounds__(256) mrg_fill_scalar_kernel(const __grid_constant__ MrgLaunch P)
 {
     using T = OutT<KIND>;
-    const MrgFpK K = load_fpk(P);
+    const MrgFpK K = load_fpk<SHV_MRG_MC_CKMASK>(P);
     const uint64_t nthr = (uint64_t)gridDim.x * blockDim.x;
     for (uint64_t it = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; it < P.items; it += nthr) {
         uint64_t i, j;
@@ -334,7 +356,7 @@ __global__ void __launch_bounds__(256) mrg_fill_scalar_kernel(const __grid_const
 
 __global__ void __launch_bounds__(256) mrg_mc_kernel(const __grid_constant__ MrgLaunch P)
 {
-    const MrgFpK K = load_fpk(P);
+    const MrgFpK K = load_fpk<SHV_MRG_MC_CKMASK>(P);
     const uint64_t nthr = (uint64_t)gridDim.x * blockDim.x;
     uint64_t total = 0;
     for (uint64_t it = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; it < P.items; it += nthr) {
