@@ -357,31 +357,38 @@ __global__ void __launch_bounds__(256) mrg_fill_scalar_kernel(const __grid_const
 __global__ void __launch_bounds__(256) mrg_mc_kernel(const __grid_constant__ MrgLaunch P)
 {
     const MrgFpK K = load_fpk<SHV_MRG_MC_CKMASK>(P);
-    const uint64_t nthr = (uint64_t)gridDim.x * blockDim.x;
+    // Warp-uniform loops (warp index via shuffle, trip counts via warp max) so
+    // ptxas keeps the FP64 constants in uniform registers, as in the fills.
+    // Lanes past their segment's end keep stepping but count no hits.
+    const unsigned lane = threadIdx.x & 31;
+    const uint64_t wstride = (uint64_t)gridDim.x * (blockDim.x >> 5) * 32;
     uint64_t total = 0;
-    for (uint64_t it = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; it < P.items; it += nthr) {
+    for (uint64_t base = ((uint64_t)blockIdx.x * (blockDim.x >> 5) + __shfl_sync(0xffffffffu, threadIdx.x >> 5, 0)) * 32;
+         base < P.items; base += wstride) {
+        const uint64_t it = base + lane;
         uint64_t i, j;
-        item_ij<false>(P, it, i, j);
+        item_ij<false>(P, it < P.items ? it : P.items - 1, i, j);
         Gen s = item_state(P, i, j);
         const uint64_t c0 = j * P.seg_len;
-        const uint32_t len = (uint32_t)min(P.seg_len, P.n - c0);
+        const uint32_t len = it < P.items ? (uint32_t)min(P.seg_len, P.n - c0) : 0u;
+        const uint32_t wlen = __reduce_max_sync(0xffffffffu, len);
         uint32_t h = 0;
         uint32_t k = 0;
-        for (; k + 12 <= len; k += 12) {
+        for (; k + 12 <= wlen; k += 12) {
 #pragma unroll
             for (int u = 0; u < 12; ++u) {
                 const uint32_t w0 = mrg_next(s, K);
                 const uint32_t w1 = mrg_next(s, K);
-                h += hit(w0, w1);
+                h += hit(w0, w1) & (k + u < len ? 1u : 0u);
             }
         }
-        for (; k < len; ++k) {
+        for (; k < wlen; ++k) {
             const uint32_t w0 = mrg_next(s, K);
             const uint32_t w1 = mrg_next(s, K);
-            h += hit(w0, w1);
+            h += hit(w0, w1) & (k < len ? 1u : 0u);
         }
         total += h;
-        if (P.counts) atomicAdd(P.counts + i, (unsigned long long)h);
+        if (P.counts && it < P.items) atomicAdd(P.counts + i, (unsigned long long)h);
     }
     block_reduce_add(total, P.hits);
 }

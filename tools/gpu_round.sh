@@ -12,6 +12,9 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:"mrg
   -o gpurun_out/prof_fill_$TAG python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu --no-parts > gpurun_out/ncu_full_$TAG.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"mrg_mc|philox_mc" -s 2 -c 2 \
   -o gpurun_out/prof_mc_$TAG python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu > gpurun_out/ncu_mc_$TAG.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"mtgp_kernel|audit_insert|audit_second" -c 3 \
+  -o gpurun_out/prof_next_$TAG python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu > gpurun_out/ncu_next_$TAG.log 2>&1
+ncu -i gpurun_out/prof_next_$TAG.ncu-rep --page details --csv > gpurun_out/ncu_full_next_details_$TAG.csv 2>/dev/null
 ls gpurun_out
 python tools/ncu_summary.py gpurun_out/ncu_traffic_$TAG.json mrg=gpurun_out/prof_fill_$TAG.ncu-rep:mrg_fill \
   philox=gpurun_out/prof_fill_$TAG.ncu-rep:philox_fill mc_mrg=gpurun_out/prof_mc_$TAG.ncu-rep:mrg_mc \
