@@ -4,7 +4,9 @@
 // Philox4x32-10 and Threefry4x64-20 handles.
 //
 // Player p's draw t is base draw p + K*t. Counter-based generators compute it
-// directly (one block per draw; a cached block serves K < words-per-block).
+// directly (one block per draw; a cached block serves K < words-per-block);
+// Philox with K % 4 == 0 evaluates each block once for the four players that
+// share it (leap_fill_grouped_kernel).
 // MRG32k3a cannot skip K-1 draws for free, so each component of the player's
 // subsequence is stepped by the order-3 linear recurrence that the
 // characteristic polynomial of B = A^K gives (Cayley-Hamilton: B^3 = tr(B) B^2
@@ -213,9 +215,144 @@ __global__ void __launch_bounds__(256) leap_mc_kernel(const __grid_constant__ Le
     block_reduce_add(total, P.hits);
 }
 
+// Grouped Philox players (K % 4 == 0): players 4G .. 4G+3 read the four words
+// of ONE counter block for every draw t (base draw p + K t lies in block
+// G + (K/4) t, word p & 3), so a work item (group G, segment j) evaluates each
+// block once and serves up to four rows from it — a quarter of the per-value
+// block evaluations of the per-player cursor. Rows outside the launch are not
+// written (partial groups at the launch edges).
+struct LeapGroup {
+    uint64_t b, step;      // next block, blocks per player draw (K/4)
+    int64_t row0;          // launch row of player 4G (may be < 0)
+    __device__ __forceinline__ void init(const LeapLaunch& P, uint64_t g, uint64_t j)
+    {
+        const uint64_t G = P.g0 + g;
+        const u128 o = ((u128)P.o_hi << 64) | P.o_lo;
+        step = P.players >> 2;
+        b = (uint64_t)((u128)G + (u128)step * (o + (u128)j * P.seg_draws));
+        row0 = (int64_t)(4 * G) - (int64_t)P.first;
+    }
+    __device__ __forceinline__ W4 next(const LeapLaunch& P)
+    {
+        const W4 v = philox_blk(b, 0, (uint32_t)P.k0, (uint32_t)P.k1);
+        b += step;
+        return v;
+    }
+    __device__ __forceinline__ bool live(const LeapLaunch& P, int l) const
+    {
+        return row0 + l >= 0 && row0 + l < (int64_t)P.ns;
+    }
+};
+
+__device__ __forceinline__ uint32_t lane_of(const W4& v, int l)
+{
+    return l == 0 ? v.x : l == 1 ? v.y : l == 2 ? v.z : v.w;
+}
+
+template <int KIND, bool VEC>
+__global__ void __launch_bounds__(256) leap_fill_grouped_kernel(const __grid_constant__ LeapLaunch P)
+{
+    using T = OutT<KIND>;
+    const uint64_t nthr = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t it = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; it < P.items; it += nthr) {
+        const uint64_t j = it / P.ngroups;
+        const uint64_t g = it - j * P.ngroups;
+        const uint64_t c0 = j * P.seg_len;
+        const uint64_t len = min(P.seg_len, P.n - c0);
+        LeapGroup cur;
+        cur.init(P, g, j);
+        T* base = reinterpret_cast<T*>(P.out) + c0;
+        if (VEC && KIND != kF64) {
+            for (uint64_t t = 0; t < len; t += 8) {
+                W4 v[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) v[u] = cur.next(P);
+#pragma unroll
+                for (int l = 0; l < 4; ++l) {
+                    if (!cur.live(P, l)) continue;
+                    uint32_t w[8];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) {
+                        const uint32_t x = lane_of(v[u], l);
+                        w[u] = KIND == kF32 ? __float_as_uint(to_f32(x)) : x;
+                    }
+                    st_v8(base + (uint64_t)(cur.row0 + l) * P.n + t, w[0], w[1], w[2], w[3], w[4], w[5], w[6], w[7]);
+                }
+            }
+        } else if (VEC) {  // f64: two player draws per value, four values per 32-byte store
+            for (uint64_t t = 0; t < len; t += 4) {
+                W4 v[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) v[u] = cur.next(P);
+#pragma unroll
+                for (int l = 0; l < 4; ++l) {
+                    if (!cur.live(P, l)) continue;
+                    st_v4d(base + (uint64_t)(cur.row0 + l) * P.n + t,
+                           philox_f64(lane_of(v[0], l), lane_of(v[1], l)), philox_f64(lane_of(v[2], l), lane_of(v[3], l)),
+                           philox_f64(lane_of(v[4], l), lane_of(v[5], l)), philox_f64(lane_of(v[6], l), lane_of(v[7], l)));
+                }
+            }
+        } else {
+            for (uint64_t t = 0; t < len; ++t) {
+                const W4 a = cur.next(P);
+                W4 b2{};
+                if (KIND == kF64) b2 = cur.next(P);
+#pragma unroll
+                for (int l = 0; l < 4; ++l) {
+                    if (!cur.live(P, l)) continue;
+                    T* o = base + (uint64_t)(cur.row0 + l) * P.n + t;
+                    if (KIND == kU32) *o = (T)lane_of(a, l);
+                    else if (KIND == kF32) *o = (T)to_f32(lane_of(a, l));
+                    else *o = (T)philox_f64(lane_of(a, l), lane_of(b2, l));
+                }
+            }
+        }
+    }
+}
+
+__global__ void __launch_bounds__(256) leap_mc_grouped_kernel(const __grid_constant__ LeapLaunch P)
+{
+    const uint64_t nthr = (uint64_t)gridDim.x * blockDim.x;
+    uint64_t total = 0;
+    for (uint64_t it = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; it < P.items; it += nthr) {
+        const uint64_t j = it / P.ngroups;
+        const uint64_t g = it - j * P.ngroups;
+        const uint32_t len = (uint32_t)min(P.seg_len, P.n - j * P.seg_len);
+        LeapGroup cur;
+        cur.init(P, g, j);
+        uint32_t h[4] = {0, 0, 0, 0};
+        for (uint32_t k = 0; k < len; ++k) {
+            const W4 a = cur.next(P), b = cur.next(P);
+            h[0] += hit_fp64(a.x, b.x);
+            h[1] += hit_fp64(a.y, b.y);
+            h[2] += hit_fp64(a.z, b.z);
+            h[3] += hit_fp64(a.w, b.w);
+        }
+#pragma unroll
+        for (int l = 0; l < 4; ++l) {
+            if (!cur.live(P, l)) continue;
+            total += h[l];
+            if (P.counts) atomicAdd(P.counts + cur.row0 + l, (unsigned long long)h[l]);
+        }
+    }
+    block_reduce_add(total, P.hits);
+}
+
 template <int G>
 cudaError_t fill_g(const LeapLaunch& p, int kind, bool vec, Grid g, cudaStream_t s)
 {
+    if (G == kLeapPhilox && p.ngroups) {
+        if (vec) {
+            if (kind == kU32) leap_fill_grouped_kernel<kU32, true><<<g.blocks, g.threads, 0, s>>>(p);
+            else if (kind == kF32) leap_fill_grouped_kernel<kF32, true><<<g.blocks, g.threads, 0, s>>>(p);
+            else leap_fill_grouped_kernel<kF64, true><<<g.blocks, g.threads, 0, s>>>(p);
+        } else {
+            if (kind == kU32) leap_fill_grouped_kernel<kU32, false><<<g.blocks, g.threads, 0, s>>>(p);
+            else if (kind == kF32) leap_fill_grouped_kernel<kF32, false><<<g.blocks, g.threads, 0, s>>>(p);
+            else leap_fill_grouped_kernel<kF64, false><<<g.blocks, g.threads, 0, s>>>(p);
+        }
+        return cudaGetLastError();
+    }
     if (vec) {
         if (kind == kU32) leap_fill_kernel<G, kU32, true><<<g.blocks, g.threads, 0, s>>>(p);
         else if (kind == kF32) leap_fill_kernel<G, kF32, true><<<g.blocks, g.threads, 0, s>>>(p);
@@ -250,7 +387,8 @@ cudaError_t launch_leap_fill(const LeapLaunch& p, int lgen, int kind, bool vec, 
 
 cudaError_t launch_leap_mc(const LeapLaunch& p, int lgen, Grid g, cudaStream_t s)
 {
-    if (lgen == kLeapMrg) leap_mc_kernel<kLeapMrg><<<g.blocks, g.threads, 0, s>>>(p);
+    if (lgen == kLeapPhilox && p.ngroups) leap_mc_grouped_kernel<<<g.blocks, g.threads, 0, s>>>(p);
+    else if (lgen == kLeapMrg) leap_mc_kernel<kLeapMrg><<<g.blocks, g.threads, 0, s>>>(p);
     else if (lgen == kLeapPhilox) leap_mc_kernel<kLeapPhilox><<<g.blocks, g.threads, 0, s>>>(p);
     else leap_mc_kernel<kLeapThreefry><<<g.blocks, g.threads, 0, s>>>(p);
     return cudaGetLastError();

@@ -457,16 +457,23 @@ int leap_gen(int gen) { return gen == SHV_GEN_MRG32K3A ? kLeapMrg : gen == SHV_G
 // A Leap Frog launch over handle rows [s0, s0+ns): len units per row (values
 // or samples), dpv player draws per unit. Segments of >= 64 units (a MRG
 // segment start costs up to 35 mat-vecs), enough work items for 8 waves.
+// Philox Leap Frog players share counter blocks four at a time when K % 4 == 0
+// (grouped kernels, kernels_leapfrog.cu).
+bool leap_grouped(const Handle& h) { return h.gen == SHV_GEN_PHILOX4X32_10 && h.players % 4 == 0; }
+
 std::unique_ptr<LeapLaunch> leap_launch(const Handle& h, uint64_t s0, uint64_t ns, uint64_t len, uint64_t dpv,
                                         uint64_t align, uint64_t resident)
 {
     auto P = std::make_unique<LeapLaunch>();
+    const bool grouped = leap_grouped(h);
+    const uint64_t first = h.first + s0;
+    const uint64_t nrow_items = grouped ? ((first + ns - 1) >> 2) - (first >> 2) + 1 : ns;
     uint64_t L;
     if (h.seg) {
         L = h.seg;
     } else {
         const uint64_t target = 8 * resident;
-        const uint64_t S = (target + ns - 1) / ns;
+        const uint64_t S = (target + nrow_items - 1) / nrow_items;
         L = (len + S - 1) / S;
         if (L < 64) L = 64;
     }
@@ -481,7 +488,11 @@ std::unique_ptr<LeapLaunch> leap_launch(const Handle& h, uint64_t s0, uint64_t n
     P->seg_len = L;
     P->seg_draws = L * dpv;
     P->n = len;
-    P->items = ns * nseg;
+    P->items = nrow_items * nseg;
+    if (grouped) {
+        P->g0 = first >> 2;
+        P->ngroups = nrow_items;
+    }
     if (h.gen == SHV_GEN_PHILOX4X32_10) {
         P->k0 = h.seed[0];
         P->k1 = h.seed[1];

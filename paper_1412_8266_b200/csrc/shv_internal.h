@@ -126,6 +126,9 @@ struct LeapLaunch {
     unsigned long long* hits;    // MC only
     unsigned long long* counts;  // MC only, optional (indexed by launch row)
     uint64_t k0, k1;             // Philox: key (k0, k1) (32-bit); Threefry: key lanes 0, 1
+    // Philox grouped mode (K % 4 == 0; ngroups != 0): work item = (group g0+g,
+    // segment j), g fastest; group G holds players 4G .. 4G+3.
+    uint64_t g0, ngroups;
     // MRG32k3a: state[k*stride + stream_begin + i] = word k of A^p * seed.
     const uint32_t* state;
     uint64_t stride;
