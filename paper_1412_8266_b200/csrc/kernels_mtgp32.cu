@@ -85,11 +85,13 @@ __global__ void __launch_bounds__(kMtThreads) mtgp_kernel(const __grid_constant_
         for (uint64_t d0 = 0; d0 < D; d0 += R) {
             const uint32_t cnt = (uint32_t)min((uint64_t)R, D - d0);
             // all loads of the round first: the ring stores below cannot then
-            // order (alias) the next element's loads behind them
+            // order (alias) the next element's loads behind them. Elements past
+            // the round (e >= cnt) load the last live element's operands
+            // instead: slots past o + R + pos may be this round's stores.
             uint32_t x1[kEpt], x2[kEpt], y[kEpt], tt[kEpt], v[kEpt];
 #pragma unroll
             for (unsigned q = 0; q < kEpt; ++q) {
-                const uint32_t k = o + t + q * kMtThreads;
+                const uint32_t k = o + min(t + q * kMtThreads, cnt - 1);
                 x1[q] = ring[k & (kRing - 1)];
                 x2[q] = ring[(k + 1) & (kRing - 1)];
                 y[q] = ring[(k + pos) & (kRing - 1)];

@@ -1,6 +1,7 @@
 """Small-shape driver for compute-sanitizer: exercises every
 kernel of libshv once (vector and scalar fill paths, all output kinds, fused
-MC, seeding, TinyMT32 preparation) so memcheck / racecheck / synccheck /
+MC, seeding, TinyMT32 preparation, Leap Frog, MTGP32, the disjointness
+audit) so memcheck / racecheck / synccheck /
 initcheck see each of them.   compute-sanitizer --tool memcheck python tools/sanitize_driver.py"""
 import os
 import sys
@@ -45,6 +46,41 @@ def run():
     shv.shv_mc_pi(h, 100, hits, None)
     torch.cuda.synchronize()
     shv.shv_streams_destroy(h)
+    # Leap Frog players (MRG recurrence, Philox per-player and grouped, Threefry)
+    for gen, seed, K in ((W.MRG32K3A, [12345], 77), (W.PHILOX4X32_10, [5], 77), (W.PHILOX4X32_10, [5], 76),
+                         (W.THREEFRY4X64_20, [1, 2], 77)):
+        st = torch.empty(6 * 70, dtype=torch.int32, device="cuda") if gen == W.MRG32K3A else None
+        h = shv.shv_streams_create_leapfrog(gen, seed, K, 5, 70, st, 0, dev, None)
+        for n in (64, 13):
+            for dt, fn in ((torch.int32, shv.shv_generate_u32), (torch.float64, shv.shv_generate_f64)):
+                out = torch.empty(70 * n, dtype=dt, device="cuda")
+                fn(h, out, n, None)
+        hits = torch.zeros(1, dtype=torch.int64, device="cuda")
+        cnt = torch.zeros(70, dtype=torch.int64, device="cuda")
+        shv.shv_mc_pi_ex(h, 101, hits, cnt, None)
+        torch.cuda.synchronize()
+        shv.shv_streams_destroy(h)
+    # MTGP32-11213 (block-cooperative ring kernel)
+    mp = W.mtgp32_params(12)
+    h = shv.shv_streams_create_mtgp32(mp, 3, 2, 10, None, 0, dev, None)
+    for n in (700, 13):
+        for dt, fn in ((torch.int32, shv.shv_generate_u32), (torch.float32, shv.shv_generate_f32),
+                       (torch.float64, shv.shv_generate_f64)):
+            out = torch.empty(10 * n, dtype=dt, device="cuda")
+            fn(h, out, n, None)
+    shv.shv_jump(h, shv.SHV_JUMP_DRAWS, 1001)
+    hits = torch.zeros(1, dtype=torch.int64, device="cuda")
+    cnt = torch.zeros(10, dtype=torch.int64, device="cuda")
+    shv.shv_mc_pi_ex(h, 333, hits, cnt, None)
+    torch.cuda.synchronize()
+    shv.shv_streams_destroy(h)
+    # disjointness audit (hash table in the workspace)
+    rows = torch.randint(0, 3, (8 * 300,), dtype=torch.int32, device="cuda")
+    wsb = shv.shv_verify_disjoint_workspace_bytes(8, 300)
+    ws = torch.empty(wsb // 8, dtype=torch.int64, device="cuda")
+    rep = torch.zeros(7, dtype=torch.int64, device="cuda")
+    shv.shv_verify_disjoint(rows, 8, 300, ws, wsb, rep, None)
+    torch.cuda.synchronize()
     print("sanitize driver done")
 
 
