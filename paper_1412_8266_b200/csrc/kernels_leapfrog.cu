@@ -310,6 +310,97 @@ __global__ void __launch_bounds__(256) leap_fill_grouped_kernel(const __grid_con
     }
 }
 
+// Grouped Philox fill with TMA stores (u32/f32; n % 32 == 0). A warp owns a
+// tile of 32 consecutive groups = 128 rows x one segment. Each round a lane
+// evaluates 32 blocks for its group — 32 values for each of its four rows —
+// into the warp's 16-KB shared-memory box (128 rows x 128 B, 128-B swizzle:
+// chunk c of box row r at c ^ (r & 7)); at store step s lane L writes row
+// 4L + ((s + L) & 3), so the eight chunk slots of a 512-B wavefront group are
+// all distinct. One lane then hands the box to the TMA engine. Rows past the
+// launch (the last partial group, tiles past the last group) lie outside the
+// tensor map and are clipped by it; a first group that starts before the
+// launch (first player not 4-aligned) has the warp store its rows itself.
+constexpr unsigned kLeapTmaWarps = 4;
+template <int KIND>
+__global__ void __launch_bounds__(kLeapTmaWarps * 32)
+    leap_fill_tma_kernel(const __grid_constant__ LeapLaunch P, const __grid_constant__ CUtensorMap tmap)
+{
+    extern __shared__ uint8_t leap_smem[];
+    const unsigned lane = threadIdx.x & 31, warp = __shfl_sync(0xffffffffu, threadIdx.x >> 5, 0);
+    const uint32_t base = ((uint32_t)__cvta_generic_to_shared(leap_smem) + 1023u) & ~1023u;
+    const uint32_t box = base + warp * 16384u;
+    const uint64_t nseg = P.items / P.ngroups;
+    const uint64_t T = (P.ngroups + 31) / 32, ntiles = T * nseg;
+    const uint64_t wstride = (uint64_t)gridDim.x * (blockDim.x >> 5);
+    for (uint64_t tile = (uint64_t)blockIdx.x * (blockDim.x >> 5) + warp; tile < ntiles; tile += wstride) {
+        const uint64_t j = tile / T, gt = tile - j * T;
+        LeapGroup cur;
+        cur.init(P, 32 * gt + lane, j);
+        const int64_t row_base = (int64_t)(4 * (P.g0 + 32 * gt)) - (int64_t)P.first;
+        const uint64_t c0 = j * P.seg_len;
+        const uint32_t len = (uint32_t)min(P.seg_len, P.n - c0);  // multiple of 32
+        for (uint32_t r = 0; r < len; r += 32) {
+            if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+            __syncwarp();
+#pragma unroll 2
+            for (uint32_t c = 0; c < 8; ++c) {
+                const W4 v0 = cur.next(P), v1 = cur.next(P), v2 = cur.next(P), v3 = cur.next(P);
+#pragma unroll
+                for (uint32_t st = 0; st < 4; ++st) {
+                    const int l = (int)((st + lane) & 3);
+                    const uint32_t row = 4 * lane + l;
+                    const uint32_t addr = box + row * 128u + ((c ^ (row & 7u)) << 4);
+                    uint32_t a = lane_of(v0, l), b = lane_of(v1, l), d = lane_of(v2, l), e = lane_of(v3, l);
+                    if (KIND == kF32) {
+                        a = __float_as_uint(to_f32(a));
+                        b = __float_as_uint(to_f32(b));
+                        d = __float_as_uint(to_f32(d));
+                        e = __float_as_uint(to_f32(e));
+                    }
+                    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(d), "r"(e)
+                                 : "memory");
+                }
+            }
+            if (row_base < 0) {
+                // first tile of a launch whose first player is not 4-aligned: the
+                // TMA engine rejects negative box coordinates, so the warp copies
+                // the box's live rows itself (lane = word of the row)
+                __syncwarp();
+                for (uint32_t rr = 0; rr < 128; ++rr) {
+                    const int64_t trow = row_base + rr;
+                    if (trow < 0 || trow >= (int64_t)P.ns) continue;
+                    uint32_t w;
+                    asm volatile("ld.shared.b32 %0, [%1];"
+                                 : "=r"(w)
+                                 : "r"(box + rr * 128u + ((((lane >> 2) ^ (rr & 7u))) << 4) + (lane & 3u) * 4u)
+                                 : "memory");
+                    reinterpret_cast<uint32_t*>(P.out)[(uint64_t)trow * P.n + c0 + r + lane] = w;
+                }
+                __syncwarp();
+                continue;
+            }
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) {
+                asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(&tmap),
+                             "r"(box), "r"((int)(c0 + r)), "r"((int)row_base)
+                             : "memory");
+                asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            }
+        }
+    }
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
+constexpr size_t leap_tma_smem() { return (size_t)kLeapTmaWarps * 16384 + 1024; }
+
+template <int KIND>
+cudaError_t leap_tma_attr()
+{
+    static std::atomic<uint64_t> done{0};
+    return ensure_dyn_smem(leap_fill_tma_kernel<KIND>, leap_tma_smem(), done);
+}
+
 __global__ void __launch_bounds__(256) leap_mc_grouped_kernel(const __grid_constant__ LeapLaunch P)
 {
     const uint64_t nthr = (uint64_t)gridDim.x * blockDim.x;
@@ -383,6 +474,23 @@ cudaError_t launch_leap_fill(const LeapLaunch& p, int lgen, int kind, bool vec, 
     if (lgen == kLeapMrg) return fill_g<kLeapMrg>(p, kind, vec, g, s);
     if (lgen == kLeapPhilox) return fill_g<kLeapPhilox>(p, kind, vec, g, s);
     return fill_g<kLeapThreefry>(p, kind, vec, g, s);
+}
+
+cudaError_t launch_leap_fill_tma(const LeapLaunch& p, const CUtensorMap& tmap, int kind, Grid g, cudaStream_t s)
+{
+    cudaError_t e = kind == kF32 ? leap_tma_attr<kF32>() : leap_tma_attr<kU32>();
+    if (e != cudaSuccess) return e;
+    if (kind == kF32) leap_fill_tma_kernel<kF32><<<g.blocks, kLeapTmaWarps * 32, leap_tma_smem(), s>>>(p, tmap);
+    else leap_fill_tma_kernel<kU32><<<g.blocks, kLeapTmaWarps * 32, leap_tma_smem(), s>>>(p, tmap);
+    return cudaGetLastError();
+}
+
+cudaError_t leap_tma_blocks_per_sm(int kind, int* out)
+{
+    cudaError_t e = kind == kF32 ? leap_tma_attr<kF32>() : leap_tma_attr<kU32>();
+    if (e != cudaSuccess) return e;
+    return kind == kF32 ? occ(leap_fill_tma_kernel<kF32>, kLeapTmaWarps * 32, leap_tma_smem(), out)
+                        : occ(leap_fill_tma_kernel<kU32>, kLeapTmaWarps * 32, leap_tma_smem(), out);
 }
 
 cudaError_t launch_leap_mc(const LeapLaunch& p, int lgen, Grid g, cudaStream_t s)

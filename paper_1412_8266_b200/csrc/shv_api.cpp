@@ -372,13 +372,13 @@ PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder()
 
 // 2D map of `ns` rows x `n` values of `elem` bytes at `out` (row-major), box
 // 128 B x 32 rows with the 128-byte swizzle (mrg_fill_tma_kernel).
-bool encode_rows_map(CUtensorMap* m, void* out, uint64_t n, uint64_t ns, int elem)
+bool encode_rows_map(CUtensorMap* m, void* out, uint64_t n, uint64_t ns, int elem, uint32_t box_rows = 32)
 {
     const auto enc = tensor_map_encoder();
     if (!enc) return false;
     const cuuint64_t dims[2] = {n, ns};
     const cuuint64_t strides[1] = {n * (uint64_t)elem};
-    const cuuint32_t box[2] = {128u / (cuuint32_t)elem, 32u};
+    const cuuint32_t box[2] = {128u / (cuuint32_t)elem, box_rows};
     const cuuint32_t estr[2] = {1, 1};
     return enc(m, elem == 8 ? CU_TENSOR_MAP_DATA_TYPE_UINT64 : CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, out, dims, strides,
                box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
@@ -571,11 +571,27 @@ shv_status generate(shv_streams hid, T* out, uint64_t n, void* stream, int kind,
             const int lg = leap_gen(h.gen);
             bool vec = aligned32 && (n % 8 == 0);
             const int kid = leap_kernel_id(kKLeapFill, lg);
-            auto P = leap_launch(h, s0, ns, n, dpv, vec ? 8 : 1, resident_threads(h, kid, kind, vec));
+            // grouped Philox, 4-byte values: TMA boxes of 32 values x 128 rows
+            bool tma = SHV_MRG_TMA && vec && leap_grouped(h) && kind != kF64 && n % 32 == 0 &&
+                       n < (1ull << 31) && ns < (1ull << 31) - 8;
+            auto P = leap_launch(h, s0, ns, n, dpv, tma ? 32 : vec ? 8 : 1, resident_threads(h, kid, kind, vec));
             if (vec && P->seg_len % 8) vec = false;
+            if (tma && P->seg_len % 32) tma = false;
             P->out = dst;
-            Grid g{blocks_for(h, kid, kind, vec, P->items), h.tpb};
-            err = launch_leap_fill(*P, lg, kind, vec, g, s);
+            CUtensorMap tmap;
+            if (tma && !encode_rows_map(&tmap, dst, n, ns, (int)sizeof(T), 128)) tma = false;
+            if (tma) {
+                int bps = 0;
+                err = leap_tma_blocks_per_sm(kind, &bps);
+                const uint64_t tiles = (P->ngroups + 31) / 32 * (P->items / P->ngroups);
+                const uint64_t cap = (uint64_t)h.sms * (uint64_t)(bps > 0 ? bps : 1);
+                const uint64_t want = (tiles + 3) / 4;
+                Grid g{(unsigned)(want < cap ? (want ? want : 1) : cap), 128};
+                if (err == cudaSuccess) err = launch_leap_fill_tma(*P, tmap, kind, g, s);
+            } else {
+                Grid g{blocks_for(h, kid, kind, vec, P->items), h.tpb};
+                err = launch_leap_fill(*P, lg, kind, vec, g, s);
+            }
         } else if (h.gen == SHV_GEN_THREEFRY4X64_20) {
             const uint64_t E = kind == kF64 ? 4 : 8;
             const bool fast = aligned32 && (n % E == 0) && ((uint32_t)h.offset & 7) == 0;

@@ -203,6 +203,11 @@ cudaError_t launch_audit(const AuditLaunch& p, unsigned blocks, cudaStream_t s);
 // Leap Frog (kernels_leapfrog.cu): vec = 32-byte aligned rows, seg_len % 8 == 0.
 cudaError_t launch_leap_fill(const LeapLaunch& p, int lgen, int kind, bool vec, Grid g, cudaStream_t s);
 cudaError_t launch_leap_mc(const LeapLaunch& p, int lgen, Grid g, cudaStream_t s);
+// Grouped Philox Leap Frog fill with TMA stores (u32/f32): `tmap` = 2D map of
+// the launch rows (dim0 = n, dim1 = ns), box 32 values x 128 rows, 128-B
+// swizzle; needs ngroups != 0, n % 32 == 0, seg_len % 32 == 0.
+cudaError_t launch_leap_fill_tma(const LeapLaunch& p, const CUtensorMap& tmap, int kind, Grid g, cudaStream_t s);
+cudaError_t leap_tma_blocks_per_sm(int kind, int* out);
 
 // Which kernel an occupancy query refers to.
 enum KernelId : int {

@@ -1,0 +1,22 @@
+"""Lab: one Leap Frog fill at the C5 shape (2^20 players x 4096 u32) for ncu.
+   python tools/lab/leap_lab.py [mrg|philox] [reps]"""
+import sys
+import os
+import torch
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
+import paper_1412_8266_b200 as shv  # noqa: E402
+
+gen = {"mrg": shv.SHV_GEN_MRG32K3A, "philox": shv.SHV_GEN_PHILOX4X32_10}[sys.argv[1] if len(sys.argv) > 1 else "philox"]
+reps = int(sys.argv[2]) if len(sys.argv) > 2 else 3
+K, n = 1 << 20, 4096
+st = torch.empty(6 * K, dtype=torch.int32, device="cuda") if gen == shv.SHV_GEN_MRG32K3A else None
+h = shv.shv_streams_create_leapfrog(gen, [12345], K, 0, K, st, 0, 0, None)
+out = torch.empty(K * n, dtype=torch.int32, device="cuda")
+for r in range(reps):
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    shv.shv_generate_u32(h, out, n, None)
+    b.record()
+    torch.cuda.synchronize()
+    print(f"leap fill {sys.argv[1:2]}: {a.elapsed_time(b):.3f} ms")
+shv.shv_streams_destroy(h)
