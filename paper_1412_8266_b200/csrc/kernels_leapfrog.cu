@@ -401,6 +401,80 @@ cudaError_t leap_tma_attr()
     return ensure_dyn_smem(leap_fill_tma_kernel<KIND>, leap_tma_smem(), done);
 }
 
+// MRG32k3a Leap Frog by transposition (u32/f32). out[p][t] = base draw
+// (first + p) + K*(o + t): the output is the TRANSPOSE of the base sequence
+// laid out as rows of K consecutive draws. A warp owns 32 consecutive t (lane
+// = t) and a segment of tr_pl players; each lane runs the FP64 MRG step
+// through consecutive base draws (players p, p+1, ...) of its t-row, starting
+// from A^(p_begin + K*t) * tr_s0 (per-bit tables: one jump per lane per
+// segment), and writes draw (p, t) as word t of box row p: all 32 lanes write
+// distinct words of one 128-B row (conflict-free; 128-B swizzle). Each
+// 128-player box (128 rows x 32 values) leaves by TMA; rows past the launch
+// and columns past n are clipped by the tensor map. Per value: the MRG step
+// (12 FP64 instructions) and one shared store, against three modular
+// products per component for the per-player recurrence.
+constexpr unsigned kTrWarps = 4;
+template <int KIND>
+__global__ void __launch_bounds__(kTrWarps * 32)
+    leap_mrg_tr_kernel(const __grid_constant__ LeapLaunch P, const __grid_constant__ CUtensorMap tmap)
+{
+    extern __shared__ uint8_t tr_smem[];
+    const unsigned lane = threadIdx.x & 31, warp = __shfl_sync(0xffffffffu, threadIdx.x >> 5, 0);
+    const uint32_t base = ((uint32_t)__cvta_generic_to_shared(tr_smem) + 1023u) & ~1023u;
+    const uint32_t box = base + warp * 16384u;
+    const MrgFpK K{P.fpk[0], P.fpk[1], P.fpk[2], P.fpk[3], P.fpk[4], P.fpk[5]};
+    // swizzled offset of word `lane` in a box row r: depends on r & 7 only
+    uint32_t off[8];
+#pragma unroll
+    for (uint32_t k = 0; k < 8; ++k) off[k] = ((((lane >> 2) ^ k)) << 4) + (lane & 3u) * 4u;
+    const uint64_t items = P.tr_tb * P.tr_ps;
+    const uint64_t wstride = (uint64_t)gridDim.x * (blockDim.x >> 5);
+    for (uint64_t it = (uint64_t)blockIdx.x * (blockDim.x >> 5) + warp; it < items; it += wstride) {
+        const uint64_t ps = it / P.tr_tb, tb = it - ps * P.tr_tb;
+        const uint64_t t = 32 * tb + lane;
+        const uint64_t p0 = ps * P.tr_pl;
+        const uint64_t p1 = min(P.ns, p0 + P.tr_pl);
+        Mrg m{P.tr_s0[0], P.tr_s0[1], P.tr_s0[2], P.tr_s0[3], P.tr_s0[4], P.tr_s0[5]};
+        for (uint64_t b = 0, x = t; x; ++b, x >>= 1)
+            if (x & 1) apply(P.segpow[b].a, P.segpow[b].b, m);
+        for (uint64_t b = 0, x = ps; x; ++b, x >>= 1)
+            if (x & 1) apply(P.tr_ppow[b].a, P.tr_ppow[b].b, m);
+        MrgFF g = to_mrg_ff(m);
+        for (uint64_t pc = p0; pc < p1; pc += 128) {
+            if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+            __syncwarp();
+#pragma unroll 1
+            for (uint32_t q8 = 0; q8 < 128; q8 += 8) {
+                const uint32_t rb = box + q8 * 128u;
+#pragma unroll
+                for (uint32_t k = 0; k < 8; ++k) {
+                    const uint32_t z = mrg_next(g, K);
+                    const uint32_t w = KIND == kF32 ? __float_as_uint(to_f32(z)) : z;
+                    asm volatile("st.shared.b32 [%0], %1;" ::"r"(rb + k * 128u + off[k]), "r"(w) : "memory");
+                }
+            }
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) {
+                asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(&tmap),
+                             "r"(box), "r"((int)(32 * tb)), "r"((int)pc)
+                             : "memory");
+                asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            }
+        }
+    }
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
+constexpr size_t leap_tr_smem() { return (size_t)kTrWarps * 16384 + 1024; }
+
+template <int KIND>
+cudaError_t leap_tr_attr()
+{
+    static std::atomic<uint64_t> done{0};
+    return ensure_dyn_smem(leap_mrg_tr_kernel<KIND>, leap_tr_smem(), done);
+}
+
 __global__ void __launch_bounds__(256) leap_mc_grouped_kernel(const __grid_constant__ LeapLaunch P)
 {
     const uint64_t nthr = (uint64_t)gridDim.x * blockDim.x;
@@ -491,6 +565,23 @@ cudaError_t leap_tma_blocks_per_sm(int kind, int* out)
     if (e != cudaSuccess) return e;
     return kind == kF32 ? occ(leap_fill_tma_kernel<kF32>, kLeapTmaWarps * 32, leap_tma_smem(), out)
                         : occ(leap_fill_tma_kernel<kU32>, kLeapTmaWarps * 32, leap_tma_smem(), out);
+}
+
+cudaError_t launch_leap_mrg_tr(const LeapLaunch& p, const CUtensorMap& tmap, int kind, unsigned blocks, cudaStream_t s)
+{
+    cudaError_t e = kind == kF32 ? leap_tr_attr<kF32>() : leap_tr_attr<kU32>();
+    if (e != cudaSuccess) return e;
+    if (kind == kF32) leap_mrg_tr_kernel<kF32><<<blocks, kTrWarps * 32, leap_tr_smem(), s>>>(p, tmap);
+    else leap_mrg_tr_kernel<kU32><<<blocks, kTrWarps * 32, leap_tr_smem(), s>>>(p, tmap);
+    return cudaGetLastError();
+}
+
+cudaError_t leap_mrg_tr_blocks_per_sm(int kind, int* out)
+{
+    cudaError_t e = kind == kF32 ? leap_tr_attr<kF32>() : leap_tr_attr<kU32>();
+    if (e != cudaSuccess) return e;
+    return kind == kF32 ? occ(leap_mrg_tr_kernel<kF32>, kTrWarps * 32, leap_tr_smem(), out)
+                        : occ(leap_mrg_tr_kernel<kU32>, kTrWarps * 32, leap_tr_smem(), out);
 }
 
 cudaError_t launch_leap_mc(const LeapLaunch& p, int lgen, Grid g, cudaStream_t s)

@@ -571,6 +571,47 @@ shv_status generate(shv_streams hid, T* out, uint64_t n, void* stream, int kind,
             const int lg = leap_gen(h.gen);
             bool vec = aligned32 && (n % 8 == 0);
             const int kid = leap_kernel_id(kKLeapFill, lg);
+            // MRG32k3a, 4-byte values: fill by transposing the base sequence (TMA boxes)
+            const bool tr = SHV_MRG_TMA && h.gen == SHV_GEN_MRG32K3A && kind != kF64 && n % 4 == 0 &&
+                            ((uintptr_t)dst % 16 == 0) && n < (1ull << 31) && ns < (1ull << 31) - 256;
+            if (tr) {
+                int bps = 0;
+                err = leap_mrg_tr_blocks_per_sm(kind, &bps);
+                auto P = std::make_unique<LeapLaunch>();
+                P->players = h.players;
+                P->first = h.first + s0;
+                P->ns = ns;
+                P->n = n;
+                P->out = dst;
+                uint32_t s6[6];
+                memcpy(s6, h.seed, sizeof s6);
+                pair_apply(pair_pow((u128)P->first + (u128)h.players * h.offset, 0), s6);
+                memcpy(P->tr_s0, s6, sizeof s6);
+                P->segpow[0] = pair_pow(h.players, 0);  // (A^K)^(2^b): t offsets
+                for (int b = 1; b < kSegBits && ((n - 1) >> b); ++b) P->segpow[b] = pair_mul(P->segpow[b - 1], P->segpow[b - 1]);
+                P->tr_tb = (n + 31) / 32;
+                const uint64_t warps = (uint64_t)h.sms * (uint64_t)(bps > 0 ? bps : 1) * 4;
+                const uint64_t want_ps = (4 * warps + P->tr_tb - 1) / P->tr_tb;
+                uint64_t pl = (ns + want_ps - 1) / want_ps;
+                if (pl < 1024) pl = 1024;  // runs long enough to amortise the start jump
+                pl = (pl + 127) / 128 * 128;
+                P->tr_pl = pl;
+                P->tr_ps = (ns + pl - 1) / pl;
+                P->tr_ppow[0] = pair_pow(pl, 0);
+                for (int b = 1; b < kSegBits && ((P->tr_ps - 1) >> b); ++b)
+                    P->tr_ppow[b] = pair_mul(P->tr_ppow[b - 1], P->tr_ppow[b - 1]);
+                const double fpk[6] = {6755399441055744.0, 1.0 / 4294967087.0, 0x1.000059451f212p-32,
+                                       4294967087.0, 4294944443.0, 1370589.0 * 4294944443.0};
+                memcpy(P->fpk, fpk, sizeof fpk);
+                CUtensorMap tmap;
+                if (err == cudaSuccess && !encode_rows_map(&tmap, dst, n, ns, (int)sizeof(T), 128))
+                    err = cudaErrorInvalidValue;
+                const uint64_t items = P->tr_tb * P->tr_ps;
+                const uint64_t cap = (uint64_t)h.sms * (uint64_t)(bps > 0 ? bps : 1);
+                const uint64_t want = (items + 3) / 4;
+                if (err == cudaSuccess)
+                    err = launch_leap_mrg_tr(*P, tmap, kind, (unsigned)(want < cap ? want : cap), s);
+            } else {
             // grouped Philox, 4-byte values: TMA boxes of 32 values x 128 rows
             bool tma = SHV_MRG_TMA && vec && leap_grouped(h) && kind != kF64 && n % 32 == 0 &&
                        n < (1ull << 31) && ns < (1ull << 31) - 8;
@@ -591,6 +632,7 @@ shv_status generate(shv_streams hid, T* out, uint64_t n, void* stream, int kind,
             } else {
                 Grid g{blocks_for(h, kid, kind, vec, P->items), h.tpb};
                 err = launch_leap_fill(*P, lg, kind, vec, g, s);
+            }
             }
         } else if (h.gen == SHV_GEN_THREEFRY4X64_20) {
             const uint64_t E = kind == kF64 ? 4 : 8;

@@ -136,7 +136,14 @@ struct LeapLaunch {
     uint32_t cp1[3], cp2[3];     // u_{t+3} = cp[2] u_{t+2} + cp[1] u_{t+1} + cp[0] u_t (mod m1 / m2)
     MatPair B;                   // A^K
     MatPair start;               // A^(1 + K*o)
-    MatPair segpow[kSegBits];  // (A^(K*seg_draws))^(2^b)
+    MatPair segpow[kSegBits];  // (A^(K*seg_draws))^(2^b); transposed mode: (A^K)^(2^b)
+    // MRG32k3a transposed mode (u32/f32): out[p][t] = base draw (first+p) + K*(o+t)
+    // is the transpose of the base sequence laid out as [t][p]; a lane steps
+    // one t-row through consecutive players (leap_mrg_tr_kernel).
+    uint32_t tr_s0[6];           // A^(first + K*o) seed
+    uint64_t tr_tb, tr_ps, tr_pl;  // t-blocks of 32, player segments, players per segment (% 128 == 0)
+    MatPair tr_ppow[kSegBits];   // (A^tr_pl)^(2^b)
+    double fpk[6];               // FP64 step constants (shv::dev::MrgFpK order)
 };
 
 struct Grid {
@@ -208,6 +215,10 @@ cudaError_t launch_leap_mc(const LeapLaunch& p, int lgen, Grid g, cudaStream_t s
 // swizzle; needs ngroups != 0, n % 32 == 0, seg_len % 32 == 0.
 cudaError_t launch_leap_fill_tma(const LeapLaunch& p, const CUtensorMap& tmap, int kind, Grid g, cudaStream_t s);
 cudaError_t leap_tma_blocks_per_sm(int kind, int* out);
+// MRG32k3a Leap Frog fill by transposition (u32/f32): tmap as above (box 32
+// values x 128 rows); needs n % 4 == 0, tr_pl % 128 == 0.
+cudaError_t launch_leap_mrg_tr(const LeapLaunch& p, const CUtensorMap& tmap, int kind, unsigned blocks, cudaStream_t s);
+cudaError_t leap_mrg_tr_blocks_per_sm(int kind, int* out);
 
 // Which kernel an occupancy query refers to.
 enum KernelId : int {
