@@ -193,6 +193,11 @@ __global__ void __launch_bounds__(256) philox_fill_generic_kernel(const __grid_c
     }
 }
 
+#ifndef SHV_PHILOX_MC_UNROLL
+#define SHV_PHILOX_MC_UNROLL 2  // two blocks in flight per thread: 412 -> 398 ms for C4 (tools/lab)
+#endif
+constexpr int kPhiloxMcUnroll = SHV_PHILOX_MC_UNROLL;
+
 // Fused Philox Monte Carlo. FAST: offset lane 0 and even segment length, so
 // sample pairs never straddle a counter block (two samples per block).
 template <bool FAST, bool KEYED>
@@ -219,6 +224,7 @@ __global__ void __launch_bounds__(256) philox_mc_kernel(const __grid_constant__ 
                 const uint32_t c0r1 = (uint32_t)(p1 >> 32) ^ (uint32_t)(b >> 32) ^ key0;
                 const uint64_t q = (uint64_t)kPM0 * c0r1;
                 uint64_t pa = (uint64_t)kPM0 * (uint32_t)b;
+#pragma unroll kPhiloxMcUnroll
                 for (uint32_t r = 0; r < nb; ++r) {
                     const W4 a = philox10_from_r2(pa, q, (uint32_t)p1, (uint32_t)(g >> 32), key0, key1);
                     h += hit_fp64(a.x, a.y) + hit_fp64(a.z, a.w);
