@@ -15,7 +15,8 @@ __global__ void mrg_rows(uint32_t* out, unsigned long long first, int ns, int n,
     st.s1[0] = s1.x; st.s1[1] = s1.y; st.s1[2] = s1.z;
     st.s2[0] = s1.w; st.s2[1] = s2.x; st.s2[2] = s2.y;
     skipahead_subsequence(first + (unsigned long long)i, &st);
-    for (int j = 0; j < n; ++j) out[(size_t)i * n + j] = (uint32_t)curand(&st);
+    // curand() scales z by 2^32/m1; curand_MRG32k3a returns z itself (an integer in [1, m1])
+    for (int j = 0; j < n; ++j) out[(size_t)i * n + j] = (uint32_t)curand_MRG32k3a(&st);
 }
 
 // Row i = curand_init(seed, first + i, offset) Philox4x32-10 stream, n u32 draws.
