@@ -286,9 +286,9 @@ const char* shv_last_error_message(void);
  *   d_rows      device u32[n_pe * horizon], row-major (row i at i*horizon);
  *   horizon     draws per PE; rows shorter than 4 have no windows;
  *   d_workspace device scratch of workspace_bytes, 8-byte aligned, at least
- *               16 * (windows + 1) bytes; shv_verify_disjoint_workspace_bytes
- *               gives the recommended size (table load 1/2; a fuller table is
- *               correct but probes longer);
+ *               shv_verify_disjoint_workspace_bytes(n_pe, horizon) bytes
+ *               (48 bytes per window + 40 per hash bucket + 48: the records,
+ *               the bucket tables at load <= 1/2 and the candidate list);
  *   d_report    device shv_disjoint_report, written stream-ordered.
  * The report is a function of the rows alone (deterministic merge, S L429):
  * if not disjoint, (pe_a, pos_a, pe_b, pos_b) is the lexicographically

@@ -1,28 +1,34 @@
 // kernels_audit.cu — disjointness audit of generated rows on the GPU
 // (SPEC verify_disjoint, S L407-415, L425-426): every
-// window of 4 consecutive draws of every PE row is put in an open-addressing
-// hash table in HBM; a window value held by two different PEs is a collision.
+// window of 4 consecutive draws of every PE row is hashed; a window value held
+// by two different PEs is a collision.
 //
-// The result is defined by the rows alone, not by the order in which threads
-// reach the table (S "internally parallel with deterministic merge"):
-//   pass 1 (insert)  one slot per distinct window value; the slot keeps the
-//                    smallest occurrence code c = pe*horizon + pos (atomicMin),
-//                    which orders occurrences as (pe, pos) lexicographically;
-//   pass 2 (second)  every occurrence whose PE differs from the slot minimum's
-//                    PE does atomicMin into the slot's second word: the
-//                    smallest occurrence in the next-smallest PE;
-//   pass 3 (reduce)  over slots with a second occurrence: count them and take
-//                    the smallest first occurrence (unique per slot);
-//   pass 4 (final)   one thread re-probes that window for its second word and
-//                    writes the report.
-// Slot word = (24-bit fingerprint << 40) | code, EMPTY = ~0: probes compare
-// fingerprints and load the 16 bytes of a candidate window only on a
-// fingerprint match. Occurrences of one value share the fingerprint, so
-// atomicMin on the packed word is atomicMin on the code. Linear probing
-// without deletion: a value's slot is reached before any empty slot.
-//
-// Roofline: random 32-byte sectors (one table probe + one row read per
-// window per pass on average at load <= 1/2), not streaming bandwidth.
+// Radix-partitioned hash aggregation, so that the hash
+// tables stay L2-resident instead of turning every probe into a random HBM
+// access:
+//   count    hash every window (64-bit mix of its 4 words); bucket = top
+//            log2(P) bits; per-CTA shared-memory histogram, one global add
+//            per CTA and bucket;
+//   scan     bucket offsets for the records and the tables (bucket b's table
+//            has 2*count_b + 1 slots: load <= 1/2);
+//   scatter  per CTA tile: histogram again, reserve a run in each bucket with
+//            one global atomicAdd, write each window's 16-byte record
+//            (hash, code) into its bucket's run (runs of tile/P records);
+//   insert   records in bucket order, so the few tables in use at any time
+//            sit in L2: open addressing, linear probing inside the bucket's
+//            table; slot word = (23-bit fingerprint << 40) | code, code =
+//            pe*horizon + pos, whose numeric order is (pe, pos) order; CAS on
+//            empty slots, atomicMin among equal windows (the slot ends with
+//            the smallest occurrence of its value);
+//   second   each record finds its slot again; an occurrence whose PE differs
+//            from the slot minimum's flags the slot (bit 63; first setter
+//            counts a colliding value), lowers the global minimum first
+//            occurrence a, and appends (slot, code) to a candidate list;
+//   cand     over the candidates of a's slot: the smallest code b;
+//   final    one thread writes the report.
+// Window data are read only to hash (sequentially) and to confirm a
+// fingerprint match (true duplicates; rare otherwise). The result is defined
+// by the rows alone, not by the order in which threads meet (S L429).
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -33,6 +39,9 @@ namespace {
 
 constexpr unsigned long long kEmpty = ~0ull;
 constexpr unsigned long long kCodeMask = (1ull << 40) - 1;
+constexpr unsigned long long kFlag = 1ull << 63;
+constexpr unsigned long long kFpMask = 0x7FFFFFull << 40;  // bits 40..62
+constexpr unsigned kThreads = 256;
 
 struct Win {
     uint32_t w[4];
@@ -63,8 +72,10 @@ __device__ __forceinline__ uint64_t mix(const Win& v)
     return x;
 }
 
-__device__ __forceinline__ uint64_t home(uint64_t x, uint64_t cap) { return __umul64hi(x, cap); }
-__device__ __forceinline__ uint64_t fp_of(uint64_t x) { return (x & 0xFFFFFFull) << 40; }
+__device__ __forceinline__ uint32_t bucket_of(uint64_t x, uint32_t lg) { return lg ? (uint32_t)(x >> (64 - lg)) : 0u; }
+__device__ __forceinline__ uint64_t fp_of(uint64_t x) { return (x << 40) & kFpMask; }
+// home slot inside a bucket table of cap slots: the hash bits below the bucket bits
+__device__ __forceinline__ uint64_t home(uint64_t x, uint32_t lg, uint64_t cap) { return __umul64hi(x << lg, cap); }
 
 __device__ __forceinline__ unsigned long long ld_slot(const unsigned long long* p)
 {
@@ -80,96 +91,188 @@ __device__ __forceinline__ uint64_t code_of(uint64_t w, uint64_t wpr, uint64_t h
     return pe * horizon + (w - pe * wpr);
 }
 
-__global__ void __launch_bounds__(256) audit_insert_kernel(AuditLaunch p)
-{
-    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    for (uint64_t w = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; w < p.windows; w += stride) {
-        const uint64_t c = code_of(w, p.wpr, p.horizon);
-        const Win v = load_win(p.rows, c);
-        const uint64_t x = mix(v);
-        const unsigned long long mine = fp_of(x) | c;
-        uint64_t i = home(x, p.cap);
-        for (;;) {
-            unsigned long long cur = ld_slot(p.slots + i);
-            if (cur == kEmpty) {
-                cur = atomicCAS(p.slots + i, kEmpty, mine);
-                if (cur == kEmpty) break;
-            }
-            if ((cur & ~kCodeMask) == fp_of(x) && same(load_win(p.rows, cur & kCodeMask), v)) {
-                if (mine < cur) atomicMin(p.slots + i, mine);
-                break;
-            }
-            if (++i == p.cap) i = 0;
+// Walks windows w0, w0 + step, ... as (pe, pos) without a 64-bit division per
+// window (one at the start, then carries).
+struct WinWalk {
+    uint64_t pe, pos;
+    __device__ __forceinline__ WinWalk(uint64_t w0, uint64_t wpr) : pe(w0 / wpr), pos(w0 - (w0 / wpr) * wpr) {}
+    __device__ __forceinline__ uint64_t code(uint64_t horizon) const { return pe * horizon + pos; }
+    __device__ __forceinline__ void advance(uint64_t step, uint64_t wpr)
+    {
+        pos += step;
+        while (pos >= wpr) {
+            pos -= wpr;
+            ++pe;
         }
+    }
+};
+
+__global__ void __launch_bounds__(kThreads) audit_count_kernel(AuditLaunch p)
+{
+    extern __shared__ uint32_t hist[];
+    for (uint32_t b = threadIdx.x; b < p.nb; b += blockDim.x) hist[b] = 0;
+    __syncthreads();
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t w = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; w < p.windows; w += stride)
+        atomicAdd(&hist[bucket_of(mix(load_win(p.rows, code_of(w, p.wpr, p.horizon))), p.lgb)], 1u);
+    __syncthreads();
+    for (uint32_t b = threadIdx.x; b < p.nb; b += blockDim.x)
+        if (hist[b]) atomicAdd(p.count + b, (unsigned long long)hist[b]);
+}
+
+// One block: exclusive scans of the bucket counts (records, tables).
+__global__ void __launch_bounds__(1024) audit_scan_kernel(AuditLaunch p)
+{
+    __shared__ unsigned long long part[1024];
+    const uint32_t per = (p.nb + blockDim.x - 1) / blockDim.x;
+    const uint32_t b0 = threadIdx.x * per, b1 = min(p.nb, b0 + per);
+    unsigned long long s = 0;
+    for (uint32_t b = b0; b < b1; ++b) s += p.count[b];
+    part[threadIdx.x] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long acc = 0;
+        for (uint32_t t = 0; t < blockDim.x; ++t) {
+            const unsigned long long v = part[t];
+            part[t] = acc;
+            acc += v;
+        }
+    }
+    __syncthreads();
+    unsigned long long r = part[threadIdx.x];
+    for (uint32_t b = b0; b < b1; ++b) {
+        p.rec_off[b] = r;
+        p.cursor[b] = r;
+        p.tab_off[b] = 2 * r + b;  // 2*count + 1 slots per bucket
+        r += p.count[b];
     }
 }
 
-__global__ void __launch_bounds__(256) audit_second_kernel(AuditLaunch p)
+// Scatter: one CTA tile of kTile windows at a time.
+constexpr uint32_t kTile = 65536;  // 32 records per bucket per tile at 2048 buckets: 512-B runs
+__global__ void __launch_bounds__(kThreads) audit_scatter_kernel(AuditLaunch p)
 {
-    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    for (uint64_t w = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; w < p.windows; w += stride) {
-        const uint64_t c = code_of(w, p.wpr, p.horizon);
-        const Win v = load_win(p.rows, c);
-        const uint64_t x = mix(v);
-        uint64_t i = home(x, p.cap);
+    extern __shared__ uint32_t sm[];
+    uint32_t* hist = sm;                                                            // nb
+    unsigned long long* base = reinterpret_cast<unsigned long long*>(sm + ((p.nb + 1) & ~1u));  // nb
+    const uint64_t ntiles = (p.windows + kTile - 1) / kTile;
+    for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const uint64_t w0 = tile * kTile, w1 = min(p.windows, w0 + kTile);
+        for (uint32_t b = threadIdx.x; b < p.nb; b += blockDim.x) hist[b] = 0;
+        __syncthreads();
+        const WinWalk start(w0 + threadIdx.x, p.wpr);
+        WinWalk ww = start;
+        for (uint64_t w = w0 + threadIdx.x; w < w1; w += blockDim.x, ww.advance(blockDim.x, p.wpr))
+            atomicAdd(&hist[bucket_of(mix(load_win(p.rows, ww.code(p.horizon))), p.lgb)], 1u);
+        __syncthreads();
+        for (uint32_t b = threadIdx.x; b < p.nb; b += blockDim.x) {
+            const uint32_t c = hist[b];
+            base[b] = c ? atomicAdd(p.cursor + b, (unsigned long long)c) : 0ull;
+            hist[b] = 0;
+        }
+        __syncthreads();
+        ww = start;
+        for (uint64_t w = w0 + threadIdx.x; w < w1; w += blockDim.x, ww.advance(blockDim.x, p.wpr)) {
+            const uint64_t c = ww.code(p.horizon);
+            const uint64_t x = mix(load_win(p.rows, c));
+            const uint32_t b = bucket_of(x, p.lgb);
+            const uint64_t at = base[b] + atomicAdd(&hist[b], 1u);
+            p.rec[2 * at] = x;
+            p.rec[2 * at + 1] = c;
+        }
+        __syncthreads();
+    }
+}
+
+// Records are taken in chunks from a global queue in increasing order, so the
+// records in flight (CTAs x kChunk) span only a few buckets and their tables
+// stay in L2; a grid-stride loop lets CTAs drift apart over a long run.
+constexpr uint32_t kChunk = 1024;
+
+__device__ __forceinline__ bool next_chunk(unsigned long long* q, uint64_t windows, uint64_t& r0)
+{
+    __shared__ unsigned long long s_r0;
+    if (threadIdx.x == 0) s_r0 = atomicAdd(q, (unsigned long long)kChunk);
+    __syncthreads();
+    r0 = s_r0;
+    __syncthreads();
+    return r0 < windows;
+}
+
+__global__ void __launch_bounds__(kThreads) audit_insert_kernel(AuditLaunch p)
+{
+    uint64_t r0;
+    while (next_chunk(p.scratch + 3, p.windows, r0))
+    for (uint64_t r = r0 + threadIdx.x; r < min(p.windows, r0 + kChunk); r += blockDim.x) {
+        const uint64_t x = p.rec[2 * r], c = p.rec[2 * r + 1];
+        const uint32_t b = bucket_of(x, p.lgb);
+        unsigned long long* tab = p.slots + p.tab_off[b];
+        const uint64_t cap = 2 * p.count[b] + 1;
+        const unsigned long long mine = fp_of(x) | c;
+        uint64_t i = home(x, p.lgb, cap);
+        Win v{};
+        bool have = false;
         for (;;) {
-            const unsigned long long cur = p.slots[i];  // final after pass 1
-            if ((cur & ~kCodeMask) == fp_of(x)) {
-                const uint64_t m1 = cur & kCodeMask;
-                if (m1 == c) break;  // the value's smallest occurrence itself
-                if (same(load_win(p.rows, m1), v)) {
-                    if (c / p.horizon != m1 / p.horizon) atomicMin(p.second + i, (unsigned long long)c);
+            unsigned long long cur = ld_slot(tab + i);
+            if (cur == kEmpty) {
+                cur = atomicCAS(tab + i, kEmpty, mine);
+                if (cur == kEmpty) break;
+            }
+            if ((cur & kFpMask) == fp_of(x)) {
+                if (!have) {
+                    v = load_win(p.rows, c);
+                    have = true;
+                }
+                if (same(load_win(p.rows, cur & kCodeMask), v)) {
+                    if (mine < cur) atomicMin(tab + i, mine);
                     break;
                 }
             }
-            if (++i == p.cap) i = 0;
+            if (++i == cap) i = 0;
         }
     }
 }
 
-__device__ __forceinline__ unsigned long long warp_min(unsigned long long v)
+__global__ void __launch_bounds__(kThreads) audit_second_kernel(AuditLaunch p)
 {
-#pragma unroll
-    for (int d = 16; d; d >>= 1) {
-        const unsigned long long o = __shfl_xor_sync(0xffffffffu, v, d);
-        v = o < v ? o : v;
+    uint64_t r0;
+    while (next_chunk(p.scratch + 4, p.windows, r0))
+    for (uint64_t r = r0 + threadIdx.x; r < min(p.windows, r0 + kChunk); r += blockDim.x) {
+        const uint64_t x = p.rec[2 * r], c = p.rec[2 * r + 1];
+        const uint32_t b = bucket_of(x, p.lgb);
+        unsigned long long* tab = p.slots + p.tab_off[b];
+        const uint64_t cap = 2 * p.count[b] + 1;
+        uint64_t i = home(x, p.lgb, cap);
+        for (;;) {
+            const unsigned long long cur = ld_slot(tab + i);  // final after insert; bit 63 may be set now
+            if ((cur & kFpMask) == fp_of(x)) {
+                const uint64_t m1 = cur & kCodeMask;
+                if (m1 == c) break;  // the value's smallest occurrence itself
+                if (same(load_win(p.rows, m1), load_win(p.rows, c))) {
+                    if (c / p.horizon != m1 / p.horizon) {
+                        const unsigned long long old = atomicOr(tab + i, kFlag);
+                        if (!(old & kFlag)) atomicAdd(reinterpret_cast<unsigned long long*>(&p.report->colliding), 1ull);
+                        atomicMin(&p.scratch[0], (unsigned long long)m1);
+                        const unsigned long long k = atomicAdd(&p.scratch[2], 1ull);
+                        p.cand[2 * k] = (unsigned long long)(tab + i - p.slots);
+                        p.cand[2 * k + 1] = c;
+                    }
+                    break;
+                }
+            }
+            if (++i == cap) i = 0;
+        }
     }
-    return v;
 }
 
-__global__ void __launch_bounds__(256) audit_reduce_kernel(AuditLaunch p)
+// Candidates of the first colliding value a: its smallest other-PE occurrence.
+__global__ void __launch_bounds__(kThreads) audit_cand_kernel(AuditLaunch p)
 {
-    __shared__ unsigned long long smin[8];
-    __shared__ unsigned long long scnt[8];
-    unsigned long long best = kEmpty, cnt = 0;
+    const unsigned long long a = p.scratch[0], n = p.scratch[2];
+    if (a == kEmpty) return;
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < p.cap; i += stride) {
-        if (p.second[i] != kEmpty) {
-            const unsigned long long a = p.slots[i] & kCodeMask;
-            best = a < best ? a : best;
-            ++cnt;
-        }
-    }
-    best = warp_min(best);
-#pragma unroll
-    for (int d = 16; d; d >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, d);
-    const unsigned wid = threadIdx.x / 32, lane = threadIdx.x % 32;
-    if (lane == 0) {
-        smin[wid] = best;
-        scnt[wid] = cnt;
-    }
-    __syncthreads();
-    if (wid == 0) {
-        best = lane < blockDim.x / 32 ? smin[lane] : kEmpty;
-        cnt = lane < blockDim.x / 32 ? scnt[lane] : 0;
-        best = warp_min(best);
-#pragma unroll
-        for (int d = 16; d; d >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, d);
-        if (lane == 0 && cnt) {
-            atomicMin(reinterpret_cast<unsigned long long*>(&p.report->pe_a), best);  // holds the code until audit_final
-            atomicAdd(reinterpret_cast<unsigned long long*>(&p.report->colliding), cnt);
-        }
-    }
+    for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += stride)
+        if ((p.slots[p.cand[2 * k]] & kCodeMask) == a) atomicMin(&p.scratch[1], p.cand[2 * k + 1]);
 }
 
 __global__ void audit_init_kernel(AuditLaunch p)
@@ -179,18 +282,20 @@ __global__ void audit_init_kernel(AuditLaunch p)
     r->windows = p.windows;
     r->colliding = 0;
     r->pe_a = r->pos_a = r->pe_b = r->pos_b = kEmpty;
+    if (p.scratch) {
+        p.scratch[0] = kEmpty;  // smallest first occurrence of a colliding value
+        p.scratch[1] = kEmpty;  // its smallest other-PE occurrence
+        p.scratch[2] = 0;       // candidates
+        p.scratch[3] = 0;       // insert queue
+        p.scratch[4] = 0;       // second queue
+    }
 }
 
 __global__ void audit_final_kernel(AuditLaunch p)
 {
-    shv_disjoint_report* r = p.report;
-    const uint64_t a = r->pe_a;
+    const unsigned long long a = p.scratch[0], b = p.scratch[1];
     if (a == kEmpty) return;
-    const Win v = load_win(p.rows, a);
-    uint64_t i = home(mix(v), p.cap);
-    while ((p.slots[i] & kCodeMask) != a)
-        if (++i == p.cap) i = 0;
-    const uint64_t b = p.second[i];
+    shv_disjoint_report* r = p.report;
     r->disjoint = 0;
     r->pe_a = a / p.horizon;
     r->pos_a = a % p.horizon;
@@ -200,17 +305,28 @@ __global__ void audit_final_kernel(AuditLaunch p)
 
 }  // namespace
 
+size_t audit_scatter_smem(uint32_t nb) { return (size_t)((nb + 1) & ~1u) * 4 + (size_t)nb * 8; }
+
 cudaError_t launch_audit(const AuditLaunch& p, unsigned blocks, cudaStream_t s)
 {
     audit_init_kernel<<<1, 1, 0, s>>>(p);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess || p.windows == 0) return e;
-    e = cudaMemsetAsync(p.slots, 0xFF, p.cap * sizeof(unsigned long long), s);
-    if (e == cudaSuccess) e = cudaMemsetAsync(p.second, 0xFF, p.cap * sizeof(unsigned long long), s);
+    e = cudaMemsetAsync(p.count, 0, (size_t)p.nb * 8, s);
+    if (e == cudaSuccess) e = cudaMemsetAsync(p.slots, 0xFF, (size_t)(2 * p.windows + p.nb) * 8, s);
     if (e != cudaSuccess) return e;
-    audit_insert_kernel<<<blocks, 256, 0, s>>>(p);
-    audit_second_kernel<<<blocks, 256, 0, s>>>(p);
-    audit_reduce_kernel<<<blocks, 256, 0, s>>>(p);
+    const size_t ssm = audit_scatter_smem(p.nb);
+    if (ssm > 48 * 1024) {
+        e = cudaFuncSetAttribute(audit_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssm);
+        if (e != cudaSuccess) return e;
+    }
+    audit_count_kernel<<<blocks, kThreads, (size_t)p.nb * 4, s>>>(p);
+    audit_scan_kernel<<<1, 1024, 0, s>>>(p);
+    const uint64_t ntiles = (p.windows + kTile - 1) / kTile;
+    audit_scatter_kernel<<<(unsigned)(ntiles < blocks ? ntiles : blocks), kThreads, ssm, s>>>(p);
+    audit_insert_kernel<<<blocks, kThreads, 0, s>>>(p);
+    audit_second_kernel<<<blocks, kThreads, 0, s>>>(p);
+    audit_cand_kernel<<<blocks, kThreads, 0, s>>>(p);
     audit_final_kernel<<<1, 1, 0, s>>>(p);
     return cudaGetLastError();
 }

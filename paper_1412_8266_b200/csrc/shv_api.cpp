@@ -1380,8 +1380,9 @@ static uint64_t audit_windows(uint64_t n_pe, uint64_t horizon)
 
 size_t shv_verify_disjoint_workspace_bytes(uint64_t n_pe, uint64_t horizon)
 {
-    if (n_pe && horizon > (((uint64_t)1 << 40) - 1) / n_pe) return 0;
-    return (size_t)16 * (2 * audit_windows(n_pe, horizon) + 1);
+    if (n_pe && horizon > (((uint64_t)1 << 40) - 2) / n_pe) return 0;
+    const uint64_t w = audit_windows(n_pe, horizon);
+    return w ? (size_t)8 * audit_workspace_words(w) : 0;
 }
 
 shv_status shv_verify_disjoint(const uint32_t* d_rows, uint64_t n_pe, uint64_t horizon, void* d_ws,
@@ -1401,12 +1402,21 @@ shv_status shv_verify_disjoint(const uint32_t* d_rows, uint64_t n_pe, uint64_t h
     if (P.windows) {
         if (!d_rows || !d_ws) return fail(SHV_ERR_INVALID_ARGUMENT, "NULL d_rows or d_workspace");
         if ((uintptr_t)d_ws & 7) return fail(SHV_ERR_MISALIGNED, "d_workspace not 8-byte aligned");
-        P.cap = ws_bytes / 16;
-        if (P.cap <= P.windows)
-            return fail(SHV_ERR_INVALID_ARGUMENT, "workspace of %zu bytes holds %llu slots; %llu windows need more",
-                        ws_bytes, (unsigned long long)P.cap, (unsigned long long)P.windows);
-        P.slots = (unsigned long long*)d_ws;
-        P.second = P.slots + P.cap;
+        const uint64_t words = audit_workspace_words(P.windows);
+        if (ws_bytes / 8 < words)
+            return fail(SHV_ERR_INVALID_ARGUMENT, "workspace of %zu bytes; %llu windows need %llu",
+                        ws_bytes, (unsigned long long)P.windows, (unsigned long long)(8 * words));
+        P.lgb = audit_lg_buckets(P.windows);
+        P.nb = 1u << P.lgb;
+        unsigned long long* w = (unsigned long long*)d_ws;
+        P.scratch = w;
+        P.count = w + 6;
+        P.rec_off = P.count + P.nb;
+        P.cursor = P.rec_off + P.nb;
+        P.tab_off = P.cursor + P.nb;
+        P.rec = P.tab_off + P.nb;
+        P.slots = P.rec + 2 * P.windows;
+        P.cand = P.slots + 2 * P.windows + P.nb;
     }
     int dev = 0, sms = 0;
     cudaError_t e = cudaGetDevice(&dev);

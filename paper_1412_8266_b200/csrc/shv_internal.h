@@ -197,15 +197,31 @@ cudaError_t launch_mtgp_seed(const MtgpLaunch& p, uint32_t seed_base, cudaStream
 cudaError_t launch_mtgp(const MtgpLaunch& p, int mode, unsigned blocks, cudaStream_t s);
 
 // Disjointness audit (kernels_audit.cu; S L407-415): rows = n_pe rows of
-// `horizon` u32, windows = n_pe * wpr (wpr = horizon - 3), table of cap slots
-// (slots, second: cap u64 each), report on the device.
+// `horizon` u32, windows = n_pe * wpr (wpr = horizon - 3). Workspace (u64
+// words): scratch[6], count/rec_off/cursor/tab_off[nb] each, rec[2*windows]
+// (hash, code), slots[2*windows + nb] (bucket b's table at tab_off[b],
+// 2*count[b] + 1 slots), cand[2*windows] (slot, code); report on the device.
 struct AuditLaunch {
     const uint32_t* rows;
-    uint64_t horizon, wpr, windows, cap;
-    unsigned long long* slots;
-    unsigned long long* second;
+    uint64_t horizon, wpr, windows;
+    uint32_t lgb, nb;  // buckets: nb = 2^lgb (top hash bits)
+    unsigned long long *scratch, *count, *rec_off, *cursor, *tab_off, *rec, *slots, *cand;
     shv_disjoint_report* report;
 };
+inline uint32_t audit_lg_buckets(uint64_t windows)
+{
+    uint32_t lg = 0;
+    // >= ~2^16 windows per bucket, <= 2048 buckets: a scatter tile of 2^16 windows
+    // then writes 32-record (512-B) runs per bucket, and a few bucket tables
+    // (<= ~17 MB each at 2^30 windows) fit in L2 at a time
+    while (lg < 11 && (windows >> (16 + lg)) > 0) ++lg;
+    return lg;
+}
+inline uint64_t audit_workspace_words(uint64_t windows)
+{
+    const uint64_t nb = 1ull << audit_lg_buckets(windows);
+    return 6 + 5 * nb + 6 * windows;
+}
 cudaError_t launch_audit(const AuditLaunch& p, unsigned blocks, cudaStream_t s);
 // Leap Frog (kernels_leapfrog.cu): vec = 32-byte aligned rows, seg_len % 8 == 0.
 cudaError_t launch_leap_fill(const LeapLaunch& p, int lgen, int kind, bool vec, Grid g, cudaStream_t s);

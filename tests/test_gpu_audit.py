@@ -91,32 +91,48 @@ def test_workspace_size_does_not_change_the_report(shv, orc):
     rows = rng.integers(0, 3, size=(6, 200)).astype(np.uint32)
     want = expect(orc.verify_disjoint(list(rows)))
     d = to_dev(rows)
-    windows = 6 * 197
-    for slots in (windows + 1, windows + 7, 3 * windows, 8 * windows):
-        assert audit(shv, d, 6, 200, ws_bytes=16 * slots) == want, slots
+    need = shv.shv_verify_disjoint_workspace_bytes(6, 200)
+    for extra in (0, 8, 4096, 1 << 20):
+        assert audit(shv, d, 6, 200, ws_bytes=need + extra) == want, extra
+
+
+def test_many_buckets_match_oracle(shv, orc):
+    """> 2^16 windows: the radix partition uses several buckets (2^17 windows -> 2
+    buckets, 2^19 -> 8); small alphabet so collisions land in many buckets."""
+    rng = np.random.default_rng(3)
+    for n_pe, horizon, alphabet in ((256, 515, 2), (64, 8195, 5), (8, 65539, 1 << 32)):
+        rows = rng.integers(0, alphabet, size=(n_pe, horizon), dtype=np.uint64).astype(np.uint32)
+        if alphabet == 1 << 32:  # plant overlaps between rows 6 -> 2 and 7 -> 5
+            rows[2, 1000:1010] = rows[6, 50000:50010]
+            rows[5, 7:9000] = rows[7, 100:9093]
+        got = audit(shv, to_dev(rows), n_pe, horizon)
+        assert got == expect(orc.verify_disjoint(list(rows))), (n_pe, horizon, alphabet)
 
 
 def test_errors(shv):
     d = to_dev(np.zeros((2, 10), dtype=np.uint32))
     rep = torch.zeros(7, dtype=torch.int64, device="cuda")
-    ws = torch.empty(64, dtype=torch.int64, device="cuda")
-    with pytest.raises(shv.ShvError) as e:  # 14 windows need more than 14 slots
-        shv.shv_verify_disjoint(d, 2, 10, ws, 16 * 14, rep)
+    need = shv.shv_verify_disjoint_workspace_bytes(2, 10)
+    # 14 windows, one bucket: 6 scratch + 5 per-bucket + 6 per-window u64 words
+    assert need == 8 * (6 + 5 + 6 * 14)
+    ws = torch.empty(need // 8 + 8, dtype=torch.int64, device="cuda")
+    with pytest.raises(shv.ShvError) as e:  # one word short
+        shv.shv_verify_disjoint(d, 2, 10, ws, need - 8, rep)
     assert e.value.status == shv.SHV_ERR_INVALID_ARGUMENT
     with pytest.raises(shv.ShvError) as e:
-        shv.shv_verify_disjoint(d, 2, 10, ws.data_ptr() + 4, 16 * 30, rep)
+        shv.shv_verify_disjoint(d, 2, 10, ws.data_ptr() + 4, need, rep)
     assert e.value.status == shv.SHV_ERR_MISALIGNED
     with pytest.raises(shv.ShvError) as e:
-        shv.shv_verify_disjoint(d, 2, 10, ws, 16 * 30, rep.data_ptr() + 4)
+        shv.shv_verify_disjoint(d, 2, 10, ws, need, rep.data_ptr() + 4)
     assert e.value.status == shv.SHV_ERR_MISALIGNED
     with pytest.raises(shv.ShvError) as e:
-        shv.shv_verify_disjoint(d, 1 << 20, 1 << 20, ws, 16 * 30, rep)
+        shv.shv_verify_disjoint(d, 1 << 20, 1 << 20, ws, need, rep)
     assert e.value.status == shv.SHV_ERR_INVALID_ARGUMENT
     with pytest.raises(shv.ShvError) as e:
-        shv.shv_verify_disjoint(None, 2, 10, ws, 16 * 30, rep)
+        shv.shv_verify_disjoint(None, 2, 10, ws, need, rep)
     assert e.value.status == shv.SHV_ERR_INVALID_ARGUMENT
-    assert shv.shv_verify_disjoint_workspace_bytes(2, 10) == 16 * (2 * 14 + 1)
     assert shv.shv_verify_disjoint_workspace_bytes(1 << 20, 1 << 21) == 0
+    assert shv.shv_verify_disjoint_workspace_bytes(5, 3) == 0  # no windows, no workspace
 
 
 def test_spec_examples_on_generated_rows(shv, orc):
