@@ -11,9 +11,10 @@
 //            per CTA and bucket;
 //   scan     bucket offsets for the records and the tables (bucket b's table
 //            has 2*count_b + 1 slots: load <= 1/2);
-//   scatter  per CTA tile: histogram again, reserve a run in each bucket with
-//            one global atomicAdd, write each window's 16-byte record
-//            (hash, code) into its bucket's run (runs of tile/P records);
+//   scatter  per CTA tile of 8192 windows: histogram again, reserve a run in
+//            each bucket with one global atomicAdd, stage the tile's 16-byte
+//            records (hash, code) in shared memory sorted by bucket, and write
+//            each run with coalesced stores;
 //   insert   records in bucket order, so the few tables in use at any time
 //            sit in L2: open addressing, linear probing inside the bucket's
 //            table; slot word = (23-bit fingerprint << 40) | code, code =
@@ -148,16 +149,62 @@ __global__ void __launch_bounds__(1024) audit_scan_kernel(AuditLaunch p)
     }
 }
 
-// Scatter: one CTA tile of kTile windows at a time.
-constexpr uint32_t kTile = 65536;  // 32 records per bucket per tile at 2048 buckets: 512-B runs
-__global__ void __launch_bounds__(kThreads) audit_scatter_kernel(AuditLaunch p)
+// Scatter: one CTA tile of kSTile windows at a time, staged in shared memory
+// sorted by bucket so that each bucket's run leaves as one coalesced write
+// (scattering records straight from the hashing threads left ~2.4M partially
+// written sectors open in L2 and doubled the DRAM traffic by read-modify-write).
+constexpr uint32_t kSTile = 8192;
+constexpr unsigned kSThreads = 512;
+
+// Exclusive scan of v[0..n) in shared memory (n <= 4 * blockDim.x), into out.
+__device__ __forceinline__ void block_exclusive_scan(const uint32_t* v, uint32_t* out, uint32_t n)
 {
-    extern __shared__ uint32_t sm[];
-    uint32_t* hist = sm;                                                            // nb
-    unsigned long long* base = reinterpret_cast<unsigned long long*>(sm + ((p.nb + 1) & ~1u));  // nb
-    const uint64_t ntiles = (p.windows + kTile - 1) / kTile;
+    __shared__ uint32_t warp_tot[32];
+    const uint32_t per = (n + blockDim.x - 1) / blockDim.x;
+    const uint32_t b0 = threadIdx.x * per;
+    uint32_t loc = 0;
+    for (uint32_t k = 0; k < per; ++k)
+        if (b0 + k < n) loc += v[b0 + k];
+    const unsigned lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    uint32_t incl = loc;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t o = __shfl_up_sync(0xffffffffu, incl, d);
+        if (lane >= (unsigned)d) incl += o;
+    }
+    if (lane == 31) warp_tot[wid] = incl;
+    __syncthreads();
+    if (wid == 0) {
+        const unsigned nw = blockDim.x >> 5;
+        uint32_t t = lane < nw ? warp_tot[lane] : 0;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const uint32_t o = __shfl_up_sync(0xffffffffu, t, d);
+            if (lane >= (unsigned)d) t += o;
+        }
+        if (lane < nw) warp_tot[lane] = t;  // inclusive over warps
+    }
+    __syncthreads();
+    uint32_t run = incl - loc + (wid ? warp_tot[wid - 1] : 0);
+    for (uint32_t k = 0; k < per; ++k)
+        if (b0 + k < n) {
+            out[b0 + k] = run;
+            run += v[b0 + k];
+        }
+    __syncthreads();
+}
+
+__global__ void __launch_bounds__(kSThreads) audit_scatter_kernel(AuditLaunch p)
+{
+    extern __shared__ unsigned long long sm64[];
+    unsigned long long* srec = sm64;                              // 2 * kSTile: (hash, code), bucket order
+    unsigned long long* base = srec + 2 * kSTile;                 // nb: global run start per bucket
+    uint32_t* hist = reinterpret_cast<uint32_t*>(base + p.nb);    // nb: counts, then ranks
+    uint32_t* loff = hist + p.nb;                                 // nb: local exclusive offsets
+    const uint64_t ntiles = (p.windows + kSTile - 1) / kSTile;
     for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        const uint64_t w0 = tile * kTile, w1 = min(p.windows, w0 + kTile);
+        const uint64_t w0 = tile * kSTile, w1 = min(p.windows, w0 + kSTile);
+        const uint32_t cnt = (uint32_t)(w1 - w0);
         for (uint32_t b = threadIdx.x; b < p.nb; b += blockDim.x) hist[b] = 0;
         __syncthreads();
         const WinWalk start(w0 + threadIdx.x, p.wpr);
@@ -165,6 +212,7 @@ __global__ void __launch_bounds__(kThreads) audit_scatter_kernel(AuditLaunch p)
         for (uint64_t w = w0 + threadIdx.x; w < w1; w += blockDim.x, ww.advance(blockDim.x, p.wpr))
             atomicAdd(&hist[bucket_of(mix(load_win(p.rows, ww.code(p.horizon))), p.lgb)], 1u);
         __syncthreads();
+        block_exclusive_scan(hist, loff, p.nb);
         for (uint32_t b = threadIdx.x; b < p.nb; b += blockDim.x) {
             const uint32_t c = hist[b];
             base[b] = c ? atomicAdd(p.cursor + b, (unsigned long long)c) : 0ull;
@@ -176,9 +224,17 @@ __global__ void __launch_bounds__(kThreads) audit_scatter_kernel(AuditLaunch p)
             const uint64_t c = ww.code(p.horizon);
             const uint64_t x = mix(load_win(p.rows, c));
             const uint32_t b = bucket_of(x, p.lgb);
-            const uint64_t at = base[b] + atomicAdd(&hist[b], 1u);
-            p.rec[2 * at] = x;
-            p.rec[2 * at + 1] = c;
+            const uint32_t at = loff[b] + atomicAdd(&hist[b], 1u);
+            srec[2 * at] = x;
+            srec[2 * at + 1] = c;
+        }
+        __syncthreads();
+        for (uint32_t i = threadIdx.x; i < cnt; i += blockDim.x) {
+            const unsigned long long x = srec[2 * i];
+            const uint32_t b = bucket_of(x, p.lgb);
+            const uint64_t g = base[b] + (i - loff[b]);
+            p.rec[2 * g] = x;
+            p.rec[2 * g + 1] = srec[2 * i + 1];
         }
         __syncthreads();
     }
@@ -305,7 +361,7 @@ __global__ void audit_final_kernel(AuditLaunch p)
 
 }  // namespace
 
-size_t audit_scatter_smem(uint32_t nb) { return (size_t)((nb + 1) & ~1u) * 4 + (size_t)nb * 8; }
+size_t audit_scatter_smem(uint32_t nb) { return (size_t)kSTile * 16 + (size_t)nb * 16; }
 
 cudaError_t launch_audit(const AuditLaunch& p, unsigned blocks, cudaStream_t s)
 {
@@ -322,8 +378,12 @@ cudaError_t launch_audit(const AuditLaunch& p, unsigned blocks, cudaStream_t s)
     }
     audit_count_kernel<<<blocks, kThreads, (size_t)p.nb * 4, s>>>(p);
     audit_scan_kernel<<<1, 1024, 0, s>>>(p);
-    const uint64_t ntiles = (p.windows + kTile - 1) / kTile;
-    audit_scatter_kernel<<<(unsigned)(ntiles < blocks ? ntiles : blocks), kThreads, ssm, s>>>(p);
+    const uint64_t ntiles = (p.windows + kSTile - 1) / kSTile;
+    int dev = 0, sms = 0;
+    e = cudaGetDevice(&dev);
+    if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (e != cudaSuccess) return e;
+    audit_scatter_kernel<<<(unsigned)(ntiles < (uint64_t)sms ? ntiles : (uint64_t)sms), kSThreads, ssm, s>>>(p);
     audit_insert_kernel<<<blocks, kThreads, 0, s>>>(p);
     audit_second_kernel<<<blocks, kThreads, 0, s>>>(p);
     audit_cand_kernel<<<blocks, kThreads, 0, s>>>(p);
