@@ -64,7 +64,10 @@ static_assert(kMtThreads % 32 == 0, "whole warps");
 template <int MODE>
 __global__ void __launch_bounds__(kMtThreads) mtgp_kernel(const __grid_constant__ MtgpLaunch P)
 {
-    __shared__ uint32_t ring[kRing];
+    // Mirrored ring: word j lives at j and j + 1024 (j < 1024) and the base o
+    // stays below 1024, so every read index o + e + {0, 1, pos - 1, pos}
+    // (< 1024 + 348 + 349) needs no wrap mask; each new word is stored twice.
+    __shared__ uint32_t ring[2 * kRing];
     __shared__ uint32_t tbl[16], ttbl[16], prm[4];
     const unsigned t = threadIdx.x, lane = t & 31;
     // draws per row of this call
@@ -76,12 +79,17 @@ __global__ void __launch_bounds__(kMtThreads) mtgp_kernel(const __grid_constant_
         else if (t < 20) tbl[t - 4] = pp[t];
         else if (t < 36) ttbl[t - 20] = pp[t];
         uint32_t* st = P.state + kMtgpStateWords * i;
-        for (uint32_t k = t; k < kN; k += kMtThreads) ring[k] = st[k];
+        for (uint32_t k = t; k < kN; k += kMtThreads) {
+            const uint32_t w = st[k];
+            ring[k] = w;
+            ring[k + kRing] = w;
+        }
         __syncthreads();
         const uint32_t pos = prm[0], sh1 = prm[1], sh2 = prm[2], mask = prm[3];
         const uint32_t R = min(kMtThreads * kEpt, (kN - pos) & ~1u);
-        uint32_t o = 0;  // ring index of the oldest word
+        uint32_t o = 0;  // ring index of the oldest word, < 1024
         uint32_t h = 0;
+        uint32_t* const orow = reinterpret_cast<uint32_t*>(P.out) + (MODE == kMtF64 ? 2 : 1) * i * P.n;
         for (uint64_t d0 = 0; d0 < D; d0 += R) {
             const uint32_t cnt = (uint32_t)min((uint64_t)R, D - d0);
             // all loads of the round first: the ring stores below cannot then
@@ -91,11 +99,11 @@ __global__ void __launch_bounds__(kMtThreads) mtgp_kernel(const __grid_constant_
             uint32_t x1[kEpt], x2[kEpt], y[kEpt], tt[kEpt], v[kEpt];
 #pragma unroll
             for (unsigned q = 0; q < kEpt; ++q) {
-                const uint32_t k = o + min(t + q * kMtThreads, cnt - 1);
-                x1[q] = ring[k & (kRing - 1)];
-                x2[q] = ring[(k + 1) & (kRing - 1)];
-                y[q] = ring[(k + pos) & (kRing - 1)];
-                tt[q] = ring[(k + pos - 1) & (kRing - 1)];
+                const uint32_t* rk = ring + o + min(t + q * kMtThreads, cnt - 1);
+                x1[q] = rk[0];
+                x2[q] = rk[1];
+                tt[q] = rk[pos - 1];
+                y[q] = rk[pos];
             }
             uint32_t r[kEpt];
 #pragma unroll
@@ -111,30 +119,35 @@ __global__ void __launch_bounds__(kMtThreads) mtgp_kernel(const __grid_constant_
             }
 #pragma unroll
             for (unsigned q = 0; q < kEpt; ++q)
-                if (t + q * kMtThreads < cnt) ring[(o + t + q * kMtThreads + kN) & (kRing - 1)] = r[q];
+                if (t + q * kMtThreads < cnt) {
+                    const uint32_t j = (o + t + q * kMtThreads + kN) & (kRing - 1);
+                    ring[j] = r[q];
+                    ring[j + kRing] = r[q];
+                }
+            uint32_t* const ob = orow + (MODE == kMtF64 ? 2 * (d0 / 2) : d0);
 #pragma unroll
             for (unsigned q = 0; q < kEpt; ++q) {
                 const uint32_t e = t + q * kMtThreads;
                 if (MODE == kMtU32 || MODE == kMtF32) {
                     if (e < cnt) {
-                        if (MODE == kMtU32) reinterpret_cast<uint32_t*>(P.out)[i * P.n + d0 + e] = v[q];
-                        else reinterpret_cast<float*>(P.out)[i * P.n + d0 + e] = to_f32(v[q]);
+                        if (MODE == kMtU32) ob[e] = v[q];
+                        else reinterpret_cast<float*>(ob)[e] = to_f32(v[q]);
                     }
                 } else if (MODE == kMtF64 || MODE == kMtMc) {
                     // d0, R and kMtThreads even: draws (d0+e, d0+e+1) of lanes e, e+1 = value (d0+e)/2
                     const uint32_t hi = __shfl_down_sync(0xffffffffu, v[q], 1);
                     if (!(lane & 1) && e < cnt) {
                         if (MODE == kMtF64)
-                            reinterpret_cast<double*>(P.out)[i * P.n + (d0 + e) / 2] = philox_f64(v[q], hi);
+                            reinterpret_cast<double*>(ob)[e / 2] = philox_f64(v[q], hi);
                         else
                             h += hit(v[q], hi);
                     }
                 }
             }
-            o += cnt;
+            o = (o + cnt) & (kRing - 1);
             __syncthreads();
         }
-        for (uint32_t k = t; k < kN; k += kMtThreads) st[k] = ring[(o + k) & (kRing - 1)];
+        for (uint32_t k = t; k < kN; k += kMtThreads) st[k] = ring[o + k];
         if (MODE == kMtMc) {
             total += h;
             if (P.counts) {
