@@ -157,3 +157,31 @@ def test_leapfrog_validation_without_gpu(shv):
         with pytest.raises(E) as ei:
             shv.shv_streams_create_leapfrog(*args, None, 0, 0, 0)
         assert ei.value.status == code, args
+
+
+def test_audit_workspace_size_without_gpu(shv):
+    """shv_verify_disjoint_workspace_bytes (host-only): 8 * (6 + 5 * nb + 6 * W)
+    for W = n_pe * (horizon - 3) windows, nb = 2^lg buckets with lg the
+    smallest value (<= 11) for which W < 2^(17 + lg), i.e. >= ~2^16 windows
+    per bucket; 0 when there are no windows or the codes
+    would not fit in 40 bits."""
+    def expect(n_pe, horizon):
+        w = n_pe * (horizon - 3) if horizon >= 4 else 0
+        if w == 0:
+            return 0
+        lg = 0
+        while lg < 11 and (w >> (16 + lg)) > 0:
+            lg += 1
+        return 8 * (6 + 5 * (1 << lg) + 6 * w)
+    for n_pe, horizon in ((1, 4), (2, 10), (8, 300), (1, 1 << 16), (256, 515), (1 << 18, 4096), (1 << 20, 4096),
+                          (3, 2), (0, 100)):
+        assert shv.shv_verify_disjoint_workspace_bytes(n_pe, horizon) == expect(n_pe, horizon), (n_pe, horizon)
+    assert shv.shv_verify_disjoint_workspace_bytes(1 << 20, 1 << 21) == 0
+    # no windows: a valid call that needs no rows or workspace; the report is
+    # written on the device, so only argument validation runs here
+    with pytest.raises(shv.ShvError) as e:
+        shv.shv_verify_disjoint(None, 1, 10, None, 0, None, 0)
+    assert e.value.status == shv.SHV_ERR_INVALID_ARGUMENT
+    with pytest.raises(shv.ShvError) as e:
+        shv.shv_verify_disjoint(None, 1, 10, None, 0, 12, 0)  # misaligned report pointer
+    assert e.value.status == shv.SHV_ERR_MISALIGNED
