@@ -153,7 +153,10 @@ __global__ void __launch_bounds__(1024) audit_scan_kernel(AuditLaunch p)
 // sorted by bucket so that each bucket's run leaves as one coalesced write
 // (scattering records straight from the hashing threads left ~2.4M partially
 // written sectors open in L2 and doubled the DRAM traffic by read-modify-write).
-constexpr uint32_t kSTile = 8192;
+#ifndef SHV_AUDIT_STILE
+#define SHV_AUDIT_STILE 8192  // 4096 / 2048 (two / four CTAs per SM) measured no faster
+#endif
+constexpr uint32_t kSTile = SHV_AUDIT_STILE;
 constexpr unsigned kSThreads = 512;
 
 // Exclusive scan of v[0..n) in shared memory (n <= 4 * blockDim.x), into out.
@@ -383,7 +386,12 @@ cudaError_t launch_audit(const AuditLaunch& p, unsigned blocks, cudaStream_t s)
     e = cudaGetDevice(&dev);
     if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     if (e != cudaSuccess) return e;
-    audit_scatter_kernel<<<(unsigned)(ntiles < (uint64_t)sms ? ntiles : (uint64_t)sms), kSThreads, ssm, s>>>(p);
+    int per_sm = 1;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, audit_scatter_kernel, kSThreads, ssm) != cudaSuccess ||
+        per_sm < 1)
+        per_sm = 1;
+    const uint64_t sgrid = (uint64_t)sms * (uint64_t)per_sm;
+    audit_scatter_kernel<<<(unsigned)(ntiles < sgrid ? ntiles : sgrid), kSThreads, ssm, s>>>(p);
     audit_insert_kernel<<<blocks, kThreads, 0, s>>>(p);
     audit_second_kernel<<<blocks, kThreads, 0, s>>>(p);
     audit_cand_kernel<<<blocks, kThreads, 0, s>>>(p);
