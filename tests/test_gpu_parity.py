@@ -512,3 +512,42 @@ def test_concurrent_handles_from_threads(shv, orc):
     assert not errors, errors
     for k, (gen, got) in results.items():
         same(got, orc.generate(gen, [1000 + k], 64, 96, first=64 * k))
+
+
+# --------------------------------------------------------------------------- index-space extremes
+# The last streams of each family at offsets just below each generator's
+# exhaustion point: every 64/128-bit carry in the kernels' counter and
+# position arithmetic (P L264-268; R4, R6, R13, R16) against the oracle.
+# Offsets are reached with shv_jump: (kind, count) pairs.
+
+U64 = (1 << 64) - 1
+
+
+@pytest.mark.parametrize("gen,seed,spacing,first,ns,jumps,m", [
+    (W.MRG32K3A, [12345], W.SPACING_STREAM, (1 << 64) - 3, 3, [(1, (1 << 51) - 1), (0, U64 - 4)], 200),
+    (W.MRG32K3A, [7, 8, 9, 10, 11, 12], W.SPACING_SUBSTREAM, (1 << 51) - 4, 4, [(2, 1), (1, 5), (0, U64)], 160),
+    (W.PHILOX4X32_10, [0xFFFFFFFF, 0xFFFFFFFF], W.SPACING_STREAM, (1 << 64) - 5, 5,
+     [(0, U64)] * 3 + [(0, U64 - 400)], 200),
+    (W.PHILOX4X32_10, [99], W.SPACING_KEYED, (1 << 32) - 3, 3, [(0, U64)] * 3 + [(0, U64 - 197)], 96),
+    (W.THREEFRY4X64_20, [1, 2, 3, 4], W.SPACING_STREAM, (1 << 64) - 2, 2, [(0, U64)] * 7 + [(0, U64 - 293)], 128),
+])
+def test_index_space_extremes(shv, orc, gen, seed, spacing, first, ns, jumps, m):
+    st = torch.empty(6 * ns, dtype=torch.int32, device="cuda") if gen == W.MRG32K3A else None
+    h = shv.shv_streams_create_ex(gen, seed, first, ns, spacing, st, 0, torch.cuda.current_device(), None)
+    for kind, count in jumps:
+        shv.shv_jump(h, kind, count)
+    for kind, dt, ndt in ((0, torch.int32, np.uint32), (2, torch.float64, np.float64)):
+        mm = m // 2 if (kind == 2 and gen != W.MRG32K3A) else m
+        out = torch.empty(ns * mm, dtype=dt, device="cuda")
+        pos = shv.shv_get_position(h)["offset"]
+        getattr(shv, "shv_generate_" + ("u32" if kind == 0 else "f64"))(h, out, mm, None)
+        torch.cuda.synchronize()
+        want = orc.generate(gen, seed, ns, mm, first=first, spacing=spacing, offset=pos, kind=kind)
+        got = out.cpu().numpy().view(ndt).reshape(ns, mm)
+        assert np.array_equal(got.view(np.uint8), np.ascontiguousarray(want).view(np.uint8)), (gen, kind)
+    if gen != W.MRG32K3A:  # the counter-based streams are now (nearly) exhausted
+        out = torch.empty(ns * 64, dtype=torch.int32, device="cuda")
+        with pytest.raises(shv.ShvError) as e:
+            shv.shv_generate_u32(h, out, 64, None)
+        assert e.value.status == shv.SHV_ERR_INVALID_ARGUMENT
+    shv.shv_streams_destroy(h)
