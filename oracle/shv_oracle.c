@@ -310,6 +310,27 @@ static void gf2_mul(const gf2mat* A, const gf2mat* B, gf2mat* C) /* C = A B */
     *C = T;
 }
 
+/* R = T^e for the transition T of t's parameter set (square-and-multiply). */
+static void tinymt32_pow(const orc_tinymt32* t, u128 e, gf2mat* out)
+{
+    gf2mat P, R;
+    memset(&R, 0, sizeof R);
+    for (int c = 0; c < 128; ++c) R.col[c][c >> 5] = 1u << (c & 31); /* identity */
+    for (int c = 0; c < 128; ++c) { /* P = T */
+        orc_tinymt32 u = *t;
+        memset(u.st, 0, sizeof u.st);
+        u.st[c >> 5] = 1u << (c & 31);
+        orc_tinymt32_next_state(&u);
+        memcpy(P.col[c], u.st, sizeof u.st);
+    }
+    while (e) {
+        if (e & 1) gf2_mul(&P, &R, &R);
+        gf2_mul(&P, &P, &P);
+        e >>= 1;
+    }
+    *out = R;
+}
+
 void orc_tinymt32_jump(orc_tinymt32* t, uint64_t e_lo, uint64_t e_hi)
 {
     gf2mat P, R;
@@ -535,6 +556,22 @@ int orc_stream_open_leapfrog(orc_stream* st, int gen, const uint32_t* seed, int 
         orc_mrg_matrices(A1, A2);
         orc_mat_pow(A1, players - 1, 0, (uint64_t)m1, st->leapA1);
         orc_mat_pow(A2, players - 1, 0, (uint64_t)m2, st->leapA2);
+    } else if (gen == ORC_TINYMT32) {
+        /* R19: the base sequence is TinyMT32 init(params, seed) with seed =
+         * {seed, mat1, mat2, tmat}; the player's state is the base state after
+         * d0 draws (T^d0, S L355 jump = iterate); each draw then discards K-1
+         * base draws by stepping (K <= 65, SPEC's per-PE stride-k stepping,
+         * S L424) or by the matrix T^(K-1) (larger K). */
+        if (nseed != 4) return -1;
+        memset(st, 0, sizeof *st);
+        st->gen = gen;
+        orc_tinymt32_init(&st->tm, seed[1], seed[2], seed[3], seed[0]);
+        orc_tinymt32_jump(&st->tm, (uint64_t)d0, (uint64_t)(d0 >> 64));
+        if (players - 1 > 64) {
+            gf2mat M;
+            tinymt32_pow(&st->tm, (u128)(players - 1), &M);
+            memcpy(st->leapT, M.col, sizeof st->leapT);
+        }
     } else if (gen == ORC_PHILOX4X32_10 || gen == ORC_THREEFRY4X64_20) {
         if (orc_stream_open(st, gen, seed, nseed, 0, 0, ORC_SPACING_STREAM, 0, 0)) return -1;
         if (d0 >= ((u128)1 << (gen == ORC_PHILOX4X32_10 ? 66 : 67))) return -1;
@@ -568,6 +605,17 @@ uint32_t orc_stream_next(orc_stream* st)
 {
     if (st->leap) {
         /* Leap Frog: serve the next base draw, then skip K-1 base draws. */
+        if (st->gen == ORC_TINYMT32) {
+            const uint32_t w = orc_tinymt32_generate(&st->tm);
+            if (st->leap - 1 > 64) {
+                gf2mat M;
+                memcpy(M.col, st->leapT, sizeof M.col);
+                gf2_apply(&M, st->tm.st, st->tm.st);
+            } else {
+                for (uint64_t k = 1; k < st->leap; ++k) orc_tinymt32_next_state(&st->tm);
+            }
+            return w;
+        }
         if (st->gen == ORC_MRG32K3A) {
             const uint32_t z = orc_mrg_step(st->s);
             uint32_t a[3], b[3];

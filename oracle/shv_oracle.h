@@ -104,6 +104,7 @@ typedef struct {
     uint64_t leap;        /* Leap Frog: players K (0: not a leap-frog stream) */
     uint64_t leapA1[9], leapA2[9]; /* MRG32k3a: A^(K-1), the K-1 skipped draws */
     uint64_t pos_lo, pos_hi;       /* counter-based: next base draw index */
+    uint32_t leapT[128][4];        /* TinyMT32 Leap Frog: T^(K-1) columns (K > 65) */
 } orc_stream;
 
 /* Open handle-stream i of a (gen, seed, first, spacing) family at draw offset
@@ -130,8 +131,10 @@ uint32_t orc_stream_next(orc_stream* st);
  * stream 0 of seed; Philox4x32-10 / Threefry4x64-20 counter stream 0 of key
  * seed. Each draw takes the next base draw, then skips K-1 base draws (MRG:
  * the jump A^(K-1), S L157-165; counter-based: the index advances by K).
- * TinyMT32: -1. Returns -1 if p >= K or the base sequence is exhausted at the
- * start position (Philox 2^66, Threefry 2^67, MRG 2^128 draws). */
+ * TinyMT32 (R19): seed = {seed, mat1, mat2, tmat}, the base sequence is
+ * init(params, seed); skips by stepping (K <= 65) or by the matrix T^(K-1).
+ * Returns -1 if p >= K or the base sequence is exhausted at the start
+ * position (Philox 2^66, Threefry 2^67, MRG 2^128 draws). */
 int orc_stream_open_leapfrog(orc_stream* st, int gen, const uint32_t* seed, int nseed,
                              uint64_t players, uint64_t player, uint64_t off_lo, uint64_t off_hi);
 

@@ -517,11 +517,37 @@ def test_leapfrog_conversions_and_dartboard_use_player_draws(orc, gen, seed):
     assert np.array_equal(counts, want) and tot == int(want.sum())
 
 
+TM_LEAP_SEED = [1, *W.TINYMT32_CHECK_PARAMS]  # {seed, mat1, mat2, tmat} (R19)
+
+
+def test_tinymt_leapfrog_one_player_is_the_base_sequence(orc):
+    # the base sequence is the authors' init(params, seed) sequence: a TinyMT32
+    # handle's stream 0 (group 0, slice 0) with the same parameter set and seed,
+    # itself pinned to the authors' check output
+    base = orc.generate(W.TINYMT32, W.tinymt32_seed_words(1, 1, [W.TINYMT32_CHECK_PARAMS]), 1, 500)
+    lf = orc.generate(W.TINYMT32, TM_LEAP_SEED, 1, 500, spacing=W.SPACING_LEAPFROG, players=1)
+    assert np.array_equal(lf, base)
+
+
+@pytest.mark.parametrize("K,offset", [(2, 0), (3, 5), (65, 1), (66, 0), (200, 3)])
+def test_tinymt_leapfrog_coverage_reinterleaves_base(orc, K, offset):
+    # K <= 65 skips by stepping, K > 65 by the matrix T^(K-1): both must deal
+    # the base sequence exactly (S L418)
+    h = 24
+    base = orc.generate(W.TINYMT32, TM_LEAP_SEED, 1, K * (offset + h), spacing=W.SPACING_LEAPFROG,
+                        players=1)[0]
+    lf = orc.generate(W.TINYMT32, TM_LEAP_SEED, K, h, spacing=W.SPACING_LEAPFROG, players=K, offset=offset)
+    assert np.array_equal(lf.T.reshape(-1), base[K * offset:])
+    sub = orc.generate(W.TINYMT32, TM_LEAP_SEED, 2, h, spacing=W.SPACING_LEAPFROG, players=K, offset=offset,
+                       first=K - 2)
+    assert np.array_equal(sub, lf[K - 2:])
+
+
 def test_leapfrog_rejects_bad_plans(orc):
     L = W.SPACING_LEAPFROG
     with pytest.raises(ValueError):  # player id >= K
         orc.generate(W.MRG32K3A, [1] * 6, 2, 4, spacing=L, players=3, first=2)
-    with pytest.raises(ValueError):  # TinyMT32 has no leap-frog layout here
+    with pytest.raises(ValueError):  # TinyMT32 leap-frog takes exactly {seed, mat1, mat2, tmat} (R19)
         orc.generate(W.TINYMT32, [1, 1, 1, 0x8F7011EE, 0xFC78FF1F, 0x3793FDFF], 1, 4, spacing=L,
                      players=2)
     with pytest.raises(ValueError):  # Philox base stream exhausted (2^66 draws)
