@@ -462,6 +462,14 @@ def main():
                                         "workspace_bytes": wsb}
         del ws_a
 
+        # TinyMT32 Leap Frog (R19) on the C5 shape: K = world * 2^20 players of the
+        # check parameter set's base sequence; each draw skips K - 1 base draws
+        # with the GF(2) matrix T^(K-1)
+        h = shv.shv_streams_create_leapfrog(W.TINYMT32, [12345, *W.TINYMT32_CHECK_PARAMS], K,
+                                            rank * wm.n_streams, wm.n_streams, None, 0, local, sp)
+        parts["leapfrog_tinymt_fill_u32"] = fill_part(fill_ms(h, out, n, reps=2), total_per_rank)
+        shv.shv_streams_destroy(h)
+
         # C6: stream-count sweep at a fixed 2^32 u32 per GPU (16 GiB),
         # n_streams = 2^13 .. 2^22, n_per_stream = total / n_streams, both generators.
         # Acceptance: every point within 10% of the C5 (2^20 x 4096) figure.

@@ -171,7 +171,11 @@ shv_status shv_streams_create_tinymt32(shv_streams* out, const uint32_t* params,
  * from the handle offset o, which counts the player's own draws). Base
  * sequence: MRG32k3a stream 0 of the seed (seed words as create_ex);
  * Philox4x32-10 / Threefry4x64-20 counter stream 0 of the key (ctr[2..3] = 0
- * resp. ctr[1] = 0). TinyMT32: SHV_ERR_UNSUPPORTED. first_player + n_players
+ * resp. ctr[1] = 0); TinyMT32 (R19): seed_words = 4, {seed, mat1, mat2, tmat},
+ * the authors' init(params, seed) sequence (player states reached with GF(2)
+ * jump tables built on the device at create; each draw skips K - 1 base draws
+ * by stepping for K <= 65, else by the matrix T^(K-1); fewer than 4 words:
+ * SHV_ERR_MISSING_PARAMETERS); MTGP32: SHV_ERR_UNSUPPORTED. first_player + n_players
  * must be <= players (else SHV_ERR_INSUFFICIENT_STREAMS). generate_* and
  * mc_pi* work as for any handle (f64 / MC consume the player's own draws,
  * R7, R9); shv_jump takes SHV_JUMP_DRAWS only (player draws); a call whose

@@ -7,6 +7,8 @@
 namespace shv {
 namespace {
 
+using u128 = unsigned __int128;
+
 // TinyMT32: 8 values -> staging pieces (u32/f32: 8 words; f64: 16 words, two
 // per value like Philox, R7/R15).
 template <int KIND>
@@ -174,6 +176,138 @@ __global__ void __launch_bounds__(256) tinymt_mc_kernel(const __grid_constant__ 
     block_reduce_add(h, P.hits);
 }
 
+// ------------------------------------------------------------------ TinyMT32 Leap Frog (R19)
+// Buffer (u32 words, TmLeapLaunch::buf): [0..2] mat1, mat2, tmat; [4..7] the
+// base state after init(params, seed); [8, 520) T^(K-1) (columns of 4 words);
+// [520 + 512 b, ...) T^(2^b), b < 128.
+constexpr uint32_t kTmBase = 4, kTmSkip = 8, kTmTab = 520;
+
+// One block of 128 threads: T from unit vectors, then 127 squarings.
+__global__ void __launch_bounds__(128) tm_leap_tables_kernel(uint32_t* __restrict__ buf)
+{
+    __shared__ uint4 M[128], N[128];
+    const unsigned c = threadIdx.x;
+    TinyMT t{0, 0, 0, 0, buf[0], buf[1], buf[2]};
+    (c < 32 ? t.s0 : c < 64 ? t.s1 : c < 96 ? t.s2 : t.s3) = 1u << (c & 31);
+    tinymt_next_state(t);
+    M[c] = make_uint4(t.s0, t.s1, t.s2, t.s3);
+    __syncthreads();
+    for (int b = 0; b < 128; ++b) {
+        reinterpret_cast<uint4*>(buf + kTmTab + 512 * b)[c] = M[c];
+        if (b == 127) break;
+        const uint4 x = M[c];
+        const uint32_t xs[4] = {x.x, x.y, x.z, x.w};
+        uint4 y = make_uint4(0, 0, 0, 0);
+        for (int k = 0; k < 128; ++k)
+            if ((xs[k >> 5] >> (k & 31)) & 1u) {
+                const uint4 col = M[k];
+                y.x ^= col.x;
+                y.y ^= col.y;
+                y.z ^= col.z;
+                y.w ^= col.w;
+            }
+        N[c] = y;
+        __syncthreads();
+        M[c] = N[c];
+        __syncthreads();
+    }
+}
+
+// One block of 128 threads: the skip matrix T^e (e = K - 1) as a product of
+// table entries (column c of A*R = A applied to column c of R), and the base
+// state init(params, seed).
+__global__ void __launch_bounds__(128) tm_leap_skip_kernel(uint32_t* __restrict__ buf, uint64_t e, uint32_t seed)
+{
+    __shared__ uint4 R[128];
+    const unsigned c = threadIdx.x;
+    R[c] = make_uint4(c < 32 ? 1u << c : 0u, c >= 32 && c < 64 ? 1u << (c - 32) : 0u,
+                      c >= 64 && c < 96 ? 1u << (c - 64) : 0u, c >= 96 ? 1u << (c - 96) : 0u);
+    __syncthreads();
+    for (int b = 0; b < 64; ++b) {
+        if (!((e >> b) & 1u)) continue;
+        TinyMT t{R[c].x, R[c].y, R[c].z, R[c].w, 0, 0, 0};
+        gf2_apply(buf + kTmTab + 512 * b, t);
+        __syncthreads();
+        R[c] = make_uint4(t.s0, t.s1, t.s2, t.s3);
+        __syncthreads();
+    }
+    reinterpret_cast<uint4*>(buf + kTmSkip)[c] = R[c];
+    if (c == 0) {
+        TinyMT t;
+        tinymt_init(t, buf[0], buf[1], buf[2], seed);
+        buf[kTmBase] = t.s0;
+        buf[kTmBase + 1] = t.s1;
+        buf[kTmBase + 2] = t.s2;
+        buf[kTmBase + 3] = t.s3;
+    }
+}
+
+// Player first + i, segment j: the base state after
+// d = first + i + K*(o + j*seg_draws) draws (per-bit tables), then each draw
+// serves the next base draw and skips K - 1.
+struct TmLeapCursor {
+    TinyMT t;
+    __device__ __forceinline__ void init(const TmLeapLaunch& P, uint64_t i, uint64_t j)
+    {
+        const uint32_t* b = P.buf;
+        t = TinyMT{b[kTmBase], b[kTmBase + 1], b[kTmBase + 2], b[kTmBase + 3], b[0], b[1], b[2]};
+        const u128 d = (u128)(P.first + i) +
+                       (u128)P.players * ((((u128)P.o_hi << 64) | P.o_lo) + (u128)j * P.seg_draws);
+        for (int k = 0; k < 128; ++k)
+            if ((uint64_t)(d >> k) & 1u) gf2_apply(b + kTmTab + 512 * k, t);
+    }
+    __device__ __forceinline__ uint32_t next(const TmLeapLaunch& P)
+    {
+        const uint32_t w = tinymt_next(t);
+        if (P.players - 1 > 64) {
+            gf2_apply(P.buf + kTmSkip, t);
+        } else {
+            for (uint64_t k = 1; k < P.players; ++k) tinymt_next_state(t);
+        }
+        return w;
+    }
+};
+
+template <int KIND>
+__global__ void __launch_bounds__(256) tm_leap_fill_kernel(const __grid_constant__ TmLeapLaunch P)
+{
+    using T = OutT<KIND>;
+    const uint64_t nthr = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t it = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; it < P.items; it += nthr) {
+        const uint64_t j = it / P.ns, i = it - j * P.ns;
+        const uint64_t c0 = j * P.seg_len, len = min(P.seg_len, P.n - c0);
+        TmLeapCursor cur;
+        cur.init(P, i, j);
+        T* o = reinterpret_cast<T*>(P.out) + i * P.n + c0;
+        for (uint64_t k = 0; k < len; ++k) {
+            const uint32_t w = cur.next(P);
+            if (KIND == kU32) o[k] = (T)w;
+            else if (KIND == kF32) o[k] = (T)to_f32(w);
+            else o[k] = (T)philox_f64(w, cur.next(P));  // two player draws per double (R7)
+        }
+    }
+}
+
+__global__ void __launch_bounds__(256) tm_leap_mc_kernel(const __grid_constant__ TmLeapLaunch P)
+{
+    const uint64_t nthr = (uint64_t)gridDim.x * blockDim.x;
+    uint64_t total = 0;
+    for (uint64_t it = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; it < P.items; it += nthr) {
+        const uint64_t j = it / P.ns, i = it - j * P.ns;
+        const uint64_t len = min(P.seg_len, P.n - j * P.seg_len);
+        TmLeapCursor cur;
+        cur.init(P, i, j);
+        uint32_t h = 0;
+        for (uint64_t k = 0; k < len; ++k) {
+            const uint32_t w0 = cur.next(P);
+            h += hit(w0, cur.next(P));
+        }
+        total += h;
+        if (P.counts) atomicAdd(P.counts + i, (unsigned long long)h);
+    }
+    block_reduce_add(total, P.hits);
+}
+
 template <int KIND>
 cudaError_t ensure_tm_smem()
 {
@@ -191,6 +325,22 @@ cudaError_t launch_tm_vec(const TinyMtLaunch& p, Grid g, cudaStream_t s)
 }
 
 }  // namespace
+
+cudaError_t launch_tm_leap_prep(uint32_t* buf, uint64_t players, uint32_t seed, cudaStream_t s)
+{
+    tm_leap_tables_kernel<<<1, 128, 0, s>>>(buf);
+    tm_leap_skip_kernel<<<1, 128, 0, s>>>(buf, players - 1, seed);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_tm_leap(const TmLeapLaunch& p, int mode, Grid g, cudaStream_t s)
+{
+    if (mode == kU32) tm_leap_fill_kernel<kU32><<<g.blocks, g.threads, 0, s>>>(p);
+    else if (mode == kF32) tm_leap_fill_kernel<kF32><<<g.blocks, g.threads, 0, s>>>(p);
+    else if (mode == kF64) tm_leap_fill_kernel<kF64><<<g.blocks, g.threads, 0, s>>>(p);
+    else tm_leap_mc_kernel<<<g.blocks, g.threads, 0, s>>>(p);
+    return cudaGetLastError();
+}
 
 cudaError_t launch_tinymt_prep(const uint32_t* params, uint64_t n_groups, int log2_gs, uint32_t* tables,
                                cudaStream_t s)

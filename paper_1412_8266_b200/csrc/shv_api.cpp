@@ -10,6 +10,7 @@
 
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <atomic>
 #include <cstdarg>
 #include <cstdio>
@@ -567,7 +568,23 @@ shv_status generate(shv_streams hid, T* out, uint64_t n, void* stream, int kind,
         T* dst = host_out ? stage[k & 1] : out;
         if (host_out && k >= 2) err = cudaStreamWaitEvent(s, copy_done[k & 1], 0);
         if (err != cudaSuccess) break;
-        if (h.spacing == SHV_SPACING_LEAPFROG) {
+        if (h.spacing == SHV_SPACING_LEAPFROG && h.gen == SHV_GEN_TINYMT32) {
+            TmLeapLaunch P{};
+            P.buf = h.params;
+            P.players = h.players;
+            P.first = h.first + s0;
+            P.ns = ns;
+            P.o_lo = (uint64_t)h.offset;
+            P.o_hi = (uint64_t)(h.offset >> 64);
+            P.out = dst;
+            P.n = n;
+            uint32_t nseg = 1;
+            split(h, ns, n, 1, 8, (uint64_t)h.sms * 2048, 1ull << 40, &P.seg_len, &nseg, 64);
+            P.seg_draws = P.seg_len * dpv;
+            P.items = ns * nseg;
+            Grid g{(unsigned)std::min<uint64_t>((P.items + 255) / 256, (uint64_t)h.sms * 8), 256};
+            err = launch_tm_leap(P, kind, g, s);
+        } else if (h.spacing == SHV_SPACING_LEAPFROG) {
             const int lg = leap_gen(h.gen);
             bool vec = aligned32 && (n % 8 == 0);
             const int kid = leap_kernel_id(kKLeapFill, lg);
@@ -1051,11 +1068,17 @@ shv_status shv_streams_create_leapfrog(shv_streams* out, int gen, const uint32_t
     Range nvtx_range("shv_streams_create_leapfrog");
     if (!out) return fail(SHV_ERR_INVALID_ARGUMENT, "NULL out handle");
     *out = 0;
-    if (gen == SHV_GEN_TINYMT32) return fail(SHV_ERR_UNSUPPORTED, "TinyMT32 has no Leap Frog layout (R17)");
     if (gen == SHV_GEN_MTGP32) return fail(SHV_ERR_UNSUPPORTED, "MTGP32 has no Leap Frog layout (R18)");
-    uint32_t s6[6];
-    shv_status st = validate_seed(gen, seed, seed_words, s6);
-    if (st) return st;
+    uint32_t s6[6] = {};
+    shv_status st = SHV_OK;
+    if (gen == SHV_GEN_TINYMT32) {  // R19: seed = {seed, mat1, mat2, tmat}
+        if (!seed || seed_words != 4)
+            return fail(SHV_ERR_MISSING_PARAMETERS, "TinyMT32 Leap Frog takes {seed, mat1, mat2, tmat}");
+        memcpy(s6, seed, 16);
+    } else {
+        st = validate_seed(gen, seed, seed_words, s6);
+        if (st) return st;
+    }
     if (players == 0) return fail(SHV_ERR_INVALID_ARGUMENT, "players must be >= 1");
     if (n_players == 0) return fail(SHV_ERR_INVALID_ARGUMENT, "n_players must be >= 1");
     if ((u128)first_player + n_players > players)
@@ -1086,6 +1109,17 @@ shv_status shv_streams_create_leapfrog(shv_streams* out, int gen, const uint32_t
     h->players = players;
     cudaError_t e = cudaDeviceGetAttribute(&h->sms, cudaDevAttrMultiProcessorCount, dev);
     if (e != cudaSuccess) return cuda_fail(e, "cudaDeviceGetAttribute");
+    if (gen == SHV_GEN_TINYMT32) {
+        e = cudaMalloc((void**)&h->params, kTmLeapBufWords * 4);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(tinymt leap tables)");
+        e = cudaMemcpyAsync(h->params, s6 + 1, 12, cudaMemcpyHostToDevice, (cudaStream_t)cuda_stream);
+        if (e == cudaSuccess) e = launch_tm_leap_prep(h->params, players, s6[0], (cudaStream_t)cuda_stream);
+        if (e == cudaSuccess) e = cudaStreamSynchronize((cudaStream_t)cuda_stream);  // host params copy
+        if (e != cudaSuccess) {
+            cudaFree(h->params);
+            return cuda_fail(e, "tinymt leap prep");
+        }
+    }
     if (gen == SHV_GEN_MRG32K3A) {
         st = ensure_tables(dev);
         if (st) return st;
@@ -1140,7 +1174,7 @@ shv_status shv_jump(shv_streams hid, int kind, uint64_t n)
         h.offset += n;
         return SHV_OK;
     }
-    if (h.gen == SHV_GEN_TINYMT32) {
+    if (h.gen == SHV_GEN_TINYMT32 && h.spacing != SHV_SPACING_LEAPFROG) {
         // sequential advance on the device (S L355), on the create stream
         if (kind != SHV_JUMP_DRAWS) return fail(SHV_ERR_UNSUPPORTED, "TinyMT32 jumps by draws only");
         if (n > 0xFFFFFFFFull) return fail(SHV_ERR_INVALID_ARGUMENT, "TinyMT32 advances at most 2^32 draws per jump");
@@ -1207,7 +1241,24 @@ shv_status shv_mc_pi_ex(shv_streams hid, uint64_t samples, uint64_t* d_hits, uin
     cudaStream_t s = (cudaStream_t)stream;
     cudaError_t err;
     const uint64_t cap = 1ull << 31;  // per-item count fits in u32
-    if (h.spacing == SHV_SPACING_LEAPFROG) {
+    if (h.spacing == SHV_SPACING_LEAPFROG && h.gen == SHV_GEN_TINYMT32) {
+        TmLeapLaunch P{};
+        P.buf = h.params;
+        P.players = h.players;
+        P.first = h.first;
+        P.ns = h.n;
+        P.o_lo = (uint64_t)h.offset;
+        P.o_hi = (uint64_t)(h.offset >> 64);
+        P.n = samples;
+        P.hits = (unsigned long long*)d_hits;
+        P.counts = (unsigned long long*)d_counts;
+        uint32_t nseg = 1;
+        split(h, h.n, samples, 1, 8, (uint64_t)h.sms * 2048, cap, &P.seg_len, &nseg, 64);
+        P.seg_draws = P.seg_len * 2;
+        P.items = h.n * nseg;
+        Grid g{(unsigned)std::min<uint64_t>((P.items + 255) / 256, (uint64_t)h.sms * 8), 256};
+        err = launch_tm_leap(P, 3, g, s);
+    } else if (h.spacing == SHV_SPACING_LEAPFROG) {
         const int lg = leap_gen(h.gen);
         const int kid = leap_kernel_id(kKLeapMc, lg);
         auto P = leap_launch(h, 0, h.n, samples, 2, 1, resident_threads(h, kid, 0, true));

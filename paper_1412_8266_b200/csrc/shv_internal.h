@@ -177,6 +177,22 @@ size_t mrg_fill_tma_smem(int threads);
 cudaError_t launch_mrg_mc(const MrgLaunch& p, Grid g, cudaStream_t s);
 cudaError_t launch_philox_fill(const PhiloxLaunch& p, int kind, bool fast, Grid g, cudaStream_t s);
 cudaError_t launch_philox_mc(const PhiloxLaunch& p, bool fast, Grid g, cudaStream_t s);
+// TinyMT32 Leap Frog launch (kernels_tinymt32.cu; R19): buf = the handle's
+// device buffer (params, base state, skip matrix T^(K-1), tables T^(2^b)).
+constexpr size_t kTmLeapBufWords = 520 + 128 * 512;
+struct TmLeapLaunch {
+    const uint32_t* buf;
+    uint64_t players, first, ns;
+    uint64_t o_lo, o_hi;       // player draw offset o (u128)
+    uint64_t seg_len, seg_draws, n, items;  // item it: segment it / ns, row it % ns
+    void* out;
+    unsigned long long* hits;
+    unsigned long long* counts;
+};
+cudaError_t launch_tm_leap_prep(uint32_t* buf, uint64_t players, uint32_t seed, cudaStream_t s);
+// mode: 0 u32, 1 f32, 2 f64 fill; 3 Monte Carlo
+cudaError_t launch_tm_leap(const TmLeapLaunch& p, int mode, Grid g, cudaStream_t s);
+
 // MTGP32-11213 launch (kernels_mtgp32.cu; R18): stream i of the launch has
 // its parameter set at params + 36*i (pos, sh1, sh2, mask, tbl[16],
 // tmp_tbl[16]) and its state at state + 352*i (the N = 351 current words,

@@ -146,7 +146,8 @@ def test_product_does_not_touch_oracle():
 def test_leapfrog_validation_without_gpu(shv):
     # Leap Frog handles (R17): rejected before any CUDA call
     E = shv.ShvError
-    for args, code in (((shv.SHV_GEN_TINYMT32, [1], 4, 0, 4), shv.SHV_ERR_UNSUPPORTED),
+    for args, code in (((shv.SHV_GEN_TINYMT32, [1], 4, 0, 4), shv.SHV_ERR_MISSING_PARAMETERS),  # R19: 4 words
+                       ((shv.SHV_GEN_MTGP32, [1], 4, 0, 4), shv.SHV_ERR_UNSUPPORTED),
                        ((shv.SHV_GEN_PHILOX4X32_10, [1], 0, 0, 4), shv.SHV_ERR_INVALID_ARGUMENT),
                        ((shv.SHV_GEN_PHILOX4X32_10, [1], 4, 0, 0), shv.SHV_ERR_INVALID_ARGUMENT),
                        ((shv.SHV_GEN_PHILOX4X32_10, [1], 4, 2, 3), shv.SHV_ERR_INSUFFICIENT_STREAMS),

@@ -168,7 +168,8 @@ def test_leapfrog_c5_shape_sampled(shv, orc, g):
 def test_leapfrog_errors(shv):
     dev = torch.cuda.current_device()
     E = shv.ShvError
-    for args, code in (((W.TINYMT32, [1], 4, 0, 4), shv.SHV_ERR_UNSUPPORTED),
+    for args, code in (((W.TINYMT32, [1], 4, 0, 4), shv.SHV_ERR_MISSING_PARAMETERS),  # R19: 4 words
+                       ((W.MTGP32, [1], 4, 0, 4), shv.SHV_ERR_UNSUPPORTED),
                        ((W.PHILOX4X32_10, [1], 0, 0, 4), shv.SHV_ERR_INVALID_ARGUMENT),
                        ((W.PHILOX4X32_10, [1], 4, 2, 3), shv.SHV_ERR_INSUFFICIENT_STREAMS),
                        ((W.MRG32K3A, [0] * 6, 4, 0, 4), shv.SHV_ERR_INVALID_SEED)):
@@ -186,3 +187,45 @@ def test_leapfrog_errors(shv):
         shv.shv_generate_u32(h, out, 64, None)  # last base draw 3 + 63 * 2^60 < 2^66
     finally:
         shv.shv_streams_destroy(h)
+
+
+# --------------------------------------------------------------------------- TinyMT32 (R19)
+TM_SEED = [1, *W.TINYMT32_CHECK_PARAMS]  # {seed, mat1, mat2, tmat}
+
+
+@pytest.mark.parametrize("kind", ["u32", "f32", "f64"])
+@pytest.mark.parametrize("K,first,n,m", [(1, 0, 1, 700), (3, 0, 3, 301), (65, 7, 40, 256), (66, 0, 66, 64),
+                                         (1000, 17, 200, 96), ((1 << 40) + 7, (1 << 39) + 5, 32, 40)])
+def test_tinymt_leapfrog_matches_oracle(shv, orc, kind, K, first, n, m):
+    """Stepping skips (K <= 65) and matrix skips (K > 65), far players
+    (u128 jump exponents through the device tables), two calls in a row."""
+    p = Players(shv, W.TINYMT32, TM_SEED, K, first, n)
+    try:
+        for _ in range(2):
+            ref = p.ref(orc, m, kind)
+            same(p.gen_(m, kind), ref)
+    finally:
+        p.close()
+
+
+def test_tinymt_leapfrog_jump_host_and_mc(shv, orc):
+    p = Players(shv, W.TINYMT32, TM_SEED, 70, 3, 50)
+    try:
+        same(p.gen_(37), p.ref(orc, 37, offset=0))
+        shv.shv_jump(p.h, shv.SHV_JUMP_DRAWS, 1001)
+        p.offset += 1001
+        shv.shv_set_launch_config(p.h, 1, 64, 8)  # short segments: per-item table jumps
+        ref = p.ref(orc, 300)
+        same(p.gen_(300), ref)
+        shv.shv_set_launch_config(p.h, 0, 0, 0)
+        ref = p.ref(orc, 64)
+        same(p.gen_(64, host=True), ref)
+        hits = torch.zeros(1, dtype=torch.int64, device="cuda")
+        counts = torch.zeros(50, dtype=torch.int64, device="cuda")
+        shv.shv_mc_pi_ex(p.h, 500, hits, counts, None)
+        torch.cuda.synchronize()
+        tot, want = orc.mc_count(W.TINYMT32, TM_SEED, 50, 500, first=3, spacing=L, players=70, offset=p.offset)
+        assert np.array_equal(counts.cpu().numpy().view(np.uint64), want)
+        assert int(hits.item()) == tot
+    finally:
+        p.close()

@@ -60,6 +60,16 @@ def run():
         shv.shv_mc_pi_ex(h, 101, hits, cnt, None)
         torch.cuda.synchronize()
         shv.shv_streams_destroy(h)
+    # TinyMT32 Leap Frog (stepping and matrix skips)
+    for K in (5, 70):
+        h = shv.shv_streams_create_leapfrog(W.TINYMT32, [3, *W.TINYMT32_CHECK_PARAMS], K, 1, 4, None, 0, dev, None)
+        for dt, fn in ((torch.int32, shv.shv_generate_u32), (torch.float64, shv.shv_generate_f64)):
+            out = torch.empty(4 * 13, dtype=dt, device="cuda")
+            fn(h, out, 13, None)
+        hits = torch.zeros(1, dtype=torch.int64, device="cuda")
+        shv.shv_mc_pi(h, 7, hits, None)
+        torch.cuda.synchronize()
+        shv.shv_streams_destroy(h)
     # MTGP32-11213 (block-cooperative ring kernel)
     mp = W.mtgp32_params(12)
     h = shv.shv_streams_create_mtgp32(mp, 3, 2, 10, None, 0, dev, None)
