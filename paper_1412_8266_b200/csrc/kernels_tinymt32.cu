@@ -308,6 +308,70 @@ __global__ void __launch_bounds__(256) tm_leap_mc_kernel(const __grid_constant__
     block_reduce_add(total, P.hits);
 }
 
+// Transposed TinyMT32 Leap Frog fill (as leap_mrg_tr_kernel, kernels_leapfrog.cu):
+// out[p][t] = base draw (first + p) + K*(o + t) is the transpose of the base
+// sequence laid out as rows of K draws, so a lane (one t-row) steps through
+// consecutive base draws — consecutive players — with one TinyMT32 step per
+// value, after one GF(2) jump to its start (per-bit tables T^(2^b)). Draw
+// (p, t) is word t of box row p; each 128-player box leaves by TMA.
+constexpr unsigned kTmTrWarps = 4;
+template <int KIND>
+__global__ void __launch_bounds__(kTmTrWarps * 32)
+    tm_leap_tr_kernel(const __grid_constant__ TmLeapLaunch P, const __grid_constant__ CUtensorMap tmap)
+{
+    extern __shared__ uint8_t tm_tr_buf[];
+    const unsigned lane = threadIdx.x & 31, warp = __shfl_sync(0xffffffffu, threadIdx.x >> 5, 0);
+    const uint32_t base = ((uint32_t)__cvta_generic_to_shared(tm_tr_buf) + 1023u) & ~1023u;
+    const uint32_t box = base + warp * 16384u;
+    uint32_t off[8];
+#pragma unroll
+    for (uint32_t k = 0; k < 8; ++k) off[k] = ((((lane >> 2) ^ k)) << 4) + (lane & 3u) * 4u;
+    const uint32_t* b = P.buf;
+    const uint64_t items = P.tr_tb * P.tr_ps;
+    const uint64_t wstride = (uint64_t)gridDim.x * (blockDim.x >> 5);
+    for (uint64_t it = (uint64_t)blockIdx.x * (blockDim.x >> 5) + warp; it < items; it += wstride) {
+        const uint64_t ps = it / P.tr_tb, tb = it - ps * P.tr_tb;
+        const uint64_t t = 32 * tb + lane;
+        const uint64_t p0 = ps * P.tr_pl, p1 = min(P.ns, p0 + P.tr_pl);
+        TinyMT g{b[kTmBase], b[kTmBase + 1], b[kTmBase + 2], b[kTmBase + 3], b[0], b[1], b[2]};
+        const u128 d = (u128)(P.first + p0) + (u128)P.players * ((((u128)P.o_hi << 64) | P.o_lo) + t);
+        for (int k = 0; k < 128; ++k)
+            if ((uint64_t)(d >> k) & 1u) gf2_apply(b + kTmTab + 512 * k, g);
+        for (uint64_t pc = p0; pc < p1; pc += 128) {
+            if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+            __syncwarp();
+#pragma unroll 1
+            for (uint32_t q8 = 0; q8 < 128; q8 += 8) {
+                const uint32_t rb = box + q8 * 128u;
+#pragma unroll
+                for (uint32_t k = 0; k < 8; ++k) {
+                    const uint32_t z = tinymt_next(g);
+                    const uint32_t w = KIND == kF32 ? __float_as_uint(to_f32(z)) : z;
+                    asm volatile("st.shared.b32 [%0], %1;" ::"r"(rb + k * 128u + off[k]), "r"(w) : "memory");
+                }
+            }
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) {
+                asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(&tmap),
+                             "r"(box), "r"((int)(32 * tb)), "r"((int)pc)
+                             : "memory");
+                asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            }
+        }
+    }
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
+constexpr size_t tm_tr_smem() { return (size_t)kTmTrWarps * 16384 + 1024; }
+
+template <int KIND>
+cudaError_t tm_tr_attr()
+{
+    static std::atomic<uint64_t> done{0};
+    return ensure_dyn_smem(tm_leap_tr_kernel<KIND>, tm_tr_smem(), done);
+}
+
 template <int KIND>
 cudaError_t ensure_tm_smem()
 {
@@ -325,6 +389,23 @@ cudaError_t launch_tm_vec(const TinyMtLaunch& p, Grid g, cudaStream_t s)
 }
 
 }  // namespace
+
+cudaError_t launch_tm_leap_tr(const TmLeapLaunch& p, const CUtensorMap& tmap, int kind, unsigned blocks, cudaStream_t s)
+{
+    cudaError_t e = kind == kF32 ? tm_tr_attr<kF32>() : tm_tr_attr<kU32>();
+    if (e != cudaSuccess) return e;
+    if (kind == kF32) tm_leap_tr_kernel<kF32><<<blocks, kTmTrWarps * 32, tm_tr_smem(), s>>>(p, tmap);
+    else tm_leap_tr_kernel<kU32><<<blocks, kTmTrWarps * 32, tm_tr_smem(), s>>>(p, tmap);
+    return cudaGetLastError();
+}
+
+cudaError_t tm_leap_tr_blocks_per_sm(int kind, int* out)
+{
+    cudaError_t e = kind == kF32 ? tm_tr_attr<kF32>() : tm_tr_attr<kU32>();
+    if (e != cudaSuccess) return e;
+    return kind == kF32 ? occ(tm_leap_tr_kernel<kF32>, kTmTrWarps * 32, tm_tr_smem(), out)
+                        : occ(tm_leap_tr_kernel<kU32>, kTmTrWarps * 32, tm_tr_smem(), out);
+}
 
 cudaError_t launch_tm_leap_prep(uint32_t* buf, uint64_t players, uint32_t seed, cudaStream_t s)
 {

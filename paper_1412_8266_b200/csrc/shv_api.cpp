@@ -578,12 +578,32 @@ shv_status generate(shv_streams hid, T* out, uint64_t n, void* stream, int kind,
             P.o_hi = (uint64_t)(h.offset >> 64);
             P.out = dst;
             P.n = n;
-            uint32_t nseg = 1;
-            split(h, ns, n, 1, 8, (uint64_t)h.sms * 2048, 1ull << 40, &P.seg_len, &nseg, 64);
-            P.seg_draws = P.seg_len * dpv;
-            P.items = ns * nseg;
-            Grid g{(unsigned)std::min<uint64_t>((P.items + 255) / 256, (uint64_t)h.sms * 8), 256};
-            err = launch_tm_leap(P, kind, g, s);
+            CUtensorMap tmap;
+            const bool tr = SHV_MRG_TMA && kind != kF64 && n % 4 == 0 && ((uintptr_t)dst % 16 == 0) &&
+                            n < (1ull << 31) && ns < (1ull << 31) - 256 &&
+                            encode_rows_map(&tmap, dst, n, ns, (int)sizeof(T), 128);
+            if (tr) {  // transpose of the base sequence, one TinyMT32 step per value (TMA boxes)
+                int bps = 0;
+                err = tm_leap_tr_blocks_per_sm(kind, &bps);
+                P.tr_tb = (n + 31) / 32;
+                const uint64_t warps = (uint64_t)h.sms * (uint64_t)(bps > 0 ? bps : 1) * 4;
+                const uint64_t want_ps = (4 * warps + P.tr_tb - 1) / P.tr_tb;
+                uint64_t pl = (ns + want_ps - 1) / want_ps;
+                if (pl < 4096) pl = 4096;  // long runs amortise the per-lane GF(2) jump
+                P.tr_pl = (pl + 127) / 128 * 128;
+                P.tr_ps = (ns + P.tr_pl - 1) / P.tr_pl;
+                const uint64_t items = P.tr_tb * P.tr_ps;
+                const uint64_t cap = (uint64_t)h.sms * (uint64_t)(bps > 0 ? bps : 1);
+                const uint64_t want = (items + 3) / 4;
+                if (err == cudaSuccess) err = launch_tm_leap_tr(P, tmap, kind, (unsigned)(want < cap ? want : cap), s);
+            } else {
+                uint32_t nseg = 1;
+                split(h, ns, n, 1, 8, (uint64_t)h.sms * 2048, 1ull << 40, &P.seg_len, &nseg, 64);
+                P.seg_draws = P.seg_len * dpv;
+                P.items = ns * nseg;
+                Grid g{(unsigned)std::min<uint64_t>((P.items + 255) / 256, (uint64_t)h.sms * 8), 256};
+                err = launch_tm_leap(P, kind, g, s);
+            }
         } else if (h.spacing == SHV_SPACING_LEAPFROG) {
             const int lg = leap_gen(h.gen);
             bool vec = aligned32 && (n % 8 == 0);

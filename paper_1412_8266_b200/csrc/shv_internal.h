@@ -188,7 +188,12 @@ struct TmLeapLaunch {
     void* out;
     unsigned long long* hits;
     unsigned long long* counts;
+    uint64_t tr_tb, tr_ps, tr_pl;  // transposed fill: t-blocks of 32, player segments, players per segment
 };
+// Transposed TinyMT32 Leap Frog fill (u32/f32, n % 4 == 0; tmap as for the
+// MRG32k3a one: box 32 values x 128 rows, 128-B swizzle; tr_pl % 128 == 0).
+cudaError_t launch_tm_leap_tr(const TmLeapLaunch& p, const CUtensorMap& tmap, int kind, unsigned blocks, cudaStream_t s);
+cudaError_t tm_leap_tr_blocks_per_sm(int kind, int* out);
 cudaError_t launch_tm_leap_prep(uint32_t* buf, uint64_t players, uint32_t seed, cudaStream_t s);
 // mode: 0 u32, 1 f32, 2 f64 fill; 3 Monte Carlo
 cudaError_t launch_tm_leap(const TmLeapLaunch& p, int mode, Grid g, cudaStream_t s);

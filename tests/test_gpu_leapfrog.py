@@ -229,3 +229,18 @@ def test_tinymt_leapfrog_jump_host_and_mc(shv, orc):
         assert int(hits.item()) == tot
     finally:
         p.close()
+
+
+def test_tinymt_leapfrog_transposed_segments_sampled(shv, orc):
+    """10000 players (three 4096-player segments of the transposed fill) x 256
+    u32 and f32 (TMA boxes; rows past the launch clipped): sampled rows."""
+    K = 10000
+    p = Players(shv, W.TINYMT32, TM_SEED, K, 0, K)
+    try:
+        rows = [0, 1, 127, 128, 4095, 4096, 8191, 8192, 9999] + W.sample_streams(K, 16)
+        for kind in ("u32", "f32"):
+            ref = p.ref(orc, 256, kind, streams=rows)
+            got = p.gen_(256, kind)
+            same(got[rows], ref)
+    finally:
+        p.close()
