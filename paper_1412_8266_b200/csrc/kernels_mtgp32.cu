@@ -60,6 +60,7 @@ __global__ void __launch_bounds__(256) mtgp_seed_kernel(const __grid_constant__ 
 #endif
 constexpr unsigned kMtThreads = SHV_MT_THREADS, kEpt = SHV_MT_EPT;
 static_assert(kMtThreads % 32 == 0, "whole warps");
+static_assert(kMtThreads * kEpt >= 348, "a round covers N - pos (<= 348) elements");
 
 template <int MODE>
 __global__ void __launch_bounds__(kMtThreads) mtgp_kernel(const __grid_constant__ MtgpLaunch P)
@@ -75,9 +76,11 @@ __global__ void __launch_bounds__(kMtThreads) mtgp_kernel(const __grid_constant_
     uint64_t total = 0;
     for (uint64_t i = blockIdx.x; i < P.ns; i += gridDim.x) {
         const uint32_t* pp = P.params + kMtgpParamWords * i;
-        if (t < 4) prm[t] = pp[t];
-        else if (t < 20) tbl[t - 4] = pp[t];
-        else if (t < 36) ttbl[t - 20] = pp[t];
+        for (uint32_t k = t; k < kMtgpParamWords; k += kMtThreads) {
+            if (k < 4) prm[k] = pp[k];
+            else if (k < 20) tbl[k - 4] = pp[k];
+            else ttbl[k - 20] = pp[k];
+        }
         uint32_t* st = P.state + kMtgpStateWords * i;
         for (uint32_t k = t; k < kN; k += kMtThreads) {
             const uint32_t w = st[k];
