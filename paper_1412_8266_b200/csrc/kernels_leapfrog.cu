@@ -466,7 +466,67 @@ __global__ void __launch_bounds__(kTrWarps * 32)
     if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
+// Philox4x32-10 Leap Frog by the same transposition (K % 4 == 0, first % 4 == 0):
+// a lane's consecutive base draws are consecutive words of consecutive counter
+// blocks of stream 0, so one block serves four players of the lane's t-row
+// (the per-player kernels evaluate one block per value or per four rows).
+template <int KIND>
+__global__ void __launch_bounds__(kTrWarps * 32)
+    leap_philox_tr_kernel(const __grid_constant__ LeapLaunch P, const __grid_constant__ CUtensorMap tmap)
+{
+    extern __shared__ uint8_t trp_smem[];
+    const unsigned lane = threadIdx.x & 31, warp = __shfl_sync(0xffffffffu, threadIdx.x >> 5, 0);
+    const uint32_t base = ((uint32_t)__cvta_generic_to_shared(trp_smem) + 1023u) & ~1023u;
+    const uint32_t box = base + warp * 16384u;
+    uint32_t off[8];
+#pragma unroll
+    for (uint32_t k = 0; k < 8; ++k) off[k] = ((((lane >> 2) ^ k)) << 4) + (lane & 3u) * 4u;
+    const uint64_t items = P.tr_tb * P.tr_ps;
+    const uint64_t wstride = (uint64_t)gridDim.x * (blockDim.x >> 5);
+    const u128 o = ((u128)P.o_hi << 64) | P.o_lo;
+    for (uint64_t it = (uint64_t)blockIdx.x * (blockDim.x >> 5) + warp; it < items; it += wstride) {
+        const uint64_t ps = it / P.tr_tb, tb = it - ps * P.tr_tb;
+        const uint64_t t = 32 * tb + lane;
+        const uint64_t p0 = ps * P.tr_pl;
+        const uint64_t p1 = min(P.ns, p0 + P.tr_pl);
+        uint64_t b = (uint64_t)(((u128)(P.first + p0) + (u128)P.players * (o + t)) >> 2);  // 4-aligned
+        for (uint64_t pc = p0; pc < p1; pc += 128) {
+            if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+            __syncwarp();
+#pragma unroll 1
+            for (uint32_t q8 = 0; q8 < 128; q8 += 8) {
+                const uint32_t rb = box + q8 * 128u;
+                const W4 v0 = philox_blk(b, 0, (uint32_t)P.k0, (uint32_t)P.k1);
+                const W4 v1 = philox_blk(b + 1, 0, (uint32_t)P.k0, (uint32_t)P.k1);
+                b += 2;
+                const uint32_t z[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+#pragma unroll
+                for (uint32_t k = 0; k < 8; ++k) {
+                    const uint32_t w = KIND == kF32 ? __float_as_uint(to_f32(z[k])) : z[k];
+                    asm volatile("st.shared.b32 [%0], %1;" ::"r"(rb + k * 128u + off[k]), "r"(w) : "memory");
+                }
+            }
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) {
+                asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(&tmap),
+                             "r"(box), "r"((int)(32 * tb)), "r"((int)pc)
+                             : "memory");
+                asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            }
+        }
+    }
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
 constexpr size_t leap_tr_smem() { return (size_t)kTrWarps * 16384 + 1024; }
+
+template <int KIND>
+cudaError_t leap_trp_attr()
+{
+    static std::atomic<uint64_t> done{0};
+    return ensure_dyn_smem(leap_philox_tr_kernel<KIND>, leap_tr_smem(), done);
+}
 
 template <int KIND>
 cudaError_t leap_tr_attr()
@@ -573,6 +633,15 @@ cudaError_t launch_leap_mrg_tr(const LeapLaunch& p, const CUtensorMap& tmap, int
     if (e != cudaSuccess) return e;
     if (kind == kF32) leap_mrg_tr_kernel<kF32><<<blocks, kTrWarps * 32, leap_tr_smem(), s>>>(p, tmap);
     else leap_mrg_tr_kernel<kU32><<<blocks, kTrWarps * 32, leap_tr_smem(), s>>>(p, tmap);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_leap_philox_tr(const LeapLaunch& p, const CUtensorMap& tmap, int kind, unsigned blocks, cudaStream_t s)
+{
+    cudaError_t e = kind == kF32 ? leap_trp_attr<kF32>() : leap_trp_attr<kU32>();
+    if (e != cudaSuccess) return e;
+    if (kind == kF32) leap_philox_tr_kernel<kF32><<<blocks, kTrWarps * 32, leap_tr_smem(), s>>>(p, tmap);
+    else leap_philox_tr_kernel<kU32><<<blocks, kTrWarps * 32, leap_tr_smem(), s>>>(p, tmap);
     return cudaGetLastError();
 }
 

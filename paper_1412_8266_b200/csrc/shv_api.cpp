@@ -609,7 +609,10 @@ shv_status generate(shv_streams hid, T* out, uint64_t n, void* stream, int kind,
             bool vec = aligned32 && (n % 8 == 0);
             const int kid = leap_kernel_id(kKLeapFill, lg);
             // MRG32k3a, 4-byte values: fill by transposing the base sequence (TMA boxes)
-            const bool tr = SHV_MRG_TMA && h.gen == SHV_GEN_MRG32K3A && kind != kF64 && n % 4 == 0 &&
+            // Philox: K % 4 == 0 and a 4-aligned first player keep every lane's run
+            // on whole counter blocks (leap_philox_tr_kernel)
+            const bool trp = h.gen == SHV_GEN_PHILOX4X32_10 && h.players % 4 == 0 && (h.first + s0) % 4 == 0;
+            const bool tr = SHV_MRG_TMA && (h.gen == SHV_GEN_MRG32K3A || trp) && kind != kF64 && n % 4 == 0 &&
                             ((uintptr_t)dst % 16 == 0) && n < (1ull << 31) && ns < (1ull << 31) - 256;
             if (tr) {
                 int bps = 0;
@@ -620,12 +623,19 @@ shv_status generate(shv_streams hid, T* out, uint64_t n, void* stream, int kind,
                 P->ns = ns;
                 P->n = n;
                 P->out = dst;
-                uint32_t s6[6];
-                memcpy(s6, h.seed, sizeof s6);
-                pair_apply(pair_pow((u128)P->first + (u128)h.players * h.offset, 0), s6);
-                memcpy(P->tr_s0, s6, sizeof s6);
-                P->segpow[0] = pair_pow(h.players, 0);  // (A^K)^(2^b): t offsets
-                for (int b = 1; b < kSegBits && ((n - 1) >> b); ++b) P->segpow[b] = pair_mul(P->segpow[b - 1], P->segpow[b - 1]);
+                P->o_lo = (uint64_t)h.offset;
+                P->o_hi = (uint64_t)(h.offset >> 64);
+                P->k0 = h.seed[0];
+                P->k1 = h.seed[1];
+                if (!trp) {
+                    uint32_t s6[6];
+                    memcpy(s6, h.seed, sizeof s6);
+                    pair_apply(pair_pow((u128)P->first + (u128)h.players * h.offset, 0), s6);
+                    memcpy(P->tr_s0, s6, sizeof s6);
+                    P->segpow[0] = pair_pow(h.players, 0);  // (A^K)^(2^b): t offsets
+                    for (int b = 1; b < kSegBits && ((n - 1) >> b); ++b)
+                        P->segpow[b] = pair_mul(P->segpow[b - 1], P->segpow[b - 1]);
+                }
                 P->tr_tb = (n + 31) / 32;
                 const uint64_t warps = (uint64_t)h.sms * (uint64_t)(bps > 0 ? bps : 1) * 4;
                 const uint64_t want_ps = (4 * warps + P->tr_tb - 1) / P->tr_tb;
@@ -647,7 +657,8 @@ shv_status generate(shv_streams hid, T* out, uint64_t n, void* stream, int kind,
                 const uint64_t cap = (uint64_t)h.sms * (uint64_t)(bps > 0 ? bps : 1);
                 const uint64_t want = (items + 3) / 4;
                 if (err == cudaSuccess)
-                    err = launch_leap_mrg_tr(*P, tmap, kind, (unsigned)(want < cap ? want : cap), s);
+                    err = trp ? launch_leap_philox_tr(*P, tmap, kind, (unsigned)(want < cap ? want : cap), s)
+                              : launch_leap_mrg_tr(*P, tmap, kind, (unsigned)(want < cap ? want : cap), s);
             } else {
             // grouped Philox, 4-byte values: TMA boxes of 32 values x 128 rows
             bool tma = SHV_MRG_TMA && vec && leap_grouped(h) && kind != kF64 && n % 32 == 0 &&
