@@ -430,7 +430,8 @@ def main():
         # of K = world*2^20)
         K = wm.n_streams * world
         for key, gen, seed in (("leapfrog_mrg_fill_u32", W.MRG32K3A, wm.seed),
-                               ("leapfrog_philox_fill_u32", W.PHILOX4X32_10, wp.seed)):
+                               ("leapfrog_philox_fill_u32", W.PHILOX4X32_10, wp.seed),
+                               ("leapfrog_threefry_fill_u32", W.THREEFRY4X64_20, (12345,))):
             h = shv.shv_streams_create_leapfrog(gen, list(seed), K, rank * wm.n_streams, wm.n_streams,
                                                 state if gen == W.MRG32K3A else None, 0, local, sp)
             parts[key] = fill_part(fill_ms(h, out, n), total_per_rank)

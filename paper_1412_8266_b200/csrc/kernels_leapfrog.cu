@@ -466,13 +466,14 @@ __global__ void __launch_bounds__(kTrWarps * 32)
     if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
-// Philox4x32-10 Leap Frog by the same transposition (K % 4 == 0, first % 4 == 0):
-// a lane's consecutive base draws are consecutive words of consecutive counter
-// blocks of stream 0, so one block serves four players of the lane's t-row
-// (the per-player kernels evaluate one block per value or per four rows).
-template <int KIND>
+// Counter-based Leap Frog by the same transposition (Philox: K % 4 == 0 and
+// first % 4 == 0; Threefry: K % 8 == 0 and first % 8 == 0): a lane's
+// consecutive base draws are consecutive words of consecutive counter blocks
+// of stream 0, so one block serves 4 (Philox) or 8 (Threefry) players of the
+// lane's t-row (the per-player kernels evaluate one block per value).
+template <int KIND, int G>
 __global__ void __launch_bounds__(kTrWarps * 32)
-    leap_philox_tr_kernel(const __grid_constant__ LeapLaunch P, const __grid_constant__ CUtensorMap tmap)
+    leap_ctr_tr_kernel(const __grid_constant__ LeapLaunch P, const __grid_constant__ CUtensorMap tmap)
 {
     extern __shared__ uint8_t trp_smem[];
     const unsigned lane = threadIdx.x & 31, warp = __shfl_sync(0xffffffffu, threadIdx.x >> 5, 0);
@@ -489,17 +490,27 @@ __global__ void __launch_bounds__(kTrWarps * 32)
         const uint64_t t = 32 * tb + lane;
         const uint64_t p0 = ps * P.tr_pl;
         const uint64_t p1 = min(P.ns, p0 + P.tr_pl);
-        uint64_t b = (uint64_t)(((u128)(P.first + p0) + (u128)P.players * (o + t)) >> 2);  // 4-aligned
+        // words per block: 4 (Philox) or 8 (Threefry); the run starts block-aligned
+        uint64_t b = (uint64_t)(((u128)(P.first + p0) + (u128)P.players * (o + t)) >> (G == kLeapPhilox ? 2 : 3));
         for (uint64_t pc = p0; pc < p1; pc += 128) {
             if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
             __syncwarp();
 #pragma unroll 1
             for (uint32_t q8 = 0; q8 < 128; q8 += 8) {
                 const uint32_t rb = box + q8 * 128u;
-                const W4 v0 = philox_blk(b, 0, (uint32_t)P.k0, (uint32_t)P.k1);
-                const W4 v1 = philox_blk(b + 1, 0, (uint32_t)P.k0, (uint32_t)P.k1);
-                b += 2;
-                const uint32_t z[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+                uint32_t z[8];
+                if constexpr (G == kLeapPhilox) {
+                    const W4 v0 = philox_blk(b, 0, (uint32_t)P.k0, (uint32_t)P.k1);
+                    const W4 v1 = philox_blk(b + 1, 0, (uint32_t)P.k0, (uint32_t)P.k1);
+                    b += 2;
+                    z[0] = v0.x; z[1] = v0.y; z[2] = v0.z; z[3] = v0.w;
+                    z[4] = v1.x; z[5] = v1.y; z[6] = v1.z; z[7] = v1.w;
+                } else {  // Threefry4x64-20: words (lo, hi) of lanes 0..3 (R16)
+                    const Q4 v = threefry20(b, 0, P.k0, P.k1);
+                    b += 1;
+                    z[0] = (uint32_t)v.x; z[1] = (uint32_t)(v.x >> 32); z[2] = (uint32_t)v.y; z[3] = (uint32_t)(v.y >> 32);
+                    z[4] = (uint32_t)v.z; z[5] = (uint32_t)(v.z >> 32); z[6] = (uint32_t)v.w; z[7] = (uint32_t)(v.w >> 32);
+                }
 #pragma unroll
                 for (uint32_t k = 0; k < 8; ++k) {
                     const uint32_t w = KIND == kF32 ? __float_as_uint(to_f32(z[k])) : z[k];
@@ -521,11 +532,11 @@ __global__ void __launch_bounds__(kTrWarps * 32)
 
 constexpr size_t leap_tr_smem() { return (size_t)kTrWarps * 16384 + 1024; }
 
-template <int KIND>
+template <int KIND, int G>
 cudaError_t leap_trp_attr()
 {
     static std::atomic<uint64_t> done{0};
-    return ensure_dyn_smem(leap_philox_tr_kernel<KIND>, leap_tr_smem(), done);
+    return ensure_dyn_smem(leap_ctr_tr_kernel<KIND, G>, leap_tr_smem(), done);
 }
 
 template <int KIND>
@@ -636,13 +647,21 @@ cudaError_t launch_leap_mrg_tr(const LeapLaunch& p, const CUtensorMap& tmap, int
     return cudaGetLastError();
 }
 
-cudaError_t launch_leap_philox_tr(const LeapLaunch& p, const CUtensorMap& tmap, int kind, unsigned blocks, cudaStream_t s)
+template <int G>
+cudaError_t launch_ctr_tr_g(const LeapLaunch& p, const CUtensorMap& tmap, int kind, unsigned blocks, cudaStream_t s)
 {
-    cudaError_t e = kind == kF32 ? leap_trp_attr<kF32>() : leap_trp_attr<kU32>();
+    cudaError_t e = kind == kF32 ? leap_trp_attr<kF32, G>() : leap_trp_attr<kU32, G>();
     if (e != cudaSuccess) return e;
-    if (kind == kF32) leap_philox_tr_kernel<kF32><<<blocks, kTrWarps * 32, leap_tr_smem(), s>>>(p, tmap);
-    else leap_philox_tr_kernel<kU32><<<blocks, kTrWarps * 32, leap_tr_smem(), s>>>(p, tmap);
+    if (kind == kF32) leap_ctr_tr_kernel<kF32, G><<<blocks, kTrWarps * 32, leap_tr_smem(), s>>>(p, tmap);
+    else leap_ctr_tr_kernel<kU32, G><<<blocks, kTrWarps * 32, leap_tr_smem(), s>>>(p, tmap);
     return cudaGetLastError();
+}
+
+cudaError_t launch_leap_ctr_tr(const LeapLaunch& p, const CUtensorMap& tmap, int lgen, int kind, unsigned blocks,
+                               cudaStream_t s)
+{
+    return lgen == kLeapPhilox ? launch_ctr_tr_g<kLeapPhilox>(p, tmap, kind, blocks, s)
+                               : launch_ctr_tr_g<kLeapThreefry>(p, tmap, kind, blocks, s);
 }
 
 cudaError_t leap_mrg_tr_blocks_per_sm(int kind, int* out)

@@ -611,7 +611,8 @@ shv_status generate(shv_streams hid, T* out, uint64_t n, void* stream, int kind,
             // MRG32k3a, 4-byte values: fill by transposing the base sequence (TMA boxes)
             // Philox: K % 4 == 0 and a 4-aligned first player keep every lane's run
             // on whole counter blocks (leap_philox_tr_kernel)
-            const bool trp = h.gen == SHV_GEN_PHILOX4X32_10 && h.players % 4 == 0 && (h.first + s0) % 4 == 0;
+            const bool trp = (h.gen == SHV_GEN_PHILOX4X32_10 && h.players % 4 == 0 && (h.first + s0) % 4 == 0) ||
+                             (h.gen == SHV_GEN_THREEFRY4X64_20 && h.players % 8 == 0 && (h.first + s0) % 8 == 0);
             const bool tr = SHV_MRG_TMA && (h.gen == SHV_GEN_MRG32K3A || trp) && kind != kF64 && n % 4 == 0 &&
                             ((uintptr_t)dst % 16 == 0) && n < (1ull << 31) && ns < (1ull << 31) - 256;
             if (tr) {
@@ -625,8 +626,13 @@ shv_status generate(shv_streams hid, T* out, uint64_t n, void* stream, int kind,
                 P->out = dst;
                 P->o_lo = (uint64_t)h.offset;
                 P->o_hi = (uint64_t)(h.offset >> 64);
-                P->k0 = h.seed[0];
-                P->k1 = h.seed[1];
+                if (h.gen == SHV_GEN_THREEFRY4X64_20) {
+                    P->k0 = (uint64_t)h.seed[0] | ((uint64_t)h.seed[1] << 32);
+                    P->k1 = (uint64_t)h.seed[2] | ((uint64_t)h.seed[3] << 32);
+                } else {
+                    P->k0 = h.seed[0];
+                    P->k1 = h.seed[1];
+                }
                 if (!trp) {
                     uint32_t s6[6];
                     memcpy(s6, h.seed, sizeof s6);
@@ -657,7 +663,7 @@ shv_status generate(shv_streams hid, T* out, uint64_t n, void* stream, int kind,
                 const uint64_t cap = (uint64_t)h.sms * (uint64_t)(bps > 0 ? bps : 1);
                 const uint64_t want = (items + 3) / 4;
                 if (err == cudaSuccess)
-                    err = trp ? launch_leap_philox_tr(*P, tmap, kind, (unsigned)(want < cap ? want : cap), s)
+                    err = trp ? launch_leap_ctr_tr(*P, tmap, leap_gen(h.gen), kind, (unsigned)(want < cap ? want : cap), s)
                               : launch_leap_mrg_tr(*P, tmap, kind, (unsigned)(want < cap ? want : cap), s);
             } else {
             // grouped Philox, 4-byte values: TMA boxes of 32 values x 128 rows

@@ -68,7 +68,7 @@ def same(a, b):
 
 @pytest.mark.parametrize("g", list(GENS))
 @pytest.mark.parametrize("kind", ["u32", "f32", "f64"])
-@pytest.mark.parametrize("K,first,n,m", [(1, 0, 1, 1000), (3, 0, 3, 1000), (1000, 17, 300, 1024), (1000, 16, 300, 1000),
+@pytest.mark.parametrize("K,first,n,m", [(1, 0, 1, 1000), (3, 0, 3, 1000), (1000, 17, 300, 1024), (1000, 16, 300, 1000), (1024, 8, 300, 520),
                                          ((1 << 40) + 7, (1 << 39) + 5, 256, 520)])
 def test_leapfrog_fill_matches_oracle(shv, orc, g, kind, K, first, n, m):
     gen, seed = GENS[g]
