@@ -47,10 +47,11 @@ def run():
     torch.cuda.synchronize()
     shv.shv_streams_destroy(h)
     # Leap Frog players (MRG recurrence, Philox per-player and grouped, Threefry)
-    for gen, seed, K in ((W.MRG32K3A, [12345], 77), (W.PHILOX4X32_10, [5], 77), (W.PHILOX4X32_10, [5], 76),
-                         (W.THREEFRY4X64_20, [1, 2], 77)):
+    for gen, seed, K, first in ((W.MRG32K3A, [12345], 77, 5), (W.PHILOX4X32_10, [5], 77, 5),
+                                (W.PHILOX4X32_10, [5], 76, 5), (W.PHILOX4X32_10, [5], 80, 8),
+                                (W.THREEFRY4X64_20, [1, 2], 77, 5), (W.THREEFRY4X64_20, [1, 2], 80, 8)):
         st = torch.empty(6 * 70, dtype=torch.int32, device="cuda") if gen == W.MRG32K3A else None
-        h = shv.shv_streams_create_leapfrog(gen, seed, K, 5, 70, st, 0, dev, None)
+        h = shv.shv_streams_create_leapfrog(gen, seed, K, first, 70, st, 0, dev, None)
         for n in (64, 13):
             for dt, fn in ((torch.int32, shv.shv_generate_u32), (torch.float64, shv.shv_generate_f64)):
                 out = torch.empty(70 * n, dtype=dt, device="cuda")
