@@ -492,6 +492,12 @@ __global__ void __launch_bounds__(kTrWarps * 32)
         const uint64_t p1 = min(P.ns, p0 + P.tr_pl);
         // words per block: 4 (Philox) or 8 (Threefry); the run starts block-aligned
         uint64_t b = (uint64_t)(((u128)(P.first + p0) + (u128)P.players * (o + t)) >> (G == kLeapPhilox ? 2 : 3));
+        // Philox: while the low counter word does not wrap within the run, round 1
+        // is hoisted (M0*b_lo by addition, M0*c0' constant; counter words 2, 3 = 0)
+        const uint64_t nblk = (p1 - p0 + 3) / 4 + 2;
+        const bool hoist = G == kLeapPhilox && (uint32_t)b <= 0xFFFFFFFFu - (uint32_t)min(nblk, (uint64_t)0xFFFFFFFFu);
+        const uint64_t q = (uint64_t)kPM0 * ((uint32_t)(b >> 32) ^ (uint32_t)P.k0);
+        uint64_t pa = (uint64_t)kPM0 * (uint32_t)b;
         for (uint64_t pc = p0; pc < p1; pc += 128) {
             if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
             __syncwarp();
@@ -500,8 +506,16 @@ __global__ void __launch_bounds__(kTrWarps * 32)
                 const uint32_t rb = box + q8 * 128u;
                 uint32_t z[8];
                 if constexpr (G == kLeapPhilox) {
-                    const W4 v0 = philox_blk(b, 0, (uint32_t)P.k0, (uint32_t)P.k1);
-                    const W4 v1 = philox_blk(b + 1, 0, (uint32_t)P.k0, (uint32_t)P.k1);
+                    W4 v0, v1;
+                    if (hoist) {
+                        v0 = philox10_from_r2(pa, q, 0u, 0u, (uint32_t)P.k0, (uint32_t)P.k1);
+                        pa = add64w(pa, kPM0);
+                        v1 = philox10_from_r2(pa, q, 0u, 0u, (uint32_t)P.k0, (uint32_t)P.k1);
+                        pa = add64w(pa, kPM0);
+                    } else {
+                        v0 = philox_blk(b, 0, (uint32_t)P.k0, (uint32_t)P.k1);
+                        v1 = philox_blk(b + 1, 0, (uint32_t)P.k0, (uint32_t)P.k1);
+                    }
                     b += 2;
                     z[0] = v0.x; z[1] = v0.y; z[2] = v0.z; z[3] = v0.w;
                     z[4] = v1.x; z[5] = v1.y; z[6] = v1.z; z[7] = v1.w;

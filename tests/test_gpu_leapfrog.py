@@ -244,3 +244,18 @@ def test_tinymt_leapfrog_transposed_segments_sampled(shv, orc):
             same(got[rows], ref)
     finally:
         p.close()
+
+
+def test_philox_transposed_counter_wrap(shv, orc):
+    """Transposed Philox fill across a wrap of the low counter word (the
+    hoisted round-1 product is only valid without one): K = 4 players, offset
+    2^32 - 40, so lanes t = 37.. run over block 2^32."""
+    p = Players(shv, W.PHILOX4X32_10, [12345, 678], 4, 0, 4)
+    try:
+        shv.shv_jump(p.h, shv.SHV_JUMP_DRAWS, (1 << 32) - 40)
+        p.offset += (1 << 32) - 40
+        for kind in ("u32", "f32"):
+            ref = p.ref(orc, 64, kind)
+            same(p.gen_(64, kind), ref)
+    finally:
+        p.close()
