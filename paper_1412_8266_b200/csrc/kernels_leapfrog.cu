@@ -414,6 +414,13 @@ cudaError_t leap_tma_attr()
 // (12 FP64 instructions) and one shared store, against three modular
 // products per component for the per-player recurrence.
 constexpr unsigned kTrWarps = 4;
+#ifndef SHV_LEAP_CKMASK
+#define SHV_LEAP_CKMASK 22  // no three-register-pair DFMA: 4.21 -> 3.99 ms at the C5 shape (tools/lab)
+#endif
+// FP64 step constants from constant memory (bit i of SHV_LEAP_CKMASK) or the
+// launch parameters, as in kernels_mrg.cu (operand placement).
+__constant__ double c_leap_fpk[6] = {6755399441055744.0, 1.0 / 4294967087.0, 0x1.000059451f212p-32,
+                                     4294967087.0, 4294944443.0, 5886603609186927.0};
 template <int KIND>
 __global__ void __launch_bounds__(kTrWarps * 32)
     leap_mrg_tr_kernel(const __grid_constant__ LeapLaunch P, const __grid_constant__ CUtensorMap tmap)
@@ -422,7 +429,9 @@ __global__ void __launch_bounds__(kTrWarps * 32)
     const unsigned lane = threadIdx.x & 31, warp = __shfl_sync(0xffffffffu, threadIdx.x >> 5, 0);
     const uint32_t base = ((uint32_t)__cvta_generic_to_shared(tr_smem) + 1023u) & ~1023u;
     const uint32_t box = base + warp * 16384u;
-    const MrgFpK K{P.fpk[0], P.fpk[1], P.fpk[2], P.fpk[3], P.fpk[4], P.fpk[5]};
+#define SHV_TRF(i) (((SHV_LEAP_CKMASK >> (i)) & 1) ? c_leap_fpk[i] : P.fpk[i])
+    const MrgFpK K{SHV_TRF(0), SHV_TRF(1), SHV_TRF(2), SHV_TRF(3), SHV_TRF(4), SHV_TRF(5)};
+#undef SHV_TRF
     // swizzled offset of word `lane` in a box row r: depends on r & 7 only
     uint32_t off[8];
 #pragma unroll
