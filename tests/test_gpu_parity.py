@@ -551,3 +551,30 @@ def test_index_space_extremes(shv, orc, gen, seed, spacing, first, ns, jumps, m)
             shv.shv_generate_u32(h, out, 64, None)
         assert e.value.status == shv.SHV_ERR_INVALID_ARGUMENT
     shv.shv_streams_destroy(h)
+
+
+def _full_compare(shv, orc, w, kind):
+    """Every value of a BASELINE full-size workload against the oracle, in
+    2^16-stream chunks (device -> host copy per chunk; the oracle on all host
+    cores)."""
+    fam = Fam(shv, w.gen, w.seed, w.n_streams, w.spacing, w.first)
+    dt, ndt = (torch.int32, np.uint32) if kind == 0 else (torch.float64, np.float64)
+    out = torch.empty(w.n_streams * w.n, dtype=dt, device="cuda")
+    (shv.shv_generate_u32 if kind == 0 else shv.shv_generate_f64)(fam.h, out, w.n, None)
+    torch.cuda.synchronize()
+    rows = out.view(w.n_streams, w.n)
+    step = 1 << 16
+    for s0 in range(0, w.n_streams, step):
+        got = rows[s0:s0 + step].cpu().numpy().view(ndt)
+        want = orc.generate(w.gen, list(w.seed), step, w.n, first=w.first + s0, spacing=w.spacing, kind=kind)
+        assert np.array_equal(got.view(np.uint8), np.ascontiguousarray(want).view(np.uint8)), (w.name, kind, s0)
+    fam.close()
+    del out
+
+
+@pytest.mark.parametrize("w,kind", [(W.C3, 0), (W.C3, 2), (W.C5_PHILOX, 0)], ids=["c3-u32", "c3-f64", "c5-philox-u32"])
+def test_full_size_every_value(shv, orc, w, kind):
+    """C3 (2^20 MRG32k3a substreams x 4096, u32 and f64) and the C5 Philox
+    rank-0 slice (2^20 counter-streams x 4096): all 2^32 values of each,
+    element by element, in the launch configuration bench.py times."""
+    _full_compare(shv, orc, w, kind)
