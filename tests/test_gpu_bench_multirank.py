@@ -38,3 +38,33 @@ def test_two_rank_bench_small(orc):
         ns, samples = 1 << 14, 1 << 12
         tot, _ = orc.mc_count(w.gen, list(w.seed), ns, samples, spacing=w.spacing)
         assert d["parts"][key]["hits"] == tot, key
+
+
+def test_single_rank_bench_contract_small():
+    """The one JSON line of the default (N = 1) bench path, small shapes: every
+    key of the contract, the binding roofline with the HBM figure beside it,
+    the oracle baseline and the end-to-end figure through host buffers."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    out = subprocess.run([sys.executable, "bench.py", "--steps", "3", "--warmup", "3", "--small"], cwd=ROOT,
+                         capture_output=True, text=True, timeout=900)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, out.stdout
+    d = json.loads(lines[0])
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
+              "scaling", "vs_baseline", "dtype", "data", "config", "roofline", "cpu_baseline", "e2e",
+              "gpu_launches", "clocks"):
+        assert k in d, k
+    assert d["n_gpus"] == 1 and d["steps"] == 3 and d["warmup"] == 3 and d["value"] > 0
+    assert d["higher_is_better"] is True and d["scaling"] == "weak" and d["dtype"] == "u32"
+    assert "workload" in d["config"] and d["gpu_launches"] == 3 * 3
+    r = d["roofline"]
+    assert r["bound"] in ("alu", "hbm") and 0 < r["frac"] and r["achieved"] > 0 and r["peak"] > 0
+    if r["bound"] == "alu":
+        assert r["hbm"]["bound"] == "hbm" and r["hbm"]["unit"] == "GB/s"
+    c = d["cpu_baseline"]
+    assert c["kind"] == "oracle" and c["cores"] >= 1 and c["value"] > 0 and c["sample"]
+    e = d["e2e"]
+    assert e["value"] > 0 and e["h2d_bytes_per_step"] == 0 and e["d2h_bytes_per_step"] > 0
+    assert "sm_mhz" in d["clocks"] and "reasons" in d["clocks"]
