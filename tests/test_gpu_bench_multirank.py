@@ -65,6 +65,7 @@ def test_single_rank_bench_contract_small():
         assert r["hbm"]["bound"] == "hbm" and r["hbm"]["unit"] == "GB/s"
     c = d["cpu_baseline"]
     assert c["kind"] == "oracle" and c["cores"] >= 1 and c["value"] > 0 and c["sample"]
+    assert c["single_thread"]["cores"] == 1 and c["single_thread"]["value"] > 0
     e = d["e2e"]
     assert e["value"] > 0 and e["h2d_bytes_per_step"] == 0 and e["d2h_bytes_per_step"] > 0
     assert "sm_mhz" in d["clocks"] and "reasons" in d["clocks"]
