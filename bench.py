@@ -63,6 +63,20 @@ def traffic_from_profiles(kernel_key):
     return None
 
 
+def profile_record(kernel_key):
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if not os.path.exists(p):
+        return None
+    return json.load(open(p)).get(kernel_key)
+
+
+# Issue roofline of the compute-bound kernels ("for the compute-bound
+# MC pi, the percentage is of the integer-pipe / issue roofline"): 148 SMs x 4
+# schedulers x 1 warp instruction per clock at the 1965 MHz maximum SM clock
+# (B200_PROFILING.md) = 1.163 T warp instructions/s.
+ISSUE_PEAK = 148 * 4 * 1.965e9
+
+
 def limiter_from_profiles(kernel_key):
     """What ncu says binds the kernel (profiles/ncu_traffic.json), for the reader."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
@@ -73,7 +87,10 @@ def limiter_from_profiles(kernel_key):
         return None
     pipes = {"fp64": v.get("fp64_pipe_pct"), "fma_heavy": v.get("fmaheavy_pipe_pct"),
              "alu": v.get("alu_pipe_pct"), "issue": v.get("issue_active_pct")}
-    top = max((k for k in pipes if pipes[k] is not None), key=lambda k: pipes[k])
+    pipes = {k: x for k, x in pipes.items() if isinstance(x, (int, float)) and x == x}
+    if not pipes:
+        return None
+    top = max(pipes, key=lambda k: pipes[k])
     return f"ncu: {top} {pipes[top]:.0f}% busy ({', '.join(f'{k} {x:.0f}%' for k, x in pipes.items() if x is not None)})"
 
 
@@ -156,6 +173,28 @@ def cpu_baseline(threads):
                               "sample": _sample_desc(k1, 1), "seconds": round(t1, 3)}}
 
 
+def _oracle_mc(k: int, threads: int) -> tuple:
+    """Oracle dartboard counts (C4 shape: 2^18 samples per stream) on the first
+    k streams of each generator; returns (seconds, samples)."""
+    import oracle
+    t = time.perf_counter()
+    for w in (W.C4_MRG, W.C4_PHILOX):
+        oracle.mc_count(w.gen, list(w.seed), k, w.n, spacing=w.spacing, nthreads=threads)
+    return time.perf_counter() - t, 2 * k * W.C4_MRG.n
+
+
+def cpu_baseline_mc(threads):
+    """the oracle on a C4 subset (1024 streams), on all host threads
+    and single-threaded (on 32 streams)."""
+    t, ns = _oracle_mc(1024, threads)
+    t1, ns1 = _oracle_mc(32, 1)
+    desc = "first {k} of 2^20 streams x 2^18 samples, MRG32k3a and Philox4x32-10 (C4 subset), {t} threads"
+    return {"value": ns / t / 1e9, "unit": "Gsamples/s", "cores": threads, "kind": "oracle",
+            "sample": desc.format(k=1024, t=threads), "seconds": round(t, 3),
+            "single_thread": {"value": ns1 / t1 / 1e9, "unit": "Gsamples/s", "cores": 1,
+                              "sample": desc.format(k=32, t=1), "seconds": round(t1, 3)}}
+
+
 def run_reference(args, rank, world):
     """--impl reference: the oracle, as it stands, on the host cores; rank 0 only."""
     if rank != 0:
@@ -206,6 +245,12 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # under torchrun the process group (and the Monte Carlo all_reduce) is set
+    # up even at world size 1, so the NCCL path runs on a one-GPU box too;
+    # NCCL's init log (nranks, transports, NVLS) stays on stderr
+    launched = "TORCHELASTIC_RUN_ID" in os.environ or world > 1
+    if launched and args.backend == "nccl":
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
     if args.impl == "reference":
         return run_reference(args, rank, world)
 
@@ -217,7 +262,7 @@ def main():
     local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
+    if launched:
         if args.backend == "nccl":
             dist.init_process_group("nccl", device_id=dev)
         else:
@@ -305,23 +350,20 @@ def main():
            "traffic": traffic_from_profiles(dom),
            "limiter": limiter_from_profiles(dom),
            "algorithmic_bytes_per_launch": alg_bytes}
+    # the metric's roofline is the HBM write of 4 B per number (0 B
+    # read) for the dominant kernel. What ncu says keeps the kernel from it (the
+    # step's pipe mix and issue rate, profiles/ncu_traffic.json) is in `limiter`
+    # and `pipes`; the MRG32k3a step is compute-bound at ~16 issue slots per
+    # number.
+    rec = profile_record(dom) or {}
+    hbm["pipes"] = {k: rec.get(k) for k in ("issue_active_pct", "fp64_pipe_pct", "fmaheavy_pipe_pct",
+                                              "alu_pipe_pct") if rec.get(k) is not None}
+    if rec.get("inst_per_unit"):
+        hbm["issue"] = {"inst_per_number": round(rec["inst_per_unit"], 3),
+                        "achieved": round(rec["inst_per_unit"] * total_per_rank / 32 / (kms[dom] * 1e-3) / 1e12, 4),
+                        "peak": round(ISSUE_PEAK / 1e12, 4), "unit": "T warp instr/s",
+                        "frac": round(rec["inst_per_unit"] * total_per_rank / 32 / (kms[dom] * 1e-3) / ISSUE_PEAK, 4)}
     roof = hbm
-    # The MRG32k3a fill binds on the FP64 pipe before it reaches the HBM-write
-    # roofline (DESIGN.md §4.2/§4.5; ncu: fp64 pipe ~76 %, DRAM ~56 %): 12 FP64
-    # instructions per number (SASS count of the step) cap it at 18.61/12 =
-    # 1.55 T numbers/s = 6.2 TB/s, below the 6.55 TB/s copy peak. Peak from unit
-    # counts and clock (B200_PROFILING: 148 SMs, 1965 MHz max; 64 FP64
-    # instructions per SM per clock, measured 62.3 by tools/lab/fp64_lab.cu).
-    # The top-level roofline is the binding one ("whichever binds", north star);
-    # the HBM figure stays beside it.
-    if dom == "mrg":
-        fp64_peak = 148 * 64 * 1.965e9 / 1e12  # T FP64 instructions / s
-        fp64_ach = 12 * total_per_rank / (kms["mrg"] * 1e-3) / 1e12
-        roof = {"bound": "alu", "pipe": "fp64", "kernel": hbm["kernel"], "achieved": round(fp64_ach, 2),
-                "peak": round(fp64_peak, 2), "unit": "T instr/s", "frac": round(fp64_ach / fp64_peak, 4),
-                "peak_source": "unit counts x clock: 148 SMs x 64 FP64/clk x 1.965 GHz (measured 18.12, fp64_lab)",
-                "per_number": "12 FP64 instructions (SASS of mrg_fill_tma_kernel<u32>)",
-                "traffic": hbm["traffic"], "limiter": hbm["limiter"], "hbm": hbm}
     parts = {k: {"ms": round(kms[k], 4), "Gnumbers_per_s": round(total_per_rank / (kms[k] * 1e-3) / 1e9, 1),
                  "GB_per_s": round(alg_bytes / (kms[k] * 1e-3) / 1e9, 1),
                  "frac_of_hbm_peak": round(alg_bytes / (kms[k] * 1e-3) / 1e9 / peak, 4)}
@@ -343,8 +385,8 @@ def main():
                 a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 a.record(stream)
                 shv.shv_mc_pi(h, ws.n, hits, sp)
-                if world > 1:
-                    dist.all_reduce(hits)
+                if launched:
+                    dist.all_reduce(hits)  # NCCL: one int64 per rank
                 b.record(stream)
                 barrier()
                 shv.shv_streams_destroy(h)
@@ -355,11 +397,26 @@ def main():
             p = 221069946527026 / 2 ** 48
             pi_hat = 4 * tot / N
             t_ms = min(times)
-            parts["mc_pi_" + ("mrg" if w.gen == W.MRG32K3A else "philox")] = {
+            key = "mc_pi_" + ("mrg" if w.gen == W.MRG32K3A else "philox")
+            parts[key] = {
                 "ms": round(t_ms, 3), "Gsamples_per_s": round(N / (t_ms * 1e-3) / 1e9, 1),
                 "Gnumbers_per_s": round(2 * N / (t_ms * 1e-3) / 1e9, 1), "hits": tot,
                 "pi_hat": pi_hat, "within_4sigma": abs(pi_hat - math.pi) <= 4 * 4 * math.sqrt(p * (1 - p) / N),
                 "scaling": "strong", "samples": N}
+            # compute-bound (0 B per sample): issue roofline from the kernel's
+            # instructions per sample (ncu, profiles/ncu_traffic.json) and the
+            # time per sample measured here; per-pipe busy fractions beside it
+            rec = profile_record(key.replace("mc_pi_", "mc_"))
+            if rec and rec.get("inst_per_unit"):
+                ach = rec["inst_per_unit"] * (N / world) / 32 / (t_ms * 1e-3)
+                parts[key]["roofline"] = {
+                    "bound": "issue", "achieved": round(ach / 1e12, 4), "peak": round(ISSUE_PEAK / 1e12, 4),
+                    "unit": "T warp instr/s", "frac": round(ach / ISSUE_PEAK, 4),
+                    "inst_per_sample": round(rec["inst_per_unit"], 3),
+                    "peak_source": "148 SMs x 4 schedulers x 1 warp instr/clk x 1.965 GHz (B200_PROFILING.md)",
+                    "pipes": {k: rec.get(k) for k in ("issue_active_pct", "fp64_pipe_pct", "fmaheavy_pipe_pct",
+                                                      "alu_pipe_pct") if rec.get(k) is not None},
+                    "limiter": limiter_from_profiles(key.replace("mc_pi_", "mc_"))}
             del st
         ws = W.rank_slice(shrink(W.C3), rank, world, weak=True)
         out64 = out.view(torch.float64)[: ws.n_streams * ws.n // 2]
@@ -511,15 +568,21 @@ def main():
     # ---- e2e: same workload through shv_generate_u32_host into pinned host memory ----
     e2e = None
     if not args.no_e2e:
-        host = torch.empty(total_per_rank, dtype=torch.int32, pin_memory=True)
+        # bounded pinned memory per rank: the rows go out in slices of at most
+        # 2 GiB (2^17 streams), each slice a handle over its stream range
+        # (first_stream) written into the same pinned buffer
+        slice_streams = max(1, min(wm.n_streams, (2 << 30) // (4 * n)))
+        host = torch.empty(slice_streams * n, dtype=torch.int32, pin_memory=True)
         e2e_steps = min(args.steps, 3)
 
         def step_host():
             for w, stt in ((wm, state), (wp, None)):
-                h = shv.shv_streams_create_ex(w.gen, list(w.seed), w.first, w.n_streams, w.spacing,
-                                              stt, 0, local, sp)
-                shv.shv_generate_u32_host(h, host, n, sp)
-                shv.shv_streams_destroy(h)
+                for s0 in range(0, w.n_streams, slice_streams):
+                    ns_ = min(slice_streams, w.n_streams - s0)
+                    h = shv.shv_streams_create_ex(w.gen, list(w.seed), w.first + s0, ns_, w.spacing,
+                                                  stt, 0, local, sp)
+                    shv.shv_generate_u32_host(h, host, n, sp)
+                    shv.shv_streams_destroy(h)
         step_host()
         barrier()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -532,15 +595,19 @@ def main():
         e2e = {"value": 2 * total_per_rank * world * e2e_steps / (e_ms * 1e-3) / 1e9, "unit": UNIT,
                "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 2 * 4 * total_per_rank,
                "steps": e2e_steps, "api": "shv_generate_u32_host (pinned host buffer)",
+               "pinned_bytes_per_rank": slice_streams * n * 4,
                "note": "inputs are seed words passed as call arguments; no input tensor is copied"}
         del host
 
     if rank == 0:
         cpu = None
-        if world == 1 and not args.no_cpu:
+        if not args.no_cpu:
             import oracle
             oracle.build()
-            cpu = cpu_baseline(len(os.sched_getaffinity(0)))
+            threads = len(os.sched_getaffinity(0))
+            cpu = cpu_baseline(threads)
+            if not args.no_parts:
+                cpu["mc_pi"] = cpu_baseline_mc(threads)
         line = {"metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 4),
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
@@ -553,7 +620,7 @@ def main():
                 "gpu_launches": 3 * args.steps, "clocks": clk, "parts": parts,
                 "per_gpu_Gnumbers_per_s": round(value / world, 2)}
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if launched:
         dist.destroy_process_group()
 
 

@@ -137,11 +137,18 @@ shv_status shv_streams_create_ex(shv_streams* out, int gen, const uint32_t* seed
                                  int spacing, void* d_state, size_t state_bytes, int device,
                                  void* cuda_stream);
 
-/* Advance every stream of the handle (host-side only; S L157-174):
- * kind = SHV_JUMP_DRAWS / SUBSTREAMS / STREAMS, see shv_jump_kind.
+/* Advance every stream of the handle by n draws, substreams or streams
+ * (jump-ahead, P L112-117 [§2.3]; S L157-174): kind = SHV_JUMP_DRAWS /
+ * SUBSTREAMS / STREAMS, see shv_jump_kind. Stream-ordered on cuda_stream like
+ * generate: for MRG32k3a, Philox, Threefry and every Leap Frog handle the jump
+ * is host-side only (the handle's offset; the next launch starts there); for
+ * the stateful TinyMT32 and MTGP32 handles the state buffer is advanced by a
+ * kernel enqueued on cuda_stream, ordered with the caller's generate / mc_pi
+ * calls on that stream (TinyMT32: any n, by the jump polynomial x^n mod the
+ * minimal polynomial of each group's transition; MTGP32: sequential steps).
  * Errors: UNSUPPORTED for Philox sub/streams; INVALID_ARGUMENT if the offset
  * would leave the stream (Philox 2^66 draws; MRG offset beyond 2^128). */
-shv_status shv_jump(shv_streams h, int kind, uint64_t n);
+shv_status shv_jump(shv_streams h, int kind, uint64_t n, void* cuda_stream);
 
 /* TinyMT32 handles (NEXT-3; P L287-317 [§4.2]; R15) — the paper's hybrid:
  * one Dynamic Creator parameter set per group of group_size streams ("the
@@ -155,7 +162,7 @@ shv_status shv_jump(shv_streams h, int kind, uint64_t n);
  *    built on the device at create).
  *  d_state: 16*n_streams bytes (SoA, four words per stream) or NULL.
  * The handle is stateful: generate/mc_pi advance the state buffer in place;
- * shv_jump(DRAWS, n <= 2^32) advances sequentially on cuda_stream (S L355).
+ * shv_jump(DRAWS, n) advances the states on the jump's cuda_stream.
  * TinyMT f64 values use two draws, like Philox (R7). Errors: params NULL or
  * n_params 0 -> SHV_ERR_MISSING_PARAMETERS; groups beyond n_params ->
  * SHV_ERR_INSUFFICIENT_STREAMS. Host-synchronous (waits for seeding). */

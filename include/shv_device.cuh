@@ -2,20 +2,18 @@
 // (arXiv 1412.8266) for sm_100a. Included by the kernels_*.cu files (and by the
 // kernel lab under tools/lab/, which times variants of the same functions).
 //
-// Pipe budget on B200 (measured, profiles/r01_microbench.json): IMAD.WIDE.U32
-// occupies the FMA-heavy pipe for 4 cycles per warp (IMAD/IADD3/LOP3: 2), and
-// the FP64 pipe (DFMA/DADD/DMUL: 2 cycles per warp) is otherwise idle. The
-// MRG32k3a step below therefore splits its two components across pipes:
-// component 1 in 32-bit integer arithmetic (FMA-heavy + ALU), component 2 in
-// exact binary64 arithmetic (FP64 pipe), as in L'Ecuyer's original
-// floating-point formulation [LEcuyer1999] (products < 2^53, exact).
+// Pipe budget on B200 (measured, profiles/r01_microbench.json): the FMA-heavy
+// pipe runs IMAD at 64 and IMAD.WIDE.U32 at ~32 per SM per clock, the ALU pipe
+// (IADD3/LOP3/ISETP) 64, the FP64 pipe (DFMA/DADD/DMUL) 64, issue 128. The
+// product's MRG32k3a step (MrgIF) therefore splits its two components across
+// pipes: component 1 in 32-bit integer arithmetic (two IMAD.WIDE + one IMAD on
+// the FMA-heavy pipe, the fold's compare/select on the ALU), component 2 in
+// exact binary64 arithmetic on the FP64 pipe, as in L'Ecuyer's original
+// floating-point formulation [LEcuyer1999] (products < 2^53, exact). Each of
+// the three pipes carries ~12 cycles per warp and number.
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
-
-#ifndef SHV_DECODE_PRED
-#define SHV_DECODE_PRED 1
-#endif
 
 namespace shv {
 namespace dev {
@@ -89,29 +87,55 @@ __device__ __forceinline__ void apply(const uint32_t* a, const uint32_t* b, Mrg&
     matvec<kC2>(b, s.y0, s.y1, s.y2);
 }
 
-// Component 1, integer: P = a12*x1 + a13n*(m1-x0) < 2^53.06, split at bit
-// 32 as (H, L). U = (H+1)*209 + L < 2^33 is congruent to P + 209 and U >= 209,
-// so P mod m1 = U - 2^32 if U >= 2^32, else U - 209. The +1 on H comes for
-// free by adding 2^32 to P; U's carry bit is read off a single IMAD.WIDE
-// v = H'*209 + (H':L) = U + H'*2^32 as v.hi != H'. (DESIGN.md §4.2.)
-__device__ __forceinline__ uint32_t mrg_c1(uint32_t x0, uint32_t x1)
+// Constants of the step. The kernels pass a copy read from their launch
+// parameters (or constant memory), so ptxas cannot constant-fold them: the
+// integer multipliers then stay plain IMAD.WIDE operands (with immediates
+// ptxas strength-reduces a13n*(m1 - x0) into IMAD/IMAD.HI/IADD3.X chains, 26
+// instead of 16 issue slots per number), and the non-immediate doubles stay
+// in (uniform) registers instead of being re-materialised inside the loop.
+// The device API (shv_rng.cuh) uses mrg_fpk() (immediates: same values).
+struct MrgFpK {
+    double magic;   // 1.5 * 2^52: ulp 1 on [2^52, 2^53)
+    double inv1;    // RN(1/m1) = 1/m1 + delta1, 0 < delta1 < 0.34 ulp
+    double inv2;    // RU(1/m2) = 1/m2 + delta2, 0 < delta2 < 0.54 ulp
+    double m1, m2;
+    double a23n_m2; // a23n * m2 = 5886603609186927, exact
+    uint32_t a12, a13n;  // component-1 multipliers for the integer half-step
+};
+__host__ __device__ __forceinline__ constexpr MrgFpK mrg_fpk()
+{
+    return MrgFpK{6755399441055744.0, 1.0 / (double)kM1, 0x1.000059451f212p-32,
+                  (double)kM1, (double)kM2, (double)kA23n * (double)kM2, kA12, kA13n};
+}
+
+// Component 1, integer: x_{1,n} = (a12 x_{1,n-2} - a13n x_{1,n-3}) mod m1 for
+// canonical x0 = x_{1,n-3}, x1 = x_{1,n-2} < m1:
+//   P = a12*x1 + a13n*(m1 - x0) <= 2214308*m1 < 2^53.1 (two IMAD.WIDE.U32),
+//   P = H*2^32 + L with H <= 2214307, so 209*H < 2^28.8;
+//   V = L + 209*H == P (mod m1, 2^32 = 209), V < 2^32 + 2^28.8;
+//   u = V mod 2^32 (one 32-bit IMAD); V >= 2^32 exactly when u < L;
+//   if V >= 2^32: V - m1 = u + 209 (< m1); else if u >= m1: u - m1 = u + 209
+//   (mod 2^32); else u. So p1 = (u < L or u >= m1) ? u + 209 : u.
+// Bounds pinned in tests/test_fp64_step_bounds.py. a12, a13n arrive in
+// registers (MrgFpK): 7 instructions, 2 IMAD.WIDE + IMAD + 4 ALU-class.
+__device__ __forceinline__ uint32_t mrg_c1_int(uint32_t x0, uint32_t x1, uint32_t a12, uint32_t a13n)
 {
     uint32_t r;
     asm("{\n\t"
-        ".reg .u64 q, v;\n\t"
-        ".reg .u32 t, l, h, vh;\n\t"
+        ".reg .u64 q;\n\t"
+        ".reg .u32 t, l, h;\n\t"
         ".reg .pred c;\n\t"
-        "mad.wide.u32 q, %2, 1403580, 4294967296;\n\t"  // a12*x1 + 2^32
-        "sub.u32 t, 4294967087, %1;\n\t"                // m1 - x0
-        "mad.wide.u32 q, t, 810728, q;\n\t"             // P + 2^32 = (H+1, L)
+        "sub.u32 t, 4294967087, %1;\n\t"          // m1 - x0
+        "mul.wide.u32 q, %2, %3;\n\t"             // a12*x1
+        "mad.wide.u32 q, t, %4, q;\n\t"           // P = (H, L)
         "mov.b64 {l, h}, q;\n\t"
-        "mad.wide.u32 v, h, 209, q;\n\t"                // U + (H+1)*2^32
-        "mov.b64 {%0, vh}, v;\n\t"
-        "setp.ne.u32 c, vh, h;\n\t"                     // U >= 2^32
-        "@!c sub.u32 %0, %0, 209;\n\t"
+        "mad.lo.u32 %0, h, 209, l;\n\t"           // u = L + 209*H mod 2^32
+        "setp.lt.u32 c, %0, l;\n\t"               // V >= 2^32
+        "setp.ge.or.u32 c, %0, 4294967087, c;\n\t"
+        "@c add.u32 %0, %0, 209;\n\t"
         "}"
         : "=r"(r)
-        : "r"(x0), "r"(x1));
+        : "r"(x0), "r"(x1), "r"(a12), "r"(a13n));
     return r;
 }
 
@@ -139,9 +163,10 @@ __device__ __forceinline__ uint32_t mrg_combine(uint32_t p1, uint32_t p2)
     return z;
 }
 
-__device__ __forceinline__ uint32_t mrg_next(Mrg& s)
+// All-integer step (reference; the lab's variant 0).
+__device__ __forceinline__ uint32_t mrg_next(Mrg& s, const MrgFpK& K = mrg_fpk())
 {
-    const uint32_t p1 = mrg_c1(s.x0, s.x1);
+    const uint32_t p1 = mrg_c1_int(s.x0, s.x1, K.a12, K.a13n);
     s.x0 = s.x1;
     s.x1 = s.x2;
     s.x2 = p1;
@@ -150,83 +175,6 @@ __device__ __forceinline__ uint32_t mrg_next(Mrg& s)
     s.y1 = s.y2;
     s.y2 = p2;
     return mrg_combine(p1, p2);
-}
-
-// One component on the FP64 pipe. The state holds *signed* residues
-// y in (-m/2 - 2, m/2 + 2) (or canonical ones, < 2^32, right after a jump):
-// p = a*yb - b*yc is exact (|p| < 2^52.4). k' = fma(p, RN(1/m), 1.5*2^52)
-// rounds p/m to the nearest integer k = k' - 1.5*2^52 with
-// |p/m - k| <= 1/2 + 2^-31, so r = fma(-k, m, p) is exact, congruent to the
-// next value, and |r| <= m/2 + 2. The canonical output in [0, m) is the low
-// word of r + 1.5*2^52 (= r mod 2^32: the sum lies in [2^52, 2^53), where the
-// ulp is 1), plus m when r < 0 (sign bit of that word). 6 FP64 operations.
-template <uint32_t M, uint32_t A, uint32_t B>
-__device__ __forceinline__ uint32_t mrg_fp64(double yb, double yc, double& r_out)
-{
-    const double kMagic = 6755399441055744.0;  // 1.5 * 2^52
-    const double t = __dmul_rn((double)B, yc);
-    const double p = __fma_rn((double)A, yb, -t);
-    const double k = __dadd_rn(__fma_rn(p, 1.0 / (double)M, kMagic), -kMagic);
-    const double r = __fma_rn(-k, (double)M, p);
-    r_out = r;
-    const uint32_t w = (uint32_t)__double2loint(__dadd_rn(r, kMagic));  // r mod 2^32
-#if SHV_DECODE_PRED
-    uint32_t c = w;
-    asm("{\n\t.reg .pred n;\n\tsetp.lt.s32 n, %0, 0;\n\t@n add.u32 %0, %0, %1;\n\t}" : "+r"(c) : "n"(M));
-    return c;
-#else
-    return w + ((uint32_t)((int32_t)w >> 31) & M);  // + m if r < 0 (sign mask, no predicate)
-#endif
-}
-
-// Component 2: y_n = a21 y_{n-1} - a23n y_{n-3} (mod m2).
-__device__ __forceinline__ uint32_t mrg_c2_fp64(double y0, double y2, double& r_out)
-{
-    return mrg_fp64<kM2, kA21, kA23n>(y2, y0, r_out);
-}
-
-// Both components on the FP64 pipe: the product's MRG32k3a step (24 issue
-// slots, 12 of them FP64, per number).
-struct MrgD {
-    double x0, x1, x2;
-    double y0, y1, y2;
-};
-
-__device__ __forceinline__ MrgD to_fp64(const Mrg& s)
-{
-    return MrgD{__uint2double_rn(s.x0), __uint2double_rn(s.x1), __uint2double_rn(s.x2),
-                __uint2double_rn(s.y0), __uint2double_rn(s.y1), __uint2double_rn(s.y2)};
-}
-
-__device__ __forceinline__ uint32_t mrg_next(MrgD& s)
-{
-    double r1, r2;
-    const uint32_t p1 = mrg_fp64<kM1, kA12, kA13n>(s.x1, s.x0, r1);  // x1,n = a12 x1,n-2 - a13n x1,n-3
-    s.x0 = s.x1;
-    s.x1 = s.x2;
-    s.x2 = r1;
-    const uint32_t p2 = mrg_c2_fp64(s.y0, s.y2, r2);
-    s.y0 = s.y1;
-    s.y1 = s.y2;
-    s.y2 = r2;
-    return mrg_combine(p1, p2);
-}
-
-// FP64 constants of the floor reductions. The kernels pass a copy read from
-// their launch parameters, so ptxas keeps them in registers instead of
-// re-materialising the non-immediate doubles inside the loop (8-14 extra
-// issue slots per 8 numbers); the device API uses mrg_fpk() (immediates).
-struct MrgFpK {
-    double magic;   // 1.5 * 2^52: ulp 1 on [2^52, 2^53)
-    double inv1;    // RN(1/m1) = 1/m1 + delta1, 0 < delta1 < 0.34 ulp
-    double inv2;    // RU(1/m2) = 1/m2 + delta2, 0 < delta2 < 0.54 ulp
-    double m1, m2;
-    double a23n_m2; // a23n * m2 = 5886603609186927, exact
-};
-__host__ __device__ __forceinline__ constexpr MrgFpK mrg_fpk()
-{
-    return MrgFpK{6755399441055744.0, 1.0 / (double)kM1, 0x1.000059451f212p-32,
-                  (double)kM1, (double)kM2, (double)kA23n * (double)kM2};
 }
 
 // Component 2 on the FP64 pipe with a floor reduction, no decode. For a
@@ -268,7 +216,8 @@ __device__ __forceinline__ uint32_t mrg_c1_floor(double x0, double x1, double& r
 }
 
 // Both components on the FP64 pipe with floor reductions: 12 FP64 ops and the
-// 3-instruction combine per number (no decode fix-ups).
+// 3-instruction combine per number (round-1 product step; FP64-bound at
+// 24 pipe cycles per warp and number).
 struct MrgFF {
     double x0, x1, x2;
     double y0, y1, y2;
@@ -294,11 +243,11 @@ __device__ __forceinline__ uint32_t mrg_next(MrgFF& s, const MrgFpK& K = mrg_fpk
     return mrg_combine(p1, p2);
 }
 
-// The product's MRG32k3a step: component 1 in integer arithmetic (FMA-heavy
-// + ALU: 3 IMAD.WIDE, 3 ALU), component 2 on the FP64 pipe (6 ops), combine on
-// the ALU (3) — 15 issue slots per number with the three pipes each ~12
-// cycles per warp, instead of 23.5 slots and 24 FP64 cycles for both
-// components on the FP64 pipe.
+// The product's MRG32k3a step: component 1 in integer arithmetic (mrg_c1_int:
+// 2 IMAD.WIDE + IMAD on the FMA-heavy pipe, compare/select on the ALU),
+// component 2 on the FP64 pipe (mrg_c2_floor: 6 ops), combine on the ALU (3):
+// 16 issue slots per number with the FMA-heavy, ALU and FP64 pipes each at
+// ~12 cycles per warp, instead of 24 FP64 cycles for MrgFF.
 struct MrgIF {
     uint32_t x0, x1, x2;
     double y0, y1, y2;
@@ -311,7 +260,7 @@ __device__ __forceinline__ MrgIF to_mrg_if(const Mrg& s)
 
 __device__ __forceinline__ uint32_t mrg_next(MrgIF& s, const MrgFpK& K = mrg_fpk())
 {
-    const uint32_t p1 = mrg_c1(s.x0, s.x1);
+    const uint32_t p1 = mrg_c1_int(s.x0, s.x1, K.a12, K.a13n);
     s.x0 = s.x1;
     s.x1 = s.x2;
     s.x2 = p1;

@@ -11,7 +11,7 @@
  *   }
  *   // host: h = shv_streams_create(...block_num * thread_num streams...);
  *   //       shv_get_device_view(h, &v); fooKernel<<<block_num, thread_num>>>(d, v);
- *   //       shv_jump(h, SHV_JUMP_DRAWS, draws_per_thread); ...; shv_streams_destroy(h);
+ *   //       shv_jump(h, SHV_JUMP_DRAWS, draws_per_thread, stream); ...; shv_streams_destroy(h);
  *
  * Thread i's sequence is stream i of the handle at the view's offset, value
  * for value the one shv_generate_u32/f32/f64 writes (R7, R8); the state lives

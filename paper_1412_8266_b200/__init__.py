@@ -88,7 +88,7 @@ def _load():
         "shv_streams_create": (st, [C.POINTER(u64), C.c_int, u32p, C.c_size_t, u64]),
         "shv_streams_create_ex": (st, [C.POINTER(u64), C.c_int, u32p, C.c_size_t, u64, u64,
                                        C.c_int, vp, C.c_size_t, C.c_int, vp]),
-        "shv_jump": (st, [u64, C.c_int, u64]),
+        "shv_jump": (st, [u64, C.c_int, u64, vp]),
         "shv_generate_u32": (st, [u64, vp, u64, vp]),
         "shv_generate_f32": (st, [u64, vp, u64, vp]),
         "shv_generate_f64": (st, [u64, vp, u64, vp]),
@@ -216,8 +216,8 @@ def shv_streams_create_leapfrog(gen: int, seed, players: int, first_player: int,
     return h.value
 
 
-def shv_jump(h: int, kind: int, n: int):
-    _check(lib.shv_jump(h, kind, n))
+def shv_jump(h: int, kind: int, n: int, stream=None):
+    _check(lib.shv_jump(h, kind, n, _stream(stream)))
 
 
 def shv_generate_u32(h: int, d_out, n_per_stream: int, stream=None):

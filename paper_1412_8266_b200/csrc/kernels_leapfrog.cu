@@ -430,7 +430,7 @@ __global__ void __launch_bounds__(kTrWarps * 32)
     const uint32_t base = ((uint32_t)__cvta_generic_to_shared(tr_smem) + 1023u) & ~1023u;
     const uint32_t box = base + warp * 16384u;
 #define SHV_TRF(i) (((SHV_LEAP_CKMASK >> (i)) & 1) ? c_leap_fpk[i] : P.fpk[i])
-    const MrgFpK K{SHV_TRF(0), SHV_TRF(1), SHV_TRF(2), SHV_TRF(3), SHV_TRF(4), SHV_TRF(5)};
+    const MrgFpK K{SHV_TRF(0), SHV_TRF(1), SHV_TRF(2), SHV_TRF(3), SHV_TRF(4), SHV_TRF(5), P.imul[0], P.imul[1]};
 #undef SHV_TRF
     // swizzled offset of word `lane` in a box row r: depends on r & 7 only
     uint32_t off[8];
@@ -448,7 +448,7 @@ __global__ void __launch_bounds__(kTrWarps * 32)
             if (x & 1) apply(P.segpow[b].a, P.segpow[b].b, m);
         for (uint64_t b = 0, x = ps; x; ++b, x >>= 1)
             if (x & 1) apply(P.tr_ppow[b].a, P.tr_ppow[b].b, m);
-        MrgFF g = to_mrg_ff(m);
+        MrgIF g = to_mrg_if(m);
         for (uint64_t pc = p0; pc < p1; pc += 128) {
             if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
             __syncwarp();

@@ -3,11 +3,10 @@
 // fused Monte Carlo pi kernel. Common pieces: kernels_common.cuh.
 //
 // Compile-time variants (the kernel lab, tools/lab/, builds each):
-//   SHV_MRG_STEP  0 = all-integer step, 2 = both components on the FP64 pipe,
-//                 3 = component 1 integer, component 2 FP64 with the floor
-//                 reduction (MrgIF in shv_device.cuh), 4 = both components on
-//                 the FP64 pipe with floor reductions (MrgFF; default, fastest
-//                 measured: tools/lab/step2_lab.cu), 9 = lab null generator
+//   SHV_MRG_STEP  3 (default) = component 1 in integer arithmetic, component 2
+//                 on the FP64 pipe (MrgIF in shv_device.cuh); 4 = both
+//                 components on the FP64 pipe with floor reductions (MrgFF, the
+//                 round-1 step), kept for A/B runs of the same kernels
 //   SHV_MRG_STAGE 0 = each lane stores its own row directly (32-byte vector
 //                 stores); 2 = lanes stage 256 B in shared memory and the warp
 //                 writes 256-byte runs; 1 (default) = stage the 8-byte (f64)
@@ -18,7 +17,7 @@
 #include "kernels_common.cuh"
 
 #ifndef SHV_MRG_STEP
-#define SHV_MRG_STEP 4
+#define SHV_MRG_STEP 3
 #endif
 #ifndef SHV_MRG_STAGE
 #define SHV_MRG_STAGE 1
@@ -56,33 +55,16 @@ template <int MASK>
 __device__ __forceinline__ MrgFpK load_fpk(const MrgLaunch& P)
 {
 #define SHV_CKF(i) (((MASK >> (i)) & 1) ? c_mrg_fpk[i] : P.fpk[i])
-    return MrgFpK{SHV_CKF(0), SHV_CKF(1), SHV_CKF(2), SHV_CKF(3), SHV_CKF(4), SHV_CKF(5)};
+    return MrgFpK{SHV_CKF(0), SHV_CKF(1), SHV_CKF(2), SHV_CKF(3), SHV_CKF(4), SHV_CKF(5), P.imul[0], P.imul[1]};
 #undef SHV_CKF
 }
 
-#if SHV_MRG_STEP == 9
-// Lab only: a trivial "generator" (one IADD per value) that keeps the fill
-// kernels' work split and stores, to measure the store path's ceiling.
-struct MrgNull {
-    uint32_t x;
-};
-using Gen = MrgNull;
-__device__ __forceinline__ Gen make_gen(const Mrg& s) { return MrgNull{s.x0 ^ s.y2}; }
-__device__ __forceinline__ uint32_t mrg_next(MrgNull& s, const MrgFpK&) { return s.x++; }
-#elif SHV_MRG_STEP == 4
+#if SHV_MRG_STEP == 4
 using Gen = MrgFF;
 __device__ __forceinline__ Gen make_gen(const Mrg& s) { return to_mrg_ff(s); }
-#elif SHV_MRG_STEP == 3
+#else
 using Gen = MrgIF;
 __device__ __forceinline__ Gen make_gen(const Mrg& s) { return to_mrg_if(s); }
-#elif SHV_MRG_STEP == 2
-using Gen = MrgD;
-__device__ __forceinline__ uint32_t mrg_next(MrgD& s, const MrgFpK&) { return mrg_next(s); }
-__device__ __forceinline__ Gen make_gen(const Mrg& s) { return to_fp64(s); }
-#else
-using Gen = Mrg;
-__device__ __forceinline__ uint32_t mrg_next(Mrg& s, const MrgFpK&) { return mrg_next(s); }
-__device__ __forceinline__ Gen make_gen(const Mrg& s) { return s; }
 #endif
 
 __device__ __forceinline__ Mrg load_state(const uint32_t* __restrict__ st, uint64_t stride, uint64_t i)
@@ -257,12 +239,77 @@ __global__ void __launch_bounds__(256, SHV_MRG_MINB) mrg_fill_vec_kernel(const _
 // sees the scattered 32-byte row pieces that cap per-lane STG.256 stores at
 // ~4.5 TB/s (tools/lab, null generator); boxes that run past the row end or
 // past the launch's last row are clipped by the tensor map bounds.
-template <int KIND, bool SEG_FASTEST>
-__global__ void __launch_bounds__(256, SHV_MRG_MINB)
-    mrg_fill_tma_kernel(const __grid_constant__ MrgLaunch P, const __grid_constant__ CUtensorMap tmap)
+#ifndef SHV_MRG_NBUF
+#define SHV_MRG_NBUF 1
+#endif
+#ifndef SHV_MRG_TMA_MINB
+#define SHV_MRG_TMA_MINB (SHV_MRG_STEP == 4 ? 4 : 2)
+#endif
+constexpr uint32_t kTmaBufs = SHV_MRG_NBUF;  // boxes per warp in flight (2: double buffering)
+
+// One TMA tile: rows 32g..32g+31 of the launch x segment j; lane l generates
+// row 32g + l. bsel (the warp's current box buffer) carries across tiles.
+template <int KIND>
+__device__ __forceinline__ void mrg_tma_tile(const MrgLaunch& P, const CUtensorMap* tmap, const MrgFpK& K,
+                                             unsigned lane, uint32_t box0, uint32_t& bsel, uint64_t g, uint64_t j)
 {
     using T = OutT<KIND>;
     constexpr uint32_t W = 128 / sizeof(T);  // values per row per box
+    const uint64_t i = 32 * g + lane;
+    // rows past the launch's last stream compute a clipped, discarded row
+    Gen s = item_state(P, i < P.ns ? i : P.ns - 1, j);
+    const uint64_t c0 = j * P.seg_len;
+    const uint32_t len = (uint32_t)min(P.seg_len, P.n - c0);  // warp-uniform
+    for (uint32_t r = 0; r < len; r += W) {
+        const uint32_t box = box0 + bsel * 4096u;
+        const uint32_t rowsw = box + lane * 128u + ((lane & 7u) << 4);  // ^ (q << 4) = chunk q
+#pragma unroll
+        for (unsigned q8 = 0; q8 < W / 8; ++q8) {
+            uint32_t v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) v[u] = mrg_next(s, K);
+            if (q8 == 0) {  // this buffer's previous box must have left shared memory
+                if (lane == 0) {
+                    if (kTmaBufs == 1) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+                    else asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+                }
+                __syncwarp();
+            }
+            if (KIND == kF64) {
+#pragma unroll
+                for (unsigned k = 0; k < 4; ++k) {
+                    const double a = mrg_f64(v[2 * k]), b = mrg_f64(v[2 * k + 1]);
+                    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(rowsw ^ ((4 * q8 + k) << 4)),
+                                 "r"(__double2loint(a)), "r"(__double2hiint(a)), "r"(__double2loint(b)),
+                                 "r"(__double2hiint(b))
+                                 : "memory");
+                }
+            } else {
+                const uint4 a = pack4<KIND>(v[0], v[1], v[2], v[3]), b = pack4<KIND>(v[4], v[5], v[6], v[7]);
+                asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(rowsw ^ ((2 * q8) << 4)), "r"(a.x),
+                             "r"(a.y), "r"(a.z), "r"(a.w)
+                             : "memory");
+                asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(rowsw ^ ((2 * q8 + 1) << 4)),
+                             "r"(b.x), "r"(b.y), "r"(b.z), "r"(b.w)
+                             : "memory");
+            }
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // st.shared -> async proxy
+        __syncwarp();
+        if (lane == 0) {
+            asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(tmap),
+                         "r"(box), "r"((int)(c0 + r)), "r"((int)(32 * g))
+                         : "memory");
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        }
+        bsel = kTmaBufs == 1 ? 0u : bsel ^ 1u;
+    }
+}
+
+template <int KIND, bool SEG_FASTEST>
+__global__ void __launch_bounds__(256, SHV_MRG_TMA_MINB)
+    mrg_fill_tma_kernel(const __grid_constant__ MrgLaunch P, const __grid_constant__ CUtensorMap tmap)
+{
     extern __shared__ uint8_t tma_smem[];
     const MrgFpK K = load_fpk<SHV_MRG_FILL_CKMASK>(P);
     // warp index through a shuffle from lane 0: ptxas then sees the tile loop as
@@ -271,8 +318,8 @@ __global__ void __launch_bounds__(256, SHV_MRG_MINB)
     const unsigned lane = threadIdx.x & 31, warp = __shfl_sync(0xffffffffu, threadIdx.x >> 5, 0);
     // 1024-byte aligned boxes (128-B swizzle); the launch adds 1 KB of slack
     const uint32_t base = ((uint32_t)__cvta_generic_to_shared(tma_smem) + 1023u) & ~1023u;
-    const uint32_t box = base + warp * 4096u;
-    const uint32_t rowsw = box + lane * 128u + ((lane & 7u) << 4);  // ^ (q << 4) = chunk q
+    const uint32_t box0 = base + warp * (4096u * kTmaBufs);
+    uint32_t bsel = 0;  // buffer of the box being generated
     const uint64_t G = (P.ns + 31) / 32, ntiles = G * P.nseg;
     const uint64_t wstride = (uint64_t)gridDim.x * (blockDim.x >> 5);
     for (uint64_t t = (uint64_t)blockIdx.x * (blockDim.x >> 5) + warp; t < ntiles; t += wstride) {
@@ -284,49 +331,7 @@ __global__ void __launch_bounds__(256, SHV_MRG_MINB)
             j = t / G;
             g = t - j * G;
         }
-        const uint64_t i = 32 * g + lane;
-        // rows past the launch's last stream compute a clipped, discarded row
-        Gen s = item_state(P, i < P.ns ? i : P.ns - 1, j);
-        const uint64_t c0 = j * P.seg_len;
-        const uint32_t len = (uint32_t)min(P.seg_len, P.n - c0);  // warp-uniform
-        for (uint32_t r = 0; r < len; r += W) {
-#pragma unroll
-            for (unsigned q8 = 0; q8 < W / 8; ++q8) {
-                uint32_t v[8];
-#pragma unroll
-                for (int u = 0; u < 8; ++u) v[u] = mrg_next(s, K);
-                if (q8 == 0) {  // the previous box must have left shared memory
-                    if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-                    __syncwarp();
-                }
-                if (KIND == kF64) {
-#pragma unroll
-                    for (unsigned k = 0; k < 4; ++k) {
-                        const double a = mrg_f64(v[2 * k]), b = mrg_f64(v[2 * k + 1]);
-                        asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(rowsw ^ ((4 * q8 + k) << 4)),
-                                     "r"(__double2loint(a)), "r"(__double2hiint(a)), "r"(__double2loint(b)),
-                                     "r"(__double2hiint(b))
-                                     : "memory");
-                    }
-                } else {
-                    const uint4 a = pack4<KIND>(v[0], v[1], v[2], v[3]), b = pack4<KIND>(v[4], v[5], v[6], v[7]);
-                    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(rowsw ^ ((2 * q8) << 4)), "r"(a.x),
-                                 "r"(a.y), "r"(a.z), "r"(a.w)
-                                 : "memory");
-                    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(rowsw ^ ((2 * q8 + 1) << 4)),
-                                 "r"(b.x), "r"(b.y), "r"(b.z), "r"(b.w)
-                                 : "memory");
-                }
-            }
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // st.shared -> async proxy
-            __syncwarp();
-            if (lane == 0) {
-                asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(&tmap),
-                             "r"(box), "r"((int)(c0 + r)), "r"((int)(32 * g))
-                             : "memory");
-                asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-            }
-        }
+        mrg_tma_tile<KIND>(P, &tmap, K, lane, box0, bsel, g, j);
     }
     if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
@@ -415,11 +420,32 @@ cudaError_t launch_vec(const MrgLaunch& p, Grid g, cudaStream_t s)
 
 }  // namespace
 
-size_t mrg_fill_tma_smem(int threads) { return (size_t)(threads / 32) * 4096 + 1024; }
+size_t mrg_fill_tma_smem(int threads) { return (size_t)(threads / 32) * 4096 * kTmaBufs + 1024; }
+
+namespace {
+// Opt the TMA fills into their dynamic shared memory (> 48 KB with two
+// boxes per warp) once per device.
+cudaError_t ensure_tma_smem(int threads)
+{
+    const size_t sm = mrg_fill_tma_smem(threads);
+    static std::atomic<uint64_t> d[6];
+    cudaError_t e = ensure_dyn_smem(mrg_fill_tma_kernel<kU32, false>, sm, d[0]);
+    if (e == cudaSuccess) e = ensure_dyn_smem(mrg_fill_tma_kernel<kU32, true>, sm, d[1]);
+    if (e == cudaSuccess) e = ensure_dyn_smem(mrg_fill_tma_kernel<kF32, false>, sm, d[2]);
+    if (e == cudaSuccess) e = ensure_dyn_smem(mrg_fill_tma_kernel<kF32, true>, sm, d[3]);
+    if (e == cudaSuccess) e = ensure_dyn_smem(mrg_fill_tma_kernel<kF64, false>, sm, d[4]);
+    if (e == cudaSuccess) e = ensure_dyn_smem(mrg_fill_tma_kernel<kF64, true>, sm, d[5]);
+    return e;
+}
+}  // namespace
+
+bool mrg_fill_tma_fits(int threads) { return mrg_fill_tma_smem(threads) <= 227u * 1024u; }
 
 cudaError_t launch_mrg_fill_tma(const MrgLaunch& p, const CUtensorMap& tmap, int kind, Grid g, cudaStream_t s)
 {
     const size_t sm = mrg_fill_tma_smem((int)g.threads);
+    const cudaError_t e = ensure_tma_smem((int)g.threads);
+    if (e != cudaSuccess) return e;
     if (kind == kF64) {
         if (p.seg_fastest) mrg_fill_tma_kernel<kF64, true><<<g.blocks, g.threads, sm, s>>>(p, tmap);
         else mrg_fill_tma_kernel<kF64, false><<<g.blocks, g.threads, sm, s>>>(p, tmap);
@@ -432,6 +458,7 @@ cudaError_t launch_mrg_fill_tma(const MrgLaunch& p, const CUtensorMap& tmap, int
     }
     return cudaGetLastError();
 }
+
 
 size_t mrg_fill_smem(int threads, int kind)
 {
@@ -498,6 +525,11 @@ cudaError_t mrg_occupancy(int kernel, int kind, bool fast, int threads, int* out
         return occ(mrg_mc_kernel, threads, 0, out);
     case kKMrgFillTma: {
         const size_t sm = mrg_fill_tma_smem(threads);
+        if (!mrg_fill_tma_fits(threads)) {
+            *out = 0;
+            return cudaSuccess;
+        }
+        if (const cudaError_t e = ensure_tma_smem(threads); e != cudaSuccess) return e;
         if (kind == kU32) return occ(mrg_fill_tma_kernel<kU32, false>, threads, sm, out);
         if (kind == kF32) return occ(mrg_fill_tma_kernel<kF32, false>, threads, sm, out);
         return occ(mrg_fill_tma_kernel<kF64, false>, threads, sm, out);

@@ -160,6 +160,142 @@ __global__ void __launch_bounds__(256) tinymt_advance_kernel(const TinyMtLaunch 
     tm_store(P, i, t);
 }
 
+// ---- jump-ahead by a polynomial (shv_jump on TinyMT32 handles, any n) ----
+// The transition T (tinymt_next_state) is linear over GF(2) on the 128-bit
+// state (bit 31 of s0 is masked out of the recurrence but carried into the
+// next s0, so it is part of the vector). For a state v, let m(x) be the
+// minimal polynomial of v under T: m(T) T^k v = 0 for every k, so all states
+// of v's orbit (the streams of one parameter set are slices of one sequence)
+// share it. Then T^n w = r(T) w with r = x^n mod m, for every w of the orbit:
+// the jump costs deg(m) <= 128 transition steps per stream, whatever n is.
+
+struct Poly256 {
+    uint32_t w[9];  // bits 0..287 (coefficient i = bit i)
+};
+
+__device__ __forceinline__ int poly_deg(const uint32_t* a, int words)
+{
+    for (int k = words - 1; k >= 0; --k)
+        if (a[k]) return 32 * k + 31 - __clz(a[k]);
+    return -1;
+}
+
+// a (< 2^(2*128)) reduced mod m (deg dm), in place.
+__device__ __forceinline__ void poly_mod(uint32_t* a, const uint32_t* m, int dm)
+{
+    for (int i = 255; i >= dm; --i) {
+        if ((a[i >> 5] >> (i & 31)) & 1u) {
+            const int sh = i - dm;
+            // a ^= m << sh (m has dm+1 <= 129 bits: 5 words)
+            const int ws = sh >> 5, bs = sh & 31;
+#pragma unroll
+            for (int k = 0; k < 5; ++k) {
+                const uint32_t lo = m[k] << bs;
+                const uint32_t hi = bs ? (m[k] >> (32 - bs)) : 0u;
+                if (ws + k < 9) a[ws + k] ^= lo;
+                if (ws + k + 1 < 9) a[ws + k + 1] ^= hi;
+            }
+        }
+    }
+}
+
+// One thread per parameter set present in the launch (absolute group
+// G = P.first / group_size + g): minimal polynomial of the state of the first
+// launch stream of group G by Krylov elimination, then
+// r_g = x^n mod m_g by left-to-right squaring (squaring over GF(2) spreads
+// the bits) and multiplication by x. out[4g..4g+3] = r_g (degree < 128).
+__global__ void __launch_bounds__(64) tinymt_jump_poly_kernel(const TinyMtLaunch P, uint64_t ngroups, uint64_t n,
+                                                              uint32_t* __restrict__ out)
+{
+    const uint64_t g = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= ngroups) return;
+    const uint64_t G = P.first / P.group_size + g;
+    TinyMT t = tm_load(P, (G * P.group_size > P.first ? G * P.group_size : P.first) - P.first);
+    // echelon basis of the Krylov vectors indexed by pivot (highest set bit),
+    // each with its polynomial tag; a new vector is reduced in decreasing pivot
+    // order, so a XOR never sets a pivot bit already cleared
+    uint32_t bv[128][4], bt[128][5];
+    uint32_t have[4] = {0, 0, 0, 0};
+    uint32_t m[5] = {0, 0, 0, 0, 0};
+    for (int k = 0; k <= 128; ++k) {
+        uint32_t v[4] = {t.s0, t.s1, t.s2, t.s3};
+        uint32_t tag[5] = {0, 0, 0, 0, 0};
+        tag[k >> 5] |= 1u << (k & 31);
+        for (int p = 127; p >= 0; --p) {
+            if (((v[p >> 5] & have[p >> 5]) >> (p & 31)) & 1u) {
+#pragma unroll
+                for (int q = 0; q < 4; ++q) v[q] ^= bv[p][q];
+#pragma unroll
+                for (int q = 0; q < 5; ++q) tag[q] ^= bt[p][q];
+            }
+        }
+        const int d = poly_deg(v, 4);
+        if (d < 0) {  // T^k v is a combination of the earlier ones: m = tag
+#pragma unroll
+            for (int q = 0; q < 5; ++q) m[q] = tag[q];
+            break;
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) bv[d][q] = v[q];
+#pragma unroll
+        for (int q = 0; q < 5; ++q) bt[d][q] = tag[q];
+        have[d >> 5] |= 1u << (d & 31);
+        tinymt_next_state(t);
+    }
+    const int dm = poly_deg(m, 5);
+    uint32_t r[9] = {1, 0, 0, 0, 0, 0, 0, 0, 0};  // x^0
+    if (dm == 0) r[0] = 0;  // v = 0: the zero state stays zero
+    for (int b = 63; b >= 0 && dm > 0; --b) {
+        uint32_t sq[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {  // r^2: bit i -> bit 2i
+            uint32_t lo = r[k] & 0xFFFFu, hi = r[k] >> 16;
+            lo = (lo | (lo << 8)) & 0x00FF00FFu;
+            lo = (lo | (lo << 4)) & 0x0F0F0F0Fu;
+            lo = (lo | (lo << 2)) & 0x33333333u;
+            lo = (lo | (lo << 1)) & 0x55555555u;
+            hi = (hi | (hi << 8)) & 0x00FF00FFu;
+            hi = (hi | (hi << 4)) & 0x0F0F0F0Fu;
+            hi = (hi | (hi << 2)) & 0x33333333u;
+            hi = (hi | (hi << 1)) & 0x55555555u;
+            sq[2 * k] = lo;
+            sq[2 * k + 1] = hi;
+        }
+        poly_mod(sq, m, dm);
+        if ((n >> b) & 1u) {  // * x
+            for (int k = 8; k > 0; --k) sq[k] = (sq[k] << 1) | (sq[k - 1] >> 31);
+            sq[0] <<= 1;
+            poly_mod(sq, m, dm);
+        }
+#pragma unroll
+        for (int k = 0; k < 9; ++k) r[k] = sq[k];
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) out[4 * g + k] = r[k];
+}
+
+// Per stream: state <- r_g(T) state by Horner's rule (deg r_g < 128 steps).
+__global__ void __launch_bounds__(256) tinymt_jump_apply_kernel(const TinyMtLaunch P, const uint32_t* __restrict__ poly)
+{
+    const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= P.ns) return;
+    const uint32_t* r = poly + 4 * ((P.first + i) / P.group_size - P.first / P.group_size);
+    const TinyMT v = tm_load(P, i);
+    TinyMT acc = v;
+    acc.s0 = acc.s1 = acc.s2 = acc.s3 = 0;
+    const int d = poly_deg(r, 4);
+    for (int k = d; k >= 0; --k) {
+        tinymt_next_state(acc);
+        if ((r[k >> 5] >> (k & 31)) & 1u) {
+            acc.s0 ^= v.s0;
+            acc.s1 ^= v.s1;
+            acc.s2 ^= v.s2;
+            acc.s3 ^= v.s3;
+        }
+    }
+    tm_store(P, i, acc);
+}
+
 __global__ void __launch_bounds__(256) tinymt_mc_kernel(const __grid_constant__ TinyMtLaunch P)
 {
     const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -454,6 +590,16 @@ cudaError_t launch_tinymt_fill(const TinyMtLaunch& p, int kind, bool vec, Grid g
 cudaError_t launch_tinymt_advance(const TinyMtLaunch& p, Grid g, cudaStream_t s)
 {
     tinymt_advance_kernel<<<g.blocks, g.threads, 0, s>>>(p);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_tinymt_jump(const TinyMtLaunch& p, uint64_t n, uint32_t* d_poly, cudaStream_t s)
+{
+    const uint64_t ngroups = (p.first + p.ns - 1) / p.group_size - p.first / p.group_size + 1;
+    tinymt_jump_poly_kernel<<<(unsigned)((ngroups + 63) / 64), 64, 0, s>>>(p, ngroups, n, d_poly);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    tinymt_jump_apply_kernel<<<(unsigned)((p.ns + 255) / 256), 256, 0, s>>>(p, d_poly);
     return cudaGetLastError();
 }
 

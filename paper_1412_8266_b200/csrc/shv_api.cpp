@@ -175,7 +175,6 @@ struct Handle {
     uint32_t* params = nullptr;  // owned, (mat1, mat2, tmat) per group from group0
     uint64_t group0 = 0;
     uint32_t group_size = 0;
-    cudaStream_t home = nullptr;  // stream of create: TinyMT jumps are enqueued there
     uint64_t players = 0;         // Leap Frog: K (spacing SHV_SPACING_LEAPFROG)
 };
 
@@ -324,6 +323,39 @@ void split(const Handle& h, uint64_t ns, uint64_t len, uint64_t align, uint64_t 
     *nseg = (uint32_t)(S ? S : 1);
 }
 
+// TMA fill of MRG32k3a (mrg_fill_tma_kernel): a warp owns a tile of 32 rows
+// x one segment, and tiles go round-robin over the resident warps, so the
+// segment count decides the tail: pick the 64-value-aligned segment length
+// that minimises rounds x (segment + start-jump cost), the start jump (state
+// load, A^o and the per-bit segment jumps) costing about as much as 16 values.
+void split_tiles(const Handle& h, uint64_t ns, uint64_t len, uint64_t resident_threads, uint64_t* seg_len,
+                 uint32_t* nseg)
+{
+    if (h.seg) {
+        split(h, ns, len, 64, 8, resident_threads, 1ull << 40, seg_len, nseg);
+        return;
+    }
+    const uint64_t warps = resident_threads / 32 ? resident_threads / 32 : 1;
+    const uint64_t G = (ns + 31) / 32;
+    uint64_t bestL = (len + 63) / 64 * 64, bestS = 1;
+    double best = -1.0;
+    for (uint64_t S = 1; S <= 256; ++S) {
+        const uint64_t L = ((len + S - 1) / S + 63) / 64 * 64;
+        const uint64_t Sa = (len + L - 1) / L;
+        if (Sa != S || (S > 1 && L < 256)) continue;
+        const uint64_t tiles = G * S;
+        const double rounds = (double)((tiles + warps - 1) / warps);
+        const double cost = rounds * (double)(L + 16);
+        if (best < 0 || cost < best) {
+            best = cost;
+            bestL = L;
+            bestS = S;
+        }
+    }
+    *seg_len = bestL;
+    *nseg = (uint32_t)bestS;
+}
+
 // Leap Frog: the last base draw a call touches is (first+n-1) + K*(o+draws-1);
 // it must exist in the base stream (R17).
 shv_status check_leap_advance(const Handle& h, u128 draws)
@@ -395,6 +427,8 @@ void fill_mrg_segments(const Handle& h, uint64_t units_per_seg, uint64_t draws_p
     const double fpk[6] = {6755399441055744.0, 1.0 / 4294967087.0, 0x1.000059451f212p-32,
                            4294967087.0, 4294944443.0, 5886603609186927.0};
     memcpy(P->fpk, fpk, sizeof fpk);
+    P->imul[0] = 1403580u;  // a12
+    P->imul[1] = 810728u;   // a13n
     P->seg0 = pair_pow(h.offset, 0);
     P->segpow[0] = pair_pow((u128)units_per_seg * draws_per_unit, 0);
     for (int b = 1; b < kSegBits && ((uint64_t)nseg - 1) >> b; ++b)
@@ -656,6 +690,8 @@ shv_status generate(shv_streams hid, T* out, uint64_t n, void* stream, int kind,
                 const double fpk[6] = {6755399441055744.0, 1.0 / 4294967087.0, 0x1.000059451f212p-32,
                                        4294967087.0, 4294944443.0, 1370589.0 * 4294944443.0};
                 memcpy(P->fpk, fpk, sizeof fpk);
+                P->imul[0] = 1403580u;  // a12
+                P->imul[1] = 810728u;   // a13n
                 CUtensorMap tmap;
                 if (err == cudaSuccess && !encode_rows_map(&tmap, dst, n, ns, (int)sizeof(T), 128))
                     err = cudaErrorInvalidValue;
@@ -733,11 +769,15 @@ shv_status generate(shv_streams hid, T* out, uint64_t n, void* stream, int kind,
             P->n = n;
             // TMA path for 4-byte values: 128-B boxes of 32 rows (16-B aligned rows, int32 box
             // coordinates). f64 keeps the staged 256-B warp stores, faster there.
-            bool tma = SHV_MRG_TMA && vec && kind != kF64 && n < (1ull << 31) && ns < (1ull << 31);
+            bool tma = SHV_MRG_TMA && vec && kind != kF64 && n < (1ull << 31) && ns < (1ull << 31) &&
+                       mrg_fill_tma_fits((int)h.tpb);
             const int kid = tma ? kKMrgFillTma : kKMrgFill;
             // vector paths: segments in whole 256-byte rounds (64 values; 2 or 4 TMA boxes)
-            split(h, ns, n, vec ? 64 : 1, 8, resident_threads(h, kid, kind, vec), 1ull << 40,
-                  &P->seg_len, &P->nseg);
+            if (tma)
+                split_tiles(h, ns, n, resident_threads(h, kid, kind, vec), &P->seg_len, &P->nseg);
+            else
+                split(h, ns, n, vec ? 64 : 1, 8, resident_threads(h, kid, kind, vec), 1ull << 40,
+                      &P->seg_len, &P->nseg);
             if (vec && P->seg_len % 64) vec = tma = false;  // user segment length: per-lane paths
             P->items = ns * P->nseg;
             P->seg_fastest = SHV_MRG_ORDER ? SHV_MRG_ORDER == 2 : row_bytes > (512u << 10);
@@ -896,7 +936,6 @@ shv_status shv_streams_create_tinymt32(shv_streams* out, const uint32_t* params,
     h->n = n_streams;
     h->group0 = g0;
     h->group_size = group_size;
-    h->home = (cudaStream_t)cuda_stream;
     cudaStream_t s = (cudaStream_t)cuda_stream;
     cudaError_t e = cudaDeviceGetAttribute(&h->sms, cudaDevAttrMultiProcessorCount, dev);
     if (e != cudaSuccess) return cuda_fail(e, "cudaDeviceGetAttribute");
@@ -973,7 +1012,6 @@ shv_status shv_streams_create_mtgp32(shv_streams* out, const uint32_t* params, s
     h->seed[1] = (uint32_t)(seed >> 32);
     h->first = first_stream;
     h->n = n_streams;
-    h->home = (cudaStream_t)cuda_stream;
     cudaStream_t s = (cudaStream_t)cuda_stream;
     cudaError_t e = cudaDeviceGetAttribute(&h->sms, cudaDevAttrMultiProcessorCount, dev);
     if (e != cudaSuccess) return cuda_fail(e, "cudaDeviceGetAttribute");
@@ -1189,7 +1227,11 @@ shv_status shv_streams_create_leapfrog(shv_streams* out, int gen, const uint32_t
     return SHV_OK;
 }
 
-shv_status shv_jump(shv_streams hid, int kind, uint64_t n)
+// TinyMT32 jumps of at most this many draws step the generator (cheaper
+// than the <= 128-step polynomial jump plus its per-group setup).
+constexpr uint64_t kTinyStepJumpMax = 256;
+
+shv_status shv_jump(shv_streams hid, int kind, uint64_t n, void* stream)
 {
     Range nvtx_range("shv_jump");
     auto hp = lookup(hid);
@@ -1197,7 +1239,7 @@ shv_status shv_jump(shv_streams hid, int kind, uint64_t n)
     Handle& h = *hp;
     u128 d;
     if (h.gen == SHV_GEN_MTGP32) {
-        // sequential advance on the device (no jump polynomial), on the create stream
+        // sequential advance on the device (no jump polynomial), on the caller's stream
         if (kind != SHV_JUMP_DRAWS) return fail(SHV_ERR_UNSUPPORTED, "MTGP32 jumps by draws only");
         if (n == 0) return SHV_OK;
         shv_status st = check_advance(h, n);
@@ -1206,23 +1248,38 @@ shv_status shv_jump(shv_streams hid, int kind, uint64_t n)
         if (dg.err != cudaSuccess) return cuda_fail(dg.err, "cudaSetDevice");
         MtgpLaunch P = mtgp_launch(h, 0, h.n);
         P.n = n;
-        cudaError_t e = launch_mtgp(P, 4, mtgp_blocks(h, h.n), h.home);
+        cudaError_t e = launch_mtgp(P, 4, mtgp_blocks(h, h.n), (cudaStream_t)stream);
         if (e != cudaSuccess) return cuda_fail(e, "mtgp32 advance");
         h.offset += n;
         return SHV_OK;
     }
     if (h.gen == SHV_GEN_TINYMT32 && h.spacing != SHV_SPACING_LEAPFROG) {
-        // sequential advance on the device (S L355), on the create stream
+        // stateful: the state buffer advances on the caller's stream; short
+        // jumps step (S L355), longer ones apply the jump polynomial x^n mod
+        // the minimal polynomial of each parameter set's orbit (deg <= 128)
         if (kind != SHV_JUMP_DRAWS) return fail(SHV_ERR_UNSUPPORTED, "TinyMT32 jumps by draws only");
-        if (n > 0xFFFFFFFFull) return fail(SHV_ERR_INVALID_ARGUMENT, "TinyMT32 advances at most 2^32 draws per jump");
         if (n == 0) return SHV_OK;
+        shv_status st = check_advance(h, n);
+        if (st) return st;
         DeviceGuard dg(h.device);
         if (dg.err != cudaSuccess) return cuda_fail(dg.err, "cudaSetDevice");
         TinyMtLaunch P = tm_launch(h, 0, h.n);
-        P.steps = n;
-        Grid g{(unsigned)((h.n + 255) / 256), 256};
-        cudaError_t e = launch_tinymt_advance(P, g, h.home);
-        if (e != cudaSuccess) return cuda_fail(e, "tinymt advance");
+        cudaStream_t s = (cudaStream_t)stream;
+        cudaError_t e;
+        if (n <= kTinyStepJumpMax) {
+            P.steps = n;
+            e = launch_tinymt_advance(P, Grid{(unsigned)((h.n + 255) / 256), 256}, s);
+        } else {
+            const uint64_t ngroups = (h.first + h.n - 1) / h.group_size - h.first / h.group_size + 1;
+            uint32_t* poly = nullptr;
+            e = cudaMallocAsync((void**)&poly, 16 * ngroups, s);
+            if (e == cudaSuccess) e = launch_tinymt_jump(P, n, poly, s);
+            if (poly) {
+                const cudaError_t ef = cudaFreeAsync(poly, s);
+                if (e == cudaSuccess) e = ef;
+            }
+        }
+        if (e != cudaSuccess) return cuda_fail(e, "tinymt jump");
         h.offset += n;
         return SHV_OK;
     }
@@ -1259,7 +1316,6 @@ shv_status shv_generate_u32_host(shv_streams h, uint32_t* h_out, uint64_t n, voi
 {
     return generate<uint32_t>(h, h_out, n, s, kU32, true);
 }
-
 shv_status shv_mc_pi_ex(shv_streams hid, uint64_t samples, uint64_t* d_hits, uint64_t* d_counts,
                         void* stream)
 {

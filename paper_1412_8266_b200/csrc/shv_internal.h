@@ -47,6 +47,8 @@ struct MrgLaunch {
     double fpk[6];                // FP64 step constants (shv::dev::MrgFpK order), set by
                                   // fill_mrg_segments: read from the parameter block so
                                   // ptxas keeps them in registers
+    uint32_t imul[2];             // a12, a13n (MrgFpK::a12/a13n): runtime values, so ptxas
+                                  // emits plain IMAD.WIDE for the integer half-step
 };
 
 // Philox4x32-10 bulk fill / Monte Carlo launch. Draw d of handle stream i
@@ -144,12 +146,14 @@ struct LeapLaunch {
     uint64_t tr_tb, tr_ps, tr_pl;  // t-blocks of 32, player segments, players per segment (% 128 == 0)
     MatPair tr_ppow[kSegBits];   // (A^tr_pl)^(2^b)
     double fpk[6];               // FP64 step constants (shv::dev::MrgFpK order)
+    uint32_t imul[2];            // a12, a13n (as MrgLaunch::imul)
 };
 
 struct Grid {
     unsigned blocks;
     unsigned threads;
 };
+
 
 // ---- launchers (kernels_mrg.cu, kernels_philox.cu, kernels_threefry.cu, kernels_tinymt32.cu,
 //      kernels_leapfrog.cu) ----
@@ -162,6 +166,10 @@ cudaError_t launch_tinymt_seed(const TinyMtLaunch& p, uint32_t seed, const uint3
                                Grid g, cudaStream_t s);
 cudaError_t launch_tinymt_fill(const TinyMtLaunch& p, int kind, bool vec, Grid g, cudaStream_t s);
 cudaError_t launch_tinymt_advance(const TinyMtLaunch& p, Grid g, cudaStream_t s);
+// Jump every stream of p (p.ns from stream 0) by n draws with the jump
+// polynomial x^n mod (minimal polynomial of the group's orbit); d_poly:
+// 16 bytes of device scratch per parameter set the launch touches.
+cudaError_t launch_tinymt_jump(const TinyMtLaunch& p, uint64_t n, uint32_t* d_poly, cudaStream_t s);
 cudaError_t launch_tinymt_mc(const TinyMtLaunch& p, Grid g, cudaStream_t s);
 cudaError_t upload_jump_tables(const MatPair* sub51, const MatPair* str64, const MatPair* draw64);
 // T = g.blocks * g.threads seeding threads; step = A^(T * spacing); table 0
@@ -174,6 +182,7 @@ cudaError_t launch_mrg_fill(const MrgLaunch& p, int kind, bool vec, Grid g, cuda
 // needs seg_len % (128 / value bytes) == 0, n and ns < 2^31.
 cudaError_t launch_mrg_fill_tma(const MrgLaunch& p, const CUtensorMap& tmap, int kind, Grid g, cudaStream_t s);
 size_t mrg_fill_tma_smem(int threads);
+bool mrg_fill_tma_fits(int threads);  // dynamic shared memory of a block within the 227-KB limit
 cudaError_t launch_mrg_mc(const MrgLaunch& p, Grid g, cudaStream_t s);
 cudaError_t launch_philox_fill(const PhiloxLaunch& p, int kind, bool fast, Grid g, cudaStream_t s);
 cudaError_t launch_philox_mc(const PhiloxLaunch& p, bool fast, Grid g, cudaStream_t s);

@@ -98,7 +98,7 @@ def test_tinymt32_validation_without_gpu(shv):
 
 def test_lifecycle_errors_without_gpu(shv):
     for fn in (lambda: shv.shv_streams_destroy(123456789),
-               lambda: shv.shv_jump(123456789, 0, 1),
+               lambda: shv.shv_jump(123456789, 0, 1, 0),
                lambda: shv.shv_get_position(123456789),
                lambda: shv.shv_generate_u32(123456789, 0, 8, 0),
                lambda: shv.shv_mc_pi(123456789, 8, 0, 0),

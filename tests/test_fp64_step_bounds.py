@@ -71,3 +71,40 @@ def test_combine_maps_m1_like_zero():
         return (z + M1) % 2**32 if p1 <= p2 else z
     for p2 in (0, 1, 12345, M2 - 1):
         assert comb(M1, p2) == comb(0, p2)
+
+
+def c1_int(x0: int, x1: int) -> int:
+    """The integer half-step mrg_c1_int (include/shv_device.cuh) in u32 arithmetic,
+    instruction by instruction: t = m1 - x0; P = a12*x1 + a13n*t (u64); (H, L);
+    u = L + 209*H mod 2^32; p1 = u + 209 if (u < L or u >= m1) else u."""
+    t = (M1 - x0) % 2**32
+    P = A12 * x1 + A13N * t
+    assert P < 2**64
+    return fold1(P)
+
+
+def fold1(P: int) -> int:
+    H, L = P >> 32, P & 0xFFFFFFFF
+    u = (L + 209 * H) % 2**32
+    return (u + 209) % 2**32 if (u < L or u >= M1) else u
+
+
+def test_integer_half_step_bounds():
+    # P = a12*x1 + a13n*(m1 - x0) for canonical x < m1: its high word times 209
+    # stays below 2^32, so u wraps at most once (u < L detects it)
+    pmax = A12 * (M1 - 1) + A13N * M1
+    assert pmax < 2**53.1 and 209 * (pmax >> 32) < 2**28.8
+    rng = random.Random(8266)
+    hmax = pmax >> 32
+    for H in [0, 1, 2, 3, hmax - 1, hmax] + [rng.randrange(hmax + 1) for _ in range(200)]:
+        c = 209 * H
+        for L in {0, 1, 208, 209, (M1 - c - 1) % 2**32, (M1 - c) % 2**32, (2**32 - c - 1) % 2**32,
+                  (2**32 - c) % 2**32, 2**32 - 1, M1 - 1, M1, rng.randrange(2**32)}:
+            P = (H << 32) | L
+            if P <= pmax:
+                assert fold1(P) == P % M1, (H, L)
+    for x0, x1 in [(0, 0), (0, M1 - 1), (M1 - 1, 0), (M1 - 1, M1 - 1), (1, 1), (0, 1)]:
+        assert c1_int(x0, x1) == (A12 * x1 - A13N * x0) % M1
+    for _ in range(50000):
+        x0, x1 = rng.randrange(M1), rng.randrange(M1)
+        assert c1_int(x0, x1) == (A12 * x1 - A13N * x0) % M1

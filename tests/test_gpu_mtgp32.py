@@ -167,3 +167,21 @@ def test_errors(shv, params):
     assert e.value.status == shv.SHV_ERR_EMPTY_EXPERIMENT
     shv.shv_streams_destroy(h)
     assert shv.shv_state_bytes(shv.SHV_GEN_MTGP32, 3) == 3 * 1408
+
+
+def test_jump_is_ordered_on_the_callers_stream(shv, orc, params):
+    """Create on stream A, jump on stream B, generate on stream C (SURVEY
+    8(b): every call is stream-ordered on its cuda_stream; the caller orders
+    the streams with events). The stateful advance must run on B."""
+    sa, sb, sc = torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream()
+    with torch.cuda.stream(sa):
+        h = shv.shv_streams_create_mtgp32(params, 5, 17, 32, None, 0, torch.cuda.current_device(), sa)
+    sb.wait_stream(sa)
+    shv.shv_jump(h, shv.SHV_JUMP_DRAWS, 3333, sb)
+    sc.wait_stream(sb)
+    out = torch.empty(32 * 700, dtype=torch.int32, device="cuda")
+    shv.shv_generate_u32(h, out, 700, sc)
+    sc.synchronize()
+    want = orc.generate(W.MTGP32, W.mtgp32_seed_words(5, params), 32, 700, first=17, offset=3333)
+    assert (out.cpu().numpy().view(np.uint32).reshape(32, 700) == want).all()
+    shv.shv_streams_destroy(h)

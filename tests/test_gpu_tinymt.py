@@ -1,7 +1,7 @@
 """TinyMT32 (NEXT-3; P L287-317 §4.2; R15) on the GPU against the oracle: the
 paper's hybrid distribution (one parameter set per group, 2^64-draw slices per
-stream inside a group), stateful generate/mc_pi, sequential jumps, ragged
-shapes, and the device API."""
+stream inside a group), stateful generate/mc_pi, jumps (stepped and by the
+jump polynomial, on the caller's stream), ragged shapes, and the device API."""
 import ctypes as C
 import os
 import shutil
@@ -99,4 +99,45 @@ def test_tinymt_device_api(shv, orc, tmp_path):
     assert lib.launch_listing1(W.TINYMT32, 0, out.data_ptr(), C.addressof(v), 9, blocks, threads) == 0
     ref = orc.generate(W.TINYMT32, W.tinymt32_seed_words(31, gs, params), n, 9)
     assert np.array_equal(out.cpu().numpy().view(np.uint32).reshape(n, 9), ref)
+    shv.shv_streams_destroy(h)
+
+
+@pytest.mark.parametrize("gs,first,ns", [(32, 0, 256), (8, 13, 70), (1, 3, 5)])
+def test_tinymt_polynomial_jumps(shv, orc, gs, first, ns):
+    """Jumps past the stepping threshold use x^n mod the minimal polynomial of
+    each parameter set's orbit (shv_api.cpp shv_jump): any n, compared with
+    the oracle's GF(2) matrix power (orc_tinymt32_jump)."""
+    params = W.tinymt32_test_params((first + ns + gs - 1) // gs)
+    sd = W.tinymt32_seed_words(99, gs, params)
+    h = shv.shv_streams_create_tinymt32(params, 99, gs, first, ns, None, 0, -1, None)
+    off = 0
+    for jump in (257, 1000, (1 << 33) + 5, (1 << 63) + 12345, 256, 1):
+        shv.shv_jump(h, shv.SHV_JUMP_DRAWS, jump)
+        off += jump
+        out = torch.empty(ns * 40, dtype=torch.int32, device="cuda")
+        shv.shv_generate_u32(h, out, 40, None)
+        torch.cuda.synchronize()
+        ref = orc.generate(W.TINYMT32, sd, ns, 40, first=first, offset=off)
+        assert np.array_equal(out.cpu().numpy().view(np.uint32).reshape(ns, 40), ref), jump
+        off += 40
+    shv.shv_streams_destroy(h)
+
+
+def test_tinymt_jump_on_callers_stream(shv, orc):
+    """Create on stream A, jump on stream B, generate on stream C; the caller
+    orders the streams with events. The state advance runs on B."""
+    gs, ns = 16, 128
+    params = W.tinymt32_test_params(ns // gs)
+    sd = W.tinymt32_seed_words(5, gs, params)
+    sa, sb, sc = torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream()
+    h = shv.shv_streams_create_tinymt32(params, 5, gs, 0, ns, None, 0, -1, sa)
+    sb.wait_stream(sa)
+    for jump in (100, 1 << 40):  # stepped, polynomial
+        shv.shv_jump(h, shv.SHV_JUMP_DRAWS, jump, sb)
+    sc.wait_stream(sb)
+    out = torch.empty(ns * 64, dtype=torch.int32, device="cuda")
+    shv.shv_generate_u32(h, out, 64, sc)
+    sc.synchronize()
+    ref = orc.generate(W.TINYMT32, sd, ns, 64, offset=100 + (1 << 40))
+    assert np.array_equal(out.cpu().numpy().view(np.uint32).reshape(ns, 64), ref)
     shv.shv_streams_destroy(h)

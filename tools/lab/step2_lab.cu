@@ -1,33 +1,35 @@
 // step2_lab.cu — compute-only throughput (no stores) of the MRG32k3a step
-// formulations in include/shv_device.cuh: MrgD (round-to-nearest, decode
-// fix-ups), MrgFF (both components, floor reductions), MrgIF (component 1
-// integer, component 2 floor), with the FP64 constants as immediates or read
-// from the parameter block; 1 or 2 streams per thread. Checks that every
-// variant gives the integer step's sequence.
+// formulations in include/shv_device.cuh: MrgFF (both components, floor
+// reductions), MrgIF (component 1 integer, component 2 floor) and the
+// all-integer step, with the constants as immediates or read from the
+// parameter block; 1 or 2 streams per thread. Checks that every variant gives
+// the integer step's sequence.
 #include <cstdio>
 #include <cstdint>
 #include <cuda_runtime.h>
-#include "../../include/shv_device.cuh"
+#include "lab_variants.cuh"
 using namespace shv::dev;
 
 constexpr int ITER = 1024;  // x 8 steps
 
-struct KP { double v[6]; };
-__device__ __forceinline__ MrgFpK kp(const KP& p) { return MrgFpK{p.v[0], p.v[1], p.v[2], p.v[3], p.v[4], p.v[5]}; }
+struct KP { double v[6]; uint32_t a12, a13n; };
+__device__ __forceinline__ MrgFpK kp(const KP& p) { return MrgFpK{p.v[0], p.v[1], p.v[2], p.v[3], p.v[4], p.v[5], p.a12, p.a13n}; }
 
 __device__ __forceinline__ Mrg seed_of(uint32_t t)
 {
     return Mrg{12345u + t, 12345u, 12345u ^ t, 12345u, 777u + t, 12345u};
 }
-__device__ __forceinline__ uint32_t nx(Mrg& s, const MrgFpK&) { return mrg_next(s); }
-__device__ __forceinline__ uint32_t nx(MrgD& s, const MrgFpK&) { return mrg_next(s); }
+__device__ __forceinline__ uint32_t nx(Mrg& s, const MrgFpK& K) { return mrg_next(s, K); }
 __device__ __forceinline__ uint32_t nx(MrgFF& s, const MrgFpK& K) { return mrg_next(s, K); }
 __device__ __forceinline__ uint32_t nx(MrgIF& s, const MrgFpK& K) { return mrg_next(s, K); }
+template <int M> __device__ __forceinline__ uint32_t nx(MrgFW<M>& s, const MrgFpK& K) { return mrg_next(s, K); }
 template <class G> __device__ __forceinline__ G mk(const Mrg& s);
 template <> __device__ __forceinline__ Mrg mk<Mrg>(const Mrg& s) { return s; }
-template <> __device__ __forceinline__ MrgD mk<MrgD>(const Mrg& s) { return to_fp64(s); }
 template <> __device__ __forceinline__ MrgFF mk<MrgFF>(const Mrg& s) { return to_mrg_ff(s); }
 template <> __device__ __forceinline__ MrgIF mk<MrgIF>(const Mrg& s) { return to_mrg_if(s); }
+template <> __device__ __forceinline__ MrgFW<1> mk<MrgFW<1>>(const Mrg& s) { return to_mrg_fw<1>(s); }
+template <> __device__ __forceinline__ MrgFW<2> mk<MrgFW<2>>(const Mrg& s) { return to_mrg_fw<2>(s); }
+template <> __device__ __forceinline__ MrgFW<3> mk<MrgFW<3>>(const Mrg& s) { return to_mrg_fw<3>(s); }
 
 // PK: constants from the parameter block (1) or immediates (0); S streams per thread
 template <class G, int PK, int S>
@@ -77,7 +79,7 @@ template <class F> float tms(F f) { cudaEvent_t a, b; cudaEventCreate(&a); cudaE
 int main()
 {
     int sms; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-    KP p{{6755399441055744.0, 1.0 / 4294967087.0, 0x1.000059451f212p-32, 4294967087.0, 4294944443.0, 5886603609186927.0}};
+    KP p{{6755399441055744.0, 1.0 / 4294967087.0, 0x1.000059451f212p-32, 4294967087.0, 4294944443.0, 5886603609186927.0}, 1403580u, 810728u};
     const int thr = 256;
     const size_t maxn = (size_t)sms * 16 * thr * 2;
     uint32_t *ref, *o; cudaMalloc(&ref, maxn * 4); cudaMalloc(&o, maxn * 4);
@@ -99,26 +101,16 @@ int main()
     };
     for (int bps : {4, 8}) {
         run("int", k_step<Mrg, 0, 1>, 1, bps);
-        run("D", k_step<MrgD, 0, 1>, 1, bps);
+        run("int_par", k_step<Mrg, 1, 1>, 1, bps);
         run("FF_imm", k_step<MrgFF, 0, 1>, 1, bps);
         run("FF_par", k_step<MrgFF, 1, 1>, 1, bps);
         run("FF_par_x2", k_step<MrgFF, 1, 2>, 2, bps);
+        run("FW1_par", k_step<MrgFW<1>, 1, 1>, 1, bps);
+        run("FW2_par", k_step<MrgFW<2>, 1, 1>, 1, bps);
+        run("FW3_par", k_step<MrgFW<3>, 1, 1>, 1, bps);
         run("IF_imm", k_step<MrgIF, 0, 1>, 1, bps);
         run("IF_par", k_step<MrgIF, 1, 1>, 1, bps);
         run("IF_par_x2", k_step<MrgIF, 1, 2>, 2, bps);
-        auto mixed = [&](const char* name, auto kern, int R) {
-            const int blocks = sms * bps;
-            const double nthr = (double)blocks * thr, nint = nthr / R;
-            for (int pct : {30, 45, 60, 75}) {
-                const int ii = ITER * pct / 100;
-                float ms = tms([&] { kern<<<blocks, thr>>>(o, p, ITER, ii); });
-                const double nums = ((nthr - nint) * ITER + nint * ii) * 8;
-                printf(",{\"v\": \"%s\", \"bps\": %d, \"int_work_pct\": %d, \"Tnum_s\": %.4f}\n", name, bps, pct, nums / (ms * 1e-3) / 1e12);
-            }
-        };
-        mixed("mixed_R2", k_mixed<2>, 2);
-        mixed("mixed_R4", k_mixed<4>, 4);
-        mixed("mixed_R8", k_mixed<8>, 8);
     }
     printf("]\n");
     return 0;

@@ -1,8 +1,10 @@
 """Summarise ncu --set full reports into profiles/ncu_traffic.json (the source
 of bench.py's roofline.traffic and roofline.limiter).
 
-usage: python tools/ncu_summary.py OUT.json KEY=report.ncu-rep[:kernel-substring] ...
-Per key: the first launch in the report whose name contains the substring."""
+usage: python tools/ncu_summary.py OUT.json KEY=report.ncu-rep[:kernel-substring[:units]] ...
+Per key: the first launch in the report whose name contains the substring;
+units (numbers or samples the launch processed) adds inst_per_unit = warp
+instructions executed per unit (the bench's issue roofline)."""
 import csv
 import io
 import json
@@ -13,6 +15,10 @@ M = {"gpu__time_duration.sum": "duration_ms_ncu", "dram__bytes_read.sum": "dram_
      "dram__bytes_write.sum": "dram_bytes_write",
      "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active": "fp64_pipe_pct",
      "sm__pipe_fmaheavy_cycles_active.avg.pct_of_peak_sustained_active": "fmaheavy_pipe_pct",
+     "sm__pipe_fmaheavy_cycles_active.avg.pct_of_peak_sustained_elapsed": "fmaheavy_pipe_pct_elapsed",
+     "sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active": "fp64_inst_pct",
+     "smsp__inst_executed.sum": "inst_executed",
+     "sm__cycles_active.avg": "sm_cycles_active",
      "sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active": "alu_pipe_pct",
      "smsp__issue_active.avg.pct_of_peak_sustained_active": "issue_active_pct",
      "launch__registers_per_thread": "registers", "launch__grid_size": "grid",
@@ -35,6 +41,7 @@ def main():
     for sp in specs:
         key, rest = sp.split("=", 1)
         rep, _, sub = rest.partition(":")
+        sub, _, units = sub.partition(":")
         for d, u in rows(rep):
             if sub and sub not in d["Kernel Name"]:
                 continue
@@ -47,6 +54,11 @@ def main():
                     continue
                 x *= UNIT.get(m, {}).get(u.get(m, ""), 1.0)
                 e[k] = x
+            if "fmaheavy_pipe_pct" not in e and "fmaheavy_pipe_pct_elapsed" in e:
+                e["fmaheavy_pipe_pct"] = e["fmaheavy_pipe_pct_elapsed"]
+            if units and e.get("inst_executed"):
+                e["units"] = float(units)
+                e["inst_per_unit"] = e["inst_executed"] / float(units)
             e["source"] = f"ncu --set full --clock-control none ({rep})"
             res[key] = e
             break
