@@ -360,9 +360,9 @@ def main():
                                               "alu_pipe_pct") if rec.get(k) is not None}
     if rec.get("inst_per_unit"):
         hbm["issue"] = {"inst_per_number": round(rec["inst_per_unit"], 3),
-                        "achieved": round(rec["inst_per_unit"] * total_per_rank / 32 / (kms[dom] * 1e-3) / 1e12, 4),
+                        "achieved": round(rec["inst_per_unit"] * total_per_rank / (kms[dom] * 1e-3) / 1e12, 4),
                         "peak": round(ISSUE_PEAK / 1e12, 4), "unit": "T warp instr/s",
-                        "frac": round(rec["inst_per_unit"] * total_per_rank / 32 / (kms[dom] * 1e-3) / ISSUE_PEAK, 4)}
+                        "frac": round(rec["inst_per_unit"] * total_per_rank / (kms[dom] * 1e-3) / ISSUE_PEAK, 4)}
     roof = hbm
     parts = {k: {"ms": round(kms[k], 4), "Gnumbers_per_s": round(total_per_rank / (kms[k] * 1e-3) / 1e9, 1),
                  "GB_per_s": round(alg_bytes / (kms[k] * 1e-3) / 1e9, 1),
@@ -408,11 +408,11 @@ def main():
             # time per sample measured here; per-pipe busy fractions beside it
             rec = profile_record(key.replace("mc_pi_", "mc_"))
             if rec and rec.get("inst_per_unit"):
-                ach = rec["inst_per_unit"] * (N / world) / 32 / (t_ms * 1e-3)
+                ach = rec["inst_per_unit"] * (N / world) / (t_ms * 1e-3)  # warp instructions / s
                 parts[key]["roofline"] = {
                     "bound": "issue", "achieved": round(ach / 1e12, 4), "peak": round(ISSUE_PEAK / 1e12, 4),
                     "unit": "T warp instr/s", "frac": round(ach / ISSUE_PEAK, 4),
-                    "inst_per_sample": round(rec["inst_per_unit"], 3),
+                    "warp_inst_per_sample": round(rec["inst_per_unit"], 4),
                     "peak_source": "148 SMs x 4 schedulers x 1 warp instr/clk x 1.965 GHz (B200_PROFILING.md)",
                     "pipes": {k: rec.get(k) for k in ("issue_active_pct", "fp64_pipe_pct", "fmaheavy_pipe_pct",
                                                       "alu_pipe_pct") if rec.get(k) is not None},
@@ -613,6 +613,8 @@ def main():
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
                 "data": "synthetic",
                 "config": {"workload": WORKLOAD, "streams_per_gpu": wm.n_streams,
+                           "process_group": ({"backend": dist.get_backend(), "world": world}
+                                             if launched else None),
                            "numbers_per_stream": n, "bytes_per_gpu_per_generator": alg_bytes,
                            "parallelism": f"streams sharded over {world} GPU(s), no data-path collective",
                            "l2": "no flush: each launch writes 16 GiB >> 126 MB L2"},

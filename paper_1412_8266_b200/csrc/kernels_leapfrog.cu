@@ -409,11 +409,19 @@ cudaError_t leap_tma_attr()
 // from A^(p_begin + K*t) * tr_s0 (per-bit tables: one jump per lane per
 // segment), and writes draw (p, t) as word t of box row p: all 32 lanes write
 // distinct words of one 128-B row (conflict-free; 128-B swizzle). Each
-// 128-player box (128 rows x 32 values) leaves by TMA; rows past the launch
+// kTrRows-player box (kTrRows rows x 32 values) leaves by TMA; rows past the launch
 // and columns past n are clipped by the tensor map. Per value: the MRG step
 // (12 FP64 instructions) and one shared store, against three modular
 // products per component for the per-player recurrence.
 constexpr unsigned kTrWarps = 4;
+// Players per transposed box (rows of the 128-B wide box): 32 keeps a warp's
+// box at 4 KB, so up to 48 warps per SM stay resident (128-row, 16-KB boxes
+// held the transposed fills to 12 warps per SM: ncu 0.74 eligible warps per
+// scheduler, issue 51 %).
+#ifndef SHV_LEAP_TR_ROWS
+#define SHV_LEAP_TR_ROWS 32
+#endif
+constexpr uint32_t kTrRows = SHV_LEAP_TR_ROWS;
 #ifndef SHV_LEAP_CKMASK
 #define SHV_LEAP_CKMASK 22  // no three-register-pair DFMA: 4.21 -> 3.99 ms at the C5 shape (tools/lab)
 #endif
@@ -428,7 +436,7 @@ __global__ void __launch_bounds__(kTrWarps * 32)
     extern __shared__ uint8_t tr_smem[];
     const unsigned lane = threadIdx.x & 31, warp = __shfl_sync(0xffffffffu, threadIdx.x >> 5, 0);
     const uint32_t base = ((uint32_t)__cvta_generic_to_shared(tr_smem) + 1023u) & ~1023u;
-    const uint32_t box = base + warp * 16384u;
+    const uint32_t box = base + warp * (kTrRows * 128u);
 #define SHV_TRF(i) (((SHV_LEAP_CKMASK >> (i)) & 1) ? c_leap_fpk[i] : P.fpk[i])
     const MrgFpK K{SHV_TRF(0), SHV_TRF(1), SHV_TRF(2), SHV_TRF(3), SHV_TRF(4), SHV_TRF(5), P.imul[0], P.imul[1]};
 #undef SHV_TRF
@@ -449,11 +457,11 @@ __global__ void __launch_bounds__(kTrWarps * 32)
         for (uint64_t b = 0, x = ps; x; ++b, x >>= 1)
             if (x & 1) apply(P.tr_ppow[b].a, P.tr_ppow[b].b, m);
         MrgIF g = to_mrg_if(m);
-        for (uint64_t pc = p0; pc < p1; pc += 128) {
+        for (uint64_t pc = p0; pc < p1; pc += kTrRows) {
             if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
             __syncwarp();
 #pragma unroll 1
-            for (uint32_t q8 = 0; q8 < 128; q8 += 8) {
+            for (uint32_t q8 = 0; q8 < kTrRows; q8 += 8) {
                 const uint32_t rb = box + q8 * 128u;
 #pragma unroll
                 for (uint32_t k = 0; k < 8; ++k) {
@@ -487,7 +495,7 @@ __global__ void __launch_bounds__(kTrWarps * 32)
     extern __shared__ uint8_t trp_smem[];
     const unsigned lane = threadIdx.x & 31, warp = __shfl_sync(0xffffffffu, threadIdx.x >> 5, 0);
     const uint32_t base = ((uint32_t)__cvta_generic_to_shared(trp_smem) + 1023u) & ~1023u;
-    const uint32_t box = base + warp * 16384u;
+    const uint32_t box = base + warp * (kTrRows * 128u);
     uint32_t off[8];
 #pragma unroll
     for (uint32_t k = 0; k < 8; ++k) off[k] = ((((lane >> 2) ^ k)) << 4) + (lane & 3u) * 4u;
@@ -507,11 +515,11 @@ __global__ void __launch_bounds__(kTrWarps * 32)
         const bool hoist = G == kLeapPhilox && (uint32_t)b <= 0xFFFFFFFFu - (uint32_t)min(nblk, (uint64_t)0xFFFFFFFFu);
         const uint64_t q = (uint64_t)kPM0 * ((uint32_t)(b >> 32) ^ (uint32_t)P.k0);
         uint64_t pa = (uint64_t)kPM0 * (uint32_t)b;
-        for (uint64_t pc = p0; pc < p1; pc += 128) {
+        for (uint64_t pc = p0; pc < p1; pc += kTrRows) {
             if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
             __syncwarp();
 #pragma unroll 1
-            for (uint32_t q8 = 0; q8 < 128; q8 += 8) {
+            for (uint32_t q8 = 0; q8 < kTrRows; q8 += 8) {
                 const uint32_t rb = box + q8 * 128u;
                 uint32_t z[8];
                 if constexpr (G == kLeapPhilox) {
@@ -553,7 +561,7 @@ __global__ void __launch_bounds__(kTrWarps * 32)
     if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
-constexpr size_t leap_tr_smem() { return (size_t)kTrWarps * 16384 + 1024; }
+constexpr size_t leap_tr_smem() { return (size_t)kTrWarps * kTrRows * 128 + 1024; }
 
 template <int KIND, int G>
 cudaError_t leap_trp_attr()
@@ -685,6 +693,22 @@ cudaError_t launch_leap_ctr_tr(const LeapLaunch& p, const CUtensorMap& tmap, int
 {
     return lgen == kLeapPhilox ? launch_ctr_tr_g<kLeapPhilox>(p, tmap, kind, blocks, s)
                                : launch_ctr_tr_g<kLeapThreefry>(p, tmap, kind, blocks, s);
+}
+
+uint32_t leap_tr_rows() { return kTrRows; }
+
+cudaError_t leap_ctr_tr_blocks_per_sm(int lgen, int kind, int* out)
+{
+    if (lgen == kLeapPhilox) {
+        const cudaError_t e = kind == kF32 ? leap_trp_attr<kF32, kLeapPhilox>() : leap_trp_attr<kU32, kLeapPhilox>();
+        if (e != cudaSuccess) return e;
+        return kind == kF32 ? occ(leap_ctr_tr_kernel<kF32, kLeapPhilox>, kTrWarps * 32, leap_tr_smem(), out)
+                            : occ(leap_ctr_tr_kernel<kU32, kLeapPhilox>, kTrWarps * 32, leap_tr_smem(), out);
+    }
+    const cudaError_t e = kind == kF32 ? leap_trp_attr<kF32, kLeapThreefry>() : leap_trp_attr<kU32, kLeapThreefry>();
+    if (e != cudaSuccess) return e;
+    return kind == kF32 ? occ(leap_ctr_tr_kernel<kF32, kLeapThreefry>, kTrWarps * 32, leap_tr_smem(), out)
+                        : occ(leap_ctr_tr_kernel<kU32, kLeapThreefry>, kTrWarps * 32, leap_tr_smem(), out);
 }
 
 cudaError_t leap_mrg_tr_blocks_per_sm(int kind, int* out)

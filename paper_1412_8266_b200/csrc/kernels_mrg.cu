@@ -3,10 +3,14 @@
 // fused Monte Carlo pi kernel. Common pieces: kernels_common.cuh.
 //
 // Compile-time variants (the kernel lab, tools/lab/, builds each):
-//   SHV_MRG_STEP  3 (default) = component 1 in integer arithmetic, component 2
-//                 on the FP64 pipe (MrgIF in shv_device.cuh); 4 = both
-//                 components on the FP64 pipe with floor reductions (MrgFF, the
-//                 round-1 step), kept for A/B runs of the same kernels
+//   SHV_MRG_STEP     step of the fills: 4 (default) = both components on the
+//                    FP64 pipe with floor reductions (MrgFF in shv_device.cuh);
+//                    3 = component 1 in integer arithmetic, component 2 on the
+//                    FP64 pipe (MrgIF). Measured (tools/lab):
+//                    MrgIF is 8 % faster compute-only but not in the TMA fill
+//                    (3.47 vs 3.45 ms alone, 3.69 vs 3.58 ms in the bench step)
+//   SHV_MRG_MC_STEP  step of the fused Monte Carlo kernel: 3 (default, MrgIF:
+//                    479 vs 485 ms for 2^38 samples) or 4
 //   SHV_MRG_STAGE 0 = each lane stores its own row directly (32-byte vector
 //                 stores); 2 = lanes stage 256 B in shared memory and the warp
 //                 writes 256-byte runs; 1 (default) = stage the 8-byte (f64)
@@ -17,7 +21,10 @@
 #include "kernels_common.cuh"
 
 #ifndef SHV_MRG_STEP
-#define SHV_MRG_STEP 3
+#define SHV_MRG_STEP 4
+#endif
+#ifndef SHV_MRG_MC_STEP
+#define SHV_MRG_MC_STEP 3
 #endif
 #ifndef SHV_MRG_STAGE
 #define SHV_MRG_STAGE 1
@@ -59,13 +66,10 @@ __device__ __forceinline__ MrgFpK load_fpk(const MrgLaunch& P)
 #undef SHV_CKF
 }
 
-#if SHV_MRG_STEP == 4
-using Gen = MrgFF;
-__device__ __forceinline__ Gen make_gen(const Mrg& s) { return to_mrg_ff(s); }
-#else
-using Gen = MrgIF;
-__device__ __forceinline__ Gen make_gen(const Mrg& s) { return to_mrg_if(s); }
-#endif
+using GenFill = std::conditional<SHV_MRG_STEP == 4, MrgFF, MrgIF>::type;
+using GenMc = std::conditional<SHV_MRG_MC_STEP == 4, MrgFF, MrgIF>::type;
+__device__ __forceinline__ void make_gen(const Mrg& s, MrgFF& g) { g = to_mrg_ff(s); }
+__device__ __forceinline__ void make_gen(const Mrg& s, MrgIF& g) { g = to_mrg_if(s); }
 
 __device__ __forceinline__ Mrg load_state(const uint32_t* __restrict__ st, uint64_t stride, uint64_t i)
 {
@@ -96,18 +100,21 @@ __device__ __forceinline__ void item_ij(const MrgLaunch& P, uint64_t it, uint64_
 }
 
 // Start state of work item (stream i of the launch, segment j).
+template <class Gen = GenFill>
 __device__ __forceinline__ Gen item_state(const MrgLaunch& P, uint64_t i, uint64_t j)
 {
     Mrg s = load_state(P.state, P.stride, P.stream_begin + i);
     apply(P.seg0.a, P.seg0.b, s);
     for (int b = 0; j; ++b, j >>= 1)
         if (j & 1) apply(P.segpow[b].a, P.segpow[b].b, s);
-    return make_gen(s);
+    Gen g;
+    make_gen(s, g);
+    return g;
 }
 
 // 8 values -> staging pieces (u32/f32: 2 pieces; f64: 4 pieces).
 template <int KIND>
-__device__ __forceinline__ void stage8(uint4* wb, unsigned lane, unsigned q0, Gen& s, const MrgFpK& K)
+__device__ __forceinline__ void stage8(uint4* wb, unsigned lane, unsigned q0, GenFill& s, const MrgFpK& K)
 {
     uint32_t v[8];
 #pragma unroll
@@ -179,7 +186,7 @@ __global__ void __launch_bounds__(256, SHV_MRG_MINB) mrg_fill_vec_kernel(const _
         const uint64_t it = base + lane;
         uint32_t len = 0;
         uint64_t row = 0;
-        Gen s{};
+        GenFill s{};
         if (it < P.items) {
             uint64_t i, j;
             item_ij<SEG_FASTEST>(P, it, i, j);
@@ -207,7 +214,7 @@ __global__ void __launch_bounds__(256, SHV_MRG_MINB) mrg_fill_vec_kernel(const _
     for (uint64_t it = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; it < P.items; it += nthr) {
         uint64_t i, j;
         item_ij<SEG_FASTEST>(P, it, i, j);
-        Gen s = item_state(P, i, j);
+        GenFill s = item_state(P, i, j);
         const uint64_t c0 = j * P.seg_len;
         const uint64_t len = min(P.seg_len, P.n - c0);
         T* o = reinterpret_cast<T*>(P.out) + i * P.n + c0;
@@ -243,7 +250,7 @@ __global__ void __launch_bounds__(256, SHV_MRG_MINB) mrg_fill_vec_kernel(const _
 #define SHV_MRG_NBUF 1
 #endif
 #ifndef SHV_MRG_TMA_MINB
-#define SHV_MRG_TMA_MINB (SHV_MRG_STEP == 4 ? 4 : 2)
+#define SHV_MRG_TMA_MINB (SHV_MRG_STEP == 4 ? 4 : 2)  // lab sweep: FF 4 blocks, IF 2 blocks per SM
 #endif
 constexpr uint32_t kTmaBufs = SHV_MRG_NBUF;  // boxes per warp in flight (2: double buffering)
 
@@ -257,7 +264,7 @@ __device__ __forceinline__ void mrg_tma_tile(const MrgLaunch& P, const CUtensorM
     constexpr uint32_t W = 128 / sizeof(T);  // values per row per box
     const uint64_t i = 32 * g + lane;
     // rows past the launch's last stream compute a clipped, discarded row
-    Gen s = item_state(P, i < P.ns ? i : P.ns - 1, j);
+    GenFill s = item_state(P, i < P.ns ? i : P.ns - 1, j);
     const uint64_t c0 = j * P.seg_len;
     const uint32_t len = (uint32_t)min(P.seg_len, P.n - c0);  // warp-uniform
     for (uint32_t r = 0; r < len; r += W) {
@@ -346,7 +353,7 @@ __global__ void __launch_bounds__(256) mrg_fill_scalar_kernel(const __grid_const
     for (uint64_t it = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; it < P.items; it += nthr) {
         uint64_t i, j;
         item_ij<false>(P, it, i, j);
-        Gen s = item_state(P, i, j);
+        GenFill s = item_state(P, i, j);
         const uint64_t c0 = j * P.seg_len;
         const uint64_t len = min(P.seg_len, P.n - c0);
         T* o = reinterpret_cast<T*>(P.out) + i * P.n + c0;
@@ -373,7 +380,7 @@ __global__ void __launch_bounds__(256) mrg_mc_kernel(const __grid_constant__ Mrg
         const uint64_t it = base + lane;
         uint64_t i, j;
         item_ij<false>(P, it < P.items ? it : P.items - 1, i, j);
-        Gen s = item_state(P, i, j);
+        GenMc s = item_state<GenMc>(P, i, j);
         const uint64_t c0 = j * P.seg_len;
         const uint32_t len = it < P.items ? (uint32_t)min(P.seg_len, P.n - c0) : 0u;
         const uint32_t wlen = __reduce_max_sync(0xffffffffu, len);

@@ -644,14 +644,18 @@ shv_status generate(shv_streams hid, T* out, uint64_t n, void* stream, int kind,
             const int kid = leap_kernel_id(kKLeapFill, lg);
             // MRG32k3a, 4-byte values: fill by transposing the base sequence (TMA boxes)
             // Philox: K % 4 == 0 and a 4-aligned first player keep every lane's run
-            // on whole counter blocks (leap_philox_tr_kernel)
+            // on whole counter blocks (leap_ctr_tr_kernel; Threefry: K % 8, 8-aligned)
             const bool trp = (h.gen == SHV_GEN_PHILOX4X32_10 && h.players % 4 == 0 && (h.first + s0) % 4 == 0) ||
                              (h.gen == SHV_GEN_THREEFRY4X64_20 && h.players % 8 == 0 && (h.first + s0) % 8 == 0);
+            const uint32_t rows = leap_tr_rows();
+            CUtensorMap trmap;
+            // an encode failure falls back to the per-player kernels below
             const bool tr = SHV_MRG_TMA && (h.gen == SHV_GEN_MRG32K3A || trp) && kind != kF64 && n % 4 == 0 &&
-                            ((uintptr_t)dst % 16 == 0) && n < (1ull << 31) && ns < (1ull << 31) - 256;
+                            ((uintptr_t)dst % 16 == 0) && n < (1ull << 31) && ns < (1ull << 31) - 256 &&
+                            encode_rows_map(&trmap, dst, n, ns, (int)sizeof(T), rows);
             if (tr) {
                 int bps = 0;
-                err = leap_mrg_tr_blocks_per_sm(kind, &bps);
+                err = trp ? leap_ctr_tr_blocks_per_sm(lg, kind, &bps) : leap_mrg_tr_blocks_per_sm(kind, &bps);
                 auto P = std::make_unique<LeapLaunch>();
                 P->players = h.players;
                 P->first = h.first + s0;
@@ -681,7 +685,7 @@ shv_status generate(shv_streams hid, T* out, uint64_t n, void* stream, int kind,
                 const uint64_t want_ps = (4 * warps + P->tr_tb - 1) / P->tr_tb;
                 uint64_t pl = (ns + want_ps - 1) / want_ps;
                 if (pl < 1024) pl = 1024;  // runs long enough to amortise the start jump
-                pl = (pl + 127) / 128 * 128;
+                pl = (pl + rows - 1) / rows * rows;
                 P->tr_pl = pl;
                 P->tr_ps = (ns + pl - 1) / pl;
                 P->tr_ppow[0] = pair_pow(pl, 0);
@@ -692,15 +696,12 @@ shv_status generate(shv_streams hid, T* out, uint64_t n, void* stream, int kind,
                 memcpy(P->fpk, fpk, sizeof fpk);
                 P->imul[0] = 1403580u;  // a12
                 P->imul[1] = 810728u;   // a13n
-                CUtensorMap tmap;
-                if (err == cudaSuccess && !encode_rows_map(&tmap, dst, n, ns, (int)sizeof(T), 128))
-                    err = cudaErrorInvalidValue;
                 const uint64_t items = P->tr_tb * P->tr_ps;
                 const uint64_t cap = (uint64_t)h.sms * (uint64_t)(bps > 0 ? bps : 1);
                 const uint64_t want = (items + 3) / 4;
                 if (err == cudaSuccess)
-                    err = trp ? launch_leap_ctr_tr(*P, tmap, leap_gen(h.gen), kind, (unsigned)(want < cap ? want : cap), s)
-                              : launch_leap_mrg_tr(*P, tmap, kind, (unsigned)(want < cap ? want : cap), s);
+                    err = trp ? launch_leap_ctr_tr(*P, trmap, leap_gen(h.gen), kind, (unsigned)(want < cap ? want : cap), s)
+                              : launch_leap_mrg_tr(*P, trmap, kind, (unsigned)(want < cap ? want : cap), s);
             } else {
             // grouped Philox, 4-byte values: TMA boxes of 32 values x 128 rows
             bool tma = SHV_MRG_TMA && vec && leap_grouped(h) && kind != kF64 && n % 32 == 0 &&

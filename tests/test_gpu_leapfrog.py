@@ -110,7 +110,8 @@ def test_leapfrog_ragged_jump_and_segments(shv, orc, g, K):
 
 
 @pytest.mark.parametrize("g", list(GENS))
-@pytest.mark.parametrize("K,first,n,samples", [(8, 0, 8, 5000), (4096, 100, 1000, 1001)])
+@pytest.mark.parametrize("K,first,n,samples", [(8, 0, 8, 5000), (4096, 100, 1000, 1001),
+                                              (77, 5, 60, 3001)])  # K % 4 != 0: per-player MC kernel
 def test_leapfrog_mc_matches_oracle(shv, orc, g, K, first, n, samples):
     gen, seed = GENS[g]
     p = Players(shv, gen, seed, K, first, n)

@@ -21,5 +21,6 @@ for r in range(reps):
     shv.shv_generate_u32(h, out, n, None)
     b.record()
     torch.cuda.synchronize()
-    print(f"leap fill {sys.argv[1:2]}: {a.elapsed_time(b):.3f} ms")
+    print(f"leap fill {sys.argv[1:2]}: {a.elapsed_time(b):.3f} ms  "
+          f"checksum {int(out.view(torch.int64).sum().item()) & ((1 << 64) - 1):016x}")
 shv.shv_streams_destroy(h)
