@@ -56,17 +56,27 @@ __device__ __forceinline__ uint32_t red64(uint64_t x)
     return (uint32_t)(x >= m ? x - m : x);
 }
 
-// r = M v (mod 2^32 - C), M row-major 3x3 with entries < m, v canonical.
+// r = M v (mod m = 2^32 - C), M row-major 3x3 with entries < m, v canonical.
+// Each product t = M_kj v_j < m^2 folds once to hi(t)*C + lo(t) < 2^46.5
+// (C <= 22853 < 2^14.48); the three folded terms sum to < 2^48.1, whose high
+// word h < 2^16.1 folds into V = lo + h*C < 2^32 + 2^30.6 < 2m: u = V mod 2^32
+// (one 32-bit IMAD), V >= 2^32 exactly when u < lo, and V mod m = u + C (mod
+// 2^32) when V >= 2^32 or u >= m, else u. 7 IMAD.WIDE + ~5 other per row.
 template <uint32_t C>
 __device__ __forceinline__ void matvec(const uint32_t* M, uint32_t& v0, uint32_t& v1, uint32_t& v2)
 {
     uint32_t r[3];
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
-        const uint64_t s = (uint64_t)red64<C>((uint64_t)M[3 * k] * v0) +
-                           red64<C>((uint64_t)M[3 * k + 1] * v1) +
-                           red64<C>((uint64_t)M[3 * k + 2] * v2);
-        r[k] = red64<C>(s);
+        uint64_t f = 0;
+#pragma unroll
+        for (int j = 0; j < 3; ++j) {
+            const uint64_t t = (uint64_t)M[3 * k + j] * (j == 0 ? v0 : j == 1 ? v1 : v2);
+            f += (t >> 32) * C + (uint32_t)t;
+        }
+        const uint32_t lo = (uint32_t)f, hi = (uint32_t)(f >> 32);
+        const uint32_t u = hi * C + lo;
+        r[k] = ((u < lo) | (u >= 0u - C)) ? u + C : u;
     }
     v0 = r[0];
     v1 = r[1];

@@ -56,6 +56,9 @@ namespace {
 #ifndef SHV_MRG_MC_CKMASK
 #define SHV_MRG_MC_CKMASK 22
 #endif
+#ifndef SHV_MRG_ROWS_CKMASK
+#define SHV_MRG_ROWS_CKMASK 21  // row-tile fill (MrgIF): magic, inv2, m2 from constant memory (lab sweep: 3.43 vs 3.50 ms)
+#endif
 __constant__ double c_mrg_fpk[6] = {6755399441055744.0, 1.0 / 4294967087.0, 0x1.000059451f212p-32,
                                     4294967087.0, 4294944443.0, 5886603609186927.0};
 template <int MASK>
@@ -66,10 +69,16 @@ __device__ __forceinline__ MrgFpK load_fpk(const MrgLaunch& P)
 #undef SHV_CKF
 }
 
-using GenFill = std::conditional<SHV_MRG_STEP == 4, MrgFF, MrgIF>::type;
-using GenMc = std::conditional<SHV_MRG_MC_STEP == 4, MrgFF, MrgIF>::type;
 __device__ __forceinline__ void make_gen(const Mrg& s, MrgFF& g) { g = to_mrg_ff(s); }
 __device__ __forceinline__ void make_gen(const Mrg& s, MrgIF& g) { g = to_mrg_if(s); }
+#ifdef SHV_LAB_GEN_HEADER  // tools/lab builds only: stand-in generators (never in libshv.so)
+#include SHV_LAB_GEN_HEADER
+using GenFill = SHV_LAB_GEN;
+#else
+using GenFill = std::conditional<SHV_MRG_STEP == 4, MrgFF, MrgIF>::type;
+#endif
+using GenMc = std::conditional<SHV_MRG_MC_STEP == 4, MrgFF, MrgIF>::type;
+
 
 __device__ __forceinline__ Mrg load_state(const uint32_t* __restrict__ st, uint64_t stride, uint64_t i)
 {
@@ -254,19 +263,14 @@ __global__ void __launch_bounds__(256, SHV_MRG_MINB) mrg_fill_vec_kernel(const _
 #endif
 constexpr uint32_t kTmaBufs = SHV_MRG_NBUF;  // boxes per warp in flight (2: double buffering)
 
-// One TMA tile: rows 32g..32g+31 of the launch x segment j; lane l generates
-// row 32g + l. bsel (the warp's current box buffer) carries across tiles.
-template <int KIND>
-__device__ __forceinline__ void mrg_tma_tile(const MrgLaunch& P, const CUtensorMap* tmap, const MrgFpK& K,
-                                             unsigned lane, uint32_t box0, uint32_t& bsel, uint64_t g, uint64_t j)
+// Generates `len` values per lane from g (lane l: box row l) in rounds of 128 B
+// and hands each 32-row x 128-B box to the TMA engine at tensor coordinates
+// (col0 + r, row0). bsel (the warp's current box buffer) carries across calls.
+template <int KIND, class Gen>
+__device__ __forceinline__ void mrg_tma_rounds(const CUtensorMap* tmap, const MrgFpK& K, unsigned lane, uint32_t box0,
+                                               uint32_t& bsel, Gen& s, uint32_t len, uint64_t col0, uint64_t row0)
 {
-    using T = OutT<KIND>;
-    constexpr uint32_t W = 128 / sizeof(T);  // values per row per box
-    const uint64_t i = 32 * g + lane;
-    // rows past the launch's last stream compute a clipped, discarded row
-    GenFill s = item_state(P, i < P.ns ? i : P.ns - 1, j);
-    const uint64_t c0 = j * P.seg_len;
-    const uint32_t len = (uint32_t)min(P.seg_len, P.n - c0);  // warp-uniform
+    constexpr uint32_t W = 128 / sizeof(OutT<KIND>);  // values per row per box
     for (uint32_t r = 0; r < len; r += W) {
         const uint32_t box = box0 + bsel * 4096u;
         const uint32_t rowsw = box + lane * 128u + ((lane & 7u) << 4);  // ^ (q << 4) = chunk q
@@ -305,12 +309,26 @@ __device__ __forceinline__ void mrg_tma_tile(const MrgLaunch& P, const CUtensorM
         __syncwarp();
         if (lane == 0) {
             asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(tmap),
-                         "r"(box), "r"((int)(c0 + r)), "r"((int)(32 * g))
+                         "r"(box), "r"((int)(col0 + r)), "r"((int)row0)
                          : "memory");
             asm volatile("cp.async.bulk.commit_group;" ::: "memory");
         }
         bsel = kTmaBufs == 1 ? 0u : bsel ^ 1u;
     }
+}
+
+// One TMA tile: rows 32g..32g+31 of the launch x segment j; lane l generates
+// row 32g + l.
+template <int KIND>
+__device__ __forceinline__ void mrg_tma_tile(const MrgLaunch& P, const CUtensorMap* tmap, const MrgFpK& K,
+                                             unsigned lane, uint32_t box0, uint32_t& bsel, uint64_t g, uint64_t j)
+{
+    const uint64_t i = 32 * g + lane;
+    // rows past the launch's last stream compute a clipped, discarded row
+    GenFill s = item_state(P, i < P.ns ? i : P.ns - 1, j);
+    const uint64_t c0 = j * P.seg_len;
+    const uint32_t len = (uint32_t)min(P.seg_len, P.n - c0);  // warp-uniform
+    mrg_tma_rounds<KIND>(tmap, K, lane, box0, bsel, s, len, c0, 32 * g);
 }
 
 template <int KIND, bool SEG_FASTEST>
@@ -339,6 +357,136 @@ __global__ void __launch_bounds__(256, SHV_MRG_TMA_MINB)
             g = t - j * G;
         }
         mrg_tma_tile<KIND>(P, &tmap, K, lane, box0, bsel, g, j);
+    }
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
+// MRG32k3a fill, row tiles (TMA). The output is viewed as
+// [ns * nseg][S] (row i = segments i*nseg .. i*nseg + nseg - 1 of S = seg_len
+// values, contiguous since S * nseg = n), and a warp tile is 32 consecutive
+// segments — for the C5 shape (S = 128, nseg = 32) one whole 16-KB stream row.
+// Lane l owns segment j of row i (32t + l = i*nseg + j) and starts from
+// (A^(32 S))^(j / 32) * lanetab[j % 32] * state_i, lanetab[k] = A^(o + k S)
+// (host-built, copied to shared memory: lanes index it divergently). Each
+// round the warp's box covers 32 segments x 128 B, 4 KB of one DRAM-local
+// region, so a row's pages are complete within a few rounds; stream-per-lane
+// tiles (mrg_fill_tma_kernel) scatter each round over 32 rows 16 KB apart and
+// cap the store path at ~4.6 TB/s (tools/lab/tma_layout_lab.cu: 6.1 vs 4.7
+// TB/s with a null generator).
+// The lane table in shared memory, FP64-split for the start jump: entry e of
+// lane matrix j at ltab[e * 32 + j] (lanes read consecutive 8-byte words),
+// e = (component c, row r, column q, half h) -> ((c * 3 + r) * 3 + q) * 2 + h,
+// half 0 = M >> 16, half 1 = M & 0xffff (exact doubles).
+constexpr uint32_t kLaneTabEntries = 36;
+
+// Row r of one component: (M v) mod m for canonical v (doubles) and the split
+// row (Mh, Ml): Ah = sum Mh_q v_q and Al = sum Ml_q v_q are exact (< 3 * 2^48),
+// Ah mod m by a floor reduction (Ah * delta * m < 0.1 for inv = RN / RU(1/m),
+// DESIGN.md §4.2), X = (Ah mod m) * 2^16 + Al < 2^50 exact, X mod m likewise.
+// 13 FP64 operations, no IMAD.WIDE (which the start jump's integer matvec
+// spends 37 of per apply, ~6 issue cycles each on B200; tools/lab/pipe_mix2_lab.cu).
+__device__ __forceinline__ double split_row_mod(const double* __restrict__ lt, uint32_t e0, uint32_t jl, double v0, double v1,
+                                                double v2, double inv, double m, double magic)
+{
+    const double h0 = lt[(e0 + 0) * 32 + jl], l0 = lt[(e0 + 1) * 32 + jl];
+    const double h1 = lt[(e0 + 2) * 32 + jl], l1 = lt[(e0 + 3) * 32 + jl];
+    const double h2 = lt[(e0 + 4) * 32 + jl], l2 = lt[(e0 + 5) * 32 + jl];
+    const double ah = __fma_rn(h2, v2, __fma_rn(h1, v1, __dmul_rn(h0, v0)));
+    const double al = __fma_rn(l2, v2, __fma_rn(l1, v1, __dmul_rn(l0, v0)));
+    const double kh = __dadd_rn(__fma_rd(ah, inv, magic), -magic);
+    const double rh = __fma_rn(-kh, m, ah);
+    const double x = __fma_rn(rh, 65536.0, al);
+    const double kx = __dadd_rn(__fma_rd(x, inv, magic), -magic);
+    return __fma_rn(-kx, m, x);
+}
+
+// Start state of a row-tile lane: lanetab[jl] * (x, y), on the FP64 pipe.
+__device__ __forceinline__ MrgIF lane_start(const double* __restrict__ lt, uint32_t jl, const uint32_t w[6], const MrgFpK& K)
+{
+    const double x0 = __uint2double_rn(w[0]), x1 = __uint2double_rn(w[1]), x2 = __uint2double_rn(w[2]);
+    const double y0 = __uint2double_rn(w[3]), y1 = __uint2double_rn(w[4]), y2 = __uint2double_rn(w[5]);
+    MrgIF g;
+    g.x0 = (uint32_t)__double2loint(__dadd_rn(split_row_mod(lt, 0, jl, x0, x1, x2, K.inv1, K.m1, K.magic), K.magic));
+    g.x1 = (uint32_t)__double2loint(__dadd_rn(split_row_mod(lt, 6, jl, x0, x1, x2, K.inv1, K.m1, K.magic), K.magic));
+    g.x2 = (uint32_t)__double2loint(__dadd_rn(split_row_mod(lt, 12, jl, x0, x1, x2, K.inv1, K.m1, K.magic), K.magic));
+    g.y0 = split_row_mod(lt, 18, jl, y0, y1, y2, K.inv2, K.m2, K.magic);
+    g.y1 = split_row_mod(lt, 24, jl, y0, y1, y2, K.inv2, K.m2, K.magic);
+    g.y2 = split_row_mod(lt, 30, jl, y0, y1, y2, K.inv2, K.m2, K.magic);
+    return g;
+}
+
+__device__ __forceinline__ void load_words(const MrgLaunch& P, uint32_t i, uint32_t w[6])
+{
+    const uint32_t* st = P.state + P.stream_begin + i;
+#pragma unroll
+    for (int k = 0; k < 6; ++k) w[k] = __ldg(st + k * P.stride);
+}
+
+// MRG32k3a fill, row tiles (TMA). The output is viewed as
+// [ns * nseg][S] (row i = segments i*nseg .. i*nseg + nseg - 1 of S = seg_len
+// values, contiguous since S * nseg = n), and a warp tile is 32 consecutive
+// segments — for the C5 shape (S = 128, nseg = 32) one whole 16-KB stream row.
+// Lane l owns segment j of row i (32t + l = i*nseg + j) and starts from
+// (A^(32 S))^(j / 32) * lanetab[j % 32] * state_i, lanetab[k] = A^(o + k S)
+// (host-built, FP64-split into shared memory). Each round the warp's box
+// covers 32 segments x 128 B, 4 KB of one DRAM-local region, so a row's pages
+// are complete within a few rounds; stream-per-lane tiles
+// (mrg_fill_tma_kernel) scatter each round over 32 rows 16 KB apart and cap
+// the store path at ~4.6 TB/s (tools/lab/tma_layout_lab.cu: 6.1 vs 4.7 TB/s
+// with a null generator). The next tile's state words are loaded while the
+// current tile generates.
+#ifndef SHV_MRG_ROWS_MINB
+#define SHV_MRG_ROWS_MINB 5  // <= 48 registers: 5 blocks of 256 per SM (lab: 3.50 vs 3.56 ms at 4)
+#endif
+template <int KIND>
+__global__ void __launch_bounds__(256, SHV_MRG_ROWS_MINB)
+    mrg_fill_rows_kernel(const __grid_constant__ MrgRowsLaunch R, const __grid_constant__ CUtensorMap tmap)
+{
+    extern __shared__ uint8_t tma_smem[];
+    const MrgLaunch& P = R.m;
+    const MrgFpK K = load_fpk<SHV_MRG_ROWS_CKMASK>(P);
+    const unsigned lane = threadIdx.x & 31, warp = __shfl_sync(0xffffffffu, threadIdx.x >> 5, 0);
+    const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(tma_smem);
+    const uint32_t base = (sbase + 1023u) & ~1023u;
+    const uint32_t nwarps = blockDim.x >> 5;
+    double* lt = reinterpret_cast<double*>(tma_smem + (base - sbase) + nwarps * 4096u * kTmaBufs);
+    for (uint32_t k = threadIdx.x; k < 32 * kLaneTabEntries; k += blockDim.x) {
+        const uint32_t j = k & 31, e = k >> 5;
+        const uint32_t c = e / 18, rq = (e % 18) >> 1, h = e & 1;
+        const uint32_t M = c ? R.lanetab[j].b[rq] : R.lanetab[j].a[rq];
+        lt[k] = (double)(h ? (M & 0xffffu) : (M >> 16));
+    }
+    __syncthreads();
+    const uint32_t box0 = base + warp * (4096u * kTmaBufs);
+    uint32_t bsel = 0;
+    const uint64_t ntiles = (P.items + 31) / 32;
+    const uint64_t wstride = (uint64_t)gridDim.x * nwarps;
+    const uint32_t len = (uint32_t)P.seg_len, items = (uint32_t)P.items, nseg = P.nseg;  // items < 2^31 (host check)
+    uint64_t t = (uint64_t)blockIdx.x * nwarps + warp;
+    auto item = [&](uint64_t tt) {
+        uint32_t it = (uint32_t)(32 * tt) + lane;
+        return it < items ? it : items - 1;  // past the last segment: a clipped, discarded row
+    };
+    uint32_t w[6];
+    if (t < ntiles) load_words(P, item(t) / nseg, w);
+    for (; t < ntiles; t += wstride) {
+        const uint32_t it = item(t);
+        const uint32_t i = it / nseg, j = it - i * nseg;
+        uint32_t cur[6];
+#pragma unroll
+        for (int k = 0; k < 6; ++k) cur[k] = w[k];
+        if (t + wstride < ntiles) load_words(P, item(t + wstride) / nseg, w);  // prefetch
+        MrgIF g;
+        if (j < 32) {
+            g = lane_start(lt, j, cur, K);
+        } else {  // rows of more than 32 segments: (A^(32 S))^(j / 32) first
+            Mrg s{cur[0], cur[1], cur[2], cur[3], cur[4], cur[5]};
+            for (uint32_t jh = j >> 5, bit = 0; jh; ++bit, jh >>= 1)
+                if (jh & 1) apply(P.segpow[bit].a, P.segpow[bit].b, s);
+            const uint32_t v[6] = {s.x0, s.x1, s.x2, s.y0, s.y1, s.y2};
+            g = lane_start(lt, j & 31, v, K);
+        }
+        mrg_tma_rounds<KIND>(&tmap, K, lane, box0, bsel, g, len, 0, 32 * t);
     }
     if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
@@ -467,6 +615,30 @@ cudaError_t launch_mrg_fill_tma(const MrgLaunch& p, const CUtensorMap& tmap, int
 }
 
 
+size_t mrg_fill_rows_smem(int threads) { return mrg_fill_tma_smem(threads) + 32 * kLaneTabEntries * 8; }
+
+namespace {
+cudaError_t ensure_rows_smem(int threads)
+{
+    const size_t sm = mrg_fill_rows_smem(threads);
+    static std::atomic<uint64_t> d[2];
+    cudaError_t e = ensure_dyn_smem(mrg_fill_rows_kernel<kU32>, sm, d[0]);
+    if (e == cudaSuccess) e = ensure_dyn_smem(mrg_fill_rows_kernel<kF32>, sm, d[1]);
+    return e;
+}
+}  // namespace
+
+cudaError_t launch_mrg_fill_rows(const MrgRowsLaunch& p, const CUtensorMap& tmap, int kind, Grid g, cudaStream_t s)
+{
+    if (kind == kF64) return cudaErrorInvalidValue;
+    const size_t sm = mrg_fill_rows_smem((int)g.threads);
+    const cudaError_t e = ensure_rows_smem((int)g.threads);
+    if (e != cudaSuccess) return e;
+    if (kind == kF32) mrg_fill_rows_kernel<kF32><<<g.blocks, g.threads, sm, s>>>(p, tmap);
+    else mrg_fill_rows_kernel<kU32><<<g.blocks, g.threads, sm, s>>>(p, tmap);
+    return cudaGetLastError();
+}
+
 size_t mrg_fill_smem(int threads, int kind)
 {
     const bool staged = kind == kU32 ? mrg_staged<kU32>() : kind == kF32 ? mrg_staged<kF32>() : mrg_staged<kF64>();
@@ -530,6 +702,16 @@ cudaError_t mrg_occupancy(int kernel, int kind, bool fast, int threads, int* out
     }
     case kKMrgMc:
         return occ(mrg_mc_kernel, threads, 0, out);
+    case kKMrgFillRows: {
+        const size_t sm = mrg_fill_rows_smem(threads);
+        if (sm > 227u * 1024u) {
+            *out = 0;
+            return cudaSuccess;
+        }
+        if (const cudaError_t e = ensure_rows_smem(threads); e != cudaSuccess) return e;
+        return kind == kF32 ? occ(mrg_fill_rows_kernel<kF32>, threads, sm, out)
+                            : occ(mrg_fill_rows_kernel<kU32>, threads, sm, out);
+    }
     case kKMrgFillTma: {
         const size_t sm = mrg_fill_tma_smem(threads);
         if (!mrg_fill_tma_fits(threads)) {

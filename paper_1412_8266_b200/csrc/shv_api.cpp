@@ -27,6 +27,9 @@
 #ifndef SHV_MRG_ORDER
 #define SHV_MRG_ORDER 0  // lab: 0 = by row length, 1 = streams fastest, 2 = segments fastest
 #endif
+#ifndef SHV_MRG_ROWS
+#define SHV_MRG_ROWS 1  // MRG32k3a u32/f32 fills in row tiles (0: stream-per-lane tiles only; lab A/B)
+#endif
 #ifndef SHV_MRG_TMA
 #define SHV_MRG_TMA 1  // MRG32k3a fills store through TMA (0: per-lane vector stores; lab A/B)
 #endif
@@ -354,6 +357,30 @@ void split_tiles(const Handle& h, uint64_t ns, uint64_t len, uint64_t resident_t
     }
     *seg_len = bestL;
     *nseg = (uint32_t)bestS;
+}
+
+// Row-tile segment length of the MRG32k3a u32/f32 fill: a divisor S of n,
+// S % 32 == 0, in [64, 512], closest to 128 (C5: 128, one warp per 16-KB row;
+// tools/lab/tma_layout_lab.cu measured S = 128 fastest); 0 if n has none.
+uint64_t mrg_rows_seg_len(uint64_t n)
+{
+    static const uint64_t pref[] = {128, 96, 160, 192, 64, 224, 256, 320, 384, 448, 512};
+    for (uint64_t S : pref)
+        if (n % S == 0) return S;
+    return 0;
+}
+
+// The row-tile path takes 4-byte kinds at 16-B aligned outputs, no launch-config
+// segment override, tensor dims < 2^31, and enough tiles (>= 2 per resident warp)
+// that the stream-per-lane path's segment split would not balance better.
+bool mrg_rows_fit(const Handle& h, int kind, bool aligned32, uint64_t ns, uint64_t n)
+{
+    if (!SHV_MRG_ROWS || !SHV_MRG_TMA || kind == kF64 || !aligned32 || h.seg) return false;
+    const uint64_t S = mrg_rows_seg_len(n);
+    if (!S || ns * (n / S) >= (1ull << 31)) return false;
+    if (mrg_fill_rows_smem((int)h.tpb) > 227u * 1024u) return false;
+    const uint64_t tiles = (ns * (n / S) + 31) / 32;
+    return tiles >= 2 * resident_threads(h, kKMrgFillRows, kind, true) / 32;
 }
 
 // Leap Frog: the last base draw a call touches is (first+n-1) + K*(o+draws-1);
@@ -759,6 +786,32 @@ shv_status generate(shv_streams hid, T* out, uint64_t n, void* stream, int kind,
             const unsigned full = (unsigned)((ns + h.tpb - 1) / h.tpb);
             Grid g{vec ? blocks_for(h, kKTinyFill, kind, true, ns) : full, h.tpb};
             err = launch_tinymt_fill(P, kind, vec, g, s);
+        } else if (h.gen == SHV_GEN_MRG32K3A && mrg_rows_fit(h, kind, aligned32, ns, n)) {
+            // row tiles: a warp writes 32 consecutive segments of S values (C5: one 16-KB row)
+            const uint64_t S = mrg_rows_seg_len(n);
+            auto R = std::make_unique<MrgRowsLaunch>();
+            MrgLaunch* P = &R->m;
+            P->state = h.state;
+            P->stride = h.n;
+            P->stream_begin = s0;
+            P->ns = ns;
+            P->out = dst;
+            P->n = n;
+            P->seg_len = S;
+            P->nseg = (uint32_t)(n / S);
+            P->items = ns * P->nseg;
+            P->seg_fastest = 1;
+            fill_mrg_segments(h, 32 * S, 1, (P->nseg + 31) / 32, P);  // segpow: (A^(32 S))^(2^b)
+            const MatPair AS = pair_pow(S, 0);
+            R->lanetab[0] = P->seg0;  // A^o
+            for (uint32_t k = 1; k < 32 && k < P->nseg; ++k) R->lanetab[k] = pair_mul(R->lanetab[k - 1], AS);
+            CUtensorMap tmap;
+            if (!encode_rows_map(&tmap, dst, S, P->items, (int)sizeof(T))) {
+                err = cudaErrorInvalidValue;
+            } else {
+                Grid g{blocks_for(h, kKMrgFillRows, kind, true, (P->items + 31) / 32 * 32), h.tpb};
+                err = launch_mrg_fill_rows(*R, tmap, kind, g, s);
+            }
         } else if (h.gen == SHV_GEN_MRG32K3A) {
             bool vec = aligned32 && (n % 8 == 0);
             auto P = std::make_unique<MrgLaunch>();

@@ -184,6 +184,16 @@ cudaError_t launch_mrg_fill_tma(const MrgLaunch& p, const CUtensorMap& tmap, int
 size_t mrg_fill_tma_smem(int threads);
 bool mrg_fill_tma_fits(int threads);  // dynamic shared memory of a block within the 227-KB limit
 cudaError_t launch_mrg_mc(const MrgLaunch& p, Grid g, cudaStream_t s);
+// MRG32k3a fill in row tiles (u32/f32): m.seg_len = S, m.nseg = n / S (S * nseg = n,
+// S % 4 == 0), items = ns * nseg; lanetab[k] = A^(o + k S) for k < min(32, nseg),
+// m.segpow[b] = (A^(32 S))^(2^b). `tmap`: 2D map of [ns * nseg][S] values, box
+// 128 B x 32 rows, 128-B swizzle.
+struct MrgRowsLaunch {
+    MrgLaunch m;
+    MatPair lanetab[32];
+};
+cudaError_t launch_mrg_fill_rows(const MrgRowsLaunch& p, const CUtensorMap& tmap, int kind, Grid g, cudaStream_t s);
+size_t mrg_fill_rows_smem(int threads);
 cudaError_t launch_philox_fill(const PhiloxLaunch& p, int kind, bool fast, Grid g, cudaStream_t s);
 cudaError_t launch_philox_mc(const PhiloxLaunch& p, bool fast, Grid g, cudaStream_t s);
 // TinyMT32 Leap Frog launch (kernels_tinymt32.cu; R19): buf = the handle's
@@ -288,6 +298,7 @@ enum KernelId : int {
     kKLeapFill = 11,  // kind = output kind; `fast` = vector path; generator via leap_kernel_id
     kKLeapMc = 14,
     kKMrgFillTma = 17,  // after the leap ids 11..16
+    kKMrgFillRows = 18,
 };
 // Leap kernels are keyed by (base id + generator): 11..13 fills, 14..16 MC.
 constexpr int leap_kernel_id(int base, int lgen) { return base + lgen; }
@@ -301,7 +312,7 @@ cudaError_t leap_occupancy(int kernel, int kind, bool fast, int threads, int* ou
 inline cudaError_t max_blocks_per_sm(int kernel, int kind, bool fast, int threads, int* out)
 {
     switch (kernel) {
-    case kKSeed: case kKMrgFill: case kKMrgMc: case kKMrgFillTma:
+    case kKSeed: case kKMrgFill: case kKMrgMc: case kKMrgFillTma: case kKMrgFillRows:
         return mrg_occupancy(kernel, kind, fast, threads, out);
     case kKPhiloxFill: case kKPhiloxMc: case kKPhiloxFillKeyed: case kKPhiloxMcKeyed:
         return philox_occupancy(kernel, kind, fast, threads, out);

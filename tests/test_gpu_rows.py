@@ -1,0 +1,99 @@
+"""GPU parity of the MRG32k3a row-tile fill (mrg_fill_rows_kernel).
+
+The row-tile path covers the C3/C5 shapes at the default launch configuration
+(tests/test_gpu_parity.py compares those). Here small shapes are forced onto it
+by shrinking the resident grid (1 block of 32 threads per SM: the path is taken
+when there are at least 2 tiles of 32 segments per resident warp), and every
+value is compared with the oracle: segment lengths S = 128, 96, 160; rows of
+fewer than 32 segments (tiles spanning several rows), of exactly 32, and of more
+than 32 (the (A^(32 S))^(j / 32) jumps); a ragged last tile; non-zero offsets;
+STREAM and SUBSTREAM spacing with first > 0; u32 and f32. A CUDA profiler trace
+checks that the row-tile kernel is the one that ran.
+"""
+import numpy as np
+import pytest
+
+import workloads as W
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def shv():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_1412_8266_b200 as shv
+    return shv
+
+
+@pytest.fixture(scope="module")
+def orc():
+    import oracle
+    return oracle
+
+
+def kernels_of(fn):
+    from torch.profiler import ProfilerActivity, profile
+    with profile(activities=[ProfilerActivity.CUDA]) as p:
+        fn()
+        torch.cuda.synchronize()
+    return [e.name for e in p.events() if e.device_type.name == "CUDA"]
+
+
+CASES = [
+    # (n_streams, n, spacing, first, pre_offset)  S = mrg_rows_seg_len(n)
+    (300, 4096, W.SPACING_SUBSTREAM, 0, 0),      # S 128, nseg 32: a warp = one row
+    (301, 4096, W.SPACING_SUBSTREAM, 7, 1000),   # ragged last tile, offset 1000, first 7
+    (150, 8192, W.SPACING_STREAM, 3, 17),        # nseg 64: segments j >= 32
+    (70, 128 * 160, W.SPACING_SUBSTREAM, 0, 5),  # nseg 160
+    (3201, 384, W.SPACING_SUBSTREAM, 11, 0),     # nseg 3: tiles span rows, ragged
+    (2000, 480, W.SPACING_STREAM, 0, 33),        # S 96
+    (1400, 1120, W.SPACING_SUBSTREAM, 0, 0),     # S 160
+]
+
+
+@pytest.mark.parametrize("ns,n,spacing,first,pre", CASES)
+@pytest.mark.parametrize("kind", ["u32", "f32"])
+def test_rows_fill_matches_oracle(shv, orc, ns, n, spacing, first, pre, kind):
+    st = torch.empty(6 * ns, dtype=torch.int32, device="cuda")
+    h = shv.shv_streams_create_ex(W.MRG32K3A, [12345, 777, 31337, 4242, 99, 5], first, ns, spacing, st, 0,
+                                  torch.cuda.current_device(), None)
+    try:
+        shv.shv_set_launch_config(h, 1, 32, 0)
+        if pre:
+            shv.shv_jump(h, 0, pre, None)
+        tdt = torch.int32 if kind == "u32" else torch.float32
+        out = torch.empty(ns * n, dtype=tdt, device="cuda")
+        names = kernels_of(lambda: getattr(shv, "shv_generate_" + kind)(h, out, n, None))
+        assert any("mrg_fill_rows_kernel" in k for k in names), names
+        got = out.cpu().numpy().view(np.uint32).reshape(ns, n)
+        ref = orc.generate(W.MRG32K3A, [12345, 777, 31337, 4242, 99, 5], ns, n, first=first, spacing=spacing,
+                           offset=pre, kind=0 if kind == "u32" else 1)
+        ref = np.ascontiguousarray(ref).view(np.uint32).reshape(ns, n)
+        bad = np.nonzero(got != ref)
+        assert len(bad[0]) == 0, f"{len(bad[0])} mismatches, first at {[x[:5] for x in bad]}"
+        # the handle advanced by n: a second call continues the streams
+        out2 = torch.empty(ns * 256, dtype=tdt, device="cuda")
+        getattr(shv, "shv_generate_" + kind)(h, out2, 256, None)
+        ref2 = orc.generate(W.MRG32K3A, [12345, 777, 31337, 4242, 99, 5], ns, 256, first=first, spacing=spacing,
+                            offset=pre + n, kind=0 if kind == "u32" else 1)
+        assert np.array_equal(out2.cpu().numpy().view(np.uint32).reshape(ns, 256),
+                              np.ascontiguousarray(ref2).view(np.uint32).reshape(ns, 256))
+    finally:
+        shv.shv_streams_destroy(h)
+
+
+def test_rows_path_not_taken_for_few_tiles(shv):
+    """At the default launch configuration a small shape keeps the stream-per-lane TMA path."""
+    ns, n = 64, 4096
+    st = torch.empty(6 * ns, dtype=torch.int32, device="cuda")
+    h = shv.shv_streams_create_ex(W.MRG32K3A, [12345], 0, ns, W.SPACING_SUBSTREAM, st, 0,
+                                  torch.cuda.current_device(), None)
+    try:
+        out = torch.empty(ns * n, dtype=torch.int32, device="cuda")
+        names = kernels_of(lambda: shv.shv_generate_u32(h, out, n, None))
+        assert not any("mrg_fill_rows_kernel" in k for k in names), names
+        assert any("mrg_fill_tma_kernel" in k for k in names), names
+    finally:
+        shv.shv_streams_destroy(h)

@@ -29,6 +29,8 @@ int main(int argc, char** argv)
     const int reps = argc > 2 ? atoi(argv[2]) : 10;
     F(shv_streams_create_ex) F(shv_generate_u32) F(shv_streams_destroy) F(shv_last_error_message) F(shv_generate_f64) F(shv_mc_pi) F(shv_set_launch_config)
     const unsigned tpb = argc > 3 ? (unsigned)atoi(argv[3]) : 0;
+    const unsigned bps = argc > 4 ? (unsigned)atoi(argv[4]) : 0;
+    const int only_u32 = argc > 5 ? atoi(argv[5]) : 0;
     const uint64_t ns = 1 << 20, n = 4096;
     uint32_t* out; uint32_t* st; unsigned long long* ck;
     cudaMalloc(&out, ns * n * 8); cudaMalloc(&st, 24 * ns); cudaMalloc(&ck, 16);
@@ -36,12 +38,12 @@ int main(int argc, char** argv)
     uint32_t seed = 12345;
     printf("{\"lib\": \"%s\"", argv[1]);
     for (int gen = 1; gen <= 2; ++gen) {
-        for (int kind = 0; kind < 2; ++kind) {
+        for (int kind = 0; kind < (only_u32 ? 1 : 2); ++kind) {
             shv_streams hd;
             uint64_t nsk = kind ? ns / 2 : ns;  // f64: 16 GiB
             if (shv_streams_create_ex(&hd, gen, &seed, 1, 0, nsk, gen == 1 ? 1 : 0, gen == 1 ? st : nullptr, 24 * ns, 0, 0)) {
                 printf("create: %s\n", shv_last_error_message()); return 1; }
-            if (tpb) shv_set_launch_config(hd, 0, tpb, 0);
+            if (tpb || bps) shv_set_launch_config(hd, bps, tpb, 0);
             float best = 1e30f, sum = 0;
             for (int r = 0; r < reps + 2; ++r) {
                 cudaEventRecord(a);
@@ -61,6 +63,7 @@ int main(int argc, char** argv)
                    gen == 1 ? "mrg" : "philox", kind ? "f64" : "u32", best, sum / reps, bytes / (best * 1e-3) / 1e9, hck[0], hck[1]);
             shv_streams_destroy(hd);
         }
+        if (only_u32) continue;
         // MC pi, 2^38 samples
         shv_streams hd;
         shv_streams_create_ex(&hd, gen, &seed, 1, 0, ns, gen == 1 ? 1 : 0, gen == 1 ? st : nullptr, 24 * ns, 0, 0);

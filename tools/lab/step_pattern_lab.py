@@ -55,3 +55,46 @@ run("alternate", ["mrg", "philox"])
 run("alternate, 50 ms rest", ["mrg", "philox"], sleep=0.05)
 run("mrg only, 50 ms rest", ["mrg"], sleep=0.05)
 run("mrg only again", ["mrg"])
+
+
+def run_b2b(name, pattern, reps=30):
+    """Back to back as bench.py times the step: no host sync between fills, NVML sampled every 2 ms."""
+    import threading
+    hs = {"mrg": shv.shv_streams_create_ex(shv.SHV_GEN_MRG32K3A, [12345], 0, ns, 1, st, 0, 0, None),
+          "philox": shv.shv_streams_create_ex(shv.SHV_GEN_PHILOX4X32_10, [12345], 0, ns, 0, None, 0, 0, None)}
+    evs = []
+    samples, stop = [], [False]
+
+    def sampler():
+        while not stop[0]:
+            samples.append((pynvml.nvmlDeviceGetClockInfo(hd, pynvml.NVML_CLOCK_SM),
+                            pynvml.nvmlDeviceGetPowerUsage(hd) / 1000))
+            time.sleep(0.002)
+    th = threading.Thread(target=sampler)
+    th.start()
+    for r in range(reps):
+        for g in pattern:
+            ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+            ev[0].record()
+            shv.shv_generate_u32(hs[g], out, n, None)
+            ev[1].record()
+            evs.append((g, ev))
+    torch.cuda.synchronize()
+    stop[0] = True
+    th.join()
+    ts = {"mrg": [], "philox": []}
+    for g, ev in evs:
+        ts[g].append(ev[0].elapsed_time(ev[1]))
+    med = {k: sorted(v)[len(v) // 2] for k, v in ts.items() if v}
+    clk = sorted(c for c, _ in samples)
+    pw = sorted(p for _, p in samples)
+    print(f"{name:28s} " + " ".join(f"{k} {v:.3f} ms" for k, v in med.items()) +
+          f"  sm_clk median {clk[len(clk)//2]} min {clk[0]} MHz  power median {pw[len(pw)//2]:.0f} max {pw[-1]:.0f} W  ({len(samples)} samples)")
+    for h in hs.values():
+        shv.shv_streams_destroy(h)
+
+
+run_b2b("b2b mrg only", ["mrg"], reps=60)
+run_b2b("b2b philox only", ["philox"], reps=60)
+run_b2b("b2b alternate", ["mrg", "philox"], reps=40)
+run_b2b("b2b mrg only again", ["mrg"], reps=60)
