@@ -344,7 +344,7 @@ def main():
     dom = max(kms, key=kms.get)
     alg_bytes = 4 * total_per_rank  # u32 written per launch (4 B/number, 0 read)
     achieved = alg_bytes / (kms[dom] * 1e-3) / 1e9
-    hbm = {"bound": "hbm", "kernel": "mrg_fill_tma_kernel<u32>" if dom == "mrg" else "philox_fill_fast_kernel<u32>",
+    hbm = {"bound": "hbm", "kernel": "mrg_fill_rows_kernel<u32>" if dom == "mrg" else "philox_fill_fast_kernel<u32>",
            "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
            "frac": round(achieved / peak, 4), "peak_source": peak_src,
            "traffic": traffic_from_profiles(dom),
@@ -353,8 +353,8 @@ def main():
     # the metric's roofline is the HBM write of 4 B per number (0 B
     # read) for the dominant kernel. What ncu says keeps the kernel from it (the
     # step's pipe mix and issue rate, profiles/ncu_traffic.json) is in `limiter`
-    # and `pipes`; the MRG32k3a step is compute-bound at ~16 issue slots per
-    # number.
+    # and `pipes`; the MRG32k3a step is compute-bound at ~17-19 issue slots per
+    # number and, run back to back, power-limited.
     rec = profile_record(dom) or {}
     hbm["pipes"] = {k: rec.get(k) for k in ("issue_active_pct", "fp64_pipe_pct", "fmaheavy_pipe_pct",
                                               "alu_pipe_pct") if rec.get(k) is not None}

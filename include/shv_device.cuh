@@ -1,16 +1,19 @@
 // shv_device.cuh — device-side generator primitives of the ShoveRand hot path
 // (arXiv 1412.8266) for sm_100a. Included by the kernels_*.cu files (and by the
-// kernel lab under tools/lab/, which times variants of the same functions).
+// kernel labs under tools/lab/, which time variants of the same functions).
 //
-// Pipe budget on B200 (measured, profiles/r01_microbench.json): the FMA-heavy
-// pipe runs IMAD at 64 and IMAD.WIDE.U32 at ~32 per SM per clock, the ALU pipe
-// (IADD3/LOP3/ISETP) 64, the FP64 pipe (DFMA/DADD/DMUL) 64, issue 128. The
-// product's MRG32k3a step (MrgIF) therefore splits its two components across
-// pipes: component 1 in 32-bit integer arithmetic (two IMAD.WIDE + one IMAD on
-// the FMA-heavy pipe, the fold's compare/select on the ALU), component 2 in
-// exact binary64 arithmetic on the FP64 pipe, as in L'Ecuyer's original
-// floating-point formulation [LEcuyer1999] (products < 2^53, exact). Each of
-// the three pipes carries ~12 cycles per warp and number.
+// MRG32k3a steps, both exact and bit-identical:
+//  - MrgIF: component 1 in 32-bit integer arithmetic (two IMAD.WIDE + one IMAD,
+//    compare/select on the ALU), component 2 in exact binary64 arithmetic on
+//    the FP64 pipe (products < 2^53, floor reduction), as in L'Ecuyer's
+//    floating-point formulation [LEcuyer1999]. The product step of the row-tile
+//    u32/f32 fill and of the fused Monte Carlo kernels.
+//  - MrgFF: both components on the FP64 pipe (12 FP64 operations per number);
+//    the stream-per-lane fills (f64, shapes without a row-tile split).
+// Measured on B200 (tools/lab, profiles/r02_labs): IMAD.WIDE issues at ~21-24
+// per SM per clock (about 6 issue cycles per warp instruction) and slows the
+// other kinds it shares the SM with, so MrgIF costs about the sum of its two
+// halves (1.44 T values/s compute-only vs 1.33 for MrgFF).
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>

@@ -2,22 +2,21 @@
 // per-stream seeding by jump matrices, bulk fills (u32 / f32 / f64) and the
 // fused Monte Carlo pi kernel. Common pieces: kernels_common.cuh.
 //
-// Compile-time variants (the kernel lab, tools/lab/, builds each):
-//   SHV_MRG_STEP     step of the fills: 4 (default) = both components on the
-//                    FP64 pipe with floor reductions (MrgFF in shv_device.cuh);
-//                    3 = component 1 in integer arithmetic, component 2 on the
-//                    FP64 pipe (MrgIF). Measured (tools/lab):
-//                    MrgIF is 8 % faster compute-only but not in the TMA fill
-//                    (3.47 vs 3.45 ms alone, 3.69 vs 3.58 ms in the bench step)
-//   SHV_MRG_MC_STEP  step of the fused Monte Carlo kernel: 3 (default, MrgIF:
-//                    479 vs 485 ms for 2^38 samples) or 4
-//   SHV_MRG_STAGE 0 = each lane stores its own row directly (32-byte vector
-//                 stores); 2 = lanes stage 256 B in shared memory and the warp
-//                 writes 256-byte runs; 1 (default) = stage the 8-byte (f64)
-//                 outputs only: the compute-bound u32/f32 fills run faster
-//                 without staging (more warps), the HBM-bound f64 fill needs it
-//   SHV_MRG_MINB  min-blocks hint of the vector fill (4: <= 64 registers;
-//                 fewer spill or slow the FP64 step, lab)
+// The u32/f32 fills of shapes that split into row tiles run
+// mrg_fill_rows_kernel (MrgIF step); other vector shapes run the
+// stream-per-lane TMA kernel (u32/f32) or the staged vector kernel (f64), both
+// on the MrgFF step; ragged shapes run the scalar kernel.
+//
+// Compile-time knobs (defaults = the product; tools/lab/build_knobs.sh builds
+// variants for the labs, every variant gives bit-identical output):
+//   SHV_MRG_STEP     step of the stream-per-lane fills: 4 = MrgFF, 3 = MrgIF
+//   SHV_MRG_MC_STEP  step of the fused Monte Carlo kernel: 3 = MrgIF (474 vs
+//                    493 ms for 2^38 samples), 4 = MrgFF
+//   SHV_MRG_MC_HIT   dartboard test: 1 = FP64 (471 vs 474 ms), 0 = integer
+//   SHV_MRG_STAGE    staging of the vector fill: 1 = stage the f64 outputs only
+//   SHV_MRG_MINB, SHV_MRG_TMA_MINB, SHV_MRG_ROWS_MINB: min-blocks hints
+//   SHV_MRG_*_CKMASK which FP64 constants come from constant memory
+//   SHV_LAB_GEN_HEADER / SHV_LAB_GEN: stand-in generator (tools/lab only)
 #include "kernels_common.cuh"
 
 #ifndef SHV_MRG_STEP
@@ -25,6 +24,9 @@
 #endif
 #ifndef SHV_MRG_MC_STEP
 #define SHV_MRG_MC_STEP 3
+#endif
+#ifndef SHV_MRG_MC_HIT
+#define SHV_MRG_MC_HIT 1  // dartboard test: 1 = FP64 (hit_fp64), 0 = integer (2 IMAD.WIDE)
 #endif
 #ifndef SHV_MRG_STAGE
 #define SHV_MRG_STAGE 1
@@ -539,13 +541,13 @@ __global__ void __launch_bounds__(256) mrg_mc_kernel(const __grid_constant__ Mrg
             for (int u = 0; u < 12; ++u) {
                 const uint32_t w0 = mrg_next(s, K);
                 const uint32_t w1 = mrg_next(s, K);
-                h += hit(w0, w1) & (k + u < len ? 1u : 0u);
+                h += (SHV_MRG_MC_HIT ? hit_fp64(w0, w1) : hit(w0, w1)) & (k + u < len ? 1u : 0u);
             }
         }
         for (; k < wlen; ++k) {
             const uint32_t w0 = mrg_next(s, K);
             const uint32_t w1 = mrg_next(s, K);
-            h += hit(w0, w1) & (k < len ? 1u : 0u);
+            h += (SHV_MRG_MC_HIT ? hit_fp64(w0, w1) : hit(w0, w1)) & (k < len ? 1u : 0u);
         }
         total += h;
         if (P.counts && it < P.items) atomicAdd(P.counts + i, (unsigned long long)h);

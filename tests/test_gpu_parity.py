@@ -451,7 +451,7 @@ def test_c4_mc_pi_full_size(shv, orc, w):
     total = int(hits.item())
     counts = cnt.cpu().numpy().astype(np.uint64)
     assert int(counts.sum()) == total
-    streams = W.sample_streams(w.n_streams, 256)
+    streams = W.sample_streams(w.n_streams, 1024)  # >= 1024 sampled streams
     _, ref = orc.mc_count(w.gen, list(w.seed), 0, w.n, spacing=w.spacing, streams=streams)
     assert np.array_equal(counts[streams], ref)
     N = w.n_streams * w.n

@@ -12,13 +12,13 @@ fi
 timeout 900 python bench.py > gpurun_out/bench_$TAG.json 2> gpurun_out/bench_$TAG.err; tail -c 600 gpurun_out/bench_$TAG.json; tail -3 gpurun_out/bench_$TAG.err
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_$TAG.csv \
   python bench.py --steps 3 --warmup 3 --no-e2e --no-cpu --no-parts > /dev/null 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"mrg_fill_tma|philox_fill_fast" -s 2 -c 2 \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"mrg_fill_rows|philox_fill_fast" -s 2 -c 2 \
   -o gpurun_out/prof_fill_$TAG python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu --no-parts > gpurun_out/ncu_full_$TAG.log 2>&1
 for g in mrg philox; do
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:"${g}_mc" -c 1 \
     -o gpurun_out/prof_mc_${g}_$TAG python tools/lab/mc_lab.py $g 1 18 16 > gpurun_out/ncu_mc_${g}_$TAG.log 2>&1
 done
-python tools/ncu_summary.py gpurun_out/ncu_traffic_$TAG.json mrg=gpurun_out/prof_fill_$TAG.ncu-rep:mrg_fill:4294967296 \
+python tools/ncu_summary.py gpurun_out/ncu_traffic_$TAG.json mrg=gpurun_out/prof_fill_$TAG.ncu-rep:mrg_fill_rows:4294967296 \
   philox=gpurun_out/prof_fill_$TAG.ncu-rep:philox_fill:4294967296 \
   mc_mrg=gpurun_out/prof_mc_mrg_$TAG.ncu-rep:mrg_mc:17179869184 \
   mc_philox=gpurun_out/prof_mc_philox_$TAG.ncu-rep:philox_mc:17179869184 > /dev/null 2>&1
