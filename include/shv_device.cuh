@@ -419,10 +419,25 @@ struct Q4 {
     uint64_t x, y, z, w;
 };
 
+// 64-bit rotate as two 32-bit funnel shifts (SHF.L.W on the ALU pipe; R = 32
+// is a register swap). ptxas lowers the shift-or form to 4-5 instructions.
 template <int R>
 __device__ __forceinline__ uint64_t rotl64(uint64_t v)
 {
-    return (v << R) | (v >> (64 - R));
+    const uint32_t lo = (uint32_t)v, hi = (uint32_t)(v >> 32);
+    constexpr uint32_t S = R >= 32 ? (uint32_t)(R - 32) : (uint32_t)R;
+    uint32_t nh, nl;
+    if (R == 32) {
+        nh = lo;
+        nl = hi;
+    } else if (R < 32) {
+        nh = __funnelshift_l(lo, hi, S);
+        nl = __funnelshift_l(hi, lo, S);
+    } else {
+        nh = __funnelshift_l(hi, lo, S);
+        nl = __funnelshift_l(lo, hi, S);
+    }
+    return ((uint64_t)nh << 32) | nl;
 }
 
 template <int A, int B, bool ODD>
