@@ -483,6 +483,61 @@ __global__ void __launch_bounds__(kTrWarps * 32)
     if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
+// One player segment [p0, p1) of a lane's t-row, in kTrRows-player boxes.
+// HOIST (Philox, the low counter word does not wrap within the run): round 1
+// is hoisted (M0*b_lo by addition, M0*c0' constant; counter words 2, 3 = 0).
+// A separate instantiation per HOIST keeps ptxas from merging the two round
+// bodies into one with selects (18 extra adds per block measured in SASS).
+template <int KIND, int G, bool HOIST>
+__device__ __forceinline__ void leap_ctr_run(const LeapLaunch& P, const CUtensorMap* tmap, unsigned lane, uint32_t box,
+                                             const uint32_t* off, uint64_t tb, uint64_t p0, uint64_t p1, uint64_t b)
+{
+    const uint64_t q = (uint64_t)kPM0 * ((uint32_t)(b >> 32) ^ (uint32_t)P.k0);
+    uint64_t pa = (uint64_t)kPM0 * (uint32_t)b;
+    for (uint64_t pc = p0; pc < p1; pc += kTrRows) {
+        if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        __syncwarp();
+#pragma unroll 1
+        for (uint32_t q8 = 0; q8 < kTrRows; q8 += 8) {
+            const uint32_t rb = box + q8 * 128u;
+            uint32_t z[8];
+            if constexpr (G == kLeapPhilox) {
+                W4 v0, v1;
+                if constexpr (HOIST) {
+                    v0 = philox10_from_r2(pa, q, 0u, 0u, (uint32_t)P.k0, (uint32_t)P.k1);
+                    pa = add64w(pa, kPM0);
+                    v1 = philox10_from_r2(pa, q, 0u, 0u, (uint32_t)P.k0, (uint32_t)P.k1);
+                    pa = add64w(pa, kPM0);
+                } else {
+                    v0 = philox_blk(b, 0, (uint32_t)P.k0, (uint32_t)P.k1);
+                    v1 = philox_blk(b + 1, 0, (uint32_t)P.k0, (uint32_t)P.k1);
+                }
+                b += 2;
+                z[0] = v0.x; z[1] = v0.y; z[2] = v0.z; z[3] = v0.w;
+                z[4] = v1.x; z[5] = v1.y; z[6] = v1.z; z[7] = v1.w;
+            } else {  // Threefry4x64-20: words (lo, hi) of lanes 0..3 (R16)
+                const Q4 v = threefry20(b, 0, P.k0, P.k1);
+                b += 1;
+                z[0] = (uint32_t)v.x; z[1] = (uint32_t)(v.x >> 32); z[2] = (uint32_t)v.y; z[3] = (uint32_t)(v.y >> 32);
+                z[4] = (uint32_t)v.z; z[5] = (uint32_t)(v.z >> 32); z[6] = (uint32_t)v.w; z[7] = (uint32_t)(v.w >> 32);
+            }
+#pragma unroll
+            for (uint32_t k = 0; k < 8; ++k) {
+                const uint32_t w = KIND == kF32 ? __float_as_uint(to_f32(z[k])) : z[k];
+                asm volatile("st.shared.b32 [%0], %1;" ::"r"(rb + k * 128u + off[k]), "r"(w) : "memory");
+            }
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) {
+            asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(tmap),
+                         "r"(box), "r"((int)(32 * tb)), "r"((int)pc)
+                         : "memory");
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        }
+    }
+}
+
 // Counter-based Leap Frog by the same transposition (Philox: K % 4 == 0 and
 // first % 4 == 0; Threefry: K % 8 == 0 and first % 8 == 0): a lane's
 // consecutive base draws are consecutive words of consecutive counter blocks
@@ -508,55 +563,11 @@ __global__ void __launch_bounds__(kTrWarps * 32)
         const uint64_t p0 = ps * P.tr_pl;
         const uint64_t p1 = min(P.ns, p0 + P.tr_pl);
         // words per block: 4 (Philox) or 8 (Threefry); the run starts block-aligned
-        uint64_t b = (uint64_t)(((u128)(P.first + p0) + (u128)P.players * (o + t)) >> (G == kLeapPhilox ? 2 : 3));
-        // Philox: while the low counter word does not wrap within the run, round 1
-        // is hoisted (M0*b_lo by addition, M0*c0' constant; counter words 2, 3 = 0)
+        const uint64_t b = (uint64_t)(((u128)(P.first + p0) + (u128)P.players * (o + t)) >> (G == kLeapPhilox ? 2 : 3));
         const uint64_t nblk = (p1 - p0 + 3) / 4 + 2;
         const bool hoist = G == kLeapPhilox && (uint32_t)b <= 0xFFFFFFFFu - (uint32_t)min(nblk, (uint64_t)0xFFFFFFFFu);
-        const uint64_t q = (uint64_t)kPM0 * ((uint32_t)(b >> 32) ^ (uint32_t)P.k0);
-        uint64_t pa = (uint64_t)kPM0 * (uint32_t)b;
-        for (uint64_t pc = p0; pc < p1; pc += kTrRows) {
-            if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-            __syncwarp();
-#pragma unroll 1
-            for (uint32_t q8 = 0; q8 < kTrRows; q8 += 8) {
-                const uint32_t rb = box + q8 * 128u;
-                uint32_t z[8];
-                if constexpr (G == kLeapPhilox) {
-                    W4 v0, v1;
-                    if (hoist) {
-                        v0 = philox10_from_r2(pa, q, 0u, 0u, (uint32_t)P.k0, (uint32_t)P.k1);
-                        pa = add64w(pa, kPM0);
-                        v1 = philox10_from_r2(pa, q, 0u, 0u, (uint32_t)P.k0, (uint32_t)P.k1);
-                        pa = add64w(pa, kPM0);
-                    } else {
-                        v0 = philox_blk(b, 0, (uint32_t)P.k0, (uint32_t)P.k1);
-                        v1 = philox_blk(b + 1, 0, (uint32_t)P.k0, (uint32_t)P.k1);
-                    }
-                    b += 2;
-                    z[0] = v0.x; z[1] = v0.y; z[2] = v0.z; z[3] = v0.w;
-                    z[4] = v1.x; z[5] = v1.y; z[6] = v1.z; z[7] = v1.w;
-                } else {  // Threefry4x64-20: words (lo, hi) of lanes 0..3 (R16)
-                    const Q4 v = threefry20(b, 0, P.k0, P.k1);
-                    b += 1;
-                    z[0] = (uint32_t)v.x; z[1] = (uint32_t)(v.x >> 32); z[2] = (uint32_t)v.y; z[3] = (uint32_t)(v.y >> 32);
-                    z[4] = (uint32_t)v.z; z[5] = (uint32_t)(v.z >> 32); z[6] = (uint32_t)v.w; z[7] = (uint32_t)(v.w >> 32);
-                }
-#pragma unroll
-                for (uint32_t k = 0; k < 8; ++k) {
-                    const uint32_t w = KIND == kF32 ? __float_as_uint(to_f32(z[k])) : z[k];
-                    asm volatile("st.shared.b32 [%0], %1;" ::"r"(rb + k * 128u + off[k]), "r"(w) : "memory");
-                }
-            }
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            __syncwarp();
-            if (lane == 0) {
-                asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(&tmap),
-                             "r"(box), "r"((int)(32 * tb)), "r"((int)pc)
-                             : "memory");
-                asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-            }
-        }
+        if (__all_sync(0xffffffffu, hoist)) leap_ctr_run<KIND, G, G == kLeapPhilox>(P, &tmap, lane, box, off, tb, p0, p1, b);
+        else leap_ctr_run<KIND, G, false>(P, &tmap, lane, box, off, tb, p0, p1, b);
     }
     if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
