@@ -488,6 +488,9 @@ __global__ void __launch_bounds__(kTrWarps * 32)
 // is hoisted (M0*b_lo by addition, M0*c0' constant; counter words 2, 3 = 0).
 // A separate instantiation per HOIST keeps ptxas from merging the two round
 // bodies into one with selects (18 extra adds per block measured in SASS).
+#ifndef SHV_LEAP_NOSTORE
+#define SHV_LEAP_NOSTORE 0  // lab knob: compute only (profiles/r02_labs/lab23: 3.03 of 3.38 ms)
+#endif
 template <int KIND, int G, bool HOIST>
 __device__ __forceinline__ void leap_ctr_run(const LeapLaunch& P, const CUtensorMap* tmap, unsigned lane, uint32_t box,
                                              const uint32_t* off, uint64_t tb, uint64_t p0, uint64_t p1, uint64_t b)
@@ -521,6 +524,14 @@ __device__ __forceinline__ void leap_ctr_run(const LeapLaunch& P, const CUtensor
                 z[0] = (uint32_t)v.x; z[1] = (uint32_t)(v.x >> 32); z[2] = (uint32_t)v.y; z[3] = (uint32_t)(v.y >> 32);
                 z[4] = (uint32_t)v.z; z[5] = (uint32_t)(v.z >> 32); z[6] = (uint32_t)v.w; z[7] = (uint32_t)(v.w >> 32);
             }
+#if SHV_LEAP_NOSTORE  // lab knob: compute only (the store path's share of the time)
+            uint32_t x = 0;
+#pragma unroll
+            for (uint32_t k = 0; k < 8; ++k) x ^= z[k];
+            if (x == 0x9E3779B9u) asm volatile("st.shared.b32 [%0], %1;" ::"r"(rb), "r"(x) : "memory");
+        }
+    }
+#else
 #pragma unroll
             for (uint32_t k = 0; k < 8; ++k) {
                 const uint32_t w = KIND == kF32 ? __float_as_uint(to_f32(z[k])) : z[k];
@@ -536,6 +547,7 @@ __device__ __forceinline__ void leap_ctr_run(const LeapLaunch& P, const CUtensor
             asm volatile("cp.async.bulk.commit_group;" ::: "memory");
         }
     }
+#endif
 }
 
 // Counter-based Leap Frog by the same transposition (Philox: K % 4 == 0 and
