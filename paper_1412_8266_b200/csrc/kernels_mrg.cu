@@ -378,7 +378,8 @@ __global__ void __launch_bounds__(256, SHV_MRG_TMA_MINB)
 // The lane table in shared memory, FP64-split for the start jump: entry e of
 // lane matrix j at ltab[e * 32 + j] (lanes read consecutive 8-byte words),
 // e = (component c, row r, column q, half h) -> ((c * 3 + r) * 3 + q) * 2 + h,
-// half 0 = M >> 16, half 1 = M & 0xffff (exact doubles).
+// half 0 = M >> 16, half 1 = M & 0xffff (exact doubles). (double2 entries with
+// LDS.128 spill at the 48-register bound: 3.50 vs 3.43 ms, lab26.)
 constexpr uint32_t kLaneTabEntries = 36;
 
 // Row r of one component: (M v) mod m for canonical v (doubles) and the split
@@ -469,15 +470,17 @@ __global__ void __launch_bounds__(256, SHV_MRG_ROWS_MINB)
         uint32_t it = (uint32_t)(32 * tt) + lane;
         return it < items ? it : items - 1;  // past the last segment: a clipped, discarded row
     };
+    // it / nseg by the host's multiply-shift (Granlund-Montgomery, 31-bit numerators)
+    auto row = [&](uint32_t it) { return R.div_m ? __umulhi(it, R.div_m) >> R.div_s : it; };
     uint32_t w[6];
-    if (t < ntiles) load_words(P, item(t) / nseg, w);
+    if (t < ntiles) load_words(P, row(item(t)), w);
     for (; t < ntiles; t += wstride) {
         const uint32_t it = item(t);
-        const uint32_t i = it / nseg, j = it - i * nseg;
+        const uint32_t i = row(it), j = it - i * nseg;
         uint32_t cur[6];
 #pragma unroll
         for (int k = 0; k < 6; ++k) cur[k] = w[k];
-        if (t + wstride < ntiles) load_words(P, item(t + wstride) / nseg, w);  // prefetch
+        if (t + wstride < ntiles) load_words(P, row(item(t + wstride)), w);  // prefetch
         MrgIF g;
         if (j < 32) {
             g = lane_start(lt, j, cur, K);

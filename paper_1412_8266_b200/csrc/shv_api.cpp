@@ -805,6 +805,17 @@ shv_status generate(shv_streams hid, T* out, uint64_t n, void* stream, int kind,
             const MatPair AS = pair_pow(S, 0);
             R->lanetab[0] = P->seg0;  // A^o
             for (uint32_t k = 1; k < 32 && k < P->nseg; ++k) R->lanetab[k] = pair_mul(R->lanetab[k - 1], AS);
+            // item / nseg for items < 2^31: l = ceil(log2 nseg), m = ceil(2^(31+l) / nseg) < 2^32,
+            // floor(it / nseg) = (it * m) >> (31 + l) = umulhi(it, m) >> (l - 1)
+            if (P->nseg > 1) {
+                uint32_t l = 0;
+                while ((1ull << l) < P->nseg) ++l;
+                R->div_m = (uint32_t)(((1ull << (31 + l)) + P->nseg - 1) / P->nseg);
+                R->div_s = l - 1;
+            } else {
+                R->div_m = 0;
+                R->div_s = 0;
+            }
             CUtensorMap tmap;
             if (!encode_rows_map(&tmap, dst, S, P->items, (int)sizeof(T))) {
                 err = cudaErrorInvalidValue;

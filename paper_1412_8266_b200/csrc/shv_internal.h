@@ -191,6 +191,7 @@ cudaError_t launch_mrg_mc(const MrgLaunch& p, Grid g, cudaStream_t s);
 struct MrgRowsLaunch {
     MrgLaunch m;
     MatPair lanetab[32];
+    uint32_t div_m, div_s;  // item / nseg = umulhi(item, div_m) >> div_s for items < 2^31 (div_m = 0: nseg = 1)
 };
 cudaError_t launch_mrg_fill_rows(const MrgRowsLaunch& p, const CUtensorMap& tmap, int kind, Grid g, cudaStream_t s);
 size_t mrg_fill_rows_smem(int threads);

@@ -1,0 +1,7 @@
+B=tools/lab/build
+for r in 1 2; do for v in rt5 rt7; do
+  echo "$v $(timeout 120 $B/fill_lab $B/libshv_$v.so 40 256 0 1 | python3 -c "
+import json,sys; d=json.loads(sys.stdin.read()); v=d['mrg_u32']; print(v['ms_best'], v['ms_mean'], v['sum'])")"
+  sleep 3
+done; done 2>&1 | tee gpurun_out/lab27.txt
+timeout 900 python -m pytest tests/test_gpu_rows.py tests/test_gpu_parity.py -m gpu -q -x 2>&1 | tail -2 | tee -a gpurun_out/lab27.txt
