@@ -408,11 +408,11 @@ cudaError_t leap_tma_attr()
 // through consecutive base draws (players p, p+1, ...) of its t-row, starting
 // from A^(p_begin + K*t) * tr_s0 (per-bit tables: one jump per lane per
 // segment), and writes draw (p, t) as word t of box row p: all 32 lanes write
-// distinct words of one 128-B row (conflict-free; 128-B swizzle). Each
+// distinct words of one 128-B row (conflict-free, unswizzled box). Each
 // kTrRows-player box (kTrRows rows x 32 values) leaves by TMA; rows past the launch
 // and columns past n are clipped by the tensor map. Per value: the MRG step
-// (12 FP64 instructions) and one shared store, against three modular
-// products per component for the per-player recurrence.
+// (MrgIF) and one shared store, against three modular products per component
+// for the per-player recurrence.
 constexpr unsigned kTrWarps = 4;
 // Players per transposed box (rows of the 128-B wide box): 32 keeps a warp's
 // box at 4 KB, so up to 48 warps per SM stay resident (128-row, 16-KB boxes
@@ -440,10 +440,7 @@ __global__ void __launch_bounds__(kTrWarps * 32)
 #define SHV_TRF(i) (((SHV_LEAP_CKMASK >> (i)) & 1) ? c_leap_fpk[i] : P.fpk[i])
     const MrgFpK K{SHV_TRF(0), SHV_TRF(1), SHV_TRF(2), SHV_TRF(3), SHV_TRF(4), SHV_TRF(5), P.imul[0], P.imul[1]};
 #undef SHV_TRF
-    // swizzled offset of word `lane` in a box row r: depends on r & 7 only
-    uint32_t off[8];
-#pragma unroll
-    for (uint32_t k = 0; k < 8; ++k) off[k] = ((((lane >> 2) ^ k)) << 4) + (lane & 3u) * 4u;
+    const uint32_t lo4 = lane * 4u;  // unswizzled box: word `lane` of each 128-B row
     const uint64_t items = P.tr_tb * P.tr_ps;
     const uint64_t wstride = (uint64_t)gridDim.x * (blockDim.x >> 5);
     for (uint64_t it = (uint64_t)blockIdx.x * (blockDim.x >> 5) + warp; it < items; it += wstride) {
@@ -467,7 +464,7 @@ __global__ void __launch_bounds__(kTrWarps * 32)
                 for (uint32_t k = 0; k < 8; ++k) {
                     const uint32_t z = mrg_next(g, K);
                     const uint32_t w = KIND == kF32 ? __float_as_uint(to_f32(z)) : z;
-                    asm volatile("st.shared.b32 [%0], %1;" ::"r"(rb + k * 128u + off[k]), "r"(w) : "memory");
+                    asm volatile("st.shared.b32 [%0], %1;" ::"r"(rb + lo4 + k * 128u), "r"(w) : "memory");
                 }
             }
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -493,7 +490,7 @@ __global__ void __launch_bounds__(kTrWarps * 32)
 #endif
 template <int KIND, int G, bool HOIST>
 __device__ __forceinline__ void leap_ctr_run(const LeapLaunch& P, const CUtensorMap* tmap, unsigned lane, uint32_t box,
-                                             const uint32_t* off, uint64_t tb, uint64_t p0, uint64_t p1, uint64_t b)
+                                             uint32_t lo4, uint64_t tb, uint64_t p0, uint64_t p1, uint64_t b)
 {
     const uint64_t q = (uint64_t)kPM0 * ((uint32_t)(b >> 32) ^ (uint32_t)P.k0);
     uint64_t pa = (uint64_t)kPM0 * (uint32_t)b;
@@ -535,7 +532,7 @@ __device__ __forceinline__ void leap_ctr_run(const LeapLaunch& P, const CUtensor
 #pragma unroll
             for (uint32_t k = 0; k < 8; ++k) {
                 const uint32_t w = KIND == kF32 ? __float_as_uint(to_f32(z[k])) : z[k];
-                asm volatile("st.shared.b32 [%0], %1;" ::"r"(rb + k * 128u + off[k]), "r"(w) : "memory");
+                asm volatile("st.shared.b32 [%0], %1;" ::"r"(rb + lo4 + k * 128u), "r"(w) : "memory");
             }
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -563,9 +560,7 @@ __global__ void __launch_bounds__(kTrWarps * 32)
     const unsigned lane = threadIdx.x & 31, warp = __shfl_sync(0xffffffffu, threadIdx.x >> 5, 0);
     const uint32_t base = ((uint32_t)__cvta_generic_to_shared(trp_smem) + 1023u) & ~1023u;
     const uint32_t box = base + warp * (kTrRows * 128u);
-    uint32_t off[8];
-#pragma unroll
-    for (uint32_t k = 0; k < 8; ++k) off[k] = ((((lane >> 2) ^ k)) << 4) + (lane & 3u) * 4u;
+    const uint32_t lo4 = lane * 4u;  // unswizzled box: word `lane` of each 128-B row
     const uint64_t items = P.tr_tb * P.tr_ps;
     const uint64_t wstride = (uint64_t)gridDim.x * (blockDim.x >> 5);
     const u128 o = ((u128)P.o_hi << 64) | P.o_lo;
@@ -578,8 +573,8 @@ __global__ void __launch_bounds__(kTrWarps * 32)
         const uint64_t b = (uint64_t)(((u128)(P.first + p0) + (u128)P.players * (o + t)) >> (G == kLeapPhilox ? 2 : 3));
         const uint64_t nblk = (p1 - p0 + 3) / 4 + 2;
         const bool hoist = G == kLeapPhilox && (uint32_t)b <= 0xFFFFFFFFu - (uint32_t)min(nblk, (uint64_t)0xFFFFFFFFu);
-        if (__all_sync(0xffffffffu, hoist)) leap_ctr_run<KIND, G, G == kLeapPhilox>(P, &tmap, lane, box, off, tb, p0, p1, b);
-        else leap_ctr_run<KIND, G, false>(P, &tmap, lane, box, off, tb, p0, p1, b);
+        if (__all_sync(0xffffffffu, hoist)) leap_ctr_run<KIND, G, G == kLeapPhilox>(P, &tmap, lane, box, lo4, tb, p0, p1, b);
+        else leap_ctr_run<KIND, G, false>(P, &tmap, lane, box, lo4, tb, p0, p1, b);
     }
     if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }

@@ -432,7 +432,10 @@ PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder()
 
 // 2D map of `ns` rows x `n` values of `elem` bytes at `out` (row-major), box
 // 128 B x 32 rows with the 128-byte swizzle (mrg_fill_tma_kernel).
-bool encode_rows_map(CUtensorMap* m, void* out, uint64_t n, uint64_t ns, int elem, uint32_t box_rows = 32)
+// Transposed fills write their boxes unswizzled: lane l stores word l of a box row, so the
+// 32 lanes of one st.shared cover one 128-B row (conflict-free) at base + row * 128 + 4 l.
+bool encode_rows_map(CUtensorMap* m, void* out, uint64_t n, uint64_t ns, int elem, uint32_t box_rows = 32,
+                     bool swizzle = true)
 {
     const auto enc = tensor_map_encoder();
     if (!enc) return false;
@@ -441,7 +444,8 @@ bool encode_rows_map(CUtensorMap* m, void* out, uint64_t n, uint64_t ns, int ele
     const cuuint32_t box[2] = {128u / (cuuint32_t)elem, box_rows};
     const cuuint32_t estr[2] = {1, 1};
     return enc(m, elem == 8 ? CU_TENSOR_MAP_DATA_TYPE_UINT64 : CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, out, dims, strides,
-               box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+               box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+               swizzle ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
@@ -679,7 +683,7 @@ shv_status generate(shv_streams hid, T* out, uint64_t n, void* stream, int kind,
             // an encode failure falls back to the per-player kernels below
             const bool tr = SHV_MRG_TMA && (h.gen == SHV_GEN_MRG32K3A || trp) && kind != kF64 && n % 4 == 0 &&
                             ((uintptr_t)dst % 16 == 0) && n < (1ull << 31) && ns < (1ull << 31) - 256 &&
-                            encode_rows_map(&trmap, dst, n, ns, (int)sizeof(T), rows);
+                            encode_rows_map(&trmap, dst, n, ns, (int)sizeof(T), rows, false);
             if (tr) {
                 int bps = 0;
                 err = trp ? leap_ctr_tr_blocks_per_sm(lg, kind, &bps) : leap_mrg_tr_blocks_per_sm(kind, &bps);
