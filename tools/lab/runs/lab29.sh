@@ -1,0 +1,6 @@
+B=tools/lab/build
+for r in 1 2; do for v in mh1 mh2; do
+  echo "$v $(timeout 120 $B/fill_lab $B/libshv_$v.so 1 256 0 0 | python3 -c "
+import json,sys; d=json.loads(sys.stdin.read()); print(d['mrg_mc'])")"
+  sleep 5
+done; done 2>&1 | tee gpurun_out/lab29.txt
