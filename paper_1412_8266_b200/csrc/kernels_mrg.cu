@@ -388,12 +388,12 @@ constexpr uint32_t kLaneTabEntries = 36;
 // DESIGN.md §4.2), X = (Ah mod m) * 2^16 + Al < 2^50 exact, X mod m likewise.
 // 13 FP64 operations, no IMAD.WIDE (which the start jump's integer matvec
 // spends 37 of per apply, ~6 issue cycles each on B200; tools/lab/pipe_mix2_lab.cu).
-__device__ __forceinline__ double split_row_mod(const double* __restrict__ lt, uint32_t e0, uint32_t jl, double v0, double v1,
-                                                double v2, double inv, double m, double magic)
+__device__ __forceinline__ double split_row_mod(const double* __restrict__ lt, uint32_t stride, uint32_t e0, double v0,
+                                                double v1, double v2, double inv, double m, double magic)
 {
-    const double h0 = lt[(e0 + 0) * 32 + jl], l0 = lt[(e0 + 1) * 32 + jl];
-    const double h1 = lt[(e0 + 2) * 32 + jl], l1 = lt[(e0 + 3) * 32 + jl];
-    const double h2 = lt[(e0 + 4) * 32 + jl], l2 = lt[(e0 + 5) * 32 + jl];
+    const double h0 = lt[(e0 + 0) * stride], l0 = lt[(e0 + 1) * stride];
+    const double h1 = lt[(e0 + 2) * stride], l1 = lt[(e0 + 3) * stride];
+    const double h2 = lt[(e0 + 4) * stride], l2 = lt[(e0 + 5) * stride];
     const double ah = __fma_rn(h2, v2, __fma_rn(h1, v1, __dmul_rn(h0, v0)));
     const double al = __fma_rn(l2, v2, __fma_rn(l1, v1, __dmul_rn(l0, v0)));
     const double kh = __dadd_rn(__fma_rd(ah, inv, magic), -magic);
@@ -403,19 +403,35 @@ __device__ __forceinline__ double split_row_mod(const double* __restrict__ lt, u
     return __fma_rn(-kx, m, x);
 }
 
-// Start state of a row-tile lane: lanetab[jl] * (x, y), on the FP64 pipe.
+// M * (x, y) on the FP64 pipe for a split matrix at `tab` (entries `stride`
+// doubles apart: the lane table with stride 32 at lane jl, or the run-step
+// matrix with stride 1), returned as the MrgIF state.
+__device__ __forceinline__ MrgIF apply_split(const double* __restrict__ tab, uint32_t stride, double x0, double x1,
+                                             double x2, double y0, double y1, double y2, const MrgFpK& K)
+{
+    MrgIF g;
+    g.x0 = (uint32_t)__double2loint(__dadd_rn(split_row_mod(tab, stride, 0, x0, x1, x2, K.inv1, K.m1, K.magic), K.magic));
+    g.x1 = (uint32_t)__double2loint(__dadd_rn(split_row_mod(tab, stride, 6, x0, x1, x2, K.inv1, K.m1, K.magic), K.magic));
+    g.x2 = (uint32_t)__double2loint(__dadd_rn(split_row_mod(tab, stride, 12, x0, x1, x2, K.inv1, K.m1, K.magic), K.magic));
+    g.y0 = split_row_mod(tab, stride, 18, y0, y1, y2, K.inv2, K.m2, K.magic);
+    g.y1 = split_row_mod(tab, stride, 24, y0, y1, y2, K.inv2, K.m2, K.magic);
+    g.y2 = split_row_mod(tab, stride, 30, y0, y1, y2, K.inv2, K.m2, K.magic);
+    return g;
+}
+
+// Start state of a row-tile lane: lanetab[jl] * (x, y).
 __device__ __forceinline__ MrgIF lane_start(const double* __restrict__ lt, uint32_t jl, const uint32_t w[6], const MrgFpK& K)
 {
-    const double x0 = __uint2double_rn(w[0]), x1 = __uint2double_rn(w[1]), x2 = __uint2double_rn(w[2]);
-    const double y0 = __uint2double_rn(w[3]), y1 = __uint2double_rn(w[4]), y2 = __uint2double_rn(w[5]);
-    MrgIF g;
-    g.x0 = (uint32_t)__double2loint(__dadd_rn(split_row_mod(lt, 0, jl, x0, x1, x2, K.inv1, K.m1, K.magic), K.magic));
-    g.x1 = (uint32_t)__double2loint(__dadd_rn(split_row_mod(lt, 6, jl, x0, x1, x2, K.inv1, K.m1, K.magic), K.magic));
-    g.x2 = (uint32_t)__double2loint(__dadd_rn(split_row_mod(lt, 12, jl, x0, x1, x2, K.inv1, K.m1, K.magic), K.magic));
-    g.y0 = split_row_mod(lt, 18, jl, y0, y1, y2, K.inv2, K.m2, K.magic);
-    g.y1 = split_row_mod(lt, 24, jl, y0, y1, y2, K.inv2, K.m2, K.magic);
-    g.y2 = split_row_mod(lt, 30, jl, y0, y1, y2, K.inv2, K.m2, K.magic);
-    return g;
+    return apply_split(lt + jl, 32, __uint2double_rn(w[0]), __uint2double_rn(w[1]), __uint2double_rn(w[2]),
+                       __uint2double_rn(w[3]), __uint2double_rn(w[4]), __uint2double_rn(w[5]), K);
+}
+
+// A lane that ended segment j of a tile (at offset (j + 1) S) continues with
+// segment j + 32 of the next tile of its row: A^(31 S) * state (run mode).
+__device__ __forceinline__ MrgIF lane_advance(const double* __restrict__ st31, const MrgIF& g, const MrgFpK& K)
+{
+    return apply_split(st31, 1, __uint2double_rn(g.x0), __uint2double_rn(g.x1), __uint2double_rn(g.x2), g.y0, g.y1,
+                       g.y2, K);
 }
 
 __device__ __forceinline__ void load_words(const MrgLaunch& P, uint32_t i, uint32_t w[6])
@@ -441,7 +457,7 @@ __device__ __forceinline__ void load_words(const MrgLaunch& P, uint32_t i, uint3
 #ifndef SHV_MRG_ROWS_MINB
 #define SHV_MRG_ROWS_MINB 5  // <= 48 registers: 5 blocks of 256 per SM (lab: 3.50 vs 3.56 ms at 4)
 #endif
-template <int KIND>
+template <int KIND, bool RUN>
 __global__ void __launch_bounds__(256, SHV_MRG_ROWS_MINB)
     mrg_fill_rows_kernel(const __grid_constant__ MrgRowsLaunch R, const __grid_constant__ CUtensorMap tmap)
 {
@@ -453,15 +469,45 @@ __global__ void __launch_bounds__(256, SHV_MRG_ROWS_MINB)
     const uint32_t base = (sbase + 1023u) & ~1023u;
     const uint32_t nwarps = blockDim.x >> 5;
     double* lt = reinterpret_cast<double*>(tma_smem + (base - sbase) + nwarps * 4096u * kTmaBufs);
-    for (uint32_t k = threadIdx.x; k < 32 * kLaneTabEntries; k += blockDim.x) {
-        const uint32_t j = k & 31, e = k >> 5;
+    double* st31 = lt + 32 * kLaneTabEntries;  // run-step matrix A^(31 S), same split layout, stride 1
+    for (uint32_t k = threadIdx.x; k < 33 * kLaneTabEntries; k += blockDim.x) {
+        const bool step = k >= 32 * kLaneTabEntries;
+        const uint32_t j = step ? 0 : (k & 31), e = step ? k - 32 * kLaneTabEntries : k >> 5;
         const uint32_t c = e / 18, rq = (e % 18) >> 1, h = e & 1;
-        const uint32_t M = c ? R.lanetab[j].b[rq] : R.lanetab[j].a[rq];
+        const MatPair& mp = step ? R.step31 : R.lanetab[j];
+        const uint32_t M = c ? mp.b[rq] : mp.a[rq];
         lt[k] = (double)(h ? (M & 0xffffu) : (M >> 16));
     }
     __syncthreads();
     const uint32_t box0 = base + warp * (4096u * kTmaBufs);
     uint32_t bsel = 0;
+    if constexpr (RUN) {
+        // Run mode (rows of nh = nseg / 32 >= 2 tiles): a warp owns a run of up to R.run
+        // consecutive tiles of one row; the first starts by the per-bit jumps of its tile
+        // index and the lane table, each next one by one A^(31 S) step per lane (the
+        // per-tile jump would cost popcount(jh) integer mat-vecs per lane).
+        const uint32_t len = (uint32_t)P.seg_len;
+        const uint64_t nruns = P.ns * (uint64_t)R.rpr;
+        const uint64_t wstride = (uint64_t)gridDim.x * nwarps;
+        for (uint64_t run = (uint64_t)blockIdx.x * nwarps + warp; run < nruns; run += wstride) {
+            const uint64_t i = run / R.rpr;
+            const uint32_t jh0 = (uint32_t)(run - i * R.rpr) * R.run;
+            const uint32_t cnt = min(R.run, R.nh - jh0);
+            uint32_t w[6];
+            load_words(P, (uint32_t)i, w);
+            Mrg s{w[0], w[1], w[2], w[3], w[4], w[5]};
+            for (uint32_t jh = jh0, bit = 0; jh; ++bit, jh >>= 1)
+                if (jh & 1) apply(P.segpow[bit].a, P.segpow[bit].b, s);
+            const uint32_t v[6] = {s.x0, s.x1, s.x2, s.y0, s.y1, s.y2};
+            MrgIF g = lane_start(lt, lane, v, K);
+            for (uint32_t k = 0; k < cnt; ++k) {
+                if (k) g = lane_advance(st31, g, K);
+                mrg_tma_rounds<KIND>(&tmap, K, lane, box0, bsel, g, len, 0, i * P.nseg + 32ull * (jh0 + k));
+            }
+        }
+        if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+        return;
+    } else {
     const uint64_t ntiles = (P.items + 31) / 32;
     const uint64_t wstride = (uint64_t)gridDim.x * nwarps;
     const uint32_t len = (uint32_t)P.seg_len, items = (uint32_t)P.items, nseg = P.nseg;  // items < 2^31 (host check)
@@ -494,6 +540,7 @@ __global__ void __launch_bounds__(256, SHV_MRG_ROWS_MINB)
         mrg_tma_rounds<KIND>(&tmap, K, lane, box0, bsel, g, len, 0, 32 * t);
     }
     if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    }
 }
 
 // MRG32k3a fill, scalar path (any row length / element-aligned pointer).
@@ -620,15 +667,17 @@ cudaError_t launch_mrg_fill_tma(const MrgLaunch& p, const CUtensorMap& tmap, int
 }
 
 
-size_t mrg_fill_rows_smem(int threads) { return mrg_fill_tma_smem(threads) + 32 * kLaneTabEntries * 8; }
+size_t mrg_fill_rows_smem(int threads) { return mrg_fill_tma_smem(threads) + 33 * kLaneTabEntries * 8; }
 
 namespace {
 cudaError_t ensure_rows_smem(int threads)
 {
     const size_t sm = mrg_fill_rows_smem(threads);
-    static std::atomic<uint64_t> d[2];
-    cudaError_t e = ensure_dyn_smem(mrg_fill_rows_kernel<kU32>, sm, d[0]);
-    if (e == cudaSuccess) e = ensure_dyn_smem(mrg_fill_rows_kernel<kF32>, sm, d[1]);
+    static std::atomic<uint64_t> d[4];
+    cudaError_t e = ensure_dyn_smem(mrg_fill_rows_kernel<kU32, false>, sm, d[0]);
+    if (e == cudaSuccess) e = ensure_dyn_smem(mrg_fill_rows_kernel<kF32, false>, sm, d[1]);
+    if (e == cudaSuccess) e = ensure_dyn_smem(mrg_fill_rows_kernel<kU32, true>, sm, d[2]);
+    if (e == cudaSuccess) e = ensure_dyn_smem(mrg_fill_rows_kernel<kF32, true>, sm, d[3]);
     return e;
 }
 }  // namespace
@@ -639,8 +688,13 @@ cudaError_t launch_mrg_fill_rows(const MrgRowsLaunch& p, const CUtensorMap& tmap
     const size_t sm = mrg_fill_rows_smem((int)g.threads);
     const cudaError_t e = ensure_rows_smem((int)g.threads);
     if (e != cudaSuccess) return e;
-    if (kind == kF32) mrg_fill_rows_kernel<kF32><<<g.blocks, g.threads, sm, s>>>(p, tmap);
-    else mrg_fill_rows_kernel<kU32><<<g.blocks, g.threads, sm, s>>>(p, tmap);
+    if (p.nh) {
+        if (kind == kF32) mrg_fill_rows_kernel<kF32, true><<<g.blocks, g.threads, sm, s>>>(p, tmap);
+        else mrg_fill_rows_kernel<kU32, true><<<g.blocks, g.threads, sm, s>>>(p, tmap);
+    } else {
+        if (kind == kF32) mrg_fill_rows_kernel<kF32, false><<<g.blocks, g.threads, sm, s>>>(p, tmap);
+        else mrg_fill_rows_kernel<kU32, false><<<g.blocks, g.threads, sm, s>>>(p, tmap);
+    }
     return cudaGetLastError();
 }
 
@@ -714,8 +768,8 @@ cudaError_t mrg_occupancy(int kernel, int kind, bool fast, int threads, int* out
             return cudaSuccess;
         }
         if (const cudaError_t e = ensure_rows_smem(threads); e != cudaSuccess) return e;
-        return kind == kF32 ? occ(mrg_fill_rows_kernel<kF32>, threads, sm, out)
-                            : occ(mrg_fill_rows_kernel<kU32>, threads, sm, out);
+        return kind == kF32 ? occ(mrg_fill_rows_kernel<kF32, false>, threads, sm, out)
+                            : occ(mrg_fill_rows_kernel<kU32, false>, threads, sm, out);
     }
     case kKMrgFillTma: {
         const size_t sm = mrg_fill_tma_smem(threads);

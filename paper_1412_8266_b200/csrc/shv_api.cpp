@@ -820,11 +820,26 @@ shv_status generate(shv_streams hid, T* out, uint64_t n, void* stream, int kind,
                 R->div_m = 0;
                 R->div_s = 0;
             }
+            // run mode for rows of several tiles: runs of consecutive tiles per warp, about
+            // four runs per resident warp (balance) and as long as possible (the first tile
+            // of a run pays the per-bit jumps)
+            R->nh = R->run = R->rpr = 0;
+            if (P->nseg % 32 == 0 && P->nseg >= 64) {
+                R->nh = P->nseg / 32;
+                const uint64_t warps = resident_threads(h, kKMrgFillRows, kind, true) / 32;
+                const uint64_t tiles = ns * R->nh;
+                uint64_t run = tiles / (4 * (warps ? warps : 1));
+                run = run < 1 ? 1 : run > R->nh ? R->nh : run;
+                R->run = (uint32_t)run;
+                R->rpr = (uint32_t)((R->nh + run - 1) / run);
+                R->step31 = pair_pow((u128)31 * S, 0);
+            }
             CUtensorMap tmap;
             if (!encode_rows_map(&tmap, dst, S, P->items, (int)sizeof(T))) {
                 err = cudaErrorInvalidValue;
             } else {
-                Grid g{blocks_for(h, kKMrgFillRows, kind, true, (P->items + 31) / 32 * 32), h.tpb};
+                const uint64_t work = R->nh ? ns * R->rpr * 32 : (P->items + 31) / 32 * 32;
+                Grid g{blocks_for(h, kKMrgFillRows, kind, true, work), h.tpb};
                 err = launch_mrg_fill_rows(*R, tmap, kind, g, s);
             }
         } else if (h.gen == SHV_GEN_MRG32K3A) {

@@ -186,12 +186,16 @@ bool mrg_fill_tma_fits(int threads);  // dynamic shared memory of a block within
 cudaError_t launch_mrg_mc(const MrgLaunch& p, Grid g, cudaStream_t s);
 // MRG32k3a fill in row tiles (u32/f32): m.seg_len = S, m.nseg = n / S (S * nseg = n,
 // S % 4 == 0), items = ns * nseg; lanetab[k] = A^(o + k S) for k < min(32, nseg),
-// m.segpow[b] = (A^(32 S))^(2^b). `tmap`: 2D map of [ns * nseg][S] values, box
+// m.segpow[b] = (A^(32 S))^(2^b) (per-bit tables of the tile index within a row). `tmap`: 2D map of [ns * nseg][S] values, box
 // 128 B x 32 rows, 128-B swizzle.
 struct MrgRowsLaunch {
     MrgLaunch m;
     MatPair lanetab[32];
     uint32_t div_m, div_s;  // item / nseg = umulhi(item, div_m) >> div_s for items < 2^31 (div_m = 0: nseg = 1)
+    // run mode (nseg = 32 nh, nh >= 2; nh = 0 otherwise): work item = run of `run` consecutive
+    // tiles of one row (rpr runs per row); lanes step between tiles by step31 = A^(31 S)
+    uint32_t nh, run, rpr;
+    MatPair step31;
 };
 cudaError_t launch_mrg_fill_rows(const MrgRowsLaunch& p, const CUtensorMap& tmap, int kind, Grid g, cudaStream_t s);
 size_t mrg_fill_rows_smem(int threads);

@@ -6,7 +6,9 @@ by shrinking the resident grid (1 block of 32 threads per SM: the path is taken
 when there are at least 2 tiles of 32 segments per resident warp), and every
 value is compared with the oracle: segment lengths S = 128, 96, 160; rows of
 fewer than 32 segments (tiles spanning several rows), of exactly 32, and of more
-than 32 (the (A^(32 S))^(j / 32) jumps); a ragged last tile; non-zero offsets;
+than 32 (the (A^(32 S))^(j / 32) jumps), and rows of 43 tiles in run mode (a
+warp carries its lanes from tile to tile by A^(31 S), ragged last run); a ragged
+last tile; non-zero offsets;
 STREAM and SUBSTREAM spacing with first > 0; u32 and f32. A CUDA profiler trace
 checks that the row-tile kernel is the one that ran.
 """
@@ -50,6 +52,7 @@ CASES = [
     (3201, 384, W.SPACING_SUBSTREAM, 11, 0),     # nseg 3: tiles span rows, ragged
     (2000, 480, W.SPACING_STREAM, 0, 33),        # S 96
     (1400, 1120, W.SPACING_SUBSTREAM, 0, 0),     # S 160
+    (64, 128 * 32 * 43, W.SPACING_SUBSTREAM, 5, 77),  # run mode: 43 tiles per row, runs of 4 (last 3)
 ]
 
 
