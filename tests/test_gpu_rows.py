@@ -6,9 +6,9 @@ by shrinking the resident grid (1 block of 32 threads per SM: the path is taken
 when there are at least 2 tiles of 32 segments per resident warp), and every
 value is compared with the oracle: segment lengths S = 128, 96, 160; rows of
 fewer than 32 segments (tiles spanning several rows), of exactly 32, and of more
-than 32 (the (A^(32 S))^(j / 32) jumps), and rows of 43 tiles in run mode (a
-warp carries its lanes from tile to tile by A^(31 S), ragged last run); a ragged
-last tile; non-zero offsets;
+than 32 (nseg 40: the per-tile (A^(32 S))^(j / 32) jumps; nseg a multiple of 32:
+run mode, where a warp carries its lanes from tile to tile by A^(31 S), with a
+ragged last run at 43 tiles per row); a ragged last tile; non-zero offsets;
 STREAM and SUBSTREAM spacing with first > 0; u32 and f32. A CUDA profiler trace
 checks that the row-tile kernel is the one that ran.
 """
@@ -47,7 +47,8 @@ CASES = [
     # (n_streams, n, spacing, first, pre_offset)  S = mrg_rows_seg_len(n)
     (300, 4096, W.SPACING_SUBSTREAM, 0, 0),      # S 128, nseg 32: a warp = one row
     (301, 4096, W.SPACING_SUBSTREAM, 7, 1000),   # ragged last tile, offset 1000, first 7
-    (150, 8192, W.SPACING_STREAM, 3, 17),        # nseg 64: segments j >= 32
+    (150, 8192, W.SPACING_STREAM, 3, 17),        # nseg 64 (run mode, runs of one tile)
+    (300, 5120, W.SPACING_STREAM, 2, 9),         # nseg 40: tiles span rows, segments j >= 32 by per-bit jumps
     (70, 128 * 160, W.SPACING_SUBSTREAM, 0, 5),  # nseg 160
     (3201, 384, W.SPACING_SUBSTREAM, 11, 0),     # nseg 3: tiles span rows, ragged
     (2000, 480, W.SPACING_STREAM, 0, 33),        # S 96
