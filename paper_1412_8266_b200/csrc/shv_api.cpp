@@ -830,8 +830,8 @@ shv_status generate(shv_streams hid, T* out, uint64_t n, void* stream, int kind,
                 const uint64_t tiles = ns * R->nh;
                 uint64_t run = tiles / (4 * (warps ? warps : 1));
                 run = run < 1 ? 1 : run > R->nh ? R->nh : run;
-                R->run = (uint32_t)run;
                 R->rpr = (uint32_t)((R->nh + run - 1) / run);
+                R->run = (R->nh + R->rpr - 1) / R->rpr;  // equal runs (the last one at most rpr - 1 shorter)
                 R->step31 = pair_pow((u128)31 * S, 0);
             }
             CUtensorMap tmap;
