@@ -405,34 +405,59 @@ __device__ __forceinline__ double split_row_mod(const double* __restrict__ lt, u
 
 // M * (x, y) on the FP64 pipe for a split matrix at `tab` (entries `stride`
 // doubles apart: the lane table with stride 32 at lane jl, or the run-step
-// matrix with stride 1), returned as the MrgIF state.
-__device__ __forceinline__ MrgIF apply_split(const double* __restrict__ tab, uint32_t stride, double x0, double x1,
-                                             double x2, double y0, double y1, double y2, const MrgFpK& K)
+// matrix with stride 1), returned as the generator state of the row tiles.
+__device__ __forceinline__ void set_state(MrgIF& g, const double r[6], const MrgFpK& K)
 {
-    MrgIF g;
-    g.x0 = (uint32_t)__double2loint(__dadd_rn(split_row_mod(tab, stride, 0, x0, x1, x2, K.inv1, K.m1, K.magic), K.magic));
-    g.x1 = (uint32_t)__double2loint(__dadd_rn(split_row_mod(tab, stride, 6, x0, x1, x2, K.inv1, K.m1, K.magic), K.magic));
-    g.x2 = (uint32_t)__double2loint(__dadd_rn(split_row_mod(tab, stride, 12, x0, x1, x2, K.inv1, K.m1, K.magic), K.magic));
-    g.y0 = split_row_mod(tab, stride, 18, y0, y1, y2, K.inv2, K.m2, K.magic);
-    g.y1 = split_row_mod(tab, stride, 24, y0, y1, y2, K.inv2, K.m2, K.magic);
-    g.y2 = split_row_mod(tab, stride, 30, y0, y1, y2, K.inv2, K.m2, K.magic);
+    g.x0 = (uint32_t)__double2loint(__dadd_rn(r[0], K.magic));
+    g.x1 = (uint32_t)__double2loint(__dadd_rn(r[1], K.magic));
+    g.x2 = (uint32_t)__double2loint(__dadd_rn(r[2], K.magic));
+    g.y0 = r[3];
+    g.y1 = r[4];
+    g.y2 = r[5];
+}
+__device__ __forceinline__ void set_state(MrgFF& g, const double r[6], const MrgFpK&)
+{
+    g = MrgFF{r[0], r[1], r[2], r[3], r[4], r[5]};
+}
+__device__ __forceinline__ double x_of(uint32_t x) { return __uint2double_rn(x); }
+__device__ __forceinline__ double x_of(double x) { return x; }
+
+template <class Gen>
+__device__ __forceinline__ Gen apply_split(const double* __restrict__ tab, uint32_t stride, double x0, double x1,
+                                           double x2, double y0, double y1, double y2, const MrgFpK& K)
+{
+    double r[6];
+    r[0] = split_row_mod(tab, stride, 0, x0, x1, x2, K.inv1, K.m1, K.magic);
+    r[1] = split_row_mod(tab, stride, 6, x0, x1, x2, K.inv1, K.m1, K.magic);
+    r[2] = split_row_mod(tab, stride, 12, x0, x1, x2, K.inv1, K.m1, K.magic);
+    r[3] = split_row_mod(tab, stride, 18, y0, y1, y2, K.inv2, K.m2, K.magic);
+    r[4] = split_row_mod(tab, stride, 24, y0, y1, y2, K.inv2, K.m2, K.magic);
+    r[5] = split_row_mod(tab, stride, 30, y0, y1, y2, K.inv2, K.m2, K.magic);
+    Gen g;
+    set_state(g, r, K);
     return g;
 }
 
 // Start state of a row-tile lane: lanetab[jl] * (x, y).
-__device__ __forceinline__ MrgIF lane_start(const double* __restrict__ lt, uint32_t jl, const uint32_t w[6], const MrgFpK& K)
+template <class Gen>
+__device__ __forceinline__ Gen lane_start(const double* __restrict__ lt, uint32_t jl, const uint32_t w[6], const MrgFpK& K)
 {
-    return apply_split(lt + jl, 32, __uint2double_rn(w[0]), __uint2double_rn(w[1]), __uint2double_rn(w[2]),
-                       __uint2double_rn(w[3]), __uint2double_rn(w[4]), __uint2double_rn(w[5]), K);
+    return apply_split<Gen>(lt + jl, 32, __uint2double_rn(w[0]), __uint2double_rn(w[1]), __uint2double_rn(w[2]),
+                            __uint2double_rn(w[3]), __uint2double_rn(w[4]), __uint2double_rn(w[5]), K);
 }
 
 // A lane that ended segment j of a tile (at offset (j + 1) S) continues with
 // segment j + 32 of the next tile of its row: A^(31 S) * state (run mode).
-__device__ __forceinline__ MrgIF lane_advance(const double* __restrict__ st31, const MrgIF& g, const MrgFpK& K)
+template <class Gen>
+__device__ __forceinline__ Gen lane_advance(const double* __restrict__ st31, const Gen& g, const MrgFpK& K)
 {
-    return apply_split(st31, 1, __uint2double_rn(g.x0), __uint2double_rn(g.x1), __uint2double_rn(g.x2), g.y0, g.y1,
-                       g.y2, K);
+    return apply_split<Gen>(st31, 1, x_of(g.x0), x_of(g.x1), x_of(g.x2), g.y0, g.y1, g.y2, K);
 }
+
+#ifndef SHV_MRG_ROWS_STEP
+#define SHV_MRG_ROWS_STEP 3  // step of the row-tile fill: 3 = MrgIF, 4 = MrgFF
+#endif
+using GenRows = std::conditional<SHV_MRG_ROWS_STEP == 4, MrgFF, MrgIF>::type;
 
 __device__ __forceinline__ void load_words(const MrgLaunch& P, uint32_t i, uint32_t w[6])
 {
@@ -499,9 +524,9 @@ __global__ void __launch_bounds__(256, SHV_MRG_ROWS_MINB)
             for (uint32_t jh = jh0, bit = 0; jh; ++bit, jh >>= 1)
                 if (jh & 1) apply(P.segpow[bit].a, P.segpow[bit].b, s);
             const uint32_t v[6] = {s.x0, s.x1, s.x2, s.y0, s.y1, s.y2};
-            MrgIF g = lane_start(lt, lane, v, K);
+            GenRows g = lane_start<GenRows>(lt, lane, v, K);
             for (uint32_t k = 0; k < cnt; ++k) {
-                if (k) g = lane_advance(st31, g, K);
+                if (k) g = lane_advance<GenRows>(st31, g, K);
                 mrg_tma_rounds<KIND>(&tmap, K, lane, box0, bsel, g, len, 0, i * P.nseg + 32ull * (jh0 + k));
             }
         }
@@ -527,15 +552,15 @@ __global__ void __launch_bounds__(256, SHV_MRG_ROWS_MINB)
 #pragma unroll
         for (int k = 0; k < 6; ++k) cur[k] = w[k];
         if (t + wstride < ntiles) load_words(P, row(item(t + wstride)), w);  // prefetch
-        MrgIF g;
+        GenRows g;
         if (j < 32) {
-            g = lane_start(lt, j, cur, K);
+            g = lane_start<GenRows>(lt, j, cur, K);
         } else {  // rows of more than 32 segments: (A^(32 S))^(j / 32) first
             Mrg s{cur[0], cur[1], cur[2], cur[3], cur[4], cur[5]};
             for (uint32_t jh = j >> 5, bit = 0; jh; ++bit, jh >>= 1)
                 if (jh & 1) apply(P.segpow[bit].a, P.segpow[bit].b, s);
             const uint32_t v[6] = {s.x0, s.x1, s.x2, s.y0, s.y1, s.y2};
-            g = lane_start(lt, j & 31, v, K);
+            g = lane_start<GenRows>(lt, j & 31, v, K);
         }
         mrg_tma_rounds<KIND>(&tmap, K, lane, box0, bsel, g, len, 0, 32 * t);
     }
