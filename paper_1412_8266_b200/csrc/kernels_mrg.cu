@@ -25,6 +25,9 @@
 #ifndef SHV_MRG_MC_STEP
 #define SHV_MRG_MC_STEP 3
 #endif
+#ifndef SHV_MRG_ROWS_STEP
+#define SHV_MRG_ROWS_STEP 3  // step of the row-tile fill: 3 = MrgIF, 4 = MrgFF (lab: IF faster, lab34)
+#endif
 #ifndef SHV_MRG_MC_HIT
 #define SHV_MRG_MC_HIT 1  // dartboard test: 1 = FP64 (hit_fp64), 0 = integer (2 IMAD.WIDE)
 #endif
@@ -415,12 +418,14 @@ __device__ __forceinline__ void set_state(MrgIF& g, const double r[6], const Mrg
     g.y1 = r[4];
     g.y2 = r[5];
 }
+#if SHV_MRG_ROWS_STEP == 4
 __device__ __forceinline__ void set_state(MrgFF& g, const double r[6], const MrgFpK&)
 {
     g = MrgFF{r[0], r[1], r[2], r[3], r[4], r[5]};
 }
-__device__ __forceinline__ double x_of(uint32_t x) { return __uint2double_rn(x); }
 __device__ __forceinline__ double x_of(double x) { return x; }
+#endif
+__device__ __forceinline__ double x_of(uint32_t x) { return __uint2double_rn(x); }
 
 template <class Gen>
 __device__ __forceinline__ Gen apply_split(const double* __restrict__ tab, uint32_t stride, double x0, double x1,
@@ -454,9 +459,6 @@ __device__ __forceinline__ Gen lane_advance(const double* __restrict__ st31, con
     return apply_split<Gen>(st31, 1, x_of(g.x0), x_of(g.x1), x_of(g.x2), g.y0, g.y1, g.y2, K);
 }
 
-#ifndef SHV_MRG_ROWS_STEP
-#define SHV_MRG_ROWS_STEP 3  // step of the row-tile fill: 3 = MrgIF, 4 = MrgFF
-#endif
 using GenRows = std::conditional<SHV_MRG_ROWS_STEP == 4, MrgFF, MrgIF>::type;
 
 __device__ __forceinline__ void load_words(const MrgLaunch& P, uint32_t i, uint32_t w[6])
@@ -609,8 +611,17 @@ __global__ void __launch_bounds__(256) mrg_mc_kernel(const __grid_constant__ Mrg
         const uint64_t c0 = j * P.seg_len;
         const uint32_t len = it < P.items ? (uint32_t)min(P.seg_len, P.n - c0) : 0u;
         const uint32_t wlen = __reduce_max_sync(0xffffffffu, len);
+        const uint32_t wmin = __reduce_min_sync(0xffffffffu, len);
         uint32_t h = 0;
         uint32_t k = 0;
+        for (; k + 12 <= wmin; k += 12) {  // every lane inside its segment: no per-sample mask
+#pragma unroll
+            for (int u = 0; u < 12; ++u) {
+                const uint32_t w0 = mrg_next(s, K);
+                const uint32_t w1 = mrg_next(s, K);
+                h += SHV_MRG_MC_HIT ? hit_fp64(w0, w1) : hit(w0, w1);
+            }
+        }
         for (; k + 12 <= wlen; k += 12) {
 #pragma unroll
             for (int u = 0; u < 12; ++u) {
