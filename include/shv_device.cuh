@@ -643,5 +643,14 @@ __device__ __forceinline__ uint32_t hit_fp64(uint32_t w0, uint32_t w1)
     return __fma_rn(x, x, __dmul_rn(y, y)) < 281474976710656.0 ? 1u : 0u;  // 2^48
 }
 
+// The same test with the conversions on the XU pipe (I2F.F64.U32) instead of
+// the 2^52 bit pattern, whose pair formation costs a MOV (often IMAD.MOV, on
+// the FMA-heavy pipe that the Philox rounds saturate) and a DADD per coordinate.
+__device__ __forceinline__ uint32_t hit_fp64_cvt(uint32_t w0, uint32_t w1)
+{
+    const double x = __uint2double_rn(w0 >> 8), y = __uint2double_rn(w1 >> 8);
+    return __fma_rn(x, x, __dmul_rn(y, y)) < 281474976710656.0 ? 1u : 0u;  // 2^48
+}
+
 }  // namespace dev
 }  // namespace shv

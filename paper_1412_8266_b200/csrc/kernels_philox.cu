@@ -198,6 +198,11 @@ __global__ void __launch_bounds__(256) philox_fill_generic_kernel(const __grid_c
 #endif
 constexpr int kPhiloxMcUnroll = SHV_PHILOX_MC_UNROLL;
 
+#ifndef SHV_PHILOX_MC_HIT
+#define SHV_PHILOX_MC_HIT 2  // 2 = hit_fp64_cvt (XU conversions: 393.8 vs 396.7 ms, lab38), 1 = hit_fp64
+#endif
+#define PHILOX_MC_HIT(a, b) (SHV_PHILOX_MC_HIT == 2 ? hit_fp64_cvt(a, b) : hit_fp64(a, b))
+
 // Fused Philox Monte Carlo. FAST: offset lane 0 and even segment length, so
 // sample pairs never straddle a counter block (two samples per block).
 template <bool FAST, bool KEYED>
@@ -227,7 +232,7 @@ __global__ void __launch_bounds__(256) philox_mc_kernel(const __grid_constant__ 
 #pragma unroll kPhiloxMcUnroll
                 for (uint32_t r = 0; r < nb; ++r) {
                     const W4 a = philox10_from_r2(pa, q, (uint32_t)p1, (uint32_t)(g >> 32), key0, key1);
-                    h += hit_fp64(a.x, a.y) + hit_fp64(a.z, a.w);
+                    h += PHILOX_MC_HIT(a.x, a.y) + PHILOX_MC_HIT(a.z, a.w);
                     pa = add64w(pa, kPM0);
                 }
                 b = add64(b, nb);
@@ -236,7 +241,7 @@ __global__ void __launch_bounds__(256) philox_mc_kernel(const __grid_constant__ 
                     const uint64_t pa = (uint64_t)kPM0 * (uint32_t)b;
                     const W4 a = philox10_from_r1((uint32_t)(pa >> 32), (uint32_t)pa, (uint32_t)(p1 >> 32),
                                                   (uint32_t)p1, (uint32_t)(b >> 32), (uint32_t)(g >> 32), key0, key1);
-                    h += hit_fp64(a.x, a.y) + hit_fp64(a.z, a.w);
+                    h += PHILOX_MC_HIT(a.x, a.y) + PHILOX_MC_HIT(a.z, a.w);
                     b = add64(b, 1u);
                 }
             }
