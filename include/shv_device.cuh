@@ -492,23 +492,39 @@ struct TinyMT {
     uint32_t mat1, mat2, tmat;
 };
 
+// The step is ALU-bound (LOP3, shifts); the conditional masks (y & 1 ? mat : 0)
+// are formed as (y & 1) * mat on the FMA-heavy pipe (IMAD), which the
+// generator otherwise leaves idle. SHV_TINYMT_IMAD = 0 keeps the mask form.
+#ifndef SHV_TINYMT_IMAD
+#define SHV_TINYMT_IMAD 1
+#endif
+__device__ __forceinline__ uint32_t bit_times(uint32_t b, uint32_t mat)
+{
+    if (SHV_TINYMT_IMAD) {
+        uint32_t r;
+        asm("mul.lo.u32 %0, %1, %2;" : "=r"(r) : "r"(b), "r"(mat));
+        return r;
+    }
+    return (0u - b) & mat;
+}
+
 __device__ __forceinline__ void tinymt_next_state(TinyMT& t)
 {
     uint32_t y = t.s3;
     uint32_t x = (t.s0 & 0x7fffffffu) ^ t.s1 ^ t.s2;
     x ^= x << 1;
     y ^= (y >> 1) ^ x;
-    const uint32_t m = 0u - (y & 1u);
+    const uint32_t b = y & 1u;
     t.s0 = t.s1;
-    t.s1 = t.s2 ^ (m & t.mat1);
-    t.s2 = x ^ (y << 10) ^ (m & t.mat2);
+    t.s1 = t.s2 ^ bit_times(b, t.mat1);
+    t.s2 = x ^ (y << 10) ^ bit_times(b, t.mat2);
     t.s3 = y;
 }
 
 __device__ __forceinline__ uint32_t tinymt_temper(const TinyMT& t)
 {
     const uint32_t t1 = t.s0 + (t.s2 >> 8);
-    return t.s3 ^ t1 ^ ((0u - (t1 & 1u)) & t.tmat);
+    return t.s3 ^ t1 ^ bit_times(t1 & 1u, t.tmat);
 }
 
 __device__ __forceinline__ uint32_t tinymt_next(TinyMT& t)
