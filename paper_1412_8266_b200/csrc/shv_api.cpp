@@ -633,6 +633,7 @@ shv_status generate(shv_streams hid, T* out, uint64_t n, void* stream, int kind,
         T* dst = host_out ? stage[k & 1] : out;
         if (host_out && k >= 2) err = cudaStreamWaitEvent(s, copy_done[k & 1], 0);
         if (err != cudaSuccess) break;
+        CUtensorMap rows_tmap;  // MRG32k3a row-tile fill (encoded in its branch condition)
         if (h.spacing == SHV_SPACING_LEAPFROG && h.gen == SHV_GEN_TINYMT32) {
             TmLeapLaunch P{};
             P.buf = h.params;
@@ -790,8 +791,11 @@ shv_status generate(shv_streams hid, T* out, uint64_t n, void* stream, int kind,
             const unsigned full = (unsigned)((ns + h.tpb - 1) / h.tpb);
             Grid g{vec ? blocks_for(h, kKTinyFill, kind, true, ns) : full, h.tpb};
             err = launch_tinymt_fill(P, kind, vec, g, s);
-        } else if (h.gen == SHV_GEN_MRG32K3A && mrg_rows_fit(h, kind, aligned32, ns, n)) {
-            // row tiles: a warp writes 32 consecutive segments of S values (C5: one 16-KB row)
+        } else if (h.gen == SHV_GEN_MRG32K3A && mrg_rows_fit(h, kind, aligned32, ns, n) &&
+                   encode_rows_map(&rows_tmap, dst, mrg_rows_seg_len(n), ns * (n / mrg_rows_seg_len(n)),
+                                   (int)sizeof(T))) {
+            // row tiles: a warp writes 32 consecutive segments of S values (C5: one 16-KB row);
+            // an encode failure falls through to the stream-per-lane paths below
             const uint64_t S = mrg_rows_seg_len(n);
             auto R = std::make_unique<MrgRowsLaunch>();
             MrgLaunch* P = &R->m;
@@ -834,14 +838,9 @@ shv_status generate(shv_streams hid, T* out, uint64_t n, void* stream, int kind,
                 R->run = (R->nh + R->rpr - 1) / R->rpr;  // equal runs (the last one at most rpr - 1 shorter)
                 R->step31 = pair_pow((u128)31 * S, 0);
             }
-            CUtensorMap tmap;
-            if (!encode_rows_map(&tmap, dst, S, P->items, (int)sizeof(T))) {
-                err = cudaErrorInvalidValue;
-            } else {
-                const uint64_t work = R->nh ? ns * R->rpr * 32 : (P->items + 31) / 32 * 32;
-                Grid g{blocks_for(h, kKMrgFillRows, kind, true, work), h.tpb};
-                err = launch_mrg_fill_rows(*R, tmap, kind, g, s);
-            }
+            const uint64_t work = R->nh ? ns * R->rpr * 32 : (P->items + 31) / 32 * 32;
+            Grid g{blocks_for(h, kKMrgFillRows, kind, true, work), h.tpb};
+            err = launch_mrg_fill_rows(*R, rows_tmap, kind, g, s);
         } else if (h.gen == SHV_GEN_MRG32K3A) {
             bool vec = aligned32 && (n % 8 == 0);
             auto P = std::make_unique<MrgLaunch>();
