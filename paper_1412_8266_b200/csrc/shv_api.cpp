@@ -653,7 +653,9 @@ shv_status generate(shv_streams hid, T* out, uint64_t n, void* stream, int kind,
                 err = tm_leap_tr_blocks_per_sm(kind, &bps);
                 P.tr_tb = (n + 31) / 32;
                 const uint64_t warps = (uint64_t)h.sms * (uint64_t)(bps > 0 ? bps : 1) * 4;
-                const uint64_t want_ps = (4 * warps + P.tr_tb - 1) / P.tr_tb;
+                // items = tr_tb * tr_ps <= 4 waves of warps (rounding up made 4.04 waves at C5: a
+                // fifth, nearly empty round)
+                const uint64_t want_ps = (4 * warps) / P.tr_tb ? (4 * warps) / P.tr_tb : 1;
                 uint64_t pl = (ns + want_ps - 1) / want_ps;
                 if (pl < 4096) pl = 4096;  // long runs amortise the per-lane GF(2) jump
                 P.tr_pl = (pl + 127) / 128 * 128;
@@ -714,7 +716,7 @@ shv_status generate(shv_streams hid, T* out, uint64_t n, void* stream, int kind,
                 }
                 P->tr_tb = (n + 31) / 32;
                 const uint64_t warps = (uint64_t)h.sms * (uint64_t)(bps > 0 ? bps : 1) * 4;
-                const uint64_t want_ps = (4 * warps + P->tr_tb - 1) / P->tr_tb;
+                const uint64_t want_ps = (4 * warps) / P->tr_tb ? (4 * warps) / P->tr_tb : 1;
                 uint64_t pl = (ns + want_ps - 1) / want_ps;
                 if (pl < 1024) pl = 1024;  // runs long enough to amortise the start jump
                 pl = (pl + rows - 1) / rows * rows;
