@@ -45,33 +45,36 @@ __device__ __forceinline__ uint4 pack4(uint32_t a, uint32_t b, uint32_t c, uint3
 constexpr unsigned kRB = SHV_MRG_RB;
 constexpr unsigned kPieces = kRB / 16;  // 16-byte pieces per lane per round
 
-// Dynamic shared memory of a staged fill with `threads` threads per block.
-constexpr size_t staged_smem(int threads) { return (size_t)(threads / 32) * 32 * kRB; }
+// Dynamic shared memory of a staged fill with `threads` threads per block
+// (RB bytes per lane per round).
+template <unsigned RB = kRB>
+constexpr size_t staged_smem(int threads) { return (size_t)(threads / 32) * 32 * RB; }
 
 // Staging slot of 16-byte piece q of lane L, conflict-free for the per-lane
 // 128-bit writes (8 lanes, same q) and for the write-out reads (8 lanes that
-// read pieces 2p resp. 2p+1 of one source lane (kRB=256) or two (kRB=128)).
+// read pieces 2p resp. 2p+1 of one source lane (RB=256) or two (RB=128)).
+template <unsigned RB = kRB>
 __device__ __forceinline__ unsigned slot(unsigned L, unsigned q)
 {
-    if (kRB == 256) return 16 * L + 8 * (q & 1) + (((q >> 1) + L) & 7);
+    if (RB == 256) return 16 * L + 8 * (q & 1) + (((q >> 1) + L) & 7);
     return 8 * L + ((q + L) & 7);
 }
 
-// Write one staged round of the warp: lane L's cnt values (kRB bytes at most)
-// go to row_L + r values; each store instruction covers 1024/kRB source lanes
-// x kRB contiguous bytes.
-template <typename T>
+// Write one staged round of the warp: lane L's cnt values (RB bytes at most)
+// go to row_L + r values; each store instruction covers 1024/RB source lanes
+// x RB contiguous bytes.
+template <typename T, unsigned RB = kRB>
 __device__ __forceinline__ void write_round(const uint4* wb, unsigned lane, uint32_t r, uint32_t cnt, uint64_t row)
 {
     __syncwarp();
 #pragma unroll
-    for (unsigned k = 0; k < kRB / 32; ++k) {
-        const unsigned src = (1024 / kRB) * k + lane / (kRB / 32), p = lane % (kRB / 32);
+    for (unsigned k = 0; k < RB / 32; ++k) {
+        const unsigned src = (1024 / RB) * k + lane / (RB / 32), p = lane % (RB / 32);
         const uint32_t scnt = __shfl_sync(0xffffffffu, cnt, src);
         const uint64_t srow = __shfl_sync(0xffffffffu, row, src);
         if (32 * p < scnt * sizeof(T))
-            st_v8(reinterpret_cast<char*>(srow) + (uint64_t)r * sizeof(T) + 32 * p, wb[slot(src, 2 * p)],
-                  wb[slot(src, 2 * p + 1)]);
+            st_v8(reinterpret_cast<char*>(srow) + (uint64_t)r * sizeof(T) + 32 * p, wb[slot<RB>(src, 2 * p)],
+                  wb[slot<RB>(src, 2 * p + 1)]);
     }
     __syncwarp();
 }

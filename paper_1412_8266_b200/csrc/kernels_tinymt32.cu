@@ -4,8 +4,14 @@
 // back.
 #include "kernels_common.cuh"
 
+#ifndef SHV_TM_RB
+#define SHV_TM_RB 256  // bytes per lane per staged round of the TinyMT32 vector fill (128: 3.72 vs 3.37 ms, lab41)
+#endif
+
 namespace shv {
 namespace {
+
+constexpr unsigned kTmRB = SHV_TM_RB;
 
 using u128 = unsigned __int128;
 
@@ -19,15 +25,15 @@ __device__ __forceinline__ void stage8_tm(uint4* wb, unsigned lane, unsigned q0,
         for (int u = 0; u < 4; ++u) {
             const uint32_t a0 = tinymt_next(t), a1 = tinymt_next(t), b0 = tinymt_next(t), b1 = tinymt_next(t);
             const double a = philox_f64(a0, a1), b = philox_f64(b0, b1);
-            wb[slot(lane, q0 + u)] = make_uint4(__double2loint(a), __double2hiint(a), __double2loint(b),
-                                                __double2hiint(b));
+            wb[slot<kTmRB>(lane, q0 + u)] = make_uint4(__double2loint(a), __double2hiint(a), __double2loint(b),
+                                                    __double2hiint(b));
         }
     } else {
         uint32_t v[8];
 #pragma unroll
         for (int u = 0; u < 8; ++u) v[u] = tinymt_next(t);
-        wb[slot(lane, q0)] = pack4<KIND>(v[0], v[1], v[2], v[3]);
-        wb[slot(lane, q0 + 1)] = pack4<KIND>(v[4], v[5], v[6], v[7]);
+        wb[slot<kTmRB>(lane, q0)] = pack4<KIND>(v[0], v[1], v[2], v[3]);
+        wb[slot<kTmRB>(lane, q0 + 1)] = pack4<KIND>(v[4], v[5], v[6], v[7]);
     }
 }
 
@@ -106,15 +112,16 @@ __global__ void __launch_bounds__(256) tinymt_seed_kernel(const TinyMtLaunch P, 
     tm_store(P, i, t);
 }
 
-// Vector fill: one stream per lane, staged 256-byte runs (as the MRG kernel).
+// Vector fill: one stream per lane, staged 256-byte runs (as the MRG kernel;
+// 128-byte runs give four blocks per SM instead of three but measured slower).
 template <int KIND>
 __global__ void __launch_bounds__(256, 4) tinymt_fill_vec_kernel(const __grid_constant__ TinyMtLaunch P)
 {
     using T = OutT<KIND>;
     const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     extern __shared__ uint4 smem[];
-    uint4* wb = smem + warp * (32 * kPieces);
-    constexpr uint32_t G = kRB / sizeof(T);
+    uint4* wb = smem + warp * (32 * (kTmRB / 16));
+    constexpr uint32_t G = kTmRB / sizeof(T);
     const uint64_t wstride = (uint64_t)gridDim.x * (blockDim.x >> 5) * 32;
     for (uint64_t base = ((uint64_t)blockIdx.x * (blockDim.x >> 5) + warp) * 32; base < P.ns; base += wstride) {
         const uint64_t i = base + lane;
@@ -125,7 +132,7 @@ __global__ void __launch_bounds__(256, 4) tinymt_fill_vec_kernel(const __grid_co
         for (uint32_t r = 0; r < (uint32_t)P.n; r += G) {
             const uint32_t cnt = len > r ? min(G, len - r) : 0u;
             for (unsigned g = 0; g < cnt / 8; ++g) stage8_tm<KIND>(wb, lane, g * (KIND == kF64 ? 4 : 2), t);
-            write_round<T>(wb, lane, r, cnt, row);
+            write_round<T, kTmRB>(wb, lane, r, cnt, row);
         }
         if (on) tm_store(P, i, t);
     }
@@ -512,7 +519,7 @@ template <int KIND>
 cudaError_t ensure_tm_smem()
 {
     static std::atomic<uint64_t> done{0};
-    return ensure_dyn_smem(tinymt_fill_vec_kernel<KIND>, staged_smem(256), done);
+    return ensure_dyn_smem(tinymt_fill_vec_kernel<KIND>, staged_smem<kTmRB>(256), done);
 }
 
 template <int KIND>
@@ -520,7 +527,7 @@ cudaError_t launch_tm_vec(const TinyMtLaunch& p, Grid g, cudaStream_t s)
 {
     const cudaError_t e = ensure_tm_smem<KIND>();
     if (e != cudaSuccess) return e;
-    tinymt_fill_vec_kernel<KIND><<<g.blocks, g.threads, staged_smem((int)g.threads), s>>>(p);
+    tinymt_fill_vec_kernel<KIND><<<g.blocks, g.threads, staged_smem<kTmRB>((int)g.threads), s>>>(p);
     return cudaGetLastError();
 }
 
@@ -617,7 +624,7 @@ cudaError_t tinymt_occupancy(int kernel, int kind, bool fast, int threads, int* 
         const cudaError_t e = kind == kU32 ? ensure_tm_smem<kU32>()
                             : kind == kF32 ? ensure_tm_smem<kF32>() : ensure_tm_smem<kF64>();
         if (e != cudaSuccess) return e;
-        const size_t sm = staged_smem(threads);
+        const size_t sm = staged_smem<kTmRB>(threads);
         if (kind == kU32) return occ(tinymt_fill_vec_kernel<kU32>, threads, sm, out);
         if (kind == kF32) return occ(tinymt_fill_vec_kernel<kF32>, threads, sm, out);
         return occ(tinymt_fill_vec_kernel<kF64>, threads, sm, out);
