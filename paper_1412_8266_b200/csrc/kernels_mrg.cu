@@ -369,7 +369,7 @@ __global__ void __launch_bounds__(256, SHV_MRG_TMA_MINB)
 // MRG32k3a fill, row tiles (TMA). The output is viewed as
 // [ns * nseg][S] (row i = segments i*nseg .. i*nseg + nseg - 1 of S = seg_len
 // values, contiguous since S * nseg = n), and a warp tile is 32 consecutive
-// segments — for the C5 shape (S = 128, nseg = 32) one whole 16-KB stream row.
+// segments — for the C5 shape (S = 256, nseg = 16) two whole 16-KB stream rows.
 // Lane l owns segment j of row i (32t + l = i*nseg + j) and starts from
 // (A^(32 S))^(j / 32) * lanetab[j % 32] * state_i, lanetab[k] = A^(o + k S)
 // (host-built, copied to shared memory: lanes index it divergently). Each
@@ -471,7 +471,7 @@ __device__ __forceinline__ void load_words(const MrgLaunch& P, uint32_t i, uint3
 // MRG32k3a fill, row tiles (TMA). The output is viewed as
 // [ns * nseg][S] (row i = segments i*nseg .. i*nseg + nseg - 1 of S = seg_len
 // values, contiguous since S * nseg = n), and a warp tile is 32 consecutive
-// segments — for the C5 shape (S = 128, nseg = 32) one whole 16-KB stream row.
+// segments — for the C5 shape (S = 256, nseg = 16) two whole 16-KB stream rows.
 // Lane l owns segment j of row i (32t + l = i*nseg + j) and starts from
 // (A^(32 S))^(j / 32) * lanetab[j % 32] * state_i, lanetab[k] = A^(o + k S)
 // (host-built, FP64-split into shared memory). Each round the warp's box

@@ -359,11 +359,20 @@ void split_tiles(const Handle& h, uint64_t ns, uint64_t len, uint64_t resident_t
     *nseg = (uint32_t)bestS;
 }
 
-// Row-tile segment length of the MRG32k3a u32/f32 fill: a divisor S of n,
-// S % 32 == 0, in [64, 512], closest to 128 (C5: 128, one warp per 16-KB row;
-// tools/lab/tma_layout_lab.cu measured S = 128 fastest); 0 if n has none.
+// Row-tile segment length of the MRG32k3a u32/f32 fill. S = 256 for rows of
+// 16 to 32 such segments (4096 <= n <= 8192, the C5 shape: a warp tile is one or
+// two whole rows, one lane start per 256 values); otherwise the first divisor of
+// n in {128, 96, 160, 192, 64, 224, 256, ...} (S = 128: a tile is one 16-KB
+// region, the best store layout — 6.1 vs 5.1 TB/s at S = 256 with a null
+// generator — which long rows (run mode) and short rows need; lab42-45:
+// C5 3.38 vs 3.46 ms, 2^13 x 2^19 3.57 vs 3.87, 2^22 x 1024 3.48 vs 3.85).
+// 0 if n has none.
 uint64_t mrg_rows_seg_len(uint64_t n)
 {
+#ifdef SHV_MRG_ROWS_S  // lab knob: preferred segment length
+    if (n % SHV_MRG_ROWS_S == 0) return SHV_MRG_ROWS_S;
+#endif
+    if (n % 256 == 0 && n >= 16 * 256 && n <= 32 * 256) return 256;
     static const uint64_t pref[] = {128, 96, 160, 192, 64, 224, 256, 320, 384, 448, 512};
     for (uint64_t S : pref)
         if (n % S == 0) return S;
@@ -796,7 +805,7 @@ shv_status generate(shv_streams hid, T* out, uint64_t n, void* stream, int kind,
         } else if (h.gen == SHV_GEN_MRG32K3A && mrg_rows_fit(h, kind, aligned32, ns, n) &&
                    encode_rows_map(&rows_tmap, dst, mrg_rows_seg_len(n), ns * (n / mrg_rows_seg_len(n)),
                                    (int)sizeof(T))) {
-            // row tiles: a warp writes 32 consecutive segments of S values (C5: one 16-KB row);
+            // row tiles: a warp writes 32 consecutive segments of S values (C5: two 16-KB rows);
             // an encode failure falls through to the stream-per-lane paths below
             const uint64_t S = mrg_rows_seg_len(n);
             auto R = std::make_unique<MrgRowsLaunch>();

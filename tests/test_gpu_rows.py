@@ -4,11 +4,11 @@ The row-tile path covers the C3/C5 shapes at the default launch configuration
 (tests/test_gpu_parity.py compares those). Here small shapes are forced onto it
 by shrinking the resident grid (1 block of 32 threads per SM: the path is taken
 when there are at least 2 tiles of 32 segments per resident warp), and every
-value is compared with the oracle: segment lengths S = 128, 96, 160; rows of
+value is compared with the oracle: segment lengths S = 256, 128, 96, 160; rows of
 fewer than 32 segments (tiles spanning several rows), of exactly 32, and of more
-than 32 (nseg 40: the per-tile (A^(32 S))^(j / 32) jumps; nseg a multiple of 32:
-run mode, where a warp carries its lanes from tile to tile by A^(31 S), with a
-ragged last run at 43 tiles per row); a ragged last tile; non-zero offsets;
+than 32 (nseg 33 / 80: the per-tile (A^(32 S))^(j / 32) jumps; nseg a multiple of
+32: run mode, where a warp carries its lanes from tile to tile by A^(31 S), with a
+ragged last run at 86 tiles per row); a ragged last tile; non-zero offsets;
 STREAM and SUBSTREAM spacing with first > 0; u32 and f32. A CUDA profiler trace
 checks that the row-tile kernel is the one that ran.
 """
@@ -44,16 +44,17 @@ def kernels_of(fn):
 
 
 CASES = [
-    # (n_streams, n, spacing, first, pre_offset)  S = mrg_rows_seg_len(n)
-    (300, 4096, W.SPACING_SUBSTREAM, 0, 0),      # S 128, nseg 32: a warp = one row
-    (301, 4096, W.SPACING_SUBSTREAM, 7, 1000),   # ragged last tile, offset 1000, first 7
-    (150, 8192, W.SPACING_STREAM, 3, 17),        # nseg 64 (run mode, runs of one tile)
-    (300, 5120, W.SPACING_STREAM, 2, 9),         # nseg 40: tiles span rows, segments j >= 32 by per-bit jumps
-    (70, 128 * 160, W.SPACING_SUBSTREAM, 0, 5),  # nseg 160
-    (3201, 384, W.SPACING_SUBSTREAM, 11, 0),     # nseg 3: tiles span rows, ragged
-    (2000, 480, W.SPACING_STREAM, 0, 33),        # S 96
-    (1400, 1120, W.SPACING_SUBSTREAM, 0, 0),     # S 160
-    (64, 128 * 32 * 43, W.SPACING_SUBSTREAM, 5, 77),  # run mode: 43 tiles per row, runs of 4 (last 3)
+    # (n_streams, n, spacing, first, pre_offset); S = mrg_rows_seg_len(n): 256 for 4096 <= n <= 8192, else 128, 96, 160, ...
+    (600, 4096, W.SPACING_SUBSTREAM, 0, 0),        # S 256, nseg 16: a tile = two rows (the C5 layout)
+    (601, 4096, W.SPACING_SUBSTREAM, 7, 1000),     # ragged last tile, offset 1000, first 7
+    (300, 8192, W.SPACING_STREAM, 3, 17),          # S 256, nseg 32: one row per tile
+    (240, 256 * 40, W.SPACING_STREAM, 2, 9),       # S 128, nseg 80: segments j >= 32 by per-tile per-bit jumps
+    (300, 128 * 33, W.SPACING_SUBSTREAM, 1, 4),    # S 128, nseg 33
+    (70, 256 * 160, W.SPACING_SUBSTREAM, 0, 5),    # S 128, nseg 320: run mode, 10 tiles per row
+    (3201, 384, W.SPACING_SUBSTREAM, 11, 0),       # S 128, nseg 3: tiles span rows, ragged
+    (2000, 480, W.SPACING_STREAM, 0, 33),          # S 96
+    (1400, 1120, W.SPACING_SUBSTREAM, 0, 0),       # S 160
+    (64, 8192 * 43, W.SPACING_SUBSTREAM, 5, 77),   # S 128, run mode: 86 tiles per row, runs of 9 (last 5)
 ]
 
 
