@@ -366,23 +366,12 @@ __global__ void __launch_bounds__(256, SHV_MRG_TMA_MINB)
     if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
-// MRG32k3a fill, row tiles (TMA). The output is viewed as
-// [ns * nseg][S] (row i = segments i*nseg .. i*nseg + nseg - 1 of S = seg_len
-// values, contiguous since S * nseg = n), and a warp tile is 32 consecutive
-// segments — for the C5 shape (S = 256, nseg = 16) two whole 16-KB stream rows.
-// Lane l owns segment j of row i (32t + l = i*nseg + j) and starts from
-// (A^(32 S))^(j / 32) * lanetab[j % 32] * state_i, lanetab[k] = A^(o + k S)
-// (host-built, copied to shared memory: lanes index it divergently). Each
-// round the warp's box covers 32 segments x 128 B, 4 KB of one DRAM-local
-// region, so a row's pages are complete within a few rounds; stream-per-lane
-// tiles (mrg_fill_tma_kernel) scatter each round over 32 rows 16 KB apart and
-// cap the store path at ~4.6 TB/s (tools/lab/tma_layout_lab.cu: 6.1 vs 4.7
-// TB/s with a null generator).
 // The lane table in shared memory, FP64-split for the start jump: entry e of
 // lane matrix j at ltab[e * 32 + j] (lanes read consecutive 8-byte words),
 // e = (component c, row r, column q, half h) -> ((c * 3 + r) * 3 + q) * 2 + h,
-// half 0 = M >> 16, half 1 = M & 0xffff (exact doubles). (double2 entries with
-// LDS.128 spill at the 48-register bound: 3.50 vs 3.43 ms, lab26.)
+// half 0 = M >> 16, half 1 = M & 0xffff (exact doubles; lanes index the table
+// divergently, so it lives in shared memory, not the parameter block).
+// (double2 entries with LDS.128 spill at the 48-register bound: lab26.)
 constexpr uint32_t kLaneTabEntries = 36;
 
 // Row r of one component: (M v) mod m for canonical v (doubles) and the split
