@@ -101,7 +101,7 @@ class Clocks:
         self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
         q = ("index,clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap,clocks.mem,power.draw")
         try:
             self.p = subprocess.Popen(["nvidia-smi", f"--query-gpu={q}", "--format=csv,noheader,nounits",
                                        "-i", ",".join(str(g) for g in gpus), "-lms", "100"],
@@ -124,8 +124,18 @@ class Clocks:
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({names[k] for r in rows for k in range(4) if r[4 + k].strip() == "Active"})
         busy = [s for s in sm if s > 0.5 * mx] or sm
-        return {"sm_mhz": statistics.median(busy), "sm_max_mhz": mx, "reasons": reasons,
-                "samples": len(rows)}
+        out = {"sm_mhz": statistics.median(busy), "sm_max_mhz": mx, "reasons": reasons, "samples": len(rows)}
+
+        def med(col):
+            v = []
+            for r in rows:
+                try:
+                    v.append(float(r[col]))
+                except (IndexError, ValueError):
+                    pass
+            return statistics.median(v) if v else None
+        out["mem_mhz"], out["power_w"] = med(8), med(9)
+        return out
 
 
 # ---------------------------------------------------------------------------- oracle arm
