@@ -114,6 +114,13 @@ struct MrgFpK {
     double m1, m2;
     double a23n_m2; // a23n * m2 = 5886603609186927, exact
     uint32_t a12, a13n;  // component-1 multipliers for the integer half-step
+    // Subnormal-state step (MrgSN): constants in units of 2^-1074 and the
+    // scaled inverses; the kernels overwrite them from their launch parameters.
+    double sn_c1q = 0x0.317b9fd79a126p-1022;  // D(202682 * m1)
+    double sn_c2p = 0x1.4e9d5b50f226fp-1022;  // D(a23n * m2)
+    double sn_c1s = 0x1.000000d10000bp+980;   // 4 * RN(1/m1) * 2^1010
+    double sn_c2s = 0x1.000059451f212p+978;   // RU(1/m2) * 2^1010
+    double sn_M = 0x1.8p-12;                  // 1.5 * 2^-12: ulp 2^-64
 };
 __host__ __device__ __forceinline__ constexpr MrgFpK mrg_fpk()
 {
@@ -284,6 +291,66 @@ __device__ __forceinline__ uint32_t mrg_next(MrgIF& s, const MrgFpK& K = mrg_fpk
     s.y2 = r;
     return mrg_combine(p1, p2);
 }
+
+// The product's MRG32k3a step since round 2b: the state as the FP64 pairs
+// D(x) = {x, 0}, i.e. x * 2^-1074 in the SUBNORMAL range.
+// For an integer v in [0, 2^53) the bit pattern of D(v) is v itself (the
+// subnormal/normal boundary at 2^52 is seamless: exponent field 1 = bit 52),
+// so a product sum p formed exactly on the FP64 pipe hands p mod 2^32 to the
+// integer pipes as its low word, and the floor quotient
+// Q = fma.rm(p, inv * 2^1010, 1.5 * 2^-12) = 1.5 * 2^-12 + floor(p / m) * 2^-64
+// hands k = floor(p / m) < 2^22 as its low word. The canonical residue is then
+// r = p - k m = lo(p) + c k (mod 2^32), m = 2^32 - c: one IMAD, no bias, no
+// conversion, no fix-up. Per component 3 DFMA + 1-2 integer instructions:
+//  - component 2: p = a21 y2 + a23n (m2 - y0) in [0, 2^52.86) (exact), the
+//    floor by inv2 = RU(1/m2) exactly as in mrg_c2_floor;
+//  - component 1: the signed form has negative values (sign-magnitude bits)
+//    and the positive form a12 x1 + a13n (m1 - x0) reaches 2^53.08, so the
+//    common factor 4 comes out: q = 350895 x1 + 202682 (m1 - x0) < 2^51.08 is
+//    exact, p = 4q, floor(4q / m1) = floor(q * 4 inv1) because
+//    4q * delta1 * m1 < 0.72 (inv1 = RN(1/m1) = 1/m1 + delta1, delta1 > 0),
+//    and r = 4 lo(q) + 209 k (mod 2^32).
+// Bounds pinned in tests/test_fp64_step_bounds.py. Compute-only on B200
+// (tools/lab/step4_lab.cu, lab47): 1.71 T numbers/s against 1.42 for MrgIF
+// and 1.34 for MrgFF: 6 DFMA, 3 IMAD, 1 shift, 2 zero moves (the pairs' high
+// words) and the 3-instruction combine per number.
+struct MrgSN {
+    uint32_t x0, x1, x2;  // component 1, oldest -> newest (canonical, < m1)
+    uint32_t y0, y1, y2;  // component 2 (< m2)
+};
+
+__device__ __forceinline__ double mrg_sn(uint32_t x) { return __hiloint2double(0, (int)x); }
+
+__device__ __forceinline__ uint32_t mrg_c1_sn(uint32_t x0, uint32_t x1, const MrgFpK& K)
+{
+    const double t = __fma_rn(-202682.0, mrg_sn(x0), K.sn_c1q);  // 202682 (m1 - x0)
+    const double q = __fma_rn(350895.0, mrg_sn(x1), t);
+    const double Q = __fma_rd(q, K.sn_c1s, K.sn_M);
+    return 4u * (uint32_t)__double2loint(q) + 209u * (uint32_t)__double2loint(Q);
+}
+
+__device__ __forceinline__ uint32_t mrg_c2_sn(uint32_t y0, uint32_t y2, const MrgFpK& K)
+{
+    const double t = __fma_rn(-(double)kA23n, mrg_sn(y0), K.sn_c2p);  // a23n (m2 - y0)
+    const double p = __fma_rn((double)kA21, mrg_sn(y2), t);
+    const double Q = __fma_rd(p, K.sn_c2s, K.sn_M);
+    return (uint32_t)__double2loint(p) + kC2 * (uint32_t)__double2loint(Q);
+}
+
+__device__ __forceinline__ uint32_t mrg_next(MrgSN& s, const MrgFpK& K = mrg_fpk())
+{
+    const uint32_t p1 = mrg_c1_sn(s.x0, s.x1, K);
+    s.x0 = s.x1;
+    s.x1 = s.x2;
+    s.x2 = p1;
+    const uint32_t p2 = mrg_c2_sn(s.y0, s.y2, K);
+    s.y0 = s.y1;
+    s.y1 = s.y2;
+    s.y2 = p2;
+    return mrg_combine(p1, p2);
+}
+
+__device__ __forceinline__ MrgSN to_mrg_sn(const Mrg& s) { return MrgSN{s.x0, s.x1, s.x2, s.y0, s.y1, s.y2}; }
 
 // ------------------------------------------------------------------ Philox4x32-10
 

@@ -10,8 +10,8 @@
 // Compile-time knobs (defaults = the product; tools/lab/build_knobs.sh builds
 // variants for the labs, every variant gives bit-identical output):
 //   SHV_MRG_STEP     step of the stream-per-lane fills: 4 = MrgFF, 3 = MrgIF
-//   SHV_MRG_MC_STEP  step of the fused Monte Carlo kernel: 3 = MrgIF (474 vs
-//                    493 ms for 2^38 samples), 4 = MrgFF
+//   SHV_MRG_MC_STEP  step of the fused Monte Carlo kernel: 5 = MrgSN, 3 = MrgIF
+//                    (474 vs 493 ms for 2^38 samples), 4 = MrgFF
 //   SHV_MRG_MC_HIT   dartboard test: 1 = FP64 (471 vs 474 ms), 0 = integer
 //   SHV_MRG_STAGE    staging of the vector fill: 1 = stage the f64 outputs only
 //   SHV_MRG_MINB, SHV_MRG_TMA_MINB, SHV_MRG_ROWS_MINB: min-blocks hints
@@ -23,10 +23,10 @@
 #define SHV_MRG_STEP 4
 #endif
 #ifndef SHV_MRG_MC_STEP
-#define SHV_MRG_MC_STEP 3
+#define SHV_MRG_MC_STEP 5
 #endif
 #ifndef SHV_MRG_ROWS_STEP
-#define SHV_MRG_ROWS_STEP 3  // step of the row-tile fill: 3 = MrgIF, 4 = MrgFF (lab: IF faster, lab34)
+#define SHV_MRG_ROWS_STEP 5  // step of the row-tile fill: 5 = MrgSN, 3 = MrgIF, 4 = MrgFF (lab: IF faster than FF, lab34)
 #endif
 #ifndef SHV_MRG_MC_HIT
 #define SHV_MRG_MC_HIT 1  // dartboard test: 1 = FP64 (hit_fp64), 0 = integer (2 IMAD.WIDE)
@@ -66,23 +66,42 @@ namespace {
 #endif
 __constant__ double c_mrg_fpk[6] = {6755399441055744.0, 1.0 / 4294967087.0, 0x1.000059451f212p-32,
                                     4294967087.0, 4294944443.0, 5886603609186927.0};
+// MrgSN constants (MrgFpK::sn_* order): bit i of SHV_MRG_SN_CKMASK takes
+// c_mrg_snk[i] instead of the launch parameter.
+#ifndef SHV_MRG_SN_CKMASK
+#define SHV_MRG_SN_CKMASK 12  // c1s, c2s from constant memory: the DFMA.RM multiplicand as a uniform-register operand
+#endif
+__constant__ double c_mrg_snk[5] = {0x0.317b9fd79a126p-1022, 0x1.4e9d5b50f226fp-1022, 0x1.000000d10000bp+980,
+                                    0x1.000059451f212p+978, 0x1.8p-12};
 template <int MASK>
 __device__ __forceinline__ MrgFpK load_fpk(const MrgLaunch& P)
 {
 #define SHV_CKF(i) (((MASK >> (i)) & 1) ? c_mrg_fpk[i] : P.fpk[i])
-    return MrgFpK{SHV_CKF(0), SHV_CKF(1), SHV_CKF(2), SHV_CKF(3), SHV_CKF(4), SHV_CKF(5), P.imul[0], P.imul[1]};
+    MrgFpK K{SHV_CKF(0), SHV_CKF(1), SHV_CKF(2), SHV_CKF(3), SHV_CKF(4), SHV_CKF(5), P.imul[0], P.imul[1]};
 #undef SHV_CKF
+#define SHV_CKS(i) (((SHV_MRG_SN_CKMASK >> (i)) & 1) ? c_mrg_snk[i] : P.snk[i])
+    K.sn_c1q = SHV_CKS(0);
+    K.sn_c2p = SHV_CKS(1);
+    K.sn_c1s = SHV_CKS(2);
+    K.sn_c2s = SHV_CKS(3);
+    K.sn_M = SHV_CKS(4);
+#undef SHV_CKS
+    return K;
 }
 
 __device__ __forceinline__ void make_gen(const Mrg& s, MrgFF& g) { g = to_mrg_ff(s); }
 __device__ __forceinline__ void make_gen(const Mrg& s, MrgIF& g) { g = to_mrg_if(s); }
+__device__ __forceinline__ void make_gen(const Mrg& s, MrgSN& g) { g = to_mrg_sn(s); }
+// Step of a kernel by knob value: 3 = MrgIF, 4 = MrgFF, 5 = MrgSN.
+template <int STEP>
+using StepGen = typename std::conditional<STEP == 4, MrgFF, typename std::conditional<STEP == 5, MrgSN, MrgIF>::type>::type;
 #ifdef SHV_LAB_GEN_HEADER  // tools/lab builds only: stand-in generators (never in libshv.so)
 #include SHV_LAB_GEN_HEADER
 using GenFill = SHV_LAB_GEN;
 #else
 using GenFill = std::conditional<SHV_MRG_STEP == 4, MrgFF, MrgIF>::type;
 #endif
-using GenMc = std::conditional<SHV_MRG_MC_STEP == 4, MrgFF, MrgIF>::type;
+using GenMc = StepGen<SHV_MRG_MC_STEP>;
 
 
 __device__ __forceinline__ Mrg load_state(const uint32_t* __restrict__ st, uint64_t stride, uint64_t i)
@@ -266,6 +285,28 @@ __global__ void __launch_bounds__(256, SHV_MRG_MINB) mrg_fill_vec_kernel(const _
 #ifndef SHV_MRG_TMA_MINB
 #define SHV_MRG_TMA_MINB (SHV_MRG_STEP == 4 ? 4 : 2)  // lab sweep: FF 4 blocks, IF 2 blocks per SM
 #endif
+#ifndef SHV_MRG_PIN
+#define SHV_MRG_PIN 1  // state through an empty volatile asm after each 4-value store (see pin_state)
+#endif
+// An empty volatile asm the state passes through: volatile asms keep their
+// order, so ptxas cannot run the serial component-2 chain of later groups
+// ahead of the current group's store (it did, holding up to 32 finished
+// words live and spilling at the 48-register bound).
+__device__ __forceinline__ void pin_state(MrgSN& g)
+{
+    asm volatile("" : "+r"(g.x0), "+r"(g.x1), "+r"(g.x2), "+r"(g.y0), "+r"(g.y1), "+r"(g.y2));
+}
+__device__ __forceinline__ void pin_state(MrgIF& g)
+{
+    asm volatile("" : "+r"(g.x0), "+r"(g.x1), "+r"(g.x2), "+d"(g.y0), "+d"(g.y1), "+d"(g.y2));
+}
+__device__ __forceinline__ void pin_state(MrgFF& g)
+{
+    asm volatile("" : "+d"(g.x0), "+d"(g.x1), "+d"(g.x2), "+d"(g.y0), "+d"(g.y1), "+d"(g.y2));
+}
+#ifndef SHV_MRG_STS4
+#define SHV_MRG_STS4 1  // u32/f32 boxes: one shared store per 4 values (0: per 8)
+#endif
 constexpr uint32_t kTmaBufs = SHV_MRG_NBUF;  // boxes per warp in flight (2: double buffering)
 
 // Generates `len` values per lane from g (lane l: box row l) in rounds of 128 B
@@ -279,6 +320,27 @@ __device__ __forceinline__ void mrg_tma_rounds(const CUtensorMap* tmap, const Mr
     for (uint32_t r = 0; r < len; r += W) {
         const uint32_t box = box0 + bsel * 4096u;
         const uint32_t rowsw = box + lane * 128u + ((lane & 7u) << 4);  // ^ (q << 4) = chunk q
+        if constexpr (KIND != kF64 && SHV_MRG_STS4) {
+            // 4 values per shared store: fewer live registers (48-register bound)
+#pragma unroll
+            for (unsigned q = 0; q < W / 4; ++q) {
+                uint32_t v[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) v[u] = mrg_next(s, K);
+                if (q == 0) {  // this buffer's previous box must have left shared memory
+                    if (lane == 0) {
+                        if (kTmaBufs == 1) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+                        else asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+                    }
+                    __syncwarp();
+                }
+                const uint4 a = pack4<KIND>(v[0], v[1], v[2], v[3]);
+                asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(rowsw ^ (q << 4)), "r"(a.x), "r"(a.y),
+                             "r"(a.z), "r"(a.w)
+                             : "memory");
+                if (SHV_MRG_PIN) pin_state(s);
+            }
+        } else {
 #pragma unroll
         for (unsigned q8 = 0; q8 < W / 8; ++q8) {
             uint32_t v[8];
@@ -309,6 +371,7 @@ __device__ __forceinline__ void mrg_tma_rounds(const CUtensorMap* tmap, const Mr
                              "r"(b.x), "r"(b.y), "r"(b.z), "r"(b.w)
                              : "memory");
             }
+        }
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // st.shared -> async proxy
         __syncwarp();
@@ -407,13 +470,22 @@ __device__ __forceinline__ void set_state(MrgIF& g, const double r[6], const Mrg
     g.y1 = r[4];
     g.y2 = r[5];
 }
+__device__ __forceinline__ void set_state(MrgSN& g, const double r[6], const MrgFpK& K)
+{
+    g.x0 = (uint32_t)__double2loint(__dadd_rn(r[0], K.magic));
+    g.x1 = (uint32_t)__double2loint(__dadd_rn(r[1], K.magic));
+    g.x2 = (uint32_t)__double2loint(__dadd_rn(r[2], K.magic));
+    g.y0 = (uint32_t)__double2loint(__dadd_rn(r[3], K.magic));
+    g.y1 = (uint32_t)__double2loint(__dadd_rn(r[4], K.magic));
+    g.y2 = (uint32_t)__double2loint(__dadd_rn(r[5], K.magic));
+}
 #if SHV_MRG_ROWS_STEP == 4
 __device__ __forceinline__ void set_state(MrgFF& g, const double r[6], const MrgFpK&)
 {
     g = MrgFF{r[0], r[1], r[2], r[3], r[4], r[5]};
 }
-__device__ __forceinline__ double x_of(double x) { return x; }
 #endif
+__device__ __forceinline__ double x_of(double x) { return x; }
 __device__ __forceinline__ double x_of(uint32_t x) { return __uint2double_rn(x); }
 
 template <class Gen>
@@ -445,10 +517,17 @@ __device__ __forceinline__ Gen lane_start(const double* __restrict__ lt, uint32_
 template <class Gen>
 __device__ __forceinline__ Gen lane_advance(const double* __restrict__ st31, const Gen& g, const MrgFpK& K)
 {
-    return apply_split<Gen>(st31, 1, x_of(g.x0), x_of(g.x1), x_of(g.x2), g.y0, g.y1, g.y2, K);
+    return apply_split<Gen>(st31, 1, x_of(g.x0), x_of(g.x1), x_of(g.x2), x_of(g.y0), x_of(g.y1), x_of(g.y2), K);
 }
 
-using GenRows = std::conditional<SHV_MRG_ROWS_STEP == 4, MrgFF, MrgIF>::type;
+using GenRows = StepGen<SHV_MRG_ROWS_STEP>;
+
+__device__ __forceinline__ void prefetch_words(const MrgLaunch& P, uint32_t i)
+{
+    const uint32_t* st = P.state + P.stream_begin + i;
+#pragma unroll
+    for (int k = 0; k < 6; ++k) asm volatile("prefetch.global.L2 [%0];" ::"l"(st + k * P.stride));
+}
 
 __device__ __forceinline__ void load_words(const MrgLaunch& P, uint32_t i, uint32_t w[6])
 {
@@ -470,11 +549,17 @@ __device__ __forceinline__ void load_words(const MrgLaunch& P, uint32_t i, uint3
 // the store path at ~4.6 TB/s (tools/lab/tma_layout_lab.cu: 6.1 vs 4.7 TB/s
 // with a null generator). The next tile's state words are loaded while the
 // current tile generates.
+#ifndef SHV_MRG_ROWS_TPB
+#define SHV_MRG_ROWS_TPB 256  // launch bound (threads per block) of the row-tile fill
+#endif
+#ifndef SHV_MRG_ROWS_PREF
+#define SHV_MRG_ROWS_PREF 0  // next tile's state words: 0 = registers, 1 = L2 prefetch hint (more spills), 2 = none
+#endif
 #ifndef SHV_MRG_ROWS_MINB
 #define SHV_MRG_ROWS_MINB 5  // <= 48 registers: 5 blocks of 256 per SM (lab: 3.50 vs 3.56 ms at 4)
 #endif
 template <int KIND, bool RUN>
-__global__ void __launch_bounds__(256, SHV_MRG_ROWS_MINB)
+__global__ void __launch_bounds__(SHV_MRG_ROWS_TPB, SHV_MRG_ROWS_MINB)
     mrg_fill_rows_kernel(const __grid_constant__ MrgRowsLaunch R, const __grid_constant__ CUtensorMap tmap)
 {
     extern __shared__ uint8_t tma_smem[];
@@ -534,15 +619,26 @@ __global__ void __launch_bounds__(256, SHV_MRG_ROWS_MINB)
     };
     // it / nseg by the host's multiply-shift (Granlund-Montgomery, 31-bit numerators)
     auto row = [&](uint32_t it) { return R.div_m ? __umulhi(it, R.div_m) >> R.div_s : it; };
+#if SHV_MRG_ROWS_PREF == 0
     uint32_t w[6];
     if (t < ntiles) load_words(P, row(item(t)), w);
+#else
+    if (t < ntiles) prefetch_words(P, row(item(t)));
+#endif
     for (; t < ntiles; t += wstride) {
         const uint32_t it = item(t);
         const uint32_t i = row(it), j = it - i * nseg;
         uint32_t cur[6];
+#if SHV_MRG_ROWS_PREF == 0
 #pragma unroll
         for (int k = 0; k < 6; ++k) cur[k] = w[k];
         if (t + wstride < ntiles) load_words(P, row(item(t + wstride)), w);  // prefetch
+#else
+        // the next tile's words go to L2 by a prefetch hint: no registers held
+        // across the tile's rounds (the register copy spilled at 48 registers)
+        load_words(P, i, cur);
+        if (SHV_MRG_ROWS_PREF == 1 && t + wstride < ntiles) prefetch_words(P, row(item(t + wstride)));
+#endif
         GenRows g;
         if (j < 32) {
             g = lane_start<GenRows>(lt, j, cur, K);

@@ -359,20 +359,18 @@ void split_tiles(const Handle& h, uint64_t ns, uint64_t len, uint64_t resident_t
     *nseg = (uint32_t)bestS;
 }
 
-// Row-tile segment length of the MRG32k3a u32/f32 fill. S = 256 for rows of
-// 16 to 32 such segments (4096 <= n <= 8192, the C5 shape: a warp tile is one or
-// two whole rows, one lane start per 256 values); otherwise the first divisor of
-// n in {128, 96, 160, 192, 64, 224, 256, ...} (S = 128: a tile is one 16-KB
-// region, the best store layout — 6.1 vs 5.1 TB/s at S = 256 with a null
-// generator — which long rows (run mode) and short rows need; lab42-45:
-// C5 3.38 vs 3.46 ms, 2^13 x 2^19 3.57 vs 3.87, 2^22 x 1024 3.48 vs 3.85).
+// Row-tile segment length of the MRG32k3a u32/f32 fill: the first divisor of
+// n in {128, 96, 160, 192, 64, 224, 256, ...}. S = 128 makes a warp tile one
+// 16-KB region, the best store layout (6.1 vs 5.1 TB/s at S = 256 with a null
+// generator). With the MrgIF step the C5 shape took S = 256 (half the lane
+// starts: 3.38 vs 3.46 ms, lab42); with MrgSN the step is cheap enough that the
+// S = 256 layout binds on its TMA stores (4.04 vs 3.17-3.25 ms, lab50).
 // 0 if n has none.
 uint64_t mrg_rows_seg_len(uint64_t n)
 {
 #ifdef SHV_MRG_ROWS_S  // lab knob: preferred segment length
     if (n % SHV_MRG_ROWS_S == 0) return SHV_MRG_ROWS_S;
 #endif
-    if (n % 256 == 0 && n >= 16 * 256 && n <= 32 * 256) return 256;
     static const uint64_t pref[] = {128, 96, 160, 192, 64, 224, 256, 320, 384, 448, 512};
     for (uint64_t S : pref)
         if (n % S == 0) return S;
@@ -469,6 +467,10 @@ void fill_mrg_segments(const Handle& h, uint64_t units_per_seg, uint64_t draws_p
     memcpy(P->fpk, fpk, sizeof fpk);
     P->imul[0] = 1403580u;  // a12
     P->imul[1] = 810728u;   // a13n
+    // shv::dev::MrgFpK::sn_*: D(202682 m1), D(a23n m2), 4 RN(1/m1) 2^1010, RU(1/m2) 2^1010, 1.5 2^-12
+    const double snk[5] = {0x0.317b9fd79a126p-1022, 0x1.4e9d5b50f226fp-1022, 0x1.000000d10000bp+980,
+                           0x1.000059451f212p+978, 0x1.8p-12};
+    memcpy(P->snk, snk, sizeof snk);
     P->seg0 = pair_pow(h.offset, 0);
     P->segpow[0] = pair_pow((u128)units_per_seg * draws_per_unit, 0);
     for (int b = 1; b < kSegBits && ((uint64_t)nseg - 1) >> b; ++b)

@@ -49,6 +49,7 @@ struct MrgLaunch {
                                   // ptxas keeps them in registers
     uint32_t imul[2];             // a12, a13n (MrgFpK::a12/a13n): runtime values, so ptxas
                                   // emits plain IMAD.WIDE for the integer half-step
+    double snk[5];                // subnormal-state step constants (MrgFpK::sn_c1q .. sn_M)
 };
 
 // Philox4x32-10 bulk fill / Monte Carlo launch. Draw d of handle stream i

@@ -9,6 +9,7 @@ GPU parity tests do)."""
 import math
 import os
 import random
+import struct
 from fractions import Fraction as Fr
 
 M1, M2 = 4294967087, 4294944443
@@ -108,3 +109,109 @@ def test_integer_half_step_bounds():
     for _ in range(50000):
         x0, x1 = rng.randrange(M1), rng.randrange(M1)
         assert c1_int(x0, x1) == (A12 * x1 - A13N * x0) % M1
+
+
+# ---- MrgSN: the subnormal-state step (include/shv_device.cuh mrg_c1_sn / mrg_c2_sn)
+
+def D(v: int) -> float:
+    """The register pair {v_lo, v_hi} as a double (v < 2^64): for v < 2^53 this is
+    v * 2^-1074 exactly (subnormal below 2^52, exponent field 1 above)."""
+    return struct.unpack("<d", struct.pack("<Q", v))[0]
+
+
+def bits(d: float) -> int:
+    return struct.unpack("<Q", struct.pack("<d", d))[0]
+
+
+SN_C1Q = float.fromhex("0x0.317b9fd79a126p-1022")
+SN_C2P = float.fromhex("0x1.4e9d5b50f226fp-1022")
+SN_C1S = float.fromhex("0x1.000000d10000bp+980")
+SN_C2S = float.fromhex("0x1.000059451f212p+978")
+SN_M = float.fromhex("0x1.8p-12")
+
+
+def fma_rd_lo(a: float, b: float, c: float) -> int:
+    """Low word of fma.rm(a, b, c) for c = 1.5*2^-12 and 0 <= a*b < 2^-33:
+    the exact a*b + c rounded down to the ulp of [2^-12, 2^-11), 2^-64."""
+    v = Fr(a) * Fr(b) + Fr(c)
+    q = math.floor(v * 2**64)
+    assert Fr(2**-12) <= Fr(q, 2**64) < Fr(2**-11)
+    return bits(float(Fr(q, 2**64))) & 0xFFFFFFFF
+
+
+def c1_sn(x0: int, x1: int) -> int:
+    t = -202682.0 * D(x0) + SN_C1Q      # exact: the fma's product and sum are representable
+    q = 350895.0 * D(x1) + t
+    assert bits(q) == 350895 * x1 + 202682 * (M1 - x0)
+    k = fma_rd_lo(q, SN_C1S, SN_M)
+    return (4 * (bits(q) & 0xFFFFFFFF) + 209 * k) % 2**32
+
+
+def c2_sn(y0: int, y2: int) -> int:
+    t = -float(A23N) * D(y0) + SN_C2P
+    p = float(A21) * D(y2) + t
+    assert bits(p) == A21 * y2 + A23N * (M2 - y0)
+    k = fma_rd_lo(p, SN_C2S, SN_M)
+    return ((bits(p) & 0xFFFFFFFF) + 22853 * k) % 2**32
+
+
+def test_sn_constants():
+    src = open(HDR).read()
+    for h in ("0x0.317b9fd79a126p-1022", "0x1.4e9d5b50f226fp-1022", "0x1.000000d10000bp+980",
+              "0x1.000059451f212p+978", "0x1.8p-12"):
+        assert h in src, h
+    assert bits(SN_C1Q) == 202682 * M1 and bits(SN_C2P) == A23N * M2
+    assert Fr(SN_C1S) == 4 * Fr(INV1) * 2**1010 and Fr(SN_C2S) == Fr(INV2) * 2**1010
+    assert SN_M == 1.5 * 2**-12
+    for v in (0, 1, 2**32 - 1, 2**52 - 1, 2**52, 2**53 - 1):  # the bit pattern of D(v) is v
+        assert Fr(D(v)) == Fr(v, 2**1074) and bits(D(v)) == v
+    assert 4 * 350895 == A12 and 4 * 202682 == A13N
+
+
+def test_sn_bounds():
+    d1 = Fr(INV1) - Fr(1, M1)
+    d2 = Fr(INV2) - Fr(1, M2)
+    qmax = 350895 * (M1 - 1) + 202682 * M1          # x canonical: x1 <= m1 - 1, m1 - x0 <= m1
+    assert qmax < 2**51.08 < 2**52 and 4 * qmax * M1 * d1 < Fr(72, 100)
+    pmax = A21 * (M2 - 1) + A23N * M2
+    assert pmax < 2**52.86 and pmax * M2 * d2 < Fr(98, 100)
+    # the quotients fit below the ulp-2^-64 window: M + k * 2^-64 < 2^-11
+    assert 4 * qmax // M1 < 2**22 and pmax // M2 < 2**22
+
+
+def test_sn_step_emulated_matches_recurrence():
+    rng = random.Random(14128266)
+    edges1 = [0, 1, 2, M1 - 2, M1 - 1]
+    edges2 = [0, 1, 2, M2 - 2, M2 - 1]
+    for x0 in edges1:
+        for x1 in edges1:
+            assert c1_sn(x0, x1) == (A12 * x1 - A13N * x0) % M1
+    for y0 in edges2:
+        for y2 in edges2:
+            assert c2_sn(y0, y2) == (A21 * y2 - A23N * y0) % M2
+    # quotient boundaries: 4q = k m1 + {0, 1, m1 - 1}, p = k m2 + {0, 1, m2 - 1}
+    i13, i23 = pow(A13N, -1, M1), pow(A23N, -1, M2)
+    for _ in range(100):
+        x1, y2 = rng.randrange(M1), rng.randrange(M2)
+        for res in (0, 1, M1 - 1):
+            x0 = (A12 * x1 - res) * i13 % M1
+            assert (A12 * x1 + A13N * (M1 - x0)) % M1 == res
+            assert c1_sn(x0, x1) == res
+        for res in (0, 1, M2 - 1):
+            y0 = (A21 * y2 - res) * i23 % M2
+            assert c2_sn(y0, y2) == res
+    for _ in range(300):
+        x0, x1 = rng.randrange(M1), rng.randrange(M1)
+        assert c1_sn(x0, x1) == (A12 * x1 - A13N * x0) % M1
+        y0, y2 = rng.randrange(M2), rng.randrange(M2)
+        assert c2_sn(y0, y2) == (A21 * y2 - A23N * y0) % M2
+    # a run of the full step from a seed, against the recurrence
+    x = [12345, 12345, 12345]
+    y = [12345, 12345, 12345]
+    for _ in range(2000):
+        n1 = c1_sn(x[0], x[1])
+        assert n1 == (A12 * x[1] - A13N * x[0]) % M1
+        n2 = c2_sn(y[0], y[2])
+        assert n2 == (A21 * y[2] - A23N * y[0]) % M2
+        x = [x[1], x[2], n1]
+        y = [y[1], y[2], n2]

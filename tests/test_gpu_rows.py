@@ -4,7 +4,7 @@ The row-tile path covers the C3/C5 shapes at the default launch configuration
 (tests/test_gpu_parity.py compares those). Here small shapes are forced onto it
 by shrinking the resident grid (1 block of 32 threads per SM: the path is taken
 when there are at least 2 tiles of 32 segments per resident warp), and every
-value is compared with the oracle: segment lengths S = 256, 128, 96, 160; rows of
+value is compared with the oracle: segment lengths S = 128, 96, 160; rows of
 fewer than 32 segments (tiles spanning several rows), of exactly 32, and of more
 than 32 (nseg 33 / 80: the per-tile (A^(32 S))^(j / 32) jumps; nseg a multiple of
 32: run mode, where a warp carries its lanes from tile to tile by A^(31 S), with a
@@ -44,10 +44,11 @@ def kernels_of(fn):
 
 
 CASES = [
-    # (n_streams, n, spacing, first, pre_offset); S = mrg_rows_seg_len(n): 256 for 4096 <= n <= 8192, else 128, 96, 160, ...
-    (600, 4096, W.SPACING_SUBSTREAM, 0, 0),        # S 256, nseg 16: a tile = two rows (the C5 layout)
+    # (n_streams, n, spacing, first, pre_offset); S = mrg_rows_seg_len(n): 128, 96, 160, ... (first divisor)
+    (600, 4096, W.SPACING_SUBSTREAM, 0, 0),        # S 128, nseg 32: a tile = one row (the C5 layout)
+    (600, 2048, W.SPACING_STREAM, 0, 3),           # S 128, nseg 16: a tile = two rows
     (601, 4096, W.SPACING_SUBSTREAM, 7, 1000),     # ragged last tile, offset 1000, first 7
-    (300, 8192, W.SPACING_STREAM, 3, 17),          # S 256, nseg 32: one row per tile
+    (300, 8192, W.SPACING_STREAM, 3, 17),          # S 128, nseg 64: run mode, 2 tiles per row
     (240, 256 * 40, W.SPACING_STREAM, 2, 9),       # S 128, nseg 80: segments j >= 32 by per-tile per-bit jumps
     (300, 128 * 33, W.SPACING_SUBSTREAM, 1, 4),    # S 128, nseg 33
     (70, 256 * 160, W.SPACING_SUBSTREAM, 0, 5),    # S 128, nseg 320: run mode, 10 tiles per row
