@@ -2,12 +2,16 @@
 // (arXiv 1412.8266) for sm_100a. Included by the kernels_*.cu files (and by the
 // kernel labs under tools/lab/, which time variants of the same functions).
 //
-// MRG32k3a steps, both exact and bit-identical:
+// MRG32k3a steps, all exact and bit-identical:
+//  - MrgSN: the state as FP64 pairs {x, 0} in the subnormal range, where a
+//    double's bit pattern is the integer it holds: per component 3 DFMA (the
+//    product sum and one floor quotient) and one IMAD (the residue from the two
+//    low words). The product step of the row-tile u32/f32 fill and of the fused
+//    Monte Carlo kernel (1.71 T values/s compute-only, lab47).
 //  - MrgIF: component 1 in 32-bit integer arithmetic (two IMAD.WIDE + one IMAD,
 //    compare/select on the ALU), component 2 in exact binary64 arithmetic on
 //    the FP64 pipe (products < 2^53, floor reduction), as in L'Ecuyer's
-//    floating-point formulation [LEcuyer1999]. The product step of the row-tile
-//    u32/f32 fill and of the fused Monte Carlo kernels.
+//    floating-point formulation [LEcuyer1999]. The transposed Leap Frog fill.
 //  - MrgFF: both components on the FP64 pipe (12 FP64 operations per number);
 //    the stream-per-lane fills (f64, shapes without a row-tile split).
 // Measured on B200 (tools/lab, profiles/r02_labs): IMAD.WIDE issues at ~21-24

@@ -429,6 +429,16 @@ constexpr uint32_t kTrRows = SHV_LEAP_TR_ROWS;
 // launch parameters, as in kernels_mrg.cu (operand placement).
 __constant__ double c_leap_fpk[6] = {6755399441055744.0, 1.0 / 4294967087.0, 0x1.000059451f212p-32,
                                      4294967087.0, 4294944443.0, 5886603609186927.0};
+// MrgSN constants (MrgFpK::sn_* order) from constant memory: the DFMA.RM
+// multiplicands become uniform-register operands (kernels_mrg.cu, lab50).
+__constant__ double c_leap_snk[5] = {0x0.317b9fd79a126p-1022, 0x1.4e9d5b50f226fp-1022, 0x1.000000d10000bp+980,
+                                     0x1.000059451f212p+978, 0x1.8p-12};
+#ifndef SHV_LEAP_STEP
+#define SHV_LEAP_STEP 3  // step of the transposed MRG32k3a Leap Frog fill: 3 = MrgIF, 5 = MrgSN (3.69 vs 3.48 ms, lab51)
+#endif
+using LeapMrgGen = std::conditional<SHV_LEAP_STEP == 5, MrgSN, MrgIF>::type;
+__device__ __forceinline__ void make_leap_gen(const Mrg& m, MrgSN& g) { g = to_mrg_sn(m); }
+__device__ __forceinline__ void make_leap_gen(const Mrg& m, MrgIF& g) { g = to_mrg_if(m); }
 template <int KIND>
 __global__ void __launch_bounds__(kTrWarps * 32)
     leap_mrg_tr_kernel(const __grid_constant__ LeapLaunch P, const __grid_constant__ CUtensorMap tmap)
@@ -438,8 +448,13 @@ __global__ void __launch_bounds__(kTrWarps * 32)
     const uint32_t base = ((uint32_t)__cvta_generic_to_shared(tr_smem) + 1023u) & ~1023u;
     const uint32_t box = base + warp * (kTrRows * 128u);
 #define SHV_TRF(i) (((SHV_LEAP_CKMASK >> (i)) & 1) ? c_leap_fpk[i] : P.fpk[i])
-    const MrgFpK K{SHV_TRF(0), SHV_TRF(1), SHV_TRF(2), SHV_TRF(3), SHV_TRF(4), SHV_TRF(5), P.imul[0], P.imul[1]};
+    MrgFpK K{SHV_TRF(0), SHV_TRF(1), SHV_TRF(2), SHV_TRF(3), SHV_TRF(4), SHV_TRF(5), P.imul[0], P.imul[1]};
 #undef SHV_TRF
+    K.sn_c1q = c_leap_snk[0];
+    K.sn_c2p = c_leap_snk[1];
+    K.sn_c1s = c_leap_snk[2];
+    K.sn_c2s = c_leap_snk[3];
+    K.sn_M = c_leap_snk[4];
     const uint32_t lo4 = lane * 4u;  // unswizzled box: word `lane` of each 128-B row
     const uint64_t items = P.tr_tb * P.tr_ps;
     const uint64_t wstride = (uint64_t)gridDim.x * (blockDim.x >> 5);
@@ -453,7 +468,8 @@ __global__ void __launch_bounds__(kTrWarps * 32)
             if (x & 1) apply(P.segpow[b].a, P.segpow[b].b, m);
         for (uint64_t b = 0, x = ps; x; ++b, x >>= 1)
             if (x & 1) apply(P.tr_ppow[b].a, P.tr_ppow[b].b, m);
-        MrgIF g = to_mrg_if(m);
+        LeapMrgGen g;
+        make_leap_gen(m, g);
         for (uint64_t pc = p0; pc < p1; pc += kTrRows) {
             if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
             __syncwarp();

@@ -67,12 +67,16 @@ namespace {
 __constant__ double c_mrg_fpk[6] = {6755399441055744.0, 1.0 / 4294967087.0, 0x1.000059451f212p-32,
                                     4294967087.0, 4294944443.0, 5886603609186927.0};
 // MrgSN constants (MrgFpK::sn_* order): bit i of SHV_MRG_SN_CKMASK takes
-// c_mrg_snk[i] instead of the launch parameter.
+// c_mrg_snk[i] instead of the launch parameter; c_mrg_snk[5] = RN(1/m1) 2^1010
+// (the lane starts reduce plain sums, not 4q).
 #ifndef SHV_MRG_SN_CKMASK
 #define SHV_MRG_SN_CKMASK 12  // c1s, c2s from constant memory: the DFMA.RM multiplicand as a uniform-register operand
 #endif
-__constant__ double c_mrg_snk[5] = {0x0.317b9fd79a126p-1022, 0x1.4e9d5b50f226fp-1022, 0x1.000000d10000bp+980,
-                                    0x1.000059451f212p+978, 0x1.8p-12};
+__constant__ double c_mrg_snk[6] = {0x0.317b9fd79a126p-1022, 0x1.4e9d5b50f226fp-1022, 0x1.000000d10000bp+980,
+                                    0x1.000059451f212p+978, 0x1.8p-12, 0x1.000000d10000bp+978};
+#ifndef SHV_MRG_SN_LANE
+#define SHV_MRG_SN_LANE 1  // MrgSN lane starts in the subnormal representation (split_row_sn)
+#endif
 template <int MASK>
 __device__ __forceinline__ MrgFpK load_fpk(const MrgLaunch& P)
 {
@@ -504,12 +508,50 @@ __device__ __forceinline__ Gen apply_split(const double* __restrict__ tab, uint3
     return g;
 }
 
+// Row r of one component in the subnormal representation (MrgSN, DESIGN.md
+// §4.2): v as the pairs D(v) = {v, 0}; Ah = sum Mh_q v_q and Al = sum Ml_q v_q
+// are exact (< 3 * 2^48 units) and their bit patterns are the integers, so
+// rh = Ah mod m = lo(Ah) + c floor(Ah / m) (one DFMA.RM and one IMAD), then
+// X = rh 2^16 + Al < 2^50 the same way. 9 FP64 + 2 IMAD, canonical u32 out.
+__device__ __forceinline__ uint32_t split_row_sn(const double* __restrict__ lt, uint32_t stride, uint32_t e0,
+                                                 double v0, double v1, double v2, double cinv, double M, uint32_t c)
+{
+    const double h0 = lt[(e0 + 0) * stride], l0 = lt[(e0 + 1) * stride];
+    const double h1 = lt[(e0 + 2) * stride], l1 = lt[(e0 + 3) * stride];
+    const double h2 = lt[(e0 + 4) * stride], l2 = lt[(e0 + 5) * stride];
+    const double ah = __fma_rn(h2, v2, __fma_rn(h1, v1, __dmul_rn(h0, v0)));
+    const double al = __fma_rn(l2, v2, __fma_rn(l1, v1, __dmul_rn(l0, v0)));
+    const uint32_t rh = (uint32_t)__double2loint(ah) + c * (uint32_t)__double2loint(__fma_rd(ah, cinv, M));
+    const double x = __fma_rn(65536.0, mrg_sn(rh), al);
+    return (uint32_t)__double2loint(x) + c * (uint32_t)__double2loint(__fma_rd(x, cinv, M));
+}
+
+__device__ __forceinline__ MrgSN apply_split_sn(const double* __restrict__ tab, uint32_t stride, const uint32_t w[6],
+                                                const MrgFpK& K)
+{
+    const double c1 = c_mrg_snk[5];  // RN(1/m1) 2^1010 (the plain, not the 4x, inverse)
+    const double x0 = mrg_sn(w[0]), x1 = mrg_sn(w[1]), x2 = mrg_sn(w[2]);
+    const double y0 = mrg_sn(w[3]), y1 = mrg_sn(w[4]), y2 = mrg_sn(w[5]);
+    MrgSN g;
+    g.x0 = split_row_sn(tab, stride, 0, x0, x1, x2, c1, K.sn_M, kC1);
+    g.x1 = split_row_sn(tab, stride, 6, x0, x1, x2, c1, K.sn_M, kC1);
+    g.x2 = split_row_sn(tab, stride, 12, x0, x1, x2, c1, K.sn_M, kC1);
+    g.y0 = split_row_sn(tab, stride, 18, y0, y1, y2, K.sn_c2s, K.sn_M, kC2);
+    g.y1 = split_row_sn(tab, stride, 24, y0, y1, y2, K.sn_c2s, K.sn_M, kC2);
+    g.y2 = split_row_sn(tab, stride, 30, y0, y1, y2, K.sn_c2s, K.sn_M, kC2);
+    return g;
+}
+
 // Start state of a row-tile lane: lanetab[jl] * (x, y).
 template <class Gen>
 __device__ __forceinline__ Gen lane_start(const double* __restrict__ lt, uint32_t jl, const uint32_t w[6], const MrgFpK& K)
 {
-    return apply_split<Gen>(lt + jl, 32, __uint2double_rn(w[0]), __uint2double_rn(w[1]), __uint2double_rn(w[2]),
-                            __uint2double_rn(w[3]), __uint2double_rn(w[4]), __uint2double_rn(w[5]), K);
+    if constexpr (std::is_same<Gen, MrgSN>::value && SHV_MRG_SN_LANE) {
+        return apply_split_sn(lt + jl, 32, w, K);
+    } else {
+        return apply_split<Gen>(lt + jl, 32, __uint2double_rn(w[0]), __uint2double_rn(w[1]), __uint2double_rn(w[2]),
+                                __uint2double_rn(w[3]), __uint2double_rn(w[4]), __uint2double_rn(w[5]), K);
+    }
 }
 
 // A lane that ended segment j of a tile (at offset (j + 1) S) continues with
@@ -517,10 +559,19 @@ __device__ __forceinline__ Gen lane_start(const double* __restrict__ lt, uint32_
 template <class Gen>
 __device__ __forceinline__ Gen lane_advance(const double* __restrict__ st31, const Gen& g, const MrgFpK& K)
 {
-    return apply_split<Gen>(st31, 1, x_of(g.x0), x_of(g.x1), x_of(g.x2), x_of(g.y0), x_of(g.y1), x_of(g.y2), K);
+    if constexpr (std::is_same<Gen, MrgSN>::value && SHV_MRG_SN_LANE) {
+        const uint32_t w[6] = {g.x0, g.x1, g.x2, g.y0, g.y1, g.y2};
+        return apply_split_sn(st31, 1, w, K);
+    } else {
+        return apply_split<Gen>(st31, 1, x_of(g.x0), x_of(g.x1), x_of(g.x2), x_of(g.y0), x_of(g.y1), x_of(g.y2), K);
+    }
 }
 
+#if defined(SHV_LAB_GEN_HEADER) && SHV_MRG_ROWS_STEP == 9
+using GenRows = MrgNullRows;  // tools/lab builds only: the store-path ceiling of the row tiles
+#else
 using GenRows = StepGen<SHV_MRG_ROWS_STEP>;
+#endif
 
 __device__ __forceinline__ void prefetch_words(const MrgLaunch& P, uint32_t i)
 {

@@ -215,3 +215,31 @@ def test_sn_step_emulated_matches_recurrence():
         assert n2 == (A21 * y[2] - A23N * y[0]) % M2
         x = [x[1], x[2], n1]
         y = [y[1], y[2], n2]
+
+
+def test_sn_lane_start_split_row():
+    """split_row_sn (kernels_mrg.cu): Ah = sum Mh v, Al = sum Ml v with 16-bit
+    halves, rh = Ah mod m by the plain inverse RN(1/m1) 2^1010 (c_mrg_snk[5]) or
+    RU(1/m2) 2^1010, X = rh 2^16 + Al, r = X mod m; emulated with exact rationals."""
+    src = open(os.path.join(os.path.dirname(HDR), "..", "paper_1412_8266_b200", "csrc", "kernels_mrg.cu")).read()
+    assert "0x1.000000d10000bp+978" in src
+    c1u = float.fromhex("0x1.000000d10000bp+978")
+    assert Fr(c1u) == Fr(INV1) * 2**1010
+    amax = 3 * 65535 * (2**32 - 1)
+    xmax = (M1 - 1) * 2**16 + amax
+    assert amax < 2**49.6 and xmax < 2**50
+    for d, m in ((Fr(INV1) - Fr(1, M1), M1), (Fr(INV2) - Fr(1, M2), M2)):
+        assert xmax * m * d < 1 and amax * m * d < 1
+    rng = random.Random(2026)
+
+    def row(Mrow, v, cinv, m, c):
+        ah = sum((Mq >> 16) * vq for Mq, vq in zip(Mrow, v))
+        al = sum((Mq & 0xFFFF) * vq for Mq, vq in zip(Mrow, v))
+        rh = ((ah & 0xFFFFFFFF) + c * fma_rd_lo(D(ah), cinv, SN_M)) % 2**32
+        x = rh * 65536 + al
+        return ((x & 0xFFFFFFFF) + c * fma_rd_lo(D(x), cinv, SN_M)) % 2**32
+    for m, c, cinv in ((M1, 209, c1u), (M2, 22853, SN_C2S)):
+        for _ in range(400):
+            Mrow = [rng.choice([0, 1, m - 1, rng.randrange(m)]) for _ in range(3)]
+            v = [rng.choice([0, 1, m - 1, rng.randrange(m)]) for _ in range(3)]
+            assert row(Mrow, v, cinv, m, c) == sum(a * b for a, b in zip(Mrow, v)) % m
