@@ -356,6 +356,7 @@ __device__ __forceinline__ uint32_t mrg_next(MrgSN& s, const MrgFpK& K = mrg_fpk
 
 __device__ __forceinline__ MrgSN to_mrg_sn(const Mrg& s) { return MrgSN{s.x0, s.x1, s.x2, s.y0, s.y1, s.y2}; }
 
+
 // ------------------------------------------------------------------ Philox4x32-10
 
 struct W4 {
