@@ -18,28 +18,6 @@
 
 namespace shv {
 namespace {
-// A 32-bit Philox key word of the u64 launch field. With SHV_LEAP_KEY32 = 1 it
-// goes through an opaque move: with the u64 visible, the front end widens the
-// round XORs to 64 bits and ptxas adds a zero high word after every IMAD.WIDE
-// (the transposed Leap Frog fill runs 15.3 instead of 11.0 instructions per
-// value). The leaner kernel measured SLOWER at the C5 shape (3.65 vs 3.22-3.31
-// ms, lab56): that fill is bound by its scattered box stores (rows 16 KB apart),
-// and faster generation congests them further, so the default keeps the cast.
-#ifndef SHV_LEAP_KEY32
-#define SHV_LEAP_KEY32 0
-#endif
-__device__ __forceinline__ uint32_t key32(uint64_t k)
-{
-    if (!SHV_LEAP_KEY32) return (uint32_t)k;
-    uint32_t r;
-    asm("mov.b32 %0, %1;" : "=r"(r) : "r"((uint32_t)k));
-    return r;
-}
-}  // namespace
-}  // namespace shv
-
-namespace shv {
-namespace {
 
 // (c0 u0 + c1 u1 + c2 u2) mod (2^32 - C), all operands < 2^32 - C. The three
 // 64-bit products are summed with carries (s = cy*2^64 + s2), then folded with
@@ -123,7 +101,7 @@ struct LeapCursor<kLeapPhilox> {
     {
         const uint64_t b = (uint64_t)(d >> 2);
         if (!valid || b != cb) {
-            v = philox_blk(b, 0, key32(P.k0), key32(P.k1));
+            v = philox_blk(b, 0, (uint32_t)P.k0, (uint32_t)P.k1);
             cb = b;
             valid = true;
         }
@@ -256,7 +234,7 @@ struct LeapGroup {
     }
     __device__ __forceinline__ W4 next(const LeapLaunch& P)
     {
-        const W4 v = philox_blk(b, 0, key32(P.k0), key32(P.k1));
+        const W4 v = philox_blk(b, 0, (uint32_t)P.k0, (uint32_t)P.k1);
         b += step;
         return v;
     }
@@ -530,8 +508,7 @@ template <int KIND, int G, bool HOIST>
 __device__ __forceinline__ void leap_ctr_run(const LeapLaunch& P, const CUtensorMap* tmap, unsigned lane, uint32_t box,
                                              uint32_t lo4, uint64_t tb, uint64_t p0, uint64_t p1, uint64_t b)
 {
-    const uint32_t pk0 = key32(P.k0), pk1 = key32(P.k1);
-    const uint64_t q = (uint64_t)kPM0 * ((uint32_t)(b >> 32) ^ pk0);
+    const uint64_t q = (uint64_t)kPM0 * ((uint32_t)(b >> 32) ^ (uint32_t)P.k0);
     uint64_t pa = (uint64_t)kPM0 * (uint32_t)b;
     for (uint64_t pc = p0; pc < p1; pc += kTrRows) {
         if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
@@ -543,13 +520,13 @@ __device__ __forceinline__ void leap_ctr_run(const LeapLaunch& P, const CUtensor
             if constexpr (G == kLeapPhilox) {
                 W4 v0, v1;
                 if constexpr (HOIST) {
-                    v0 = philox10_from_r2(pa, q, 0u, 0u, pk0, pk1);
+                    v0 = philox10_from_r2(pa, q, 0u, 0u, (uint32_t)P.k0, (uint32_t)P.k1);
                     pa = add64w(pa, kPM0);
-                    v1 = philox10_from_r2(pa, q, 0u, 0u, pk0, pk1);
+                    v1 = philox10_from_r2(pa, q, 0u, 0u, (uint32_t)P.k0, (uint32_t)P.k1);
                     pa = add64w(pa, kPM0);
                 } else {
-                    v0 = philox_blk(b, 0, pk0, pk1);
-                    v1 = philox_blk(b + 1, 0, pk0, pk1);
+                    v0 = philox_blk(b, 0, (uint32_t)P.k0, (uint32_t)P.k1);
+                    v1 = philox_blk(b + 1, 0, (uint32_t)P.k0, (uint32_t)P.k1);
                 }
                 b += 2;
                 z[0] = v0.x; z[1] = v0.y; z[2] = v0.z; z[3] = v0.w;
