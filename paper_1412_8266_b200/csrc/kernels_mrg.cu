@@ -290,7 +290,7 @@ __global__ void __launch_bounds__(256, SHV_MRG_MINB) mrg_fill_vec_kernel(const _
 #define SHV_MRG_TMA_MINB (SHV_MRG_STEP == 4 ? 4 : 2)  // lab sweep: FF 4 blocks, IF 2 blocks per SM
 #endif
 #ifndef SHV_MRG_PIN
-#define SHV_MRG_PIN 1  // state through an empty volatile asm after each 4-value store (see pin_state)
+#define SHV_MRG_PIN 1  // state through an empty volatile asm after every SHV_MRG_PIN-th 4-value store (0: never)
 #endif
 // An empty volatile asm the state passes through: volatile asms keep their
 // order, so ptxas cannot run the serial component-2 chain of later groups
@@ -342,7 +342,7 @@ __device__ __forceinline__ void mrg_tma_rounds(const CUtensorMap* tmap, const Mr
                 asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(rowsw ^ (q << 4)), "r"(a.x), "r"(a.y),
                              "r"(a.z), "r"(a.w)
                              : "memory");
-                if (SHV_MRG_PIN) pin_state(s);
+                if (SHV_MRG_PIN && q % SHV_MRG_PIN == SHV_MRG_PIN - 1) pin_state(s);
             }
         } else {
 #pragma unroll
