@@ -97,7 +97,7 @@ def run():
         shv.shv_streams_destroy(h)
     # MRG32k3a row-tile fill (mrg_fill_rows_kernel): forced at a small shape by a
     # 1-block x 32-thread grid; nseg 32 and nseg 3 (tiles spanning rows, ragged)
-    for ns_, n in ((600, 4096), (3201, 384), (64, 256 * 32 * 5)):  # S 256 nseg 16; S 128 nseg 3; run mode (10 tiles per row)
+    for ns_, n in ((600, 4096), (3201, 384), (64, 256 * 32 * 5)):  # S 128 nseg 32; S 128 nseg 3; run mode (10 tiles per row)
         st = torch.empty(6 * ns_, dtype=torch.int32, device="cuda")
         h = shv.shv_streams_create_ex(W.MRG32K3A, [12345], 3, ns_, 1, st, 0, dev, None)
         shv.shv_set_launch_config(h, 1, 32, 0)
