@@ -20,6 +20,14 @@
 #define SHV_LEAP_MRG_UNROLL 4  // 8-value groups per box unrolled in the transposed MRG32k3a fill (4: 3.28 vs 3.49 ms, lab61)
 #endif
 constexpr int kLeapMrgUnroll = SHV_LEAP_MRG_UNROLL;
+// the same for the counter-based transposed fills (lab62): Philox 1 (3.16 vs
+// 3.53-3.64 ms unrolled), Threefry 4 (6.00 vs 6.20 ms)
+#ifndef SHV_LEAP_PHILOX_UNROLL
+#define SHV_LEAP_PHILOX_UNROLL 1
+#endif
+#ifndef SHV_LEAP_THREEFRY_UNROLL
+#define SHV_LEAP_THREEFRY_UNROLL 4
+#endif
 
 namespace shv {
 namespace {
@@ -513,12 +521,13 @@ template <int KIND, int G, bool HOIST>
 __device__ __forceinline__ void leap_ctr_run(const LeapLaunch& P, const CUtensorMap* tmap, unsigned lane, uint32_t box,
                                              uint32_t lo4, uint64_t tb, uint64_t p0, uint64_t p1, uint64_t b)
 {
+    constexpr int kUnroll = G == kLeapPhilox ? SHV_LEAP_PHILOX_UNROLL : SHV_LEAP_THREEFRY_UNROLL;
     const uint64_t q = (uint64_t)kPM0 * ((uint32_t)(b >> 32) ^ (uint32_t)P.k0);
     uint64_t pa = (uint64_t)kPM0 * (uint32_t)b;
     for (uint64_t pc = p0; pc < p1; pc += kTrRows) {
         if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
         __syncwarp();
-#pragma unroll 1
+#pragma unroll kUnroll
         for (uint32_t q8 = 0; q8 < kTrRows; q8 += 8) {
             const uint32_t rb = box + q8 * 128u;
             uint32_t z[8];
