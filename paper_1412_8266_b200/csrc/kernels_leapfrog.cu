@@ -426,7 +426,10 @@ cudaError_t leap_tma_attr()
 // and columns past n are clipped by the tensor map. Per value: the MRG step
 // (MrgIF) and one shared store, against three modular products per component
 // for the per-player recurrence.
-constexpr unsigned kTrWarps = 4;
+#ifndef SHV_LEAP_TR_WARPS
+#define SHV_LEAP_TR_WARPS 4
+#endif
+constexpr unsigned kTrWarps = SHV_LEAP_TR_WARPS;
 // Players per transposed box (rows of the 128-B wide box): 32 keeps a warp's
 // box at 4 KB, so up to 48 warps per SM stay resident (128-row, 16-KB boxes
 // held the transposed fills to 12 warps per SM: ncu 0.74 eligible warps per

@@ -458,6 +458,10 @@ __global__ void __launch_bounds__(256) tm_leap_mc_kernel(const __grid_constant__
 // value, after one GF(2) jump to its start (per-bit tables T^(2^b)). Draw
 // (p, t) is word t of box row p; each 128-player box leaves by TMA.
 constexpr unsigned kTmTrWarps = 4;
+#ifndef SHV_TM_LEAP_UNROLL
+#define SHV_TM_LEAP_UNROLL 1  // 8-value groups per iteration of the transposed fill's box loop
+#endif
+constexpr int kTmLeapUnroll = SHV_TM_LEAP_UNROLL;
 template <int KIND>
 __global__ void __launch_bounds__(kTmTrWarps * 32)
     tm_leap_tr_kernel(const __grid_constant__ TmLeapLaunch P, const __grid_constant__ CUtensorMap tmap)
@@ -483,7 +487,7 @@ __global__ void __launch_bounds__(kTmTrWarps * 32)
         for (uint64_t pc = p0; pc < p1; pc += 128) {
             if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
             __syncwarp();
-#pragma unroll 1
+#pragma unroll kTmLeapUnroll
             for (uint32_t q8 = 0; q8 < 128; q8 += 8) {
                 const uint32_t rb = box + q8 * 128u;
 #pragma unroll
