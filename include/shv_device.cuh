@@ -356,6 +356,43 @@ __device__ __forceinline__ uint32_t mrg_next(MrgSN& s, const MrgFpK& K = mrg_fpk
 
 __device__ __forceinline__ MrgSN to_mrg_sn(const Mrg& s) { return MrgSN{s.x0, s.x1, s.x2, s.y0, s.y1, s.y2}; }
 
+// MrgMF: the same subnormal representation with magic-free quotients. In the
+// subnormal range every double has ulp 2^-1074, so for p_sub = D(p)
+//   k_sub = mul.rm(p_sub, inv) = floor(p * inv) * 2^-1074 = D(k)
+// exactly (the product is rounded once, toward -inf, onto the 2^-1074 grid;
+// floor(p * inv) = floor(p / m) by the floor step's inverse bounds), and
+//   r_sub = fma(-k_sub, m, p_sub) = D(p - k m)
+// is the next state pair itself (bits {r, 0}) with the output in its low word.
+// 4 FP64 instructions per component and no integer or move instructions:
+// component 1 takes the signed form (|p| < 2^52.42; r in [0, m1], m1 only at
+// p = k m1 < 0, as in mrg_c1_floor), component 2 the positive form.
+struct MrgMF {
+    double x0, x1, x2;  // D(x), component 1
+    double y0, y1, y2;  // D(y), component 2
+};
+
+__device__ __forceinline__ uint32_t mrg_next(MrgMF& s, const MrgFpK& K = mrg_fpk())
+{
+    const double t1 = __dmul_rn((double)kA13n, s.x0);
+    const double p1 = __fma_rn((double)kA12, s.x1, -t1);
+    const double r1 = __fma_rn(-__dmul_rd(p1, K.inv1), K.m1, p1);
+    s.x0 = s.x1;
+    s.x1 = s.x2;
+    s.x2 = r1;
+    const double t2 = __fma_rn(-(double)kA23n, s.y0, K.sn_c2p);
+    const double p2 = __fma_rn((double)kA21, s.y2, t2);
+    const double r2 = __fma_rn(-__dmul_rd(p2, K.inv2), K.m2, p2);
+    s.y0 = s.y1;
+    s.y1 = s.y2;
+    s.y2 = r2;
+    return mrg_combine((uint32_t)__double2loint(r1), (uint32_t)__double2loint(r2));
+}
+
+__device__ __forceinline__ MrgMF to_mrg_mf(const Mrg& s)
+{
+    return MrgMF{mrg_sn(s.x0), mrg_sn(s.x1), mrg_sn(s.x2), mrg_sn(s.y0), mrg_sn(s.y1), mrg_sn(s.y2)};
+}
+
 
 // ------------------------------------------------------------------ Philox4x32-10
 

@@ -452,8 +452,10 @@ __constant__ double c_leap_snk[5] = {0x0.317b9fd79a126p-1022, 0x1.4e9d5b50f226fp
 #ifndef SHV_LEAP_STEP
 #define SHV_LEAP_STEP 3  // step of the transposed MRG32k3a Leap Frog fill: 3 = MrgIF, 5 = MrgSN (3.69 vs 3.48 ms, lab51)
 #endif
-using LeapMrgGen = std::conditional<SHV_LEAP_STEP == 5, MrgSN, MrgIF>::type;
+using LeapMrgGen = std::conditional<SHV_LEAP_STEP == 5, MrgSN,
+                                    std::conditional<SHV_LEAP_STEP == 7, MrgMF, MrgIF>::type>::type;
 __device__ __forceinline__ void make_leap_gen(const Mrg& m, MrgSN& g) { g = to_mrg_sn(m); }
+__device__ __forceinline__ void make_leap_gen(const Mrg& m, MrgMF& g) { g = to_mrg_mf(m); }
 __device__ __forceinline__ void make_leap_gen(const Mrg& m, MrgIF& g) { g = to_mrg_if(m); }
 template <int KIND>
 __global__ void __launch_bounds__(kTrWarps * 32)

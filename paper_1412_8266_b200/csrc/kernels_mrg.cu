@@ -3,15 +3,15 @@
 // fused Monte Carlo pi kernel. Common pieces: kernels_common.cuh.
 //
 // The u32/f32 fills of shapes that split into row tiles run
-// mrg_fill_rows_kernel (MrgIF step); other vector shapes run the
+// mrg_fill_rows_kernel (MrgMF step); other vector shapes run the
 // stream-per-lane TMA kernel (u32/f32) or the staged vector kernel (f64), both
 // on the MrgFF step; ragged shapes run the scalar kernel.
 //
 // Compile-time knobs (defaults = the product; tools/lab/build_knobs.sh builds
 // variants for the labs, every variant gives bit-identical output):
 //   SHV_MRG_STEP     step of the stream-per-lane fills: 4 = MrgFF, 3 = MrgIF
-//   SHV_MRG_MC_STEP  step of the fused Monte Carlo kernel: 5 = MrgSN, 3 = MrgIF
-//                    (474 vs 493 ms for 2^38 samples), 4 = MrgFF
+//   SHV_MRG_MC_STEP  step of the fused Monte Carlo kernel: 7 = MrgMF (385 ms for
+//                    2^38 samples), 5 = MrgSN (405-409), 3 = MrgIF (464-474), 4 = MrgFF
 //   SHV_MRG_MC_HIT   dartboard test: 1 = FP64 (471 vs 474 ms), 0 = integer
 //   SHV_MRG_STAGE    staging of the vector fill: 1 = stage the f64 outputs only
 //   SHV_MRG_MINB, SHV_MRG_TMA_MINB, SHV_MRG_ROWS_MINB: min-blocks hints
@@ -23,10 +23,10 @@
 #define SHV_MRG_STEP 4
 #endif
 #ifndef SHV_MRG_MC_STEP
-#define SHV_MRG_MC_STEP 5
+#define SHV_MRG_MC_STEP 7
 #endif
 #ifndef SHV_MRG_ROWS_STEP
-#define SHV_MRG_ROWS_STEP 5  // step of the row-tile fill: 5 = MrgSN, 3 = MrgIF, 4 = MrgFF (lab: IF faster than FF, lab34)
+#define SHV_MRG_ROWS_STEP 7  // step of the row-tile fill: 7 = MrgMF (2.75 vs 3.21 ms for MrgSN, lab65), 5 = MrgSN, 3 = MrgIF, 4 = MrgFF
 #endif
 #ifndef SHV_MRG_MC_HIT
 #define SHV_MRG_MC_HIT 1  // dartboard test: 1 = FP64 (hit_fp64), 0 = integer (2 IMAD.WIDE)
@@ -96,9 +96,12 @@ __device__ __forceinline__ MrgFpK load_fpk(const MrgLaunch& P)
 __device__ __forceinline__ void make_gen(const Mrg& s, MrgFF& g) { g = to_mrg_ff(s); }
 __device__ __forceinline__ void make_gen(const Mrg& s, MrgIF& g) { g = to_mrg_if(s); }
 __device__ __forceinline__ void make_gen(const Mrg& s, MrgSN& g) { g = to_mrg_sn(s); }
-// Step of a kernel by knob value: 3 = MrgIF, 4 = MrgFF, 5 = MrgSN.
+__device__ __forceinline__ void make_gen(const Mrg& s, MrgMF& g) { g = to_mrg_mf(s); }
+// Step of a kernel by knob value: 3 = MrgIF, 4 = MrgFF, 5 = MrgSN, 7 = MrgMF.
 template <int STEP>
-using StepGen = typename std::conditional<STEP == 4, MrgFF, typename std::conditional<STEP == 5, MrgSN, MrgIF>::type>::type;
+using StepGen = typename std::conditional<
+    STEP == 4, MrgFF,
+    typename std::conditional<STEP == 5, MrgSN, typename std::conditional<STEP == 7, MrgMF, MrgIF>::type>::type>::type;
 #ifdef SHV_LAB_GEN_HEADER  // tools/lab builds only: stand-in generators (never in libshv.so)
 #include SHV_LAB_GEN_HEADER
 using GenFill = SHV_LAB_GEN;
@@ -299,6 +302,10 @@ __global__ void __launch_bounds__(256, SHV_MRG_MINB) mrg_fill_vec_kernel(const _
 __device__ __forceinline__ void pin_state(MrgSN& g)
 {
     asm volatile("" : "+r"(g.x0), "+r"(g.x1), "+r"(g.x2), "+r"(g.y0), "+r"(g.y1), "+r"(g.y2));
+}
+__device__ __forceinline__ void pin_state(MrgMF& g)
+{
+    asm volatile("" : "+d"(g.x0), "+d"(g.x1), "+d"(g.x2), "+d"(g.y0), "+d"(g.y1), "+d"(g.y2));
 }
 __device__ __forceinline__ void pin_state(MrgIF& g)
 {
@@ -542,11 +549,18 @@ __device__ __forceinline__ MrgSN apply_split_sn(const double* __restrict__ tab, 
     return g;
 }
 
+__device__ __forceinline__ MrgMF mf_of(const MrgSN& g)
+{
+    return MrgMF{mrg_sn(g.x0), mrg_sn(g.x1), mrg_sn(g.x2), mrg_sn(g.y0), mrg_sn(g.y1), mrg_sn(g.y2)};
+}
+
 // Start state of a row-tile lane: lanetab[jl] * (x, y).
 template <class Gen>
 __device__ __forceinline__ Gen lane_start(const double* __restrict__ lt, uint32_t jl, const uint32_t w[6], const MrgFpK& K)
 {
-    if constexpr (std::is_same<Gen, MrgSN>::value && SHV_MRG_SN_LANE) {
+    if constexpr (std::is_same<Gen, MrgMF>::value) {
+        return mf_of(apply_split_sn(lt + jl, 32, w, K));
+    } else if constexpr (std::is_same<Gen, MrgSN>::value && SHV_MRG_SN_LANE) {
         return apply_split_sn(lt + jl, 32, w, K);
     } else {
         return apply_split<Gen>(lt + jl, 32, __uint2double_rn(w[0]), __uint2double_rn(w[1]), __uint2double_rn(w[2]),
@@ -559,7 +573,12 @@ __device__ __forceinline__ Gen lane_start(const double* __restrict__ lt, uint32_
 template <class Gen>
 __device__ __forceinline__ Gen lane_advance(const double* __restrict__ st31, const Gen& g, const MrgFpK& K)
 {
-    if constexpr (std::is_same<Gen, MrgSN>::value && SHV_MRG_SN_LANE) {
+    if constexpr (std::is_same<Gen, MrgMF>::value) {
+        const uint32_t w[6] = {(uint32_t)__double2loint(g.x0), (uint32_t)__double2loint(g.x1),
+                               (uint32_t)__double2loint(g.x2), (uint32_t)__double2loint(g.y0),
+                               (uint32_t)__double2loint(g.y1), (uint32_t)__double2loint(g.y2)};
+        return mf_of(apply_split_sn(st31, 1, w, K));
+    } else if constexpr (std::is_same<Gen, MrgSN>::value && SHV_MRG_SN_LANE) {
         const uint32_t w[6] = {g.x0, g.x1, g.x2, g.y0, g.y1, g.y2};
         return apply_split_sn(st31, 1, w, K);
     } else {

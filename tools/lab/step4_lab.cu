@@ -68,6 +68,29 @@ __device__ __forceinline__ double c2_fp(double y0, double y2, const SK& K)
     return __fma_rn(-__dadd_rn(Q, -K.M), K.m2s, p);
 }
 
+// Magic-free quotients: in the subnormal range every double has ulp 2^-1074,
+// so k_sub = mul.rm(p_sub, inv) = floor(p inv) 2^-1074 = D(k) exactly (no
+// magic constant), and r_sub = fma(-k_sub, m, p_sub) = D(p - k m) is the next
+// state pair itself (bits {r, 0}) and its low word the output. 4 FP64 ops per
+// component, no integer instructions, no zero moves.
+__device__ __forceinline__ double c1_mf(double x0, double x1, double inv1, double m1)
+{
+    const double t = __dmul_rn(810728.0, x0);
+    const double p = __fma_rn(1403580.0, x1, -t);            // signed, |p| < 2^52.42
+    const double k = __dmul_rd(p, inv1);                      // D(floor(p / m1)) (negative allowed)
+    return __fma_rn(-k, m1, p);                               // D(r), r in [0, m1]
+}
+__device__ __forceinline__ double c2_mf(double y0, double y2, double inv2, double m2, double c2p)
+{
+    const double t = __fma_rn(-1370589.0, y0, c2p);
+    const double p = __fma_rn(527612.0, y2, t);
+    const double k = __dmul_rd(p, inv2);
+    return __fma_rn(-k, m2, p);
+}
+struct SE { double x0, x1, x2, y0, y1, y2; };
+struct SF { uint32_t x0, x1, x2; double y0, y1, y2; };
+struct SG { double x0, x1, x2; uint32_t y0, y1, y2; };
+
 struct SA { uint32_t x0, x1, x2, y0, y1, y2; };
 struct SB { double x0, x1, x2; uint32_t y0, y1, y2; };
 struct SC { double x0, x1, x2, y0, y1, y2; };
@@ -106,6 +129,32 @@ __device__ __forceinline__ uint32_t nxt(SDs& s, const SK& K)
     return mrg_combine(p1, lo(r2));
 }
 
+struct MK { double inv1, inv2, m1, m2; };
+__device__ __forceinline__ uint32_t nxt(SE& s, const SK& K, const MK& Q)
+{
+    const double r1 = c1_mf(s.x0, s.x1, Q.inv1, Q.m1);
+    s.x0 = s.x1; s.x1 = s.x2; s.x2 = r1;
+    const double r2 = c2_mf(s.y0, s.y2, Q.inv2, Q.m2, K.c2p);
+    s.y0 = s.y1; s.y1 = s.y2; s.y2 = r2;
+    return mrg_combine(lo(r1), lo(r2));
+}
+__device__ __forceinline__ uint32_t nxt(SF& s, const SK& K, const MK& Q)
+{
+    const uint32_t p1 = c1_int(s.x0, s.x1, K);
+    s.x0 = s.x1; s.x1 = s.x2; s.x2 = p1;
+    const double r2 = c2_mf(s.y0, s.y2, Q.inv2, Q.m2, K.c2p);
+    s.y0 = s.y1; s.y1 = s.y2; s.y2 = r2;
+    return mrg_combine(p1, lo(r2));
+}
+__device__ __forceinline__ uint32_t nxt(SG& s, const SK& K, const MK& Q)
+{
+    const double r1 = c1_mf(s.x0, s.x1, Q.inv1, Q.m1);
+    s.x0 = s.x1; s.x1 = s.x2; s.x2 = r1;
+    const uint32_t p2 = c2_int(s.y0, s.y2, K);
+    s.y0 = s.y1; s.y1 = s.y2; s.y2 = p2;
+    return mrg_combine(lo(r1), p2);
+}
+
 // combine without ISETP: w = r2 - r1 with borrow b = (r1 > r2) as a mask;
 // r1 <= r2: z = -w + m1 (r1 == r2 -> m1), else z = -w.
 __device__ __forceinline__ uint32_t combine_cc(uint32_t p1, uint32_t p2)
@@ -142,6 +191,10 @@ __global__ void __launch_bounds__(256) k(uint32_t* out, const __grid_constant__ 
     SB b{D(s0.x0), D(s0.x1), D(s0.x2), s0.y0, s0.y1, s0.y2};
     SC c{D(s0.x0), D(s0.x1), D(s0.x2), D(s0.y0), D(s0.y1), D(s0.y2)};
     SDs d{s0.x0, s0.x1, s0.x2, D(s0.y0), D(s0.y1), D(s0.y2)};
+    SE e{D(s0.x0), D(s0.x1), D(s0.x2), D(s0.y0), D(s0.y1), D(s0.y2)};
+    SF ff{s0.x0, s0.x1, s0.x2, D(s0.y0), D(s0.y1), D(s0.y2)};
+    SG gg{D(s0.x0), D(s0.x1), D(s0.x2), s0.y0, s0.y1, s0.y2};
+    const MK Q{p.v[1], p.v[2], p.v[3], p.v[4]};
     Mrg ri = s0;
     uint32_t acc = 0;
     for (int i = 0; i < iters; ++i) {
@@ -155,6 +208,9 @@ __global__ void __launch_bounds__(256) k(uint32_t* out, const __grid_constant__ 
             else if (V == 4) z = nxt(c, S);
             else if (V == 5) z = nxt(d, S);
             else if (V == 7) z = nxt(ac, S);
+            else if (V == 8) z = nxt(e, S, Q);
+            else if (V == 9) z = nxt(ff, S, Q);
+            else if (V == 10) z = nxt(gg, S, Q);
             else z = mrg_next(ri, K);
             acc += z;
         }
@@ -184,7 +240,7 @@ int main()
     memcpy(&p.c2p, &c2p, 8);
     uint32_t* o; cudaMalloc(&o, (size_t)sms * 16 * 256 * 4);
     const int iters = 768;
-    const char* names[] = {"if", "ff", "sA", "sB", "sC", "sD", "int", "sAc"};
+    const char* names[] = {"if", "ff", "sA", "sB", "sC", "sD", "int", "sAc", "sE", "sF", "sG"};
     printf("{");
     auto run = [&](int v, auto kern) {
         for (int bps : {4, 8}) {
@@ -194,7 +250,7 @@ int main()
         }
     };
     for (int rep = 0; rep < 2; ++rep) {
-        run(0, k<0>); run(1, k<1>); run(2, k<2>); run(3, k<3>); run(4, k<4>); run(5, k<5>); run(7, k<7>);
+        run(0, k<0>); run(2, k<2>); run(4, k<4>); run(8, k<8>); run(9, k<9>); run(10, k<10>);
     }
     const size_t n = (size_t)sms * 8 * 256;
     uint32_t* h = new uint32_t[n]; uint32_t* ref = new uint32_t[n];
@@ -205,7 +261,7 @@ int main()
         size_t bad = 0; for (size_t i = 0; i < n; ++i) bad += h[i] != ref[i];
         printf("\"%s_mismatch\": %zu, ", names[v], bad);
     };
-    chk(0, k<0>); chk(1, k<1>); chk(2, k<2>); chk(3, k<3>); chk(4, k<4>); chk(5, k<5>); chk(7, k<7>);
+    chk(0, k<0>); chk(2, k<2>); chk(4, k<4>); chk(8, k<8>); chk(9, k<9>); chk(10, k<10>);
     int clk; cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, 0);
     printf("\"sms\": %d, \"clock_khz\": %d, \"err\": \"%s\"}\n", sms, clk, cudaGetErrorString(cudaGetLastError()));
 }
