@@ -243,3 +243,59 @@ def test_sn_lane_start_split_row():
             Mrow = [rng.choice([0, 1, m - 1, rng.randrange(m)]) for _ in range(3)]
             v = [rng.choice([0, 1, m - 1, rng.randrange(m)]) for _ in range(3)]
             assert row(Mrow, v, cinv, m, c) == sum(a * b for a, b in zip(Mrow, v)) % m
+
+
+# ---- MrgMF: magic-free subnormal quotients (include/shv_device.cuh, MrgMF)
+
+def mul_rd_sub(a: float, b: float) -> float:
+    """mul.rm(a, b) for a subnormal-range result (|a*b| < 2^-1022): the exact
+    product rounded toward -inf onto the 2^-1074 grid (IEEE 754 directed rounding;
+    every subnormal has ulp 2^-1074)."""
+    v = Fr(a) * Fr(b)
+    assert abs(v) < Fr(2) ** -1022
+    q = math.floor(v * 2**1074)
+    return float(Fr(q, 2**1074))
+
+
+def c1_mf(x0: int, x1: int) -> int:
+    t = 810728.0 * D(x0)                       # exact products and sums (integers < 2^53 units)
+    p = 1403580.0 * D(x1) - t
+    assert Fr(p) * 2**1074 == A12 * x1 - A13N * x0
+    k = mul_rd_sub(p, INV1)                    # D(floor(p / m1)), sign allowed
+    r = float(Fr(p) - Fr(k) * M1)              # fma(-k, m1, p): exact (r is an integer < 2^32 units)
+    assert Fr(r) == Fr(p) - Fr(k) * M1
+    return bits(r)                             # the pair {r, 0}: r in [0, m1]
+
+
+def c2_mf(y0: int, y2: int) -> int:
+    t = -float(A23N) * D(y0) + SN_C2P
+    p = float(A21) * D(y2) + t
+    k = mul_rd_sub(p, INV2)
+    r = float(Fr(p) - Fr(k) * M2)
+    return bits(r)
+
+
+def test_mf_step_emulated_matches_recurrence():
+    rng = random.Random(20261018)
+    i13, i23 = pow(A13N, -1, M1), pow(A23N, -1, M2)
+    for x0 in (0, 1, M1 - 1, M1):
+        for x1 in (0, 1, M1 - 1, M1):
+            r = c1_mf(x0, x1)
+            assert r < 2**32 and (r == (A12 * x1 - A13N * x0) % M1 or (r == M1 and (A12 * x1 - A13N * x0) % M1 == 0))
+    for _ in range(300):  # quotient boundaries: p = k m + {0, 1, m - 1}
+        x1, y2 = rng.randrange(M1), rng.randrange(M2)
+        for res in (0, 1, M1 - 1):
+            x0 = (A12 * x1 - res) * i13 % M1
+            r = c1_mf(x0, x1)
+            assert r == res or (res == 0 and r == M1 and A12 * x1 - A13N * x0 < 0)
+        for res in (0, 1, M2 - 1):
+            y0 = (A21 * y2 - res) * i23 % M2
+            assert c2_mf(y0, y2) == res
+    x = [12345] * 3
+    y = [12345] * 3
+    for _ in range(2000):
+        n1, n2 = c1_mf(x[0], x[1]), c2_mf(y[0], y[2])
+        assert n1 % M1 == (A12 * x[1] - A13N * x[0]) % M1 and n1 <= M1
+        assert n2 == (A21 * y[2] - A23N * y[0]) % M2
+        x = [x[1], x[2], n1]
+        y = [y[1], y[2], n2]
