@@ -12,7 +12,7 @@
 //   SHV_MRG_STEP     step of the stream-per-lane fills: 4 = MrgFF, 3 = MrgIF
 //   SHV_MRG_MC_STEP  step of the fused Monte Carlo kernel: 7 = MrgMF (385 ms for
 //                    2^38 samples), 5 = MrgSN (405-409), 3 = MrgIF (464-474), 4 = MrgFF
-//   SHV_MRG_MC_HIT   dartboard test: 1 = FP64 (471 vs 474 ms), 0 = integer
+//   SHV_MRG_MC_HIT   dartboard test: 0 = integer (MrgMF: 355 vs 387 ms), 1 = FP64 (MrgIF: 471 vs 474)
 //   SHV_MRG_STAGE    staging of the vector fill: 1 = stage the f64 outputs only
 //   SHV_MRG_MINB, SHV_MRG_TMA_MINB, SHV_MRG_ROWS_MINB: min-blocks hints
 //   SHV_MRG_*_CKMASK which FP64 constants come from constant memory
@@ -29,7 +29,7 @@
 #define SHV_MRG_ROWS_STEP 7  // step of the row-tile fill: 7 = MrgMF (2.75 vs 3.21 ms for MrgSN, lab65), 5 = MrgSN, 3 = MrgIF, 4 = MrgFF
 #endif
 #ifndef SHV_MRG_MC_HIT
-#define SHV_MRG_MC_HIT 1  // dartboard test: 1 = FP64 (hit_fp64), 0 = integer (2 IMAD.WIDE)
+#define SHV_MRG_MC_HIT 0  // dartboard test: 0 = integer (2 IMAD.WIDE; with MrgMF the FP64 pipe binds: 355 vs 387 ms, lab67), 1 = FP64 (hit_fp64)
 #endif
 #ifndef SHV_MRG_STAGE
 #define SHV_MRG_STAGE 1
@@ -74,6 +74,9 @@ __constant__ double c_mrg_fpk[6] = {6755399441055744.0, 1.0 / 4294967087.0, 0x1.
 #endif
 __constant__ double c_mrg_snk[6] = {0x0.317b9fd79a126p-1022, 0x1.4e9d5b50f226fp-1022, 0x1.000000d10000bp+980,
                                     0x1.000059451f212p+978, 0x1.8p-12, 0x1.000000d10000bp+978};
+#ifndef SHV_MRG_MF_LANE
+#define SHV_MRG_MF_LANE 1  // MrgMF lane starts by magic-free split rows (split_row_mf)
+#endif
 #ifndef SHV_MRG_SN_LANE
 #define SHV_MRG_SN_LANE 1  // MrgSN lane starts in the subnormal representation (split_row_sn)
 #endif
@@ -549,6 +552,36 @@ __device__ __forceinline__ MrgSN apply_split_sn(const double* __restrict__ tab, 
     return g;
 }
 
+// Row r in the subnormal representation with magic-free quotients (MrgMF):
+// Ah, Al as in split_row_sn, kh = mul.rm(Ah, inv) = D(floor(Ah / m)), D(rh) =
+// fma(-kh, m, Ah), X = 2^16 D(rh) + Al, then the same for X: 11 FP64, no
+// integer or move instructions, the result already the state pair D(r).
+__device__ __forceinline__ double split_row_mf(const double* __restrict__ lt, uint32_t stride, uint32_t e0,
+                                               double v0, double v1, double v2, double inv, double m)
+{
+    const double h0 = lt[(e0 + 0) * stride], l0 = lt[(e0 + 1) * stride];
+    const double h1 = lt[(e0 + 2) * stride], l1 = lt[(e0 + 3) * stride];
+    const double h2 = lt[(e0 + 4) * stride], l2 = lt[(e0 + 5) * stride];
+    const double ah = __fma_rn(h2, v2, __fma_rn(h1, v1, __dmul_rn(h0, v0)));
+    const double al = __fma_rn(l2, v2, __fma_rn(l1, v1, __dmul_rn(l0, v0)));
+    const double rh = __fma_rn(-__dmul_rd(ah, inv), m, ah);
+    const double x = __fma_rn(65536.0, rh, al);
+    return __fma_rn(-__dmul_rd(x, inv), m, x);
+}
+
+__device__ __forceinline__ MrgMF apply_split_mf(const double* __restrict__ tab, uint32_t stride, double x0, double x1,
+                                                double x2, double y0, double y1, double y2, const MrgFpK& K)
+{
+    MrgMF g;
+    g.x0 = split_row_mf(tab, stride, 0, x0, x1, x2, K.inv1, K.m1);
+    g.x1 = split_row_mf(tab, stride, 6, x0, x1, x2, K.inv1, K.m1);
+    g.x2 = split_row_mf(tab, stride, 12, x0, x1, x2, K.inv1, K.m1);
+    g.y0 = split_row_mf(tab, stride, 18, y0, y1, y2, K.inv2, K.m2);
+    g.y1 = split_row_mf(tab, stride, 24, y0, y1, y2, K.inv2, K.m2);
+    g.y2 = split_row_mf(tab, stride, 30, y0, y1, y2, K.inv2, K.m2);
+    return g;
+}
+
 __device__ __forceinline__ MrgMF mf_of(const MrgSN& g)
 {
     return MrgMF{mrg_sn(g.x0), mrg_sn(g.x1), mrg_sn(g.x2), mrg_sn(g.y0), mrg_sn(g.y1), mrg_sn(g.y2)};
@@ -559,6 +592,9 @@ template <class Gen>
 __device__ __forceinline__ Gen lane_start(const double* __restrict__ lt, uint32_t jl, const uint32_t w[6], const MrgFpK& K)
 {
     if constexpr (std::is_same<Gen, MrgMF>::value) {
+        if (SHV_MRG_MF_LANE)
+            return apply_split_mf(lt + jl, 32, mrg_sn(w[0]), mrg_sn(w[1]), mrg_sn(w[2]), mrg_sn(w[3]), mrg_sn(w[4]),
+                                  mrg_sn(w[5]), K);
         return mf_of(apply_split_sn(lt + jl, 32, w, K));
     } else if constexpr (std::is_same<Gen, MrgSN>::value && SHV_MRG_SN_LANE) {
         return apply_split_sn(lt + jl, 32, w, K);
@@ -574,6 +610,7 @@ template <class Gen>
 __device__ __forceinline__ Gen lane_advance(const double* __restrict__ st31, const Gen& g, const MrgFpK& K)
 {
     if constexpr (std::is_same<Gen, MrgMF>::value) {
+        if (SHV_MRG_MF_LANE) return apply_split_mf(st31, 1, g.x0, g.x1, g.x2, g.y0, g.y1, g.y2, K);
         const uint32_t w[6] = {(uint32_t)__double2loint(g.x0), (uint32_t)__double2loint(g.x1),
                                (uint32_t)__double2loint(g.x2), (uint32_t)__double2loint(g.y0),
                                (uint32_t)__double2loint(g.y1), (uint32_t)__double2loint(g.y2)};
