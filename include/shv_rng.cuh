@@ -15,7 +15,8 @@
  *
  * Thread i's sequence is stream i of the handle at the view's offset, value
  * for value the one shv_generate_u32/f32/f64 writes (R7, R8); the state lives
- * in registers. The arithmetic is shv_device.cuh's (MRG32k3a on the FP64 pipe,
+ * in registers. The arithmetic is shv_device.cuh's (MRG32k3a on the FP64 pipe in
+ * the subnormal range,
  * Philox4x32-10 with the warp-uniform key schedule when keys are shared).
  */
 #pragma once
@@ -37,15 +38,15 @@ public:
         const uint64_t n = v.n_streams;
         dev::Mrg m{st[i], st[n + i], st[2 * n + i], st[3 * n + i], st[4 * n + i], st[5 * n + i]};
         dev::apply(v.jump, v.jump + 9, m);
-        s_ = dev::to_mrg_ff(m);
+        s_ = dev::to_mrg_mf(m);
     }
-    // z in [1, m1]; the library fills' step (both components on the FP64 pipe, floor reductions)
+    // z in [1, m1]; the row-tile fill's step (MrgMF: subnormal-range state, magic-free quotients)
     __device__ uint32_t next_u32() { return dev::mrg_next(s_); }
     __device__ float next_f32() { return dev::to_f32(next_u32()); }
     __device__ double next_f64() { return dev::mrg_f64(next_u32()); }
 
 private:
-    dev::MrgFF s_;
+    dev::MrgMF s_;
 };
 
 template <>
