@@ -79,8 +79,8 @@ __global__ void __launch_bounds__(256) philox_fill_fast_kernel(const __grid_cons
                     uint64_t pa = pa0;
                     for (uint32_t r = 0; r < mine; ++r) {
                         const uint64_t pb = add64w(pa, kPM0);
-                        const W4 a = philox10_from_r2(pa, q, (uint32_t)p1, (uint32_t)(g >> 32), k0, k1);
-                        const W4 d = philox10_from_r2(pb, q, (uint32_t)p1, (uint32_t)(g >> 32), k0, k1);
+                        const W4 a = philox10_from_r2<true>(pa, q, (uint32_t)p1, (uint32_t)(g >> 32), k0, k1);
+                        const W4 d = philox10_from_r2<true>(pb, q, (uint32_t)p1, (uint32_t)(g >> 32), k0, k1);
                         store_chunk<KIND>(o, a, d);
                         pa = add64w(pa, 64ull * kPM0);
                         o += 1024;
@@ -122,8 +122,8 @@ __global__ void __launch_bounds__(256) philox_fill_fast_kernel(const __grid_cons
             uint64_t pa = (uint64_t)kPM0 * (uint32_t)blk;
             for (uint32_t r = 0; r < mine; ++r) {
                 const uint64_t pb = add64w(pa, kPM0);
-                const W4 a = philox10_from_r2(pa, q, (uint32_t)p1, (uint32_t)(g >> 32), k0, k1);
-                const W4 d = philox10_from_r2(pb, q, (uint32_t)p1, (uint32_t)(g >> 32), k0, k1);
+                const W4 a = philox10_from_r2<true>(pa, q, (uint32_t)p1, (uint32_t)(g >> 32), k0, k1);
+                const W4 d = philox10_from_r2<true>(pb, q, (uint32_t)p1, (uint32_t)(g >> 32), k0, k1);
                 store_chunk<KIND>(o, a, d);
                 pa = add64w(pa, 64ull * kPM0);
                 o += 1024;
