@@ -3,11 +3,15 @@
 // kernel labs under tools/lab/, which time variants of the same functions).
 //
 // MRG32k3a steps, all exact and bit-identical:
-//  - MrgSN: the state as FP64 pairs {x, 0} in the subnormal range, where a
-//    double's bit pattern is the integer it holds: per component 3 DFMA (the
-//    product sum and one floor quotient) and one IMAD (the residue from the two
-//    low words). The product step of the row-tile u32/f32 fill and of the fused
-//    Monte Carlo kernel (1.71 T values/s compute-only, lab47).
+//  - MrgMF: the state as FP64 pairs {x, 0} in the subnormal range (the double
+//    x * 2^-1074, whose bit pattern is x and whose ulp is 2^-1074): per
+//    component the exact product sum, one round-down multiply that IS the pair
+//    D(floor(p/m)), and one FMA that IS the next state pair D(p - k m): 4 FP64
+//    instructions, no integer or move instructions. The product step of the
+//    row-tile u32/f32 fill, the fused Monte Carlo kernel and the device API
+//    (1.91 T values/s compute-only, lab65).
+//  - MrgSN: the same representation with magic-number quotients and integer
+//    residues (3 DFMA + 1 IMAD + a zero move per component; 1.71 T/s, lab47).
 //  - MrgIF: component 1 in 32-bit integer arithmetic (two IMAD.WIDE + one IMAD,
 //    compare/select on the ALU), component 2 in exact binary64 arithmetic on
 //    the FP64 pipe (products < 2^53, floor reduction), as in L'Ecuyer's

@@ -62,7 +62,7 @@ namespace {
 #define SHV_MRG_MC_CKMASK 22
 #endif
 #ifndef SHV_MRG_ROWS_CKMASK
-#define SHV_MRG_ROWS_CKMASK 21  // row-tile fill (MrgIF): magic, inv2, m2 from constant memory (lab sweep: 3.43 vs 3.50 ms)
+#define SHV_MRG_ROWS_CKMASK 21  // row-tile fill: magic, inv2, m2 from constant memory (MrgIF lab sweep: 3.43 vs 3.50 ms)
 #endif
 __constant__ double c_mrg_fpk[6] = {6755399441055744.0, 1.0 / 4294967087.0, 0x1.000059451f212p-32,
                                     4294967087.0, 4294944443.0, 5886603609186927.0};
