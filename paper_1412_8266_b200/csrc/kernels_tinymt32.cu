@@ -469,7 +469,7 @@ __global__ void __launch_bounds__(kTmTrWarps * 32)
     extern __shared__ uint8_t tm_tr_buf[];
     const unsigned lane = threadIdx.x & 31, warp = __shfl_sync(0xffffffffu, threadIdx.x >> 5, 0);
     const uint32_t base = ((uint32_t)__cvta_generic_to_shared(tm_tr_buf) + 1023u) & ~1023u;
-    const uint32_t box = base + warp * 16384u;
+    const uint32_t box = base + warp * (kTmTrRows * 128u);
     uint32_t off[8];
 #pragma unroll
     for (uint32_t k = 0; k < 8; ++k) off[k] = ((((lane >> 2) ^ k)) << 4) + (lane & 3u) * 4u;
@@ -484,11 +484,11 @@ __global__ void __launch_bounds__(kTmTrWarps * 32)
         const u128 d = (u128)(P.first + p0) + (u128)P.players * ((((u128)P.o_hi << 64) | P.o_lo) + t);
         for (int k = 0; k < 128; ++k)
             if ((uint64_t)(d >> k) & 1u) gf2_apply(b + kTmTab + 512 * k, g);
-        for (uint64_t pc = p0; pc < p1; pc += 128) {
+        for (uint64_t pc = p0; pc < p1; pc += kTmTrRows) {
             if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
             __syncwarp();
 #pragma unroll kTmLeapUnroll
-            for (uint32_t q8 = 0; q8 < 128; q8 += 8) {
+            for (uint32_t q8 = 0; q8 < kTmTrRows; q8 += 8) {
                 const uint32_t rb = box + q8 * 128u;
 #pragma unroll
                 for (uint32_t k = 0; k < 8; ++k) {
@@ -510,7 +510,7 @@ __global__ void __launch_bounds__(kTmTrWarps * 32)
     if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
-constexpr size_t tm_tr_smem() { return (size_t)kTmTrWarps * 16384 + 1024; }
+constexpr size_t tm_tr_smem() { return (size_t)kTmTrWarps * kTmTrRows * 128 + 1024; }
 
 template <int KIND>
 cudaError_t tm_tr_attr()

@@ -658,7 +658,7 @@ shv_status generate(shv_streams hid, T* out, uint64_t n, void* stream, int kind,
             CUtensorMap tmap;
             const bool tr = SHV_MRG_TMA && kind != kF64 && n % 4 == 0 && ((uintptr_t)dst % 16 == 0) &&
                             n < (1ull << 31) && ns < (1ull << 31) - 256 &&
-                            encode_rows_map(&tmap, dst, n, ns, (int)sizeof(T), 128);
+                            encode_rows_map(&tmap, dst, n, ns, (int)sizeof(T), kTmTrRows);
             if (tr) {  // transpose of the base sequence, one TinyMT32 step per value (TMA boxes)
                 int bps = 0;
                 err = tm_leap_tr_blocks_per_sm(kind, &bps);
@@ -669,7 +669,7 @@ shv_status generate(shv_streams hid, T* out, uint64_t n, void* stream, int kind,
                 const uint64_t want_ps = (4 * warps) / P.tr_tb ? (4 * warps) / P.tr_tb : 1;
                 uint64_t pl = (ns + want_ps - 1) / want_ps;
                 if (pl < 4096) pl = 4096;  // long runs amortise the per-lane GF(2) jump
-                P.tr_pl = (pl + 127) / 128 * 128;
+                P.tr_pl = (pl + kTmTrRows - 1) / kTmTrRows * kTmTrRows;
                 P.tr_ps = (ns + P.tr_pl - 1) / P.tr_pl;
                 const uint64_t items = P.tr_tb * P.tr_ps;
                 const uint64_t cap = (uint64_t)h.sms * (uint64_t)(bps > 0 ? bps : 1);

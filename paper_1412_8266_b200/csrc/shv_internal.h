@@ -205,6 +205,11 @@ cudaError_t launch_philox_mc(const PhiloxLaunch& p, bool fast, Grid g, cudaStrea
 // TinyMT32 Leap Frog launch (kernels_tinymt32.cu; R19): buf = the handle's
 // device buffer (params, base state, skip matrix T^(K-1), tables T^(2^b)).
 constexpr size_t kTmLeapBufWords = 520 + 128 * 512;
+// Player rows per TMA box of the transposed TinyMT32 Leap Frog fill (128-B rows, 128-B swizzle).
+#ifndef SHV_TM_TR_ROWS
+#define SHV_TM_TR_ROWS 128
+#endif
+constexpr uint32_t kTmTrRows = SHV_TM_TR_ROWS;
 struct TmLeapLaunch {
     const uint32_t* buf;
     uint64_t players, first, ns;
