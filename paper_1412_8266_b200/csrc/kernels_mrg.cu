@@ -901,26 +901,29 @@ namespace {
 cudaError_t ensure_rows_smem(int threads)
 {
     const size_t sm = mrg_fill_rows_smem(threads);
-    static std::atomic<uint64_t> d[4];
+    static std::atomic<uint64_t> d[6];
     cudaError_t e = ensure_dyn_smem(mrg_fill_rows_kernel<kU32, false>, sm, d[0]);
     if (e == cudaSuccess) e = ensure_dyn_smem(mrg_fill_rows_kernel<kF32, false>, sm, d[1]);
     if (e == cudaSuccess) e = ensure_dyn_smem(mrg_fill_rows_kernel<kU32, true>, sm, d[2]);
     if (e == cudaSuccess) e = ensure_dyn_smem(mrg_fill_rows_kernel<kF32, true>, sm, d[3]);
+    if (e == cudaSuccess) e = ensure_dyn_smem(mrg_fill_rows_kernel<kF64, false>, sm, d[4]);
+    if (e == cudaSuccess) e = ensure_dyn_smem(mrg_fill_rows_kernel<kF64, true>, sm, d[5]);
     return e;
 }
 }  // namespace
 
 cudaError_t launch_mrg_fill_rows(const MrgRowsLaunch& p, const CUtensorMap& tmap, int kind, Grid g, cudaStream_t s)
 {
-    if (kind == kF64) return cudaErrorInvalidValue;
     const size_t sm = mrg_fill_rows_smem((int)g.threads);
     const cudaError_t e = ensure_rows_smem((int)g.threads);
     if (e != cudaSuccess) return e;
     if (p.nh) {
-        if (kind == kF32) mrg_fill_rows_kernel<kF32, true><<<g.blocks, g.threads, sm, s>>>(p, tmap);
+        if (kind == kF64) mrg_fill_rows_kernel<kF64, true><<<g.blocks, g.threads, sm, s>>>(p, tmap);
+        else if (kind == kF32) mrg_fill_rows_kernel<kF32, true><<<g.blocks, g.threads, sm, s>>>(p, tmap);
         else mrg_fill_rows_kernel<kU32, true><<<g.blocks, g.threads, sm, s>>>(p, tmap);
     } else {
-        if (kind == kF32) mrg_fill_rows_kernel<kF32, false><<<g.blocks, g.threads, sm, s>>>(p, tmap);
+        if (kind == kF64) mrg_fill_rows_kernel<kF64, false><<<g.blocks, g.threads, sm, s>>>(p, tmap);
+        else if (kind == kF32) mrg_fill_rows_kernel<kF32, false><<<g.blocks, g.threads, sm, s>>>(p, tmap);
         else mrg_fill_rows_kernel<kU32, false><<<g.blocks, g.threads, sm, s>>>(p, tmap);
     }
     return cudaGetLastError();
@@ -996,8 +999,9 @@ cudaError_t mrg_occupancy(int kernel, int kind, bool fast, int threads, int* out
             return cudaSuccess;
         }
         if (const cudaError_t e = ensure_rows_smem(threads); e != cudaSuccess) return e;
-        return kind == kF32 ? occ(mrg_fill_rows_kernel<kF32, false>, threads, sm, out)
-                            : occ(mrg_fill_rows_kernel<kU32, false>, threads, sm, out);
+        return kind == kF64   ? occ(mrg_fill_rows_kernel<kF64, false>, threads, sm, out)
+               : kind == kF32 ? occ(mrg_fill_rows_kernel<kF32, false>, threads, sm, out)
+                              : occ(mrg_fill_rows_kernel<kU32, false>, threads, sm, out);
     }
     case kKMrgFillTma: {
         const size_t sm = mrg_fill_tma_smem(threads);

@@ -30,6 +30,9 @@
 #ifndef SHV_MRG_ROWS
 #define SHV_MRG_ROWS 1  // MRG32k3a u32/f32 fills in row tiles (0: stream-per-lane tiles only; lab A/B)
 #endif
+#ifndef SHV_MRG_ROWS_F64
+#define SHV_MRG_ROWS_F64 1  // f64 fills in row tiles too (0: the staged vector kernel)
+#endif
 #ifndef SHV_MRG_TMA
 #define SHV_MRG_TMA 1  // MRG32k3a fills store through TMA (0: per-lane vector stores; lab A/B)
 #endif
@@ -366,8 +369,15 @@ void split_tiles(const Handle& h, uint64_t ns, uint64_t len, uint64_t resident_t
 // starts: 3.38 vs 3.46 ms, lab42); with MrgSN the step is cheap enough that the
 // S = 256 layout binds on its TMA stores (4.04 vs 3.17-3.25 ms, lab50).
 // 0 if n has none.
-uint64_t mrg_rows_seg_len(uint64_t n)
+uint64_t mrg_rows_seg_len(uint64_t n, int kind = kU32)
 {
+    // f64: half the values per segment (the same 512-B segments and 16-KB tiles in bytes;
+    // rounds of 16 doubles): S = S_u32(2n) / 2
+    if (kind == kF64) {
+        if (n > (~0ull >> 1)) return 0;
+        const uint64_t S2 = mrg_rows_seg_len(2 * n, kU32);
+        return S2 % 32 == 0 ? S2 / 2 : 0;
+    }
 #ifdef SHV_MRG_ROWS_S  // lab knob: preferred segment length
     if (n % SHV_MRG_ROWS_S == 0) return SHV_MRG_ROWS_S;
 #endif
@@ -382,8 +392,8 @@ uint64_t mrg_rows_seg_len(uint64_t n)
 // that the stream-per-lane path's segment split would not balance better.
 bool mrg_rows_fit(const Handle& h, int kind, bool aligned32, uint64_t ns, uint64_t n)
 {
-    if (!SHV_MRG_ROWS || !SHV_MRG_TMA || kind == kF64 || !aligned32 || h.seg) return false;
-    const uint64_t S = mrg_rows_seg_len(n);
+    if (!SHV_MRG_ROWS || !SHV_MRG_TMA || (kind == kF64 && !SHV_MRG_ROWS_F64) || !aligned32 || h.seg) return false;
+    const uint64_t S = mrg_rows_seg_len(n, kind);
     if (!S || ns * (n / S) >= (1ull << 31)) return false;
     if (mrg_fill_rows_smem((int)h.tpb) > 227u * 1024u) return false;
     const uint64_t tiles = (ns * (n / S) + 31) / 32;
@@ -805,11 +815,11 @@ shv_status generate(shv_streams hid, T* out, uint64_t n, void* stream, int kind,
             Grid g{vec ? blocks_for(h, kKTinyFill, kind, true, ns) : full, h.tpb};
             err = launch_tinymt_fill(P, kind, vec, g, s);
         } else if (h.gen == SHV_GEN_MRG32K3A && mrg_rows_fit(h, kind, aligned32, ns, n) &&
-                   encode_rows_map(&rows_tmap, dst, mrg_rows_seg_len(n), ns * (n / mrg_rows_seg_len(n)),
+                   encode_rows_map(&rows_tmap, dst, mrg_rows_seg_len(n, kind), ns * (n / mrg_rows_seg_len(n, kind)),
                                    (int)sizeof(T))) {
             // row tiles: a warp writes 32 consecutive segments of S values (C5: two 16-KB rows);
             // an encode failure falls through to the stream-per-lane paths below
-            const uint64_t S = mrg_rows_seg_len(n);
+            const uint64_t S = mrg_rows_seg_len(n, kind);
             auto R = std::make_unique<MrgRowsLaunch>();
             MrgLaunch* P = &R->m;
             P->state = h.state;

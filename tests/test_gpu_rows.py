@@ -9,7 +9,8 @@ fewer than 32 segments (tiles spanning several rows), of exactly 32, and of more
 than 32 (nseg 33 / 80: the per-tile (A^(32 S))^(j / 32) jumps; nseg a multiple of
 32: run mode, where a warp carries its lanes from tile to tile by A^(31 S), with a
 ragged last run at 86 tiles per row); a ragged last tile; non-zero offsets;
-STREAM and SUBSTREAM spacing with first > 0; u32 and f32. A CUDA profiler trace
+STREAM and SUBSTREAM spacing with first > 0; u32, f32 and f64 (f64 segments hold half the values:
+the same 512-B segments). A CUDA profiler trace
 checks that the row-tile kernel is the one that ran.
 """
 import numpy as np
@@ -60,7 +61,7 @@ CASES = [
 
 
 @pytest.mark.parametrize("ns,n,spacing,first,pre", CASES)
-@pytest.mark.parametrize("kind", ["u32", "f32"])
+@pytest.mark.parametrize("kind", ["u32", "f32", "f64"])
 def test_rows_fill_matches_oracle(shv, orc, ns, n, spacing, first, pre, kind):
     st = torch.empty(6 * ns, dtype=torch.int32, device="cuda")
     h = shv.shv_streams_create_ex(W.MRG32K3A, [12345, 777, 31337, 4242, 99, 5], first, ns, spacing, st, 0,
@@ -69,23 +70,25 @@ def test_rows_fill_matches_oracle(shv, orc, ns, n, spacing, first, pre, kind):
         shv.shv_set_launch_config(h, 1, 32, 0)
         if pre:
             shv.shv_jump(h, 0, pre, None)
-        tdt = torch.int32 if kind == "u32" else torch.float32
+        tdt = {"u32": torch.int32, "f32": torch.float32, "f64": torch.float64}[kind]
+        okind = {"u32": 0, "f32": 1, "f64": 2}[kind]
+        vdt = np.uint64 if kind == "f64" else np.uint32
         out = torch.empty(ns * n, dtype=tdt, device="cuda")
         names = kernels_of(lambda: getattr(shv, "shv_generate_" + kind)(h, out, n, None))
         assert any("mrg_fill_rows_kernel" in k for k in names), names
-        got = out.cpu().numpy().view(np.uint32).reshape(ns, n)
+        got = out.cpu().numpy().view(vdt).reshape(ns, n)
         ref = orc.generate(W.MRG32K3A, [12345, 777, 31337, 4242, 99, 5], ns, n, first=first, spacing=spacing,
-                           offset=pre, kind=0 if kind == "u32" else 1)
-        ref = np.ascontiguousarray(ref).view(np.uint32).reshape(ns, n)
+                           offset=pre, kind=okind)
+        ref = np.ascontiguousarray(ref).view(vdt).reshape(ns, n)
         bad = np.nonzero(got != ref)
         assert len(bad[0]) == 0, f"{len(bad[0])} mismatches, first at {[x[:5] for x in bad]}"
         # the handle advanced by n: a second call continues the streams
         out2 = torch.empty(ns * 256, dtype=tdt, device="cuda")
         getattr(shv, "shv_generate_" + kind)(h, out2, 256, None)
         ref2 = orc.generate(W.MRG32K3A, [12345, 777, 31337, 4242, 99, 5], ns, 256, first=first, spacing=spacing,
-                            offset=pre + n, kind=0 if kind == "u32" else 1)
-        assert np.array_equal(out2.cpu().numpy().view(np.uint32).reshape(ns, 256),
-                              np.ascontiguousarray(ref2).view(np.uint32).reshape(ns, 256))
+                            offset=pre + n, kind=okind)
+        assert np.array_equal(out2.cpu().numpy().view(vdt).reshape(ns, 256),
+                              np.ascontiguousarray(ref2).view(vdt).reshape(ns, 256))
     finally:
         shv.shv_streams_destroy(h)
 
