@@ -22,6 +22,10 @@
 constexpr int kLeapMrgUnroll = SHV_LEAP_MRG_UNROLL;
 // the same for the counter-based transposed fills (lab62): Philox 1 (3.16 vs
 // 3.53-3.64 ms unrolled), Threefry 4 (6.00 vs 6.20 ms)
+#ifndef SHV_LEAP_PHILOX_COLS
+#define SHV_LEAP_PHILOX_COLS 1  // t-columns per lane of the transposed Philox fill (2: 256-B box rows)
+#endif
+__host__ __device__ constexpr uint32_t leap_ctr_cols_of(int lgen) { return lgen == 1 ? SHV_LEAP_PHILOX_COLS : 1; }
 #ifndef SHV_LEAP_PHILOX_UNROLL
 #define SHV_LEAP_PHILOX_UNROLL 1
 #endif
@@ -524,17 +528,42 @@ __global__ void __launch_bounds__(kTrWarps * 32)
 #endif
 template <int KIND, int G, bool HOIST>
 __device__ __forceinline__ void leap_ctr_run(const LeapLaunch& P, const CUtensorMap* tmap, unsigned lane, uint32_t box,
-                                             uint32_t lo4, uint64_t tb, uint64_t p0, uint64_t p1, uint64_t b)
+                                             uint32_t lo4, uint64_t tb, uint64_t p0, uint64_t p1, uint64_t b,
+                                             uint64_t b2)
 {
     constexpr int kUnroll = G == kLeapPhilox ? SHV_LEAP_PHILOX_UNROLL : SHV_LEAP_THREEFRY_UNROLL;
+    constexpr uint32_t kCols = leap_ctr_cols_of(G), kRowB = 128u * kCols;
     const uint64_t q = (uint64_t)kPM0 * ((uint32_t)(b >> 32) ^ (uint32_t)P.k0);
     uint64_t pa = (uint64_t)kPM0 * (uint32_t)b;
+    const uint64_t q2 = (uint64_t)kPM0 * ((uint32_t)(b2 >> 32) ^ (uint32_t)P.k0);
+    uint64_t pa2 = (uint64_t)kPM0 * (uint32_t)b2;
     for (uint64_t pc = p0; pc < p1; pc += kTrRows) {
         if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
         __syncwarp();
 #pragma unroll kUnroll
         for (uint32_t q8 = 0; q8 < kTrRows; q8 += 8) {
-            const uint32_t rb = box + q8 * 128u;
+            const uint32_t rb = box + q8 * kRowB;
+            if constexpr (kCols == 2) {  // second column t + 32 (Philox only): word 32 + lane of the 256-B row
+                uint32_t y[8];
+                W4 u0, u1;
+                if constexpr (HOIST) {
+                    u0 = philox10_from_r2(pa2, q2, 0u, 0u, (uint32_t)P.k0, (uint32_t)P.k1);
+                    pa2 = add64w(pa2, kPM0);
+                    u1 = philox10_from_r2(pa2, q2, 0u, 0u, (uint32_t)P.k0, (uint32_t)P.k1);
+                    pa2 = add64w(pa2, kPM0);
+                } else {
+                    u0 = philox_blk(b2, 0, (uint32_t)P.k0, (uint32_t)P.k1);
+                    u1 = philox_blk(b2 + 1, 0, (uint32_t)P.k0, (uint32_t)P.k1);
+                }
+                b2 += 2;
+                y[0] = u0.x; y[1] = u0.y; y[2] = u0.z; y[3] = u0.w;
+                y[4] = u1.x; y[5] = u1.y; y[6] = u1.z; y[7] = u1.w;
+#pragma unroll
+                for (uint32_t k = 0; k < 8; ++k) {
+                    const uint32_t w = KIND == kF32 ? __float_as_uint(to_f32(y[k])) : y[k];
+                    asm volatile("st.shared.b32 [%0], %1;" ::"r"(rb + 128u + lo4 + k * kRowB), "r"(w) : "memory");
+                }
+            }
             uint32_t z[8];
             if constexpr (G == kLeapPhilox) {
                 W4 v0, v1;
@@ -567,14 +596,14 @@ __device__ __forceinline__ void leap_ctr_run(const LeapLaunch& P, const CUtensor
 #pragma unroll
             for (uint32_t k = 0; k < 8; ++k) {
                 const uint32_t w = KIND == kF32 ? __float_as_uint(to_f32(z[k])) : z[k];
-                asm volatile("st.shared.b32 [%0], %1;" ::"r"(rb + lo4 + k * 128u), "r"(w) : "memory");
+                asm volatile("st.shared.b32 [%0], %1;" ::"r"(rb + lo4 + k * kRowB), "r"(w) : "memory");
             }
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncwarp();
         if (lane == 0) {
             asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(tmap),
-                         "r"(box), "r"((int)(32 * tb)), "r"((int)pc)
+                         "r"(box), "r"((int)(32 * kCols * tb)), "r"((int)pc)
                          : "memory");
             asm volatile("cp.async.bulk.commit_group;" ::: "memory");
         }
@@ -594,33 +623,38 @@ __global__ void __launch_bounds__(kTrWarps * 32)
     extern __shared__ uint8_t trp_smem[];
     const unsigned lane = threadIdx.x & 31, warp = __shfl_sync(0xffffffffu, threadIdx.x >> 5, 0);
     const uint32_t base = ((uint32_t)__cvta_generic_to_shared(trp_smem) + 1023u) & ~1023u;
-    const uint32_t box = base + warp * (kTrRows * 128u);
-    const uint32_t lo4 = lane * 4u;  // unswizzled box: word `lane` of each 128-B row
+    constexpr uint32_t kCols = leap_ctr_cols_of(G);
+    const uint32_t box = base + warp * (kTrRows * 128u * kCols);
+    const uint32_t lo4 = lane * 4u;  // unswizzled box: word `lane` (and 32 + lane) of each row
     const uint64_t items = P.tr_tb * P.tr_ps;
     const uint64_t wstride = (uint64_t)gridDim.x * (blockDim.x >> 5);
     const u128 o = ((u128)P.o_hi << 64) | P.o_lo;
     for (uint64_t it = (uint64_t)blockIdx.x * (blockDim.x >> 5) + warp; it < items; it += wstride) {
         const uint64_t ps = it / P.tr_tb, tb = it - ps * P.tr_tb;
-        const uint64_t t = 32 * tb + lane;
+        const uint64_t t = 32 * kCols * tb + lane;
         const uint64_t p0 = ps * P.tr_pl;
         const uint64_t p1 = min(P.ns, p0 + P.tr_pl);
         // words per block: 4 (Philox) or 8 (Threefry); the run starts block-aligned
         const uint64_t b = (uint64_t)(((u128)(P.first + p0) + (u128)P.players * (o + t)) >> (G == kLeapPhilox ? 2 : 3));
+        const uint64_t b2 =
+            kCols == 2 ? (uint64_t)(((u128)(P.first + p0) + (u128)P.players * (o + t + 32)) >> 2) : 0;
         const uint64_t nblk = (p1 - p0 + 3) / 4 + 2;
-        const bool hoist = G == kLeapPhilox && (uint32_t)b <= 0xFFFFFFFFu - (uint32_t)min(nblk, (uint64_t)0xFFFFFFFFu);
-        if (__all_sync(0xffffffffu, hoist)) leap_ctr_run<KIND, G, G == kLeapPhilox>(P, &tmap, lane, box, lo4, tb, p0, p1, b);
-        else leap_ctr_run<KIND, G, false>(P, &tmap, lane, box, lo4, tb, p0, p1, b);
+        const uint32_t lim = 0xFFFFFFFFu - (uint32_t)min(nblk, (uint64_t)0xFFFFFFFFu);
+        const bool hoist = G == kLeapPhilox && (uint32_t)b <= lim && (kCols == 1 || (uint32_t)b2 <= lim);
+        if (__all_sync(0xffffffffu, hoist))
+            leap_ctr_run<KIND, G, G == kLeapPhilox>(P, &tmap, lane, box, lo4, tb, p0, p1, b, b2);
+        else leap_ctr_run<KIND, G, false>(P, &tmap, lane, box, lo4, tb, p0, p1, b, b2);
     }
     if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
-constexpr size_t leap_tr_smem() { return (size_t)kTrWarps * kTrRows * 128 + 1024; }
+constexpr size_t leap_tr_smem(uint32_t cols = 1) { return (size_t)kTrWarps * kTrRows * 128 * cols + 1024; }
 
 template <int KIND, int G>
 cudaError_t leap_trp_attr()
 {
     static std::atomic<uint64_t> done{0};
-    return ensure_dyn_smem(leap_ctr_tr_kernel<KIND, G>, leap_tr_smem(), done);
+    return ensure_dyn_smem(leap_ctr_tr_kernel<KIND, G>, leap_tr_smem(leap_ctr_cols_of(G)), done);
 }
 
 template <int KIND>
@@ -736,8 +770,8 @@ cudaError_t launch_ctr_tr_g(const LeapLaunch& p, const CUtensorMap& tmap, int ki
 {
     cudaError_t e = kind == kF32 ? leap_trp_attr<kF32, G>() : leap_trp_attr<kU32, G>();
     if (e != cudaSuccess) return e;
-    if (kind == kF32) leap_ctr_tr_kernel<kF32, G><<<blocks, kTrWarps * 32, leap_tr_smem(), s>>>(p, tmap);
-    else leap_ctr_tr_kernel<kU32, G><<<blocks, kTrWarps * 32, leap_tr_smem(), s>>>(p, tmap);
+    if (kind == kF32) leap_ctr_tr_kernel<kF32, G><<<blocks, kTrWarps * 32, leap_tr_smem(leap_ctr_cols_of(G)), s>>>(p, tmap);
+    else leap_ctr_tr_kernel<kU32, G><<<blocks, kTrWarps * 32, leap_tr_smem(leap_ctr_cols_of(G)), s>>>(p, tmap);
     return cudaGetLastError();
 }
 
@@ -749,14 +783,15 @@ cudaError_t launch_leap_ctr_tr(const LeapLaunch& p, const CUtensorMap& tmap, int
 }
 
 uint32_t leap_tr_rows() { return kTrRows; }
+uint32_t leap_ctr_cols(int lgen) { return leap_ctr_cols_of(lgen); }
 
 cudaError_t leap_ctr_tr_blocks_per_sm(int lgen, int kind, int* out)
 {
     if (lgen == kLeapPhilox) {
         const cudaError_t e = kind == kF32 ? leap_trp_attr<kF32, kLeapPhilox>() : leap_trp_attr<kU32, kLeapPhilox>();
         if (e != cudaSuccess) return e;
-        return kind == kF32 ? occ(leap_ctr_tr_kernel<kF32, kLeapPhilox>, kTrWarps * 32, leap_tr_smem(), out)
-                            : occ(leap_ctr_tr_kernel<kU32, kLeapPhilox>, kTrWarps * 32, leap_tr_smem(), out);
+        return kind == kF32 ? occ(leap_ctr_tr_kernel<kF32, kLeapPhilox>, kTrWarps * 32, leap_tr_smem(leap_ctr_cols_of(kLeapPhilox)), out)
+                            : occ(leap_ctr_tr_kernel<kU32, kLeapPhilox>, kTrWarps * 32, leap_tr_smem(leap_ctr_cols_of(kLeapPhilox)), out);
     }
     const cudaError_t e = kind == kF32 ? leap_trp_attr<kF32, kLeapThreefry>() : leap_trp_attr<kU32, kLeapThreefry>();
     if (e != cudaSuccess) return e;

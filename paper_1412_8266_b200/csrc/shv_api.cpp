@@ -452,13 +452,13 @@ PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder()
 // Transposed fills write their boxes unswizzled: lane l stores word l of a box row, so the
 // 32 lanes of one st.shared cover one 128-B row (conflict-free) at base + row * 128 + 4 l.
 bool encode_rows_map(CUtensorMap* m, void* out, uint64_t n, uint64_t ns, int elem, uint32_t box_rows = 32,
-                     bool swizzle = true)
+                     bool swizzle = true, uint32_t row_bytes = 128)
 {
     const auto enc = tensor_map_encoder();
     if (!enc) return false;
     const cuuint64_t dims[2] = {n, ns};
     const cuuint64_t strides[1] = {n * (uint64_t)elem};
-    const cuuint32_t box[2] = {128u / (cuuint32_t)elem, box_rows};
+    const cuuint32_t box[2] = {row_bytes / (cuuint32_t)elem, box_rows};
     const cuuint32_t estr[2] = {1, 1};
     return enc(m, elem == 8 ? CU_TENSOR_MAP_DATA_TYPE_UINT64 : CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, out, dims, strides,
                box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
@@ -703,11 +703,12 @@ shv_status generate(shv_streams hid, T* out, uint64_t n, void* stream, int kind,
             const bool trp = (h.gen == SHV_GEN_PHILOX4X32_10 && h.players % 4 == 0 && (h.first + s0) % 4 == 0) ||
                              (h.gen == SHV_GEN_THREEFRY4X64_20 && h.players % 8 == 0 && (h.first + s0) % 8 == 0);
             const uint32_t rows = leap_tr_rows();
+            const uint32_t cols = trp ? leap_ctr_cols(lg) : 1u;  // 128-B box columns per lane
             CUtensorMap trmap;
             // an encode failure falls back to the per-player kernels below
             const bool tr = SHV_MRG_TMA && (h.gen == SHV_GEN_MRG32K3A || trp) && kind != kF64 && n % 4 == 0 &&
                             ((uintptr_t)dst % 16 == 0) && n < (1ull << 31) && ns < (1ull << 31) - 256 &&
-                            encode_rows_map(&trmap, dst, n, ns, (int)sizeof(T), rows, false);
+                            encode_rows_map(&trmap, dst, n, ns, (int)sizeof(T), rows, false, 128u * cols);
             if (tr) {
                 int bps = 0;
                 err = trp ? leap_ctr_tr_blocks_per_sm(lg, kind, &bps) : leap_mrg_tr_blocks_per_sm(kind, &bps);
@@ -735,7 +736,7 @@ shv_status generate(shv_streams hid, T* out, uint64_t n, void* stream, int kind,
                     for (int b = 1; b < kSegBits && ((n - 1) >> b); ++b)
                         P->segpow[b] = pair_mul(P->segpow[b - 1], P->segpow[b - 1]);
                 }
-                P->tr_tb = (n + 31) / 32;
+                P->tr_tb = (n + 32 * cols - 1) / (32 * cols);
                 const uint64_t warps = (uint64_t)h.sms * (uint64_t)(bps > 0 ? bps : 1) * 4;
                 const uint64_t want_ps = (4 * warps) / P->tr_tb ? (4 * warps) / P->tr_tb : 1;
                 uint64_t pl = (ns + want_ps - 1) / want_ps;
