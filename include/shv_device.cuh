@@ -122,7 +122,7 @@ struct MrgFpK {
     double m1, m2;
     double a23n_m2; // a23n * m2 = 5886603609186927, exact
     uint32_t a12, a13n;  // component-1 multipliers for the integer half-step
-    // Subnormal-state step (MrgSN): constants in units of 2^-1074 and the
+    // Subnormal-state steps (MrgSN; MrgMF uses sn_c2p): constants in units of 2^-1074 and the
     // scaled inverses; the kernels overwrite them from their launch parameters.
     double sn_c1q = 0x0.317b9fd79a126p-1022;  // D(202682 * m1)
     double sn_c2p = 0x1.4e9d5b50f226fp-1022;  // D(a23n * m2)

@@ -366,7 +366,7 @@ void split_tiles(const Handle& h, uint64_t ns, uint64_t len, uint64_t resident_t
 // n in {128, 96, 160, 192, 64, 224, 256, ...}. S = 128 makes a warp tile one
 // 16-KB region, the best store layout (6.1 vs 5.1 TB/s at S = 256 with a null
 // generator). With the MrgIF step the C5 shape took S = 256 (half the lane
-// starts: 3.38 vs 3.46 ms, lab42); with MrgSN the step is cheap enough that the
+// starts: 3.38 vs 3.46 ms, lab42); with MrgSN / MrgMF the step is cheap enough that the
 // S = 256 layout binds on its TMA stores (4.04 vs 3.17-3.25 ms, lab50).
 // 0 if n has none.
 uint64_t mrg_rows_seg_len(uint64_t n, int kind = kU32)
