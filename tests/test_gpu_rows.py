@@ -106,3 +106,37 @@ def test_rows_path_not_taken_for_few_tiles(shv):
         assert any("mrg_fill_tma_kernel" in k for k in names), names
     finally:
         shv.shv_streams_destroy(h)
+
+
+def test_rows_fill_component1_edge_state(shv, orc):
+    """MrgMF's component-1 edge: a negative product sum that is an exact multiple
+    of m1 floors to k - 1 and leaves the residue m1 (= 0) as the next state word. The seed puts
+    it on the first step of stream 0 (x1 = 1, x0 = a12 / a13n mod m1, so a12 x1 - a13n x0 = k m1 < 0);
+    every value of the row-tile fill, and the fused MC totals, must equal the oracle's."""
+    M1, A12, A13N = 4294967087, 1403580, 810728
+    x0 = A12 * pow(A13N, -1, M1) % M1
+    assert (A12 * 1 - A13N * x0) % M1 == 0 and A12 - A13N * x0 < 0
+    seed = [x0, 1, 12345, 777, 31337, 4242]
+    ns, n = 600, 4096
+    st = torch.empty(6 * ns, dtype=torch.int32, device="cuda")
+    h = shv.shv_streams_create_ex(W.MRG32K3A, seed, 0, ns, W.SPACING_SUBSTREAM, st, 0, torch.cuda.current_device(), None)
+    try:
+        shv.shv_set_launch_config(h, 1, 32, 0)
+        out = torch.empty(ns * n, dtype=torch.int32, device="cuda")
+        names = kernels_of(lambda: shv.shv_generate_u32(h, out, n, None))
+        assert any("mrg_fill_rows_kernel" in k for k in names), names
+        ref = orc.generate(W.MRG32K3A, seed, ns, n, first=0, spacing=W.SPACING_SUBSTREAM, offset=0, kind=0)
+        got = out.cpu().numpy().view(np.uint32).reshape(ns, n)
+        assert np.array_equal(got, np.ascontiguousarray(ref).view(np.uint32).reshape(ns, n))
+    finally:
+        shv.shv_streams_destroy(h)
+    h = shv.shv_streams_create_ex(W.MRG32K3A, seed, 0, ns, W.SPACING_SUBSTREAM, st, 0, torch.cuda.current_device(), None)
+    try:
+        hits = torch.zeros(1, dtype=torch.int64, device="cuda")
+        cnt = torch.zeros(ns, dtype=torch.int64, device="cuda")
+        shv.shv_mc_pi_ex(h, n, hits, cnt, None)
+        torch.cuda.synchronize()
+        tot, cref = orc.mc_count(W.MRG32K3A, seed, ns, n, spacing=W.SPACING_SUBSTREAM)
+        assert np.array_equal(cnt.cpu().numpy().astype(np.uint64), cref) and int(hits.item()) == tot
+    finally:
+        shv.shv_streams_destroy(h)
