@@ -434,6 +434,11 @@ cudaError_t leap_tma_attr()
 #define SHV_LEAP_TR_WARPS 4
 #endif
 constexpr unsigned kTrWarps = SHV_LEAP_TR_WARPS;
+// warps per block of the transposed MRG32k3a fill (8: 3.22 vs 3.28 ms with 4-warp grid sizing, lab64; 3.34-3.43 with 8-warp sizing)
+#ifndef SHV_LEAP_MRG_WARPS
+#define SHV_LEAP_MRG_WARPS 4
+#endif
+constexpr unsigned kTrWarpsMrg = SHV_LEAP_MRG_WARPS;
 // Players per transposed box (rows of the 128-B wide box): 32 keeps a warp's
 // box at 4 KB, so up to 48 warps per SM stay resident (128-row, 16-KB boxes
 // held the transposed fills to 12 warps per SM: ncu 0.74 eligible warps per
@@ -462,7 +467,7 @@ __device__ __forceinline__ void make_leap_gen(const Mrg& m, MrgSN& g) { g = to_m
 __device__ __forceinline__ void make_leap_gen(const Mrg& m, MrgMF& g) { g = to_mrg_mf(m); }
 __device__ __forceinline__ void make_leap_gen(const Mrg& m, MrgIF& g) { g = to_mrg_if(m); }
 template <int KIND>
-__global__ void __launch_bounds__(kTrWarps * 32)
+__global__ void __launch_bounds__(kTrWarpsMrg * 32)
     leap_mrg_tr_kernel(const __grid_constant__ LeapLaunch P, const __grid_constant__ CUtensorMap tmap)
 {
     extern __shared__ uint8_t tr_smem[];
@@ -649,6 +654,7 @@ __global__ void __launch_bounds__(kTrWarps * 32)
 }
 
 constexpr size_t leap_tr_smem(uint32_t cols = 1) { return (size_t)kTrWarps * kTrRows * 128 * cols + 1024; }
+constexpr size_t leap_tr_smem_mrg() { return (size_t)kTrWarpsMrg * kTrRows * 128 + 1024; }
 
 template <int KIND, int G>
 cudaError_t leap_trp_attr()
@@ -661,7 +667,7 @@ template <int KIND>
 cudaError_t leap_tr_attr()
 {
     static std::atomic<uint64_t> done{0};
-    return ensure_dyn_smem(leap_mrg_tr_kernel<KIND>, leap_tr_smem(), done);
+    return ensure_dyn_smem(leap_mrg_tr_kernel<KIND>, leap_tr_smem_mrg(), done);
 }
 
 __global__ void __launch_bounds__(256) leap_mc_grouped_kernel(const __grid_constant__ LeapLaunch P)
@@ -760,8 +766,8 @@ cudaError_t launch_leap_mrg_tr(const LeapLaunch& p, const CUtensorMap& tmap, int
 {
     cudaError_t e = kind == kF32 ? leap_tr_attr<kF32>() : leap_tr_attr<kU32>();
     if (e != cudaSuccess) return e;
-    if (kind == kF32) leap_mrg_tr_kernel<kF32><<<blocks, kTrWarps * 32, leap_tr_smem(), s>>>(p, tmap);
-    else leap_mrg_tr_kernel<kU32><<<blocks, kTrWarps * 32, leap_tr_smem(), s>>>(p, tmap);
+    if (kind == kF32) leap_mrg_tr_kernel<kF32><<<blocks, kTrWarpsMrg * 32, leap_tr_smem_mrg(), s>>>(p, tmap);
+    else leap_mrg_tr_kernel<kU32><<<blocks, kTrWarpsMrg * 32, leap_tr_smem_mrg(), s>>>(p, tmap);
     return cudaGetLastError();
 }
 
@@ -784,6 +790,7 @@ cudaError_t launch_leap_ctr_tr(const LeapLaunch& p, const CUtensorMap& tmap, int
 
 uint32_t leap_tr_rows() { return kTrRows; }
 uint32_t leap_ctr_cols(int lgen) { return leap_ctr_cols_of(lgen); }
+uint32_t leap_tr_warps(bool mrg) { return mrg ? kTrWarpsMrg : kTrWarps; }
 
 cudaError_t leap_ctr_tr_blocks_per_sm(int lgen, int kind, int* out)
 {
@@ -803,8 +810,8 @@ cudaError_t leap_mrg_tr_blocks_per_sm(int kind, int* out)
 {
     cudaError_t e = kind == kF32 ? leap_tr_attr<kF32>() : leap_tr_attr<kU32>();
     if (e != cudaSuccess) return e;
-    return kind == kF32 ? occ(leap_mrg_tr_kernel<kF32>, kTrWarps * 32, leap_tr_smem(), out)
-                        : occ(leap_mrg_tr_kernel<kU32>, kTrWarps * 32, leap_tr_smem(), out);
+    return kind == kF32 ? occ(leap_mrg_tr_kernel<kF32>, kTrWarpsMrg * 32, leap_tr_smem_mrg(), out)
+                        : occ(leap_mrg_tr_kernel<kU32>, kTrWarpsMrg * 32, leap_tr_smem_mrg(), out);
 }
 
 cudaError_t launch_leap_mc(const LeapLaunch& p, int lgen, Grid g, cudaStream_t s)

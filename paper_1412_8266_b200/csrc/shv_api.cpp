@@ -737,7 +737,8 @@ shv_status generate(shv_streams hid, T* out, uint64_t n, void* stream, int kind,
                         P->segpow[b] = pair_mul(P->segpow[b - 1], P->segpow[b - 1]);
                 }
                 P->tr_tb = (n + 32 * cols - 1) / (32 * cols);
-                const uint64_t warps = (uint64_t)h.sms * (uint64_t)(bps > 0 ? bps : 1) * 4;
+                const uint64_t wpb = leap_tr_warps(!trp);  // warps per block
+                const uint64_t warps = (uint64_t)h.sms * (uint64_t)(bps > 0 ? bps : 1) * wpb;
                 const uint64_t want_ps = (4 * warps) / P->tr_tb ? (4 * warps) / P->tr_tb : 1;
                 uint64_t pl = (ns + want_ps - 1) / want_ps;
                 if (pl < 1024) pl = 1024;  // runs long enough to amortise the start jump
@@ -754,7 +755,7 @@ shv_status generate(shv_streams hid, T* out, uint64_t n, void* stream, int kind,
                 P->imul[1] = 810728u;   // a13n
                 const uint64_t items = P->tr_tb * P->tr_ps;
                 const uint64_t cap = (uint64_t)h.sms * (uint64_t)(bps > 0 ? bps : 1);
-                const uint64_t want = (items + 3) / 4;
+                const uint64_t want = (items + wpb - 1) / wpb;
                 if (err == cudaSuccess)
                     err = trp ? launch_leap_ctr_tr(*P, trmap, leap_gen(h.gen), kind, (unsigned)(want < cap ? want : cap), s)
                               : launch_leap_mrg_tr(*P, trmap, kind, (unsigned)(want < cap ? want : cap), s);

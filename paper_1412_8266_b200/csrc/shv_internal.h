@@ -287,6 +287,7 @@ cudaError_t leap_tma_blocks_per_sm(int kind, int* out);
 cudaError_t launch_leap_mrg_tr(const LeapLaunch& p, const CUtensorMap& tmap, int kind, unsigned blocks, cudaStream_t s);
 cudaError_t leap_mrg_tr_blocks_per_sm(int kind, int* out);
 cudaError_t leap_ctr_tr_blocks_per_sm(int lgen, int kind, int* out);
+uint32_t leap_tr_warps(bool mrg);   // warps per block of leap_mrg_tr_kernel (mrg) / leap_ctr_tr_kernel
 uint32_t leap_ctr_cols(int lgen);  // t-columns per lane (box row = 128 B per column) of leap_ctr_tr_kernel
 uint32_t leap_tr_rows();  // players (box rows) per transposed TMA box; tr_pl is a multiple
 // Counter-based Leap Frog fill by transposition (u32/f32): Philox with K % 4 == 0
