@@ -785,6 +785,10 @@ __global__ void __launch_bounds__(256) mrg_fill_scalar_kernel(const __grid_const
     }
 }
 
+#ifndef SHV_MRG_MC_UNROLL
+#define SHV_MRG_MC_UNROLL 12  // samples per unrolled iteration of the MC loop
+#endif
+constexpr uint32_t kMcU = SHV_MRG_MC_UNROLL;
 __global__ void __launch_bounds__(256) mrg_mc_kernel(const __grid_constant__ MrgLaunch P)
 {
     const MrgFpK K = load_fpk<SHV_MRG_MC_CKMASK>(P);
@@ -806,17 +810,17 @@ __global__ void __launch_bounds__(256) mrg_mc_kernel(const __grid_constant__ Mrg
         const uint32_t wmin = __reduce_min_sync(0xffffffffu, len);
         uint32_t h = 0;
         uint32_t k = 0;
-        for (; k + 12 <= wmin; k += 12) {  // every lane inside its segment: no per-sample mask
+        for (; k + kMcU <= wmin; k += kMcU) {  // every lane inside its segment: no per-sample mask
 #pragma unroll
-            for (int u = 0; u < 12; ++u) {
+            for (int u = 0; u < (int)kMcU; ++u) {
                 const uint32_t w0 = mrg_next(s, K);
                 const uint32_t w1 = mrg_next(s, K);
                 h += SHV_MRG_MC_HIT ? hit_fp64(w0, w1) : hit(w0, w1);
             }
         }
-        for (; k + 12 <= wlen; k += 12) {
+        for (; k + kMcU <= wlen; k += kMcU) {
 #pragma unroll
-            for (int u = 0; u < 12; ++u) {
+            for (int u = 0; u < (int)kMcU; ++u) {
                 const uint32_t w0 = mrg_next(s, K);
                 const uint32_t w1 = mrg_next(s, K);
                 h += (SHV_MRG_MC_HIT ? hit_fp64(w0, w1) : hit(w0, w1)) & (k + u < len ? 1u : 0u);
