@@ -9,7 +9,8 @@
 //
 // Compile-time knobs (defaults = the product; tools/lab/build_knobs.sh builds
 // variants for the labs, every variant gives bit-identical output):
-//   SHV_MRG_STEP     step of the stream-per-lane fills: 4 = MrgFF, 3 = MrgIF
+//   SHV_MRG_STEP     step of the stream-per-lane / vector / scalar fills: 4 = MrgFF,
+//                    3 = MrgIF, 5 = MrgSN, 7 = MrgMF
 //   SHV_MRG_MC_STEP  step of the fused Monte Carlo kernel: 7 = MrgMF (385 ms for
 //                    2^38 samples), 5 = MrgSN (405-409), 3 = MrgIF (464-474), 4 = MrgFF
 //   SHV_MRG_MC_HIT   dartboard test: 0 = integer (MrgMF: 355 vs 387 ms), 1 = FP64 (MrgIF: 471 vs 474)
@@ -20,7 +21,7 @@
 #include "kernels_common.cuh"
 
 #ifndef SHV_MRG_STEP
-#define SHV_MRG_STEP 4
+#define SHV_MRG_STEP 7  // stream-per-lane / vector fills: MrgMF (f64 vector 3.79 vs 3.88 ms, u32 TMA equal, lab77)
 #endif
 #ifndef SHV_MRG_MC_STEP
 #define SHV_MRG_MC_STEP 7
@@ -109,9 +110,13 @@ using StepGen = typename std::conditional<
 #include SHV_LAB_GEN_HEADER
 using GenFill = SHV_LAB_GEN;
 #else
-using GenFill = std::conditional<SHV_MRG_STEP == 4, MrgFF, MrgIF>::type;
+using GenFill = StepGen<SHV_MRG_STEP>;
 #endif
 using GenMc = StepGen<SHV_MRG_MC_STEP>;
+#ifndef SHV_MRG_SCALAR_STEP
+#define SHV_MRG_SCALAR_STEP 4  // step of the scalar (ragged) fill: MrgFF (MrgMF: 9.71 vs 8.82 ms, lab77)
+#endif
+using GenScalar = StepGen<SHV_MRG_SCALAR_STEP>;
 
 
 __device__ __forceinline__ Mrg load_state(const uint32_t* __restrict__ st, uint64_t stride, uint64_t i)
@@ -772,7 +777,7 @@ __global__ void __launch_bounds__(256) mrg_fill_scalar_kernel(const __grid_const
     for (uint64_t it = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; it < P.items; it += nthr) {
         uint64_t i, j;
         item_ij<false>(P, it, i, j);
-        GenFill s = item_state(P, i, j);
+        GenScalar s = item_state<GenScalar>(P, i, j);
         const uint64_t c0 = j * P.seg_len;
         const uint64_t len = min(P.seg_len, P.n - c0);
         T* o = reinterpret_cast<T*>(P.out) + i * P.n + c0;
