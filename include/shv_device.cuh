@@ -8,8 +8,8 @@
 //    component the exact product sum, one round-down multiply that IS the pair
 //    D(floor(p/m)), and one FMA that IS the next state pair D(p - k m): 4 FP64
 //    instructions, no integer or move instructions. The product step of the
-//    row-tile u32/f32 fill, the fused Monte Carlo kernel and the device API
-//    (1.91 T values/s compute-only, lab65).
+//    row-tile, stream-per-lane and vector fills, the fused Monte Carlo kernel
+//    and the device API (1.91 T values/s compute-only, lab65).
 //  - MrgSN: the same representation with magic-number quotients and integer
 //    residues (3 DFMA + 1 IMAD + a zero move per component; 1.71 T/s, lab47).
 //  - MrgIF: component 1 in 32-bit integer arithmetic (two IMAD.WIDE + one IMAD,
@@ -17,7 +17,7 @@
 //    the FP64 pipe (products < 2^53, floor reduction), as in L'Ecuyer's
 //    floating-point formulation [LEcuyer1999]. The transposed Leap Frog fill.
 //  - MrgFF: both components on the FP64 pipe (12 FP64 operations per number);
-//    the stream-per-lane fills (f64, shapes without a row-tile split).
+//    the scalar (ragged-shape) fill.
 // Measured on B200 (tools/lab, profiles/r02_labs): IMAD.WIDE issues at ~21-24
 // per SM per clock (about 6 issue cycles per warp instruction) and slows the
 // other kinds it shares the SM with, so MrgIF costs about the sum of its two
